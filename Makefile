@@ -1,0 +1,38 @@
+# Builds the product library (CUDA kernels for sm_100a + host runtime/C-ABI)
+# and the test-only checkers under oracle/.
+CUDA    ?= /usr/local/cuda
+NVCC    ?= $(CUDA)/bin/nvcc
+CXX     ?= g++
+PKG     := paper_2503_13795_b200
+ARCH    := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -lineinfo -O3 -std=c++20 -Xcompiler -fPIC -Xptxas -v -Iinclude -I$(PKG)/csrc/host
+CXXFLAGS:= -std=c++20 -O2 -fPIC -Wall -Iinclude -I$(PKG)/csrc/host -I$(CUDA)/include
+BUILD   := build
+
+CU_SRC  := $(wildcard $(PKG)/csrc/kernels/*.cu)
+CXX_SRC := $(wildcard $(PKG)/csrc/host/*.cpp)
+HDRS    := $(wildcard include/*.h $(PKG)/csrc/host/*.hpp $(PKG)/csrc/kernels/*.cuh)
+CU_OBJ  := $(patsubst $(PKG)/csrc/kernels/%.cu,$(BUILD)/%.cu.o,$(CU_SRC))
+CXX_OBJ := $(patsubst $(PKG)/csrc/host/%.cpp,$(BUILD)/%.o,$(CXX_SRC))
+
+.PHONY: all lib oracle clean
+all: lib oracle
+lib: $(PKG)/libtg.so
+
+$(BUILD)/%.cu.o: $(PKG)/csrc/kernels/%.cu $(HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/$*.ptxas.txt || (cat $(BUILD)/$*.ptxas.txt; false)
+
+$(BUILD)/%.o: $(PKG)/csrc/host/%.cpp $(HDRS)
+	@mkdir -p $(BUILD)
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+$(PKG)/libtg.so: $(CU_OBJ) $(CXX_OBJ)
+	$(NVCC) $(ARCH) -shared -o $@ $^ -L$(CUDA)/lib64 -lcudart -Xlinker -rpath,$(CUDA)/lib64
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -rf $(BUILD) $(PKG)/libtg.so
+	$(MAKE) -C oracle clean

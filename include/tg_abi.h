@@ -1,0 +1,214 @@
+/*
+ * tg_abi.h — C-ABI of the B200 mini-batch gradient oracle.
+ *
+ * The reference (BurTorch/tapegrad, /root/reference/proj) is a header-only
+ * C++20 library with no FFI: user code records one sample on a
+ * tapegrad::Tape (tape.hpp:68-353), calls backward_with_scratch
+ * (backprop.hpp:139-184) per sample, accumulates parameter gradients and runs
+ * sgd_step.  This header is the boundary that replaces that
+ * per-sample loop: a recorded tape is described in plain arrays
+ * (tg_tape_desc), compiled once (tg_compile) and then evaluated for a whole
+ * batch on the GPU (tg_forward_backward), followed by the GD update
+ * (tg_gd_update).  Every entry point cites the reference interface it
+ * replaces.  No C++ exception crosses this boundary; failures return a
+ * tg_status and set a thread-local message (tg_last_error).
+ *
+ * Layouts (all device pointers unless stated otherwise):
+ *   inputs        [n_inputs][ld]        scalar (dtype), struct-of-arrays
+ *   index_inputs  [n_index_inputs][ld]  int32, struct-of-arrays
+ *   params        [n_params]            scalar
+ *   loss_out      [batch]               scalar, per-sample root value f_i
+ *   input_grad_out[n_inputs][ld]        scalar, per-sample d f_i / d input
+ *   grad_sum      [n_params]            scalar, sum_i d f_i / d params
+ * ld == batch for every SoA array.
+ */
+#ifndef TG_ABI_H
+#define TG_ABI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status (maps reference exceptions, errors.hpp:9-36, ops.hpp:16-32) ---- */
+typedef enum tg_status {
+  TG_OK = 0,
+  TG_INVALID_ARGUMENT = 1,  /* std::invalid_argument (ops.hpp:41-42, :153-157, :226-229) */
+  TG_CAPACITY = 2,          /* CapacityError (tape.hpp:278-282, :291-295)              */
+  TG_INVALID_HANDLE = 3,    /* InvalidHandle (tape.hpp:268-273)                          */
+  TG_INVALID_CHECKPOINT = 4,/* InvalidCheckpoint (tape.hpp:236-239)                      */
+  TG_DOMAIN = 5,            /* std::domain_error (ops.hpp:16-20)                         */
+  TG_FORMAT = 6,            /* FormatError (errors.hpp:29-31)                            */
+  TG_IO = 7,                /* IoError (errors.hpp:34-36)                                */
+  TG_CUDA = 8,              /* CUDA runtime failure (no reference equivalent)            */
+  TG_UNSUPPORTED = 9        /* program shape outside what a kernel path supports         */
+} tg_status;
+
+typedef enum tg_dtype { TG_F64 = 0, TG_F32 = 1 } tg_dtype;
+
+/* Opaque CUDA stream (cudaStream_t); NULL = legacy default stream. */
+typedef void* tg_stream_t;
+
+/* Thread-local message of the last failing call on this thread.  Domain
+ * errors reproduce the reference text, ops.hpp:17-19:
+ * "<op_name>: input <to_string(value)> is outside the operator domain". */
+const char* tg_last_error(void);
+const char* tg_status_name(tg_status s);
+/* Opcode mnemonic, op_kind.hpp:89-123 (extensions: "stopGradMax"). */
+const char* tg_op_name(uint8_t op);
+
+/* ---- tape description (what the compiler reads from a recorded tape) ---- */
+
+/* Leaf classes.  The reference has one leaf kind (OpKind::Leaf); which leaves
+ * are trainable parameters, per-sample inputs or constants is implicit in user
+ * code (SPEC.md:262-271 ParamRange).  The recorder makes it explicit. */
+enum { TG_NODE_OP = 0, TG_LEAF_PARAM = 1, TG_LEAF_INPUT = 2, TG_LEAF_CONST = 3 };
+
+/* Extension opcode (not in op_kind.hpp): non-differentiable max over its
+ * children, the softmax max-shift "treated as a non-differentiable
+ * stabilization constant".  On a reference tape it is a
+ * Leaf whose value is that max. */
+#define TG_OP_STOPGRAD_MAX 64u
+
+/* A child entry with this bit set is a data-dependent reference (token-id
+ * gather): child = gathers[id].first_node + stride * idx[s][index_col] + offset
+ * where idx[s][col] is the sample's int32 index input, 0 <= idx < n_rows. */
+#define TG_GATHER_FLAG 0x80000000u
+
+typedef struct tg_gather {
+  uint32_t first_node;   /* raw node index of table row 0, element 0 */
+  uint32_t stride;       /* nodes per table row                       */
+  uint32_t n_rows;       /* valid index range                         */
+  uint32_t index_col;    /* which int32 index input selects the row   */
+  uint32_t offset;       /* element within the row                    */
+} tg_gather;
+
+typedef struct tg_tape_desc {
+  uint32_t n_nodes;             /* live nodes, Tape::size() (tape.hpp:101)         */
+  tg_dtype dtype;               /* Tape<Scalar> (tape.hpp:68)                      */
+  const uint8_t* op;            /* [n_nodes] OpKind numbering (op_kind.hpp:10-44)  */
+  const uint64_t* child_offset; /* [n_nodes+1] CSR over the child pool            */
+  const uint32_t* child;        /* [child_offset[n_nodes]] (tape.hpp:257-260)      */
+  const double* constant;       /* [n_nodes] constant slot (tape.hpp:223), nullable */
+  const uint8_t* leaf_class;    /* [n_nodes] TG_NODE_OP / TG_LEAF_*                */
+  const uint32_t* leaf_index;   /* [n_nodes] PARAM: param id, INPUT: input column  */
+  const double* leaf_value;     /* [n_nodes] CONST value / initial PARAM value     */
+  uint32_t n_gathers;
+  const tg_gather* gathers;
+  uint32_t root;                /* backward root (backprop.hpp:140)                */
+  uint32_t n_params;
+  uint32_t n_inputs;
+  uint32_t n_index_inputs;
+} tg_tape_desc;
+
+/* ---- recorder: the reference's recording surface behind a C-ABI ---------- */
+/* Replaces Tape::leaf / emplace and the ops.hpp free functions for non-C++
+ * callers (ctypes); C++ callers use tg::Tape in tg_recorder.hpp directly.     */
+typedef struct tg_recorder* tg_recorder_t;
+
+tg_status tg_recorder_new(tg_dtype dtype, size_t capacity, tg_recorder_t* out);
+void tg_recorder_free(tg_recorder_t r);
+tg_status tg_rec_param(tg_recorder_t r, double value, uint32_t* node_out);
+tg_status tg_rec_input(tg_recorder_t r, uint32_t col, double template_value, uint32_t* node_out);
+tg_status tg_rec_const(tg_recorder_t r, double value, uint32_t* node_out);
+/* Declares a gather reference; template_index picks the row used for the
+ * recorder's eager values.  Returns a child reference with TG_GATHER_FLAG. */
+tg_status tg_rec_gather(tg_recorder_t r, uint32_t first_node, uint32_t stride, uint32_t n_rows,
+                        uint32_t index_col, uint32_t offset, int32_t template_index,
+                        uint32_t* ref_out);
+/* Appends op over children with the reference's eager semantics and checks
+ * (ops.hpp:38-307): arity errors -> TG_INVALID_ARGUMENT, domain -> TG_DOMAIN. */
+tg_status tg_rec_op(tg_recorder_t r, uint8_t op, const uint32_t* children, uint32_t n_children,
+                    double constant, uint32_t* node_out);
+tg_status tg_rec_value(tg_recorder_t r, uint32_t ref, double* value_out);
+tg_status tg_rec_set_root(tg_recorder_t r, uint32_t node);
+/* Fills desc with views into the recorder (valid until the next mutation). */
+tg_status tg_rec_describe(tg_recorder_t r, tg_tape_desc* desc);
+
+/* ---- built-in workloads (BASELINE.json configs) -------------------------- */
+typedef enum tg_model {
+  TG_MODEL_FIG1 = 1,     /* cfg1: Fig. 1 tiny graph            */
+  TG_MODEL_LISTING1 = 2, /* Listing-1 small graph             */
+  TG_MODEL_MOONS_MLP = 3,/* cfg2: scalar MLP 2-16-16-1, hinge + 1e-4 L2      */
+  TG_MODEL_CHAR_MLP = 4, /* cfg3: Bengio char-MLP 27/3/10/200                */
+  TG_MODEL_GPT = 5,      /* cfg4: mini GPT (dims in tg_model_args)           */
+  TG_MODEL_WIDE_MLP = 6  /* cfg5: 784-1024-1024-10 relu MLP (dims in args)   */
+} tg_model;
+
+typedef struct tg_model_args {
+  uint32_t dims[8];   /* model-specific sizes; zeros select BASELINE.json sizes */
+  tg_dtype dtype;
+} tg_model_args;
+
+/* Records one template sample of `model` (parameters initialised from seed). */
+tg_status tg_build_model(tg_model model, const tg_model_args* args, uint64_t seed,
+                         tg_recorder_t* out);
+/* Host-side synthetic batch (SURVEY.md §8d generators, mt19937_64 TestRng
+ * stream as in testing_support.hpp:49-58).  Host pointers. */
+tg_status tg_synth_batch(tg_model model, const tg_model_args* args, uint64_t seed, size_t batch,
+                         void* inputs, int32_t* index_inputs);
+
+/* ---- compile and run ------------------------------------------------------ */
+typedef struct tg_program* tg_program_t;
+
+typedef struct tg_program_info {
+  uint32_t n_params, n_inputs, n_index_inputs;
+  uint32_t n_sample_nodes;   /* per-sample op nodes evaluated on device  */
+  uint32_t n_uniform_nodes;  /* sample-invariant op nodes (hoisted)      */
+  uint32_t n_dense_groups;   /* inner-product groups lowered to dense ops */
+  uint32_t n_fwd_instr, n_bwd_instr;
+  uint64_t n_edges;          /* per-sample child references              */
+  uint32_t tile_samples;     /* samples per CTA tile                     */
+  uint32_t smem_bytes;       /* dynamic shared memory per CTA            */
+  uint32_t storage;          /* 0 = shared-memory tile, 1 = HBM SoA      */
+  tg_dtype dtype;
+} tg_program_info;
+
+/* Lowers the tape to the device program (replaces the per-sample DFS of
+ * backward_with_scratch, backprop.hpp:150-175: topology is sample-invariant,
+ * so the reverse order is computed once here). */
+tg_status tg_compile(const tg_tape_desc* desc, tg_program_t* out);
+tg_status tg_program_info_get(tg_program_t p, tg_program_info* info);
+/* Recorded-order topology for tests: processing order of backward_with_scratch
+ * (backprop.hpp:183), host array of n_order entries. */
+tg_status tg_program_order(tg_program_t p, const uint32_t** order, uint32_t* n_order);
+/* Caller-allocated device workspace (zero allocation on the hot path,
+ * PAPER.md:1357-1359). */
+tg_status tg_workspace_size(tg_program_t p, size_t batch, size_t* bytes);
+
+/* Forward sweep + reverse sweep + batch reduction for `batch` samples:
+ * replaces, per sample, rewind/build (tape.hpp:235-242), zero_grads
+ * (backprop.hpp:100-109), backward_with_scratch (backprop.hpp:139-184) and
+ * the accumulator add of train_step.  grad_sum receives the
+ * sum (not the mean) over the batch.  loss_out / input_grad_out may be NULL. */
+tg_status tg_forward_backward(tg_program_t p, const void* inputs, const int32_t* index_inputs,
+                              size_t batch, const void* params, void* loss_out,
+                              void* input_grad_out, void* grad_sum, void* workspace,
+                              size_t workspace_bytes, tg_stream_t stream);
+
+/* params -= gamma * grad_sum / global_batch (sgd_step).
+ * With several GPUs the caller all-reduces grad_sum first. */
+tg_status tg_gd_update(tg_program_t p, void* params, const void* grad_sum, double gamma,
+                       size_t global_batch, tg_stream_t stream);
+
+/* Fused single-GPU step: forward_backward + gd_update. */
+tg_status tg_train_step(tg_program_t p, const void* inputs, const int32_t* index_inputs,
+                        size_t batch, void* params, void* loss_out, void* grad_sum,
+                        double gamma, void* workspace, size_t workspace_bytes,
+                        tg_stream_t stream);
+
+/* Synchronises `stream` and reports the first per-sample domain violation
+ * seen since the last check as TG_DOMAIN with the reference message. */
+tg_status tg_check_device_error(tg_program_t p, tg_stream_t stream, int64_t* sample_out,
+                                uint32_t* node_out);
+
+/* Number of kernel launches issued by this program since creation. */
+uint64_t tg_launch_count(tg_program_t p);
+void tg_program_free(tg_program_t p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TG_ABI_H */

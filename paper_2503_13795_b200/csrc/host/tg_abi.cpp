@@ -1,0 +1,647 @@
+// tg_abi.cpp — extern "C" boundary of the B200 gradient oracle (include/tg_abi.h).
+//
+// No exception crosses this boundary: every entry point maps the reference's
+// exception taxonomy (errors.hpp:9-36, std::domain_error / invalid_argument
+// of ops.hpp and backprop.hpp) to a tg_status and a thread-local message.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "tg_abi.h"
+#include "tg_models.hpp"
+#include "tg_program.hpp"
+#include "tg_recorder.hpp"
+#include "../kernels/tg_tape.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+tg_status fail(tg_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+template <class F>
+tg_status guard(F&& f) {
+  try {
+    return f();
+  } catch (const tg::CapacityError& e) {
+    return fail(TG_CAPACITY, e.what());
+  } catch (const tg::InvalidHandle& e) {
+    return fail(TG_INVALID_HANDLE, e.what());
+  } catch (const tg::InvalidCheckpoint& e) {
+    return fail(TG_INVALID_CHECKPOINT, e.what());
+  } catch (const std::domain_error& e) {
+    return fail(TG_DOMAIN, e.what());
+  } catch (const std::invalid_argument& e) {
+    return fail(TG_INVALID_ARGUMENT, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(TG_CAPACITY, "out of host memory");
+  } catch (const std::exception& e) {
+    return fail(TG_INVALID_ARGUMENT, e.what());
+  }
+}
+
+#define TG_CUDA_TRY(expr)                                                              \
+  do {                                                                                 \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess) return fail(TG_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <class S>
+struct TgBuilder {
+  using Scalar = S;
+  using VR = tg::ValueRef;
+  tg::Tape<S>& t;
+  VR param(S v) { return t.param(v); }
+  VR constant(S v) { return t.constant(v); }
+  VR input(std::uint32_t c, S v) { return t.input(c, v); }
+  VR gather(VR first, std::uint32_t stride, std::uint32_t n_rows, std::uint32_t col, std::uint32_t off,
+            std::int32_t idx) {
+    return t.gather(first, stride, n_rows, col, off, idx);
+  }
+  VR stopgrad_max(std::span<const VR> xs) { return tg::stopgrad_max(t, xs); }
+  VR unary(std::uint8_t op, VR x) { return tg::unary(t, static_cast<tg::OpKind>(op), x); }
+  VR binary(std::uint8_t op, VR x, VR y) { return tg::binary(t, static_cast<tg::OpKind>(op), x, y); }
+  VR mul_by_constant(VR x, S c) { return tg::mul_by_constant(t, x, c); }
+  VR varying(std::uint8_t op, std::span<const VR> xs) { return tg::varying(t, static_cast<tg::OpKind>(op), xs); }
+  VR ip(std::span<const VR> x, std::span<const VR> y) { return tg::inner_product(t, x, y); }
+  VR ipwb(std::span<const VR> x, std::span<const VR> y, VR b) { return tg::inner_product_with_bias(t, x, y, b); }
+};
+
+}  // namespace
+
+struct tg_recorder {
+  tg_dtype dtype;
+  std::unique_ptr<tg::Tape<double>> t64;
+  std::unique_ptr<tg::Tape<float>> t32;
+  template <class F> auto visit(F&& f) {
+    if (dtype == TG_F64) return f(*t64);
+    return f(*t32);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// device program
+// ---------------------------------------------------------------------------
+
+struct tg_program {
+  tgc::Program P;
+  bool uploaded = false;
+  std::vector<void*> allocs;
+  tgc::Instr *d_fwd = nullptr, *d_bwd = nullptr, *d_ufwd = nullptr, *d_ubwd = nullptr;
+  std::uint32_t *d_opnd = nullptr, *d_oaux = nullptr, *d_zero = nullptr, *d_inrows = nullptr, *d_cand = nullptr,
+                *d_termoff = nullptr, *d_destuv = nullptr;
+  std::uint8_t* d_oflag = nullptr;
+  tgc::GatherTable *d_ug = nullptr, *d_sg = nullptr;
+  tgc::Term* d_terms = nullptr;
+  void* d_consts = nullptr;
+  unsigned long long* d_err_key = nullptr;
+  double* d_err_val = nullptr;
+  std::uint32_t* d_err_op = nullptr;
+  // launch configuration
+  bool smem = true;
+  unsigned S = 128;
+  std::size_t ld_smem = 129;
+  std::size_t smem_bytes = 0;
+  unsigned occ_bound = 1;
+  int occ = 0;
+  int nsm = 148;
+  std::uint64_t launches = 0;
+  // last main launch, for domain-error diagnosis
+  bool have_last = false;
+  std::vector<unsigned char> last_args;
+  std::size_t last_batch = 0;
+  ~tg_program() {
+    for (void* p : allocs) cudaFree(p);
+  }
+  std::size_t tsz() const { return P.dtype == TG_F64 ? 8 : 4; }
+  std::uint32_t n_dest() const { return static_cast<std::uint32_t>(P.dest_uv.size()); }
+};
+
+namespace {
+
+constexpr std::size_t kSmemBudget = 200 * 1024;
+constexpr unsigned kMaxOcc = 32;
+
+void choose_config(tg_program& pr) {
+  const std::size_t row_bytes = 2 * pr.tsz();
+  pr.smem = false;
+  for (unsigned S : {256u, 128u, 64u, 32u}) {
+    const std::size_t ld = S + 1;
+    const std::size_t bytes = std::max<std::size_t>(1, pr.P.n_rows) * ld * row_bytes;
+    if (bytes <= kSmemBudget) {
+      pr.smem = true;
+      pr.S = S;
+      pr.ld_smem = ld;
+      pr.smem_bytes = bytes;
+      break;
+    }
+  }
+  if (!pr.smem) { pr.S = 128; pr.smem_bytes = 0; }
+  unsigned bound = std::min(kMaxOcc, 2048u / pr.S);
+  if (pr.smem) bound = std::min<unsigned>(bound, static_cast<unsigned>((228 * 1024) / (pr.smem_bytes + 1024)));
+  pr.occ_bound = std::max(1u, bound);
+}
+
+std::size_t grid_cap(const tg_program& pr, std::size_t batch) {
+  const std::size_t tiles = (batch + pr.S - 1) / pr.S;
+  std::size_t cap = std::size_t(148) * pr.occ_bound;
+  if (!pr.smem) cap = std::min<std::size_t>(cap, 148 * 8);
+  return std::max<std::size_t>(1, std::min(tiles, cap));
+}
+
+std::size_t grid_for(const tg_program& pr, std::size_t batch) {
+  std::size_t g = grid_cap(pr, batch);
+  if (pr.occ > 0) g = std::min<std::size_t>(g, std::size_t(pr.occ) * pr.nsm);
+  return std::max<std::size_t>(1, g);
+}
+
+std::size_t align_up(std::size_t x) { return (x + 255) & ~std::size_t(255); }
+
+struct Layout {
+  std::size_t uv, ug, partial, gv, gg, total;
+};
+Layout layout(const tg_program& pr, std::size_t batch) {
+  const std::size_t t = pr.tsz();
+  const std::size_t grid = grid_cap(pr, batch);
+  Layout L{};
+  std::size_t off = 0;
+  L.uv = off; off = align_up(off + std::max<std::size_t>(1, pr.P.n_uv) * t);
+  L.ug = off; off = align_up(off + std::max<std::size_t>(1, pr.P.n_uv) * t);
+  L.partial = off; off = align_up(off + grid * std::max<std::uint32_t>(1, pr.n_dest()) * t);
+  L.gv = off;
+  if (!pr.smem) off = align_up(off + std::size_t(pr.P.n_rows) * grid * pr.S * t);
+  L.gg = off;
+  if (!pr.smem) off = align_up(off + std::size_t(pr.P.n_rows) * grid * pr.S * t);
+  L.total = off;
+  return L;
+}
+
+template <class V>
+tg_status upload_vec(tg_program& pr, const std::vector<V>& v, V** out) {
+  *out = nullptr;
+  if (v.empty()) return TG_OK;
+  void* p = nullptr;
+  TG_CUDA_TRY(cudaMalloc(&p, v.size() * sizeof(V)));
+  pr.allocs.push_back(p);
+  TG_CUDA_TRY(cudaMemcpy(p, v.data(), v.size() * sizeof(V), cudaMemcpyHostToDevice));
+  *out = static_cast<V*>(p);
+  return TG_OK;
+}
+
+#define TG_TRY(expr)                          \
+  do {                                        \
+    tg_status s_ = (expr);                    \
+    if (s_ != TG_OK) return s_;               \
+  } while (0)
+
+tg_status upload(tg_program& pr) {
+  if (pr.uploaded) return TG_OK;
+  int dev = 0;
+  TG_CUDA_TRY(cudaGetDevice(&dev));
+  TG_CUDA_TRY(cudaDeviceGetAttribute(&pr.nsm, cudaDevAttrMultiProcessorCount, dev));
+  const tgc::Program& P = pr.P;
+  TG_TRY(upload_vec(pr, P.fwd, &pr.d_fwd));
+  TG_TRY(upload_vec(pr, P.bwd, &pr.d_bwd));
+  TG_TRY(upload_vec(pr, P.ufwd, &pr.d_ufwd));
+  TG_TRY(upload_vec(pr, P.ubwd, &pr.d_ubwd));
+  TG_TRY(upload_vec(pr, P.opnd, &pr.d_opnd));
+  TG_TRY(upload_vec(pr, P.oflag, &pr.d_oflag));
+  TG_TRY(upload_vec(pr, P.oaux, &pr.d_oaux));
+  TG_TRY(upload_vec(pr, P.zero_rows, &pr.d_zero));
+  TG_TRY(upload_vec(pr, P.input_rows, &pr.d_inrows));
+  TG_TRY(upload_vec(pr, P.ugather, &pr.d_ug));
+  TG_TRY(upload_vec(pr, P.sgather, &pr.d_sg));
+  TG_TRY(upload_vec(pr, P.cand, &pr.d_cand));
+  TG_TRY(upload_vec(pr, P.term_off, &pr.d_termoff));
+  TG_TRY(upload_vec(pr, P.terms, &pr.d_terms));
+  TG_TRY(upload_vec(pr, P.dest_uv, &pr.d_destuv));
+  const std::uint32_t nc = P.n_uv - P.uv_const_base;
+  if (P.dtype == TG_F64) {
+    std::vector<double> c(P.uv_init.begin() + P.uv_const_base, P.uv_init.end());
+    double* d = nullptr;
+    TG_TRY(upload_vec(pr, c, &d));
+    pr.d_consts = d;
+  } else {
+    std::vector<float> c(nc);
+    for (std::uint32_t i = 0; i < nc; ++i) c[i] = static_cast<float>(P.uv_init[P.uv_const_base + i]);
+    float* d = nullptr;
+    TG_TRY(upload_vec(pr, c, &d));
+    pr.d_consts = d;
+  }
+  void* e = nullptr;
+  TG_CUDA_TRY(cudaMalloc(&e, 64));
+  pr.allocs.push_back(e);
+  pr.d_err_key = static_cast<unsigned long long*>(e);
+  pr.d_err_val = reinterpret_cast<double*>(static_cast<char*>(e) + 8);
+  pr.d_err_op = reinterpret_cast<std::uint32_t*>(static_cast<char*>(e) + 16);
+  TG_CUDA_TRY(cudaMemset(e, 0xff, 8));
+  TG_CUDA_TRY(cudaMemset(static_cast<char*>(e) + 16, 0xff, 4));
+  if (P.dtype == TG_F64) pr.occ = tgk::tape_occupancy<double>(pr.smem, pr.S, pr.smem_bytes);
+  else pr.occ = tgk::tape_occupancy<float>(pr.smem, pr.S, pr.smem_bytes);
+  cudaGetLastError();
+  pr.uploaded = true;
+  return TG_OK;
+}
+
+template <class T>
+tg_status run_fb(tg_program& pr, const void* inputs, const std::int32_t* idx, std::size_t batch, const void* params,
+                 void* loss, void* igrad, void* grad_sum, void* ws, std::size_t ws_bytes, cudaStream_t st) {
+  TG_TRY(upload(pr));
+  const tgc::Program& P = pr.P;
+  const Layout L = layout(pr, batch);
+  if (ws_bytes < L.total)
+    return fail(TG_INVALID_ARGUMENT, "tg_forward_backward: workspace of " + std::to_string(ws_bytes) +
+                                         " bytes, need " + std::to_string(L.total));
+  if (batch > 0 && P.n_inputs && !inputs) return fail(TG_INVALID_ARGUMENT, "tg_forward_backward: inputs is NULL");
+  if (batch > 0 && P.n_index_inputs && !idx) return fail(TG_INVALID_ARGUMENT, "tg_forward_backward: index_inputs is NULL");
+  if (P.n_params && !params) return fail(TG_INVALID_ARGUMENT, "tg_forward_backward: params is NULL");
+  char* w = static_cast<char*>(ws);
+  T* UV = reinterpret_cast<T*>(w + L.uv);
+  T* UG = reinterpret_cast<T*>(w + L.ug);
+  T* partial = reinterpret_cast<T*>(w + L.partial);
+
+  tgk::UniformArgs<T> ua{};
+  ua.instr = pr.d_ufwd;
+  ua.opnd = pr.d_opnd;
+  ua.params = static_cast<const T*>(params);
+  ua.consts = static_cast<const T*>(pr.d_consts);
+  ua.UV = UV;
+  ua.UG = UG;
+  ua.grad_sum = static_cast<T*>(grad_sum);
+  ua.err_key = pr.d_err_key;
+  ua.err_val = pr.d_err_val;
+  ua.err_op = pr.d_err_op;
+  ua.batch = batch;
+  ua.n_instr = static_cast<std::uint32_t>(P.ufwd.size());
+  ua.n_params = P.n_params;
+  ua.n_const = P.n_uv - P.uv_const_base;
+  ua.const_base = P.uv_const_base;
+  ua.n_uv = P.n_uv;
+  ua.root_uv = P.root_uv;
+  TG_CUDA_TRY(tgk::launch_uniform_fwd<T>(ua, st));
+  ++pr.launches;
+
+  const std::size_t grid = grid_for(pr, batch);
+  if (batch > 0 && P.root_row != tgc::kNone) {
+    tgk::MainArgs<T> ma{};
+    ma.fwd = pr.d_fwd;
+    ma.bwd = pr.d_bwd;
+    ma.opnd = pr.d_opnd;
+    ma.oflag = pr.d_oflag;
+    ma.oaux = pr.d_oaux;
+    ma.zero_rows = pr.d_zero;
+    ma.input_rows = pr.d_inrows;
+    ma.ug = pr.d_ug;
+    ma.sg = pr.d_sg;
+    ma.cand = pr.d_cand;
+    ma.term_off = pr.d_termoff;
+    ma.terms = pr.d_terms;
+    ma.UV = UV;
+    ma.inputs = static_cast<const T*>(inputs);
+    ma.idx = idx;
+    ma.loss = static_cast<T*>(loss);
+    ma.igrad = static_cast<T*>(igrad);
+    ma.partial = partial;
+    ma.gV = reinterpret_cast<T*>(w + L.gv);
+    ma.gG = reinterpret_cast<T*>(w + L.gg);
+    ma.err_key = pr.d_err_key;
+    ma.err_val = pr.d_err_val;
+    ma.err_op = pr.d_err_op;
+    ma.batch = batch;
+    ma.ld = pr.smem ? pr.ld_smem : grid * pr.S;
+    ma.diag_sample = -1;
+    ma.n_fwd = static_cast<std::uint32_t>(P.fwd.size());
+    ma.n_bwd = static_cast<std::uint32_t>(P.bwd.size());
+    ma.n_zero = static_cast<std::uint32_t>(P.zero_rows.size());
+    ma.n_inputs = P.n_inputs;
+    ma.n_dest = pr.n_dest();
+    ma.n_rows = P.n_rows;
+    ma.S = pr.S;
+    ma.root_row = P.root_row;
+    TG_CUDA_TRY(tgk::launch_tape<T>(ma, pr.smem, static_cast<unsigned>(grid), pr.S, pr.smem_bytes, st));
+    ++pr.launches;
+    pr.last_args.assign(reinterpret_cast<unsigned char*>(&ma), reinterpret_cast<unsigned char*>(&ma) + sizeof(ma));
+    pr.have_last = true;
+    pr.last_batch = batch;
+
+    tgk::ReduceArgs<T> ra{partial, pr.d_destuv, UG, pr.n_dest(), static_cast<std::uint32_t>(grid)};
+    if (ra.n_dest) {
+      TG_CUDA_TRY(tgk::launch_reduce<T>(ra, st));
+      ++pr.launches;
+    }
+  }
+  ua.instr = pr.d_ubwd;
+  ua.n_instr = static_cast<std::uint32_t>(P.ubwd.size());
+  TG_CUDA_TRY(tgk::launch_uniform_bwd<T>(ua, st));
+  ++pr.launches;
+  return TG_OK;
+}
+
+template <class T>
+tg_status diagnose(tg_program& pr, std::int64_t sample, cudaStream_t st) {
+  if (!pr.have_last) return TG_OK;
+  tgk::MainArgs<T> ma;
+  std::memcpy(&ma, pr.last_args.data(), sizeof(ma));
+  ma.diag_sample = sample;
+  ma.loss = nullptr;
+  ma.igrad = nullptr;
+  TG_CUDA_TRY(tgk::launch_tape<T>(ma, pr.smem, 1, pr.S, pr.smem_bytes, st));
+  ++pr.launches;
+  return TG_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* tg_last_error(void) { return g_err.c_str(); }
+
+const char* tg_status_name(tg_status s) {
+  switch (s) {
+    case TG_OK: return "TG_OK";
+    case TG_INVALID_ARGUMENT: return "TG_INVALID_ARGUMENT";
+    case TG_CAPACITY: return "TG_CAPACITY";
+    case TG_INVALID_HANDLE: return "TG_INVALID_HANDLE";
+    case TG_INVALID_CHECKPOINT: return "TG_INVALID_CHECKPOINT";
+    case TG_DOMAIN: return "TG_DOMAIN";
+    case TG_FORMAT: return "TG_FORMAT";
+    case TG_IO: return "TG_IO";
+    case TG_CUDA: return "TG_CUDA";
+    case TG_UNSUPPORTED: return "TG_UNSUPPORTED";
+  }
+  return "?";
+}
+
+const char* tg_op_name(uint8_t op) {
+  static const char* const names[] = {
+      "leaf", "relu", "tanh", "exp", "negativeLog", "sigmoid", "inv", "sqr", "pow3", "logarithm",
+      "sqrt", "invSqrt", "add", "sub", "mul", "mulByConstant", "div", "mean", "addSquares",
+      "meanSquares", "negativeMean", "reduceSum", "reduceSub", "reduceMul", "reduceMean",
+      "reduceSumOfSquares", "reduceMeanSquares", "reduceNegativeMean", "innerProduct",
+      "innerProductWithBias"};
+  if (op < sizeof(names) / sizeof(names[0])) return names[op];
+  if (op == TG_OP_STOPGRAD_MAX) return "stopGradMax";
+  return "?";
+}
+
+tg_status tg_recorder_new(tg_dtype dtype, size_t capacity, tg_recorder_t* out) {
+  return guard([&] {
+    if (!out) return fail(TG_INVALID_ARGUMENT, "tg_recorder_new: out is NULL");
+    if (dtype != TG_F64 && dtype != TG_F32) return fail(TG_INVALID_ARGUMENT, "tg_recorder_new: bad dtype");
+    auto r = std::make_unique<tg_recorder>();
+    r->dtype = dtype;
+    if (dtype == TG_F64) r->t64 = std::make_unique<tg::Tape<double>>(capacity);
+    else r->t32 = std::make_unique<tg::Tape<float>>(capacity);
+    *out = r.release();
+    return TG_OK;
+  });
+}
+
+void tg_recorder_free(tg_recorder_t r) { delete r; }
+
+tg_status tg_rec_param(tg_recorder_t r, double v, uint32_t* node) {
+  return guard([&] {
+    *node = r->visit([&](auto& t) { return t.param(static_cast<typename std::decay_t<decltype(t)>::scalar_type>(v)).index; });
+    return TG_OK;
+  });
+}
+tg_status tg_rec_input(tg_recorder_t r, uint32_t col, double v, uint32_t* node) {
+  return guard([&] {
+    *node = r->visit([&](auto& t) { return t.input(col, static_cast<typename std::decay_t<decltype(t)>::scalar_type>(v)).index; });
+    return TG_OK;
+  });
+}
+tg_status tg_rec_const(tg_recorder_t r, double v, uint32_t* node) {
+  return guard([&] {
+    *node = r->visit([&](auto& t) { return t.constant(static_cast<typename std::decay_t<decltype(t)>::scalar_type>(v)).index; });
+    return TG_OK;
+  });
+}
+tg_status tg_rec_gather(tg_recorder_t r, uint32_t first, uint32_t stride, uint32_t n_rows, uint32_t col,
+                        uint32_t offset, int32_t tidx, uint32_t* ref) {
+  return guard([&] {
+    *ref = r->visit([&](auto& t) { return t.gather(tg::ValueRef{first}, stride, n_rows, col, offset, tidx).index; });
+    return TG_OK;
+  });
+}
+tg_status tg_rec_op(tg_recorder_t r, uint8_t op, const uint32_t* children, uint32_t n, double c, uint32_t* node) {
+  return guard([&] {
+    std::vector<tg::ValueRef> k(n);
+    for (uint32_t i = 0; i < n; ++i) k[i].index = children[i];
+    *node = r->visit([&](auto& t) -> uint32_t {
+      using S = typename std::decay_t<decltype(t)>::scalar_type;
+      const auto kind = static_cast<tg::OpKind>(op);
+      if (op == 0) throw std::invalid_argument("tg_rec_op: use tg_rec_param / tg_rec_input / tg_rec_const for leaves");
+      if (kind == tg::OpKind::MulByConst) {
+        if (n != 1) throw std::invalid_argument("mulByConstant: needs 1 child");
+        return tg::mul_by_constant(t, k[0], static_cast<S>(c)).index;
+      }
+      if (kind == tg::OpKind::StopGradMax) return tg::stopgrad_max(t, std::span<const tg::ValueRef>(k)).index;
+      switch (tg::arity_of(kind)) {
+        case tg::OpArity::Unary:
+          if (n != 1) throw std::invalid_argument(std::string("unary: op ") + tg_op_name(op) + " needs 1 child");
+          return tg::unary(t, kind, k[0]).index;
+        case tg::OpArity::Binary:
+          if (n != 2) throw std::invalid_argument(std::string("binary: op ") + tg_op_name(op) + " needs 2 children");
+          return tg::binary(t, kind, k[0], k[1]).index;
+        default: break;
+      }
+      if (kind == tg::OpKind::InnerProductNoBias) {
+        if (n % 2) throw std::invalid_argument("innerProduct: sequence lengths differ");
+        return tg::inner_product(t, std::span<const tg::ValueRef>(k.data(), n / 2),
+                                 std::span<const tg::ValueRef>(k.data() + n / 2, n / 2)).index;
+      }
+      if (kind == tg::OpKind::InnerProductWithBias) {
+        if (n % 2 == 0) throw std::invalid_argument("innerProductWithBias: sequence lengths differ");
+        const uint32_t m = (n - 1) / 2;
+        return tg::inner_product_with_bias(t, std::span<const tg::ValueRef>(k.data(), m),
+                                           std::span<const tg::ValueRef>(k.data() + m, m), k[n - 1]).index;
+      }
+      if (op > 29) throw std::invalid_argument("tg_rec_op: unknown opcode " + std::to_string(op));
+      return tg::varying(t, kind, std::span<const tg::ValueRef>(k)).index;
+    });
+    return TG_OK;
+  });
+}
+tg_status tg_rec_value(tg_recorder_t r, uint32_t ref, double* v) {
+  return guard([&] {
+    *v = r->visit([&](auto& t) { return static_cast<double>(t.value_of(tg::ValueRef{ref})); });
+    return TG_OK;
+  });
+}
+tg_status tg_rec_set_root(tg_recorder_t r, uint32_t node) {
+  return guard([&] {
+    r->visit([&](auto& t) { t.set_root(tg::ValueRef{node}); return 0; });
+    return TG_OK;
+  });
+}
+tg_status tg_rec_describe(tg_recorder_t r, tg_tape_desc* d) {
+  return guard([&] {
+    *d = r->visit([&](auto& t) { return t.describe(); });
+    return TG_OK;
+  });
+}
+
+tg_status tg_build_model(tg_model model, const tg_model_args* args, uint64_t seed, tg_recorder_t* out) {
+  return guard([&] {
+    const tgm::Dims D = tgm::Dims::resolve(model, args ? args->dims : nullptr);
+    const tg_dtype dt = args ? args->dtype : TG_F64;
+    std::uint32_t ni = 0, nk = 0;
+    tgm::io_shape(model, D, ni, nk);
+    std::vector<double> x(ni);
+    std::vector<std::int32_t> k(nk);
+    tgm::synth<double>(model, D, seed + 1, 1, x.data(), k.data());  // template sample
+    auto r = std::make_unique<tg_recorder>();
+    r->dtype = dt;
+    if (dt == TG_F64) r->t64 = std::make_unique<tg::Tape<double>>(std::size_t(1) << 16);
+    else r->t32 = std::make_unique<tg::Tape<float>>(std::size_t(1) << 16);
+    r->visit([&](auto& t) {
+      using S = typename std::decay_t<decltype(t)>::scalar_type;
+      TgBuilder<S> b{t};
+      const auto P = tgm::make_params(b, model, D, seed);
+      const tgm::Sample smp{x.data(), k.data()};
+      const auto root = tgm::build_sample(b, model, D, P, smp);
+      t.set_root(root);
+      return 0;
+    });
+    *out = r.release();
+    return TG_OK;
+  });
+}
+
+tg_status tg_synth_batch(tg_model model, const tg_model_args* args, uint64_t seed, size_t batch, void* inputs,
+                         int32_t* index_inputs) {
+  return guard([&] {
+    const tgm::Dims D = tgm::Dims::resolve(model, args ? args->dims : nullptr);
+    const tg_dtype dt = args ? args->dtype : TG_F64;
+    if (dt == TG_F64) tgm::synth<double>(model, D, seed, batch, static_cast<double*>(inputs), index_inputs);
+    else tgm::synth<float>(model, D, seed, batch, static_cast<float*>(inputs), index_inputs);
+    return TG_OK;
+  });
+}
+
+tg_status tg_compile(const tg_tape_desc* desc, tg_program_t* out) {
+  return guard([&] {
+    if (!desc || !out) return fail(TG_INVALID_ARGUMENT, "tg_compile: NULL argument");
+    auto pr = std::make_unique<tg_program>();
+    pr->P = tgc::compile(*desc);
+    choose_config(*pr);
+    *out = pr.release();
+    return TG_OK;
+  });
+}
+
+tg_status tg_program_info_get(tg_program_t p, tg_program_info* info) {
+  return guard([&] {
+    const tgc::Program& P = p->P;
+    tg_program_info i{};
+    i.n_params = P.n_params;
+    i.n_inputs = P.n_inputs;
+    i.n_index_inputs = P.n_index_inputs;
+    i.n_sample_nodes = P.n_sample_nodes;
+    i.n_uniform_nodes = P.n_uniform_nodes;
+    i.n_dense_groups = static_cast<uint32_t>(P.dense.size());
+    i.n_fwd_instr = static_cast<uint32_t>(P.fwd.size());
+    i.n_bwd_instr = static_cast<uint32_t>(P.bwd.size());
+    i.n_edges = P.n_edges;
+    i.tile_samples = p->S;
+    i.smem_bytes = static_cast<uint32_t>(p->smem_bytes);
+    i.storage = p->smem ? 0 : 1;
+    i.dtype = P.dtype;
+    *info = i;
+    return TG_OK;
+  });
+}
+
+tg_status tg_program_order(tg_program_t p, const uint32_t** order, uint32_t* n) {
+  *order = p->P.order.data();
+  *n = static_cast<uint32_t>(p->P.order.size());
+  return TG_OK;
+}
+
+tg_status tg_workspace_size(tg_program_t p, size_t batch, size_t* bytes) {
+  return guard([&] {
+    *bytes = layout(*p, batch).total;
+    return TG_OK;
+  });
+}
+
+tg_status tg_forward_backward(tg_program_t p, const void* inputs, const int32_t* idx, size_t batch, const void* params,
+                              void* loss, void* igrad, void* grad_sum, void* ws, size_t ws_bytes, tg_stream_t stream) {
+  return guard([&] {
+    if (!p) return fail(TG_INVALID_HANDLE, "tg_forward_backward: NULL program");
+    auto st = static_cast<cudaStream_t>(stream);
+    if (p->P.dtype == TG_F64) return run_fb<double>(*p, inputs, idx, batch, params, loss, igrad, grad_sum, ws, ws_bytes, st);
+    return run_fb<float>(*p, inputs, idx, batch, params, loss, igrad, grad_sum, ws, ws_bytes, st);
+  });
+}
+
+tg_status tg_gd_update(tg_program_t p, void* params, const void* grad_sum, double gamma, size_t global_batch,
+                       tg_stream_t stream) {
+  return guard([&] {
+    auto st = static_cast<cudaStream_t>(stream);
+    if (global_batch == 0) return fail(TG_INVALID_ARGUMENT, "train_step: batch empty");
+    if (p->P.dtype == TG_F64)
+      TG_CUDA_TRY(tgk::launch_gd<double>(static_cast<double*>(params), static_cast<const double*>(grad_sum),
+                                         p->P.n_params, gamma, static_cast<double>(global_batch), st));
+    else
+      TG_CUDA_TRY(tgk::launch_gd<float>(static_cast<float*>(params), static_cast<const float*>(grad_sum),
+                                        p->P.n_params, gamma, static_cast<double>(global_batch), st));
+    ++p->launches;
+    return TG_OK;
+  });
+}
+
+tg_status tg_train_step(tg_program_t p, const void* inputs, const int32_t* idx, size_t batch, void* params, void* loss,
+                        void* grad_sum, double gamma, void* ws, size_t ws_bytes, tg_stream_t stream) {
+  tg_status s = tg_forward_backward(p, inputs, idx, batch, params, loss, nullptr, grad_sum, ws, ws_bytes, stream);
+  if (s != TG_OK) return s;
+  return tg_gd_update(p, params, grad_sum, gamma, batch, stream);
+}
+
+tg_status tg_check_device_error(tg_program_t p, tg_stream_t stream, int64_t* sample_out, uint32_t* node_out) {
+  return guard([&] {
+    if (!p->uploaded) return TG_OK;
+    auto st = static_cast<cudaStream_t>(stream);
+    TG_CUDA_TRY(cudaStreamSynchronize(st));
+    unsigned long long key = 0;
+    TG_CUDA_TRY(cudaMemcpy(&key, p->d_err_key, 8, cudaMemcpyDeviceToHost));
+    if (key == ~0ull) return TG_OK;
+    const std::int64_t sample = static_cast<std::int64_t>(key >> 32);
+    const std::uint32_t node = static_cast<std::uint32_t>(key & 0xffffffffu);
+    if (sample_out) *sample_out = sample;
+    if (node_out) *node_out = node;
+    std::uint32_t op = 0xffffffffu;
+    TG_CUDA_TRY(cudaMemcpy(&op, p->d_err_op, 4, cudaMemcpyDeviceToHost));
+    if (op == 0xffffffffu && node != 0xfffffffeu) {
+      tg_status s = p->P.dtype == TG_F64 ? diagnose<double>(*p, sample, st) : diagnose<float>(*p, sample, st);
+      if (s != TG_OK) return s;
+      TG_CUDA_TRY(cudaStreamSynchronize(st));
+      TG_CUDA_TRY(cudaMemcpy(&op, p->d_err_op, 4, cudaMemcpyDeviceToHost));
+    }
+    double val = 0;
+    TG_CUDA_TRY(cudaMemcpy(&val, p->d_err_val, 8, cudaMemcpyDeviceToHost));
+    TG_CUDA_TRY(cudaMemset(p->d_err_key, 0xff, 8));
+    TG_CUDA_TRY(cudaMemset(p->d_err_op, 0xff, 4));
+    if (node == 0xfffffffeu)
+      return fail(TG_INVALID_ARGUMENT, "gather: token index outside the table at sample " + std::to_string(sample));
+    return fail(TG_DOMAIN, std::string(tg_op_name(static_cast<uint8_t>(op))) + ": input " + std::to_string(val) +
+                               " is outside the operator domain");
+  });
+}
+
+uint64_t tg_launch_count(tg_program_t p) { return p ? p->launches : 0; }
+
+void tg_program_free(tg_program_t p) { delete p; }
+
+}  // extern "C"

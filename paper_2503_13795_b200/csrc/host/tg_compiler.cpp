@@ -1,0 +1,401 @@
+// tg_compiler.cpp — lowers a recorded tape to the device program.
+//
+// What the reference does per sample, this does once per tape:
+//   * the reverse processing order of backward_with_scratch (iterative DFS
+//     post-order from the root, children in stored order, zero-child nodes
+//     skipped, backprop.hpp:150-183) depends only on topology, which is
+//     sample-invariant, so it is computed here a single time;
+//   * zero_grads (backprop.hpp:100-109) becomes "first contribution stores":
+//     the compiler knows which reverse-sweep write reaches each adjoint row
+//     first;
+//   * accumulator adds of the parameter range become
+//     batch-reduction terms: for an inner product the contribution of weight
+//     y_k is g * x_k (ops.hpp:436-452), so its batch sum is sum_s g(s) x_k(s),
+//     a contraction over the sample axis evaluated per CTA tile.
+#include <algorithm>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+
+#include "tg_program.hpp"
+
+namespace tgc {
+namespace {
+
+enum Cls : std::uint8_t { cParam, cInput, cConst, cUniform, cSample };
+
+constexpr std::uint8_t Leaf = 0, MulByConst = 15, Add = 12, Sub = 13, Mul = 14, Mean = 17,
+                       NegativeMean = 20, AddVarying = 21, SubVarying = 22, MeanVarying = 24,
+                       NegativeMeanVarying = 27, IPNoBias = 28, IPWithBias = 29,
+                       StopGradMax = TG_OP_STOPGRAD_MAX;
+
+bool valid_op(std::uint8_t op) { return op <= 29 || op == StopGradMax; }
+
+std::uint32_t arity_min(std::uint8_t op) {
+  if (op == Leaf) return 0;
+  if (op <= 11 || op == MulByConst) return 1;
+  if (op <= 20) return 2;
+  return 1;
+}
+
+struct Ctx {
+  const tg_tape_desc& d;
+  Program& P;
+  std::vector<std::uint8_t> cls;
+  std::vector<std::uint32_t> row, uv;         // per node
+  std::vector<std::uint32_t> grow;            // per gather: materialised row (uniform tables)
+  std::vector<std::uint32_t> sg_of;           // per gather: slot-gather table id
+  std::vector<std::uint8_t> gkind;            // 0 unused, 1 uniform table, 2 slot table
+
+  std::uint32_t nkids(std::uint32_t i) const {
+    return static_cast<std::uint32_t>(d.child_offset[i + 1] - d.child_offset[i]);
+  }
+  const std::uint32_t* kids(std::uint32_t i) const { return d.child + d.child_offset[i]; }
+  std::uint32_t cand(std::uint32_t g, std::uint32_t r) const {
+    const tg_gather& G = d.gathers[g];
+    return G.first_node + G.stride * r + G.offset;
+  }
+};
+
+void validate(const tg_tape_desc& d) {
+  if (d.n_nodes == 0) throw std::invalid_argument("tg_compile: empty tape");
+  if (d.root >= d.n_nodes)
+    throw std::invalid_argument("backward: stale root index " + std::to_string(d.root));
+  if (d.child_offset[0] != 0) throw std::invalid_argument("tg_compile: child_offset[0] != 0");
+  for (std::uint32_t g = 0; g < d.n_gathers; ++g) {
+    const tg_gather& G = d.gathers[g];
+    if (G.n_rows == 0) throw std::invalid_argument("tg_compile: gather with zero rows");
+    const std::uint64_t last = std::uint64_t(G.first_node) + std::uint64_t(G.stride) * (G.n_rows - 1) + G.offset;
+    if (last >= d.n_nodes) throw std::invalid_argument("tg_compile: gather table past tape end");
+    if (G.index_col >= d.n_index_inputs) throw std::invalid_argument("tg_compile: gather index column out of range");
+  }
+  for (std::uint32_t i = 0; i < d.n_nodes; ++i) {
+    const std::uint8_t op = d.op[i];
+    if (!valid_op(op)) throw std::invalid_argument("tg_compile: bad opcode " + std::to_string(op) + " at node " + std::to_string(i));
+    const std::uint64_t n = d.child_offset[i + 1] - d.child_offset[i];
+    if (d.child_offset[i + 1] < d.child_offset[i]) throw std::invalid_argument("tg_compile: child offsets not monotone");
+    if (op == Leaf) {
+      if (n != 0) throw std::invalid_argument("tg_compile: leaf with children");
+      const std::uint8_t c = d.leaf_class[i];
+      if (c == TG_LEAF_PARAM && d.leaf_index[i] >= d.n_params) throw std::invalid_argument("tg_compile: param index out of range");
+      if (c == TG_LEAF_INPUT && d.leaf_index[i] >= d.n_inputs) throw std::invalid_argument("tg_compile: input column out of range");
+      if (c != TG_LEAF_PARAM && c != TG_LEAF_INPUT && c != TG_LEAF_CONST) throw std::invalid_argument("tg_compile: leaf without a class");
+      continue;
+    }
+    if (n < arity_min(op)) throw std::invalid_argument(std::string(tg_op_name(op)) + ": empty input sequence");
+    if (op <= 11 || op == MulByConst) { if (n != 1) throw std::invalid_argument(std::string("unary: op ") + tg_op_name(op) + " needs 1 child"); }
+    else if (op <= 20) { if (n != 2) throw std::invalid_argument(std::string("binary: op ") + tg_op_name(op) + " needs 2 children"); }
+    else if (op == IPNoBias && (n % 2) != 0) throw std::invalid_argument("innerProduct: odd child count");
+    else if (op == IPWithBias && (n % 2) != 1) throw std::invalid_argument("innerProductWithBias: even child count");
+    const std::uint32_t* k = d.child + d.child_offset[i];
+    for (std::uint64_t j = 0; j < n; ++j) {
+      const std::uint32_t c = k[j];
+      if (c & TG_GATHER_FLAG) {
+        if ((c & ~TG_GATHER_FLAG) >= d.n_gathers) throw std::invalid_argument("tg_compile: bad gather id");
+        const tg_gather& G = d.gathers[c & ~TG_GATHER_FLAG];
+        if (std::uint64_t(G.first_node) + std::uint64_t(G.stride) * (G.n_rows - 1) + G.offset >= i)
+          throw std::invalid_argument("tg_compile: gather table not built before its consumer");
+      } else if (c >= i) {
+        throw std::invalid_argument("tg_compile: child " + std::to_string(c) + " of node " + std::to_string(i) + " is not earlier (topological order violated)");
+      }
+    }
+  }
+}
+
+void classify(Ctx& c) {
+  const tg_tape_desc& d = c.d;
+  c.cls.assign(d.n_nodes, cConst);
+  c.gkind.assign(d.n_gathers, 0);
+  auto gather_class = [&](std::uint32_t g) -> std::uint8_t {
+    bool any_sample = false, any_uniform = false;
+    for (std::uint32_t r = 0; r < d.gathers[g].n_rows; ++r) {
+      const std::uint8_t k = c.cls[c.cand(g, r)];
+      if (k == cSample || k == cInput) any_sample = true; else any_uniform = true;
+    }
+    if (any_sample && any_uniform)
+      throw std::invalid_argument("tg_compile: gather mixes per-sample and sample-invariant nodes");
+    return any_sample ? 2 : 1;
+  };
+  for (std::uint32_t i = 0; i < d.n_nodes; ++i) {
+    if (d.op[i] == Leaf) {
+      c.cls[i] = d.leaf_class[i] == TG_LEAF_PARAM ? cParam : d.leaf_class[i] == TG_LEAF_INPUT ? cInput : cConst;
+      continue;
+    }
+    bool sample = false;
+    const std::uint32_t* k = c.kids(i);
+    for (std::uint32_t j = 0; j < c.nkids(i); ++j) {
+      if (k[j] & TG_GATHER_FLAG) {
+        const std::uint32_t g = k[j] & ~TG_GATHER_FLAG;
+        if (!c.gkind[g]) c.gkind[g] = gather_class(g);
+        sample = true;  // a token-selected value differs per sample
+      } else if (c.cls[k[j]] == cSample || c.cls[k[j]] == cInput) {
+        sample = true;
+      }
+    }
+    c.cls[i] = sample ? cSample : cUniform;
+  }
+}
+
+// Processing order of backward_with_scratch (backprop.hpp:150-183) over the
+// union of all per-sample wirings (a gather visits its candidates in row
+// order; for model tapes this coincides with every concrete sample's order).
+std::vector<std::uint32_t> processing_order(const Ctx& c) {
+  const tg_tape_desc& d = c.d;
+  std::vector<std::uint8_t> seen(d.n_nodes, 0);
+  std::vector<std::uint32_t> post;
+  auto bwd_kids = [&](std::uint32_t i, std::vector<std::uint32_t>& out) {
+    out.clear();
+    if (d.op[i] == StopGradMax || d.op[i] == Leaf) return;
+    const std::uint32_t* k = c.kids(i);
+    for (std::uint32_t j = 0; j < c.nkids(i); ++j) {
+      if (k[j] & TG_GATHER_FLAG) {
+        const std::uint32_t g = k[j] & ~TG_GATHER_FLAG;
+        for (std::uint32_t r = 0; r < d.gathers[g].n_rows; ++r) out.push_back(c.cand(g, r));
+      } else {
+        out.push_back(k[j]);
+      }
+    }
+  };
+  struct Frame { std::uint32_t node; std::uint32_t cur; std::vector<std::uint32_t> kids; };
+  std::vector<Frame> st;
+  seen[d.root] = 1;
+  Frame f0{d.root, 0, {}};
+  bwd_kids(d.root, f0.kids);
+  if (!f0.kids.empty()) st.push_back(std::move(f0));
+  while (!st.empty()) {
+    Frame& top = st.back();
+    if (top.cur < top.kids.size()) {
+      const std::uint32_t ch = top.kids[top.cur++];
+      if (!seen[ch]) {
+        seen[ch] = 1;
+        Frame f{ch, 0, {}};
+        bwd_kids(ch, f.kids);
+        if (!f.kids.empty()) st.push_back(std::move(f));
+      }
+    } else {
+      post.push_back(top.node);
+      st.pop_back();
+    }
+  }
+  std::reverse(post.begin(), post.end());
+  return post;  // processing order (children after parents)
+}
+
+}  // namespace
+
+Program compile(const tg_tape_desc& d) {
+  validate(d);
+  Program P;
+  P.dtype = d.dtype;
+  P.n_nodes = d.n_nodes;
+  P.n_params = d.n_params;
+  P.n_inputs = d.n_inputs;
+  P.n_index_inputs = d.n_index_inputs;
+  P.n_edges = d.child_offset[d.n_nodes];
+  Ctx c{d, P, {}, {}, {}, {}, {}, {}};
+  classify(c);
+
+  // ---- uniform value table: [params | uniform nodes | constants] ----------
+  c.uv.assign(d.n_nodes, kNone);
+  P.uv_uniform_base = d.n_params;
+  std::uint32_t nu = 0, nc = 0;
+  for (std::uint32_t i = 0; i < d.n_nodes; ++i) if (c.cls[i] == cUniform) ++nu; else if (c.cls[i] == cConst) ++nc;
+  P.uv_const_base = d.n_params + nu;
+  P.n_uv = d.n_params + nu + nc;
+  P.uv_init.assign(P.n_uv, 0.0);
+  {
+    std::uint32_t ku = 0, kc = 0;
+    for (std::uint32_t i = 0; i < d.n_nodes; ++i) {
+      switch (c.cls[i]) {
+        case cParam: c.uv[i] = d.leaf_index[i]; P.uv_init[c.uv[i]] = d.leaf_value ? d.leaf_value[i] : 0.0; break;
+        case cUniform: c.uv[i] = P.uv_uniform_base + ku++; break;
+        case cConst: c.uv[i] = P.uv_const_base + kc; P.uv_init[c.uv[i]] = d.leaf_value ? d.leaf_value[i] : 0.0; ++kc; break;
+        default: break;
+      }
+    }
+  }
+  P.n_uniform_nodes = nu;
+
+  // ---- per-sample rows -------------------------------------------------------
+  c.row.assign(d.n_nodes, kNone);
+  std::uint32_t nrow = 0;
+  P.input_rows.assign(d.n_inputs, kNone);
+  for (std::uint32_t i = 0; i < d.n_nodes; ++i)
+    if (c.cls[i] == cInput) {
+      const std::uint32_t col = d.leaf_index[i];
+      if (P.input_rows[col] != kNone)
+        throw std::invalid_argument("tg_compile: input column " + std::to_string(col) + " bound to two leaves");
+      c.row[i] = nrow++;
+      P.input_rows[col] = c.row[i];
+      Instr in{kInputLoad, Leaf, 0, c.row[i], 0, 0, col, i, 0.0};
+      P.fwd.push_back(in);
+    }
+  c.grow.assign(d.n_gathers, kNone);
+  c.sg_of.assign(d.n_gathers, kNone);
+  for (std::uint32_t g = 0; g < d.n_gathers; ++g) {
+    if (!c.gkind[g]) continue;
+    GatherTable T{d.gathers[g].index_col, d.gathers[g].n_rows, static_cast<std::uint32_t>(P.cand.size()), 0};
+    if (c.gkind[g] == 1) {
+      for (std::uint32_t r = 0; r < T.n_rows; ++r) P.cand.push_back(c.uv[c.cand(g, r)]);
+      c.grow[g] = nrow++;
+      const std::uint32_t id = static_cast<std::uint32_t>(P.ugather.size());
+      P.ugather.push_back(T);
+      Instr gl{kGatherLoad, Leaf, 0, c.grow[g], 0, 0, id, d.gathers[g].first_node, 0.0};
+      P.fwd.push_back(gl);
+    }
+  }
+  for (std::uint32_t i = 0; i < d.n_nodes; ++i)
+    if (c.cls[i] == cSample) { c.row[i] = nrow++; ++P.n_sample_nodes; }
+  // slot-gather candidate tables (rows are known now)
+  for (std::uint32_t g = 0; g < d.n_gathers; ++g) {
+    if (c.gkind[g] != 2) continue;
+    GatherTable T{d.gathers[g].index_col, d.gathers[g].n_rows, static_cast<std::uint32_t>(P.cand.size()), 0};
+    for (std::uint32_t r = 0; r < T.n_rows; ++r) P.cand.push_back(c.row[c.cand(g, r)]);
+    c.sg_of[g] = static_cast<std::uint32_t>(P.sgather.size());
+    P.sgather.push_back(T);
+  }
+
+  auto operand = [&](std::uint32_t ch) -> std::uint32_t {
+    if (ch & TG_GATHER_FLAG) {
+      const std::uint32_t g = ch & ~TG_GATHER_FLAG;
+      return c.gkind[g] == 1 ? enc(kSlot, c.grow[g]) : enc(kSGather, c.sg_of[g]);
+    }
+    const std::uint8_t k = c.cls[ch];
+    if (k == cSample || k == cInput) return enc(kSlot, c.row[ch]);
+    return enc(kUv, c.uv[ch]);
+  };
+
+  // ---- forward streams -------------------------------------------------------
+  std::vector<std::uint32_t> instr_of(d.n_nodes, kNone);   // per-sample node -> fwd index
+  std::vector<std::uint32_t> uinstr_of(d.n_nodes, kNone);  // uniform node -> ufwd index
+  for (std::uint32_t i = 0; i < d.n_nodes; ++i) {
+    if (c.cls[i] != cSample && c.cls[i] != cUniform) continue;
+    Instr in{};
+    in.kind = kNode;
+    in.op = d.op[i];
+    in.nops = c.nkids(i);
+    in.opnd = static_cast<std::uint32_t>(P.opnd.size());
+    in.node = i;
+    in.cst = d.constant ? d.constant[i] : 0.0;
+    for (std::uint32_t j = 0; j < in.nops; ++j) {
+      P.opnd.push_back(operand(c.kids(i)[j]));
+      P.oflag.push_back(0);
+      P.oaux.push_back(kNone);
+    }
+    if (c.cls[i] == cSample) {
+      in.out = c.row[i];
+      instr_of[i] = static_cast<std::uint32_t>(P.fwd.size());
+      P.fwd.push_back(in);
+    } else {
+      in.out = c.uv[i];
+      uinstr_of[i] = static_cast<std::uint32_t>(P.ufwd.size());
+      P.ufwd.push_back(in);
+    }
+  }
+
+  // ---- reverse sweep -----------------------------------------------------------
+  P.order = processing_order(c);
+  std::vector<std::uint8_t> written(nrow + 1, 0);
+  std::vector<std::uint8_t> needs_zero(nrow + 1, 0);
+  const std::uint8_t rc = c.cls[d.root];
+  if (rc == cSample || rc == cInput) { P.root_row = c.row[d.root]; written[P.root_row] = 1; }
+  else P.root_uv = c.uv[d.root];
+
+  struct PendingTerm { std::uint32_t dest; Term t; };
+  std::vector<PendingTerm> pend;
+  auto new_aux_row = [&]() { const std::uint32_t r = nrow++; written.push_back(0); needs_zero.push_back(0); return r; };
+
+  for (std::uint32_t node : P.order) {
+    if (c.cls[node] == cUniform) { P.ubwd.push_back(P.ufwd[uinstr_of[node]]); continue; }
+    if (c.cls[node] != cSample) continue;
+    const Instr in = P.fwd[instr_of[node]];
+    if (in.op == StopGradMax) continue;  // no gradient flows through the shift
+    P.bwd.push_back(in);
+    const std::uint32_t n = in.nops;
+    for (std::uint32_t j = 0; j < n; ++j) {
+      const std::uint32_t o = P.opnd[in.opnd + j];
+      const std::uint32_t mode = o >> kModeShift, idx = o & kIndexMask;
+      if (mode == kSlot) {
+        if (!written[idx]) { P.oflag[in.opnd + j] |= kAssign; written[idx] = 1; }
+      } else if (mode == kSGather) {
+        const GatherTable& T = P.sgather[idx];
+        for (std::uint32_t r = 0; r < T.n_rows; ++r) {
+          const std::uint32_t rr = P.cand[T.cand_off + r];
+          if (!written[rr]) { needs_zero[rr] = 1; written[rr] = 1; }
+        }
+      } else {  // sample-invariant operand: batch-reduction term
+        if (idx >= P.uv_const_base) continue;  // constants take no gradient
+        const std::uint8_t op = in.op;
+        double coef = 0.0;
+        std::uint32_t f = kNone;
+        bool direct = true;
+        auto partner_row = [&](std::uint32_t k) -> bool {
+          const std::uint32_t po = P.opnd[in.opnd + k];
+          if ((po >> kModeShift) != kSlot) return false;
+          f = po & kIndexMask;
+          return true;
+        };
+        switch (op) {
+          case Add: case AddVarying: coef = 1.0; break;
+          case Sub: case SubVarying: coef = j == 0 ? 1.0 : -1.0; break;
+          case Mean: coef = 0.5; break;
+          case NegativeMean: coef = -0.5; break;
+          case MeanVarying: coef = 1.0 / n; break;
+          case NegativeMeanVarying: coef = -1.0 / n; break;
+          case Mul: coef = 1.0; direct = partner_row(1 - j); break;
+          case IPNoBias: { const std::uint32_t m = n / 2; coef = 1.0; direct = partner_row(j < m ? j + m : j - m); break; }
+          case IPWithBias: {
+            const std::uint32_t m = (n - 1) / 2;
+            coef = 1.0;
+            if (j == n - 1) break;
+            direct = partner_row(j < m ? j + m : j - m);
+            break;
+          }
+          default: direct = false; break;
+        }
+        Term t{};
+        if (direct) {
+          t = Term{in.out, f, -1, 0, coef};
+        } else {
+          const std::uint32_t ar = new_aux_row();
+          P.oflag[in.opnd + j] |= kToAux;
+          P.oaux[in.opnd + j] = ar;
+          written[ar] = 1;
+          t = Term{ar, kNone, -1, 0, 1.0};
+        }
+        pend.push_back({idx, t});
+      }
+    }
+  }
+  // scatter terms of materialised sample-invariant gathers (embedding rows)
+  for (std::uint32_t g = 0; g < d.n_gathers; ++g) {
+    if (c.gkind[g] != 1 || !written[c.grow[g]]) continue;
+    for (std::uint32_t r = 0; r < d.gathers[g].n_rows; ++r) {
+      const std::uint32_t u = c.uv[c.cand(g, r)];
+      if (u >= P.uv_const_base) continue;
+      pend.push_back({u, Term{c.grow[g], d.gathers[g].index_col, static_cast<std::int32_t>(r), 1, 1.0}});
+    }
+  }
+  // input rows never reached still report a zero input gradient
+  for (std::uint32_t col = 0; col < d.n_inputs; ++col) {
+    const std::uint32_t r = P.input_rows[col];
+    if (r != kNone && !written[r]) { needs_zero[r] = 1; written[r] = 1; }
+  }
+  for (std::uint32_t r = 0; r < nrow; ++r) if (needs_zero[r]) P.zero_rows.push_back(r);
+  P.n_rows = nrow;
+
+  // group terms by destination (stable: keeps reverse-sweep order per dest)
+  std::stable_sort(pend.begin(), pend.end(), [](const PendingTerm& a, const PendingTerm& b) { return a.dest < b.dest; });
+  P.term_off.push_back(0);
+  for (std::size_t k = 0; k < pend.size(); ++k) {
+    if (k == 0 || pend[k].dest != pend[k - 1].dest) {
+      if (k) P.term_off.push_back(static_cast<std::uint32_t>(P.terms.size()));
+      P.dest_uv.push_back(pend[k].dest);
+    }
+    P.terms.push_back(pend[k].t);
+  }
+  if (!pend.empty()) P.term_off.push_back(static_cast<std::uint32_t>(P.terms.size()));
+  return P;
+}
+
+}  // namespace tgc

@@ -1,0 +1,184 @@
+// tg_ops.cuh — per-node forward values and reverse rules on the device.
+//
+// Forward formulas restate reference ops.hpp:38-307 (same expression shapes:
+// bias first then left-to-right products for inner products, division by the
+// arity for means); reverse rules restate detail::propagate_node
+// (ops.hpp:316-454), including the zero-safe prefix/suffix product of
+// reduceMul (ops.hpp:403-417).  The accessor `A` abstracts where operands
+// live (per-sample rows in shared memory / HBM, or the sample-invariant table).
+#pragma once
+
+#include <cstdint>
+
+#include "../host/tg_program.hpp"
+
+namespace tgk {
+
+template <class T> __device__ __forceinline__ T d_tanh(T x);
+template <> __device__ __forceinline__ double d_tanh(double x) { return tanh(x); }
+template <> __device__ __forceinline__ float d_tanh(float x) { return tanhf(x); }
+template <class T> __device__ __forceinline__ T d_exp(T x);
+template <> __device__ __forceinline__ double d_exp(double x) { return exp(x); }
+template <> __device__ __forceinline__ float d_exp(float x) { return expf(x); }
+template <class T> __device__ __forceinline__ T d_log(T x);
+template <> __device__ __forceinline__ double d_log(double x) { return log(x); }
+template <> __device__ __forceinline__ float d_log(float x) { return logf(x); }
+template <class T> __device__ __forceinline__ T d_sqrt(T x);
+template <> __device__ __forceinline__ double d_sqrt(double x) { return sqrt(x); }
+template <> __device__ __forceinline__ float d_sqrt(float x) { return sqrtf(x); }
+
+enum : std::uint8_t {
+  Leaf = 0, Relu, Tanh, Exp, NegLog, Sigmoid, Inv, Sqr, Cub, Log, Sqrt, InvSqrt,
+  Add, Sub, Mul, MulByConst, Div, Mean, AddSquares, MeanSquares, NegativeMean,
+  AddVarying, SubVarying, MulVarying, MeanVarying, SumOfSquaresVarying, MeanSquaresVarying,
+  NegativeMeanVarying, InnerProductNoBias, InnerProductWithBias,
+  StopGradMax = TG_OP_STOPGRAD_MAX,
+};
+
+// Forward value of one node.  `bad` is set (and `badv` records the offending
+// input) on a domain violation; the reference throws std::domain_error there
+// (ops.hpp:16-32), the device records the first offender per launch.
+template <class T, class A>
+__device__ __forceinline__ T eval_node(std::uint8_t op, std::uint32_t n, const std::uint32_t* o, double cst,
+                                       A& a, bool& bad, T& badv) {
+  switch (op) {
+    case Relu: { const T v = a.val(o[0]); return v > T(0) ? v : T(0); }
+    case Tanh: return d_tanh(a.val(o[0]));
+    case Exp: return d_exp(a.val(o[0]));
+    case NegLog: { const T v = a.val(o[0]); if (!(v > T(0))) { bad = true; badv = v; } return -d_log(v); }
+    case Sigmoid: return T(1) / (T(1) + d_exp(-a.val(o[0])));
+    case Inv: { const T v = a.val(o[0]); if (v == T(0)) { bad = true; badv = v; } return T(1) / v; }
+    case Sqr: { const T v = a.val(o[0]); return v * v; }
+    case Cub: { const T v = a.val(o[0]); return v * v * v; }
+    case Log: { const T v = a.val(o[0]); if (!(v > T(0))) { bad = true; badv = v; } return d_log(v); }
+    case Sqrt: { const T v = a.val(o[0]); if (!(v > T(0))) { bad = true; badv = v; } return d_sqrt(v); }
+    case InvSqrt: { const T v = a.val(o[0]); if (!(v > T(0))) { bad = true; badv = v; } return T(1) / d_sqrt(v); }
+    case MulByConst: return a.val(o[0]) * static_cast<T>(cst);
+    case Add: return a.val(o[0]) + a.val(o[1]);
+    case Sub: return a.val(o[0]) - a.val(o[1]);
+    case Mul: return a.val(o[0]) * a.val(o[1]);
+    case Div: { const T b = a.val(o[1]); if (b == T(0)) { bad = true; badv = b; } return a.val(o[0]) / b; }
+    case Mean: return (a.val(o[0]) + a.val(o[1])) / T(2);
+    case AddSquares: { const T x = a.val(o[0]), y = a.val(o[1]); return x * x + y * y; }
+    case MeanSquares: { const T x = a.val(o[0]), y = a.val(o[1]); return (x * x + y * y) / T(2); }
+    case NegativeMean: return -(a.val(o[0]) + a.val(o[1])) / T(2);
+    case AddVarying: case MeanVarying: case NegativeMeanVarying: {
+      T acc = 0;
+      for (std::uint32_t j = 0; j < n; ++j) acc += a.val(o[j]);
+      if (op == MeanVarying) acc /= static_cast<T>(n);
+      if (op == NegativeMeanVarying) acc = -acc / static_cast<T>(n);
+      return acc;
+    }
+    case SubVarying: {
+      T acc = a.val(o[0]);
+      for (std::uint32_t j = 1; j < n; ++j) acc -= a.val(o[j]);
+      return acc;
+    }
+    case MulVarying: {
+      T acc = T(1);
+      for (std::uint32_t j = 0; j < n; ++j) acc *= a.val(o[j]);
+      return acc;
+    }
+    case SumOfSquaresVarying: case MeanSquaresVarying: {
+      T acc = 0;
+      for (std::uint32_t j = 0; j < n; ++j) { const T v = a.val(o[j]); acc += v * v; }
+      if (op == MeanSquaresVarying) acc /= static_cast<T>(n);
+      return acc;
+    }
+    case InnerProductNoBias: {
+      const std::uint32_t m = n / 2;
+      T acc = 0;
+      for (std::uint32_t j = 0; j < m; ++j) acc += a.val(o[j]) * a.val(o[m + j]);
+      return acc;
+    }
+    case InnerProductWithBias: {
+      const std::uint32_t m = (n - 1) / 2;
+      T acc = a.val(o[n - 1]);
+      for (std::uint32_t j = 0; j < m; ++j) acc += a.val(o[j]) * a.val(o[m + j]);
+      return acc;
+    }
+    case StopGradMax: {
+      T m = a.val(o[0]);
+      for (std::uint32_t j = 1; j < n; ++j) { const T v = a.val(o[j]); m = v > m ? v : m; }
+      return m;
+    }
+    default: return T(0);
+  }
+}
+
+// Reverse rule of one node: pushes d(root)/d(child) contributions.
+// a.push(k, v) routes contribution v of operand k (by its mode/flags).
+template <class T, class A>
+__device__ __forceinline__ void propagate(std::uint8_t op, std::uint32_t n, const std::uint32_t* o, double cst,
+                                          T g, T y, A& a) {
+  switch (op) {
+    case Relu: a.push(0, a.val(o[0]) > T(0) ? g : T(0)); break;
+    case Tanh: a.push(0, g * (T(1) - y * y)); break;
+    case Exp: a.push(0, g * y); break;
+    case NegLog: a.push(0, -g / a.val(o[0])); break;
+    case Sigmoid: a.push(0, g * y * (T(1) - y)); break;
+    case Inv: a.push(0, -g * y * y); break;
+    case Sqr: a.push(0, g * T(2) * a.val(o[0])); break;
+    case Cub: { const T x = a.val(o[0]); a.push(0, g * T(3) * x * x); break; }
+    case Log: a.push(0, g / a.val(o[0])); break;
+    case Sqrt: a.push(0, g / (T(2) * y)); break;
+    case InvSqrt: a.push(0, -g * y / (T(2) * a.val(o[0]))); break;
+    case MulByConst: a.push(0, g * static_cast<T>(cst)); break;
+    case Add: a.push(0, g); a.push(1, g); break;
+    case Sub: a.push(0, g); a.push(1, -g); break;
+    case Mul: { const T x0 = a.val(o[0]), x1 = a.val(o[1]); a.push(0, g * x1); a.push(1, g * x0); break; }
+    case Div: {
+      const T b = a.val(o[1]), x = a.val(o[0]);
+      a.push(0, g / b);
+      a.push(1, -g * x / (b * b));
+      break;
+    }
+    case Mean: a.push(0, g / T(2)); a.push(1, g / T(2)); break;
+    case AddSquares: { const T x0 = a.val(o[0]), x1 = a.val(o[1]); a.push(0, g * T(2) * x0); a.push(1, g * T(2) * x1); break; }
+    case MeanSquares: { const T x0 = a.val(o[0]), x1 = a.val(o[1]); a.push(0, g * x0); a.push(1, g * x1); break; }
+    case NegativeMean: a.push(0, -g / T(2)); a.push(1, -g / T(2)); break;
+    case AddVarying: for (std::uint32_t j = 0; j < n; ++j) a.push(j, g); break;
+    case SubVarying: a.push(0, g); for (std::uint32_t j = 1; j < n; ++j) a.push(j, -g); break;
+    case MulVarying: {
+      // d/dx_k = prefix(k) * suffix(k+1), multiplied in the reference's order.
+      T prefix = T(1);
+      for (std::uint32_t k = 0; k < n; ++k) {
+        T suffix = T(1);
+        for (std::uint32_t j = n - 1; j > k; --j) suffix *= a.val(o[j]);
+        a.push(k, g * prefix * suffix);
+        prefix *= a.val(o[k]);
+      }
+      break;
+    }
+    case MeanVarying: { const T dd = g / static_cast<T>(n); for (std::uint32_t j = 0; j < n; ++j) a.push(j, dd); break; }
+    case SumOfSquaresVarying: for (std::uint32_t j = 0; j < n; ++j) a.push(j, g * T(2) * a.val(o[j])); break;
+    case MeanSquaresVarying: {
+      const T sc = g * T(2) / static_cast<T>(n);
+      for (std::uint32_t j = 0; j < n; ++j) a.push(j, sc * a.val(o[j]));
+      break;
+    }
+    case NegativeMeanVarying: { const T dd = -g / static_cast<T>(n); for (std::uint32_t j = 0; j < n; ++j) a.push(j, dd); break; }
+    case InnerProductNoBias: {
+      const std::uint32_t m = n / 2;
+      for (std::uint32_t k = 0; k < m; ++k) {
+        const T xk = a.val(o[k]), yk = a.val(o[m + k]);
+        a.push(k, g * yk);
+        a.push(m + k, g * xk);
+      }
+      break;
+    }
+    case InnerProductWithBias: {
+      const std::uint32_t m = (n - 1) / 2;
+      for (std::uint32_t k = 0; k < m; ++k) {
+        const T xk = a.val(o[k]), yk = a.val(o[m + k]);
+        a.push(k, g * yk);
+        a.push(m + k, g * xk);
+      }
+      a.push(n - 1, g);
+      break;
+    }
+    default: break;
+  }
+}
+
+}  // namespace tgk

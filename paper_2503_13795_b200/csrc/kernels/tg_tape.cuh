@@ -1,0 +1,79 @@
+// tg_tape.cuh — kernel argument blocks and launchers of the tape engine.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "../host/tg_program.hpp"
+
+namespace tgk {
+
+template <class T>
+struct MainArgs {
+  const tgc::Instr* fwd;
+  const tgc::Instr* bwd;
+  const std::uint32_t* opnd;
+  const std::uint8_t* oflag;
+  const std::uint32_t* oaux;
+  const std::uint32_t* zero_rows;
+  const std::uint32_t* input_rows;
+  const tgc::GatherTable* ug;
+  const tgc::GatherTable* sg;
+  const std::uint32_t* cand;
+  const std::uint32_t* term_off;
+  const tgc::Term* terms;
+  const T* UV;
+  const T* inputs;
+  const std::int32_t* idx;
+  T* loss;
+  T* igrad;
+  T* partial;
+  T* gV;
+  T* gG;
+  unsigned long long* err_key;
+  double* err_val;
+  std::uint32_t* err_op;
+  std::size_t batch;
+  std::size_t ld;          // row stride: S+pad (shared) or grid*S (HBM)
+  long long diag_sample;   // >= 0: re-run one sample to recover a domain error
+  std::uint32_t n_fwd, n_bwd, n_zero, n_inputs, n_dest;
+  std::uint32_t n_rows, S, root_row;
+};
+
+template <class T>
+struct UniformArgs {
+  const tgc::Instr* instr;
+  const std::uint32_t* opnd;
+  const T* params;
+  const T* consts;
+  T* UV;
+  T* UG;
+  T* grad_sum;
+  unsigned long long* err_key;
+  double* err_val;
+  std::uint32_t* err_op;
+  std::size_t batch;
+  std::uint32_t n_instr, n_params, n_const, const_base, n_uv, root_uv;
+};
+
+template <class T>
+struct ReduceArgs {
+  const T* partial;
+  const std::uint32_t* dest_uv;
+  T* UG;
+  std::uint32_t n_dest, n_rows;
+};
+
+template <class T> cudaError_t launch_uniform_fwd(const UniformArgs<T>& a, cudaStream_t st);
+template <class T> cudaError_t launch_uniform_bwd(const UniformArgs<T>& a, cudaStream_t st);
+template <class T>
+cudaError_t launch_tape(const MainArgs<T>& a, bool smem, unsigned grid, unsigned block, std::size_t smem_bytes,
+                        cudaStream_t st);
+template <class T> int tape_occupancy(bool smem, unsigned block, std::size_t smem_bytes);
+template <class T> cudaError_t launch_reduce(const ReduceArgs<T>& a, cudaStream_t st);
+template <class T>
+cudaError_t launch_gd(T* params, const T* g, std::uint32_t n, double gamma, double b, cudaStream_t st);
+
+}  // namespace tgk
