@@ -15,8 +15,8 @@ HDRS    := $(wildcard include/*.h $(PKG)/csrc/host/*.hpp $(PKG)/csrc/kernels/*.c
 CU_OBJ  := $(patsubst $(PKG)/csrc/kernels/%.cu,$(BUILD)/%.cu.o,$(CU_SRC))
 CXX_OBJ := $(patsubst $(PKG)/csrc/host/%.cpp,$(BUILD)/%.o,$(CXX_SRC))
 
-.PHONY: all lib oracle clean
-all: lib oracle
+.PHONY: all lib oracle clean tools
+all: lib oracle tools
 lib: $(PKG)/libtg.so
 
 $(BUILD)/%.cu.o: $(PKG)/csrc/kernels/%.cu $(HDRS)
@@ -28,7 +28,7 @@ $(BUILD)/%.o: $(PKG)/csrc/host/%.cpp $(HDRS)
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
 $(PKG)/libtg.so: $(CU_OBJ) $(CXX_OBJ)
-	$(NVCC) $(ARCH) -shared -o $@ $^ -L$(CUDA)/lib64 -lcudart -Xlinker -rpath,$(CUDA)/lib64
+	$(NVCC) $(ARCH) -shared -o $@ $^ -L$(CUDA)/lib64 -lcudart -lnvrtc -Xlinker -rpath,$(CUDA)/lib64
 
 oracle:
 	$(MAKE) -C oracle
@@ -36,3 +36,8 @@ oracle:
 clean:
 	rm -rf $(BUILD) $(PKG)/libtg.so
 	$(MAKE) -C oracle clean
+
+tools: build/fp_peak
+build/fp_peak: tools/fp_peak.cu
+	@mkdir -p $(BUILD)
+	$(NVCC) $(ARCH) -O3 $< -o $@

@@ -162,7 +162,9 @@ typedef struct tg_program_info {
   uint64_t n_edges;          /* per-sample child references              */
   uint32_t tile_samples;     /* samples per CTA tile                     */
   uint32_t smem_bytes;       /* dynamic shared memory per CTA            */
-  uint32_t storage;          /* 0 = shared-memory tile, 1 = HBM SoA      */
+  uint32_t storage;          /* 0 = shared-memory tile interpreter,
+                                1 = HBM SoA interpreter,
+                                2 = register-resident specialised kernel */
   tg_dtype dtype;
 } tg_program_info;
 
@@ -203,6 +205,18 @@ tg_status tg_train_step(tg_program_t p, const void* inputs, const int32_t* index
  * seen since the last check as TG_DOMAIN with the reference message. */
 tg_status tg_check_device_error(tg_program_t p, tg_stream_t stream, int64_t* sample_out,
                                 uint32_t* node_out);
+
+/* Kernel-level timing: when enabled, CUDA events bracket the per-sample tape
+ * kernel on the launch stream; tg_profile_read synchronises and returns the
+ * accumulated milliseconds and launch count since the last read. */
+tg_status tg_profile_enable(tg_program_t p, int on);
+tg_status tg_profile_read(tg_program_t p, double* tape_ms, uint64_t* tape_launches);
+
+/* Short tapes are specialised into a register-resident kernel (NVRTC,
+ * sm_100a) on first use.  Returns its CUDA source and compiler log;
+ * TG_UNSUPPORTED when the program runs on the interpreter kernel instead.
+ * Requires a device.  Set TG_JIT=0 to force the interpreter. */
+tg_status tg_program_jit(tg_program_t p, const char** source, const char** log, double* compile_ms);
 
 /* Number of kernel launches issued by this program since creation. */
 uint64_t tg_launch_count(tg_program_t p);

@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -14,6 +16,7 @@
 #include <vector>
 
 #include "tg_abi.h"
+#include "tg_jit.hpp"
 #include "tg_models.hpp"
 #include "tg_program.hpp"
 #include "tg_recorder.hpp"
@@ -119,7 +122,15 @@ struct tg_program {
   bool have_last = false;
   std::vector<unsigned char> last_args;
   std::size_t last_batch = 0;
+  // kernel timing (tg_profile_enable)
+  bool profiling = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  std::size_t ev_used = 0;
+  // register-resident specialisation (tg_jit.cpp)
+  tgj::JitKernel jit;
   ~tg_program() {
+    tgj::release(jit);
+    for (auto& e : ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
     for (void* p : allocs) cudaFree(p);
   }
   std::size_t tsz() const { return P.dtype == TG_F64 ? 8 : 4; }
@@ -158,6 +169,18 @@ std::size_t grid_cap(const tg_program& pr, std::size_t batch) {
   return std::max<std::size_t>(1, std::min(tiles, cap));
 }
 
+// Upper bound on CTAs of any tape kernel variant (>= 32 samples per tile,
+// <= 32 resident CTAs per SM): sizes the partial-sum rows of the workspace.
+std::size_t partial_rows(std::size_t batch) {
+  return std::max<std::size_t>(1, std::min<std::size_t>((batch + 31) / 32, std::size_t(148) * 32));
+}
+
+std::size_t jit_grid(const tg_program& pr, std::size_t batch) {
+  const std::size_t tiles = (batch + pr.jit.tile - 1) / pr.jit.tile;
+  std::size_t g = std::min<std::size_t>(tiles, std::size_t(pr.jit.occ) * pr.nsm);
+  return std::max<std::size_t>(1, std::min(g, partial_rows(batch)));
+}
+
 std::size_t grid_for(const tg_program& pr, std::size_t batch) {
   std::size_t g = grid_cap(pr, batch);
   if (pr.occ > 0) g = std::min<std::size_t>(g, std::size_t(pr.occ) * pr.nsm);
@@ -167,16 +190,17 @@ std::size_t grid_for(const tg_program& pr, std::size_t batch) {
 std::size_t align_up(std::size_t x) { return (x + 255) & ~std::size_t(255); }
 
 struct Layout {
-  std::size_t uv, ug, partial, gv, gg, total;
+  std::size_t done, uv, ug, partial, gv, gg, total;
 };
 Layout layout(const tg_program& pr, std::size_t batch) {
   const std::size_t t = pr.tsz();
   const std::size_t grid = grid_cap(pr, batch);
   Layout L{};
   std::size_t off = 0;
+  L.done = off; off = align_up(off + 16);
   L.uv = off; off = align_up(off + std::max<std::size_t>(1, pr.P.n_uv) * t);
   L.ug = off; off = align_up(off + std::max<std::size_t>(1, pr.P.n_uv) * t);
-  L.partial = off; off = align_up(off + grid * std::max<std::uint32_t>(1, pr.n_dest()) * t);
+  L.partial = off; off = align_up(off + std::max(grid, partial_rows(batch)) * std::max<std::uint32_t>(1, pr.n_dest()) * t);
   L.gv = off;
   if (!pr.smem) off = align_up(off + std::size_t(pr.P.n_rows) * grid * pr.S * t);
   L.gg = off;
@@ -248,13 +272,18 @@ tg_status upload(tg_program& pr) {
   if (P.dtype == TG_F64) pr.occ = tgk::tape_occupancy<double>(pr.smem, pr.S, pr.smem_bytes);
   else pr.occ = tgk::tape_occupancy<float>(pr.smem, pr.S, pr.smem_bytes);
   cudaGetLastError();
+  const char* env = std::getenv("TG_JIT");
+  if (!(env && env[0] == '0') && tgj::eligible(P)) pr.jit = tgj::build(P);
+  if (env && env[0] == 'v' && !pr.jit.ok) std::fprintf(stderr, "[tg] JIT not used: %s\n", pr.jit.log.c_str());
+  cudaGetLastError();
   pr.uploaded = true;
   return TG_OK;
 }
 
 template <class T>
 tg_status run_fb(tg_program& pr, const void* inputs, const std::int32_t* idx, std::size_t batch, const void* params,
-                 void* loss, void* igrad, void* grad_sum, void* ws, std::size_t ws_bytes, cudaStream_t st) {
+                 void* loss, void* igrad, void* grad_sum, void* ws, std::size_t ws_bytes, cudaStream_t st,
+                 void* gd_params = nullptr, double gamma = 0.0) {
   TG_TRY(upload(pr));
   const tgc::Program& P = pr.P;
   const Layout L = layout(pr, batch);
@@ -275,6 +304,7 @@ tg_status run_fb(tg_program& pr, const void* inputs, const std::int32_t* idx, st
   ua.params = static_cast<const T*>(params);
   ua.consts = static_cast<const T*>(pr.d_consts);
   ua.UV = UV;
+  ua.UVc = pr.jit.ok ? static_cast<T*>(pr.jit.cuv) : nullptr;
   ua.UG = UG;
   ua.grad_sum = static_cast<T*>(grad_sum);
   ua.err_key = pr.d_err_key;
@@ -287,7 +317,9 @@ tg_status run_fb(tg_program& pr, const void* inputs, const std::int32_t* idx, st
   ua.const_base = P.uv_const_base;
   ua.n_uv = P.n_uv;
   ua.root_uv = P.root_uv;
+  ua.done = reinterpret_cast<unsigned*>(w + L.done);
   TG_CUDA_TRY(tgk::launch_uniform_fwd<T>(ua, st));
+  tgk::ReduceArgs<T> ra{partial, pr.d_destuv, 0, 1};
   ++pr.launches;
 
   const std::size_t grid = grid_for(pr, batch);
@@ -327,21 +359,48 @@ tg_status run_fb(tg_program& pr, const void* inputs, const std::int32_t* idx, st
     ma.n_rows = P.n_rows;
     ma.S = pr.S;
     ma.root_row = P.root_row;
-    TG_CUDA_TRY(tgk::launch_tape<T>(ma, pr.smem, static_cast<unsigned>(grid), pr.S, pr.smem_bytes, st));
+    cudaEvent_t e1 = nullptr;
+    if (pr.profiling) {
+      if (pr.ev_used == pr.ev.size()) {
+        cudaEvent_t a, b;
+        TG_CUDA_TRY(cudaEventCreate(&a));
+        TG_CUDA_TRY(cudaEventCreate(&b));
+        pr.ev.emplace_back(a, b);
+      }
+      TG_CUDA_TRY(cudaEventRecord(pr.ev[pr.ev_used].first, st));
+      e1 = pr.ev[pr.ev_used].second;
+      ++pr.ev_used;
+    }
+    std::size_t rows = grid;
+    if (pr.jit.ok) {
+      rows = jit_grid(pr, batch);
+      unsigned grid_rows = static_cast<unsigned>(rows);
+      unsigned long long nb = batch;
+      const T* uvg = UV;
+      void* args[] = {&ma.inputs, &ma.idx, &nb, &ma.loss, &ma.igrad, &ma.partial, &grid_rows,
+                      &ma.err_key, &uvg, &ma.cand, &pr.jit.d_toff, &pr.jit.d_terms};
+      TG_CUDA_TRY(cudaLaunchKernel(reinterpret_cast<const void*>(pr.jit.fn), dim3(grid_rows), dim3(pr.jit.cfg.block),
+                                   args, pr.jit.smem_bytes, st));
+    } else {
+      TG_CUDA_TRY(tgk::launch_tape<T>(ma, pr.smem, static_cast<unsigned>(grid), pr.S, pr.smem_bytes, st));
+    }
+    if (e1) TG_CUDA_TRY(cudaEventRecord(e1, st));
     ++pr.launches;
     pr.last_args.assign(reinterpret_cast<unsigned char*>(&ma), reinterpret_cast<unsigned char*>(&ma) + sizeof(ma));
     pr.have_last = true;
     pr.last_batch = batch;
 
-    tgk::ReduceArgs<T> ra{partial, pr.d_destuv, UG, pr.n_dest(), static_cast<std::uint32_t>(grid)};
-    if (ra.n_dest) {
-      TG_CUDA_TRY(tgk::launch_reduce<T>(ra, st));
-      ++pr.launches;
-    }
+    ra = tgk::ReduceArgs<T>{partial, pr.d_destuv, pr.n_dest(), static_cast<std::uint32_t>(rows)};
   }
+  // fused: per-CTA partial reduction -> uniform reverse sweep -> grad_sum (-> GD)
   ua.instr = pr.d_ubwd;
   ua.n_instr = static_cast<std::uint32_t>(P.ubwd.size());
-  TG_CUDA_TRY(tgk::launch_uniform_bwd<T>(ua, st));
+  if (gd_params) {
+    ua.gd_params = static_cast<T*>(gd_params);
+    ua.gamma = static_cast<T>(gamma);
+    ua.gd_batch = static_cast<T>(static_cast<double>(batch));
+  }
+  TG_CUDA_TRY(tgk::launch_reduce_epilogue<T>(ra, ua, st));
   ++pr.launches;
   return TG_OK;
 }
@@ -556,7 +615,7 @@ tg_status tg_program_info_get(tg_program_t p, tg_program_info* info) {
     i.n_edges = P.n_edges;
     i.tile_samples = p->S;
     i.smem_bytes = static_cast<uint32_t>(p->smem_bytes);
-    i.storage = p->smem ? 0 : 1;
+    i.storage = p->jit.ok ? 2 : (p->smem ? 0 : 1);
     i.dtype = P.dtype;
     *info = i;
     return TG_OK;
@@ -604,9 +663,15 @@ tg_status tg_gd_update(tg_program_t p, void* params, const void* grad_sum, doubl
 
 tg_status tg_train_step(tg_program_t p, const void* inputs, const int32_t* idx, size_t batch, void* params, void* loss,
                         void* grad_sum, double gamma, void* ws, size_t ws_bytes, tg_stream_t stream) {
-  tg_status s = tg_forward_backward(p, inputs, idx, batch, params, loss, nullptr, grad_sum, ws, ws_bytes, stream);
-  if (s != TG_OK) return s;
-  return tg_gd_update(p, params, grad_sum, gamma, batch, stream);
+  // GD fused into the reduction epilogue (one launch fewer per step).
+  return guard([&] {
+    if (!p) return fail(TG_INVALID_HANDLE, "tg_train_step: NULL program");
+    if (batch == 0) return fail(TG_INVALID_ARGUMENT, "train_step: batch empty");
+    auto st = static_cast<cudaStream_t>(stream);
+    if (p->P.dtype == TG_F64)
+      return run_fb<double>(*p, inputs, idx, batch, params, loss, nullptr, grad_sum, ws, ws_bytes, st, params, gamma);
+    return run_fb<float>(*p, inputs, idx, batch, params, loss, nullptr, grad_sum, ws, ws_bytes, st, params, gamma);
+  });
 }
 
 tg_status tg_check_device_error(tg_program_t p, tg_stream_t stream, int64_t* sample_out, uint32_t* node_out) {
@@ -637,6 +702,44 @@ tg_status tg_check_device_error(tg_program_t p, tg_stream_t stream, int64_t* sam
       return fail(TG_INVALID_ARGUMENT, "gather: token index outside the table at sample " + std::to_string(sample));
     return fail(TG_DOMAIN, std::string(tg_op_name(static_cast<uint8_t>(op))) + ": input " + std::to_string(val) +
                                " is outside the operator domain");
+  });
+}
+
+tg_status tg_profile_enable(tg_program_t p, int on) {
+  p->profiling = on != 0;
+  p->ev_used = 0;
+  return TG_OK;
+}
+
+tg_status tg_profile_read(tg_program_t p, double* ms, uint64_t* n) {
+  return guard([&] {
+    double tot = 0;
+    for (std::size_t i = 0; i < p->ev_used; ++i) {
+      TG_CUDA_TRY(cudaEventSynchronize(p->ev[i].second));
+      float t = 0;
+      TG_CUDA_TRY(cudaEventElapsedTime(&t, p->ev[i].first, p->ev[i].second));
+      tot += t;
+    }
+    *ms = tot;
+    *n = p->ev_used;
+    p->ev_used = 0;
+    return TG_OK;
+  });
+}
+
+tg_status tg_program_jit(tg_program_t p, const char** source, const char** log, double* compile_ms) {
+  return guard([&] {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+      cudaGetLastError();
+      if (p->jit.source.empty()) p->jit = tgj::build(p->P);  // NVRTC compile only
+    } else {
+      TG_TRY(upload(*p));
+    }
+    *source = p->jit.source.c_str();
+    *log = p->jit.log.c_str();
+    if (compile_ms) *compile_ms = p->jit.compile_ms;
+    return p->jit.ok ? TG_OK : fail(TG_UNSUPPORTED, "JIT not used: " + p->jit.log);
   });
 }
 

@@ -395,6 +395,67 @@ Program compile(const tg_tape_desc& d) {
     P.terms.push_back(pend[k].t);
   }
   if (!pend.empty()) P.term_off.push_back(static_cast<std::uint32_t>(P.terms.size()));
+
+  // ---- dense layers: runs of inner products over the same per-sample x rows
+  // whose y operands walk a row-major parameter block (linear layers,
+  // SPEC.md:272-280).  Their weight gradients are outer-product contractions.
+  P.dest_dense.assign(P.dest_uv.size(), 0);
+  {
+    std::unordered_map<std::uint32_t, std::uint32_t> dest_of_uv;
+    for (std::uint32_t dd = 0; dd < P.dest_uv.size(); ++dd) dest_of_uv[P.dest_uv[dd]] = dd;
+    auto ip_shape = [&](std::uint32_t node, std::vector<std::uint32_t>& xs, std::uint32_t& w) -> bool {
+      if (c.cls[node] != cSample || (d.op[node] != IPNoBias && d.op[node] != IPWithBias)) return false;
+      const Instr& in = P.fwd[instr_of[node]];
+      const std::uint32_t m = d.op[node] == IPWithBias ? (in.nops - 1) / 2 : in.nops / 2;
+      xs.resize(m);
+      for (std::uint32_t k = 0; k < m; ++k) {
+        const std::uint32_t xo = P.opnd[in.opnd + k], yo = P.opnd[in.opnd + m + k];
+        if ((xo >> kModeShift) != kSlot || (yo >> kModeShift) != kUv) return false;
+        if (k == 0) w = yo & kIndexMask;
+        if ((yo & kIndexMask) != w + k || w + k >= d.n_params) return false;
+        xs[k] = xo & kIndexMask;
+      }
+      return m > 0;
+    };
+    std::vector<std::uint32_t> xs0, xs1;
+    std::uint32_t i = 0;
+    while (i < d.n_nodes) {
+      std::uint32_t w0 = 0;
+      if (!ip_shape(i, xs0, w0)) { ++i; continue; }
+      std::vector<std::uint32_t> group{i};
+      std::uint32_t nxt = i + 1, w1 = 0;
+      while (nxt < d.n_nodes && ip_shape(nxt, xs1, w1) && xs1 == xs0 &&
+             w1 == w0 + static_cast<std::uint32_t>(group.size() * xs0.size())) {
+        group.push_back(nxt++);
+      }
+      i = nxt;
+      const std::uint32_t n_out = static_cast<std::uint32_t>(group.size()), n_in = static_cast<std::uint32_t>(xs0.size());
+      if (std::uint64_t(n_out) * n_in < 8) continue;
+      auto it = dest_of_uv.find(w0);
+      if (it == dest_of_uv.end()) continue;
+      const std::uint32_t d0 = it->second;
+      bool ok = d0 + n_out * n_in <= P.dest_uv.size();
+      for (std::uint32_t j = 0; ok && j < n_out; ++j)
+        for (std::uint32_t k = 0; ok && k < n_in; ++k) {
+          const std::uint32_t dd = d0 + j * n_in + k;
+          if (P.dest_uv[dd] != w0 + j * n_in + k || P.term_off[dd + 1] - P.term_off[dd] != 1) { ok = false; break; }
+          const Term& t = P.terms[P.term_off[dd]];
+          if (t.kind != 0 || t.a != c.row[group[j]] || t.f != xs0[k] || t.coef != 1.0) ok = false;
+        }
+      if (!ok) continue;
+      DenseGrad g{n_out, n_in, static_cast<std::uint32_t>(P.dg_rows.size()), d0};
+      for (std::uint32_t j = 0; j < n_out; ++j) P.dg_rows.push_back(c.row[group[j]]);
+      for (std::uint32_t k = 0; k < n_in; ++k) P.dg_rows.push_back(xs0[k]);
+      for (std::uint32_t q = 0; q < n_out * n_in; ++q) P.dest_dense[d0 + q] = 1;
+      P.dgrad.push_back(g);
+    }
+  }
+  // uniform reverse sweep: children pairwise distinct -> pushes may run in parallel
+  for (Instr& in : P.ubwd) {
+    std::vector<std::uint32_t> ch(P.opnd.begin() + in.opnd, P.opnd.begin() + in.opnd + in.nops);
+    std::sort(ch.begin(), ch.end());
+    in.pad = std::adjacent_find(ch.begin(), ch.end()) == ch.end() ? 1 : 0;
+  }
   return P;
 }
 

@@ -1,0 +1,60 @@
+// tg_jit.hpp — register-resident specialisation of short tapes.
+//
+// The interpreter (kernels/tg_tape.cu) keeps per-sample values in shared
+// memory because an instruction stream cannot index registers.  For short
+// tapes (cfg1, cfg2, fuzz graphs) the compiler instead emits the program as
+// straight-line CUDA C++ — every node value and adjoint a register, every
+// sample-invariant operand a constant-bank operand — and compiles it with
+// NVRTC for sm_100a at tg_compile time.  Semantics are those of the
+// interpreter, instruction by instruction (same forward formulas, same
+// reverse processing order, same first-write analysis, same contraction).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "tg_program.hpp"
+
+namespace tgj {
+
+struct JitConfig {
+  unsigned block = 128;          // threads per CTA
+  unsigned spt = 1;              // samples per thread per tile
+  bool const_uv = true;          // sample-invariant table in __constant__
+  unsigned ndpt = 0;             // reduction destinations per thread (registers)
+  unsigned min_blocks = 0;       // __launch_bounds__ minBlocksPerSM (0 = unset)
+};
+
+struct JitKernel {
+  bool ok = false;
+  std::string log;               // NVRTC log / failure reason
+  std::string source;
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t fn = nullptr;
+  void* cuv = nullptr;           // __constant__ table address (const_uv)
+  std::size_t cuv_bytes = 0;
+  JitConfig cfg;
+  unsigned tile = 128;           // samples per tile = block * spt
+  std::size_t smem_bytes = 0;    // contraction rows
+  unsigned n_crow_g = 0, n_crow_v = 0;
+  int occ = 0;
+  void* d_terms = nullptr;       // remapped terms
+  void* d_toff = nullptr;
+  double compile_ms = 0;
+  std::size_t cubin_bytes = 0;
+};
+
+/// Whether the program is small enough to specialise.
+bool eligible(const tgc::Program& P);
+/// Emits the CUDA source for P (exposed for tests / inspection).
+std::string generate(const tgc::Program& P, const JitConfig& cfg, unsigned& n_crow_g, unsigned& n_crow_v,
+                     std::vector<tgc::Term>& terms_out, std::vector<std::uint32_t>& toff_out,
+                     std::size_t& smem_elems);
+/// Generates, compiles (NVRTC, sm_100a) and loads; requires a device.
+JitKernel build(const tgc::Program& P);
+void release(JitKernel& k);
+
+}  // namespace tgj

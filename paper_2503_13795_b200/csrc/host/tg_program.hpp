@@ -88,6 +88,15 @@ struct Dense {
   std::uint32_t x_is_slot_run;  // 1 if the x operands are consecutive rows
 };
 
+// Weight-gradient block of a dense layer: dest (j, k) = dest0 + j * n_in + k
+// receives sum_s G[arow[j]][s] * V[frow[k]][s] — an outer-product
+// contraction over the sample axis, evaluated register-tiled.
+struct DenseGrad {
+  std::uint32_t n_out, n_in;
+  std::uint32_t arow_off;  // offset into dg_rows: n_out adjoint rows, then n_in value rows
+  std::uint32_t dest0;
+};
+
 struct GatherTable {          // candidate list of one gather
   std::uint32_t col;          // index column
   std::uint32_t n_rows;
@@ -124,6 +133,9 @@ struct Program {
   std::vector<std::uint32_t> dest_uv;     // destination uv of each dest
   std::vector<std::uint32_t> term_off;    // CSR over terms, size n_dest+1
   std::vector<Term> terms;
+  std::vector<DenseGrad> dgrad;           // register-tiled weight-gradient blocks
+  std::vector<std::uint32_t> dg_rows;
+  std::vector<std::uint8_t> dest_dense;   // 1 if the dest is produced by a DenseGrad block
 
   // uniform (sample-invariant) program
   std::vector<Instr> ufwd;                // evaluated once per launch

@@ -181,4 +181,23 @@ __device__ __forceinline__ void propagate(std::uint8_t op, std::uint32_t n, cons
   }
 }
 
+// Accessor over the sample-invariant table (uniform forward / reverse sweeps).
+template <class T>
+struct UvAcc {
+  T* UV;
+  T* UG;
+  const std::uint32_t* o;
+  std::uint32_t const_base;
+  __device__ __forceinline__ T val(std::uint32_t op) const { return UV[op & tgc::kIndexMask]; }
+  __device__ __forceinline__ void push(std::uint32_t k, T v) {
+    const std::uint32_t i = o[k] & tgc::kIndexMask;
+    if (i < const_base) UG[i] += v;
+  }
+};
+
+// First domain violation of a launch: min over (sample << 32 | node).
+__device__ __forceinline__ void record_error(unsigned long long* key, std::size_t s, std::uint32_t node) {
+  atomicMin(key, (static_cast<unsigned long long>(s) << 32) | node);
+}
+
 }  // namespace tgk

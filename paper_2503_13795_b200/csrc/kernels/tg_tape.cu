@@ -76,50 +76,9 @@ struct RowAcc {
   }
 };
 
-template <class T>
-struct UvAcc {
-  T* UV;
-  T* UG;
-  const std::uint32_t* o;
-  std::uint32_t const_base;
-  __device__ __forceinline__ T val(std::uint32_t op) const { return UV[op & kIndexMask]; }
-  __device__ __forceinline__ void push(std::uint32_t k, T v) {
-    const std::uint32_t i = o[k] & kIndexMask;
-    if (i < const_base) UG[i] += v;
-  }
-};
-
-__device__ __forceinline__ void record_error(unsigned long long* key, std::size_t s, std::uint32_t node) {
-  atomicMin(key, (static_cast<unsigned long long>(s) << 32) | node);
-}
-
 // ---------------------------------------------------------------------------
 // kernels
 // ---------------------------------------------------------------------------
-
-// Sample-invariant prologue: UV <- [params | uniform nodes | constants],
-// UG <- 0.  Runs once per launch on one CTA.
-template <class T>
-__global__ void k_uniform_fwd(UniformArgs<T> a) {
-  for (std::uint32_t i = threadIdx.x; i < a.n_params; i += blockDim.x) a.UV[i] = a.params[i];
-  for (std::uint32_t i = threadIdx.x; i < a.n_const; i += blockDim.x) a.UV[a.const_base + i] = a.consts[i];
-  for (std::uint32_t i = threadIdx.x; i < a.n_uv; i += blockDim.x) a.UG[i] = T(0);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    UvAcc<T> acc{a.UV, a.UG, nullptr, a.const_base};
-    for (std::uint32_t k = 0; k < a.n_instr; ++k) {
-      const Instr in = a.instr[k];
-      acc.o = a.opnd + in.opnd;
-      bool bad = false;
-      T badv = 0;
-      a.UV[in.out] = eval_node<T>(in.op, in.nops, acc.o, in.cst, acc, bad, badv);
-      if (bad) {
-        record_error(a.err_key, 0, in.node);
-        if (*a.err_op == 0xffffffffu) { *a.err_op = in.op; *a.err_val = static_cast<double>(badv); }
-      }
-    }
-  }
-}
 
 template <class T, bool kSmem>
 __global__ void __launch_bounds__(256) k_tape(MainArgs<T> a) {
@@ -216,38 +175,11 @@ __global__ void __launch_bounds__(256) k_tape(MainArgs<T> a) {
         }
         tot += static_cast<T>(t.coef) * part;
       }
-      T* dst = a.partial + std::size_t(blockIdx.x) * a.n_dest + d;
+      T* dst = a.partial + std::size_t(d) * gridDim.x + blockIdx.x;   // [dest][cta]
       *dst = (tile == blockIdx.x) ? tot : *dst + tot;
     }
     __syncthreads();
   }
-}
-
-// Fixed-order reduction of the per-CTA partial rows into UG.
-template <class T>
-__global__ void k_reduce(ReduceArgs<T> a) {
-  const std::uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
-  if (d >= a.n_dest) return;
-  T tot = 0;
-  for (std::uint32_t c = 0; c < a.n_rows; ++c) tot += a.partial[std::size_t(c) * a.n_dest + d];
-  a.UG[a.dest_uv[d]] = tot;
-}
-
-// Uniform reverse sweep + copy of the parameter adjoints into grad_sum.
-template <class T>
-__global__ void k_uniform_bwd(UniformArgs<T> a) {
-  if (threadIdx.x == 0) {
-    if (a.root_uv != tgc::kNone) a.UG[a.root_uv] += static_cast<T>(a.batch);
-    UvAcc<T> acc{a.UV, a.UG, nullptr, a.const_base};
-    for (std::uint32_t k = 0; k < a.n_instr; ++k) {
-      const Instr in = a.instr[k];
-      acc.o = a.opnd + in.opnd;
-      propagate<T>(in.op, in.nops, acc.o, in.cst, a.UG[in.out], a.UV[in.out], acc);
-    }
-  }
-  __syncthreads();
-  if (a.grad_sum)
-    for (std::uint32_t i = threadIdx.x; i < a.n_params; i += blockDim.x) a.grad_sum[i] = a.UG[i];
 }
 
 // sgd_step: x -= gamma * g / b, in the tape's scalar type.
@@ -261,16 +193,6 @@ __global__ void k_gd(T* __restrict__ params, const T* __restrict__ g, std::uint3
 // host-side launchers
 // ---------------------------------------------------------------------------
 
-template <class T>
-cudaError_t launch_uniform_fwd(const UniformArgs<T>& a, cudaStream_t st) {
-  k_uniform_fwd<T><<<1, 256, 0, st>>>(a);
-  return cudaGetLastError();
-}
-template <class T>
-cudaError_t launch_uniform_bwd(const UniformArgs<T>& a, cudaStream_t st) {
-  k_uniform_bwd<T><<<1, 256, 0, st>>>(a);
-  return cudaGetLastError();
-}
 template <class T>
 cudaError_t launch_tape(const MainArgs<T>& a, bool smem, unsigned grid, unsigned block, std::size_t smem_bytes,
                         cudaStream_t st) {
@@ -296,12 +218,6 @@ int tape_occupancy(bool smem, unsigned block, std::size_t smem_bytes) {
   return occ;
 }
 template <class T>
-cudaError_t launch_reduce(const ReduceArgs<T>& a, cudaStream_t st) {
-  if (a.n_dest == 0) return cudaSuccess;
-  k_reduce<T><<<(a.n_dest + 255) / 256, 256, 0, st>>>(a);
-  return cudaGetLastError();
-}
-template <class T>
 cudaError_t launch_gd(T* params, const T* g, std::uint32_t n, double gamma, double b, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   k_gd<T><<<(n + 255) / 256, 256, 0, st>>>(params, g, n, static_cast<T>(gamma), static_cast<T>(b));
@@ -309,12 +225,9 @@ cudaError_t launch_gd(T* params, const T* g, std::uint32_t n, double gamma, doub
 }
 
 #define TG_INSTANTIATE(T)                                                                              \
-  template cudaError_t launch_uniform_fwd<T>(const UniformArgs<T>&, cudaStream_t);                     \
-  template cudaError_t launch_uniform_bwd<T>(const UniformArgs<T>&, cudaStream_t);                     \
   template cudaError_t launch_tape<T>(const MainArgs<T>&, bool, unsigned, unsigned, std::size_t,       \
                                       cudaStream_t);                                                   \
   template int tape_occupancy<T>(bool, unsigned, std::size_t);                                         \
-  template cudaError_t launch_reduce<T>(const ReduceArgs<T>&, cudaStream_t);                           \
   template cudaError_t launch_gd<T>(T*, const T*, std::uint32_t, double, double, cudaStream_t);
 TG_INSTANTIATE(double)
 TG_INSTANTIATE(float)

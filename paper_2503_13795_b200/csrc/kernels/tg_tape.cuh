@@ -7,6 +7,7 @@
 #include <cstdint>
 
 #include "../host/tg_program.hpp"
+#include "tg_epilogue.cuh"
 
 namespace tgk {
 
@@ -41,38 +42,10 @@ struct MainArgs {
   std::uint32_t n_fwd, n_bwd, n_zero, n_inputs, n_dest;
   std::uint32_t n_rows, S, root_row;
 };
-
-template <class T>
-struct UniformArgs {
-  const tgc::Instr* instr;
-  const std::uint32_t* opnd;
-  const T* params;
-  const T* consts;
-  T* UV;
-  T* UG;
-  T* grad_sum;
-  unsigned long long* err_key;
-  double* err_val;
-  std::uint32_t* err_op;
-  std::size_t batch;
-  std::uint32_t n_instr, n_params, n_const, const_base, n_uv, root_uv;
-};
-
-template <class T>
-struct ReduceArgs {
-  const T* partial;
-  const std::uint32_t* dest_uv;
-  T* UG;
-  std::uint32_t n_dest, n_rows;
-};
-
-template <class T> cudaError_t launch_uniform_fwd(const UniformArgs<T>& a, cudaStream_t st);
-template <class T> cudaError_t launch_uniform_bwd(const UniformArgs<T>& a, cudaStream_t st);
 template <class T>
 cudaError_t launch_tape(const MainArgs<T>& a, bool smem, unsigned grid, unsigned block, std::size_t smem_bytes,
                         cudaStream_t st);
 template <class T> int tape_occupancy(bool smem, unsigned block, std::size_t smem_bytes);
-template <class T> cudaError_t launch_reduce(const ReduceArgs<T>& a, cudaStream_t st);
 template <class T>
 cudaError_t launch_gd(T* params, const T* g, std::uint32_t n, double gamma, double b, cudaStream_t st);
 

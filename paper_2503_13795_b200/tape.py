@@ -386,6 +386,24 @@ class Program:
                                 self._ptr(params), self._ptr(loss), self._ptr(grad_sum), float(gamma),
                                 self._ptr(workspace), workspace.numel(), self._stream(stream)))
 
+    def jit(self):
+        """(source, log, compile_ms) of the register-resident kernel, or None."""
+        src, log, ms = C.c_char_p(), C.c_char_p(), C.c_double()
+        st = lib.tg_program_jit(self._h, C.byref(src), C.byref(log), C.byref(ms))
+        if st == 9:
+            return None
+        check(st)
+        return src.value.decode(), log.value.decode(), ms.value
+
+    def profile(self, on: bool = True):
+        check(lib.tg_profile_enable(self._h, 1 if on else 0))
+
+    def profile_read(self):
+        """(total ms, launches) of the tape kernel since the last read."""
+        ms, n = C.c_double(), C.c_uint64()
+        check(lib.tg_profile_read(self._h, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
     def check_device_error(self, stream=None):
         """Raises DomainError for the first per-sample domain violation."""
         s = C.c_int64(-1)

@@ -1,0 +1,26 @@
+"""One forward_backward + gd step of a bench config (for ncu captures)."""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import bench
+import paper_2503_13795_b200 as tg
+cfgname = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+cfg = bench.CONFIGS[cfgname]
+desc = tg.build_model(cfg["model"], cfg["dims"], cfg["dtype"], seed=0).describe()
+prog = tg.Program(desc)
+b = cfg["batch"]
+x, k = tg.synth_batch(cfg["model"], cfg["dims"], cfg["dtype"], seed=1000, batch=b, n_inputs=desc.n_inputs, n_index=desc.n_index_inputs)
+tdt = torch.float64 if cfg["dtype"] == "f64" else torch.float32
+X = torch.tensor(x, device="cuda") if x.size else None
+K = torch.tensor(k, device="cuda") if k.size else None
+P = torch.tensor(desc.param_values(), device="cuda", dtype=tdt)
+L = torch.zeros(b, device="cuda", dtype=tdt)
+G = torch.zeros(max(desc.n_params, 1), device="cuda", dtype=tdt)
+W = prog.alloc_workspace(b)
+for _ in range(n):
+    prog.forward_backward(X, K, b, P, L, None, G, W)
+    prog.gd_update(P, G, cfg["gamma"], b)
+torch.cuda.synchronize()
+prog.check_device_error()
+print("ok", cfgname, prog.info)

@@ -1,0 +1,168 @@
+"""CPU: the C-ABI boundary, the recorder's reference-compatible behaviour and
+the compiler's lowering decisions (no device needed)."""
+import ctypes
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2503_13795_b200 as tg
+from paper_2503_13795_b200 import _lib
+from paper_2503_13795_b200.tape import OpKind, model_id
+from helpers import GOLDEN
+
+
+def test_library_exports_every_header_symbol():
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    syms = _lib.header_symbols()
+    assert len(syms) >= 25
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+
+
+def test_oracle_libraries_load():
+    assert os.path.exists(oracle.ORACLE_SO)
+    oracle._lib()
+
+
+def test_status_and_op_names():
+    assert _lib.lib.tg_status_name(5).decode() == "TG_DOMAIN"
+    # op_kind.hpp:89-123 mnemonics
+    assert tg.op_name(OpKind.Cub) == "pow3"
+    assert tg.op_name(OpKind.Log) == "logarithm"
+    assert tg.op_name(OpKind.InnerProductWithBias) == "innerProductWithBias"
+    assert tg.op_name(OpKind.StopGradMax) == "stopGradMax"
+
+
+def test_recorder_eager_values_and_indices():
+    # SPEC.md leaf / raw index examples
+    t = tg.Tape(capacity=16)
+    a = t.leaf(-41.0)
+    b = t.leaf(2.0)
+    assert (a, b) == (0, 1)
+    assert t.value_of(t.add_squares(t.leaf(3.0), t.leaf(4.0))) == 25.0
+    assert t.value_of(t.mean(t.leaf(1.0), t.leaf(3.0))) == 2.0
+    x = [t.leaf(1.0), t.leaf(2.0)]
+    y = [t.leaf(3.0), t.leaf(4.0)]
+    assert t.value_of(t.inner_product_with_bias(x, y, t.leaf(5.0))) == 16.0
+    assert t.value_of(t.reduce_mul([t.leaf(2.0), t.leaf(3.0), t.leaf(0.0)])) == 0.0
+    assert t.value_of(t.tanh(t.leaf(0.0))) == 0.0
+    assert t.value_of(t.relu(t.leaf(-3.0))) == 0.0
+
+
+@pytest.mark.parametrize("op,val,msg", [
+    (OpKind.Log, -1.0, "logarithm: input -1.000000 is outside the operator domain"),
+    (OpKind.Sqrt, 0.0, "sqrt: input 0.000000 is outside the operator domain"),
+    (OpKind.NegLog, 0.0, "negativeLog: input 0.000000 is outside the operator domain"),
+    (OpKind.Inv, 0.0, "inv: input 0.000000 is outside the operator domain"),
+    (OpKind.InvSqrt, -2.0, "invSqrt: input -2.000000 is outside the operator domain"),
+])
+def test_recorder_domain_errors_match_reference(op, val, msg):
+    # ops.hpp:16-32 throw std::domain_error with this exact text
+    t = tg.Tape()
+    x = t.leaf(val)
+    with pytest.raises(tg.DomainError) as e:
+        t.op(op, [x])
+    assert str(e.value).endswith(msg)
+
+
+def test_recorder_div_by_zero_and_arity_errors():
+    t = tg.Tape()
+    one, zero = t.leaf(1.0), t.leaf(0.0)
+    with pytest.raises(tg.DomainError, match="div: input 0.000000 is outside the operator domain"):
+        t.div(one, zero)
+    with pytest.raises(tg.InvalidArgument, match="reduceSum: empty input sequence"):
+        t.reduce_sum([])
+    with pytest.raises(tg.InvalidArgument, match=r"innerProduct: sequence lengths differ \(2 vs 1\)"):
+        t.inner_product([one, one], [one])
+    with pytest.raises(tg.TgError, match="TG_INVALID_HANDLE"):
+        t.add(one, 9999)
+
+
+def test_recorder_topology_matches_reference_tape():
+    """Same composition recorded on tg::Tape and on the reference tapegrad::Tape:
+    opcodes, child lists (gathers resolved with the template sample) and
+    constants identical."""
+    for name, dims, dt, _ in [("fig1", None, "f64", 0), ("listing1", None, "f64", 0), ("moons", None, "f64", 0),
+                              ("char_mlp", None, "f32", 0), ("wide_mlp", [24, 16, 12, 10], "f32", 0),
+                              ("gpt", [11, 6, 8, 2, 2, 16], "f32", 0)]:
+        d = tg.build_model(name, dims, dt, seed=5).describe()
+        x1, k1 = tg.synth_batch(name, dims, "f64", seed=6, batch=1, n_inputs=d.n_inputs, n_index=d.n_index_inputs)
+        # resolve my tape to the reference's form: gathers -> template rows, stop-gradient max -> Leaf
+        ops = d.op.copy()
+        ops[ops == OpKind.StopGradMax] = OpKind.Leaf
+        child, off = [], [0]
+        for i in range(d.n_nodes):
+            if d.op[i] != OpKind.StopGradMax:
+                for c in d.children(i):
+                    if c & _lib.TG_GATHER_FLAG:
+                        first, stride, n_rows, col, o = (int(v) for v in d.gathers[int(c) & 0x7FFFFFFF])
+                        c = first + stride * int(k1[col, 0]) + o
+                    child.append(c)
+            off.append(len(child))
+        h = hashlib.sha256()
+        h.update(ops.tobytes())
+        h.update(np.array(off, np.uint64).tobytes())
+        h.update(np.array(child, np.uint32).tobytes())
+        h.update(np.where(d.op == OpKind.StopGradMax, 0.0, d.constant).astype(np.float64).tobytes())
+        assert h.hexdigest() == str(GOLDEN[f"w_{name}_topo_sha256"]), name
+        assert d.n_nodes == int(GOLDEN[f"w_{name}_n_nodes"])
+
+
+def test_param_counts():
+    # BASELINE.json: cfg2 d=337, cfg3 ~11.9k, cfg5 1,863,690, cfg4 ~0.21M
+    assert tg.build_model("moons").describe().n_params == 337
+    assert tg.build_model("char_mlp").describe().n_params == 11897
+    d5 = tg.build_model("wide_mlp", dims=[784, 64, 64, 10]).describe()
+    assert d5.n_params == 784 * 64 + 64 + 64 * 64 + 64 + 64 * 10 + 10
+
+
+def test_compiler_hoists_sample_invariant_nodes():
+    # the 1e-4 * sum p^2 regulariser of cfg2 depends on parameters only
+    p = tg.Program(tg.build_model("moons"))
+    i = p.info
+    assert i["n_uniform_nodes"] == 2
+    assert i["n_params"] == 337 and i["n_inputs"] == 3
+
+
+def test_compiler_rejects_malformed_tapes():
+    d = tg.build_model("fig1").describe()
+    bad = tg.TapeDesc(**{k: getattr(d, k) for k in ("op", "child_offset", "child", "constant", "leaf_class",
+                                                     "leaf_index", "leaf_value", "gathers", "root", "n_params",
+                                                     "n_inputs", "n_index_inputs", "dtype")})
+    bad.child = bad.child.copy()
+    bad.child[0] = 50  # forward reference: not a topological order
+    with pytest.raises(tg.InvalidArgument, match="topological"):
+        tg.Program(bad)
+    bad2 = tg.TapeDesc(**{**bad.__dict__, "child": d.child.copy(), "root": 999})
+    with pytest.raises(tg.InvalidArgument, match="stale root"):
+        tg.Program(bad2)
+
+
+def test_workspace_size_is_bounded_and_monotone():
+    p = tg.Program(tg.build_model("moons"))
+    a, b = p.workspace_size(1024), p.workspace_size(65536)
+    assert 0 < a <= b < 64 << 20
+
+
+def test_jit_source_compiles_with_nvrtc():
+    """The register-resident specialisation is generated and compiled (NVRTC,
+    sm_100a) without a device; only loading needs the GPU."""
+    p = tg.Program(tg.build_model("moons"))
+    src, log, ms = ctypes.c_char_p(), ctypes.c_char_p(), ctypes.c_double()
+    st = _lib.lib.tg_program_jit(p._h, ctypes.byref(src), ctypes.byref(log), ctypes.byref(ms))
+    text = src.value.decode()
+    assert "tg_jit_tape" in text and "dense weight gradient 16x16" in text
+    assert "compiled" in log.value.decode() or st == 0, log.value
+
+
+def test_synthetic_generators_are_prefix_stable():
+    x1, _ = tg.synth_batch("moons", batch=10, seed=9)
+    x2, _ = tg.synth_batch("moons", batch=100, seed=9)
+    np.testing.assert_array_equal(x1, x2[:, :10])
+    _, k = tg.synth_batch("char_mlp", batch=2000, seed=1)
+    assert k.min() >= 0 and k.max() < 27
+    counts = np.bincount(k.ravel(), minlength=27)
+    assert counts[0] > counts[5] > counts[20]   # Zipf: rank 1 most frequent

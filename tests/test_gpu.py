@@ -1,0 +1,262 @@
+"""GPU parity: the device program vs the reference (golden fixtures) and the
+oracle restatement, through the C-ABI, for both kernel tiers:
+  * "jit"    — register-resident specialised kernel (short tapes),
+  * "interp" — the instruction-stream interpreter (TG_JIT=0).
+Tolerances (north_star): rel 1e-12 fp64 / 1e-5 fp32, normwise for batch sums.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2503_13795_b200 as tg
+from helpers import GOLDEN, TOL, close_rel, recipes, rel, replay, tdtype
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+TIERS = ["jit", "interp"]
+
+
+def make_prog(desc, tier):
+    os.environ["TG_JIT"] = "1" if tier == "jit" else "0"
+    p = tg.Program(desc)
+    return p
+
+
+def run(prog, desc, x, k, params, b, want_igrad=True):
+    dt = tdtype(desc.dtype)
+    X = torch.tensor(x, device="cuda", dtype=dt) if desc.n_inputs else None
+    K = torch.tensor(k, device="cuda", dtype=torch.int32) if desc.n_index_inputs else None
+    P = torch.tensor(params, device="cuda", dtype=dt)
+    L = torch.zeros(b, device="cuda", dtype=dt)
+    IG = torch.zeros((max(desc.n_inputs, 1), b), device="cuda", dtype=dt)
+    G = torch.zeros(max(desc.n_params, 1), device="cuda", dtype=dt)
+    prog.forward_backward(X, K, b, P, L, IG if (want_igrad and desc.n_inputs) else None, G)
+    torch.cuda.synchronize()
+    prog.check_device_error()
+    return (L.cpu().double().numpy(), IG.cpu().double().numpy()[:desc.n_inputs],
+            G.cpu().double().numpy()[:desc.n_params])
+
+
+WORK = [("fig1", None, "f64", 64), ("listing1", None, "f64", 64), ("moons", None, "f64", 64),
+        ("char_mlp", None, "f32", 32), ("wide_mlp", [24, 16, 12, 10], "f32", 16), ("gpt", [11, 6, 8, 2, 2, 16], "f32", 4)]
+
+
+@pytest.mark.parametrize("tier", TIERS)
+@pytest.mark.parametrize("name,dims,dt,b", WORK)
+def test_workloads_vs_reference_golden(tier, name, dims, dt, b):
+    desc = tg.build_model(name, dims, dt, seed=5).describe()
+    x, k = tg.synth_batch(name, dims, dt, seed=77, batch=b, n_inputs=desc.n_inputs, n_index=desc.n_index_inputs)
+    prog = make_prog(desc, tier)
+    L, IG, G = run(prog, desc, x, k, desc.param_values(), b)
+    tol = TOL[dt]
+    assert close_rel(L, GOLDEN[f"w_{name}_loss"], tol), rel(L, GOLDEN[f"w_{name}_loss"])
+    if desc.n_inputs:
+        assert rel(IG, GOLDEN[f"w_{name}_input_grad"][:desc.n_inputs]) <= tol
+    if desc.n_params:
+        assert rel(G, GOLDEN[f"w_{name}_grad_sum"]) <= tol
+
+
+@pytest.mark.parametrize("tier", TIERS)
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_reference_fuzzer_graphs(tier, dt):
+    """All 30 opcodes through the reference's random_recipe graphs; leaf 0 is
+    a trainable parameter (batch-summed), the rest per-sample inputs."""
+    n = 0
+    for rec in recipes():
+        t, npar = replay(rec, dt, n_params=1)
+        desc = t.describe()
+        b = rec["batch"]
+        lv = rec["lv"]
+        x = lv[npar:]
+        params = lv[:npar, 0]
+        if npar:  # the param leaf takes sample 0's value for every sample
+            lv = lv.copy()
+            lv[:npar, :] = lv[:npar, :1]
+        if oracle.ref_available():   # the reference itself, per sample
+            root, grad, _, _, _ = oracle.ref_recipe_eval(rec, lv, dt, 1)
+            gsum, igrad = grad[:npar].sum(axis=1), grad[npar:]
+        else:
+            r = oracle.run(desc, x, np.zeros((0, b), np.int32), params)
+            root, gsum, igrad = r["loss"], r["grad_sum"], r["input_grad"]
+        prog = make_prog(desc, tier)
+        L, IG, G = run(prog, desc, x, np.zeros((0, b), np.int32), params, b)
+        tol = 1e-12 if dt == "f64" else 2e-5
+        assert close_rel(L, root, tol, 1e-10 if dt == "f64" else 1e-5), (rec["seed"], L, root)
+        assert close_rel(IG, igrad, tol * 10, 1e-9 if dt == "f64" else 1e-4), rec["seed"]
+        assert close_rel(G, gsum, tol * 10, 1e-9 if dt == "f64" else 1e-4), rec["seed"]
+        n += 1
+    assert n == len(GOLDEN["recipe_seed"])
+
+
+@pytest.mark.parametrize("tier", TIERS)
+@pytest.mark.parametrize("name,dims,dt,b", [("moons", None, "f64", 8192), ("char_mlp", None, "f32", 2048),
+                                            ("listing1", None, "f64", 5000), ("gpt", [17, 8, 16, 2, 2, 32], "f32", 24)])
+def test_larger_batches_vs_oracle(tier, name, dims, dt, b):
+    desc = tg.build_model(name, dims, dt, seed=2).describe()
+    x, k = tg.synth_batch(name, dims, dt, seed=11, batch=b, n_inputs=desc.n_inputs, n_index=desc.n_index_inputs)
+    r = oracle.run(desc, x.astype(np.float64), k, desc.param_values(), threads=8)
+    prog = make_prog(desc, tier)
+    L, IG, G = run(prog, desc, x, k, desc.param_values(), b)
+    assert close_rel(L, r["loss"], TOL[dt], 1e-10 if dt == "f64" else 1e-5)
+    if desc.n_params:
+        assert rel(G, r["grad_sum"]) <= TOL[dt]
+    if desc.n_inputs:
+        assert rel(IG, r["input_grad"]) <= TOL[dt] * 10
+
+
+def test_cfg1_full_size_closed_form():
+    """cfg1 at b = 1e6: every sample against the closed form of Fig. 1
+    (g = e^2/2, e = (a+b) - (ab+b^3); dg/da = e(1-b), dg/db = e(1-a-3b^2))."""
+    desc = tg.build_model("fig1").describe()
+    b = 1_000_000
+    x, k = tg.synth_batch("fig1", batch=b, seed=123, n_inputs=2, n_index=0)
+    prog = make_prog(desc, "jit")
+    L, IG, _ = run(prog, desc, x, k, np.zeros(0), b)
+    a, bb = x
+    e = (a + bb) - (a * bb + bb ** 3)
+    scale = np.maximum(1.0, np.abs(e) * (1 + np.abs(a) + 3 * bb ** 2))
+    assert np.max(np.abs(L - e * e / 2) / np.maximum(1.0, e * e)) < 1e-12
+    assert np.max(np.abs(IG[0] - e * (1 - bb)) / scale) < 1e-12
+    assert np.max(np.abs(IG[1] - e * (1 - a - 3 * bb ** 2)) / scale) < 1e-12
+    # and a sampled oracle check
+    sel = np.random.default_rng(0).choice(b, 4096, replace=False)
+    r = oracle.run(desc, x[:, sel], np.zeros((0, 4096), np.int32), np.zeros(0))
+    assert close_rel(L[sel], r["loss"], 1e-12)
+    assert close_rel(IG[:, sel], r["input_grad"], 1e-12, 1e-9)
+
+
+def test_cfg2_full_batch_and_gd_trajectory():
+    """cfg2: 100 GD steps (gamma 0.05) full batch, fused train_step on the GPU
+    vs the oracle's per-sample loop + sgd_step."""
+    desc = tg.build_model("moons").describe()
+    b, steps = 2048, 100
+    x, k = tg.synth_batch("moons", batch=b, seed=5)
+    p_ref = desc.param_values().copy()
+    prog = make_prog(desc, "jit")
+    X = torch.tensor(x, device="cuda")
+    P = torch.tensor(p_ref, device="cuda")
+    L = torch.zeros(b, device="cuda", dtype=torch.float64)
+    G = torch.zeros(desc.n_params, device="cuda", dtype=torch.float64)
+    W = prog.alloc_workspace(b)
+    losses_gpu, losses_ref = [], []
+    for _ in range(steps):
+        prog.train_step(X, None, b, P, L, G, 0.05, W)
+        losses_gpu.append(L.mean().item())
+        r = oracle.run(desc, x, k, p_ref, threads=8)
+        losses_ref.append(r["loss"].mean())
+        oracle.sgd("f64", p_ref, r["grad_sum"], 0.05, b)
+    torch.cuda.synchronize()
+    prog.check_device_error()
+    assert rel(P.cpu().numpy(), p_ref) <= 1e-10
+    assert max(abs(a - c) / abs(c) for a, c in zip(losses_gpu, losses_ref)) <= 1e-10
+    assert losses_ref[-1] < losses_ref[0]   # it trains
+
+
+def test_train_step_equals_forward_backward_plus_gd():
+    desc = tg.build_model("moons").describe()
+    b = 3000
+    x, _ = tg.synth_batch("moons", batch=b, seed=8)
+    prog = make_prog(desc, "jit")
+    X = torch.tensor(x, device="cuda")
+    P1 = torch.tensor(desc.param_values(), device="cuda")
+    P2 = P1.clone()
+    L = torch.zeros(b, device="cuda", dtype=torch.float64)
+    G = torch.zeros(desc.n_params, device="cuda", dtype=torch.float64)
+    W = prog.alloc_workspace(b)
+    prog.train_step(X, None, b, P1, L, G, 0.05, W)
+    prog.forward_backward(X, None, b, P2, L, None, G, W)
+    prog.gd_update(P2, G, 0.05, b)
+    torch.cuda.synchronize()
+    assert torch.equal(P1, P2)
+
+
+@pytest.mark.parametrize("tier", TIERS)
+def test_deterministic(tier):
+    desc = tg.build_model("char_mlp").describe()
+    b = 5000
+    x, k = tg.synth_batch("char_mlp", batch=b, seed=3, n_inputs=0, n_index=4)
+    prog = make_prog(desc, tier)
+    a = run(prog, desc, x, k, desc.param_values(), b)
+    c = run(prog, desc, x, k, desc.param_values(), b)
+    for u, v in zip(a, c):
+        np.testing.assert_array_equal(u, v)
+
+
+@pytest.mark.parametrize("tier", TIERS)
+def test_shard_invariance(tier):
+    """G virtual data-parallel shards reduced by addition == one full batch
+    (the multi-GPU reduction identity)."""
+    desc = tg.build_model("moons").describe()
+    b, shards = 4096, 4
+    x, k = tg.synth_batch("moons", batch=b, seed=21)
+    prog = make_prog(desc, tier)
+    full = run(prog, desc, x, k, desc.param_values(), b)[2]
+    acc = np.zeros_like(full)
+    for r in range(shards):
+        lo, hi = b * r // shards, b * (r + 1) // shards
+        acc += run(prog, desc, np.ascontiguousarray(x[:, lo:hi]), k[:, lo:hi], desc.param_values(), hi - lo)[2]
+    assert rel(acc, full) <= 1e-13
+
+
+@pytest.mark.parametrize("tier", TIERS)
+def test_domain_error_reported_like_reference(tier):
+    t = tg.Tape(dtype="f64")
+    a = t.input(0, 2.0)
+    lg = t.log(a)
+    t.set_root(t.mul(lg, lg))
+    desc = t.describe()
+    b = 300
+    x = np.full((1, b), 2.0)
+    x[0, 37] = -1.5
+    x[0, 200] = -3.0
+    prog = make_prog(desc, tier)
+    with pytest.raises(tg.DomainError) as e:
+        run(prog, desc, x, np.zeros((0, b), np.int32), np.zeros(0), b)
+    assert str(e.value).endswith("logarithm: input -1.500000 is outside the operator domain")
+    assert e.value.sample == 37
+    # cleared after reporting
+    x[0, 37] = x[0, 200] = 2.0
+    run(prog, desc, x, np.zeros((0, b), np.int32), np.zeros(0), b)
+
+
+@pytest.mark.parametrize("tier", TIERS)
+@pytest.mark.parametrize("b", [1, 2, 127, 129, 1000])
+def test_ragged_batches(tier, b):
+    desc = tg.build_model("moons").describe()
+    x, k = tg.synth_batch("moons", batch=b, seed=b)
+    r = oracle.run(desc, x, k, desc.param_values())
+    prog = make_prog(desc, tier)
+    L, IG, G = run(prog, desc, x, k, desc.param_values(), b)
+    assert close_rel(L, r["loss"], 1e-12)
+    assert rel(G, r["grad_sum"]) <= 1e-12
+
+
+def test_sample_invariant_root_and_lone_leaf():
+    # backward on a lone leaf: grad(leaf) = 1 per sample (SPEC.md backward examples)
+    t = tg.Tape(dtype="f64")
+    p = t.param(3.0)
+    t.set_root(t.sqr(p))            # root depends on the parameter only
+    desc = t.describe()
+    prog = make_prog(desc, "interp")
+    L, _, G = run(prog, desc, np.zeros((0, 5)), np.zeros((0, 5), np.int32), np.array([3.0]), 5)
+    assert G[0] == 5 * 6.0
+    t2 = tg.Tape(dtype="f64")
+    a = t2.input(0, 1.0)
+    t2.set_root(a)
+    d2 = t2.describe()
+    L, IG, _ = run(make_prog(d2, "interp"), d2, np.arange(4.0).reshape(1, 4), np.zeros((0, 4), np.int32), np.zeros(0), 4)
+    np.testing.assert_array_equal(L, [0, 1, 2, 3])
+    np.testing.assert_array_equal(IG, [[1, 1, 1, 1]])
+
+
+def test_jit_is_used_for_short_tapes():
+    for name in ("fig1", "moons"):
+        prog = make_prog(tg.build_model(name).describe(), "jit")
+        src = prog.jit()
+        assert src is not None and "tg_jit_tape" in src[0]
+        assert prog.info["storage"] == 2
