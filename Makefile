@@ -4,9 +4,10 @@ CUDA    ?= /usr/local/cuda
 NVCC    ?= $(CUDA)/bin/nvcc
 CXX     ?= g++
 PKG     := paper_2503_13795_b200
+BUILD   := build
 ARCH    := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -lineinfo -O3 -std=c++20 -Xcompiler -fPIC -Xptxas -v -Iinclude -I$(PKG)/csrc/host
-CXXFLAGS:= -std=c++20 -O2 -fPIC -Wall -Iinclude -I$(PKG)/csrc/host -I$(CUDA)/include
+CXXFLAGS:= -std=c++20 -O2 -fPIC -Wall -Iinclude -I$(PKG)/csrc/host -I$(CUDA)/include -I$(BUILD)
 BUILD   := build
 
 CU_SRC  := $(wildcard $(PKG)/csrc/kernels/*.cu)
@@ -23,7 +24,12 @@ $(BUILD)/%.cu.o: $(PKG)/csrc/kernels/%.cu $(HDRS)
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/$*.ptxas.txt || (cat $(BUILD)/$*.ptxas.txt; false)
 
-$(BUILD)/%.o: $(PKG)/csrc/host/%.cpp $(HDRS)
+# tg_math.cuh embedded verbatim into the NVRTC-specialised kernels
+$(BUILD)/tg_math.inc: $(PKG)/csrc/kernels/tg_math.cuh
+	@mkdir -p $(BUILD)
+	python3 -c "import sys; open(sys.argv[2],'w').write('R\"TGMATH(' + open(sys.argv[1]).read() + ')TGMATH\"')" $< $@
+
+$(BUILD)/%.o: $(PKG)/csrc/host/%.cpp $(HDRS) $(BUILD)/tg_math.inc
 	@mkdir -p $(BUILD)
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 

@@ -105,6 +105,7 @@ struct tg_program {
   std::uint8_t* d_oflag = nullptr;
   tgc::GatherTable *d_ug = nullptr, *d_sg = nullptr;
   tgc::Term* d_terms = nullptr;
+  tgc::Dense* d_dense = nullptr;
   void* d_consts = nullptr;
   unsigned long long* d_err_key = nullptr;
   double* d_err_val = nullptr;
@@ -248,6 +249,7 @@ tg_status upload(tg_program& pr) {
   TG_TRY(upload_vec(pr, P.term_off, &pr.d_termoff));
   TG_TRY(upload_vec(pr, P.terms, &pr.d_terms));
   TG_TRY(upload_vec(pr, P.dest_uv, &pr.d_destuv));
+  TG_TRY(upload_vec(pr, P.dense, &pr.d_dense));
   const std::uint32_t nc = P.n_uv - P.uv_const_base;
   if (P.dtype == TG_F64) {
     std::vector<double> c(P.uv_init.begin() + P.uv_const_base, P.uv_init.end());
@@ -337,6 +339,7 @@ tg_status run_fb(tg_program& pr, const void* inputs, const std::int32_t* idx, st
     ma.cand = pr.d_cand;
     ma.term_off = pr.d_termoff;
     ma.terms = pr.d_terms;
+    ma.dense = pr.d_dense;
     ma.UV = UV;
     ma.inputs = static_cast<const T*>(inputs);
     ma.idx = idx;

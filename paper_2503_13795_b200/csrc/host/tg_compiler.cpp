@@ -293,8 +293,114 @@ Program compile(const tg_tape_desc& d) {
     }
   }
 
-  // ---- reverse sweep -----------------------------------------------------------
   P.order = processing_order(c);
+
+  // ---- dense layers (kDense) -----------------------------------------------------
+  // A run of consecutive per-sample inner products over the same x rows whose
+  // y operands walk a row-major parameter block, plus (when each output's only
+  // consumer is one) the elementwise activation run that follows, becomes one
+  // macro-instruction: forward = loop over outputs, reverse = activation
+  // derivative + x-adjoint accumulation, weight gradients = outer products.
+  std::vector<std::int32_t> dense_of(d.n_nodes, -1);
+  const std::vector<Instr> nodefwd = P.fwd;
+  {
+    std::vector<std::uint32_t> uses(nrow + 1, 0);
+    std::vector<std::uint8_t> reach(d.n_nodes, 0);
+    for (std::uint32_t nd : P.order) reach[nd] = 1;
+    for (const Instr& in : nodefwd) {
+      if (in.kind != kNode) continue;
+      for (std::uint32_t j = 0; j < in.nops; ++j) {
+        const std::uint32_t o = P.opnd[in.opnd + j];
+        if ((o >> kModeShift) == kSlot) ++uses[o & kIndexMask];
+        else if ((o >> kModeShift) == kSGather) {
+          const GatherTable& T = P.sgather[o & kIndexMask];
+          for (std::uint32_t r = 0; r < T.n_rows; ++r) uses[P.cand[T.cand_off + r]] += 2;
+        }
+      }
+    }
+    if (c.cls[d.root] == cSample) uses[c.row[d.root]] += 2;
+    auto ip_shape = [&](std::uint32_t node, std::uint32_t& xo, std::uint32_t& m, std::uint32_t& w, std::uint32_t& b) -> bool {
+      if (node >= d.n_nodes || c.cls[node] != cSample || !reach[node] || (d.op[node] != IPNoBias && d.op[node] != IPWithBias))
+        return false;
+      const Instr& in = nodefwd[instr_of[node]];
+      const bool bias = d.op[node] == IPWithBias;
+      m = bias ? (in.nops - 1) / 2 : in.nops / 2;
+      xo = in.opnd;
+      for (std::uint32_t k = 0; k < m; ++k) {
+        const std::uint32_t xk = P.opnd[in.opnd + k], yk = P.opnd[in.opnd + m + k];
+        if ((xk >> kModeShift) != kSlot || (yk >> kModeShift) != kUv) return false;
+        if (k == 0) w = yk & kIndexMask;
+        if ((yk & kIndexMask) != w + k || w + k >= d.n_params) return false;
+      }
+      b = kNone;
+      if (bias) {
+        const std::uint32_t bo = P.opnd[in.opnd + in.nops - 1];
+        if ((bo >> kModeShift) != kUv || (bo & kIndexMask) >= d.n_params) return false;
+        b = bo & kIndexMask;
+      }
+      return m > 0;
+    };
+    auto same_x = [&](std::uint32_t o1, std::uint32_t o2, std::uint32_t m) {
+      for (std::uint32_t k = 0; k < m; ++k) if (P.opnd[o1 + k] != P.opnd[o2 + k]) return false;
+      return true;
+    };
+    std::uint32_t i = 0;
+    while (i < d.n_nodes) {
+      std::uint32_t xo, m, w0, b0;
+      if (!ip_shape(i, xo, m, w0, b0)) { ++i; continue; }
+      std::uint32_t n_out = 1;
+      for (;;) {
+        std::uint32_t xo1, m1, w1, b1;
+        const std::uint32_t nx = i + n_out;
+        if (!ip_shape(nx, xo1, m1, w1, b1) || m1 != m || d.op[nx] != d.op[i] || !same_x(xo, xo1, m) ||
+            w1 != w0 + n_out * m || (b0 == kNone) != (b1 == kNone) || (b0 != kNone && b1 != b0 + n_out) ||
+            c.row[nx] != c.row[i] + n_out)
+          break;
+        ++n_out;
+      }
+      const std::uint32_t first = i;
+      i += n_out;
+      if (std::uint64_t(n_out) * m < 8) continue;
+      // fused activation: the next n_out nodes apply one domain-free unary op to z_j,
+      // the only consumer of z_j
+      std::uint32_t act = 0, act_row = kNone;
+      {
+        const std::uint8_t op0 = i < d.n_nodes ? d.op[i] : 0;
+        bool ok = op0 == 1 /*Relu*/ || op0 == 2 /*Tanh*/ || op0 == 3 /*Exp*/ || op0 == 5 /*Sigmoid*/ ||
+                  op0 == 7 /*Sqr*/ || op0 == 8 /*Cub*/;
+        for (std::uint32_t j = 0; ok && j < n_out; ++j) {
+          const std::uint32_t an = i + j;
+          ok = an < d.n_nodes && c.cls[an] == cSample && reach[an] && d.op[an] == op0 &&
+               P.opnd[nodefwd[instr_of[an]].opnd] == enc(kSlot, c.row[first + j]) &&
+               uses[c.row[first + j]] == 1 && c.row[an] == c.row[i] + j;
+        }
+        if (ok) { act = op0; act_row = c.row[i]; }
+      }
+      const std::uint32_t id = static_cast<std::uint32_t>(P.dense.size());
+      P.dense.push_back(Dense{c.row[first], n_out, m, xo, w0, b0, first, act, act_row, 0});
+      for (std::uint32_t j = 0; j < n_out; ++j) dense_of[first + j] = static_cast<std::int32_t>(id);
+      if (act) {
+        for (std::uint32_t j = 0; j < n_out; ++j) dense_of[i + j] = static_cast<std::int32_t>(id);
+        i += n_out;
+      }
+      P.n_dense_nodes += n_out * (act ? 2 : 1);
+    }
+    // forward stream: the group at its first member, members / activations dropped
+    P.fwd.clear();
+    for (const Instr& in : nodefwd) {
+      if (in.kind == kNode && dense_of[in.node] >= 0) {
+        const std::uint32_t id = static_cast<std::uint32_t>(dense_of[in.node]);
+        const Dense& D = P.dense[id];
+        if (in.node == D.first_node)
+          P.fwd.push_back(Instr{kDense, static_cast<std::uint8_t>(D.act_op), 0, D.out_row, D.n_in, D.x_opnd, id, D.first_node, 0.0});
+        continue;
+      }
+      P.fwd.push_back(in);
+    }
+  }
+
+  // ---- reverse sweep -----------------------------------------------------------
+  std::vector<std::uint32_t> dense_seen(P.dense.size(), 0);
   std::vector<std::uint8_t> written(nrow + 1, 0);
   std::vector<std::uint8_t> needs_zero(nrow + 1, 0);
   const std::uint8_t rc = c.cls[d.root];
@@ -308,7 +414,27 @@ Program compile(const tg_tape_desc& d) {
   for (std::uint32_t node : P.order) {
     if (c.cls[node] == cUniform) { P.ubwd.push_back(P.ufwd[uinstr_of[node]]); continue; }
     if (c.cls[node] != cSample) continue;
-    const Instr in = P.fwd[instr_of[node]];
+    if (dense_of[node] >= 0) {
+      // the fused group runs where its last member would: every member's
+      // adjoint is final there (parents precede children in this order)
+      const std::uint32_t id = static_cast<std::uint32_t>(dense_of[node]);
+      const Dense& D = P.dense[id];
+      if (++dense_seen[id] < D.n_out * (D.act_op ? 2u : 1u)) continue;
+      P.bwd.push_back(Instr{kDense, static_cast<std::uint8_t>(D.act_op), 0, D.out_row, D.n_in, D.x_opnd, id,
+                            D.first_node, 0.0});
+      for (std::uint32_t j = 0; j < D.n_out; ++j) written[D.out_row + j] = 1;
+      for (std::uint32_t k = 0; k < D.n_in; ++k) {
+        const std::uint32_t xr = P.opnd[D.x_opnd + k] & kIndexMask;
+        if (!written[xr]) { P.oflag[D.x_opnd + k] |= kAssign; written[xr] = 1; }
+      }
+      for (std::uint32_t j = 0; j < D.n_out; ++j) {
+        for (std::uint32_t k = 0; k < D.n_in; ++k)
+          pend.push_back({D.w_uv + j * D.n_in + k, Term{D.out_row + j, P.opnd[D.x_opnd + k] & kIndexMask, -1, 0, 1.0}});
+        if (D.b_uv != kNone) pend.push_back({D.b_uv + j, Term{D.out_row + j, kNone, -1, 0, 1.0}});
+      }
+      continue;
+    }
+    const Instr in = nodefwd[instr_of[node]];
     if (in.op == StopGradMax) continue;  // no gradient flows through the shift
     P.bwd.push_back(in);
     const std::uint32_t n = in.nops;
@@ -396,57 +522,23 @@ Program compile(const tg_tape_desc& d) {
   }
   if (!pend.empty()) P.term_off.push_back(static_cast<std::uint32_t>(P.terms.size()));
 
-  // ---- dense layers: runs of inner products over the same per-sample x rows
-  // whose y operands walk a row-major parameter block (linear layers,
-  // SPEC.md:272-280).  Their weight gradients are outer-product contractions.
+  // ---- weight gradients of dense layers: outer-product contractions -----------
   P.dest_dense.assign(P.dest_uv.size(), 0);
   {
     std::unordered_map<std::uint32_t, std::uint32_t> dest_of_uv;
     for (std::uint32_t dd = 0; dd < P.dest_uv.size(); ++dd) dest_of_uv[P.dest_uv[dd]] = dd;
-    auto ip_shape = [&](std::uint32_t node, std::vector<std::uint32_t>& xs, std::uint32_t& w) -> bool {
-      if (c.cls[node] != cSample || (d.op[node] != IPNoBias && d.op[node] != IPWithBias)) return false;
-      const Instr& in = P.fwd[instr_of[node]];
-      const std::uint32_t m = d.op[node] == IPWithBias ? (in.nops - 1) / 2 : in.nops / 2;
-      xs.resize(m);
-      for (std::uint32_t k = 0; k < m; ++k) {
-        const std::uint32_t xo = P.opnd[in.opnd + k], yo = P.opnd[in.opnd + m + k];
-        if ((xo >> kModeShift) != kSlot || (yo >> kModeShift) != kUv) return false;
-        if (k == 0) w = yo & kIndexMask;
-        if ((yo & kIndexMask) != w + k || w + k >= d.n_params) return false;
-        xs[k] = xo & kIndexMask;
-      }
-      return m > 0;
-    };
-    std::vector<std::uint32_t> xs0, xs1;
-    std::uint32_t i = 0;
-    while (i < d.n_nodes) {
-      std::uint32_t w0 = 0;
-      if (!ip_shape(i, xs0, w0)) { ++i; continue; }
-      std::vector<std::uint32_t> group{i};
-      std::uint32_t nxt = i + 1, w1 = 0;
-      while (nxt < d.n_nodes && ip_shape(nxt, xs1, w1) && xs1 == xs0 &&
-             w1 == w0 + static_cast<std::uint32_t>(group.size() * xs0.size())) {
-        group.push_back(nxt++);
-      }
-      i = nxt;
-      const std::uint32_t n_out = static_cast<std::uint32_t>(group.size()), n_in = static_cast<std::uint32_t>(xs0.size());
-      if (std::uint64_t(n_out) * n_in < 8) continue;
-      auto it = dest_of_uv.find(w0);
+    for (const Dense& D : P.dense) {
+      auto it = dest_of_uv.find(D.w_uv);
       if (it == dest_of_uv.end()) continue;
       const std::uint32_t d0 = it->second;
-      bool ok = d0 + n_out * n_in <= P.dest_uv.size();
-      for (std::uint32_t j = 0; ok && j < n_out; ++j)
-        for (std::uint32_t k = 0; ok && k < n_in; ++k) {
-          const std::uint32_t dd = d0 + j * n_in + k;
-          if (P.dest_uv[dd] != w0 + j * n_in + k || P.term_off[dd + 1] - P.term_off[dd] != 1) { ok = false; break; }
-          const Term& t = P.terms[P.term_off[dd]];
-          if (t.kind != 0 || t.a != c.row[group[j]] || t.f != xs0[k] || t.coef != 1.0) ok = false;
-        }
+      bool ok = d0 + D.n_out * D.n_in <= P.dest_uv.size();
+      for (std::uint32_t q = 0; ok && q < D.n_out * D.n_in; ++q)  // each W dest fed by this layer only
+        ok = P.dest_uv[d0 + q] == D.w_uv + q && P.term_off[d0 + q + 1] - P.term_off[d0 + q] == 1;
       if (!ok) continue;
-      DenseGrad g{n_out, n_in, static_cast<std::uint32_t>(P.dg_rows.size()), d0};
-      for (std::uint32_t j = 0; j < n_out; ++j) P.dg_rows.push_back(c.row[group[j]]);
-      for (std::uint32_t k = 0; k < n_in; ++k) P.dg_rows.push_back(xs0[k]);
-      for (std::uint32_t q = 0; q < n_out * n_in; ++q) P.dest_dense[d0 + q] = 1;
+      DenseGrad g{D.n_out, D.n_in, static_cast<std::uint32_t>(P.dg_rows.size()), d0};
+      for (std::uint32_t j = 0; j < D.n_out; ++j) P.dg_rows.push_back(D.out_row + j);
+      for (std::uint32_t k = 0; k < D.n_in; ++k) P.dg_rows.push_back(P.opnd[D.x_opnd + k] & kIndexMask);
+      for (std::uint32_t q = 0; q < D.n_out * D.n_in; ++q) P.dest_dense[d0 + q] = 1;
       P.dgrad.push_back(g);
     }
   }

@@ -10,6 +10,7 @@
 
 #include <nvrtc.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdlib>
 #include <functional>
@@ -54,13 +55,19 @@ struct Gen {
   bool f64;
   std::ostringstream o;
   int tmp = 0;
-  std::vector<int> crow_g, crow_v;   // row -> contraction smem row (or -1)
+  std::vector<int> vslot, gslot;     // row -> shared-memory slot of its value / adjoint (or -1)
+  std::vector<char> vsm, gsm;        // value / adjoint lives in shared memory (written in place)
+  unsigned ld = 0;                   // shared-memory row stride (tile + 1)
 
   Gen(const tgc::Program& p, const JitConfig& c) : P(p), cfg(c), f64(p.dtype == TG_F64) {}
 
   std::string fn(const char* d, const char* f) const { return f64 ? d : f; }
   std::string v(std::uint32_t r) const { return "v" + std::to_string(r); }
   std::string g(std::uint32_t r) const { return "g" + std::to_string(r); }
+  std::string sv(std::uint32_t r) const { return "sV[" + std::to_string(std::size_t(vslot[r]) * ld) + "u + col]"; }
+  std::string sg_(std::uint32_t r) const { return "sG[" + std::to_string(std::size_t(gslot[r]) * ld) + "u + col]"; }
+  std::string V(std::uint32_t r) const { return vsm[r] ? sv(r) : v(r); }   // value of row r
+  std::string Gx(std::uint32_t r) const { return gsm[r] ? sg_(r) : g(r); } // adjoint of row r
   std::string uv(std::uint32_t i) const {
     return cfg.const_uv ? "cUV[" + std::to_string(i) + "]" : "UVg[" + std::to_string(i) + "]";
   }
@@ -71,14 +78,14 @@ struct Gen {
   // Operand value expression; slot gathers are materialised into a temp.
   std::string val(std::uint32_t op) {
     const std::uint32_t m = op >> kModeShift, i = op & kIndexMask;
-    if (m == tgc::kSlot) return v(i);
+    if (m == tgc::kSlot) return V(i);
     if (m == tgc::kUv) return uv(i);
     const tgc::GatherTable& t = P.sgather[i];
     const std::string name = "sg" + std::to_string(tmp++);
     o << "      T " << name << "; { const int ix = " << ix_expr(t) << "; switch (ix) {";
     for (std::uint32_t r = 0; r < t.n_rows; ++r)
-      o << " case " << r << ": " << name << " = " << v(P.cand[t.cand_off + r]) << "; break;";
-    o << " default: " << name << " = " << v(P.cand[t.cand_off]) << "; } }\n";
+      o << " case " << r << ": " << name << " = " << V(P.cand[t.cand_off + r]) << "; break;";
+    o << " default: " << name << " = " << V(P.cand[t.cand_off]) << "; } }\n";
     return name;
   }
 
@@ -87,14 +94,15 @@ struct Gen {
     const std::uint32_t m = op >> kModeShift, i = op & kIndexMask;
     const std::uint8_t fl = P.oflag[in.opnd + k];
     if (m == tgc::kSlot) {
-      if (fl & tgc::kAssign) o << "      T " << g(i) << " = " << expr << ";\n";
+      if (gsm[i]) o << "      " << sg_(i) << (fl & tgc::kAssign ? " = " : " += ") << expr << ";\n";
+      else if (fl & tgc::kAssign) o << "      T " << g(i) << " = " << expr << ";\n";
       else o << "      " << g(i) << " += " << expr << ";\n";
     } else if (m == tgc::kSGather) {
       const tgc::GatherTable& t = P.sgather[i];
       o << "      { const T c_ = " << expr << "; const int ix = " << ix_expr(t) << "; switch (ix) {";
       for (std::uint32_t r = 0; r < t.n_rows; ++r)
-        o << " case " << r << ": " << g(P.cand[t.cand_off + r]) << " += c_; break;";
-      o << " default: " << g(P.cand[t.cand_off]) << " += c_; } }\n";
+        o << " case " << r << ": " << Gx(P.cand[t.cand_off + r]) << " += c_; break;";
+      o << " default: " << Gx(P.cand[t.cand_off]) << " += c_; } }\n";
     } else if (fl & tgc::kToAux) {
       o << "      T " << g(P.oaux[in.opnd + k]) << " = " << expr << ";\n";
     }
@@ -109,6 +117,7 @@ struct Gen {
       o << "      const T " << v(in.out) << " = in[" << in.aux << "ull * batch + s];\n";
       return;
     }
+    if (in.kind == tgc::kDense) { dense_fwd(P.dense[in.aux]); return; }
     if (in.kind == tgc::kGatherLoad) {
       const tgc::GatherTable& t = P.ugather[in.aux];
       o << "      const T " << v(in.out) << " = UVg[cand[" << t.cand_off << "u + " << ix_expr(t) << "]];\n";
@@ -121,7 +130,7 @@ struct Gen {
     const std::string Z = "(T)0", ONE = "(T)1", TWO = "(T)2";
     switch (in.op) {
       case Relu: o << out << a[0] << " > " << Z << " ? " << a[0] << " : " << Z << ";\n"; break;
-      case Tanh: o << out << fn("tanh", "tanhf") << "(" << a[0] << ");\n"; break;
+      case Tanh: o << out << fn("tg_tanh", "tanhf") << "(" << a[0] << ");\n"; break;
       case Exp: o << out << fn("exp", "expf") << "(" << a[0] << ");\n"; break;
       case NegLog: check("!(" + a[0] + " > (T)0)", in); o << out << "-" << fn("log", "logf") << "(" << a[0] << ");\n"; break;
       case Sigmoid: o << out << ONE << " / (" << ONE << " + " << fn("exp", "expf") << "(-" << a[0] << "));\n"; break;
@@ -193,14 +202,116 @@ struct Gen {
     }
   }
 
+  std::string act_f(std::uint32_t op, const std::string& z) const {
+    switch (op) {
+      case Relu: return "(" + z + " > (T)0 ? " + z + " : (T)0)";
+      case Tanh: {
+        const char* sk = std::getenv("TG_JIT_SKIP");  // profiling-only ablation
+        if (sk && std::string(sk) == "tanh") return "(" + z + ")";
+        return fn("tg_tanh", "tanhf") + "(" + z + ")";
+      }
+      case Exp: return fn("exp", "expf") + "(" + z + ")";
+      case Sigmoid: return "((T)1 / ((T)1 + " + fn("exp", "expf") + "(-" + z + ")))";
+      case Sqr: return "(" + z + " * " + z + ")";
+      case Cub: return "(" + z + " * " + z + " * " + z + ")";
+      default: return z;
+    }
+  }
+  std::string act_b(std::uint32_t op, const std::string& g, const std::string& y, const std::string& z) const {
+    switch (op) {
+      case Relu: return "(" + z + " > (T)0 ? " + g + " : (T)0)";
+      case Tanh: return g + " * ((T)1 - " + y + " * " + y + ")";
+      case Exp: return g + " * " + y;
+      case Sigmoid: return g + " * " + y + " * ((T)1 - " + y + ")";
+      case Sqr: return g + " * (T)2 * " + z;
+      case Cub: return g + " * (T)3 * " + z + " * " + z;
+      default: return g;
+    }
+  }
+  std::string wexpr(const tgc::Dense& D, std::uint32_t k) const {
+    const std::string idx = std::to_string(D.w_uv) + "u + j * " + std::to_string(D.n_in) + "u + " + std::to_string(k) + "u";
+    return cfg.const_uv ? "cUV[" + idx + "]" : "UVg[" + idx + "]";
+  }
+  // Dense layer forward: loop over the outputs (static code O(n_in)),
+  // x operands held in registers, weights from the constant bank.
+  std::string wconst(const tgc::Dense& D, std::uint32_t j, std::uint32_t k) const {
+    return uv(D.w_uv + j * D.n_in + k);
+  }
+  void dense_fwd(const tgc::Dense& D) {
+    std::vector<std::string> x(D.n_in);
+    for (std::uint32_t k = 0; k < D.n_in; ++k) {
+      x[k] = "dx" + std::to_string(tmp++);
+      o << "      const T " << x[k] << " = " << val(P.opnd[D.x_opnd + k]) << ";\n";
+    }
+    if (!cfg.dense_loop) {  // unrolled: every output a register, weights constant-bank operands
+      for (std::uint32_t j = 0; j < D.n_out; ++j) {
+        const std::string acc = "a" + std::to_string(tmp++);
+        o << "      T " << acc << " = " << (D.b_uv != kNone ? uv(D.b_uv + j) : std::string("(T)0")) << ";";
+        for (std::uint32_t k = 0; k < D.n_in; ++k) o << " " << acc << " += " << x[k] << " * " << wconst(D, j, k) << ";";
+        o << "\n      const T " << v(D.out_row + j) << " = " << acc << ";\n";
+        if (D.act_op) o << "      const T " << v(D.act_row + j) << " = " << act_f(D.act_op, v(D.out_row + j)) << ";\n";
+      }
+      return;
+    }
+    o << "#pragma unroll " << cfg.unroll_j << "\n      for (unsigned j = 0; j < " << D.n_out << "u; ++j) {\n";
+    if (D.b_uv != kNone) o << "        T z = " << (cfg.const_uv ? "cUV[" : "UVg[") << D.b_uv << "u + j];\n";
+    else o << "        T z = (T)0;\n";
+    for (std::uint32_t k = 0; k < D.n_in; ++k) o << "        z += " << x[k] << " * " << wexpr(D, k) << ";\n";
+    if (vslot[D.out_row] >= 0) o << "        sV[(" << vslot[D.out_row] << "u + j) * " << ld << "u + col] = z;\n";
+    if (D.act_op) o << "        sV[(" << vslot[D.act_row] << "u + j) * " << ld << "u + col] = " << act_f(D.act_op, "z") << ";\n";
+    o << "      }\n";
+  }
+  // Dense layer reverse: activation derivative, adjoint of z (kept for the
+  // weight-gradient contraction), x adjoints accumulated in registers.
+  void dense_bwd(const tgc::Dense& D) {
+    std::vector<std::string> dx(D.n_in);
+    for (std::uint32_t k = 0; k < D.n_in; ++k) {
+      dx[k] = "gx" + std::to_string(tmp++);
+      o << "      T " << dx[k] << " = (T)0;\n";
+    }
+    if (!cfg.dense_loop) {
+      for (std::uint32_t j = 0; j < D.n_out; ++j) {
+        const std::uint32_t zr = D.out_row + j;
+        if (D.act_op) {
+          const std::uint32_t hr = D.act_row + j;
+          o << "      T " << g(zr) << " = " << act_b(D.act_op, Gx(hr), V(hr), V(zr)) << ";\n";
+        }
+        o << "     ";
+        for (std::uint32_t k = 0; k < D.n_in; ++k) o << " " << dx[k] << " += " << g(zr) << " * " << wconst(D, j, k) << ";";
+        o << "\n";
+      }
+      Instr pseudo{};
+      pseudo.opnd = D.x_opnd;
+      for (std::uint32_t k = 0; k < D.n_in; ++k) push(pseudo, k, dx[k]);
+      return;
+    }
+    o << "#pragma unroll " << cfg.unroll_j << "\n      for (unsigned j = 0; j < " << D.n_out << "u; ++j) {\n";
+    const std::string gz = "sG[(" + std::to_string(gslot[D.out_row]) + "u + j) * " + std::to_string(ld) + "u + col]";
+    if (D.act_op) {
+      const std::string gh = "sG[(" + std::to_string(gslot[D.act_row]) + "u + j) * " + std::to_string(ld) + "u + col]";
+      const std::string y = "sV[(" + std::to_string(vslot[D.act_row]) + "u + j) * " + std::to_string(ld) + "u + col]";
+      const std::string z = vslot[D.out_row] >= 0
+          ? "sV[(" + std::to_string(vslot[D.out_row]) + "u + j) * " + std::to_string(ld) + "u + col]" : std::string("(T)0");
+      o << "        const T gz = " << act_b(D.act_op, gh, y, z) << ";\n        " << gz << " = gz;\n";
+    } else {
+      o << "        const T gz = " << gz << ";\n";
+    }
+    for (std::uint32_t k = 0; k < D.n_in; ++k) o << "        " << dx[k] << " += gz * " << wexpr(D, k) << ";\n";
+    o << "      }\n";
+    Instr pseudo{};
+    pseudo.opnd = D.x_opnd;
+    for (std::uint32_t k = 0; k < D.n_in; ++k) push(pseudo, k, dx[k]);
+  }
+
   void reverse(const Instr& in) {
+    if (in.kind == tgc::kDense) { dense_bwd(P.dense[in.aux]); return; }
     const std::uint32_t n = in.nops;
     std::vector<std::string> a(n);
     auto A = [&](std::uint32_t j) -> const std::string& {
       if (a[j].empty()) a[j] = val(P.opnd[in.opnd + j]);
       return a[j];
     };
-    const std::string G = g(in.out), Y = v(in.out);
+    const std::string G = Gx(in.out), Y = V(in.out);
     const std::string ONE = "(T)1", TWO = "(T)2";
     switch (in.op) {
       case Relu: push(in, 0, "(" + A(0) + " > (T)0 ? " + G + " : (T)0)"); break;
@@ -260,6 +371,10 @@ struct Gen {
   }
 };
 
+const char* kMath =
+#include "tg_math.inc"
+    ;
+
 const char* kPrelude = R"(
 struct TermC { unsigned a; unsigned f; int row; unsigned kind; double coef; };
 __device__ __forceinline__ void tg_err(unsigned long long* key, unsigned long long s, unsigned node) {
@@ -282,13 +397,34 @@ std::string generate(const tgc::Program& P, const JitConfig& cfg, unsigned& n_cr
                      std::size_t& smem_elems) {
   Gen G(P, cfg);
   const bool f64 = P.dtype == TG_F64;
-  // contraction rows used by the batch-reduction terms
-  G.crow_g.assign(P.n_rows, -1);
-  G.crow_v.assign(P.n_rows, -1);
+  const unsigned tile = cfg.block * cfg.spt;
+  G.ld = tile + 1;
+  // shared-memory slots: rows produced inside dense loops live there (written
+  // in place); rows read by the batch-reduction terms get a slot too and are
+  // stored from registers at the end of the sample.
+  G.vslot.assign(P.n_rows, -1);
+  G.gslot.assign(P.n_rows, -1);
+  G.vsm.assign(P.n_rows, 0);
+  G.gsm.assign(P.n_rows, 0);
   n_crow_g = n_crow_v = 0;
+  auto vrange = [&](std::uint32_t r0, std::uint32_t n) {
+    for (std::uint32_t j = 0; j < n; ++j) { G.vslot[r0 + j] = static_cast<int>(n_crow_v++); G.vsm[r0 + j] = 1; }
+  };
+  auto grange = [&](std::uint32_t r0, std::uint32_t n) {
+    for (std::uint32_t j = 0; j < n; ++j) { G.gslot[r0 + j] = static_cast<int>(n_crow_g++); G.gsm[r0 + j] = 1; }
+  };
+  for (const auto& D : P.dense) {
+    if (!cfg.dense_loop) break;  // unrolled dense layers keep their rows in registers
+    // z values are kept only when something reads them: the activation's
+    // derivative (relu / sqr / cub) or, without a fused activation, the consumers
+    const bool need_z = !D.act_op || D.act_op == Relu || D.act_op == Sqr || D.act_op == Cub;
+    if (need_z) vrange(D.out_row, D.n_out);
+    grange(D.out_row, D.n_out);
+    if (D.act_op) { vrange(D.act_row, D.n_out); grange(D.act_row, D.n_out); }
+  }
   for (const auto& t : P.terms) {
-    if (G.crow_g[t.a] < 0) G.crow_g[t.a] = static_cast<int>(n_crow_g++);
-    if (t.kind == 0 && t.f != kNone && G.crow_v[t.f] < 0) G.crow_v[t.f] = static_cast<int>(n_crow_v++);
+    if (G.gslot[t.a] < 0) G.gslot[t.a] = static_cast<int>(n_crow_g++);
+    if (t.kind == 0 && t.f != kNone && G.vslot[t.f] < 0) G.vslot[t.f] = static_cast<int>(n_crow_v++);
   }
   // generic terms (dense-block destinations are produced by the register-tiled blocks)
   const unsigned nd = static_cast<unsigned>(P.dest_uv.size());
@@ -298,14 +434,13 @@ std::string generate(const tgc::Program& P, const JitConfig& cfg, unsigned& n_cr
     if (!P.dest_dense[d])
       for (std::uint32_t q = P.term_off[d]; q < P.term_off[d + 1]; ++q) {
         tgc::Term t = P.terms[q];
-        t.a = static_cast<std::uint32_t>(G.crow_g[t.a]);
-        if (t.kind == 0 && t.f != kNone) t.f = static_cast<std::uint32_t>(G.crow_v[t.f]);
+        t.a = static_cast<std::uint32_t>(G.gslot[t.a]);
+        if (t.kind == 0 && t.f != kNone) t.f = static_cast<std::uint32_t>(G.vslot[t.f]);
         terms_out.push_back(t);
       }
     toff_out.push_back(static_cast<std::uint32_t>(terms_out.size()));
   }
-  const unsigned tile = cfg.block * cfg.spt;
-  const unsigned ld = tile + 1;
+  const unsigned ld = G.ld;
   const unsigned ndpt = (nd + cfg.block - 1) / cfg.block;
   const bool reg_acc = ndpt <= 8;
   const bool dense = !P.dgrad.empty();
@@ -316,7 +451,9 @@ std::string generate(const tgc::Program& P, const JitConfig& cfg, unsigned& n_cr
   for (const auto& dg : P.dgrad) {
     DB b{dg.n_out, dg.n_in, (dg.n_out + 3) / 4, (dg.n_in + 3) / 4, 0, 0, dg.dest0, dg.arow_off};
     b.nb = b.bj * b.bk;
-    b.c = std::max(1u, std::min(cfg.block / b.nb, tile / 8));
+    // sample chunks per 4x4 tile: enough threads busy, scratch <= 512 partials
+    // (keeps shared memory from limiting occupancy below the register limit)
+    b.c = std::max(1u, std::min({cfg.block / b.nb, tile / 8, 512u / std::max(1u, b.nj * b.nk)}));
     if (b.nb > cfg.block) b.c = 1;
     scratch = std::max<std::size_t>(scratch, std::size_t(b.c) * b.nj * b.nk);
     dbs.push_back(b);
@@ -324,13 +461,13 @@ std::string generate(const tgc::Program& P, const JitConfig& cfg, unsigned& n_cr
   smem_elems = std::size_t(n_crow_g + n_crow_v) * ld + (dense ? nd + scratch : 0);
 
   std::ostringstream& o = G.o;
-  o << "typedef " << (f64 ? "double" : "float") << " T;\n" << kPrelude;
+  o << "typedef " << (f64 ? "double" : "float") << " T;\n" << kMath << kPrelude;
   if (cfg.const_uv) o << "__constant__ T cUV[" << std::max<std::uint32_t>(1, P.n_uv) << "];\n";
   for (std::size_t bi = 0; bi < dbs.size(); ++bi) {
     const DB& b = dbs[bi];
     o << "__constant__ unsigned cDG" << bi << "[" << b.nj + b.nk << "] = {";
-    for (unsigned j = 0; j < b.nj; ++j) o << (j ? ", " : "") << G.crow_g[P.dg_rows[b.off + j]];
-    for (unsigned k = 0; k < b.nk; ++k) o << ", " << G.crow_v[P.dg_rows[b.off + b.nj + k]];
+    for (unsigned j = 0; j < b.nj; ++j) o << (j ? ", " : "") << G.gslot[P.dg_rows[b.off + j]];
+    for (unsigned k = 0; k < b.nk; ++k) o << ", " << G.vslot[P.dg_rows[b.off + b.nj + k]];
     o << "};\n";
   }
   o << "extern \"C\" __global__ void __launch_bounds__(" << cfg.block;
@@ -358,20 +495,32 @@ std::string generate(const tgc::Program& P, const JitConfig& cfg, unsigned& n_cr
     << "    (void)col;\n"
     << "    if (s < batch) {\n";
   for (const Instr& in : P.fwd) G.forward(in);
-  o << "      if (loss) loss[s] = " << G.v(P.root_row) << ";\n";
-  for (std::uint32_t r : P.zero_rows) o << "      T " << G.g(r) << " = (T)0;\n";
-  o << "      T " << G.g(P.root_row) << " = (T)1;\n";
-  for (const Instr& in : P.bwd) G.reverse(in);
+  o << "      if (loss) loss[s] = " << G.V(P.root_row) << ";\n";
+  for (std::uint32_t r : P.zero_rows) {
+    if (G.gsm[r]) o << "      " << G.sg_(r) << " = (T)0;\n";
+    else o << "      T " << G.g(r) << " = (T)0;\n";
+  }
+  if (G.gsm[P.root_row]) o << "      " << G.sg_(P.root_row) << " = (T)1;\n";
+  else o << "      T " << G.g(P.root_row) << " = (T)1;\n";
+  // profiling-only ablations (wrong results): TG_JIT_SKIP=bwd|contract
+  const char* skip = std::getenv("TG_JIT_SKIP");
+  const bool skip_bwd = skip && std::string(skip) == "bwd", skip_con = skip && std::string(skip) == "contract";
+  if (!skip_bwd)
+    for (const Instr& in : P.bwd) G.reverse(in);
+  else
+    for (std::uint32_t r = 0; r < P.n_rows; ++r)
+      if (!G.gsm[r] && r != P.root_row && std::find(P.zero_rows.begin(), P.zero_rows.end(), r) == P.zero_rows.end())
+        o << "      T " << G.g(r) << " = " << G.V(r) << ";\n";
   for (std::uint32_t c = 0; c < P.n_inputs; ++c) {
     const std::uint32_t r = P.input_rows[c];
-    if (r != kNone) o << "      if (igrad) igrad[" << c << "ull * batch + s] = " << G.g(r) << ";\n";
+    if (r != kNone) o << "      if (igrad) igrad[" << c << "ull * batch + s] = " << G.Gx(r) << ";\n";
   }
   for (std::uint32_t r = 0; r < P.n_rows; ++r) {
-    if (G.crow_g[r] >= 0) o << "      sG[" << G.crow_g[r] << " * " << ld << " + col] = " << G.g(r) << ";\n";
-    if (G.crow_v[r] >= 0) o << "      sV[" << G.crow_v[r] << " * " << ld << " + col] = " << G.v(r) << ";\n";
+    if (G.gslot[r] >= 0 && !G.gsm[r]) o << "      " << G.sg_(r) << " = " << G.g(r) << ";\n";
+    if (G.vslot[r] >= 0 && !G.vsm[r]) o << "      " << G.sv(r) << " = " << G.v(r) << ";\n";
   }
   o << "    }\n    }\n";
-  if (nd) {
+  if (nd && !skip_con) {
     o << "    __syncthreads();\n"
       << "    const unsigned valid = (unsigned)((batch - base) < " << tile << "ull ? (batch - base) : " << tile << "ull);\n"
       << "    T totq[" << ndpt << "];\n"
@@ -470,12 +619,15 @@ JitKernel build(const tgc::Program& P) {
   JitConfig cfg;
   const std::size_t ts = P.dtype == TG_F64 ? 8 : 4;
   cfg.const_uv = std::size_t(std::max<std::uint32_t>(1, P.n_uv)) * ts <= kMaxConstBytes;
+  if (const char* e = std::getenv("TG_JIT_CONST")) cfg.const_uv = cfg.const_uv && std::atoi(e) != 0;
   cfg.block = 128;
   cfg.spt = P.dest_uv.empty() ? (P.n_rows <= 32 ? 4 : 2) : 1;
   // tuning overrides (profiling sweeps): TG_JIT_BLOCK, TG_JIT_SPT, TG_JIT_MINB
   if (const char* e = std::getenv("TG_JIT_BLOCK")) cfg.block = static_cast<unsigned>(std::atoi(e));
   if (const char* e = std::getenv("TG_JIT_SPT")) cfg.spt = static_cast<unsigned>(std::atoi(e));
   if (const char* e = std::getenv("TG_JIT_MINB")) cfg.min_blocks = static_cast<unsigned>(std::atoi(e));
+  if (const char* e = std::getenv("TG_JIT_UJ")) cfg.unroll_j = static_cast<unsigned>(std::atoi(e));
+  if (const char* e = std::getenv("TG_JIT_DLOOP")) cfg.dense_loop = std::atoi(e) != 0;
   std::vector<tgc::Term> terms;
   std::vector<std::uint32_t> toff;
   std::size_t smem_elems = 0;

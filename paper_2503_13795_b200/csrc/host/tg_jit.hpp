@@ -26,6 +26,8 @@ struct JitConfig {
   bool const_uv = true;          // sample-invariant table in __constant__
   unsigned ndpt = 0;             // reduction destinations per thread (registers)
   unsigned min_blocks = 0;       // __launch_bounds__ minBlocksPerSM (0 = unset)
+  unsigned unroll_j = 4;         // dense-layer output loop unroll (independent chains)
+  bool dense_loop = false;       // dense layers as loops (rows in smem) vs unrolled (rows in registers)
 };
 
 struct JitKernel {

@@ -76,16 +76,20 @@ struct Term {
 static_assert(sizeof(Term) == 24, "Term layout");
 
 // A run of inner-product nodes that share their x operands and read a
-// contiguous row-major weight block (a dense layer).
+// contiguous row-major weight block (a dense layer),
+// optionally followed by the elementwise activation node of each output.
+// Executed as one macro-instruction (kDense) forward and backward.
 struct Dense {
-  std::uint32_t out_row;   // first output row (rows out_row .. out_row+n_out-1)
+  std::uint32_t out_row;   // rows of z_j = <x, W[j]> (+ b_j): out_row .. out_row+n_out-1
   std::uint32_t n_out;
   std::uint32_t n_in;
-  std::uint32_t x_opnd;    // offset of the n_in shared x operands
+  std::uint32_t x_opnd;    // offset of the n_in shared x operands (kSlot)
   std::uint32_t w_uv;      // UV index of W[0][0]; W[j][k] = w_uv + j*n_in + k
-  std::uint32_t b_uv;      // UV index of b[0], or kNone
+  std::uint32_t b_uv;      // UV index of b[0] (b_j = b_uv + j), or kNone
   std::uint32_t first_node;
-  std::uint32_t x_is_slot_run;  // 1 if the x operands are consecutive rows
+  std::uint32_t act_op;    // fused activation opcode (0 = none)
+  std::uint32_t act_row;   // rows of act(z_j), or kNone
+  std::uint32_t pad;
 };
 
 // Weight-gradient block of a dense layer: dest (j, k) = dest0 + j * n_in + k

@@ -1,0 +1,46 @@
+// tg_math.cuh — branch-free fp64 transcendental used on the tape hot path.
+//
+// This file is compiled by nvcc into the interpreter kernels AND embedded
+// verbatim (Makefile -> build/tg_math.inc) into every NVRTC-specialised
+// kernel, so both tiers run the same instructions.  No preprocessor lines
+// below this comment block.
+//
+// tg_tanh(x): the libdevice tanh(double) costs ~80 SASS instructions per call
+// with sample-dependent branches (warp divergence); tanh dominates cfg2's
+// instruction count.  Here, branch-free, ~33 instructions:
+//   tanh|x| = -u / (2 + u),  u = expm1(-2|x|)   (no cancellation for small x)
+//   expm1(t) = 2^k * p(r) + (2^k - 1),  t = k ln2 + r,  |r| <= ln2/2,
+//   p(r) = r + r^2 Q(r), Q the degree-11 Taylor tail (trunc. error < 2e-17),
+//   exact for k = 0 (fma(1, p, 0) = p); quotient by a float reciprocal seed,
+//   two Newton steps and one residual correction.
+// Accuracy vs correctly rounded tanh: a few ulp (tested against numpy).
+__device__ __forceinline__ double tg_tanh(double x) {
+  const double a = fmin(fabs(x), 20.0);  // tanh(20) = 1 - 8.5e-18 rounds to 1
+  const double t = -2.0 * a;
+  const double kf = rint(t * 1.4426950408889634);
+  double r = fma(kf, -6.93147180369123816490e-01, t);
+  r = fma(kf, -1.90821492927058770002e-10, r);
+  double q = 1.0 / 6227020800.0;   // 1/13!
+  q = fma(q, r, 1.0 / 479001600.0);
+  q = fma(q, r, 1.0 / 39916800.0);
+  q = fma(q, r, 1.0 / 3628800.0);
+  q = fma(q, r, 1.0 / 362880.0);
+  q = fma(q, r, 1.0 / 40320.0);
+  q = fma(q, r, 1.0 / 5040.0);
+  q = fma(q, r, 1.0 / 720.0);
+  q = fma(q, r, 1.0 / 120.0);
+  q = fma(q, r, 1.0 / 24.0);
+  q = fma(q, r, 1.0 / 6.0);
+  q = fma(q, r, 0.5);
+  const double em = fma(r * r, q, r);
+  const double sc = __longlong_as_double(static_cast<long long>(static_cast<int>(kf) + 1023) << 52);
+  const double u = fma(sc, em, sc - 1.0);
+  const double d = 2.0 + u;
+  const double n = -u;
+  double rc = static_cast<double>(__frcp_rn(static_cast<float>(d)));
+  rc = fma(rc, fma(-d, rc, 1.0), rc);
+  rc = fma(rc, fma(-d, rc, 1.0), rc);
+  const double q0 = n * rc;
+  const double res = fma(-d, q0, n);
+  return copysign(fma(res, rc, q0), x);
+}

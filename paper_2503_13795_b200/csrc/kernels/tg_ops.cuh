@@ -11,11 +11,12 @@
 #include <cstdint>
 
 #include "../host/tg_program.hpp"
+#include "tg_math.cuh"
 
 namespace tgk {
 
 template <class T> __device__ __forceinline__ T d_tanh(T x);
-template <> __device__ __forceinline__ double d_tanh(double x) { return tanh(x); }
+template <> __device__ __forceinline__ double d_tanh(double x) { return tg_tanh(x); }
 template <> __device__ __forceinline__ float d_tanh(float x) { return tanhf(x); }
 template <class T> __device__ __forceinline__ T d_exp(T x);
 template <> __device__ __forceinline__ double d_exp(double x) { return exp(x); }
@@ -178,6 +179,33 @@ __device__ __forceinline__ void propagate(std::uint8_t op, std::uint32_t n, cons
       break;
     }
     default: break;
+  }
+}
+
+// Fused activations of kDense groups (domain-free unary ops only); same
+// formulas as eval_node / propagate above.
+template <class T>
+__device__ __forceinline__ T act_fwd(std::uint32_t op, T z) {
+  switch (op) {
+    case Relu: return z > T(0) ? z : T(0);
+    case Tanh: return d_tanh(z);
+    case Exp: return d_exp(z);
+    case Sigmoid: return T(1) / (T(1) + d_exp(-z));
+    case Sqr: return z * z;
+    case Cub: return z * z * z;
+    default: return z;
+  }
+}
+template <class T>
+__device__ __forceinline__ T act_bwd(std::uint32_t op, T g, T y, T z) {
+  switch (op) {
+    case Relu: return z > T(0) ? g : T(0);
+    case Tanh: return g * (T(1) - y * y);
+    case Exp: return g * y;
+    case Sigmoid: return g * y * (T(1) - y);
+    case Sqr: return g * T(2) * z;
+    case Cub: return g * T(3) * z * z;
+    default: return g;
   }
 }
 

@@ -124,6 +124,17 @@ __global__ void __launch_bounds__(256) k_tape(MainArgs<T> a) {
           }
         } else if (in.kind == tgc::kInputLoad) {
           v = a.inputs[std::size_t(in.aux) * a.batch + s];
+        } else if (in.kind == tgc::kDense) {  // dense layer: z_j = b_j + <x, W[j]>, h_j = act(z_j)
+          const tgc::Dense D = a.dense[in.aux];
+          const std::uint32_t* xo = a.opnd + D.x_opnd;
+          for (std::uint32_t j = 0; j < D.n_out; ++j) {
+            T z = D.b_uv != tgc::kNone ? a.UV[D.b_uv + j] : T(0);
+            const T* w = a.UV + D.w_uv + std::size_t(j) * D.n_in;
+            for (std::uint32_t q = 0; q < D.n_in; ++q) z += V[std::size_t(xo[q] & kIndexMask) * ld + col] * w[q];
+            V[std::size_t(D.out_row + j) * ld + col] = z;
+            if (D.act_op) V[std::size_t(D.act_row + j) * ld + col] = act_fwd<T>(D.act_op, z);
+          }
+          continue;
         } else {  // kGatherLoad: embedding row element selected by a token id
           const GatherTable t = a.ug[in.aux];
           std::int32_t r = a.idx[std::size_t(t.col) * a.batch + s];
@@ -139,6 +150,24 @@ __global__ void __launch_bounds__(256) k_tape(MainArgs<T> a) {
       // ---- reverse sweep (reference processing order) ----
       for (std::uint32_t k = 0; k < a.n_bwd; ++k) {
         const Instr in = a.bwd[k];
+        if (in.kind == tgc::kDense) {
+          const tgc::Dense D = a.dense[in.aux];
+          if (D.act_op)
+            for (std::uint32_t j = 0; j < D.n_out; ++j) {
+              const std::size_t hr = std::size_t(D.act_row + j) * ld + col, zr = std::size_t(D.out_row + j) * ld + col;
+              G[zr] = act_bwd<T>(D.act_op, G[hr], V[hr], V[zr]);
+            }
+          const std::uint32_t* xo = a.opnd + D.x_opnd;
+          const std::uint8_t* xf = a.oflag + D.x_opnd;
+          for (std::uint32_t q = 0; q < D.n_in; ++q) {
+            T dx = 0;
+            for (std::uint32_t j = 0; j < D.n_out; ++j)
+              dx += G[std::size_t(D.out_row + j) * ld + col] * a.UV[D.w_uv + std::size_t(j) * D.n_in + q];
+            T* p = &G[std::size_t(xo[q] & kIndexMask) * ld + col];
+            *p = (xf[q] & tgc::kAssign) ? dx : *p + dx;
+          }
+          continue;
+        }
         acc.o = a.opnd + in.opnd;
         acc.fl = a.oflag + in.opnd;
         acc.ax = a.oaux + in.opnd;

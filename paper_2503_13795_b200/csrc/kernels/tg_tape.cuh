@@ -25,6 +25,7 @@ struct MainArgs {
   const std::uint32_t* cand;
   const std::uint32_t* term_off;
   const tgc::Term* terms;
+  const tgc::Dense* dense;
   const T* UV;
   const T* inputs;
   const std::int32_t* idx;

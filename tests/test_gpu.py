@@ -254,6 +254,28 @@ def test_sample_invariant_root_and_lone_leaf():
     np.testing.assert_array_equal(IG, [[1, 1, 1, 1]])
 
 
+@pytest.mark.parametrize("tier", TIERS)
+def test_fp64_tanh_accuracy(tier):
+    """The branch-free fp64 tanh of the hot path (kernels/tg_math.cuh) vs a
+    correctly rounded reference: a few ulp over the whole range."""
+    t = tg.Tape(dtype="f64")
+    a = t.input(0, 0.5)
+    t.set_root(t.tanh(a))
+    desc = t.describe()
+    rng = np.random.default_rng(7)
+    x = np.concatenate([rng.uniform(-1, 1, 200000), rng.uniform(-25, 25, 100000), 10.0 ** rng.uniform(-300, 1, 50000),
+                        -10.0 ** rng.uniform(-300, 1, 50000), [0.0, -0.0, 0.3465, 0.3466, 0.3467, 19.99, 20.0, 700.0, -700.0]])
+    b = x.size
+    L, IG, _ = run(make_prog(desc, tier), desc, x.reshape(1, b), np.zeros((0, b), np.int32), np.zeros(0), b)
+    want = np.tanh(x)
+    ulp = np.spacing(np.abs(want))
+    err = np.abs(L - want) / np.maximum(ulp, 1e-320)
+    assert np.max(err) <= 4, (x[np.argmax(err)], np.max(err))
+    np.testing.assert_array_equal(np.signbit(L[x == 0]), np.signbit(x[x == 0]))
+    # derivative 1 - y^2 (ops.hpp:327-329)
+    assert np.max(np.abs(IG[0] - (1 - L * L))) <= 1e-15
+
+
 def test_jit_is_used_for_short_tapes():
     for name in ("fig1", "moons"):
         prog = make_prog(tg.build_model(name).describe(), "jit")
