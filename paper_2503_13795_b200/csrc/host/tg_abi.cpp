@@ -13,6 +13,7 @@
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "tg_abi.h"
@@ -20,6 +21,7 @@
 #include "tg_models.hpp"
 #include "tg_program.hpp"
 #include "tg_recorder.hpp"
+#include "../kernels/tg_staged.cuh"
 #include "../kernels/tg_tape.cuh"
 
 namespace {
@@ -129,6 +131,22 @@ struct tg_program {
   std::size_t ev_used = 0;
   // register-resident specialisation (tg_jit.cpp)
   tgj::JitKernel jit;
+  // staged execution over an HBM SoA workspace (large tapes, dense layers as GEMMs)
+  struct Stage { int dense; std::uint32_t begin, end; };     // dense >= 0: GEMM stage of that group
+  struct DensePlan {
+    bool gemm = false;
+    std::uint32_t xrow0 = 0;
+    std::uint32_t dw_dest0 = tgc::kNone, db_dest0 = tgc::kNone;
+    int beta = 0;                 // dX: 0 store, 1 accumulate
+    std::vector<std::uint32_t> zero_x;   // assign-flagged x rows zeroed first (mixed flags)
+    std::uint32_t* d_zero_x = nullptr;
+  };
+  bool staged = false;
+  std::vector<Stage> sfwd, sbwd;
+  std::vector<DensePlan> dplan;
+  std::vector<std::uint32_t> gen_dests;
+  std::uint32_t* d_gen_dests = nullptr;
+  std::size_t chunk = 0;          // samples per chunk (0 = by batch)
   ~tg_program() {
     tgj::release(jit);
     for (auto& e : ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
@@ -142,6 +160,96 @@ namespace {
 
 constexpr std::size_t kSmemBudget = 200 * 1024;
 constexpr unsigned kMaxOcc = 32;
+
+// Dense layers with consecutive x rows run as GEMMs over the chunk; the rest of
+// the instruction stream runs on the interpreter in ranges between them.
+void build_staged_plan(tg_program& pr) {
+  const tgc::Program& P = pr.P;
+  const char* env = std::getenv("TG_STAGED");
+  bool big = false;
+  pr.dplan.assign(P.dense.size(), {});
+  for (std::size_t i = 0; i < P.dense.size(); ++i) {
+    const tgc::Dense& D = P.dense[i];
+    tg_program::DensePlan& dp = pr.dplan[i];
+    dp.xrow0 = P.opnd[D.x_opnd] & tgc::kIndexMask;
+    bool consec = true;
+    for (std::uint32_t k = 0; k < D.n_in; ++k)
+      consec = consec && (P.opnd[D.x_opnd + k] >> tgc::kModeShift) == tgc::kSlot &&
+               (P.opnd[D.x_opnd + k] & tgc::kIndexMask) == dp.xrow0 + k;
+    dp.gemm = consec && std::uint64_t(D.n_out) * D.n_in >= 256;
+    if (std::uint64_t(D.n_out) * D.n_in >= 2048) big = true;
+  }
+  pr.staged = env ? env[0] == '1' : (big && !tgj::eligible(P));
+  if (!pr.staged || P.root_row == tgc::kNone) { pr.staged = false; return; }
+  // weight / bias gradient destinations handled by the GEMM path
+  std::vector<std::uint8_t> covered(P.dest_uv.size(), 0);
+  std::unordered_map<std::uint32_t, std::uint32_t> dest_of_uv;
+  for (std::uint32_t d = 0; d < P.dest_uv.size(); ++d) dest_of_uv[P.dest_uv[d]] = d;
+  for (std::size_t i = 0; i < P.dense.size(); ++i) {
+    const tgc::Dense& D = P.dense[i];
+    tg_program::DensePlan& dp = pr.dplan[i];
+    if (!dp.gemm) continue;
+    for (const tgc::DenseGrad& g : P.dgrad)
+      if (P.dest_uv[g.dest0] == D.w_uv && g.n_out == D.n_out && g.n_in == D.n_in) dp.dw_dest0 = g.dest0;
+    if (dp.dw_dest0 != tgc::kNone)
+      for (std::uint32_t q = 0; q < D.n_out * D.n_in; ++q) covered[dp.dw_dest0 + q] = 1;
+    if (D.b_uv != tgc::kNone) {
+      auto it = dest_of_uv.find(D.b_uv);
+      bool ok = it != dest_of_uv.end();
+      for (std::uint32_t j = 0; ok && j < D.n_out; ++j) {
+        const std::uint32_t d = it->second + j;
+        ok = d < P.dest_uv.size() && P.dest_uv[d] == D.b_uv + j && P.term_off[d + 1] - P.term_off[d] == 1 &&
+             P.terms[P.term_off[d]].kind == 0 && P.terms[P.term_off[d]].f == tgc::kNone &&
+             P.terms[P.term_off[d]].a == D.out_row + j;
+      }
+      if (ok) {
+        dp.db_dest0 = it->second;
+        for (std::uint32_t j = 0; j < D.n_out; ++j) covered[dp.db_dest0 + j] = 1;
+      }
+    }
+    std::uint32_t n_assign = 0;
+    for (std::uint32_t k = 0; k < D.n_in; ++k) n_assign += (P.oflag[D.x_opnd + k] & tgc::kAssign) ? 1 : 0;
+    dp.beta = n_assign == D.n_in ? 0 : 1;
+    if (n_assign && n_assign != D.n_in)
+      for (std::uint32_t k = 0; k < D.n_in; ++k)
+        if (P.oflag[D.x_opnd + k] & tgc::kAssign) dp.zero_x.push_back(dp.xrow0 + k);
+  }
+  pr.gen_dests.clear();
+  for (std::uint32_t d = 0; d < P.dest_uv.size(); ++d) if (!covered[d]) pr.gen_dests.push_back(d);
+  auto split = [&](const std::vector<tgc::Instr>& list, std::vector<tg_program::Stage>& out) {
+    out.clear();
+    std::uint32_t b = 0;
+    for (std::uint32_t k = 0; k < list.size(); ++k) {
+      if (list[k].kind == tgc::kDense && pr.dplan[list[k].aux].gemm) {
+        if (k > b) out.push_back({-1, b, k});
+        out.push_back({static_cast<int>(list[k].aux), k, k + 1});
+        b = k + 1;
+      }
+    }
+    if (b < list.size()) out.push_back({-1, b, static_cast<std::uint32_t>(list.size())});
+  };
+  split(P.fwd, pr.sfwd);
+  split(P.bwd, pr.sbwd);
+}
+
+// Samples per chunk of the staged path: rows of V and G for the chunk within
+// ~4 GB (TG_STAGED_MB overrides), a multiple of 128.
+std::size_t staged_chunk(const tg_program& pr, std::size_t batch) {
+  std::size_t budget = std::size_t(4096) << 20;
+  if (const char* e = std::getenv("TG_STAGED_MB")) budget = std::size_t(std::atoll(e)) << 20;
+  const std::size_t per = 2 * std::max<std::size_t>(1, pr.P.n_rows) * pr.tsz();
+  std::size_t cb = std::max<std::size_t>(128, (budget / per) / 128 * 128);
+  const std::size_t need = (std::max<std::size_t>(batch, 1) + 127) / 128 * 128;
+  return std::min(cb, need);
+}
+
+std::uint32_t splitk_splits(const tgc::Dense& D, std::size_t n, std::size_t tsz) {
+  const std::uint32_t bm = tsz == 8 ? 64 : 128;
+  const std::uint32_t tiles = ((D.n_out + bm - 1) / bm) * ((D.n_in + bm - 1) / bm);
+  std::uint32_t s = std::max<std::uint32_t>(1, 296 / std::max(1u, tiles));
+  s = std::min<std::uint32_t>(s, static_cast<std::uint32_t>(std::max<std::size_t>(1, n / 256)));
+  return std::max(1u, s);
+}
 
 void choose_config(tg_program& pr) {
   const std::size_t row_bytes = 2 * pr.tsz();
@@ -161,6 +269,7 @@ void choose_config(tg_program& pr) {
   unsigned bound = std::min(kMaxOcc, 2048u / pr.S);
   if (pr.smem) bound = std::min<unsigned>(bound, static_cast<unsigned>((228 * 1024) / (pr.smem_bytes + 1024)));
   pr.occ_bound = std::max(1u, bound);
+  build_staged_plan(pr);
 }
 
 std::size_t grid_cap(const tg_program& pr, std::size_t batch) {
@@ -191,10 +300,28 @@ std::size_t grid_for(const tg_program& pr, std::size_t batch) {
 std::size_t align_up(std::size_t x) { return (x + 255) & ~std::size_t(255); }
 
 struct Layout {
-  std::size_t done, uv, ug, partial, gv, gg, total;
+  std::size_t done, uv, ug, partial, gv, gg, sk, total;
 };
 Layout layout(const tg_program& pr, std::size_t batch) {
   const std::size_t t = pr.tsz();
+  if (pr.staged) {  // [done | UV | UG | acc[n_dest] | V | G | split-K partials]
+    Layout L{};
+    std::size_t off = 0;
+    const std::size_t cb = staged_chunk(pr, batch);
+    L.done = off; off = align_up(off + 16);
+    L.uv = off; off = align_up(off + std::max<std::size_t>(1, pr.P.n_uv) * t);
+    L.ug = off; off = align_up(off + std::max<std::size_t>(1, pr.P.n_uv) * t);
+    L.partial = off; off = align_up(off + std::max<std::uint32_t>(1, pr.n_dest()) * t);
+    L.gv = off; off = align_up(off + std::size_t(pr.P.n_rows) * cb * t);
+    L.gg = off; off = align_up(off + std::size_t(pr.P.n_rows) * cb * t);
+    std::size_t sk = 0;
+    for (std::size_t i = 0; i < pr.P.dense.size(); ++i)
+      if (pr.dplan[i].gemm && pr.dplan[i].dw_dest0 != tgc::kNone)
+        sk = std::max<std::size_t>(sk, std::size_t(splitk_splits(pr.P.dense[i], cb, t)) * pr.P.dense[i].n_out * pr.P.dense[i].n_in);
+    L.sk = off; off = align_up(off + std::max<std::size_t>(1, sk) * t);
+    L.total = off;
+    return L;
+  }
   const std::size_t grid = grid_cap(pr, batch);
   Layout L{};
   std::size_t off = 0;
@@ -275,10 +402,263 @@ tg_status upload(tg_program& pr) {
   else pr.occ = tgk::tape_occupancy<float>(pr.smem, pr.S, pr.smem_bytes);
   cudaGetLastError();
   const char* env = std::getenv("TG_JIT");
-  if (!(env && env[0] == '0') && tgj::eligible(P)) pr.jit = tgj::build(P);
+  if (!pr.staged && !(env && env[0] == '0') && tgj::eligible(P)) pr.jit = tgj::build(P);
+  if (pr.staged) {
+    TG_TRY(upload_vec(pr, pr.gen_dests, &pr.d_gen_dests));
+    for (auto& dp : pr.dplan) TG_TRY(upload_vec(pr, dp.zero_x, &dp.d_zero_x));
+  }
   if (env && env[0] == 'v' && !pr.jit.ok) std::fprintf(stderr, "[tg] JIT not used: %s\n", pr.jit.log.c_str());
   cudaGetLastError();
   pr.uploaded = true;
+  return TG_OK;
+}
+
+bool P_inputs_missing(const tg_program& pr, const void* inputs, const std::int32_t* idx) {
+  return (pr.P.n_inputs && !inputs) || (pr.P.n_index_inputs && !idx);
+}
+
+// Staged execution: chunks of the batch through HBM-resident rows; dense
+// layers as GEMMs, everything else on the interpreter in ranges.
+template <class T>
+tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx, std::size_t batch, const void* params,
+                     void* loss, void* igrad, void* grad_sum, void* ws, std::size_t ws_bytes, cudaStream_t st,
+                     void* gd_params, double gamma) {
+  const tgc::Program& P = pr.P;
+  const Layout L = layout(pr, batch);
+  if (ws_bytes < L.total)
+    return fail(TG_INVALID_ARGUMENT, "tg_forward_backward: workspace of " + std::to_string(ws_bytes) +
+                                         " bytes, need " + std::to_string(L.total));
+  char* w = static_cast<char*>(ws);
+  T* UV = reinterpret_cast<T*>(w + L.uv);
+  T* UG = reinterpret_cast<T*>(w + L.ug);
+  T* acc = reinterpret_cast<T*>(w + L.partial);
+  T* V = reinterpret_cast<T*>(w + L.gv);
+  T* G = reinterpret_cast<T*>(w + L.gg);
+  T* sk = reinterpret_cast<T*>(w + L.sk);
+  const std::size_t cb = staged_chunk(pr, batch);
+
+  tgk::UniformArgs<T> ua{};
+  ua.instr = pr.d_ufwd;
+  ua.opnd = pr.d_opnd;
+  ua.params = static_cast<const T*>(params);
+  ua.consts = static_cast<const T*>(pr.d_consts);
+  ua.UV = UV;
+  ua.UG = UG;
+  ua.grad_sum = static_cast<T*>(grad_sum);
+  ua.err_key = pr.d_err_key;
+  ua.err_val = pr.d_err_val;
+  ua.err_op = pr.d_err_op;
+  ua.batch = batch;
+  ua.n_instr = static_cast<std::uint32_t>(P.ufwd.size());
+  ua.n_params = P.n_params;
+  ua.n_const = P.n_uv - P.uv_const_base;
+  ua.const_base = P.uv_const_base;
+  ua.n_uv = P.n_uv;
+  ua.root_uv = P.root_uv;
+  ua.done = reinterpret_cast<unsigned*>(w + L.done);
+  TG_CUDA_TRY(tgk::launch_uniform_fwd<T>(ua, st));
+  ++pr.launches;
+  TG_CUDA_TRY(cudaMemsetAsync(acc, 0, std::max<std::uint32_t>(1, pr.n_dest()) * sizeof(T), st));
+
+  tgk::RangeArgs<T> ra{};
+  ra.fwd = pr.d_fwd;
+  ra.bwd = pr.d_bwd;
+  ra.opnd = pr.d_opnd;
+  ra.oflag = pr.d_oflag;
+  ra.oaux = pr.d_oaux;
+  ra.zero_rows = pr.d_zero;
+  ra.input_rows = pr.d_inrows;
+  ra.ug = pr.d_ug;
+  ra.sg = pr.d_sg;
+  ra.cand = pr.d_cand;
+  ra.dense = pr.d_dense;
+  ra.UV = UV;
+  ra.inputs = static_cast<const T*>(inputs);
+  ra.idx = idx;
+  ra.loss = static_cast<T*>(loss);
+  ra.igrad = static_cast<T*>(igrad);
+  ra.V = V;
+  ra.G = G;
+  ra.err_key = pr.d_err_key;
+  ra.batch = batch;
+  ra.ld = cb;
+  ra.n_zero = static_cast<std::uint32_t>(P.zero_rows.size());
+  ra.n_inputs = P.n_inputs;
+  ra.root_row = P.root_row;
+
+  // Interpreter arguments for domain-error diagnosis (k_tape re-runs the one
+  // offending sample; the staged V / G buffers serve as its row storage).
+  {
+    tgk::MainArgs<T> ma{};
+    ma.fwd = pr.d_fwd;
+    ma.bwd = pr.d_bwd;
+    ma.opnd = pr.d_opnd;
+    ma.oflag = pr.d_oflag;
+    ma.oaux = pr.d_oaux;
+    ma.zero_rows = pr.d_zero;
+    ma.input_rows = pr.d_inrows;
+    ma.ug = pr.d_ug;
+    ma.sg = pr.d_sg;
+    ma.cand = pr.d_cand;
+    ma.term_off = pr.d_termoff;
+    ma.terms = pr.d_terms;
+    ma.dense = pr.d_dense;
+    ma.UV = UV;
+    ma.inputs = static_cast<const T*>(inputs);
+    ma.idx = idx;
+    ma.partial = acc;
+    ma.gV = V;
+    ma.gG = G;
+    ma.err_key = pr.d_err_key;
+    ma.err_val = pr.d_err_val;
+    ma.err_op = pr.d_err_op;
+    ma.batch = batch;
+    ma.ld = pr.smem ? pr.ld_smem : cb;
+    ma.diag_sample = -1;
+    ma.n_fwd = static_cast<std::uint32_t>(P.fwd.size());
+    ma.n_bwd = static_cast<std::uint32_t>(P.bwd.size());
+    ma.n_zero = static_cast<std::uint32_t>(P.zero_rows.size());
+    ma.n_inputs = P.n_inputs;
+    ma.n_dest = 0;
+    ma.n_rows = P.n_rows;
+    ma.S = pr.S;
+    ma.root_row = P.root_row;
+    pr.last_args.assign(reinterpret_cast<unsigned char*>(&ma), reinterpret_cast<unsigned char*>(&ma) + sizeof(ma));
+    pr.have_last = true;
+  }
+  cudaEvent_t e1 = nullptr;   // tg_profile_enable: time the staged chain
+  if (pr.profiling) {
+    if (pr.ev_used == pr.ev.size()) {
+      cudaEvent_t a0, b0;
+      TG_CUDA_TRY(cudaEventCreate(&a0));
+      TG_CUDA_TRY(cudaEventCreate(&b0));
+      pr.ev.emplace_back(a0, b0);
+    }
+    TG_CUDA_TRY(cudaEventRecord(pr.ev[pr.ev_used].first, st));
+    e1 = pr.ev[pr.ev_used].second;
+    ++pr.ev_used;
+  }
+
+  for (std::size_t s0 = 0; s0 < batch; s0 += cb) {
+    const std::size_t n = std::min(cb, batch - s0);
+    ra.s0 = s0;
+    ra.n = n;
+    // ---- forward stages ----
+    for (const auto& stg : pr.sfwd) {
+      if (stg.dense < 0) {
+        ra.flags = tgk::kRFwd;
+        ra.fwd_begin = stg.begin;
+        ra.fwd_end = stg.end;
+        TG_CUDA_TRY(tgk::launch_tape_range<T>(ra, st));
+      } else {
+        const tgc::Dense& D = P.dense[stg.dense];
+        const auto& dp = pr.dplan[stg.dense];
+        tgk::GemmArgs<T> g{};   // Z[n_out][n] = W[n_out][n_in] . X[n_in][n] + b
+        g.A = UV + D.w_uv;
+        g.lda = D.n_in;
+        g.a_kmaj = true;
+        g.B = V + std::size_t(dp.xrow0) * cb;
+        g.ldb = cb;
+        g.b_nmaj = true;
+        g.C = V + std::size_t(D.out_row) * cb;
+        g.C2 = D.act_op ? V + std::size_t(D.act_row) * cb : nullptr;
+        g.ldc = cb;
+        g.bias = D.b_uv != tgc::kNone ? UV + D.b_uv : nullptr;
+        g.M = D.n_out;
+        g.N = static_cast<std::uint32_t>(n);
+        g.K = D.n_in;
+        g.act = D.act_op;
+        g.epi = tgk::kEpiBiasAct;
+        TG_CUDA_TRY(tgk::launch_gemm<T>(g, 1, st));
+      }
+      ++pr.launches;
+    }
+    ra.flags = tgk::kRSeed;
+    TG_CUDA_TRY(tgk::launch_tape_range<T>(ra, st));
+    ++pr.launches;
+    // ---- reverse stages ----
+    for (const auto& stg : pr.sbwd) {
+      if (stg.dense < 0) {
+        ra.flags = tgk::kRBwd;
+        ra.bwd_begin = stg.begin;
+        ra.bwd_end = stg.end;
+        TG_CUDA_TRY(tgk::launch_tape_range<T>(ra, st));
+        ++pr.launches;
+        continue;
+      }
+      const tgc::Dense& D = P.dense[stg.dense];
+      const auto& dp = pr.dplan[stg.dense];
+      if (D.act_op) {
+        TG_CUDA_TRY(tgk::launch_act_bwd<T>(G, V, D.out_row, D.act_row, D.n_out, n, cb, D.act_op, st));
+        ++pr.launches;
+      }
+      if (!dp.zero_x.empty()) {
+        TG_CUDA_TRY(tgk::launch_zero_rows<T>(G, dp.d_zero_x, static_cast<std::uint32_t>(dp.zero_x.size()), n, cb, st));
+        ++pr.launches;
+      }
+      {  // dX[n_in][n] (+)= W^T[n_in][n_out] . dZ[n_out][n]
+        tgk::GemmArgs<T> g{};
+        g.A = UV + D.w_uv;
+        g.lda = D.n_in;
+        g.a_kmaj = false;
+        g.B = G + std::size_t(D.out_row) * cb;
+        g.ldb = cb;
+        g.b_nmaj = true;
+        g.C = G + std::size_t(dp.xrow0) * cb;
+        g.ldc = cb;
+        g.M = D.n_in;
+        g.N = static_cast<std::uint32_t>(n);
+        g.K = D.n_out;
+        g.beta = dp.beta;
+        g.epi = tgk::kEpiAccum;
+        TG_CUDA_TRY(tgk::launch_gemm<T>(g, 1, st));
+        ++pr.launches;
+      }
+      if (dp.dw_dest0 != tgc::kNone) {  // dW[n_out][n_in] = dZ[n_out][n] . X^T, split-K over samples
+        const std::uint32_t splits = splitk_splits(D, n, sizeof(T));
+        tgk::GemmArgs<T> g{};
+        g.A = G + std::size_t(D.out_row) * cb;
+        g.lda = cb;
+        g.a_kmaj = true;
+        g.B = V + std::size_t(dp.xrow0) * cb;
+        g.ldb = cb;
+        g.b_nmaj = false;
+        g.C = sk;
+        g.M = D.n_out;
+        g.N = D.n_in;
+        g.K = static_cast<std::uint32_t>(n);
+        g.k_chunk = static_cast<std::uint32_t>((n + splits - 1) / splits);
+        g.epi = tgk::kEpiSplitK;
+        TG_CUDA_TRY(tgk::launch_gemm<T>(g, splits, st));
+        TG_CUDA_TRY(tgk::launch_splitk_reduce<T>(sk, acc + dp.dw_dest0, D.n_out * D.n_in, splits, st));
+        pr.launches += 2;
+      }
+      if (dp.db_dest0 != tgc::kNone) {
+        TG_CUDA_TRY(tgk::launch_rowsum<T>(G, D.out_row, D.n_out, n, cb, acc + dp.db_dest0, st));
+        ++pr.launches;
+      }
+    }
+    if (igrad) {
+      ra.flags = tgk::kROut;
+      TG_CUDA_TRY(tgk::launch_tape_range<T>(ra, st));
+      ++pr.launches;
+    }
+    TG_CUDA_TRY(tgk::launch_contract<T>(pr.d_gen_dests, static_cast<std::uint32_t>(pr.gen_dests.size()), pr.d_termoff,
+                                        pr.d_terms, G, V, idx, batch, s0, n, cb, acc, st));
+    ++pr.launches;
+  }
+  if (e1) TG_CUDA_TRY(cudaEventRecord(e1, st));
+  // fused: acc -> UG -> uniform reverse sweep -> grad_sum (-> GD)
+  tgk::ReduceArgs<T> rd{acc, pr.d_destuv, pr.n_dest(), 1};
+  ua.instr = pr.d_ubwd;
+  ua.n_instr = static_cast<std::uint32_t>(P.ubwd.size());
+  if (gd_params) {
+    ua.gd_params = static_cast<T*>(gd_params);
+    ua.gamma = static_cast<T>(gamma);
+    ua.gd_batch = static_cast<T>(static_cast<double>(batch));
+  }
+  TG_CUDA_TRY(tgk::launch_reduce_epilogue<T>(rd, ua, st));
+  ++pr.launches;
   return TG_OK;
 }
 
@@ -287,6 +667,10 @@ tg_status run_fb(tg_program& pr, const void* inputs, const std::int32_t* idx, st
                  void* loss, void* igrad, void* grad_sum, void* ws, std::size_t ws_bytes, cudaStream_t st,
                  void* gd_params = nullptr, double gamma = 0.0) {
   TG_TRY(upload(pr));
+  if (pr.staged) {
+    if (batch > 0 && P_inputs_missing(pr, inputs, idx)) return fail(TG_INVALID_ARGUMENT, "tg_forward_backward: inputs are NULL");
+    return run_staged<T>(pr, inputs, idx, batch, params, loss, igrad, grad_sum, ws, ws_bytes, st, gd_params, gamma);
+  }
   const tgc::Program& P = pr.P;
   const Layout L = layout(pr, batch);
   if (ws_bytes < L.total)
@@ -618,7 +1002,7 @@ tg_status tg_program_info_get(tg_program_t p, tg_program_info* info) {
     i.n_edges = P.n_edges;
     i.tile_samples = p->S;
     i.smem_bytes = static_cast<uint32_t>(p->smem_bytes);
-    i.storage = p->jit.ok ? 2 : (p->smem ? 0 : 1);
+    i.storage = p->staged ? 3 : (p->jit.ok ? 2 : (p->smem ? 0 : 1));
     i.dtype = P.dtype;
     *info = i;
     return TG_OK;

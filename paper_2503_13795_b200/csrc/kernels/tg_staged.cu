@@ -1,0 +1,410 @@
+// tg_staged.cu — kernels of the staged (HBM SoA) execution of large tapes.
+//
+// * k_tape_range: the tape interpreter over a range of the instruction stream,
+//   one thread per sample of the chunk, rows persistent in HBM [row][sample]
+//   between stages (same per-node semantics as k_tape, ops.hpp / propagate_node).
+// * k_gemm: register-tiled SIMT matrix product for dense layers (kDense):
+//     forward  Z = W X + b, H = act(Z)       (bias + activation epilogue)
+//     reverse  dX (+)= W^T dZ                 (adjoints of the layer inputs)
+//              dW  = dZ X^T  (split-K over the sample axis, fixed-order reduce)
+//   inner-product order per output matches the reference's left-to-right sum
+//   up to the K-tiling of the contraction.
+// * deterministic row sums (bias gradients) and generic batch-term contraction.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "tg_ops.cuh"
+#include "tg_staged.cuh"
+
+namespace tgk {
+
+using tgc::GatherTable;
+using tgc::Instr;
+using tgc::kIndexMask;
+using tgc::kModeShift;
+using tgc::Term;
+
+namespace {
+
+template <class T>
+struct RowAccS {
+  T* V;
+  T* G;
+  std::size_t ld, col;
+  const T* __restrict__ UV;
+  const std::int32_t* __restrict__ idx;
+  std::size_t batch, s;
+  const GatherTable* __restrict__ sg;
+  const std::uint32_t* __restrict__ cand;
+  const std::uint32_t* o;
+  const std::uint8_t* fl;
+  const std::uint32_t* ax;
+
+  __device__ __forceinline__ std::uint32_t sg_row(std::uint32_t i) const {
+    const GatherTable t = sg[i];
+    std::int32_t r = idx[std::size_t(t.col) * batch + s];
+    if (r < 0 || static_cast<std::uint32_t>(r) >= t.n_rows) r = 0;
+    return cand[t.cand_off + r];
+  }
+  __device__ __forceinline__ T val(std::uint32_t op) const {
+    const std::uint32_t m = op >> kModeShift, i = op & kIndexMask;
+    if (m == tgc::kSlot) return V[i * ld + col];
+    if (m == tgc::kUv) return UV[i];
+    return V[sg_row(i) * ld + col];
+  }
+  __device__ __forceinline__ void push(std::uint32_t k, T v) {
+    const std::uint32_t op = o[k];
+    const std::uint32_t m = op >> kModeShift, i = op & kIndexMask;
+    const std::uint8_t f = fl[k];
+    if (m == tgc::kSlot) {
+      T* p = &G[i * ld + col];
+      *p = (f & tgc::kAssign) ? v : *p + v;
+    } else if (m == tgc::kSGather) {
+      G[sg_row(i) * ld + col] += v;
+    } else if (f & tgc::kToAux) {
+      G[std::size_t(ax[k]) * ld + col] = v;
+    }
+  }
+};
+
+template <class T>
+__global__ void __launch_bounds__(128) k_tape_range(RangeArgs<T> a) {
+  const std::size_t col = std::size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (col >= a.n) return;
+  const std::size_t s = a.s0 + col;
+  T* V = a.V;
+  T* G = a.G;
+  const std::size_t ld = a.ld;
+  RowAccS<T> acc{V, G, ld, col, a.UV, a.idx, a.batch, s, a.sg, a.cand, nullptr, nullptr, nullptr};
+  if (a.flags & kRFwd) {
+    for (std::uint32_t k = a.fwd_begin; k < a.fwd_end; ++k) {
+      const Instr in = a.fwd[k];
+      T v;
+      if (in.kind == tgc::kNode) {
+        acc.o = a.opnd + in.opnd;
+        bool bad = false;
+        T badv = 0;
+        v = eval_node<T>(in.op, in.nops, acc.o, in.cst, acc, bad, badv);
+        if (bad) record_error(a.err_key, s, in.node);
+      } else if (in.kind == tgc::kInputLoad) {
+        v = a.inputs[std::size_t(in.aux) * a.batch + s];
+      } else if (in.kind == tgc::kDense) {
+        const tgc::Dense D = a.dense[in.aux];
+        const std::uint32_t* xo = a.opnd + D.x_opnd;
+        for (std::uint32_t j = 0; j < D.n_out; ++j) {
+          T z = D.b_uv != tgc::kNone ? a.UV[D.b_uv + j] : T(0);
+          const T* w = a.UV + D.w_uv + std::size_t(j) * D.n_in;
+          for (std::uint32_t q = 0; q < D.n_in; ++q) z += V[std::size_t(xo[q] & kIndexMask) * ld + col] * w[q];
+          V[std::size_t(D.out_row + j) * ld + col] = z;
+          if (D.act_op) V[std::size_t(D.act_row + j) * ld + col] = act_fwd<T>(D.act_op, z);
+        }
+        continue;
+      } else {
+        const GatherTable t = a.ug[in.aux];
+        std::int32_t r = a.idx[std::size_t(t.col) * a.batch + s];
+        if (r < 0 || static_cast<std::uint32_t>(r) >= t.n_rows) { record_error(a.err_key, s, 0xfffffffeu); r = 0; }
+        v = a.UV[a.cand[t.cand_off + r]];
+      }
+      V[std::size_t(in.out) * ld + col] = v;
+    }
+  }
+  if (a.flags & kRSeed) {
+    for (std::uint32_t z = 0; z < a.n_zero; ++z) G[std::size_t(a.zero_rows[z]) * ld + col] = T(0);
+    if (a.loss) a.loss[s] = V[std::size_t(a.root_row) * ld + col];
+    G[std::size_t(a.root_row) * ld + col] = T(1);
+  }
+  if (a.flags & kRBwd) {
+    for (std::uint32_t k = a.bwd_begin; k < a.bwd_end; ++k) {
+      const Instr in = a.bwd[k];
+      if (in.kind == tgc::kDense) {
+        const tgc::Dense D = a.dense[in.aux];
+        if (D.act_op)
+          for (std::uint32_t j = 0; j < D.n_out; ++j) {
+            const std::size_t hr = std::size_t(D.act_row + j) * ld + col, zr = std::size_t(D.out_row + j) * ld + col;
+            G[zr] = act_bwd<T>(D.act_op, G[hr], V[hr], V[zr]);
+          }
+        const std::uint32_t* xo = a.opnd + D.x_opnd;
+        const std::uint8_t* xf = a.oflag + D.x_opnd;
+        for (std::uint32_t q = 0; q < D.n_in; ++q) {
+          T dx = 0;
+          for (std::uint32_t j = 0; j < D.n_out; ++j)
+            dx += G[std::size_t(D.out_row + j) * ld + col] * a.UV[D.w_uv + std::size_t(j) * D.n_in + q];
+          T* p = &G[std::size_t(xo[q] & kIndexMask) * ld + col];
+          *p = (xf[q] & tgc::kAssign) ? dx : *p + dx;
+        }
+        continue;
+      }
+      acc.o = a.opnd + in.opnd;
+      acc.fl = a.oflag + in.opnd;
+      acc.ax = a.oaux + in.opnd;
+      const T g = G[std::size_t(in.out) * ld + col];
+      const T y = V[std::size_t(in.out) * ld + col];
+      propagate<T>(in.op, in.nops, acc.o, in.cst, g, y, acc);
+    }
+  }
+  if ((a.flags & kROut) && a.igrad)
+    for (std::uint32_t c = 0; c < a.n_inputs; ++c) {
+      const std::uint32_t r = a.input_rows[c];
+      if (r != tgc::kNone) a.igrad[std::size_t(c) * a.batch + s] = G[std::size_t(r) * ld + col];
+    }
+}
+
+// ---- register-tiled SIMT GEMM ------------------------------------------------
+template <class T> struct GemmTile;
+template <> struct GemmTile<float> { static constexpr int BM = 128, BN = 128, BK = 8, TM = 8, TN = 8; };
+template <> struct GemmTile<double> { static constexpr int BM = 64, BN = 64, BK = 8, TM = 4, TN = 4; };
+
+template <class T, bool AK, bool BN_>
+__global__ void __launch_bounds__(256) k_gemm(GemmArgs<T> g) {
+  constexpr int BM = GemmTile<T>::BM, BN = GemmTile<T>::BN, BK = GemmTile<T>::BK;
+  constexpr int TM = GemmTile<T>::TM, TN = GemmTile<T>::TN;
+  __shared__ T As[2][BK][BM + 4];
+  __shared__ T Bs[2][BK][BN + 4];
+  const int tid = threadIdx.x;
+  const int tx = tid % (BN / TN), ty = tid / (BN / TN);
+  const std::uint32_t m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  std::uint32_t k_begin = 0, k_end = g.K;
+  if (g.epi == kEpiSplitK) {
+    k_begin = blockIdx.z * g.k_chunk;
+    k_end = min(g.K, k_begin + g.k_chunk);
+  }
+  T acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
+
+  constexpr int A_PER = BM * BK / 256, B_PER = BN * BK / 256;
+  T ra[A_PER], rb[B_PER];
+  auto load = [&](std::uint32_t k0) {
+#pragma unroll
+    for (int e = 0; e < A_PER; ++e) {
+      const int li = tid + e * 256;
+      int mm, kk;
+      if (AK) { kk = li % BK; mm = li / BK; } else { mm = li % BM; kk = li / BM; }
+      const std::uint32_t gm = m0 + mm, gk = k0 + kk;
+      ra[e] = (gm < g.M && gk < k_end) ? (AK ? g.A[std::size_t(gm) * g.lda + gk] : g.A[std::size_t(gk) * g.lda + gm]) : T(0);
+    }
+#pragma unroll
+    for (int e = 0; e < B_PER; ++e) {
+      const int li = tid + e * 256;
+      int nn, kk;
+      if (BN_) { nn = li % BN; kk = li / BN; } else { kk = li % BK; nn = li / BK; }
+      const std::uint32_t gn = n0 + nn, gk = k0 + kk;
+      rb[e] = (gn < g.N && gk < k_end) ? (BN_ ? g.B[std::size_t(gk) * g.ldb + gn] : g.B[std::size_t(gn) * g.ldb + gk]) : T(0);
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int e = 0; e < A_PER; ++e) {
+      const int li = tid + e * 256;
+      int mm, kk;
+      if (AK) { kk = li % BK; mm = li / BK; } else { mm = li % BM; kk = li / BM; }
+      As[buf][kk][mm] = ra[e];
+    }
+#pragma unroll
+    for (int e = 0; e < B_PER; ++e) {
+      const int li = tid + e * 256;
+      int nn, kk;
+      if (BN_) { nn = li % BN; kk = li / BN; } else { kk = li % BK; nn = li / BK; }
+      Bs[buf][kk][nn] = rb[e];
+    }
+  };
+  int buf = 0;
+  load(k_begin);
+  store(0);
+  __syncthreads();
+  for (std::uint32_t k0 = k_begin; k0 < k_end; k0 += BK) {
+    const bool more = k0 + BK < k_end;
+    if (more) load(k0 + BK);   // next tile in flight while this one is consumed
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      T a[TM], b[TN];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) a[i] = As[buf][kk][ty * TM + i];
+#pragma unroll
+      for (int j = 0; j < TN; ++j) b[j] = Bs[buf][kk][tx * TN + j];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] += a[i] * b[j];
+    }
+    if (more) {
+      store(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+  // epilogue
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const std::uint32_t m = m0 + ty * TM + i;
+    if (m >= g.M) continue;
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const std::uint32_t n = n0 + tx * TN + j;
+      if (n >= g.N) continue;
+      if (g.epi == kEpiBiasAct) {
+        const T z = (g.bias ? g.bias[m] : T(0)) + acc[i][j];
+        g.C[std::size_t(m) * g.ldc + n] = z;
+        if (g.act) g.C2[std::size_t(m) * g.ldc + n] = act_fwd<T>(g.act, z);
+      } else if (g.epi == kEpiAccum) {
+        T* p = &g.C[std::size_t(m) * g.ldc + n];
+        *p = g.beta ? *p + acc[i][j] : acc[i][j];
+      } else {
+        g.C[(std::size_t(blockIdx.z) * g.M + m) * g.N + n] = acc[i][j];
+      }
+    }
+  }
+}
+
+template <class T>
+__global__ void k_splitk_reduce(const T* __restrict__ part, T* __restrict__ dst, std::uint32_t MN, std::uint32_t splits) {
+  const std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= MN) return;
+  T t = 0;
+  for (std::uint32_t z = 0; z < splits; ++z) t += part[std::size_t(z) * MN + i];
+  dst[i] += t;
+}
+
+template <class T>
+__global__ void k_act_bwd(T* G, const T* V, std::uint32_t z_row, std::uint32_t h_row, std::size_t n, std::size_t ld,
+                          std::uint32_t act) {
+  const std::size_t s = std::size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const std::size_t zr = std::size_t(z_row + blockIdx.y) * ld + s, hr = std::size_t(h_row + blockIdx.y) * ld + s;
+  G[zr] = act_bwd<T>(act, G[hr], V[hr], V[zr]);
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) k_rowsum(const T* G, std::uint32_t row0, std::size_t n, std::size_t ld, T* dst) {
+  __shared__ T red[256];
+  const T* row = G + std::size_t(row0 + blockIdx.x) * ld;
+  T t = 0;
+  for (std::size_t s = threadIdx.x; s < n; s += 256) t += row[s];
+  red[threadIdx.x] = t;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) dst[blockIdx.x] += red[0];
+}
+
+template <class T>
+__global__ void k_zero_rows(T* X, const std::uint32_t* rows, std::size_t n, std::size_t ld) {
+  const std::size_t s = std::size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s < n) X[std::size_t(rows[blockIdx.y]) * ld + s] = T(0);
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) k_contract(const std::uint32_t* dests, const std::uint32_t* term_off, const Term* terms,
+                                                  const T* G, const T* V, const std::int32_t* idx, std::size_t batch,
+                                                  std::size_t s0, std::size_t n, std::size_t ld, T* acc) {
+  __shared__ T red[256];
+  const std::uint32_t d = dests[blockIdx.x];
+  T tot = 0;
+  for (std::uint32_t q = term_off[d]; q < term_off[d + 1]; ++q) {
+    const Term t = terms[q];
+    const T* ga = G + std::size_t(t.a) * ld;
+    T part = 0;
+    if (t.kind == 0) {
+      if (t.f == tgc::kNone) {
+        for (std::size_t s = threadIdx.x; s < n; s += 256) part += ga[s];
+      } else {
+        const T* vf = V + std::size_t(t.f) * ld;
+        for (std::size_t s = threadIdx.x; s < n; s += 256) part += ga[s] * vf[s];
+      }
+    } else {
+      const std::int32_t* ix = idx + std::size_t(t.f) * batch + s0;
+      for (std::size_t s = threadIdx.x; s < n; s += 256) part += ix[s] == t.row ? ga[s] : T(0);
+    }
+    tot += static_cast<T>(t.coef) * part;
+  }
+  red[threadIdx.x] = tot;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) acc[d] += red[0];
+}
+
+}  // namespace
+
+template <class T>
+cudaError_t launch_tape_range(const RangeArgs<T>& a, cudaStream_t st) {
+  if (a.n == 0) return cudaSuccess;
+  k_tape_range<T><<<static_cast<unsigned>((a.n + 127) / 128), 128, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t launch_gemm(const GemmArgs<T>& g, std::uint32_t splits, cudaStream_t st) {
+  constexpr int BM = GemmTile<T>::BM, BN = GemmTile<T>::BN;
+  if (g.M == 0 || g.N == 0) return cudaSuccess;
+  const dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, g.epi == kEpiSplitK ? splits : 1);
+  if (g.a_kmaj && g.b_nmaj) k_gemm<T, true, true><<<grid, 256, 0, st>>>(g);
+  else if (g.a_kmaj && !g.b_nmaj) k_gemm<T, true, false><<<grid, 256, 0, st>>>(g);
+  else if (!g.a_kmaj && g.b_nmaj) k_gemm<T, false, true><<<grid, 256, 0, st>>>(g);
+  else k_gemm<T, false, false><<<grid, 256, 0, st>>>(g);
+  return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t launch_splitk_reduce(const T* part, T* dst, std::uint32_t MN, std::uint32_t splits, cudaStream_t st) {
+  k_splitk_reduce<T><<<(MN + 255) / 256, 256, 0, st>>>(part, dst, MN, splits);
+  return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t launch_act_bwd(T* G, const T* V, std::uint32_t z_row, std::uint32_t h_row, std::uint32_t n_out, std::size_t n,
+                           std::size_t ld, std::uint32_t act, cudaStream_t st) {
+  if (n == 0 || n_out == 0) return cudaSuccess;
+  k_act_bwd<T><<<dim3(static_cast<unsigned>((n + 255) / 256), n_out), 256, 0, st>>>(G, V, z_row, h_row, n, ld, act);
+  return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t launch_rowsum(const T* G, std::uint32_t row0, std::uint32_t rows, std::size_t n, std::size_t ld, T* dst,
+                          cudaStream_t st) {
+  if (rows == 0) return cudaSuccess;
+  k_rowsum<T><<<rows, 256, 0, st>>>(G, row0, n, ld, dst);
+  return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t launch_zero_rows(T* X, const std::uint32_t* rows, std::uint32_t count, std::size_t n, std::size_t ld,
+                             cudaStream_t st) {
+  if (count == 0 || n == 0) return cudaSuccess;
+  k_zero_rows<T><<<dim3(static_cast<unsigned>((n + 255) / 256), count), 256, 0, st>>>(X, rows, n, ld);
+  return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t launch_contract(const std::uint32_t* dests, std::uint32_t n_dests, const std::uint32_t* term_off,
+                            const Term* terms, const T* G, const T* V, const std::int32_t* idx, std::size_t batch,
+                            std::size_t s0, std::size_t n, std::size_t ld, T* acc, cudaStream_t st) {
+  if (n_dests == 0) return cudaSuccess;
+  k_contract<T><<<n_dests, 256, 0, st>>>(dests, term_off, terms, G, V, idx, batch, s0, n, ld, acc);
+  return cudaGetLastError();
+}
+
+#define TG_STAGED_INST(T)                                                                                                  \
+  template cudaError_t launch_tape_range<T>(const RangeArgs<T>&, cudaStream_t);                                            \
+  template cudaError_t launch_gemm<T>(const GemmArgs<T>&, std::uint32_t, cudaStream_t);                                    \
+  template cudaError_t launch_splitk_reduce<T>(const T*, T*, std::uint32_t, std::uint32_t, cudaStream_t);                  \
+  template cudaError_t launch_act_bwd<T>(T*, const T*, std::uint32_t, std::uint32_t, std::uint32_t, std::size_t,           \
+                                         std::size_t, std::uint32_t, cudaStream_t);                                        \
+  template cudaError_t launch_rowsum<T>(const T*, std::uint32_t, std::uint32_t, std::size_t, std::size_t, T*,              \
+                                        cudaStream_t);                                                                     \
+  template cudaError_t launch_zero_rows<T>(T*, const std::uint32_t*, std::uint32_t, std::size_t, std::size_t,              \
+                                           cudaStream_t);                                                                  \
+  template cudaError_t launch_contract<T>(const std::uint32_t*, std::uint32_t, const std::uint32_t*, const Term*,          \
+                                          const T*, const T*, const std::int32_t*, std::size_t, std::size_t, std::size_t,  \
+                                          std::size_t, T*, cudaStream_t);
+TG_STAGED_INST(float)
+TG_STAGED_INST(double)
+
+}  // namespace tgk

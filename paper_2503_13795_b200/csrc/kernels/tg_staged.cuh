@@ -1,0 +1,97 @@
+// tg_staged.cuh — staged execution of large tapes over an HBM SoA workspace.
+//
+// Tapes whose per-sample rows do not fit a shared-memory tile (cfg3/4/5) run
+// stage by stage over a chunk of the batch: per-sample segments of the
+// instruction stream on the interpreter (one thread per sample, rows in HBM
+// [row][sample]), dense layers (kDense) as matrix products over the chunk.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "../host/tg_program.hpp"
+
+namespace tgk {
+
+enum RangeFlags : std::uint32_t {
+  kRFwd = 1,      // forward instructions [fwd_begin, fwd_end)
+  kRSeed = 2,     // zero_rows <- 0, loss out, root adjoint <- 1
+  kRBwd = 4,      // reverse instructions [bwd_begin, bwd_end)
+  kROut = 8,      // input gradients out
+};
+
+template <class T>
+struct RangeArgs {
+  const tgc::Instr* fwd;
+  const tgc::Instr* bwd;
+  const std::uint32_t* opnd;
+  const std::uint8_t* oflag;
+  const std::uint32_t* oaux;
+  const std::uint32_t* zero_rows;
+  const std::uint32_t* input_rows;
+  const tgc::GatherTable* ug;
+  const tgc::GatherTable* sg;
+  const std::uint32_t* cand;
+  const tgc::Dense* dense;
+  const T* UV;
+  const T* inputs;
+  const std::int32_t* idx;
+  T* loss;
+  T* igrad;
+  T* V;
+  T* G;
+  unsigned long long* err_key;
+  std::size_t batch;      // global batch (leading dim of inputs / idx / outputs)
+  std::size_t s0;         // first sample of the chunk
+  std::size_t n;          // samples in the chunk
+  std::size_t ld;         // row stride of V / G (chunk capacity)
+  std::uint32_t fwd_begin, fwd_end, bwd_begin, bwd_end;
+  std::uint32_t n_zero, n_inputs, root_row, flags;
+};
+
+// C(m, n) = sum_k A(m, k) B(k, n) over an operand view:
+//   A(m, k) = A[m * lda + k]  (a_kmaj)   or  A[k * lda + m]
+//   B(k, n) = B[k * ldb + n]  (b_nmaj)   or  B[n * ldb + k]
+enum GemmEpi : int {
+  kEpiBiasAct = 0,   // C = acc (+ bias[m]); C2 = act(C) if act
+  kEpiAccum = 1,     // C = beta ? C + acc : acc
+  kEpiSplitK = 2,    // part[kz][m][n] = acc over this CTA's K slice
+};
+
+template <class T>
+struct GemmArgs {
+  const T* A;
+  const T* B;
+  T* C;
+  T* C2;
+  const T* bias;
+  std::size_t lda, ldb, ldc;
+  std::uint32_t M, N, K;
+  std::uint32_t k_chunk;   // split-K slice (kEpiSplitK)
+  std::uint32_t act;
+  int beta;
+  bool a_kmaj, b_nmaj;
+  int epi;
+};
+
+template <class T> cudaError_t launch_tape_range(const RangeArgs<T>& a, cudaStream_t st);
+template <class T> cudaError_t launch_gemm(const GemmArgs<T>& g, std::uint32_t splits, cudaStream_t st);
+// dst[m * N + n] += sum_kz part[kz][m][n]   (fixed order)
+template <class T> cudaError_t launch_splitk_reduce(const T* part, T* dst, std::uint32_t MN, std::uint32_t splits, cudaStream_t st);
+// G[z rows] = act'(G[h rows], V[h rows], V[z rows]) for n_out consecutive rows
+template <class T> cudaError_t launch_act_bwd(T* G, const T* V, std::uint32_t z_row, std::uint32_t h_row, std::uint32_t n_out,
+                                              std::size_t n, std::size_t ld, std::uint32_t act, cudaStream_t st);
+// dst[j] += sum_s G[(row0 + j) * ld + s]   (fixed-order block tree per row)
+template <class T> cudaError_t launch_rowsum(const T* G, std::uint32_t row0, std::uint32_t rows, std::size_t n, std::size_t ld,
+                                             T* dst, cudaStream_t st);
+// zero `count` rows of X starting at row0 (first n columns)
+template <class T> cudaError_t launch_zero_rows(T* X, const std::uint32_t* rows, std::uint32_t count, std::size_t n, std::size_t ld, cudaStream_t st);
+// generic batch terms of the listed destinations over the chunk: acc[d] += ...
+template <class T>
+cudaError_t launch_contract(const std::uint32_t* dests, std::uint32_t n_dests, const std::uint32_t* term_off, const tgc::Term* terms,
+                            const T* G, const T* V, const std::int32_t* idx, std::size_t batch, std::size_t s0, std::size_t n,
+                            std::size_t ld, T* acc, cudaStream_t st);
+
+}  // namespace tgk

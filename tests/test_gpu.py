@@ -18,12 +18,16 @@ pytestmark = pytest.mark.gpu
 if not torch.cuda.is_available():
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
-TIERS = ["jit", "interp"]
+TIERS = ["jit", "interp", "staged"]
 
 
 def make_prog(desc, tier):
+    """jit: register-resident specialised kernel; interp: shared-memory tile
+    interpreter; staged: HBM-resident rows, dense layers as GEMMs."""
     os.environ["TG_JIT"] = "1" if tier == "jit" else "0"
+    os.environ["TG_STAGED"] = "1" if tier == "staged" else "0"
     p = tg.Program(desc)
+    os.environ.pop("TG_STAGED")
     return p
 
 
@@ -107,6 +111,22 @@ def test_larger_batches_vs_oracle(tier, name, dims, dt, b):
         assert rel(G, r["grad_sum"]) <= TOL[dt]
     if desc.n_inputs:
         assert rel(IG, r["input_grad"]) <= TOL[dt] * 10
+
+
+@pytest.mark.parametrize("name,dims,b", [("char_mlp", None, 262144), ("wide_mlp", None, 512)])
+def test_full_size_tensor_configs(name, dims, b):
+    """cfg3 at its full batch (262,144) and cfg5 at full width through the
+    default tier (staged: dense layers as GEMMs) against the oracle on a
+    sampled subset and on the batch gradient (cfg3: oracle over all samples)."""
+    desc = tg.build_model(name, dims, "f32", seed=3).describe()
+    x, k = tg.synth_batch(name, dims, "f32", seed=17, batch=b, n_inputs=desc.n_inputs, n_index=desc.n_index_inputs)
+    os.environ.pop("TG_JIT", None)
+    prog = tg.Program(desc)
+    assert prog.info["storage"] == 3
+    L, IG, G = run(prog, desc, x, k, desc.param_values(), b, want_igrad=False)
+    r = oracle.run(desc, x.astype(np.float64), k, desc.param_values(), threads=os.cpu_count() or 8)
+    assert close_rel(L, r["loss"], 1e-5, 1e-6)
+    assert rel(G, r["grad_sum"]) <= 1e-5
 
 
 def test_cfg1_full_size_closed_form():
