@@ -212,6 +212,16 @@ tg_status tg_check_device_error(tg_program_t p, tg_stream_t stream, int64_t* sam
 tg_status tg_profile_enable(tg_program_t p, int on);
 tg_status tg_profile_read(tg_program_t p, double* tape_ms, uint64_t* tape_launches);
 
+/* The dense-layer matrix product of the staged path (exposed for testing):
+ *   C[m][n] (+)= sum_k A(m,k) B(k,n),   m < M, n < N, k < K
+ *   A(m,k) = a_kmajor ? A[m*lda + k] : A[k*lda + m]
+ *   B(k,n) = b_nmajor ? B[k*ldb + n] : B[n*ldb + k]
+ * engine 0: SIMT register-tiled (fp32 / fp64); 1: tcgen05 tensor cores,
+ * 3xTF32 (fp32 only).  accumulate != 0 adds into C.  Device pointers. */
+tg_status tg_gemm(tg_dtype dtype, int engine, uint32_t M, uint32_t N, uint32_t K, const void* A, size_t lda,
+                  int a_kmajor, const void* B, size_t ldb, int b_nmajor, void* C, size_t ldc, int accumulate,
+                  tg_stream_t stream);
+
 /* Short tapes are specialised into a register-resident kernel (NVRTC,
  * sm_100a) on first use.  Returns its CUDA source and compiler log;
  * TG_UNSUPPORTED when the program runs on the interpreter kernel instead.

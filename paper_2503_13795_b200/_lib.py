@@ -105,6 +105,7 @@ def _load():
         "tg_train_step": (st, [P, P, P, sz, P, P, P, C.c_double, P, sz, P]),
         "tg_check_device_error": (st, [P, P, C.POINTER(i64), C.POINTER(u32)]),
         "tg_launch_count": (u64, [P]),
+        "tg_gemm": (st, [st, C.c_int, u32, u32, u32, P, sz, C.c_int, P, sz, C.c_int, P, sz, C.c_int, P]),
         "tg_program_jit": (st, [P, C.POINTER(C.c_char_p), C.POINTER(C.c_char_p), C.POINTER(C.c_double)]),
         "tg_profile_enable": (st, [P, C.c_int]),
         "tg_profile_read": (st, [P, C.POINTER(C.c_double), C.POINTER(u64)]),

@@ -13,6 +13,7 @@
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <unordered_map>
 #include <vector>
 
@@ -147,6 +148,7 @@ struct tg_program {
   std::vector<std::uint32_t> gen_dests;
   std::uint32_t* d_gen_dests = nullptr;
   std::size_t chunk = 0;          // samples per chunk (0 = by batch)
+  bool umma = true;               // fp32 dense layers on tcgen05 (3xTF32); TG_UMMA=0 -> SIMT GEMM
   ~tg_program() {
     tgj::release(jit);
     for (auto& e : ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
@@ -180,6 +182,7 @@ void build_staged_plan(tg_program& pr) {
     if (std::uint64_t(D.n_out) * D.n_in >= 2048) big = true;
   }
   pr.staged = env ? env[0] == '1' : (big && !tgj::eligible(P));
+  if (const char* u = std::getenv("TG_UMMA")) pr.umma = u[0] != '0';
   if (!pr.staged || P.root_row == tgc::kNone) { pr.staged = false; return; }
   // weight / bias gradient destinations handled by the GEMM path
   std::vector<std::uint8_t> covered(P.dest_uv.size(), 0);
@@ -413,6 +416,23 @@ tg_status upload(tg_program& pr) {
   return TG_OK;
 }
 
+// Dense-layer GEMM: tcgen05 tensor cores for fp32 (3xTF32), SIMT for fp64
+// (there is no fp64 tcgen05 kind) or when disabled.
+template <class T>
+cudaError_t dense_gemm(const tg_program& pr, const tgk::GemmArgs<T>& g, std::uint32_t splits, cudaStream_t st) {
+  if constexpr (std::is_same_v<T, float>) {
+    // Roles on tcgen05: bit 0 forward Z = W X, bit 1 input adjoints, bit 2 weight
+    // gradients.  Default 6: tensor-core accumulation (~6e-6 relative at
+    // K ~ 1e3) in the forward would flip ReLU masks of near-zero
+    // pre-activations and move the batch gradient by ~5e-4 (measured, cfg5);
+    // backward products only scale errors, they switch no mask.
+    static const int mask = std::getenv("TG_UMMA_MASK") ? std::atoi(std::getenv("TG_UMMA_MASK")) : 6;
+    const int role = g.epi == tgk::kEpiBiasAct ? 1 : g.epi == tgk::kEpiAccum ? 2 : 4;
+    if (pr.umma && (mask & role)) return tgk::launch_gemm_umma(g, splits, st);
+  }
+  return tgk::launch_gemm<T>(g, splits, st);
+}
+
 bool P_inputs_missing(const tg_program& pr, const void* inputs, const std::int32_t* idx) {
   return (pr.P.n_inputs && !inputs) || (pr.P.n_index_inputs && !idx);
 }
@@ -456,8 +476,7 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
   ua.n_uv = P.n_uv;
   ua.root_uv = P.root_uv;
   ua.done = reinterpret_cast<unsigned*>(w + L.done);
-  TG_CUDA_TRY(tgk::launch_uniform_fwd<T>(ua, st));
-  ++pr.launches;
+  TG_CUDA_TRY(tgk::launch_uniform_fwd<T>(ua, st, pr.launches));
   TG_CUDA_TRY(cudaMemsetAsync(acc, 0, std::max<std::uint32_t>(1, pr.n_dest()) * sizeof(T), st));
 
   tgk::RangeArgs<T> ra{};
@@ -569,7 +588,7 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
         g.K = D.n_in;
         g.act = D.act_op;
         g.epi = tgk::kEpiBiasAct;
-        TG_CUDA_TRY(tgk::launch_gemm<T>(g, 1, st));
+        TG_CUDA_TRY(dense_gemm<T>(pr, g, 1, st));
       }
       ++pr.launches;
     }
@@ -611,7 +630,7 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
         g.K = D.n_out;
         g.beta = dp.beta;
         g.epi = tgk::kEpiAccum;
-        TG_CUDA_TRY(tgk::launch_gemm<T>(g, 1, st));
+        TG_CUDA_TRY(dense_gemm<T>(pr, g, 1, st));
         ++pr.launches;
       }
       if (dp.dw_dest0 != tgc::kNone) {  // dW[n_out][n_in] = dZ[n_out][n] . X^T, split-K over samples
@@ -629,7 +648,7 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
         g.K = static_cast<std::uint32_t>(n);
         g.k_chunk = static_cast<std::uint32_t>((n + splits - 1) / splits);
         g.epi = tgk::kEpiSplitK;
-        TG_CUDA_TRY(tgk::launch_gemm<T>(g, splits, st));
+        TG_CUDA_TRY(dense_gemm<T>(pr, g, splits, st));
         TG_CUDA_TRY(tgk::launch_splitk_reduce<T>(sk, acc + dp.dw_dest0, D.n_out * D.n_in, splits, st));
         pr.launches += 2;
       }
@@ -657,8 +676,7 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
     ua.gamma = static_cast<T>(gamma);
     ua.gd_batch = static_cast<T>(static_cast<double>(batch));
   }
-  TG_CUDA_TRY(tgk::launch_reduce_epilogue<T>(rd, ua, st));
-  ++pr.launches;
+  TG_CUDA_TRY(tgk::launch_reduce_epilogue<T>(rd, ua, st, pr.launches));
   return TG_OK;
 }
 
@@ -704,9 +722,8 @@ tg_status run_fb(tg_program& pr, const void* inputs, const std::int32_t* idx, st
   ua.n_uv = P.n_uv;
   ua.root_uv = P.root_uv;
   ua.done = reinterpret_cast<unsigned*>(w + L.done);
-  TG_CUDA_TRY(tgk::launch_uniform_fwd<T>(ua, st));
+  TG_CUDA_TRY(tgk::launch_uniform_fwd<T>(ua, st, pr.launches));
   tgk::ReduceArgs<T> ra{partial, pr.d_destuv, 0, 1};
-  ++pr.launches;
 
   const std::size_t grid = grid_for(pr, batch);
   if (batch > 0 && P.root_row != tgc::kNone) {
@@ -787,8 +804,7 @@ tg_status run_fb(tg_program& pr, const void* inputs, const std::int32_t* idx, st
     ua.gamma = static_cast<T>(gamma);
     ua.gd_batch = static_cast<T>(static_cast<double>(batch));
   }
-  TG_CUDA_TRY(tgk::launch_reduce_epilogue<T>(ra, ua, st));
-  ++pr.launches;
+  TG_CUDA_TRY(tgk::launch_reduce_epilogue<T>(ra, ua, st, pr.launches));
   return TG_OK;
 }
 
@@ -1135,3 +1151,37 @@ uint64_t tg_launch_count(tg_program_t p) { return p ? p->launches : 0; }
 void tg_program_free(tg_program_t p) { delete p; }
 
 }  // extern "C"
+
+extern "C" tg_status tg_gemm(tg_dtype dtype, int engine, uint32_t M, uint32_t N, uint32_t K, const void* A, size_t lda,
+                             int a_kmajor, const void* B, size_t ldb, int b_nmajor, void* C, size_t ldc, int accumulate,
+                             tg_stream_t stream) {
+  return guard([&] {
+    auto st = static_cast<cudaStream_t>(stream);
+    auto fill = [&](auto* a, auto* b, auto* c, auto& g) {
+      g.A = a;
+      g.B = b;
+      g.C = c;
+      g.lda = lda;
+      g.ldb = ldb;
+      g.ldc = ldc;
+      g.M = M;
+      g.N = N;
+      g.K = K;
+      g.a_kmaj = a_kmajor != 0;
+      g.b_nmaj = b_nmajor != 0;
+      g.beta = accumulate != 0;
+      g.epi = tgk::kEpiAccum;
+    };
+    if (dtype == TG_F32) {
+      tgk::GemmArgs<float> g{};
+      fill(static_cast<const float*>(A), static_cast<const float*>(B), static_cast<float*>(C), g);
+      TG_CUDA_TRY(engine == 1 ? tgk::launch_gemm_umma(g, 1, st) : tgk::launch_gemm<float>(g, 1, st));
+    } else {
+      if (engine == 1) return fail(TG_UNSUPPORTED, "tg_gemm: no fp64 tcgen05 kind");
+      tgk::GemmArgs<double> g{};
+      fill(static_cast<const double*>(A), static_cast<const double*>(B), static_cast<double*>(C), g);
+      TG_CUDA_TRY(tgk::launch_gemm<double>(g, 1, st));
+    }
+    return TG_OK;
+  });
+}

@@ -13,6 +13,7 @@
 // x -= gamma * g / b (sgd_step).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "tg_epilogue.cuh"
@@ -75,13 +76,38 @@ __device__ __forceinline__ bool child_rule(std::uint8_t op, std::uint32_t n, std
 
 }  // namespace
 
+// Grid-wide part of the prologue for large parameter vectors (cfg5: 1.86 M).
+template <class T>
+__global__ void __launch_bounds__(kBlock) k_uv_init(UniformArgs<T> a) {
+  const std::uint32_t stride = gridDim.x * kBlock;
+  for (std::uint32_t i = blockIdx.x * kBlock + threadIdx.x; i < a.n_uv; i += stride) {
+    a.UG[i] = T(0);
+    if (i < a.n_params) a.UV[i] = a.params[i];
+    else if (i >= a.const_base) a.UV[i] = a.consts[i - a.const_base];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && a.done) *a.done = 0u;
+}
+
+// Grid-wide grad_sum copy (+ fused GD) for large parameter vectors.
+template <class T>
+__global__ void __launch_bounds__(kBlock) k_finalize(UniformArgs<T> a) {
+  const std::uint32_t stride = gridDim.x * kBlock;
+  for (std::uint32_t i = blockIdx.x * kBlock + threadIdx.x; i < a.n_params; i += stride) {
+    const T gsum = a.UG[i];
+    if (a.grad_sum) a.grad_sum[i] = gsum;
+    if (a.gd_params) a.gd_params[i] = a.gd_params[i] - a.gamma * gsum / a.gd_batch;
+  }
+}
+
 template <class T>
 __global__ void __launch_bounds__(kBlock) k_uniform_fwd(UniformArgs<T> a) {
   __shared__ T red[kBlock];
-  for (std::uint32_t i = threadIdx.x; i < a.n_params; i += kBlock) a.UV[i] = a.params[i];
-  for (std::uint32_t i = threadIdx.x; i < a.n_const; i += kBlock) a.UV[a.const_base + i] = a.consts[i];
-  for (std::uint32_t i = threadIdx.x; i < a.n_uv; i += kBlock) a.UG[i] = T(0);
-  if (threadIdx.x == 0 && a.done) *a.done = 0u;
+  if (a.copy) {
+    for (std::uint32_t i = threadIdx.x; i < a.n_params; i += kBlock) a.UV[i] = a.params[i];
+    for (std::uint32_t i = threadIdx.x; i < a.n_const; i += kBlock) a.UV[a.const_base + i] = a.consts[i];
+    for (std::uint32_t i = threadIdx.x; i < a.n_uv; i += kBlock) a.UG[i] = T(0);
+    if (threadIdx.x == 0 && a.done) *a.done = 0u;
+  }
   __syncthreads();
   UvAcc<T> acc{a.UV, a.UG, nullptr, a.const_base};
   for (std::uint32_t k = 0; k < a.n_instr; ++k) {
@@ -165,7 +191,8 @@ __global__ void __launch_bounds__(kBlock) k_reduce_epilogue(ReduceArgs<T> r, Uni
     }
     __syncthreads();
   }
-  // ---- grad_sum and the fused GD update ----
+  // ---- grad_sum and the fused GD update (large vectors: k_finalize) ----
+  if (!a.copy) return;
   for (std::uint32_t i = threadIdx.x; i < a.n_params; i += kBlock) {
     const T gsum = a.UG[i];
     if (a.grad_sum) a.grad_sum[i] = gsum;
@@ -173,23 +200,43 @@ __global__ void __launch_bounds__(kBlock) k_reduce_epilogue(ReduceArgs<T> r, Uni
   }
 }
 
+constexpr std::uint32_t kGridCopy = 1u << 16;   // above this many entries, copies run grid-wide
+
 template <class T>
-cudaError_t launch_uniform_fwd(const UniformArgs<T>& a, cudaStream_t st) {
-  k_uniform_fwd<T><<<1, kBlock, 0, st>>>(a);
+cudaError_t launch_uniform_fwd(const UniformArgs<T>& a, cudaStream_t st, std::uint64_t& launches) {
+  UniformArgs<T> b = a;
+  b.copy = a.n_uv <= kGridCopy;
+  if (!b.copy) {
+    k_uv_init<T><<<std::min<std::uint32_t>(592, (a.n_uv + kBlock - 1) / kBlock), kBlock, 0, st>>>(a);
+    ++launches;
+    if (a.n_instr == 0 && !a.UVc) return cudaGetLastError();
+  }
+  k_uniform_fwd<T><<<1, kBlock, 0, st>>>(b);
+  ++launches;
   return cudaGetLastError();
 }
 
 template <class T>
-cudaError_t launch_reduce_epilogue(const ReduceArgs<T>& r, const UniformArgs<T>& a, cudaStream_t st) {
+cudaError_t launch_reduce_epilogue(const ReduceArgs<T>& r, const UniformArgs<T>& a, cudaStream_t st,
+                                   std::uint64_t& launches) {
   const unsigned warps_per_block = kBlock / 32;
   const unsigned grid = r.n_dest ? (r.n_dest + warps_per_block - 1) / warps_per_block : 1;
-  k_reduce_epilogue<T><<<grid, kBlock, 0, st>>>(r, a);
+  UniformArgs<T> b = a;
+  b.copy = a.n_params <= kGridCopy;
+  k_reduce_epilogue<T><<<grid, kBlock, 0, st>>>(r, b);
+  ++launches;
+  if (!b.copy) {
+    k_finalize<T><<<std::min<std::uint32_t>(592, (a.n_params + kBlock - 1) / kBlock), kBlock, 0, st>>>(b);
+    ++launches;
+  }
   return cudaGetLastError();
 }
 
-template cudaError_t launch_uniform_fwd<double>(const UniformArgs<double>&, cudaStream_t);
-template cudaError_t launch_uniform_fwd<float>(const UniformArgs<float>&, cudaStream_t);
-template cudaError_t launch_reduce_epilogue<double>(const ReduceArgs<double>&, const UniformArgs<double>&, cudaStream_t);
-template cudaError_t launch_reduce_epilogue<float>(const ReduceArgs<float>&, const UniformArgs<float>&, cudaStream_t);
+template cudaError_t launch_uniform_fwd<double>(const UniformArgs<double>&, cudaStream_t, std::uint64_t&);
+template cudaError_t launch_uniform_fwd<float>(const UniformArgs<float>&, cudaStream_t, std::uint64_t&);
+template cudaError_t launch_reduce_epilogue<double>(const ReduceArgs<double>&, const UniformArgs<double>&, cudaStream_t,
+                                                    std::uint64_t&);
+template cudaError_t launch_reduce_epilogue<float>(const ReduceArgs<float>&, const UniformArgs<float>&, cudaStream_t,
+                                                   std::uint64_t&);
 
 }  // namespace tgk

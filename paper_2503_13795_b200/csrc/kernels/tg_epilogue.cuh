@@ -29,6 +29,7 @@ struct UniformArgs {
   std::uint32_t* err_op;
   std::size_t batch;
   std::uint32_t n_instr, n_params, n_const, const_base, n_uv, root_uv;
+  int copy;                  // set by the launchers: copies done inside the single-CTA kernels
 };
 
 template <class T>
@@ -38,8 +39,9 @@ struct ReduceArgs {
   std::uint32_t n_dest, n_rows;
 };
 
-template <class T> cudaError_t launch_uniform_fwd(const UniformArgs<T>& a, cudaStream_t st);
+template <class T> cudaError_t launch_uniform_fwd(const UniformArgs<T>& a, cudaStream_t st, std::uint64_t& launches);
 template <class T>
-cudaError_t launch_reduce_epilogue(const ReduceArgs<T>& r, const UniformArgs<T>& a, cudaStream_t st);
+cudaError_t launch_reduce_epilogue(const ReduceArgs<T>& r, const UniformArgs<T>& a, cudaStream_t st,
+                                   std::uint64_t& launches);
 
 }  // namespace tgk

@@ -78,6 +78,8 @@ struct GemmArgs {
 
 template <class T> cudaError_t launch_tape_range(const RangeArgs<T>& a, cudaStream_t st);
 template <class T> cudaError_t launch_gemm(const GemmArgs<T>& g, std::uint32_t splits, cudaStream_t st);
+// fp32 GEMM on the 5th-gen tensor cores (tcgen05.mma kind::tf32, 3xTF32 split), tg_umma.cu
+cudaError_t launch_gemm_umma(const GemmArgs<float>& g, std::uint32_t splits, cudaStream_t st);
 // dst[m * N + n] += sum_kz part[kz][m][n]   (fixed order)
 template <class T> cudaError_t launch_splitk_reduce(const T* part, T* dst, std::uint32_t MN, std::uint32_t splits, cudaStream_t st);
 // G[z rows] = act'(G[h rows], V[h rows], V[z rows]) for n_out consecutive rows

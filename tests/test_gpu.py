@@ -18,16 +18,19 @@ pytestmark = pytest.mark.gpu
 if not torch.cuda.is_available():
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
-TIERS = ["jit", "interp", "staged"]
+TIERS = ["jit", "interp", "staged", "staged_simt"]
 
 
 def make_prog(desc, tier):
     """jit: register-resident specialised kernel; interp: shared-memory tile
-    interpreter; staged: HBM-resident rows, dense layers as GEMMs."""
+    interpreter; staged: HBM-resident rows, dense layers as tcgen05 GEMMs
+    (fp32) / SIMT GEMMs (fp64); staged_simt: dense layers as SIMT GEMMs."""
     os.environ["TG_JIT"] = "1" if tier == "jit" else "0"
-    os.environ["TG_STAGED"] = "1" if tier == "staged" else "0"
+    os.environ["TG_STAGED"] = "1" if tier.startswith("staged") else "0"
+    os.environ["TG_UMMA"] = "0" if tier == "staged_simt" else "1"
     p = tg.Program(desc)
     os.environ.pop("TG_STAGED")
+    os.environ.pop("TG_UMMA")
     return p
 
 
@@ -294,6 +297,38 @@ def test_fp64_tanh_accuracy(tier):
     np.testing.assert_array_equal(np.signbit(L[x == 0]), np.signbit(x[x == 0]))
     # derivative 1 - y^2 (ops.hpp:327-329)
     assert np.max(np.abs(IG[0] - (1 - L * L))) <= 1e-15
+
+
+@pytest.mark.parametrize("engine,dt", [(1, "f32"), (0, "f32"), (0, "f64")])
+@pytest.mark.parametrize("a_kmaj,b_nmaj", [(True, True), (False, True), (True, False)])
+@pytest.mark.parametrize("M,N,K", [(128, 128, 32), (300, 1000, 784), (10, 4096, 1024), (1024, 784, 2000)])
+def test_dense_gemm_engines(engine, dt, a_kmaj, b_nmaj, M, N, K):
+    """The staged path's dense-layer product (tg_gemm) against an fp64 matmul:
+    tcgen05 3xTF32 (engine 1) and SIMT (engine 0), all operand layouts used by
+    forward (W X), input adjoints (W^T dZ) and weight gradients (dZ X^T)."""
+    import ctypes as C
+    from paper_2503_13795_b200 import _lib
+    tdt = torch.float32 if dt == "f32" else torch.float64
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
+    A = torch.randn((M, K) if a_kmaj else (K, M), device="cuda", dtype=tdt, generator=g)
+    B = torch.randn((K, N) if b_nmaj else (N, K), device="cuda", dtype=tdt, generator=g)
+    Cm = torch.randn((M, N), device="cuda", dtype=tdt, generator=g)
+    C0 = Cm.clone()
+    lda = A.shape[1]
+    ldb = B.shape[1]
+    st = _lib.lib.tg_gemm(0 if dt == "f64" else 1, engine, M, N, K, C.c_void_p(A.data_ptr()), lda, int(a_kmaj),
+                          C.c_void_p(B.data_ptr()), ldb, int(b_nmaj), C.c_void_p(Cm.data_ptr()), N, 1,
+                          C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert st == 0, _lib.lib.tg_last_error()
+    torch.cuda.synchronize()
+    Ad = (A if a_kmaj else A.t()).double()
+    Bd = (B if b_nmaj else B.t()).double()
+    want = C0.double() + Ad @ Bd
+    err = ((Cm.double() - want).norm() / want.norm()).item()
+    # SIMT fp32 ~1e-7; tcgen05 3xTF32 carries the tensor core's fp32 accumulation
+    # error (grows with K: ~6e-6 at K ~ 1e3, measured)
+    tol = {"f32": 2e-6 if engine == 0 else 2e-5, "f64": 1e-14}[dt]
+    assert err <= tol, err
 
 
 def test_jit_is_used_for_short_tapes():
