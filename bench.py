@@ -212,11 +212,16 @@ def main():
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
 
-    def step(Xs=X, Ks=K):
-        prog.forward_backward(Xs, Ks, b, P, L, None, G, W, stream)
-        if world > 1:
-            dist.all_reduce(G)
-        prog.gd_update(P, G, cfg["gamma"], b * world, stream)
+    from paper_2503_13795_b200.dp import DataParallelStep
+    dp = DataParallelStep(prog)
+
+    def step(Xs=X, Ks=K, st=None):
+        st = st or stream
+        if world == 1:   # fused: GD applied in the reduction epilogue
+            prog.train_step(Xs, Ks, b, P, L, G, cfg["gamma"], W, st)
+        else:            # local sum -> NCCL all-reduce of the d-vector -> GD with the global batch
+            prog.forward_backward(Xs, Ks, b, P, L, None, G, W, st)
+            dp.step(P, G, cfg["gamma"], b * world, stream=st)
 
     l0 = prog.launches
     step()
@@ -230,12 +235,11 @@ def main():
         s2.wait_stream(stream)
         with torch.cuda.stream(s2):
             for _ in range(2):
-                step()
+                step(st=s2)
         stream.wait_stream(s2)
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, stream=s2):
-            prog.forward_backward(X, K, b, P, L, None, G, W, s2)
-            prog.gd_update(P, G, cfg["gamma"], b, s2)
+            step(st=s2)
         torch.cuda.synchronize()
 
     def run_step():
@@ -337,9 +341,13 @@ def main():
                 "algorithmic_flops_per_launch": alg,
                 "peak_source": "profiles/fp_peaks.json (FMA-throughput microbenchmark on this B200)",
                 "hbm_achieved_gbs": b * cfg["bytes"] / (tape_ms * 1e-3) / 1e9}
-    roof["kernel"] = "tgk::k_tape"
+    tier = ["smem-interpreter", "hbm-interpreter", "jit-register", "staged"][info["storage"]]
+    roof["kernel"] = {"smem-interpreter": "tgk::k_tape<T,true>", "hbm-interpreter": "tgk::k_tape<T,false>",
+                      "jit-register": "tg_jit_tape (NVRTC sm_100a)",
+                      "staged": "staged chain: k_gemm / k_umma_tf32x3 / k_tape_range"}[tier]
     roof["kernel_ms"] = tape_ms
     roof["kernel_share_of_step"] = tape_ms / ms
+    roof["traffic"] = measured_traffic(args.config, b)
 
     line = {
         "metric": "per-sample gradient evals/sec (∇f_i/s)", "value": value, "unit": "grad/s",
@@ -349,7 +357,7 @@ def main():
         "config": {"workload": f"{args.config}: {cfg['desc']}", "batch_per_gpu": b, "global_batch": b * world,
                    "parallelism": f"dp{world}", "l2": "flushed between timed steps (256 MiB write)",
                    "cuda_graph": graph is not None, "tile_samples": info["tile_samples"],
-                   "storage": "smem" if info["storage"] == 0 else "hbm"},
+                   "kernel_tier": tier},
         "node_evals_per_s": value * (info["n_sample_nodes"] + info["n_uniform_nodes"] / max(b, 1)),
         "roofline": roof,
         "gpu_launches": launches_per_step * args.steps,
@@ -368,6 +376,20 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def measured_traffic(config: str, batch: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
+    kernel from the committed ncu --set full capture (profiles/traffic.json),
+    scaled to this batch; None when not captured for this config."""
+    path = os.path.join(HERE, "profiles", "traffic.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f).get(config)
+    if not d:
+        return None
+    return d["dram_bytes_per_launch"] * batch / d["batch"]
 
 
 def measured_simt_peak(dtype: str):
