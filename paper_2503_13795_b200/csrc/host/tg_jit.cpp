@@ -58,6 +58,17 @@ struct Gen {
   std::vector<int> vslot, gslot;     // row -> shared-memory slot of its value / adjoint (or -1)
   std::vector<char> vsm, gsm;        // value / adjoint lives in shared memory (written in place)
   unsigned ld = 0;                   // shared-memory row stride (tile + 1)
+  std::vector<char> vstored, gstored;  // register-homed contraction rows already stored
+
+  // Rows read by the batch-reduction terms are stored to shared memory as soon
+  // as they are final, so their registers die early (register pressure sets
+  // the occupancy of this kernel).
+  void vstore(std::uint32_t r) {
+    if (vslot[r] >= 0 && !vsm[r] && !vstored[r]) { o << "      " << sv(r) << " = " << v(r) << ";\n"; vstored[r] = 1; }
+  }
+  void gstore(std::uint32_t r) {
+    if (gslot[r] >= 0 && !gsm[r] && !gstored[r]) { o << "      " << sg_(r) << " = " << g(r) << ";\n"; gstored[r] = 1; }
+  }
 
   Gen(const tgc::Program& p, const JitConfig& c) : P(p), cfg(c), f64(p.dtype == TG_F64) {}
 
@@ -66,7 +77,11 @@ struct Gen {
   std::string g(std::uint32_t r) const { return "g" + std::to_string(r); }
   std::string sv(std::uint32_t r) const { return "sV[" + std::to_string(std::size_t(vslot[r]) * ld) + "u + col]"; }
   std::string sg_(std::uint32_t r) const { return "sG[" + std::to_string(std::size_t(gslot[r]) * ld) + "u + col]"; }
-  std::string V(std::uint32_t r) const { return vsm[r] ? sv(r) : v(r); }   // value of row r
+  // value of row r: once a register-homed row has been stored for the
+  // contraction, later reads (the reverse sweep) reload it from shared memory
+  // so the register dies at the store (TG_JIT_RELOAD=0 keeps registers)
+  std::string V(std::uint32_t r) const { return vsm[r] || (reload && !vstored.empty() && vstored[r]) ? sv(r) : v(r); }
+  bool reload = true;
   std::string Gx(std::uint32_t r) const { return gsm[r] ? sg_(r) : g(r); } // adjoint of row r
   std::string uv(std::uint32_t i) const {
     return cfg.const_uv ? "cUV[" + std::to_string(i) + "]" : "UVg[" + std::to_string(i) + "]";
@@ -494,7 +509,21 @@ std::string generate(const tgc::Program& P, const JitConfig& cfg, unsigned& n_cr
     << "    const unsigned col = jj * " << cfg.block << "u + tid;\n"
     << "    (void)col;\n"
     << "    if (s < batch) {\n";
-  for (const Instr& in : P.fwd) G.forward(in);
+  G.vstored.assign(P.n_rows, 0);
+  if (const char* e = std::getenv("TG_JIT_RELOAD")) G.reload = std::atoi(e) != 0;
+  G.gstored.assign(P.n_rows, 0);
+  for (const Instr& in : P.fwd) {
+    G.forward(in);
+    if (in.kind == tgc::kDense) {
+      const tgc::Dense& D = P.dense[in.aux];
+      for (std::uint32_t j = 0; j < D.n_out; ++j) {
+        G.vstore(D.out_row + j);
+        if (D.act_op) G.vstore(D.act_row + j);
+      }
+    } else {
+      G.vstore(in.out);
+    }
+  }
   o << "      if (loss) loss[s] = " << G.V(P.root_row) << ";\n";
   for (std::uint32_t r : P.zero_rows) {
     if (G.gsm[r]) o << "      " << G.sg_(r) << " = (T)0;\n";
@@ -506,7 +535,12 @@ std::string generate(const tgc::Program& P, const JitConfig& cfg, unsigned& n_cr
   const char* skip = std::getenv("TG_JIT_SKIP");
   const bool skip_bwd = skip && std::string(skip) == "bwd", skip_con = skip && std::string(skip) == "contract";
   if (!skip_bwd)
-    for (const Instr& in : P.bwd) G.reverse(in);
+    for (const Instr& in : P.bwd) {
+      if (in.kind == tgc::kNode) G.gstore(in.out);   // adjoint final when its node is processed
+      G.reverse(in);
+      if (in.kind == tgc::kDense)
+        for (std::uint32_t j = 0; j < P.dense[in.aux].n_out; ++j) G.gstore(P.dense[in.aux].out_row + j);
+    }
   else
     for (std::uint32_t r = 0; r < P.n_rows; ++r)
       if (!G.gsm[r] && r != P.root_row && std::find(P.zero_rows.begin(), P.zero_rows.end(), r) == P.zero_rows.end())
@@ -516,8 +550,8 @@ std::string generate(const tgc::Program& P, const JitConfig& cfg, unsigned& n_cr
     if (r != kNone) o << "      if (igrad) igrad[" << c << "ull * batch + s] = " << G.Gx(r) << ";\n";
   }
   for (std::uint32_t r = 0; r < P.n_rows; ++r) {
-    if (G.gslot[r] >= 0 && !G.gsm[r]) o << "      " << G.sg_(r) << " = " << G.g(r) << ";\n";
-    if (G.vslot[r] >= 0 && !G.vsm[r]) o << "      " << G.sv(r) << " = " << G.v(r) << ";\n";
+    G.gstore(r);
+    G.vstore(r);
   }
   o << "    }\n    }\n";
   if (nd && !skip_con) {
