@@ -296,7 +296,12 @@ def main():
     h2d = (xh.numel() * xh.element_size() if xh is not None else 0) + (kh.numel() * 4 if kh is not None else 0)
     d2h = b * L.element_size()
 
+    pipe = prog.pipeline(b, P, stream) if world == 1 else None
+
     def e2e_step():
+        if pipe is not None:   # public host-buffer API: H2D / compute / D2H overlapped across steps
+            pipe.step(xh, kh, lh, cfg["gamma"])
+            return
         if Xd is not None:
             Xd.copy_(xh, non_blocking=True)
         if Kd is not None:
@@ -304,19 +309,43 @@ def main():
         step(Xd, Kd)
         lh.copy_(L, non_blocking=True)
 
-    for _ in range(3):
+    for _ in range(max(args.warmup, 10)):
         e2e_step()
+    if pipe is not None:
+        pipe.sync()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    n_e2e = max(min(args.steps, 100), 5)
+    n_e2e = max(args.steps, 100)
     e0.record(stream)
     for _ in range(n_e2e):
         e2e_step()
+    if pipe is not None:
+        pipe.join(stream)      # e1 after the last step's loss has reached host memory
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / n_e2e
+    # the same step's host<->device copies alone (no compute): the link bound of e2e
+    cs_in, cs_out = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record(stream)
+    cs_in.wait_stream(stream)
+    cs_out.wait_stream(stream)
+    for _ in range(n_e2e):
+        with torch.cuda.stream(cs_in):
+            if Xd is not None:
+                Xd.copy_(xh, non_blocking=True)
+            if Kd is not None:
+                Kd.copy_(kh, non_blocking=True)
+        with torch.cuda.stream(cs_out):
+            lh.copy_(L, non_blocking=True)
+    stream.wait_stream(cs_in)
+    stream.wait_stream(cs_out)
+    c1.record(stream)
+    torch.cuda.synchronize()
+    copy_ms = c0.elapsed_time(c1) / n_e2e
     if world > 1:
         t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -362,7 +391,11 @@ def main():
         "roofline": roof,
         "gpu_launches": launches_per_step * args.steps,
         "e2e": {"value": b * world / (e2e_ms * 1e-3), "unit": "grad/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                "copies_only_ms_per_step": copy_ms,
+                "h2d_link_gbs": h2d / (copy_ms * 1e-3) / 1e9 if h2d else None,
+                "api": ("tg_pipeline_step (pinned host inputs in, per-sample losses out, 4 steps in flight)"
+                        if pipe is not None else "copies + tg_forward_backward + NCCL all-reduce + tg_gd_update")},
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

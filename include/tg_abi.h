@@ -201,6 +201,36 @@ tg_status tg_train_step(tg_program_t p, const void* inputs, const int32_t* index
                         double gamma, void* workspace, size_t workspace_bytes,
                         tg_stream_t stream);
 
+/* ---- host-buffer training loop -----------------------------------------------
+ * The reference's calling convention: each step's samples arrive in host
+ * memory and its per-sample losses go back to host memory (train_step,
+ * SPEC.md:431-439, the loop of PAPER.md:1357-1359).  A pipeline owns the
+ * device staging for `depth` in-flight steps (4; env TG_PIPE_DEPTH).  Step i's host->device input copy
+ * runs on a copy stream while step i-1 computes.  Step i's losses return on
+ * a second copy stream while step i+1 computes.  Parameters stay resident on
+ * the device (`params`, updated in place by the fused GD).
+ * Host buffers passed to step i may be reused once step i+depth has been
+ * submitted or after tg_pipeline_sync; h_loss of step i is valid after
+ * tg_pipeline_sync.  Pinned host memory (tg_host_alloc) gives overlapped
+ * copies; pageable memory is accepted but the copies serialise. */
+typedef struct tg_pipeline* tg_pipeline_t;
+tg_status tg_pipeline_new(tg_program_t p, size_t batch, void* params, tg_stream_t stream, tg_pipeline_t* out);
+/* One training step over host buffers: inputs [n_inputs][batch],
+ * index_inputs [n_index_inputs][batch] (may be NULL if unused), h_loss
+ * [batch] (may be NULL).  Returns after enqueueing. */
+tg_status tg_pipeline_step(tg_pipeline_t pl, const void* h_inputs, const int32_t* h_index_inputs, void* h_loss,
+                           double gamma);
+/* Makes `stream` wait for every enqueued step (copies included), without
+ * blocking the host. */
+tg_status tg_pipeline_join(tg_pipeline_t pl, tg_stream_t stream);
+/* Blocks the host until every enqueued step has finished. */
+tg_status tg_pipeline_sync(tg_pipeline_t pl);
+/* Device pointer of the batch-summed gradient of the last completed step. */
+tg_status tg_pipeline_grad_sum(tg_pipeline_t pl, void** grad_sum);
+void tg_pipeline_free(tg_pipeline_t pl);
+tg_status tg_host_alloc(size_t bytes, void** out);
+void tg_host_free(void* ptr);
+
 /* Synchronises `stream` and reports the first per-sample domain violation
  * seen since the last check as TG_DOMAIN with the reference message. */
 tg_status tg_check_device_error(tg_program_t p, tg_stream_t stream, int64_t* sample_out,

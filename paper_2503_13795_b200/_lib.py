@@ -110,6 +110,14 @@ def _load():
         "tg_profile_enable": (st, [P, C.c_int]),
         "tg_profile_read": (st, [P, C.POINTER(C.c_double), C.POINTER(u64)]),
         "tg_program_free": (None, [P]),
+        "tg_pipeline_new": (st, [P, sz, P, P, C.POINTER(P)]),
+        "tg_pipeline_step": (st, [P, P, P, P, C.c_double]),
+        "tg_pipeline_join": (st, [P, P]),
+        "tg_pipeline_sync": (st, [P]),
+        "tg_pipeline_grad_sum": (st, [P, C.POINTER(P)]),
+        "tg_pipeline_free": (None, [P]),
+        "tg_host_alloc": (st, [sz, C.POINTER(P)]),
+        "tg_host_free": (None, [P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <chrono>
 #include <memory>
 #include <new>
 #include <stdexcept>
@@ -1185,3 +1186,225 @@ extern "C" tg_status tg_gemm(tg_dtype dtype, int engine, uint32_t M, uint32_t N,
     return TG_OK;
   });
 }
+
+// ===========================================================================
+// Host-buffer training loop.  Slot k of `depth` owns the device buffers of
+// one in-flight step.  Per step:
+//   copy-in stream : H2D(inputs -> slot)            -> record ready
+//   caller's stream: wait ready -> forward/backward/reduce/GD -> record computed
+//   copy-out stream: wait computed -> D2H(losses)   -> record done
+// All compute stays on one stream (back to back, no cross-stream hop between
+// steps); the copies of neighbouring steps overlap it.  The compute of a slot
+// is a CUDA graph captured once (TG_PIPE_GRAPH=0: direct launches).
+struct tg_pipeline {
+  tg_program* p = nullptr;
+  std::size_t batch = 0;
+  void* params = nullptr;
+  cudaStream_t cs = nullptr;                  // compute: the caller's stream
+  cudaStream_t in = nullptr, out = nullptr;   // copy streams
+  cudaStream_t cap = nullptr;                 // capture stream
+  int depth = 4;                              // steps in flight (TG_PIPE_DEPTH)
+  bool use_graph = true;
+  struct Slot {
+    void *X = nullptr, *K = nullptr, *L = nullptr;
+    cudaEvent_t ready = nullptr, computed = nullptr, done = nullptr;
+    bool used = false;
+    cudaGraphExec_t ge = nullptr;
+    double gamma = 0;
+    std::uint64_t launches = 0;
+  };
+  std::vector<Slot> slot;
+  void* G = nullptr;
+  void* ws = nullptr;
+  std::size_t ws_bytes = 0, x_bytes = 0, k_bytes = 0, l_bytes = 0;
+  std::uint64_t steps = 0;
+  bool trace = false;           // TG_PIPE_TRACE=1: host time per section, printed at free
+  double t_sync = 0, t_in = 0, t_compute = 0, t_out = 0, t_total = 0;
+  ~tg_pipeline() {
+    if (trace && steps)
+      std::fprintf(stderr, "[tg pipeline] %llu steps, host us/step: total %.2f sync %.2f copy-in %.2f compute %.2f "
+                           "copy-out %.2f\n", static_cast<unsigned long long>(steps), t_total / steps,
+                   t_sync / steps, t_in / steps, t_compute / steps, t_out / steps);
+    for (cudaStream_t s : {in, out, cap})
+      if (s) cudaStreamSynchronize(s);
+    cudaStreamSynchronize(cs);
+    for (Slot& s : slot) {
+      if (s.ge) cudaGraphExecDestroy(s.ge);
+      cudaFree(s.X);
+      cudaFree(s.K);
+      cudaFree(s.L);
+      if (s.ready) cudaEventDestroy(s.ready);
+      if (s.computed) cudaEventDestroy(s.computed);
+      if (s.done) cudaEventDestroy(s.done);
+    }
+    for (cudaStream_t s : {in, out, cap})
+      if (s) cudaStreamDestroy(s);
+    cudaFree(G);
+    cudaFree(ws);
+  }
+};
+
+namespace {
+
+tg_status pipe_compute(tg_pipeline& pl, tg_pipeline::Slot& sl, double gamma, cudaStream_t st) {
+  tg_program& pr = *pl.p;
+  const std::uint64_t l0 = pr.launches;
+  const tg_status s =
+      pr.P.dtype == TG_F64
+          ? run_fb<double>(pr, sl.X, static_cast<const std::int32_t*>(sl.K), pl.batch, pl.params, sl.L, nullptr,
+                           pl.G, pl.ws, pl.ws_bytes, st, pl.params, gamma)
+          : run_fb<float>(pr, sl.X, static_cast<const std::int32_t*>(sl.K), pl.batch, pl.params, sl.L, nullptr,
+                          pl.G, pl.ws, pl.ws_bytes, st, pl.params, gamma);
+  sl.launches = pr.launches - l0;
+  return s;
+}
+
+tg_status pipe_capture(tg_pipeline& pl, tg_pipeline::Slot& sl, double gamma) {
+  if (sl.ge) TG_CUDA_TRY(cudaGraphExecDestroy(sl.ge));
+  sl.ge = nullptr;
+  const std::uint64_t l0 = pl.p->launches;
+  TG_CUDA_TRY(cudaStreamBeginCapture(pl.cap, cudaStreamCaptureModeThreadLocal));
+  const tg_status st = pipe_compute(pl, sl, gamma, pl.cap);
+  cudaGraph_t g = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(pl.cap, &g);
+  pl.p->launches = l0;   // counted per replay instead
+  if (st != TG_OK) {
+    if (g) cudaGraphDestroy(g);
+    return st;
+  }
+  TG_CUDA_TRY(ce);
+  const cudaError_t ie = cudaGraphInstantiate(&sl.ge, g, 0);
+  cudaGraphDestroy(g);
+  TG_CUDA_TRY(ie);
+  sl.gamma = gamma;
+  return TG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+tg_status tg_pipeline_new(tg_program_t p, size_t batch, void* params, tg_stream_t stream, tg_pipeline_t* out) {
+  return guard([&] {
+    if (!p) return fail(TG_INVALID_HANDLE, "tg_pipeline_new: NULL program");
+    if (!out) return fail(TG_INVALID_ARGUMENT, "tg_pipeline_new: NULL out");
+    if (batch == 0) return fail(TG_INVALID_ARGUMENT, "tg_pipeline_new: batch empty");
+    if (p->P.n_params && !params) return fail(TG_INVALID_ARGUMENT, "tg_pipeline_new: params is NULL");
+    TG_TRY(upload(*p));   // synchronous set-up (and the JIT build) outside any capture
+    auto pl = std::make_unique<tg_pipeline>();
+    pl->p = p;
+    pl->batch = batch;
+    pl->params = params;
+    pl->cs = static_cast<cudaStream_t>(stream);
+    if (const char* e = std::getenv("TG_PIPE_DEPTH")) pl->depth = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("TG_PIPE_GRAPH")) pl->use_graph = e[0] != '0';
+    if (const char* e = std::getenv("TG_PIPE_TRACE")) pl->trace = e[0] == '1';
+    const std::size_t t = p->tsz();
+    pl->x_bytes = std::size_t(p->P.n_inputs) * batch * t;
+    pl->k_bytes = std::size_t(p->P.n_index_inputs) * batch * 4;
+    pl->l_bytes = batch * t;
+    TG_CUDA_TRY(cudaStreamCreateWithFlags(&pl->in, cudaStreamNonBlocking));
+    TG_CUDA_TRY(cudaStreamCreateWithFlags(&pl->out, cudaStreamNonBlocking));
+    TG_CUDA_TRY(cudaStreamCreateWithFlags(&pl->cap, cudaStreamNonBlocking));
+    pl->slot.resize(pl->depth);
+    for (tg_pipeline::Slot& sl : pl->slot) {
+      if (pl->x_bytes) TG_CUDA_TRY(cudaMalloc(&sl.X, pl->x_bytes));
+      if (pl->k_bytes) TG_CUDA_TRY(cudaMalloc(&sl.K, pl->k_bytes));
+      TG_CUDA_TRY(cudaMalloc(&sl.L, pl->l_bytes));
+      TG_CUDA_TRY(cudaEventCreateWithFlags(&sl.ready, cudaEventDisableTiming));
+      TG_CUDA_TRY(cudaEventCreateWithFlags(&sl.computed, cudaEventDisableTiming));
+      TG_CUDA_TRY(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
+    }
+    TG_CUDA_TRY(cudaMalloc(&pl->G, std::max<std::size_t>(1, p->P.n_params) * t));
+    pl->ws_bytes = layout(*p, batch).total;
+    TG_CUDA_TRY(cudaMalloc(&pl->ws, pl->ws_bytes));
+    *out = pl.release();
+    return TG_OK;
+  });
+}
+
+tg_status tg_pipeline_step(tg_pipeline_t pl, const void* h_inputs, const int32_t* h_idx, void* h_loss, double gamma) {
+  return guard([&] {
+    if (!pl) return fail(TG_INVALID_HANDLE, "tg_pipeline_step: NULL pipeline");
+    tg_program& pr = *pl->p;
+    if (pr.P.n_inputs && !h_inputs) return fail(TG_INVALID_ARGUMENT, "tg_pipeline_step: inputs is NULL");
+    if (pr.P.n_index_inputs && !h_idx) return fail(TG_INVALID_ARGUMENT, "tg_pipeline_step: index_inputs is NULL");
+    using clk = std::chrono::steady_clock;
+    const auto t0 = clk::now();
+    auto t = t0;
+    auto lap = [&](double& acc) {
+      if (!pl->trace) return;
+      const auto n = clk::now();
+      acc += std::chrono::duration<double, std::micro>(n - t).count();
+      t = n;
+    };
+    tg_pipeline::Slot& sl = pl->slot[pl->steps % pl->slot.size()];
+    // the slot was last used `depth` steps ago: that step must be complete
+    if (sl.used) TG_CUDA_TRY(cudaEventSynchronize(sl.done));
+    lap(pl->t_sync);
+    if (pl->x_bytes) TG_CUDA_TRY(cudaMemcpyAsync(sl.X, h_inputs, pl->x_bytes, cudaMemcpyHostToDevice, pl->in));
+    if (pl->k_bytes) TG_CUDA_TRY(cudaMemcpyAsync(sl.K, h_idx, pl->k_bytes, cudaMemcpyHostToDevice, pl->in));
+    TG_CUDA_TRY(cudaEventRecord(sl.ready, pl->in));
+    lap(pl->t_in);
+    TG_CUDA_TRY(cudaStreamWaitEvent(pl->cs, sl.ready, 0));
+    if (pl->use_graph && !pr.profiling) {
+      if (!sl.ge || sl.gamma != gamma) TG_TRY(pipe_capture(*pl, sl, gamma));
+      TG_CUDA_TRY(cudaGraphLaunch(sl.ge, pl->cs));
+      pr.launches += sl.launches;
+    } else {
+      TG_TRY(pipe_compute(*pl, sl, gamma, pl->cs));
+    }
+    TG_CUDA_TRY(cudaEventRecord(sl.computed, pl->cs));
+    lap(pl->t_compute);
+    TG_CUDA_TRY(cudaStreamWaitEvent(pl->out, sl.computed, 0));
+    if (h_loss) TG_CUDA_TRY(cudaMemcpyAsync(h_loss, sl.L, pl->l_bytes, cudaMemcpyDeviceToHost, pl->out));
+    TG_CUDA_TRY(cudaEventRecord(sl.done, pl->out));
+    lap(pl->t_out);
+    if (pl->trace) pl->t_total += std::chrono::duration<double, std::micro>(clk::now() - t0).count();
+    sl.used = true;
+    ++pl->steps;
+    return TG_OK;
+  });
+}
+
+tg_status tg_pipeline_join(tg_pipeline_t pl, tg_stream_t stream) {
+  return guard([&] {
+    if (!pl) return fail(TG_INVALID_HANDLE, "tg_pipeline_join: NULL pipeline");
+    for (const tg_pipeline::Slot& sl : pl->slot)
+      if (sl.used) TG_CUDA_TRY(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), sl.done, 0));
+    return TG_OK;
+  });
+}
+
+tg_status tg_pipeline_sync(tg_pipeline_t pl) {
+  return guard([&] {
+    if (!pl) return fail(TG_INVALID_HANDLE, "tg_pipeline_sync: NULL pipeline");
+    for (const tg_pipeline::Slot& sl : pl->slot)
+      if (sl.used) TG_CUDA_TRY(cudaEventSynchronize(sl.done));
+    return TG_OK;
+  });
+}
+
+tg_status tg_pipeline_grad_sum(tg_pipeline_t pl, void** grad_sum) {
+  return guard([&] {
+    if (!pl || !grad_sum) return fail(TG_INVALID_ARGUMENT, "tg_pipeline_grad_sum: NULL argument");
+    *grad_sum = pl->G;
+    return TG_OK;
+  });
+}
+
+void tg_pipeline_free(tg_pipeline_t pl) { delete pl; }
+
+tg_status tg_host_alloc(size_t bytes, void** out) {
+  return guard([&] {
+    if (!out) return fail(TG_INVALID_ARGUMENT, "tg_host_alloc: NULL out");
+    TG_CUDA_TRY(cudaHostAlloc(out, std::max<std::size_t>(1, bytes), cudaHostAllocDefault));
+    return TG_OK;
+  });
+}
+
+void tg_host_free(void* ptr) {
+  if (ptr) cudaFreeHost(ptr);
+}
+
+}  // extern "C"

@@ -386,6 +386,10 @@ class Program:
                                 self._ptr(params), self._ptr(loss), self._ptr(grad_sum), float(gamma),
                                 self._ptr(workspace), workspace.numel(), self._stream(stream)))
 
+    def pipeline(self, batch: int, params, stream=None) -> "Pipeline":
+        """Host-buffer training loop with overlapped copies (tg_pipeline_new)."""
+        return Pipeline(self, batch, params, stream)
+
     def jit(self):
         """(source, log, compile_ms) of the register-resident kernel, or None."""
         src, log, ms = C.c_char_p(), C.c_char_p(), C.c_double()
@@ -414,3 +418,56 @@ class Program:
             err = _lib.DomainError(st, msg) if st == 5 else _lib.TgError(st, msg)
             err.sample, err.node = s.value, n.value
             raise err
+
+
+class Pipeline:
+    """The reference's training loop over host buffers (tg_pipeline_*).
+
+    Each step() takes that step's samples from host memory (numpy arrays or
+    pinned torch tensors: inputs [n_inputs, batch], index_inputs
+    [n_index_inputs, batch]) and writes its per-sample losses to a host array.
+    Parameters stay on the device and are updated in place.  Up to four steps
+    are in flight: a host buffer passed to step i may be reused after step i+4
+    is submitted or after sync()."""
+
+    def __init__(self, prog: Program, batch: int, params, stream=None):
+        self.prog = prog
+        self.batch = int(batch)
+        self._params = params   # keep the device tensor alive
+        h = C.c_void_p()
+        check(lib.tg_pipeline_new(prog._h, self.batch, Program._ptr(params), Program._stream(stream), C.byref(h)))
+        self._h = h
+
+    @staticmethod
+    def _host(a):
+        if a is None:
+            return None
+        if isinstance(a, np.ndarray):
+            if not a.flags["C_CONTIGUOUS"]:
+                raise ValueError("host buffers must be C-contiguous")
+            return C.c_void_p(a.ctypes.data)
+        if a.is_cuda:
+            raise ValueError("Pipeline.step takes host buffers")
+        return C.c_void_p(a.data_ptr())
+
+    def step(self, inputs, index_inputs, loss, gamma: float) -> None:
+        check(lib.tg_pipeline_step(self._h, self._host(inputs), self._host(index_inputs), self._host(loss),
+                                   float(gamma)))
+
+    def join(self, stream=None) -> None:
+        """Makes `stream` wait for every enqueued step (no host block)."""
+        check(lib.tg_pipeline_join(self._h, Program._stream(stream)))
+
+    def sync(self) -> None:
+        check(lib.tg_pipeline_sync(self._h))
+
+    def grad_sum_ptr(self) -> int:
+        p = C.c_void_p()
+        check(lib.tg_pipeline_grad_sum(self._h, C.byref(p)))
+        return p.value
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and lib is not None:
+            lib.tg_pipeline_free(h)
+            self._h = None

@@ -337,3 +337,50 @@ def test_jit_is_used_for_short_tapes():
         src = prog.jit()
         assert src is not None and "tg_jit_tape" in src[0]
         assert prog.info["storage"] == 2
+
+
+@pytest.mark.parametrize("model,pinned,b", [("moons", True, 2000), ("moons", False, 2000), ("char_mlp", True, 2000),
+                                            ("moons", True, 262144), ("char_mlp", True, 65536)])
+def test_pipeline_host_buffers_equal_device_steps(model, pinned, b):
+    """tg_pipeline_step (host buffers, overlapped copies, 4 steps in flight;
+    pinned buffers take the per-slot CUDA-graph path, pageable ones the plain
+    stream path) produces exactly the parameters and per-step losses of
+    device-buffer train_step calls over the same batches.  The large batches
+    make each step long, so a missing cross-step dependency would let two
+    steps update the parameters concurrently and break the equality."""
+    desc = tg.build_model(model).describe()
+    steps, gamma = 7, 0.05
+    dt = tdtype(desc.dtype)
+    batches = [tg.synth_batch(model, batch=b, seed=50 + i, n_inputs=desc.n_inputs, n_index=desc.n_index_inputs)
+               for i in range(steps)]
+    prog = make_prog(desc, "jit")
+    # reference: device buffers, one train_step per batch
+    P1 = torch.tensor(desc.param_values(), device="cuda", dtype=dt)
+    G = torch.zeros(max(desc.n_params, 1), device="cuda", dtype=dt)
+    W = prog.alloc_workspace(b)
+    want = []
+    for x, k in batches:
+        L = torch.zeros(b, device="cuda", dtype=dt)
+        X = torch.tensor(x, device="cuda", dtype=dt) if desc.n_inputs else None
+        K = torch.tensor(k, device="cuda", dtype=torch.int32) if desc.n_index_inputs else None
+        prog.train_step(X, K, b, P1, L, G, gamma, W)
+        want.append(L.cpu())
+    # pipeline: host buffers
+    P2 = torch.tensor(desc.param_values(), device="cuda", dtype=dt)
+    pl = prog.pipeline(b, P2)
+    host = []
+    for x, k in batches:
+        xh = torch.tensor(x, dtype=dt) if desc.n_inputs else None
+        kh = torch.tensor(k, dtype=torch.int32) if desc.n_index_inputs else None
+        lh = torch.zeros(b, dtype=dt)
+        if pinned:
+            xh = xh.pin_memory() if xh is not None else None
+            kh = kh.pin_memory() if kh is not None else None
+            lh = lh.pin_memory()
+        host.append((xh, kh, lh))
+        pl.step(xh, kh, lh, gamma)
+    pl.sync()
+    torch.cuda.synchronize()
+    assert torch.equal(P1, P2)
+    for (xh, kh, lh), w in zip(host, want):
+        assert torch.equal(lh, w)
