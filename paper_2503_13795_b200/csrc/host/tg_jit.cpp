@@ -80,7 +80,15 @@ struct Gen {
   // value of row r: once a register-homed row has been stored for the
   // contraction, later reads (the reverse sweep) reload it from shared memory
   // so the register dies at the store (TG_JIT_RELOAD=0 keeps registers)
-  std::string V(std::uint32_t r) const { return vsm[r] || (reload && !vstored.empty() && vstored[r]) ? sv(r) : v(r); }
+  std::string V(std::uint32_t r) const {
+    if (!vov.empty() && !vov[r].empty()) return vov[r];
+    return vsm[r] || (reload && !vstored.empty() && vstored[r]) ? sv(r) : v(r);
+  }
+  // grouped mode (generate_grouped): a dense-layer output row lives in lane j
+  // of the sample's lane group; its value is read from the group's exchange
+  // buffer (vov) and contributions to its adjoint go to the owner lane (gov).
+  std::vector<std::string> vov, gov, gcond;
+  std::vector<int> gj;
   bool reload = true;
   std::string Gx(std::uint32_t r) const { return gsm[r] ? sg_(r) : g(r); } // adjoint of row r
   std::string uv(std::uint32_t i) const {
@@ -108,7 +116,10 @@ struct Gen {
     const std::uint32_t op = P.opnd[in.opnd + k];
     const std::uint32_t m = op >> kModeShift, i = op & kIndexMask;
     const std::uint8_t fl = P.oflag[in.opnd + k];
-    if (m == tgc::kSlot) {
+    if (m == tgc::kSlot && !gov.empty() && !gov[i].empty()) {
+      const std::string cond = gcond.empty() ? "q == " + std::to_string(gj[i]) + "u" : gcond[i];
+      o << "      if (" << cond << ") " << gov[i] << " += " << expr << ";\n";
+    } else if (m == tgc::kSlot) {
       if (gsm[i]) o << "      " << sg_(i) << (fl & tgc::kAssign ? " = " : " += ") << expr << ";\n";
       else if (fl & tgc::kAssign) o << "      T " << g(i) << " = " << expr << ";\n";
       else o << "      " << g(i) << " += " << expr << ";\n";
@@ -646,6 +657,742 @@ std::string generate(const tgc::Program& P, const JitConfig& cfg, unsigned& n_cr
   return o.str();
 }
 
+// ---------------------------------------------------------------------------
+// Grouped specialisation: G lanes (8 / 16 / 32) per sample.  Lane q of the
+// group owns neuron q of every dense layer (forward value, activation,
+// adjoint), so one sample's layers run G-wide instead of serially in one
+// thread; per-lane state is a handful of registers, which raises the number
+// of resident warps.  Layer vectors are exchanged through a per-sample
+// shared-memory buffer (broadcast reads); weights sit in shared memory in
+// both orientations so every lane access is conflict-free.  Weight and bias
+// gradients accumulate in the owner lanes' registers across all samples the
+// warp processes (no per-tile contraction), then a fixed-order block
+// reduction writes the per-CTA partials.  Everything that is not a dense
+// layer (inputs, loss glue) is emitted exactly as in generate(), replicated
+// across the group's lanes.
+// Dense-chain analysis shared by the grouped and the DMMA forms: every
+// dense layer reads either per-sample scalar rows or exactly the outputs of
+// one earlier layer; the loss glue reads layer outputs but never a
+// pre-activation of a fused layer; every batch term is a layer's weight
+// block, a layer's bias (sum of its z adjoint) or a product of scalar rows.
+struct DenseGroup {
+  const tgc::Dense* D = nullptr;
+  bool xvec = false;               // x = outputs of dense[src]
+  int src = -1;
+  std::vector<std::uint32_t> xr;   // x rows
+  std::uint32_t crow = 0;          // consumed output rows (act rows if fused, else z rows)
+  std::uint32_t dw0 = kNone;       // weight-gradient dest block
+  std::vector<std::uint32_t> bdest;  // bias dest per output (or kNone)
+  std::vector<double> bcoef;
+  unsigned wf = 0, wb = 0, bb = 0, xo = 0, xg = 0;   // generator scratch (shared-memory offsets)
+  bool has_bias() const {
+    for (auto d : bdest) if (d != kNone) return true;
+    return false;
+  }
+  bool unit_bias() const {
+    for (auto c : bcoef) if (c != 1.0) return false;
+    return true;
+  }
+};
+struct DensePlan {
+  std::vector<DenseGroup> gr;
+  std::vector<int> rg, rj, zg, zj;  // row -> (group, output) for consumed rows / z rows
+  std::vector<char> internal;       // pre-activation of a fused layer
+  std::vector<unsigned> sdests;     // dests over scalar rows only
+};
+
+bool plan_dense(const tgc::Program& P, DensePlan& pl, std::string& why) {
+  auto no = [&](const std::string& w) { why = w; return false; };
+  if (P.root_row == kNone) return no("root is sample-invariant");
+  if (P.dense.empty()) return no("no dense layers");
+  if (!P.sgather.empty()) return no("slot gathers");
+  const unsigned nd = static_cast<unsigned>(P.dest_uv.size());
+  const std::size_t ng = P.dense.size();
+  auto& gr = pl.gr;
+  auto& rg = pl.rg;
+  auto& rj = pl.rj;
+  auto& zg = pl.zg;
+  auto& zj = pl.zj;
+  auto& internal = pl.internal;
+  gr.assign(ng, {});
+  rg.assign(P.n_rows, -1);
+  rj.assign(P.n_rows, -1);
+  zg.assign(P.n_rows, -1);
+  zj.assign(P.n_rows, -1);
+  internal.assign(P.n_rows, 0);
+  for (std::size_t i = 0; i < ng; ++i) {
+    const tgc::Dense& D = P.dense[i];
+    gr[i].D = &D;
+    gr[i].crow = D.act_op ? D.act_row : D.out_row;
+    gr[i].bdest.assign(D.n_out, kNone);
+    gr[i].bcoef.assign(D.n_out, 1.0);
+    for (std::uint32_t j = 0; j < D.n_out; ++j) {
+      rg[gr[i].crow + j] = static_cast<int>(i);
+      rj[gr[i].crow + j] = static_cast<int>(j);
+      zg[D.out_row + j] = static_cast<int>(i);
+      zj[D.out_row + j] = static_cast<int>(j);
+      if (D.act_op) internal[D.out_row + j] = 1;
+    }
+  }
+  for (std::size_t i = 0; i < ng; ++i) {
+    const tgc::Dense& D = *gr[i].D;
+    bool any = false;
+    for (std::uint32_t k = 0; k < D.n_in; ++k) {
+      const std::uint32_t op = P.opnd[D.x_opnd + k];
+      if ((op >> kModeShift) != tgc::kSlot) return no("dense x operand is not a per-sample row");
+      const std::uint32_t r = op & kIndexMask;
+      if (internal[r]) return no("pre-activation read by another layer");
+      gr[i].xr.push_back(r);
+      any = any || rg[r] >= 0;
+    }
+    if (any) {
+      const int src = rg[gr[i].xr[0]];
+      if (P.dense[src].n_out != D.n_in) return no("dense x is part of a layer");
+      for (std::uint32_t k = 0; k < D.n_in; ++k)
+        if (rg[gr[i].xr[k]] != src || rj[gr[i].xr[k]] != static_cast<int>(k)) return no("dense x mixes rows");
+      gr[i].xvec = true;
+      gr[i].src = src;
+    } else if (D.n_in > 32) {
+      return no("too many scalar inputs to one dense layer");
+    }
+  }
+  for (const Instr& in : P.fwd) {
+    if (in.kind != tgc::kNode) continue;
+    for (std::uint32_t j = 0; j < in.nops; ++j) {
+      const std::uint32_t op = P.opnd[in.opnd + j];
+      if ((op >> kModeShift) == tgc::kSlot && internal[op & kIndexMask]) return no("pre-activation read outside its layer");
+    }
+  }
+  if (rg[P.root_row] >= 0 || internal[P.root_row]) return no("root is a dense-layer row");
+  for (std::size_t b = 0; b < P.dgrad.size(); ++b) {
+    const tgc::DenseGrad& dg = P.dgrad[b];
+    const std::uint32_t a0 = P.dg_rows[dg.arow_off];
+    bool found = false;
+    for (std::size_t i = 0; i < ng && !found; ++i)
+      if (gr[i].D->out_row == a0 && gr[i].D->n_out == dg.n_out && gr[i].D->n_in == dg.n_in) {
+        gr[i].dw0 = dg.dest0;
+        found = true;
+      }
+    if (!found) return no("weight-gradient block without its layer");
+  }
+  std::vector<char> covered(nd, 0);
+  for (const auto& g : gr)
+    if (g.dw0 != kNone)
+      for (std::uint32_t q = 0; q < g.D->n_out * g.D->n_in; ++q) covered[g.dw0 + q] = 1;
+  pl.sdests.clear();
+  auto scalar_row = [&](std::uint32_t r) { return rg[r] < 0 && zg[r] < 0; };
+  for (unsigned d = 0; d < nd; ++d) {
+    if (covered[d]) continue;
+    if (P.dest_dense[d]) return no("dense gradient dest outside its block");
+    const std::uint32_t t0 = P.term_off[d], t1 = P.term_off[d + 1];
+    const tgc::Term& t = P.terms[t0];
+    if (t1 - t0 == 1 && t.kind == 0 && t.f == kNone && zg[t.a] >= 0) {
+      DenseGroup& g = gr[zg[t.a]];
+      if (g.bdest[zj[t.a]] != kNone) return no("two bias dests on one neuron");
+      g.bdest[zj[t.a]] = d;
+      g.bcoef[zj[t.a]] = t.coef;
+      continue;
+    }
+    for (std::uint32_t u = t0; u < t1; ++u) {
+      const tgc::Term& tu = P.terms[u];
+      if (tu.kind != 0 || !scalar_row(tu.a) || (tu.f != kNone && !scalar_row(tu.f)))
+        return no("batch term over a dense-layer row");
+    }
+    pl.sdests.push_back(d);
+  }
+  if (pl.sdests.size() > 32) return no("too many scalar gradient destinations");
+  return true;
+}
+
+std::string generate_grouped(const tgc::Program& P, const JitConfig& cfg, unsigned& G_out, unsigned& spb,
+                             std::size_t& smem_bytes, std::string& why) {
+  const bool f64 = P.dtype == TG_F64;
+  const std::size_t ts = f64 ? 8 : 4;
+  auto no = [&](const std::string& w) { why = w; return std::string(); };
+  DensePlan plan;
+  if (!plan_dense(P, plan, why)) return std::string();
+  const unsigned nd = static_cast<unsigned>(P.dest_uv.size());
+  unsigned maxw = 1;
+  for (const auto& D : P.dense) maxw = std::max(maxw, D.n_out);
+  if (maxw > 32) return no("dense layer wider than a warp");
+  const unsigned G = maxw <= 8 ? 8 : maxw <= 16 ? 16 : 32;
+  const unsigned SPW = 32 / G, WPB = cfg.block / 32;
+  using Grp = DenseGroup;
+  const std::size_t ng = P.dense.size();
+  auto& gr = plan.gr;
+  auto& rg = plan.rg;
+  auto& zg = plan.zg;
+  auto& sdests = plan.sdests;
+
+  // shared memory (elements): weights, per-sample exchange buffers, block reduction
+  unsigned off = 0, xs = 0;
+  for (auto& g : gr) {
+    g.wf = off;
+    off += g.D->n_in * G;
+    if (g.xvec) { g.wb = off; off += g.D->n_out * G; }
+    g.bb = off;
+    off += G;
+    g.xo = xs;
+    xs += G;
+    if (g.xvec) { g.xg = xs; xs += G; }
+  }
+  const std::size_t elems = std::size_t(off) + std::size_t(WPB) * SPW * xs + std::size_t(WPB) * nd;
+  if (elems * ts > 160 * 1024) return no("shared memory");
+  smem_bytes = elems * ts;
+  G_out = G;
+  spb = WPB * SPW;
+
+  Gen Gn(P, cfg);
+  Gn.vslot.assign(P.n_rows, -1);
+  Gn.gslot.assign(P.n_rows, -1);
+  Gn.vsm.assign(P.n_rows, 0);
+  Gn.gsm.assign(P.n_rows, 0);
+  Gn.vov.assign(P.n_rows, "");
+  Gn.gov.assign(P.n_rows, "");
+  Gn.gj.assign(P.n_rows, -1);
+  for (std::size_t i = 0; i < ng; ++i)
+    for (std::uint32_t j = 0; j < gr[i].D->n_out; ++j) {
+      const std::uint32_t r = gr[i].crow + j;
+      Gn.vov[r] = "sX[" + std::to_string(gr[i].xo + j) + "u]";
+      Gn.gov[r] = "gh" + std::to_string(i);
+      Gn.gj[r] = static_cast<int>(j);
+    }
+  std::ostringstream& o = Gn.o;
+  const std::string Gs = std::to_string(G) + "u";
+  o << "typedef " << (f64 ? "double" : "float") << " T;\n" << kMath << kPrelude;
+  if (cfg.const_uv) o << "__constant__ T cUV[" << std::max<std::uint32_t>(1, P.n_uv) << "];\n";
+  o << "extern \"C\" __global__ void __launch_bounds__(" << cfg.block;
+  if (cfg.min_blocks) o << ", " << cfg.min_blocks;
+  o << ") tg_jit_tape(\n"
+    << "    const T* __restrict__ in, const int* __restrict__ idx, unsigned long long batch,\n"
+    << "    T* __restrict__ loss, T* __restrict__ igrad, T* __restrict__ partial, unsigned grid_rows,\n"
+    << "    unsigned long long* err_key, const T* __restrict__ UVg, const unsigned* __restrict__ cand,\n"
+    << "    const unsigned* __restrict__ toff, const TermC* __restrict__ terms) {\n"
+    << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
+    << "  T* sm = reinterpret_cast<T*>(smem_raw);\n"
+    << "  T* sRed = sm + " << off + WPB * SPW * xs << "u;\n"
+    << "  const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;\n"
+    << "  const unsigned q = lane & " << G - 1 << "u, slot = lane / " << Gs << ";\n"
+    << "  T* sX = sm + " << off << "u + (warp * " << SPW << "u + slot) * " << xs << "u;\n"
+    << "  (void)toff; (void)terms; (void)cand; (void)idx; (void)in; (void)err_key;\n";
+  // weights: forward / scalar-x layout [k][j] (lane j), vector-x backward layout [j][k] (lane k)
+  for (const auto& g : gr) {
+    const tgc::Dense& D = *g.D;
+    o << "  for (unsigned e = tid; e < " << D.n_in * G << "u; e += " << cfg.block << "u) { const unsigned k = e / " << Gs
+      << ", j = e % " << Gs << "; sm[" << g.wf << "u + e] = j < " << D.n_out << "u ? UVg[" << D.w_uv << "u + j * "
+      << D.n_in << "u + k] : (T)0; }\n";
+    if (g.xvec)
+      o << "  for (unsigned e = tid; e < " << D.n_out * G << "u; e += " << cfg.block << "u) { const unsigned j = e / "
+        << Gs << ", k = e % " << Gs << "; sm[" << g.wb << "u + e] = k < " << D.n_in << "u ? UVg[" << D.w_uv
+        << "u + j * " << D.n_in << "u + k] : (T)0; }\n";
+    o << "  for (unsigned e = tid; e < " << Gs << "; e += " << cfg.block << "u) sm[" << g.bb << "u + e] = ";
+    if (D.b_uv != kNone) o << "e < " << D.n_out << "u ? UVg[" << D.b_uv << "u + e] : (T)0;\n";
+    else o << "(T)0;\n";
+  }
+  o << "  for (unsigned e = tid; e < " << WPB * nd << "u; e += " << cfg.block << "u) sRed[e] = (T)0;\n"
+    << "  __syncthreads();\n";
+  // accumulators
+  for (std::size_t i = 0; i < ng; ++i) {
+    const Grp& g = gr[i];
+    if (g.dw0 != kNone) {
+      const unsigned na = g.xvec ? g.D->n_out : g.D->n_in;
+      for (unsigned c = 0; c < na; ++c) o << "  T aw" << i << "_" << c << " = (T)0;\n";
+    }
+    bool anyb = false, unit = true;
+    for (std::uint32_t j = 0; j < g.D->n_out; ++j) {
+      anyb = anyb || g.bdest[j] != kNone;
+      unit = unit && g.bcoef[j] == 1.0;
+    }
+    if (anyb) {
+      o << "  T ab" << i << " = (T)0;\n";
+      if (!unit) {
+        o << "  T bc" << i << " = (T)0;\n";
+        for (std::uint32_t j = 0; j < g.D->n_out; ++j)
+          o << "  if (q == " << j << "u) bc" << i << " = " << lit(g.bcoef[j], f64) << ";\n";
+      }
+    }
+  }
+  for (std::size_t e = 0; e < sdests.size(); ++e) o << "  T as" << e << " = (T)0;\n";
+
+  o << "  const unsigned long long TW = (unsigned long long)gridDim.x * " << WPB << "u;\n"
+    << "  for (unsigned long long base = ((unsigned long long)blockIdx.x * " << WPB << "u + warp) * " << SPW
+    << "u; base < batch; base += TW * " << SPW << "u) {\n"
+    << "    const unsigned long long sa = base + slot;\n"
+    << "    const bool active = sa < batch;\n"
+    << "    const unsigned long long s = active ? sa : batch - 1;\n"
+    << "    {\n";
+  auto group_fwd = [&](std::size_t i) {
+    const Grp& g = gr[i];
+    const tgc::Dense& D = *g.D;
+    const std::string I = std::to_string(i);
+    o << "      // dense " << I << ": " << D.n_out << " x " << D.n_in << (g.xvec ? " (x from dense " + std::to_string(g.src) + ")" : " (scalar x)") << "\n";
+    std::vector<std::string> x(D.n_in);
+    for (std::uint32_t k = 0; k < D.n_in; ++k)
+      x[k] = g.xvec ? "sX[" + std::to_string(gr[g.src].xo + k) + "u]" : Gn.V(g.xr[k]);
+    o << "      T zz" << I << " = sm[" << g.bb << "u + q];";
+    for (std::uint32_t k = 0; k < D.n_in; ++k)
+      o << " zz" << I << " += " << x[k] << " * sm[" << g.wf + k * G << "u + q];";
+    o << "\n";
+    if (D.act_op) o << "      const T hh" << I << " = " << Gn.act_f(D.act_op, "zz" + I) << ";\n";
+    o << "      sX[" << g.xo << "u + q] = " << (D.act_op ? "hh" : "zz") << I << ";\n      __syncwarp();\n";
+  };
+  auto group_bwd = [&](std::size_t i) {
+    const Grp& g = gr[i];
+    const tgc::Dense& D = *g.D;
+    const std::string I = std::to_string(i);
+    o << "      // dense " << I << " reverse\n";
+    o << "      T gz" << I << " = " << (D.act_op ? Gn.act_b(D.act_op, "gh" + I, "hh" + I, "zz" + I) : "gh" + I) << ";\n";
+    if (D.n_out < G) o << "      if (q >= " << D.n_out << "u) gz" << I << " = (T)0;\n";
+    bool anyb = false, unit = true;
+    for (std::uint32_t j = 0; j < D.n_out; ++j) {
+      anyb = anyb || g.bdest[j] != kNone;
+      unit = unit && g.bcoef[j] == 1.0;
+    }
+    if (anyb) o << "      if (active) ab" << I << " += " << (unit ? "gz" + I : "bc" + I + " * gz" + I) << ";\n";
+    if (g.xvec) {
+      const Grp& sg = gr[g.src];
+      const std::string xk = sg.D->act_op ? "hh" + std::to_string(g.src) : "zz" + std::to_string(g.src);
+      o << "      sX[" << g.xg << "u + q] = gz" << I << ";\n      __syncwarp();\n"
+        << "      { T dx = (T)0;\n";
+      for (std::uint32_t j = 0; j < D.n_out; ++j) {
+        o << "        { const T gj = sX[" << g.xg + j << "u]; dx += gj * sm[" << g.wb + j * G << "u + q];";
+        if (g.dw0 != kNone) o << " if (active) aw" << I << "_" << j << " += gj * " << xk << ";";
+        o << " }\n";
+      }
+      o << "        gh" << g.src << " += dx; }\n";
+    } else {
+      Instr pseudo{};
+      pseudo.opnd = D.x_opnd;
+      for (std::uint32_t k = 0; k < D.n_in; ++k) {
+        const std::string pk = "px" + std::to_string(Gn.tmp++);
+        o << "      T " << pk << " = gz" << I << " * sm[" << g.wf + k * G << "u + q];";
+        for (unsigned m = G / 2; m >= 1; m /= 2)
+          o << " " << pk << " += __shfl_xor_sync(0xffffffffu, " << pk << ", " << m << ");";
+        o << "\n";
+        if (g.dw0 != kNone) o << "      if (active) aw" << I << "_" << k << " += gz" << I << " * " << Gn.V(g.xr[k]) << ";\n";
+        Gn.push(pseudo, k, pk);
+      }
+    }
+  };
+  for (const Instr& in : P.fwd) {
+    if (in.kind == tgc::kDense) group_fwd(in.aux);
+    else Gn.forward(in);
+  }
+  o << "      if (loss && active && q == 0u) loss[s] = " << Gn.V(P.root_row) << ";\n";
+  for (std::size_t i = 0; i < ng; ++i) o << "      T gh" << i << " = (T)0;\n";
+  for (std::uint32_t r : P.zero_rows)
+    if (rg[r] < 0 && zg[r] < 0) o << "      T " << Gn.g(r) << " = (T)0;\n";
+  o << "      T " << Gn.g(P.root_row) << " = (T)1;\n";
+  for (const Instr& in : P.bwd) {
+    if (in.kind == tgc::kDense) group_bwd(in.aux);
+    else Gn.reverse(in);
+  }
+  for (std::uint32_t c = 0; c < P.n_inputs; ++c) {
+    const std::uint32_t r = P.input_rows[c];
+    if (r != kNone) o << "      if (igrad && active && q == 0u) igrad[" << c << "ull * batch + s] = " << Gn.Gx(r) << ";\n";
+  }
+  if (!sdests.empty()) {
+    o << "      if (active) {\n";
+    for (std::size_t e = 0; e < sdests.size(); ++e) {
+      const unsigned d = sdests[e];
+      for (std::uint32_t u = P.term_off[d]; u < P.term_off[d + 1]; ++u) {
+        const tgc::Term& t = P.terms[u];
+        o << "        as" << e << " += " << lit(t.coef, f64) << " * " << Gn.Gx(t.a);
+        if (t.f != kNone) o << " * " << Gn.V(t.f);
+        o << ";\n";
+      }
+    }
+    o << "      }\n";
+  }
+  o << "    }\n    __syncwarp();\n  }\n";
+  // reduction: sample slots of a warp (lanes q, q+G, ...), then warps in fixed order
+  auto slot_sum = [&](const std::string& a) {
+    for (unsigned m = G; m < 32; m *= 2) o << "  " << a << " += __shfl_xor_sync(0xffffffffu, " << a << ", " << m << ");\n";
+  };
+  for (std::size_t i = 0; i < ng; ++i) {
+    const Grp& g = gr[i];
+    const std::string I = std::to_string(i);
+    if (g.dw0 != kNone) {
+      const unsigned na = g.xvec ? g.D->n_out : g.D->n_in;
+      for (unsigned c = 0; c < na; ++c) slot_sum("aw" + I + "_" + std::to_string(c));
+    }
+    bool anyb = false;
+    for (auto d : g.bdest) anyb = anyb || d != kNone;
+    if (anyb) slot_sum("ab" + I);
+  }
+  for (std::size_t e = 0; e < sdests.size(); ++e) slot_sum("as" + std::to_string(e));
+  o << "  if (slot == 0u) {\n    T* red = sRed + warp * " << nd << "u;\n";
+  for (std::size_t i = 0; i < ng; ++i) {
+    const Grp& g = gr[i];
+    const tgc::Dense& D = *g.D;
+    const std::string I = std::to_string(i);
+    if (g.dw0 != kNone) {
+      if (g.xvec) {
+        o << "    if (q < " << D.n_in << "u) {";
+        for (std::uint32_t j = 0; j < D.n_out; ++j)
+          o << " red[" << g.dw0 + j * D.n_in << "u + q] = aw" << I << "_" << j << ";";
+        o << " }\n";
+      } else {
+        o << "    if (q < " << D.n_out << "u) {";
+        for (std::uint32_t k = 0; k < D.n_in; ++k)
+          o << " red[" << g.dw0 + k << "u + q * " << D.n_in << "u] = aw" << I << "_" << k << ";";
+        o << " }\n";
+      }
+    }
+    for (std::uint32_t j = 0; j < D.n_out; ++j)
+      if (g.bdest[j] != kNone) o << "    if (q == " << j << "u) red[" << g.bdest[j] << "u] = ab" << I << ";\n";
+  }
+  for (std::size_t e = 0; e < sdests.size(); ++e) o << "    if (q == 0u) red[" << sdests[e] << "u] = as" << e << ";\n";
+  o << "  }\n  __syncthreads();\n"
+    << "  for (unsigned d = tid; d < " << nd << "u; d += " << cfg.block << "u) {\n"
+    << "    T t = (T)0;\n"
+    << "    for (unsigned w = 0; w < " << WPB << "u; ++w) t += sRed[w * " << nd << "u + d];\n"
+    << "    partial[(unsigned long long)d * grid_rows + blockIdx.x] = t;\n  }\n}\n";
+  return o.str();
+}
+
+// ---------------------------------------------------------------------------
+// FP64 tensor-core form: mma.sync m8n8k4 f64 (DMMA).  A warp runs 8 samples
+// at a time; lane (g, c) = (lane / 4, lane % 4) belongs to sample g.  The
+// outputs of a dense layer live in the accumulator (D) layout: lane (g, c)
+// holds neurons 8u + 2c + {0, 1} of sample g for every 8-wide tile u.  The
+// next layer's A operand is read straight from those registers by ordering
+// its k axis as k = 8 (t / 2) + 2c + (t % 2) for k-step t; the weights'
+// B fragments are staged in shared memory in the same order, so activations
+// never move between layers.  Biases of scalar-input layers ride in A as a
+// ones column; those of chained layers initialise the accumulator.  Weight
+// and bias gradients are a DMMA contraction over the samples of each step
+// through a per-warp transpose buffer, accumulated in registers across the
+// warp's samples, then reduced over the block in a fixed order.  The loss
+// glue runs replicated on the 4 lanes of each sample, as in generate().
+std::string generate_dmma(const tgc::Program& P, const JitConfig& cfg, unsigned& spb, std::size_t& smem_bytes,
+                          std::string& why) {
+  auto no = [&](const std::string& w) { why = w; return std::string(); };
+  if (P.dtype != TG_F64) return no("DMMA form is fp64 only");
+  DensePlan plan;
+  if (!plan_dense(P, plan, why)) return std::string();
+  const unsigned nd = static_cast<unsigned>(P.dest_uv.size());
+  const unsigned WPB = cfg.block / 32;
+  auto& gr = plan.gr;
+  auto& rg = plan.rg;
+  auto& zg = plan.zg;
+  auto& sdests = plan.sdests;
+  const std::size_t ng = gr.size();
+  for (const auto& g : gr)
+    if (g.D->n_out > 64 || g.D->n_in > 64) return no("dense layer wider than 64");
+  auto tiles = [](unsigned n) { return (n + 7) / 8; };
+  auto ld16 = [](unsigned n) { unsigned l = n; while (l % 16 != 4) ++l; return l; };   // conflict-free fragment loads
+  struct Geo { unsigned ntO = 0, ks = 0, ntX = 0, ntK = 0, kin = 0; bool fb = false, contract = false; unsigned bf = 0, bk = 0, bb = 0; };
+  std::vector<Geo> ge(ng);
+  unsigned off = 0, maxg = 0, maxx = 0;
+  for (std::size_t i = 0; i < ng; ++i) {
+    const tgc::Dense& D = *gr[i].D;
+    Geo& q = ge[i];
+    q.ntO = tiles(D.n_out);
+    q.fb = D.b_uv != kNone;
+    q.ks = gr[i].xvec ? 2 * tiles(D.n_in) : (D.n_in + (q.fb ? 1 : 0) + 3) / 4;
+    q.ntX = tiles(D.n_in);
+    q.contract = gr[i].dw0 != kNone || gr[i].has_bias();
+    q.kin = D.n_in + (gr[i].has_bias() ? 1 : 0);
+    q.ntK = tiles(q.kin);
+    q.bf = off;
+    off += q.ks * q.ntO * 32;
+    q.bk = off;
+    off += 2 * q.ntO * q.ntX * 32;
+    q.bb = off;
+    off += 8 * q.ntO;
+    if (q.contract) {
+      maxg = std::max(maxg, 8 * q.ntO);
+      maxx = std::max(maxx, 8 * q.ntK);
+    }
+  }
+  const unsigned ldg = maxg ? ld16(maxg) : 0, ldx = maxx ? ld16(maxx) : 0;
+  const unsigned per_warp = 8 * (ldg + ldx);
+  const std::size_t elems = std::size_t(off) + std::size_t(WPB) * per_warp + std::size_t(WPB) * nd;
+  if (elems * 8 > 160 * 1024) return no("shared memory");
+  smem_bytes = elems * 8;
+  spb = WPB * 8;
+
+  // glue reads of layer outputs are materialised once (lane shuffle from the owner)
+  std::vector<char> needv(P.n_rows, 0);
+  for (const Instr& in : P.fwd) {
+    if (in.kind != tgc::kNode) continue;
+    for (std::uint32_t j = 0; j < in.nops; ++j) {
+      const std::uint32_t op = P.opnd[in.opnd + j];
+      if ((op >> kModeShift) == tgc::kSlot && rg[op & kIndexMask] >= 0) needv[op & kIndexMask] = 1;
+    }
+  }
+  for (unsigned d : sdests)
+    for (std::uint32_t u = P.term_off[d]; u < P.term_off[d + 1]; ++u)
+      if (P.terms[u].f != kNone && rg[P.terms[u].f] >= 0) needv[P.terms[u].f] = 1;
+
+  Gen Gn(P, cfg);
+  Gn.vslot.assign(P.n_rows, -1);
+  Gn.gslot.assign(P.n_rows, -1);
+  Gn.vsm.assign(P.n_rows, 0);
+  Gn.gsm.assign(P.n_rows, 0);
+  Gn.vov.assign(P.n_rows, "");
+  Gn.gov.assign(P.n_rows, "");
+  Gn.gcond.assign(P.n_rows, "");
+  Gn.gj.assign(P.n_rows, -1);
+  auto nm = [](const char* p, std::size_t i, unsigned u, unsigned e) {
+    return std::string(p) + std::to_string(i) + "_" + std::to_string(u) + "_" + std::to_string(e);
+  };
+  auto outn = [&](std::size_t i, unsigned u, unsigned e) { return nm(gr[i].D->act_op ? "dh" : "dz", i, u, e); };
+  for (std::size_t i = 0; i < ng; ++i)
+    for (std::uint32_t j = 0; j < gr[i].D->n_out; ++j) {
+      const std::uint32_t r = gr[i].crow + j;
+      Gn.vov[r] = "bv" + std::to_string(r);
+      Gn.gov[r] = nm("gh", i, j / 8, j % 2);
+      Gn.gcond[r] = "c == " + std::to_string((j % 8) / 2) + "u";
+    }
+  std::ostringstream& o = Gn.o;
+  o << "typedef double T;\n" << kMath << kPrelude
+    << "__device__ __forceinline__ void tg_dmma(double& d0, double& d1, double a, double b) {\n"
+    << "  asm(\"mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\"\n"
+    << "      : \"+d\"(d0), \"+d\"(d1) : \"d\"(a), \"d\"(b));\n}\n";
+  if (cfg.const_uv) o << "__constant__ T cUV[" << std::max<std::uint32_t>(1, P.n_uv) << "];\n";
+  for (std::size_t i = 0; i < ng; ++i) {
+    if (!gr[i].has_bias()) continue;
+    o << "__constant__ unsigned cBD" << i << "[" << gr[i].D->n_out << "] = {";
+    for (std::uint32_t j = 0; j < gr[i].D->n_out; ++j) o << (j ? ", " : "") << gr[i].bdest[j] << "u";
+    o << "};\n";
+    if (!gr[i].unit_bias()) {
+      o << "__constant__ T cBC" << i << "[" << gr[i].D->n_out << "] = {";
+      for (std::uint32_t j = 0; j < gr[i].D->n_out; ++j) o << (j ? ", " : "") << lit(gr[i].bcoef[j], true);
+      o << "};\n";
+    }
+  }
+  o << "extern \"C\" __global__ void __launch_bounds__(" << cfg.block;
+  if (cfg.min_blocks) o << ", " << cfg.min_blocks;
+  o << ") tg_jit_tape(\n"
+    << "    const T* __restrict__ in, const int* __restrict__ idx, unsigned long long batch,\n"
+    << "    T* __restrict__ loss, T* __restrict__ igrad, T* __restrict__ partial, unsigned grid_rows,\n"
+    << "    unsigned long long* err_key, const T* __restrict__ UVg, const unsigned* __restrict__ cand,\n"
+    << "    const unsigned* __restrict__ toff, const TermC* __restrict__ terms) {\n"
+    << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
+    << "  T* sm = reinterpret_cast<T*>(smem_raw);\n"
+    << "  const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;\n"
+    << "  const unsigned g = lane >> 2, c = lane & 3u;\n"
+    << "  T* gzb = sm + " << off << "u + warp * " << per_warp << "u;\n"
+    << "  T* xb = gzb + " << 8 * ldg << "u;\n"
+    << "  T* sRed = sm + " << off + WPB * per_warp << "u;\n"
+    << "  (void)toff; (void)terms; (void)cand; (void)idx; (void)in; (void)err_key; (void)gzb; (void)xb;\n";
+  // B fragments of every layer, in the lane order of mma.sync m8n8k4 (b0 = B[lane % 4][lane / 4])
+  for (std::size_t i = 0; i < ng; ++i) {
+    const tgc::Dense& D = *gr[i].D;
+    const Geo& q = ge[i];
+    const std::string W = std::to_string(D.w_uv) + "u", NI = std::to_string(D.n_in) + "u",
+                      NO = std::to_string(D.n_out) + "u";
+    o << "  for (unsigned e = tid; e < " << q.ks * q.ntO * 32 << "u; e += " << cfg.block << "u) {\n"
+      << "    const unsigned t = e / " << q.ntO * 32 << "u, u = (e >> 5) % " << q.ntO << "u, L = e & 31u;\n"
+      << "    const unsigned n = 8u * u + (L >> 2), cc = L & 3u;\n";
+    if (gr[i].xvec)
+      o << "    const unsigned k = 8u * (t >> 1) + 2u * cc + (t & 1u);\n"
+        << "    sm[" << q.bf << "u + e] = (n < " << NO << " && k < " << NI << ") ? UVg[" << W << " + n * " << NI << " + k] : (T)0;\n";
+    else {
+      o << "    const unsigned k = 4u * t + cc;\n"
+        << "    T w = (T)0;\n"
+        << "    if (n < " << NO << ") { if (k < " << NI << ") w = UVg[" << W << " + n * " << NI << " + k];";
+      if (q.fb) o << " else if (k == " << NI << ") w = UVg[" << D.b_uv << "u + n];";
+      o << " }\n    sm[" << q.bf << "u + e] = w;\n";
+    }
+    o << "  }\n"
+      << "  for (unsigned e = tid; e < " << 2 * q.ntO * q.ntX * 32 << "u; e += " << cfg.block << "u) {\n"
+      << "    const unsigned t = e / " << q.ntX * 32 << "u, u = (e >> 5) % " << q.ntX << "u, L = e & 31u;\n"
+      << "    const unsigned n = 8u * u + (L >> 2), k = 8u * (t >> 1) + 2u * (L & 3u) + (t & 1u);\n"
+      << "    sm[" << q.bk << "u + e] = (k < " << NO << " && n < " << NI << ") ? UVg[" << W << " + k * " << NI << " + n] : (T)0;\n"
+      << "  }\n";
+    if (gr[i].xvec && q.fb)
+      o << "  for (unsigned e = tid; e < " << 8 * q.ntO << "u; e += " << cfg.block << "u) sm[" << q.bb << "u + e] = e < "
+        << NO << " ? UVg[" << D.b_uv << "u + e] : (T)0;\n";
+  }
+  o << "  for (unsigned e = tid; e < " << WPB * nd << "u; e += " << cfg.block << "u) sRed[e] = (T)0;\n"
+    << "  __syncthreads();\n";
+  for (std::size_t i = 0; i < ng; ++i)
+    if (ge[i].contract)
+      for (unsigned u = 0; u < ge[i].ntO; ++u)
+        for (unsigned v = 0; v < ge[i].ntK; ++v)
+          o << "  T aw" << i << "_" << u << "_" << v << "_0 = (T)0, aw" << i << "_" << u << "_" << v << "_1 = (T)0;\n";
+  for (std::size_t e = 0; e < sdests.size(); ++e) o << "  T as" << e << " = (T)0;\n";
+  o << "  const unsigned long long TW = (unsigned long long)gridDim.x * " << WPB << "u;\n"
+    << "  for (unsigned long long base = ((unsigned long long)blockIdx.x * " << WPB
+    << "u + warp) * 8u; base < batch; base += TW * 8u) {\n"
+    << "    const unsigned long long sa = base + g;\n"
+    << "    const bool active = sa < batch;\n"
+    << "    const unsigned long long s = active ? sa : batch - 1;\n"
+    << "    {\n";
+  auto group_fwd = [&](std::size_t i) {
+    const DenseGroup& G = gr[i];
+    const tgc::Dense& D = *G.D;
+    const Geo& q = ge[i];
+    const std::string I = std::to_string(i);
+    o << "      // dense " << I << ": " << D.n_out << " x " << D.n_in << " on DMMA\n";
+    for (unsigned u = 0; u < q.ntO; ++u)
+      for (unsigned e = 0; e < 2; ++e) {
+        o << "      T " << nm("dz", i, u, e) << " = ";
+        if (G.xvec && q.fb) o << "sm[" << q.bb + 8 * u + e << "u + 2u * c];\n";
+        else o << "(T)0;\n";
+      }
+    for (unsigned t = 0; t < q.ks; ++t) {
+      std::string a;
+      if (G.xvec) {
+        a = outn(G.src, t / 2, t % 2);
+      } else {
+        auto X = [&](unsigned k) -> std::string {
+          if (k < D.n_in) return Gn.V(G.xr[k]);
+          return (k == D.n_in && q.fb) ? "(T)1" : "(T)0";
+        };
+        a = "da" + std::to_string(Gn.tmp++);
+        o << "      const T " << a << " = c == 0u ? " << X(4 * t) << " : c == 1u ? " << X(4 * t + 1) << " : c == 2u ? "
+          << X(4 * t + 2) << " : " << X(4 * t + 3) << ";\n";
+      }
+      for (unsigned u = 0; u < q.ntO; ++u)
+        o << "      tg_dmma(" << nm("dz", i, u, 0) << ", " << nm("dz", i, u, 1) << ", " << a << ", sm["
+          << q.bf + (t * q.ntO + u) * 32 << "u + lane]);\n";
+    }
+    if (D.act_op)
+      for (unsigned u = 0; u < q.ntO; ++u)
+        for (unsigned e = 0; e < 2; ++e)
+          o << "      const T " << nm("dh", i, u, e) << " = " << Gn.act_f(D.act_op, nm("dz", i, u, e)) << ";\n";
+    for (std::uint32_t j = 0; j < D.n_out; ++j) {
+      const std::uint32_t r = G.crow + j;
+      if (needv[r])
+        o << "      const T bv" << r << " = __shfl_sync(0xffffffffu, " << outn(i, j / 8, j % 2) << ", (lane & ~3u) | "
+          << (j % 8) / 2 << "u);\n";
+    }
+  };
+  auto group_bwd = [&](std::size_t i) {
+    const DenseGroup& G = gr[i];
+    const tgc::Dense& D = *G.D;
+    const Geo& q = ge[i];
+    const std::string I = std::to_string(i);
+    o << "      // dense " << I << " reverse\n";
+    for (unsigned u = 0; u < q.ntO; ++u)
+      for (unsigned e = 0; e < 2; ++e) {
+        const std::string gz = nm("gz", i, u, e);
+        o << "      T " << gz << " = "
+          << (D.act_op ? Gn.act_b(D.act_op, nm("gh", i, u, e), nm("dh", i, u, e), nm("dz", i, u, e)) : nm("gh", i, u, e)) << ";\n";
+        if (8 * u + 8 > D.n_out)
+          o << "      if (" << 8 * u + e << "u + 2u * c >= " << D.n_out << "u) " << gz << " = (T)0;\n";
+      }
+    // input adjoints: dX = gz . W (k axis = this layer's outputs in D-layout order)
+    if (G.xvec) {
+      for (unsigned t = 0; t < 2 * q.ntO; ++t)
+        for (unsigned u = 0; u < q.ntX; ++u)
+          o << "      tg_dmma(" << nm("gh", G.src, u, 0) << ", " << nm("gh", G.src, u, 1) << ", " << nm("gz", i, t / 2, t % 2)
+            << ", sm[" << q.bk + (t * q.ntX + u) * 32 << "u + lane]);\n";
+    } else {
+      for (unsigned u = 0; u < q.ntX; ++u)
+        o << "      T " << nm("dx", i, u, 0) << " = (T)0, " << nm("dx", i, u, 1) << " = (T)0;\n";
+      for (unsigned t = 0; t < 2 * q.ntO; ++t)
+        for (unsigned u = 0; u < q.ntX; ++u)
+          o << "      tg_dmma(" << nm("dx", i, u, 0) << ", " << nm("dx", i, u, 1) << ", " << nm("gz", i, t / 2, t % 2)
+            << ", sm[" << q.bk + (t * q.ntX + u) * 32 << "u + lane]);\n";
+      Instr pseudo{};
+      pseudo.opnd = D.x_opnd;
+      for (std::uint32_t k = 0; k < D.n_in; ++k) {
+        const std::string px = "px" + std::to_string(Gn.tmp++);
+        o << "      const T " << px << " = __shfl_sync(0xffffffffu, " << nm("dx", i, k / 8, k % 2) << ", (lane & ~3u) | "
+          << (k % 8) / 2 << "u);\n";
+        Gn.push(pseudo, k, px);
+      }
+    }
+    if (!q.contract) return;
+    // weight / bias gradients: Acc[n][k] += sum over this step's 8 samples of gz[s][n] x[s][k]
+    for (unsigned u = 0; u < q.ntO; ++u)
+      for (unsigned e = 0; e < 2; ++e)
+        o << "      gzb[g * " << ldg << "u + " << 8 * u + e << "u + 2u * c] = active ? " << nm("gz", i, u, e) << " : (T)0;\n";
+    if (G.xvec) {
+      const unsigned nts = ge[G.src].ntO;
+      for (unsigned u = 0; u < nts; ++u)
+        for (unsigned e = 0; e < 2; ++e) {
+          o << "      ";
+          if (8 * u + 8 > D.n_in) o << "if (" << 8 * u + e << "u + 2u * c < " << D.n_in << "u) ";
+          o << "xb[g * " << ldx << "u + " << 8 * u + e << "u + 2u * c] = active ? " << outn(G.src, u, e) << " : (T)0;\n";
+        }
+    } else {
+      for (std::uint32_t k = 0; k < D.n_in; ++k)
+        o << "      if (c == " << k % 4 << "u) xb[g * " << ldx << "u + " << k << "u] = active ? " << Gn.V(G.xr[k]) << " : (T)0;\n";
+    }
+    if (G.has_bias()) o << "      if (c == 0u) xb[g * " << ldx << "u + " << D.n_in << "u] = active ? (T)1 : (T)0;\n";
+    o << "      __syncwarp();\n";
+    for (unsigned t = 0; t < 2; ++t) {
+      for (unsigned u = 0; u < q.ntO; ++u)
+        o << "      const T qa" << i << "_" << t << "_" << u << " = gzb[(" << 4 * t << "u + c) * " << ldg << "u + " << 8 * u << "u + g];\n";
+      for (unsigned v = 0; v < q.ntK; ++v)
+        o << "      const T qb" << i << "_" << t << "_" << v << " = xb[(" << 4 * t << "u + c) * " << ldx << "u + " << 8 * v << "u + g];\n";
+      for (unsigned u = 0; u < q.ntO; ++u)
+        for (unsigned v = 0; v < q.ntK; ++v)
+          o << "      tg_dmma(aw" << i << "_" << u << "_" << v << "_0, aw" << i << "_" << u << "_" << v << "_1, qa" << i << "_"
+            << t << "_" << u << ", qb" << i << "_" << t << "_" << v << ");\n";
+    }
+    o << "      __syncwarp();\n";
+  };
+  for (const Instr& in : P.fwd) {
+    if (in.kind == tgc::kDense) group_fwd(in.aux);
+    else Gn.forward(in);
+  }
+  o << "      if (loss && active && c == 0u) loss[s] = " << Gn.V(P.root_row) << ";\n";
+  for (std::size_t i = 0; i < ng; ++i)
+    for (unsigned u = 0; u < ge[i].ntO; ++u)
+      o << "      T " << nm("gh", i, u, 0) << " = (T)0, " << nm("gh", i, u, 1) << " = (T)0;\n";
+  for (std::uint32_t r : P.zero_rows)
+    if (rg[r] < 0 && zg[r] < 0) o << "      T " << Gn.g(r) << " = (T)0;\n";
+  o << "      T " << Gn.g(P.root_row) << " = (T)1;\n";
+  for (const Instr& in : P.bwd) {
+    if (in.kind == tgc::kDense) group_bwd(in.aux);
+    else Gn.reverse(in);
+  }
+  for (std::uint32_t cI = 0; cI < P.n_inputs; ++cI) {
+    const std::uint32_t r = P.input_rows[cI];
+    if (r != kNone) o << "      if (igrad && active && c == 0u) igrad[" << cI << "ull * batch + s] = " << Gn.Gx(r) << ";\n";
+  }
+  if (!sdests.empty()) {
+    o << "      if (active && c == 0u) {\n";
+    for (std::size_t e = 0; e < sdests.size(); ++e) {
+      const unsigned d = sdests[e];
+      for (std::uint32_t u = P.term_off[d]; u < P.term_off[d + 1]; ++u) {
+        const tgc::Term& t = P.terms[u];
+        o << "        as" << e << " += " << lit(t.coef, true) << " * " << Gn.Gx(t.a);
+        if (t.f != kNone) o << " * " << Gn.V(t.f);
+        o << ";\n";
+      }
+    }
+    o << "      }\n";
+  }
+  o << "    }\n    __syncwarp();\n  }\n";
+  for (std::size_t e = 0; e < sdests.size(); ++e)
+    for (unsigned m = 4; m < 32; m *= 2)
+      o << "  as" << e << " += __shfl_xor_sync(0xffffffffu, as" << e << ", " << m << ");\n";
+  o << "  {\n    T* red = sRed + warp * " << nd << "u;\n";
+  for (std::size_t i = 0; i < ng; ++i) {
+    const DenseGroup& G = gr[i];
+    const Geo& q = ge[i];
+    if (!q.contract) continue;
+    const unsigned no_ = G.D->n_out, ni = G.D->n_in;
+    for (unsigned u = 0; u < q.ntO; ++u)
+      for (unsigned v = 0; v < q.ntK; ++v)
+        for (unsigned e = 0; e < 2; ++e) {
+          o << "    { const unsigned n = " << 8 * u << "u + g, k = " << 8 * v + e << "u + 2u * c; if (n < " << no_ << "u) {";
+          if (G.dw0 != kNone) o << " if (k < " << ni << "u) red[" << G.dw0 << "u + n * " << ni << "u + k] = aw" << i << "_" << u << "_" << v << "_" << e << ";";
+          if (G.has_bias()) {
+            o << " if (k == " << ni << "u && cBD" << i << "[n] != 0xffffffffu) red[cBD" << i << "[n]] = ";
+            if (!G.unit_bias()) o << "cBC" << i << "[n] * ";
+            o << "aw" << i << "_" << u << "_" << v << "_" << e << ";";
+          }
+          o << " } }\n";
+        }
+  }
+  for (std::size_t e = 0; e < sdests.size(); ++e) o << "    if (lane == 0u) red[" << sdests[e] << "u] = as" << e << ";\n";
+  o << "  }\n  __syncthreads();\n"
+    << "  for (unsigned d = tid; d < " << nd << "u; d += " << cfg.block << "u) {\n"
+    << "    T t = (T)0;\n"
+    << "    for (unsigned w = 0; w < " << WPB << "u; ++w) t += sRed[w * " << nd << "u + d];\n"
+    << "    partial[(unsigned long long)d * grid_rows + blockIdx.x] = t;\n  }\n}\n";
+  return o.str();
+}
+
 JitKernel build(const tgc::Program& P) {
   JitKernel k;
   if (!eligible(P)) { k.log = "not eligible"; return k; }
@@ -664,12 +1411,55 @@ JitKernel build(const tgc::Program& P) {
   if (const char* e = std::getenv("TG_JIT_DLOOP")) cfg.dense_loop = std::atoi(e) != 0;
   std::vector<tgc::Term> terms;
   std::vector<std::uint32_t> toff;
-  std::size_t smem_elems = 0;
-  k.source = generate(P, cfg, k.n_crow_g, k.n_crow_v, terms, toff, smem_elems);
-  k.cfg = cfg;
-  k.tile = cfg.block * cfg.spt;
-  k.smem_bytes = smem_elems * ts;
-  if (k.smem_bytes > 200 * 1024) { k.log = "contraction rows exceed shared memory"; return k; }
+  // specialised forms for dense-layer chains before the one-thread-per-sample form
+  // form: TG_JIT_FORM = dmma | group | classic (default: first that applies, in that order)
+  const char* fe = std::getenv("TG_JIT_FORM");
+  const std::string form = fe ? fe : "";
+  if (form.empty() || form == "dmma") {
+    JitConfig dc = cfg;
+    dc.block = 128;
+    dc.min_blocks = 0;
+    if (const char* e = std::getenv("TG_JIT_GBLOCK")) dc.block = static_cast<unsigned>(std::atoi(e));
+    if (const char* e = std::getenv("TG_JIT_GMINB")) dc.min_blocks = static_cast<unsigned>(std::atoi(e));
+    unsigned spb = 0;
+    std::size_t sb = 0;
+    std::string src = generate_dmma(P, dc, spb, sb, k.group_log);
+    if (!src.empty()) {
+      k.source = std::move(src);
+      k.cfg = dc;
+      k.tile = spb;
+      k.smem_bytes = sb;
+      k.group = 4;
+      k.form = "dmma";
+    }
+  }
+  if (!k.group && (form.empty() || form == "group")) {
+    JitConfig gc = cfg;
+    gc.block = 256;
+    gc.min_blocks = 0;
+    if (const char* e = std::getenv("TG_JIT_GBLOCK")) gc.block = static_cast<unsigned>(std::atoi(e));
+    if (const char* e = std::getenv("TG_JIT_GMINB")) gc.min_blocks = static_cast<unsigned>(std::atoi(e));
+    unsigned G = 0, spb = 0;
+    std::size_t sb = 0;
+    std::string src = generate_grouped(P, gc, G, spb, sb, k.group_log);
+    if (!src.empty()) {
+      k.source = std::move(src);
+      k.cfg = gc;
+      k.tile = spb;
+      k.smem_bytes = sb;
+      k.group = G;
+      k.form = "group";
+    }
+  }
+  if (!k.group) {
+    k.form = "classic";
+    std::size_t smem_elems = 0;
+    k.source = generate(P, cfg, k.n_crow_g, k.n_crow_v, terms, toff, smem_elems);
+    k.cfg = cfg;
+    k.tile = cfg.block * cfg.spt;
+    k.smem_bytes = smem_elems * ts;
+    if (k.smem_bytes > 200 * 1024) { k.log = "contraction rows exceed shared memory"; return k; }
+  }
 
   nvrtcProgram prog;
   // TG_JIT_DUMP=<dir>: write the source there and name it so -lineinfo maps to it (ncu source page)
@@ -716,8 +1506,8 @@ JitKernel build(const tgc::Program& P) {
     k.log = "smem attribute failed";
     return k;
   }
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k.occ, f, static_cast<int>(cfg.block), k.smem_bytes);
-  if (!P.dest_uv.empty()) {
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k.occ, f, static_cast<int>(k.cfg.block), k.smem_bytes);
+  if (!P.dest_uv.empty() && !k.group) {
     cudaMalloc(&k.d_terms, std::max<std::size_t>(1, terms.size()) * sizeof(tgc::Term));
     if (!terms.empty()) cudaMemcpy(k.d_terms, terms.data(), terms.size() * sizeof(tgc::Term), cudaMemcpyHostToDevice);
     cudaMalloc(&k.d_toff, toff.size() * sizeof(std::uint32_t));

@@ -39,7 +39,10 @@ struct JitKernel {
   void* cuv = nullptr;           // __constant__ table address (const_uv)
   std::size_t cuv_bytes = 0;
   JitConfig cfg;
-  unsigned tile = 128;           // samples per tile = block * spt
+  unsigned tile = 128;           // samples per tile = block * spt (grouped: per block iteration)
+  unsigned group = 0;            // lanes per sample (grouped form), 0 = one thread per sample
+  std::string group_log;         // why the dmma / grouped form was not used
+  std::string form;              // "dmma" | "group" | "classic"
   std::size_t smem_bytes = 0;    // contraction rows
   unsigned n_crow_g = 0, n_crow_v = 0;
   int occ = 0;
