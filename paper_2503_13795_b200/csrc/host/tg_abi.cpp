@@ -114,6 +114,7 @@ struct tg_program {
   unsigned long long* d_err_key = nullptr;
   double* d_err_val = nullptr;
   std::uint32_t* d_err_op = nullptr;
+  unsigned* d_ticket = nullptr;   // last-CTA ticket of the generated epilogue (self-resetting)
   // launch configuration
   bool smem = true;
   unsigned S = 128;
@@ -400,8 +401,10 @@ tg_status upload(tg_program& pr) {
   pr.d_err_key = static_cast<unsigned long long*>(e);
   pr.d_err_val = reinterpret_cast<double*>(static_cast<char*>(e) + 8);
   pr.d_err_op = reinterpret_cast<std::uint32_t*>(static_cast<char*>(e) + 16);
+  pr.d_ticket = reinterpret_cast<unsigned*>(static_cast<char*>(e) + 32);
   TG_CUDA_TRY(cudaMemset(e, 0xff, 8));
   TG_CUDA_TRY(cudaMemset(static_cast<char*>(e) + 16, 0xff, 4));
+  TG_CUDA_TRY(cudaMemset(static_cast<char*>(e) + 32, 0, 4));
   if (P.dtype == TG_F64) pr.occ = tgk::tape_occupancy<double>(pr.smem, pr.S, pr.smem_bytes);
   else pr.occ = tgk::tape_occupancy<float>(pr.smem, pr.S, pr.smem_bytes);
   cudaGetLastError();
@@ -681,6 +684,114 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
   return TG_OK;
 }
 
+// Launch with programmatic stream serialisation: the kernel may be scheduled
+// while its stream predecessor drains; it waits (griddepcontrol.wait) before
+// its first dependent read.
+cudaError_t launch_pdl(cudaKernel_t fn, unsigned grid, unsigned block, std::size_t smem, void** args, cudaStream_t st) {
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(grid);
+  lc.blockDim = dim3(block);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  return cudaLaunchKernelExC(&lc, reinterpret_cast<const void*>(fn), args);
+}
+
+// One step as two launches of the program's module: tg_jit_tape (uniform
+// prologue per CTA + per-sample sweeps + per-CTA partials) and tg_jit_epi
+// (fixed-order reduction, uniform reverse sweep, grad_sum, GD).
+template <class T>
+tg_status run_fused(tg_program& pr, const void* inputs, const std::int32_t* idx, std::size_t batch, const void* params,
+                    void* loss, void* igrad, void* grad_sum, T* UV, T* UG, T* partial, char* w, const Layout& L,
+                    cudaStream_t st, void* gd_params, double gamma) {
+  tgj::JitArgs<T> ja{};
+  const std::size_t rows = jit_grid(pr, batch);
+  ja.in = static_cast<const T*>(inputs);
+  ja.idx = idx;
+  ja.batch = batch;
+  ja.loss = static_cast<T*>(loss);
+  ja.igrad = static_cast<T*>(igrad);
+  ja.partial = partial;
+  ja.grid_rows = static_cast<unsigned>(rows);
+  ja.err_key = pr.d_err_key;
+  ja.err_val = pr.d_err_val;
+  ja.err_op = pr.d_err_op;
+  ja.UVg = UV;
+  ja.cand = pr.d_cand;
+  ja.toff = static_cast<const unsigned*>(pr.jit.d_toff);
+  ja.terms = pr.jit.d_terms;
+  ja.params = static_cast<const T*>(params);
+  ja.consts = static_cast<const T*>(pr.d_consts);
+  ja.UVw = UV;
+  ja.tickets = pr.d_ticket;
+  ja.partial2 = UG;
+  ja.grad_sum = static_cast<T*>(grad_sum);
+  ja.gd_params = static_cast<T*>(gd_params);
+  ja.gamma = static_cast<T>(gamma);
+  ja.gd_batch = static_cast<T>(static_cast<double>(batch));
+  void* args[] = {&ja};
+  cudaEvent_t e1 = nullptr;
+  if (pr.profiling) {
+    if (pr.ev_used == pr.ev.size()) {
+      cudaEvent_t a, b;
+      TG_CUDA_TRY(cudaEventCreate(&a));
+      TG_CUDA_TRY(cudaEventCreate(&b));
+      pr.ev.emplace_back(a, b);
+    }
+    TG_CUDA_TRY(cudaEventRecord(pr.ev[pr.ev_used].first, st));
+    e1 = pr.ev[pr.ev_used].second;
+    ++pr.ev_used;
+  }
+  TG_CUDA_TRY(launch_pdl(pr.jit.fn, ja.grid_rows, pr.jit.cfg.block, pr.jit.smem_bytes, args, st));
+  if (e1) TG_CUDA_TRY(cudaEventRecord(e1, st));
+  const unsigned nd = pr.n_dest();
+  TG_CUDA_TRY(launch_pdl(pr.jit.fn_epi, std::max(1u, (nd + 7) / 8), 256, 0, args, st));
+  pr.launches += 2;
+  // diagnosis of a domain error re-runs the interpreter on this launch's inputs
+  tgk::MainArgs<T> ma{};
+  ma.fwd = pr.d_fwd;
+  ma.bwd = pr.d_bwd;
+  ma.opnd = pr.d_opnd;
+  ma.oflag = pr.d_oflag;
+  ma.oaux = pr.d_oaux;
+  ma.zero_rows = pr.d_zero;
+  ma.input_rows = pr.d_inrows;
+  ma.ug = pr.d_ug;
+  ma.sg = pr.d_sg;
+  ma.cand = pr.d_cand;
+  ma.term_off = pr.d_termoff;
+  ma.terms = pr.d_terms;
+  ma.dense = pr.d_dense;
+  ma.UV = UV;
+  ma.inputs = static_cast<const T*>(inputs);
+  ma.idx = idx;
+  ma.partial = partial;
+  ma.gV = reinterpret_cast<T*>(w + L.gv);
+  ma.gG = reinterpret_cast<T*>(w + L.gg);
+  ma.err_key = pr.d_err_key;
+  ma.err_val = pr.d_err_val;
+  ma.err_op = pr.d_err_op;
+  ma.batch = batch;
+  ma.ld = pr.smem ? pr.ld_smem : grid_for(pr, batch) * pr.S;
+  ma.diag_sample = -1;
+  ma.n_fwd = static_cast<std::uint32_t>(pr.P.fwd.size());
+  ma.n_bwd = static_cast<std::uint32_t>(pr.P.bwd.size());
+  ma.n_zero = static_cast<std::uint32_t>(pr.P.zero_rows.size());
+  ma.n_inputs = pr.P.n_inputs;
+  ma.n_dest = pr.n_dest();
+  ma.n_rows = pr.P.n_rows;
+  ma.S = pr.S;
+  ma.root_row = pr.P.root_row;
+  pr.last_args.assign(reinterpret_cast<unsigned char*>(&ma), reinterpret_cast<unsigned char*>(&ma) + sizeof(ma));
+  pr.have_last = true;
+  pr.last_batch = batch;
+  return TG_OK;
+}
+
 template <class T>
 tg_status run_fb(tg_program& pr, const void* inputs, const std::int32_t* idx, std::size_t batch, const void* params,
                  void* loss, void* igrad, void* grad_sum, void* ws, std::size_t ws_bytes, cudaStream_t st,
@@ -703,6 +814,8 @@ tg_status run_fb(tg_program& pr, const void* inputs, const std::int32_t* idx, st
   T* UG = reinterpret_cast<T*>(w + L.ug);
   T* partial = reinterpret_cast<T*>(w + L.partial);
 
+  if (pr.jit.ok && pr.jit.fused && batch > 0)
+    return run_fused<T>(pr, inputs, idx, batch, params, loss, igrad, grad_sum, UV, UG, partial, w, L, st, gd_params, gamma);
   tgk::UniformArgs<T> ua{};
   ua.instr = pr.d_ufwd;
   ua.opnd = pr.d_opnd;
@@ -779,12 +892,23 @@ tg_status run_fb(tg_program& pr, const void* inputs, const std::int32_t* idx, st
     std::size_t rows = grid;
     if (pr.jit.ok) {
       rows = jit_grid(pr, batch);
-      unsigned grid_rows = static_cast<unsigned>(rows);
-      unsigned long long nb = batch;
-      const T* uvg = UV;
-      void* args[] = {&ma.inputs, &ma.idx, &nb, &ma.loss, &ma.igrad, &ma.partial, &grid_rows,
-                      &ma.err_key, &uvg, &ma.cand, &pr.jit.d_toff, &pr.jit.d_terms};
-      TG_CUDA_TRY(cudaLaunchKernel(reinterpret_cast<const void*>(pr.jit.fn), dim3(grid_rows), dim3(pr.jit.cfg.block),
+      tgj::JitArgs<T> ja{};
+      ja.in = ma.inputs;
+      ja.idx = ma.idx;
+      ja.batch = batch;
+      ja.loss = ma.loss;
+      ja.igrad = ma.igrad;
+      ja.partial = ma.partial;
+      ja.grid_rows = static_cast<unsigned>(rows);
+      ja.err_key = ma.err_key;
+      ja.err_val = ma.err_val;
+      ja.err_op = ma.err_op;
+      ja.UVg = UV;
+      ja.cand = ma.cand;
+      ja.toff = static_cast<const unsigned*>(pr.jit.d_toff);
+      ja.terms = pr.jit.d_terms;
+      void* args[] = {&ja};
+      TG_CUDA_TRY(cudaLaunchKernel(reinterpret_cast<const void*>(pr.jit.fn), dim3(ja.grid_rows), dim3(pr.jit.cfg.block),
                                    args, pr.jit.smem_bytes, st));
     } else {
       TG_CUDA_TRY(tgk::launch_tape<T>(ma, pr.smem, static_cast<unsigned>(grid), pr.S, pr.smem_bytes, st));

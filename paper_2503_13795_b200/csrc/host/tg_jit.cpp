@@ -81,6 +81,7 @@ struct Gen {
   // contraction, later reads (the reverse sweep) reload it from shared memory
   // so the register dies at the store (TG_JIT_RELOAD=0 keeps registers)
   std::string V(std::uint32_t r) const {
+    if (umode) return "sU[" + std::to_string(r) + "]";
     if (!vov.empty() && !vov[r].empty()) return vov[r];
     return vsm[r] || (reload && !vstored.empty() && vstored[r]) ? sv(r) : v(r);
   }
@@ -90,10 +91,18 @@ struct Gen {
   std::vector<std::string> vov, gov, gcond;
   std::vector<int> gj;
   bool reload = true;
-  std::string Gx(std::uint32_t r) const { return gsm[r] ? sg_(r) : g(r); } // adjoint of row r
+  std::string Gx(std::uint32_t r) const {  // adjoint of row r
+    if (umode) return "sG[" + std::to_string(r) + "]";
+    return gsm[r] ? sg_(r) : g(r);
+  }
   std::string uv(std::uint32_t i) const {
+    if (su) return "sU[" + std::to_string(i) + "]";
     return cfg.const_uv ? "cUV[" + std::to_string(i) + "]" : "UVg[" + std::to_string(i) + "]";
   }
+  // fused kernels: the sample-invariant table lives in shared memory (sU),
+  // evaluated by each CTA; umode emits the uniform program itself (values
+  // sU[u], adjoints sG[u]).
+  bool su = false, umode = false;
   std::string ix_expr(const tgc::GatherTable& t) const {
     return "tg_ix(idx, " + std::to_string(t.col) + "ull * batch + s, " + std::to_string(t.n_rows) + "u)";
   }
@@ -116,6 +125,10 @@ struct Gen {
     const std::uint32_t op = P.opnd[in.opnd + k];
     const std::uint32_t m = op >> kModeShift, i = op & kIndexMask;
     const std::uint8_t fl = P.oflag[in.opnd + k];
+    if (umode) {
+      if (m == tgc::kUv && i < P.uv_const_base) o << "      sG[" << i << "] += " << expr << ";\n";
+      return;
+    }
     if (m == tgc::kSlot && !gov.empty() && !gov[i].empty()) {
       const std::string cond = gcond.empty() ? "q == " + std::to_string(gj[i]) + "u" : gcond[i];
       o << "      if (" << cond << ") " << gov[i] << " += " << expr << ";\n";
@@ -134,7 +147,13 @@ struct Gen {
     }
   }
 
-  void check(const std::string& cond, const Instr& in) {
+  void check(const std::string& cond, const Instr& in, const std::string& bad) {
+    if (umode) {  // sample-invariant node: CTA 0 reports it like the interpreter's prologue
+      o << "      if (blockIdx.x == 0u && (" << cond << ")) { tg_err(err_key, 0ull, " << in.node
+        << "u); if (atomicCAS(A.err_op, 0xffffffffu, " << unsigned(in.op) << "u) == 0xffffffffu) *A.err_val = (double)("
+        << bad << "); }\n";
+      return;
+    }
     o << "      if (" << cond << ") tg_err(err_key, s, " << in.node << "u);\n";
   }
 
@@ -146,7 +165,7 @@ struct Gen {
     if (in.kind == tgc::kDense) { dense_fwd(P.dense[in.aux]); return; }
     if (in.kind == tgc::kGatherLoad) {
       const tgc::GatherTable& t = P.ugather[in.aux];
-      o << "      const T " << v(in.out) << " = UVg[cand[" << t.cand_off << "u + " << ix_expr(t) << "]];\n";
+      o << "      const T " << v(in.out) << " = UVt[cand[" << t.cand_off << "u + " << ix_expr(t) << "]];\n";
       return;
     }
     const std::uint32_t n = in.nops;
@@ -158,19 +177,19 @@ struct Gen {
       case Relu: o << out << a[0] << " > " << Z << " ? " << a[0] << " : " << Z << ";\n"; break;
       case Tanh: o << out << fn("tg_tanh", "tanhf") << "(" << a[0] << ");\n"; break;
       case Exp: o << out << fn("exp", "expf") << "(" << a[0] << ");\n"; break;
-      case NegLog: check("!(" + a[0] + " > (T)0)", in); o << out << "-" << fn("log", "logf") << "(" << a[0] << ");\n"; break;
+      case NegLog: check("!(" + a[0] + " > (T)0)", in, a[0]); o << out << "-" << fn("log", "logf") << "(" << a[0] << ");\n"; break;
       case Sigmoid: o << out << ONE << " / (" << ONE << " + " << fn("exp", "expf") << "(-" << a[0] << "));\n"; break;
-      case Inv: check(a[0] + " == (T)0", in); o << out << ONE << " / " << a[0] << ";\n"; break;
+      case Inv: check(a[0] + " == (T)0", in, a[0]); o << out << ONE << " / " << a[0] << ";\n"; break;
       case Sqr: o << out << a[0] << " * " << a[0] << ";\n"; break;
       case Cub: o << out << a[0] << " * " << a[0] << " * " << a[0] << ";\n"; break;
-      case Log: check("!(" + a[0] + " > (T)0)", in); o << out << fn("log", "logf") << "(" << a[0] << ");\n"; break;
-      case Sqrt: check("!(" + a[0] + " > (T)0)", in); o << out << fn("sqrt", "sqrtf") << "(" << a[0] << ");\n"; break;
-      case InvSqrt: check("!(" + a[0] + " > (T)0)", in); o << out << ONE << " / " << fn("sqrt", "sqrtf") << "(" << a[0] << ");\n"; break;
+      case Log: check("!(" + a[0] + " > (T)0)", in, a[0]); o << out << fn("log", "logf") << "(" << a[0] << ");\n"; break;
+      case Sqrt: check("!(" + a[0] + " > (T)0)", in, a[0]); o << out << fn("sqrt", "sqrtf") << "(" << a[0] << ");\n"; break;
+      case InvSqrt: check("!(" + a[0] + " > (T)0)", in, a[0]); o << out << ONE << " / " << fn("sqrt", "sqrtf") << "(" << a[0] << ");\n"; break;
       case MulByConst: o << out << a[0] << " * " << lit(in.cst, f64) << ";\n"; break;
       case Add: o << out << a[0] << " + " << a[1] << ";\n"; break;
       case Sub: o << out << a[0] << " - " << a[1] << ";\n"; break;
       case Mul: o << out << a[0] << " * " << a[1] << ";\n"; break;
-      case Div: check(a[1] + " == (T)0", in); o << out << a[0] << " / " << a[1] << ";\n"; break;
+      case Div: check(a[1] + " == (T)0", in, a[1]); o << out << a[0] << " / " << a[1] << ";\n"; break;
       case Mean: o << out << "(" << a[0] << " + " << a[1] << ") / " << TWO << ";\n"; break;
       case AddSquares: o << out << a[0] << " * " << a[0] << " + " << a[1] << " * " << a[1] << ";\n"; break;
       case MeanSquares: o << out << "(" << a[0] << " * " << a[0] << " + " << a[1] << " * " << a[1] << ") / " << TWO << ";\n"; break;
@@ -256,6 +275,7 @@ struct Gen {
   }
   std::string wexpr(const tgc::Dense& D, std::uint32_t k) const {
     const std::string idx = std::to_string(D.w_uv) + "u + j * " + std::to_string(D.n_in) + "u + " + std::to_string(k) + "u";
+    if (su) return "sU[" + idx + "]";
     return cfg.const_uv ? "cUV[" + idx + "]" : "UVg[" + idx + "]";
   }
   // Dense layer forward: loop over the outputs (static code O(n_in)),
@@ -280,7 +300,7 @@ struct Gen {
       return;
     }
     o << "#pragma unroll " << cfg.unroll_j << "\n      for (unsigned j = 0; j < " << D.n_out << "u; ++j) {\n";
-    if (D.b_uv != kNone) o << "        T z = " << (cfg.const_uv ? "cUV[" : "UVg[") << D.b_uv << "u + j];\n";
+    if (D.b_uv != kNone) o << "        T z = " << (su ? "sU[" : cfg.const_uv ? "cUV[" : "UVg[") << D.b_uv << "u + j];\n";
     else o << "        T z = (T)0;\n";
     for (std::uint32_t k = 0; k < D.n_in; ++k) o << "        z += " << x[k] << " * " << wexpr(D, k) << ";\n";
     if (vslot[D.out_row] >= 0) o << "        sV[(" << vslot[D.out_row] << "u + j) * " << ld << "u + col] = z;\n";
@@ -410,9 +430,214 @@ __device__ __forceinline__ int tg_ix(const int* __restrict__ idx, unsigned long 
   const int r = idx[at];
   return (unsigned)r < n ? r : 0;
 }
+// kernel argument block; host mirror: tgj::JitArgs<T> (tg_jit.hpp), same field order
+struct JitArgs {
+  const T* in; const int* idx; unsigned long long batch;
+  T* loss; T* igrad; T* partial; unsigned grid_rows; unsigned n_groups;
+  unsigned long long* err_key; double* err_val; unsigned* err_op;
+  const T* UVg; const unsigned* cand; const unsigned* toff; const TermC* terms;
+  const T* params; const T* consts; T* UVw;
+  unsigned* tickets; T* partial2;
+  T* grad_sum; T* gd_params; T gamma; T gd_batch;
+};
 )";
 
+const char* kArgAliases =
+    "  const T* __restrict__ in = A.in; const int* __restrict__ idx = A.idx; const unsigned long long batch = A.batch;\n"
+    "  T* __restrict__ loss = A.loss; T* __restrict__ igrad = A.igrad; T* __restrict__ partial = A.partial;\n"
+    "  const unsigned grid_rows = A.grid_rows; unsigned long long* err_key = A.err_key;\n"
+    "  const T* __restrict__ UVg = A.UVg; const unsigned* __restrict__ cand = A.cand;\n"
+    "  const unsigned* __restrict__ toff = A.toff; const TermC* __restrict__ terms = A.terms;\n"
+    "  (void)in; (void)idx; (void)loss; (void)igrad; (void)UVg; (void)cand; (void)toff; (void)terms; (void)err_key;\n";
+
 }  // namespace
+
+// ---------------------------------------------------------------------------
+// Fused prologue / generated epilogue (one module per program).
+//
+// Prologue: every CTA of tg_jit_tape stages UV = [params | uniform nodes |
+// consts] in shared memory (sU) and evaluates the uniform program there, as
+// straight-line code (block-parallel fixed-order sums for wide reductions).
+// That replaces the separate single-CTA k_uniform_fwd launch and its chain of
+// global round trips; the per-sample code reads uniform operands from sU.
+//
+// Epilogue (tg_jit_epi, same module): one warp per reduction destination sums
+// the per-CTA partials in a fixed order; the last CTA to finish runs the
+// uniform reverse sweep as straight-line code on shared memory, writes
+// grad_sum and applies GD.  Both kernels are launched with programmatic
+// stream serialisation, so each one's launch overlaps the tail of the kernel
+// before it (griddepcontrol.wait before the first dependent read).
+constexpr std::uint32_t kFuseMaxUv = 2048;
+
+bool wide_op(std::uint8_t op) {
+  return op == AddVarying || op == MeanVarying || op == NegativeMeanVarying || op == SumOfSquaresVarying ||
+         op == MeanSquaresVarying || op == InnerProductNoBias || op == InnerProductWithBias;
+}
+
+bool fusable(const tgc::Program& P, std::string& why) {
+  if (P.n_uv > kFuseMaxUv) { why = "uniform table too large to fuse"; return false; }
+  for (const auto* list : {&P.ufwd, &P.ubwd})
+    for (const Instr& in : *list) {
+      if (in.kind != tgc::kNode) { why = "uniform instruction kind"; return false; }
+      for (std::uint32_t j = 0; j < in.nops; ++j)
+        if ((P.opnd[in.opnd + j] >> kModeShift) != tgc::kUv) { why = "uniform operand mode"; return false; }
+    }
+  return true;
+}
+
+struct FuseCode {
+  std::string decl;   // file scope: operand lists, helpers
+  std::string pro;    // inside tg_jit_tape, after the argument aliases
+  std::string epi;    // the tg_jit_epi kernel
+};
+
+FuseCode fuse_code(const tgc::Program& P, const JitConfig& cfg, const std::string& launch_bounds) {
+  const bool f64 = P.dtype == TG_F64;
+  FuseCode fc;
+  std::vector<std::uint32_t> ops;   // operand uv lists of the wide uniform instructions
+  auto list = [&](const Instr& in) {
+    const std::size_t off = ops.size();
+    for (std::uint32_t j = 0; j < in.nops; ++j) ops.push_back(P.opnd[in.opnd + j] & kIndexMask);
+    return off;
+  };
+  const unsigned B = cfg.block;
+  const std::string NUV = std::to_string(std::max<std::uint32_t>(1, P.n_uv));
+  // ---- prologue ----
+  {
+    Gen U(P, cfg);
+    U.umode = true;
+    U.su = true;
+    std::ostringstream& o = U.o;
+    o << "  __shared__ T sU[" << NUV << "];\n  __shared__ T sRed_[32];\n  {\n"
+      << "    for (unsigned i = threadIdx.x; i < " << P.n_params << "u; i += " << B << "u) sU[i] = A.params[i];\n"
+      << "    for (unsigned i = threadIdx.x; i < " << P.n_uv - P.uv_const_base << "u; i += " << B << "u) sU["
+      << P.uv_const_base << "u + i] = A.consts[i];\n"
+      << "    __syncthreads();\n";
+    for (const Instr& in : P.ufwd) {
+      if (in.nops >= 64 && wide_op(in.op)) {
+        const std::size_t off = list(in);
+        const std::uint32_t n = in.nops;
+        const bool ip = in.op == InnerProductNoBias || in.op == InnerProductWithBias;
+        const std::uint32_t m = in.op == InnerProductWithBias ? (n - 1) / 2 : (ip ? n / 2 : n);
+        o << "    { T part = (T)0;\n"
+          << "      for (unsigned j = threadIdx.x; j < " << m << "u; j += " << B << "u) { const T v = sU[cUO[" << off
+          << "u + j]]; part += ";
+        if (ip) o << "v * sU[cUO[" << off + m << "u + j]]";
+        else if (in.op == SumOfSquaresVarying || in.op == MeanSquaresVarying) o << "v * v";
+        else o << "v";
+        o << "; }\n      part = tg_block_sum(part, sRed_);\n"
+          << "      if (threadIdx.x == 0) { T r = part;";
+        if (in.op == InnerProductWithBias) o << " r = sU[" << (P.opnd[in.opnd + n - 1] & kIndexMask) << "] + r;";
+        if (in.op == MeanVarying || in.op == MeanSquaresVarying) o << " r /= (T)" << n << ";";
+        if (in.op == NegativeMeanVarying) o << " r = -r / (T)" << n << ";";
+        o << " sU[" << in.out << "] = r; }\n      __syncthreads(); }\n";
+      } else {
+        o << "    if (threadIdx.x == 0) {\n";
+        U.forward(in);
+        o << "      sU[" << in.out << "] = " << U.v(in.out) << ";\n    }\n    __syncthreads();\n";
+      }
+    }
+    o << "    if (blockIdx.x == 0)  // UV for the epilogue and for diagnostics\n"
+      << "      for (unsigned i = threadIdx.x; i < " << P.n_uv << "u; i += " << B << "u) A.UVw[i] = sU[i];\n  }\n";
+    fc.pro = o.str();
+  }
+  // ---- epilogue kernel ----
+  {
+    const unsigned nd = static_cast<unsigned>(P.dest_uv.size());
+    Gen U(P, cfg);
+    U.umode = true;
+    U.su = true;
+    std::ostringstream& o = U.o;
+    o << "extern \"C\" __global__ void __launch_bounds__(256) tg_jit_epi(const JitArgs A) {\n"
+      << "  __shared__ T sU[" << NUV << "];\n  __shared__ T sG[" << NUV << "];\n  __shared__ unsigned last;\n"
+      << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");   // tg_jit_tape's partials / UV\n"
+      << "  const unsigned warp = (blockIdx.x * 256u + threadIdx.x) >> 5, lane = threadIdx.x & 31u;\n"
+      << "  if (warp < " << nd << "u) {\n"
+      << "    const T* row = A.partial + (unsigned long long)warp * A.grid_rows;\n"
+      << "    T t = (T)0;\n"
+      << "    unsigned c = lane;\n"
+      << "    for (; c + 224u < A.grid_rows; c += 256u) {  // 8 loads in flight, added in sequential order\n"
+      << "      T x[8];\n"
+      << "#pragma unroll\n"
+      << "      for (int u = 0; u < 8; ++u) x[u] = __ldcg(row + c + 32u * u);\n"
+      << "#pragma unroll\n"
+      << "      for (int u = 0; u < 8; ++u) t += x[u];\n"
+      << "    }\n"
+      << "    for (; c < A.grid_rows; c += 32u) t += __ldcg(row + c);\n"
+      << "    for (int m = 16; m > 0; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);\n"
+      << "    if (lane == 0) A.partial2[warp] = t;\n  }\n"
+      << "  __threadfence();\n  __syncthreads();\n"
+      << "  if (threadIdx.x == 0) last = atomicAdd(A.tickets, 1u) == gridDim.x - 1u;\n"
+      << "  __syncthreads();\n  if (!last) return;\n  __threadfence();\n"
+      << "  for (unsigned i = threadIdx.x; i < " << P.n_uv << "u; i += 256u) { sU[i] = __ldcg(A.UVw + i); sG[i] = (T)0; }\n"
+      << "  __syncthreads();\n"
+      << "  for (unsigned d = threadIdx.x; d < " << nd << "u; d += 256u) sG[cDU[d]] = __ldcg(A.partial2 + d);\n"
+      << "  if (threadIdx.x == 0) A.tickets[0] = 0u;\n"
+      << "  __syncthreads();\n";
+    if (P.root_uv != kNone) o << "  if (threadIdx.x == 0) sG[" << P.root_uv << "] += (T)A.batch;\n  __syncthreads();\n";
+    for (const Instr& in : P.ubwd) {
+      const bool par = (in.pad & 1) && in.nops >= 32 &&
+                       (in.op == AddVarying || in.op == SubVarying || in.op == MeanVarying || in.op == NegativeMeanVarying ||
+                        in.op == SumOfSquaresVarying || in.op == MeanSquaresVarying || in.op == InnerProductNoBias ||
+                        in.op == InnerProductWithBias);
+      if (par) {  // distinct children: one thread per child
+        const std::size_t off = list(in);
+        const std::uint32_t n = in.nops;
+        o << "  { const T g = sG[" << in.out << "];\n"
+          << "    for (unsigned j = threadIdx.x; j < " << n << "u; j += 256u) {\n"
+          << "      const unsigned u = cUO[" << off << "u + j];\n      T c;\n";
+        switch (in.op) {
+          case AddVarying: o << "      c = g;\n"; break;
+          case SubVarying: o << "      c = j == 0u ? g : -g;\n"; break;
+          case MeanVarying: o << "      c = g / (T)" << n << ";\n"; break;
+          case NegativeMeanVarying: o << "      c = -g / (T)" << n << ";\n"; break;
+          case SumOfSquaresVarying: o << "      c = g * (T)2 * sU[u];\n"; break;
+          case MeanSquaresVarying: o << "      c = (g * (T)2 / (T)" << n << ") * sU[u];\n"; break;
+          case InnerProductNoBias:
+            o << "      c = g * sU[cUO[" << off << "u + (j < " << n / 2 << "u ? j + " << n / 2 << "u : j - " << n / 2
+              << "u)]];\n";
+            break;
+          default: {
+            const std::uint32_t m = (n - 1) / 2;
+            o << "      c = j == " << n - 1 << "u ? g : g * sU[cUO[" << off << "u + (j < " << m << "u ? j + " << m
+              << "u : j - " << m << "u)]];\n";
+          }
+        }
+        o << "      if (u < " << P.uv_const_base << "u) sG[u] += c;\n    }\n    __syncthreads(); }\n";
+      } else {
+        o << "  if (threadIdx.x == 0) {\n";
+        U.reverse(in);
+        o << "  }\n  __syncthreads();\n";
+      }
+    }
+    o << "  for (unsigned i = threadIdx.x; i < " << P.n_params << "u; i += 256u) {\n"
+      << "    const T gs = sG[i];\n"
+      << "    if (A.grad_sum) A.grad_sum[i] = gs;\n"
+      << "    if (A.gd_params) A.gd_params[i] = A.gd_params[i] - A.gamma * gs / A.gd_batch;\n  }\n}\n";
+    fc.epi = o.str();
+    std::ostringstream d;
+    d << "__constant__ unsigned cDU[" << std::max(1u, nd) << "] = {";
+    for (unsigned i = 0; i < nd; ++i) d << (i ? ", " : "") << P.dest_uv[i] << "u";
+    d << "};\n";
+    fc.decl += d.str();
+  }
+  std::ostringstream d;
+  d << "__constant__ unsigned cUO[" << std::max<std::size_t>(1, ops.size()) << "] = {";
+  for (std::size_t i = 0; i < ops.size(); ++i) d << (i ? ", " : "") << ops[i] << "u";
+  d << "};\n"
+    << "__device__ __forceinline__ T tg_block_sum(T v, T* red) {  // fixed order; result in thread 0\n"
+    << "  for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);\n"
+    << "  __syncthreads();\n"
+    << "  if ((threadIdx.x & 31u) == 0) red[threadIdx.x >> 5] = v;\n"
+    << "  __syncthreads();\n"
+    << "  T t = (T)0;\n"
+    << "  if (threadIdx.x == 0) for (unsigned i = 0; i < (blockDim.x >> 5); ++i) t += red[i];\n"
+    << "  return t;\n}\n";
+  fc.decl += d.str();
+  (void)launch_bounds;
+  (void)f64;
+  return fc;
+}
 
 bool eligible(const tgc::Program& P) {
   return P.root_row != kNone && P.n_edges <= kMaxEdges && P.n_rows <= 4096;
@@ -422,6 +647,8 @@ std::string generate(const tgc::Program& P, const JitConfig& cfg, unsigned& n_cr
                      std::vector<tgc::Term>& terms_out, std::vector<std::uint32_t>& toff_out,
                      std::size_t& smem_elems) {
   Gen G(P, cfg);
+  G.su = cfg.fuse;
+  const FuseCode fc = cfg.fuse ? fuse_code(P, cfg, "") : FuseCode{};
   const bool f64 = P.dtype == TG_F64;
   const unsigned tile = cfg.block * cfg.spt;
   G.ld = tile + 1;
@@ -487,8 +714,8 @@ std::string generate(const tgc::Program& P, const JitConfig& cfg, unsigned& n_cr
   smem_elems = std::size_t(n_crow_g + n_crow_v) * ld + (dense ? nd + scratch : 0);
 
   std::ostringstream& o = G.o;
-  o << "typedef " << (f64 ? "double" : "float") << " T;\n" << kMath << kPrelude;
-  if (cfg.const_uv) o << "__constant__ T cUV[" << std::max<std::uint32_t>(1, P.n_uv) << "];\n";
+  o << "typedef " << (f64 ? "double" : "float") << " T;\n" << kMath << kPrelude << fc.decl;
+  if (cfg.const_uv && !cfg.fuse) o << "__constant__ T cUV[" << std::max<std::uint32_t>(1, P.n_uv) << "];\n";
   for (std::size_t bi = 0; bi < dbs.size(); ++bi) {
     const DB& b = dbs[bi];
     o << "__constant__ unsigned cDG" << bi << "[" << b.nj + b.nk << "] = {";
@@ -498,11 +725,10 @@ std::string generate(const tgc::Program& P, const JitConfig& cfg, unsigned& n_cr
   }
   o << "extern \"C\" __global__ void __launch_bounds__(" << cfg.block;
   if (cfg.min_blocks) o << ", " << cfg.min_blocks;
-  o << ") tg_jit_tape(\n"
-    << "    const T* __restrict__ in, const int* __restrict__ idx, unsigned long long batch,\n"
-    << "    T* __restrict__ loss, T* __restrict__ igrad, T* __restrict__ partial, unsigned grid_rows,\n"
-    << "    unsigned long long* err_key, const T* __restrict__ UVg, const unsigned* __restrict__ cand,\n"
-    << "    const unsigned* __restrict__ toff, const TermC* __restrict__ terms) {\n";
+  o << ") tg_jit_tape(const JitArgs A) {\n" << kArgAliases
+    << (cfg.fuse ? "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");   // params of the previous step\n" : "")
+    << fc.pro
+    << (cfg.fuse ? "  const T* __restrict__ UVt = sU;\n" : "  const T* __restrict__ UVt = UVg;\n") << "  (void)UVt;\n";
   o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
     << "  T* sG = reinterpret_cast<T*>(smem_raw);\n"
     << "  T* sV = sG + " << n_crow_g << " * " << ld << ";\n"
@@ -653,7 +879,7 @@ std::string generate(const tgc::Program& P, const JitConfig& cfg, unsigned& n_cr
   if (reg_acc && nd)
     o << "  for (int q = 0; q < " << ndpt << "; ++q) { const unsigned d = q * " << cfg.block << "u + tid;\n"
       << "    if (d < " << nd << "u) partial[(unsigned long long)d * grid_rows + blockIdx.x] = acc[q]; }\n";
-  o << "}\n";
+  o << "}\n" << fc.epi;
   return o.str();
 }
 
@@ -843,6 +1069,8 @@ std::string generate_grouped(const tgc::Program& P, const JitConfig& cfg, unsign
   spb = WPB * SPW;
 
   Gen Gn(P, cfg);
+  Gn.su = cfg.fuse;
+  const FuseCode fc = cfg.fuse ? fuse_code(P, cfg, "") : FuseCode{};
   Gn.vslot.assign(P.n_rows, -1);
   Gn.gslot.assign(P.n_rows, -1);
   Gn.vsm.assign(P.n_rows, 0);
@@ -859,15 +1087,14 @@ std::string generate_grouped(const tgc::Program& P, const JitConfig& cfg, unsign
     }
   std::ostringstream& o = Gn.o;
   const std::string Gs = std::to_string(G) + "u";
-  o << "typedef " << (f64 ? "double" : "float") << " T;\n" << kMath << kPrelude;
-  if (cfg.const_uv) o << "__constant__ T cUV[" << std::max<std::uint32_t>(1, P.n_uv) << "];\n";
+  o << "typedef " << (f64 ? "double" : "float") << " T;\n" << kMath << kPrelude << fc.decl;
+  if (cfg.const_uv && !cfg.fuse) o << "__constant__ T cUV[" << std::max<std::uint32_t>(1, P.n_uv) << "];\n";
   o << "extern \"C\" __global__ void __launch_bounds__(" << cfg.block;
   if (cfg.min_blocks) o << ", " << cfg.min_blocks;
-  o << ") tg_jit_tape(\n"
-    << "    const T* __restrict__ in, const int* __restrict__ idx, unsigned long long batch,\n"
-    << "    T* __restrict__ loss, T* __restrict__ igrad, T* __restrict__ partial, unsigned grid_rows,\n"
-    << "    unsigned long long* err_key, const T* __restrict__ UVg, const unsigned* __restrict__ cand,\n"
-    << "    const unsigned* __restrict__ toff, const TermC* __restrict__ terms) {\n"
+  o << ") tg_jit_tape(const JitArgs A) {\n" << kArgAliases
+    << (cfg.fuse ? "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");   // params of the previous step\n" : "")
+    << fc.pro
+    << (cfg.fuse ? "  const T* __restrict__ UVt = sU;\n" : "  const T* __restrict__ UVt = UVg;\n") << "  (void)UVt;\n"
     << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
     << "  T* sm = reinterpret_cast<T*>(smem_raw);\n"
     << "  T* sRed = sm + " << off + WPB * SPW * xs << "u;\n"
@@ -879,14 +1106,14 @@ std::string generate_grouped(const tgc::Program& P, const JitConfig& cfg, unsign
   for (const auto& g : gr) {
     const tgc::Dense& D = *g.D;
     o << "  for (unsigned e = tid; e < " << D.n_in * G << "u; e += " << cfg.block << "u) { const unsigned k = e / " << Gs
-      << ", j = e % " << Gs << "; sm[" << g.wf << "u + e] = j < " << D.n_out << "u ? UVg[" << D.w_uv << "u + j * "
+      << ", j = e % " << Gs << "; sm[" << g.wf << "u + e] = j < " << D.n_out << "u ? UVt[" << D.w_uv << "u + j * "
       << D.n_in << "u + k] : (T)0; }\n";
     if (g.xvec)
       o << "  for (unsigned e = tid; e < " << D.n_out * G << "u; e += " << cfg.block << "u) { const unsigned j = e / "
-        << Gs << ", k = e % " << Gs << "; sm[" << g.wb << "u + e] = k < " << D.n_in << "u ? UVg[" << D.w_uv
+        << Gs << ", k = e % " << Gs << "; sm[" << g.wb << "u + e] = k < " << D.n_in << "u ? UVt[" << D.w_uv
         << "u + j * " << D.n_in << "u + k] : (T)0; }\n";
     o << "  for (unsigned e = tid; e < " << Gs << "; e += " << cfg.block << "u) sm[" << g.bb << "u + e] = ";
-    if (D.b_uv != kNone) o << "e < " << D.n_out << "u ? UVg[" << D.b_uv << "u + e] : (T)0;\n";
+    if (D.b_uv != kNone) o << "e < " << D.n_out << "u ? UVt[" << D.b_uv << "u + e] : (T)0;\n";
     else o << "(T)0;\n";
   }
   o << "  for (unsigned e = tid; e < " << WPB * nd << "u; e += " << cfg.block << "u) sRed[e] = (T)0;\n"
@@ -1047,7 +1274,7 @@ std::string generate_grouped(const tgc::Program& P, const JitConfig& cfg, unsign
     << "  for (unsigned d = tid; d < " << nd << "u; d += " << cfg.block << "u) {\n"
     << "    T t = (T)0;\n"
     << "    for (unsigned w = 0; w < " << WPB << "u; ++w) t += sRed[w * " << nd << "u + d];\n"
-    << "    partial[(unsigned long long)d * grid_rows + blockIdx.x] = t;\n  }\n}\n";
+    << "    partial[(unsigned long long)d * grid_rows + blockIdx.x] = t;\n  }\n}\n" << fc.epi;
   return o.str();
 }
 
@@ -1127,6 +1354,8 @@ std::string generate_dmma(const tgc::Program& P, const JitConfig& cfg, unsigned&
       if (P.terms[u].f != kNone && rg[P.terms[u].f] >= 0) needv[P.terms[u].f] = 1;
 
   Gen Gn(P, cfg);
+  Gn.su = cfg.fuse;
+  const FuseCode fc = cfg.fuse ? fuse_code(P, cfg, "") : FuseCode{};
   Gn.vslot.assign(P.n_rows, -1);
   Gn.gslot.assign(P.n_rows, -1);
   Gn.vsm.assign(P.n_rows, 0);
@@ -1147,11 +1376,11 @@ std::string generate_dmma(const tgc::Program& P, const JitConfig& cfg, unsigned&
       Gn.gcond[r] = "c == " + std::to_string((j % 8) / 2) + "u";
     }
   std::ostringstream& o = Gn.o;
-  o << "typedef double T;\n" << kMath << kPrelude
+  o << "typedef double T;\n" << kMath << kPrelude << fc.decl
     << "__device__ __forceinline__ void tg_dmma(double& d0, double& d1, double a, double b) {\n"
     << "  asm(\"mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\"\n"
     << "      : \"+d\"(d0), \"+d\"(d1) : \"d\"(a), \"d\"(b));\n}\n";
-  if (cfg.const_uv) o << "__constant__ T cUV[" << std::max<std::uint32_t>(1, P.n_uv) << "];\n";
+  if (cfg.const_uv && !cfg.fuse) o << "__constant__ T cUV[" << std::max<std::uint32_t>(1, P.n_uv) << "];\n";
   for (std::size_t i = 0; i < ng; ++i) {
     if (!gr[i].has_bias()) continue;
     o << "__constant__ unsigned cBD" << i << "[" << gr[i].D->n_out << "] = {";
@@ -1165,11 +1394,10 @@ std::string generate_dmma(const tgc::Program& P, const JitConfig& cfg, unsigned&
   }
   o << "extern \"C\" __global__ void __launch_bounds__(" << cfg.block;
   if (cfg.min_blocks) o << ", " << cfg.min_blocks;
-  o << ") tg_jit_tape(\n"
-    << "    const T* __restrict__ in, const int* __restrict__ idx, unsigned long long batch,\n"
-    << "    T* __restrict__ loss, T* __restrict__ igrad, T* __restrict__ partial, unsigned grid_rows,\n"
-    << "    unsigned long long* err_key, const T* __restrict__ UVg, const unsigned* __restrict__ cand,\n"
-    << "    const unsigned* __restrict__ toff, const TermC* __restrict__ terms) {\n"
+  o << ") tg_jit_tape(const JitArgs A) {\n" << kArgAliases
+    << (cfg.fuse ? "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");   // params of the previous step\n" : "")
+    << fc.pro
+    << (cfg.fuse ? "  const T* __restrict__ UVt = sU;\n" : "  const T* __restrict__ UVt = UVg;\n") << "  (void)UVt;\n"
     << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
     << "  T* sm = reinterpret_cast<T*>(smem_raw);\n"
     << "  const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;\n"
@@ -1189,23 +1417,23 @@ std::string generate_dmma(const tgc::Program& P, const JitConfig& cfg, unsigned&
       << "    const unsigned n = 8u * u + (L >> 2), cc = L & 3u;\n";
     if (gr[i].xvec)
       o << "    const unsigned k = 8u * (t >> 1) + 2u * cc + (t & 1u);\n"
-        << "    sm[" << q.bf << "u + e] = (n < " << NO << " && k < " << NI << ") ? UVg[" << W << " + n * " << NI << " + k] : (T)0;\n";
+        << "    sm[" << q.bf << "u + e] = (n < " << NO << " && k < " << NI << ") ? UVt[" << W << " + n * " << NI << " + k] : (T)0;\n";
     else {
       o << "    const unsigned k = 4u * t + cc;\n"
         << "    T w = (T)0;\n"
-        << "    if (n < " << NO << ") { if (k < " << NI << ") w = UVg[" << W << " + n * " << NI << " + k];";
-      if (q.fb) o << " else if (k == " << NI << ") w = UVg[" << D.b_uv << "u + n];";
+        << "    if (n < " << NO << ") { if (k < " << NI << ") w = UVt[" << W << " + n * " << NI << " + k];";
+      if (q.fb) o << " else if (k == " << NI << ") w = UVt[" << D.b_uv << "u + n];";
       o << " }\n    sm[" << q.bf << "u + e] = w;\n";
     }
     o << "  }\n"
       << "  for (unsigned e = tid; e < " << 2 * q.ntO * q.ntX * 32 << "u; e += " << cfg.block << "u) {\n"
       << "    const unsigned t = e / " << q.ntX * 32 << "u, u = (e >> 5) % " << q.ntX << "u, L = e & 31u;\n"
       << "    const unsigned n = 8u * u + (L >> 2), k = 8u * (t >> 1) + 2u * (L & 3u) + (t & 1u);\n"
-      << "    sm[" << q.bk << "u + e] = (k < " << NO << " && n < " << NI << ") ? UVg[" << W << " + k * " << NI << " + n] : (T)0;\n"
+      << "    sm[" << q.bk << "u + e] = (k < " << NO << " && n < " << NI << ") ? UVt[" << W << " + k * " << NI << " + n] : (T)0;\n"
       << "  }\n";
     if (gr[i].xvec && q.fb)
       o << "  for (unsigned e = tid; e < " << 8 * q.ntO << "u; e += " << cfg.block << "u) sm[" << q.bb << "u + e] = e < "
-        << NO << " ? UVg[" << D.b_uv << "u + e] : (T)0;\n";
+        << NO << " ? UVt[" << D.b_uv << "u + e] : (T)0;\n";
   }
   o << "  for (unsigned e = tid; e < " << WPB * nd << "u; e += " << cfg.block << "u) sRed[e] = (T)0;\n"
     << "  __syncthreads();\n";
@@ -1215,13 +1443,23 @@ std::string generate_dmma(const tgc::Program& P, const JitConfig& cfg, unsigned&
         for (unsigned v = 0; v < ge[i].ntK; ++v)
           o << "  T aw" << i << "_" << u << "_" << v << "_0 = (T)0, aw" << i << "_" << u << "_" << v << "_1 = (T)0;\n";
   for (std::size_t e = 0; e < sdests.size(); ++e) o << "  T as" << e << " = (T)0;\n";
+  // inputs of the next 8-sample step are loaded at the top of the current one
+  // (register double buffer), so their latency hides behind a whole step
+  std::vector<std::uint32_t> incols;
+  for (const Instr& in : P.fwd)
+    if (in.kind == tgc::kInputLoad) incols.push_back(in.aux);
   o << "  const unsigned long long TW = (unsigned long long)gridDim.x * " << WPB << "u;\n"
-    << "  for (unsigned long long base = ((unsigned long long)blockIdx.x * " << WPB
-    << "u + warp) * 8u; base < batch; base += TW * 8u) {\n"
+    << "  unsigned long long base = ((unsigned long long)blockIdx.x * " << WPB << "u + warp) * 8u;\n"
+    << "  const unsigned long long s0 = base + g < batch ? base + g : batch - 1;\n";
+  for (std::uint32_t col : incols) o << "  T pf" << col << " = in[" << col << "ull * batch + s0];\n";
+  o << "  for (; base < batch; base += TW * 8u) {\n"
     << "    const unsigned long long sa = base + g;\n"
     << "    const bool active = sa < batch;\n"
-    << "    const unsigned long long s = active ? sa : batch - 1;\n"
-    << "    {\n";
+    << "    const unsigned long long s = active ? sa : batch - 1;\n";
+  for (std::uint32_t col : incols) o << "    const T in" << col << " = pf" << col << ";\n";
+  o << "    {\n      const unsigned long long sn = base + TW * 8u + g < batch ? base + TW * 8u + g : batch - 1;\n";
+  for (std::uint32_t col : incols) o << "      pf" << col << " = in[" << col << "ull * batch + sn];\n";
+  o << "    }\n    {\n";
   auto group_fwd = [&](std::size_t i) {
     const DenseGroup& G = gr[i];
     const tgc::Dense& D = *G.D;
@@ -1243,9 +1481,11 @@ std::string generate_dmma(const tgc::Program& P, const JitConfig& cfg, unsigned&
           if (k < D.n_in) return Gn.V(G.xr[k]);
           return (k == D.n_in && q.fb) ? "(T)1" : "(T)0";
         };
+        // lane c takes x[4t + c]: a chain of selects (a nested ?: becomes a jump table)
         a = "da" + std::to_string(Gn.tmp++);
-        o << "      const T " << a << " = c == 0u ? " << X(4 * t) << " : c == 1u ? " << X(4 * t + 1) << " : c == 2u ? "
-          << X(4 * t + 2) << " : " << X(4 * t + 3) << ";\n";
+        o << "      T " << a << " = " << X(4 * t + 3) << "; " << a << " = c == 2u ? " << X(4 * t + 2) << " : " << a << "; "
+          << a << " = c == 1u ? " << X(4 * t + 1) << " : " << a << "; " << a << " = c == 0u ? " << X(4 * t) << " : " << a
+          << ";\n";
       }
       for (unsigned u = 0; u < q.ntO; ++u)
         o << "      tg_dmma(" << nm("dz", i, u, 0) << ", " << nm("dz", i, u, 1) << ", " << a << ", sm["
@@ -1331,6 +1571,7 @@ std::string generate_dmma(const tgc::Program& P, const JitConfig& cfg, unsigned&
   };
   for (const Instr& in : P.fwd) {
     if (in.kind == tgc::kDense) group_fwd(in.aux);
+    else if (in.kind == tgc::kInputLoad) o << "      const T " << Gn.v(in.out) << " = in" << in.aux << ";\n";
     else Gn.forward(in);
   }
   o << "      if (loss && active && c == 0u) loss[s] = " << Gn.V(P.root_row) << ";\n";
@@ -1389,7 +1630,7 @@ std::string generate_dmma(const tgc::Program& P, const JitConfig& cfg, unsigned&
     << "  for (unsigned d = tid; d < " << nd << "u; d += " << cfg.block << "u) {\n"
     << "    T t = (T)0;\n"
     << "    for (unsigned w = 0; w < " << WPB << "u; ++w) t += sRed[w * " << nd << "u + d];\n"
-    << "    partial[(unsigned long long)d * grid_rows + blockIdx.x] = t;\n  }\n}\n";
+    << "    partial[(unsigned long long)d * grid_rows + blockIdx.x] = t;\n  }\n}\n" << fc.epi;
   return o.str();
 }
 
@@ -1411,6 +1652,13 @@ JitKernel build(const tgc::Program& P) {
   if (const char* e = std::getenv("TG_JIT_DLOOP")) cfg.dense_loop = std::atoi(e) != 0;
   std::vector<tgc::Term> terms;
   std::vector<std::uint32_t> toff;
+  // TG_JIT_FUSE=0 keeps the separate prologue / epilogue kernels
+  {
+    const char* fu = std::getenv("TG_JIT_FUSE");
+    std::string why;
+    cfg.fuse = !(fu && fu[0] == '0') && fusable(P, why);
+    if (cfg.fuse) cfg.const_uv = false;
+  }
   // specialised forms for dense-layer chains before the one-thread-per-sample form
   // form: TG_JIT_FORM = dmma | group | classic (default: first that applies, in that order)
   const char* fe = std::getenv("TG_JIT_FORM");
@@ -1472,8 +1720,11 @@ JitKernel build(const tgc::Program& P) {
     k.log = "nvrtcCreateProgram failed";
     return k;
   }
-  const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "--fmad=true"};
-  const nvrtcResult rc = nvrtcCompileProgram(prog, 4, opts);
+  // TG_JIT_VERBOSE=1: ptxas register / spill report in the compile log
+  const bool verbose = std::getenv("TG_JIT_VERBOSE") && std::getenv("TG_JIT_VERBOSE")[0] == '1';
+  const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "--fmad=true",
+                        "--diag-suppress=550,177", "--ptxas-options=-v"};
+  const nvrtcResult rc = nvrtcCompileProgram(prog, verbose ? 6 : 5, opts);
   std::size_t logn = 0;
   nvrtcGetProgramLogSize(prog, &logn);
   if (logn > 1) { k.log.resize(logn); nvrtcGetProgramLog(prog, k.log.data()); }
@@ -1488,7 +1739,7 @@ JitKernel build(const tgc::Program& P) {
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {  // compile-only (no GPU here)
     cudaGetLastError();
-    k.log = "compiled (" + std::to_string(cubin.size()) + " bytes cubin); no device to load it";
+    k.log += "compiled (" + std::to_string(cubin.size()) + " bytes cubin); no device to load it";
     return k;
   }
   if (cudaLibraryLoadData(&k.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess ||
@@ -1496,7 +1747,12 @@ JitKernel build(const tgc::Program& P) {
     k.log = std::string("library load failed: ") + cudaGetErrorString(cudaGetLastError());
     return k;
   }
-  if (cfg.const_uv && cudaLibraryGetGlobal(&k.cuv, &k.cuv_bytes, k.lib, "cUV") != cudaSuccess) {
+  if (k.cfg.fuse && cudaLibraryGetKernel(&k.fn_epi, k.lib, "tg_jit_epi") != cudaSuccess) {
+    k.log = "tg_jit_epi lookup failed";
+    return k;
+  }
+  k.fused = k.cfg.fuse;
+  if (k.cfg.const_uv && cudaLibraryGetGlobal(&k.cuv, &k.cuv_bytes, k.lib, "cUV") != cudaSuccess) {
     k.log = "cUV lookup failed";
     return k;
   }

@@ -28,6 +28,20 @@ struct JitConfig {
   unsigned min_blocks = 0;       // __launch_bounds__ minBlocksPerSM (0 = unset)
   unsigned unroll_j = 4;         // dense-layer output loop unroll (independent chains)
   bool dense_loop = false;       // dense layers as loops (rows in smem) vs unrolled (rows in registers)
+  bool fuse = false;             // prologue in the kernel + generated epilogue kernel (tg_jit_epi)
+};
+
+// Kernel argument block of tg_jit_tape, passed by value; the generated code
+// declares the same struct (tg_jit.cpp kPrelude), field for field.
+template <class T>
+struct JitArgs {
+  const T* in; const int* idx; unsigned long long batch;
+  T* loss; T* igrad; T* partial; unsigned grid_rows; unsigned n_groups;
+  unsigned long long* err_key; double* err_val; unsigned* err_op;
+  const T* UVg; const unsigned* cand; const unsigned* toff; const void* terms;
+  const T* params; const T* consts; T* UVw;      // fused prologue: each CTA evaluates the uniform program
+  unsigned* tickets; T* partial2;                // fused epilogue: two-level last-CTA reduction
+  T* grad_sum; T* gd_params; T gamma; T gd_batch;
 };
 
 struct JitKernel {
@@ -36,6 +50,7 @@ struct JitKernel {
   std::string source;
   cudaLibrary_t lib = nullptr;
   cudaKernel_t fn = nullptr;
+  cudaKernel_t fn_epi = nullptr;  // generated epilogue (fused programs)
   void* cuv = nullptr;           // __constant__ table address (const_uv)
   std::size_t cuv_bytes = 0;
   JitConfig cfg;
@@ -43,6 +58,7 @@ struct JitKernel {
   unsigned group = 0;            // lanes per sample (grouped form), 0 = one thread per sample
   std::string group_log;         // why the dmma / grouped form was not used
   std::string form;              // "dmma" | "group" | "classic"
+  bool fused = false;            // prologue + epilogue (+ GD) inside the kernel: one launch per step
   std::size_t smem_bytes = 0;    // contraction rows
   unsigned n_crow_g = 0, n_crow_v = 0;
   int occ = 0;

@@ -102,14 +102,19 @@ __global__ void __launch_bounds__(kBlock) k_finalize(UniformArgs<T> a) {
 template <class T>
 __global__ void __launch_bounds__(kBlock) k_uniform_fwd(UniformArgs<T> a) {
   __shared__ T red[kBlock];
+  // small tables (a.smem): the uniform program runs on a shared-memory copy of
+  // UV (each instruction is a few shared-memory round trips, not global ones)
+  extern __shared__ __align__(16) unsigned char dyn[];
+  T* V = a.smem ? reinterpret_cast<T*>(dyn) : a.UV;
   if (a.copy) {
-    for (std::uint32_t i = threadIdx.x; i < a.n_params; i += kBlock) a.UV[i] = a.params[i];
-    for (std::uint32_t i = threadIdx.x; i < a.n_const; i += kBlock) a.UV[a.const_base + i] = a.consts[i];
-    for (std::uint32_t i = threadIdx.x; i < a.n_uv; i += kBlock) a.UG[i] = T(0);
+    for (std::uint32_t i = threadIdx.x; i < a.n_params; i += kBlock) V[i] = a.params[i];
+    for (std::uint32_t i = threadIdx.x; i < a.n_const; i += kBlock) V[a.const_base + i] = a.consts[i];
+    if (!a.smem)  // the smem epilogue reads only the reduced entries of UG
+      for (std::uint32_t i = threadIdx.x; i < a.n_uv; i += kBlock) a.UG[i] = T(0);
     if (threadIdx.x == 0 && a.done) *a.done = 0u;
   }
   __syncthreads();
-  UvAcc<T> acc{a.UV, a.UG, nullptr, a.const_base};
+  UvAcc<T> acc{V, a.UG, nullptr, a.const_base};
   for (std::uint32_t k = 0; k < a.n_instr; ++k) {
     const Instr in = a.instr[k];
     const std::uint32_t* o = a.opnd + in.opnd;
@@ -119,23 +124,23 @@ __global__ void __launch_bounds__(kBlock) k_uniform_fwd(UniformArgs<T> a) {
       const std::uint32_t m = in.op == InnerProductWithBias ? (n - 1) / 2 : (ip ? n / 2 : n);
       T part = 0;
       for (std::uint32_t j = threadIdx.x; j < m; j += kBlock) {
-        const T v = a.UV[o[j] & kIndexMask];
-        if (ip) part += v * a.UV[o[m + j] & kIndexMask];
+        const T v = V[o[j] & kIndexMask];
+        if (ip) part += v * V[o[m + j] & kIndexMask];
         else if (in.op == SumOfSquaresVarying || in.op == MeanSquaresVarying) part += v * v;
         else part += v;
       }
       T s = block_sum(part, red);
       if (threadIdx.x == 0) {
-        if (in.op == InnerProductWithBias) s = a.UV[o[n - 1] & kIndexMask] + s;
+        if (in.op == InnerProductWithBias) s = V[o[n - 1] & kIndexMask] + s;
         if (in.op == MeanVarying || in.op == MeanSquaresVarying) s /= static_cast<T>(n);
         if (in.op == NegativeMeanVarying) s = -s / static_cast<T>(n);
-        a.UV[in.out] = s;
+        V[in.out] = s;
       }
     } else if (threadIdx.x == 0) {
       acc.o = o;
       bool bad = false;
       T badv = 0;
-      a.UV[in.out] = eval_node<T>(in.op, in.nops, o, in.cst, acc, bad, badv);
+      V[in.out] = eval_node<T>(in.op, in.nops, o, in.cst, acc, bad, badv);
       if (bad) {
         record_error(a.err_key, 0, in.node);
         if (*a.err_op == 0xffffffffu) { *a.err_op = in.op; *a.err_val = static_cast<double>(badv); }
@@ -143,8 +148,11 @@ __global__ void __launch_bounds__(kBlock) k_uniform_fwd(UniformArgs<T> a) {
     }
     __syncthreads();
   }
-  if (a.UVc)  // mirror into the specialised kernel's __constant__ table
-    for (std::uint32_t i = threadIdx.x; i < a.n_uv; i += kBlock) a.UVc[i] = a.UV[i];
+  for (std::uint32_t i = threadIdx.x; i < a.n_uv; i += kBlock) {
+    const T v = V[i];
+    if (a.smem) a.UV[i] = v;
+    if (a.UVc) a.UVc[i] = v;   // mirror into the specialised kernel's __constant__ table
+  }
 }
 
 template <class T>
@@ -168,22 +176,38 @@ __global__ void __launch_bounds__(kBlock) k_reduce_epilogue(ReduceArgs<T> r, Uni
   if (!last) return;
   __threadfence();
   // ---- uniform reverse sweep (last CTA) ----
-  if (threadIdx.x == 0 && a.root_uv != tgc::kNone) a.UG[a.root_uv] += static_cast<T>(a.batch);
+  // small tables (a.smem): on shared-memory copies of UV / UG; UG starts from
+  // the reduced destinations only (the prologue does not zero it)
+  extern __shared__ __align__(16) unsigned char dyn[];
+  T* V = a.UV;
+  T* G = a.UG;
+  if (a.smem) {
+    V = reinterpret_cast<T*>(dyn);
+    G = V + a.n_uv;
+    for (std::uint32_t i = threadIdx.x; i < a.n_uv; i += kBlock) {
+      V[i] = a.UV[i];
+      G[i] = T(0);
+    }
+    __syncthreads();
+    for (std::uint32_t d = threadIdx.x; d < r.n_dest; d += kBlock) G[r.dest_uv[d]] = a.UG[r.dest_uv[d]];
+  }
   __syncthreads();
-  UvAcc<T> acc{a.UV, a.UG, nullptr, a.const_base};
+  if (threadIdx.x == 0 && a.root_uv != tgc::kNone) G[a.root_uv] += static_cast<T>(a.batch);
+  __syncthreads();
+  UvAcc<T> acc{V, G, nullptr, a.const_base};
   for (std::uint32_t k = 0; k < a.n_instr; ++k) {
     const Instr in = a.instr[k];
     const std::uint32_t* o = a.opnd + in.opnd;
-    const T g = a.UG[in.out];
-    const T y = a.UV[in.out];
+    const T g = G[in.out];
+    const T y = V[in.out];
     T dummy;
-    const bool parallel = (in.pad & 1) && in.nops >= 32 && child_rule<T>(in.op, in.nops, 0, o, a.UV, g, dummy);
+    const bool parallel = (in.pad & 1) && in.nops >= 32 && child_rule<T>(in.op, in.nops, 0, o, V, g, dummy);
     if (parallel) {  // distinct children: one thread per child
       for (std::uint32_t j = threadIdx.x; j < in.nops; j += kBlock) {
         T c;
-        child_rule<T>(in.op, in.nops, j, o, a.UV, g, c);
+        child_rule<T>(in.op, in.nops, j, o, V, g, c);
         const std::uint32_t u = o[j] & kIndexMask;
-        if (u < a.const_base) a.UG[u] += c;
+        if (u < a.const_base) G[u] += c;
       }
     } else if (threadIdx.x == 0) {
       acc.o = o;
@@ -194,24 +218,26 @@ __global__ void __launch_bounds__(kBlock) k_reduce_epilogue(ReduceArgs<T> r, Uni
   // ---- grad_sum and the fused GD update (large vectors: k_finalize) ----
   if (!a.copy) return;
   for (std::uint32_t i = threadIdx.x; i < a.n_params; i += kBlock) {
-    const T gsum = a.UG[i];
+    const T gsum = G[i];
     if (a.grad_sum) a.grad_sum[i] = gsum;
     if (a.gd_params) a.gd_params[i] = a.gd_params[i] - a.gamma * gsum / a.gd_batch;
   }
 }
 
 constexpr std::uint32_t kGridCopy = 1u << 16;   // above this many entries, copies run grid-wide
+constexpr std::uint32_t kSmemUV = 3072;         // up to this many entries, UV / UG are staged in shared memory
 
 template <class T>
 cudaError_t launch_uniform_fwd(const UniformArgs<T>& a, cudaStream_t st, std::uint64_t& launches) {
   UniformArgs<T> b = a;
   b.copy = a.n_uv <= kGridCopy;
+  b.smem = a.n_uv <= kSmemUV;
   if (!b.copy) {
     k_uv_init<T><<<std::min<std::uint32_t>(592, (a.n_uv + kBlock - 1) / kBlock), kBlock, 0, st>>>(a);
     ++launches;
     if (a.n_instr == 0 && !a.UVc) return cudaGetLastError();
   }
-  k_uniform_fwd<T><<<1, kBlock, 0, st>>>(b);
+  k_uniform_fwd<T><<<1, kBlock, b.smem ? a.n_uv * sizeof(T) : 0, st>>>(b);
   ++launches;
   return cudaGetLastError();
 }
@@ -223,7 +249,8 @@ cudaError_t launch_reduce_epilogue(const ReduceArgs<T>& r, const UniformArgs<T>&
   const unsigned grid = r.n_dest ? (r.n_dest + warps_per_block - 1) / warps_per_block : 1;
   UniformArgs<T> b = a;
   b.copy = a.n_params <= kGridCopy;
-  k_reduce_epilogue<T><<<grid, kBlock, 0, st>>>(r, b);
+  b.smem = a.n_uv <= kSmemUV;
+  k_reduce_epilogue<T><<<grid, kBlock, b.smem ? 2 * a.n_uv * sizeof(T) : 0, st>>>(r, b);
   ++launches;
   if (!b.copy) {
     k_finalize<T><<<std::min<std::uint32_t>(592, (a.n_params + kBlock - 1) / kBlock), kBlock, 0, st>>>(b);

@@ -30,6 +30,7 @@ struct UniformArgs {
   std::size_t batch;
   std::uint32_t n_instr, n_params, n_const, const_base, n_uv, root_uv;
   int copy;                  // set by the launchers: copies done inside the single-CTA kernels
+  int smem;                  // set by the launchers: UV / UG staged in shared memory (small tables)
 };
 
 template <class T>
