@@ -147,14 +147,21 @@ def test_workspace_size_is_bounded_and_monotone():
     assert 0 < a <= b < 64 << 20
 
 
-def test_jit_source_compiles_with_nvrtc():
-    """The register-resident specialisation is generated and compiled (NVRTC,
-    sm_100a) without a device; only loading needs the GPU."""
+@pytest.mark.parametrize("form,marker", [("dmma", "mma.sync.aligned.m8n8k4.row.col.f64"),
+                                         ("group", "lane & 15u"),
+                                         ("classic", "dense weight gradient 16x16")])
+def test_jit_source_compiles_with_nvrtc(form, marker, monkeypatch):
+    """The specialised kernels are generated and compiled (NVRTC, sm_100a)
+    without a device; only loading needs the GPU.  cfg2's dense chain takes the
+    FP64 tensor-core form by default; the fused module carries the uniform
+    prologue in tg_jit_tape and the generated epilogue kernel tg_jit_epi."""
+    monkeypatch.setenv("TG_JIT_FORM", form)
     p = tg.Program(tg.build_model("moons"))
     src, log, ms = ctypes.c_char_p(), ctypes.c_char_p(), ctypes.c_double()
     st = _lib.lib.tg_program_jit(p._h, ctypes.byref(src), ctypes.byref(log), ctypes.byref(ms))
     text = src.value.decode()
-    assert "tg_jit_tape" in text and "dense weight gradient 16x16" in text
+    assert "tg_jit_tape" in text and marker in text
+    assert "tg_jit_epi" in text and "griddepcontrol.wait" in text
     assert "compiled" in log.value.decode() or st == 0, log.value
 
 

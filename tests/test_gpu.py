@@ -384,3 +384,44 @@ def test_pipeline_host_buffers_equal_device_steps(model, pinned, b):
     assert torch.equal(P1, P2)
     for (xh, kh, lh), w in zip(host, want):
         assert torch.equal(lh, w)
+
+
+@pytest.mark.parametrize("form", ["dmma", "group", "classic"])
+@pytest.mark.parametrize("fuse", ["1", "0"])
+@pytest.mark.parametrize("name,dt,b", [("moons", "f64", 64), ("listing1", "f64", 64), ("fig1", "f64", 64),
+                                       ("moons", "f64", 3001), ("moons", "f32", 3001)])
+def test_jit_forms_vs_reference(form, fuse, name, dt, b, monkeypatch):
+    """Every specialised form (FP64 DMMA, grouped lanes-per-sample, one thread
+    per sample), with the fused prologue / generated epilogue and without,
+    against the reference's golden outputs (b = 64) or the oracle (larger,
+    ragged batches; fp32).  Forms that do not apply to a tape fall back to the
+    next one; all must match.  The fused GD step equals forward_backward +
+    gd_update bit for bit."""
+    monkeypatch.setenv("TG_JIT_FORM", form)
+    monkeypatch.setenv("TG_JIT_FUSE", fuse)
+    desc = tg.build_model(name, None, dt, seed=5).describe()
+    x, k = tg.synth_batch(name, None, dt, seed=77, batch=b, n_inputs=desc.n_inputs, n_index=desc.n_index_inputs)
+    prog = make_prog(desc, "jit")
+    L, IG, G = run(prog, desc, x, k, desc.param_values(), b)
+    assert prog.info["storage"] == 2
+    tol = TOL[dt]
+    if b == 64 and dt == "f64":
+        want = (GOLDEN[f"w_{name}_loss"], GOLDEN[f"w_{name}_input_grad"][:desc.n_inputs], GOLDEN[f"w_{name}_grad_sum"])
+    else:
+        r = oracle.run(desc, x.astype(np.float64), k, desc.param_values())
+        want = (r["loss"], r["input_grad"][:desc.n_inputs], r["grad_sum"])
+    assert close_rel(L, want[0], tol), rel(L, want[0])
+    if desc.n_inputs:
+        assert rel(IG, want[1]) <= tol
+    assert rel(G, want[2]) <= tol
+    P1 = torch.tensor(desc.param_values(), device="cuda", dtype=tdtype(dt))
+    P2 = P1.clone()
+    X = torch.tensor(x, device="cuda", dtype=tdtype(dt))
+    Lt = torch.zeros(b, device="cuda", dtype=tdtype(dt))
+    Gt = torch.zeros(desc.n_params, device="cuda", dtype=tdtype(dt))
+    W = prog.alloc_workspace(b)
+    prog.train_step(X, None, b, P1, Lt, Gt, 0.05, W)
+    prog.forward_backward(X, None, b, P2, Lt, None, Gt, W)
+    prog.gd_update(P2, Gt, 0.05, b)
+    torch.cuda.synchronize()
+    assert torch.equal(P1, P2)
