@@ -696,8 +696,9 @@ cudaError_t launch_pdl(cudaKernel_t fn, unsigned grid, unsigned block, std::size
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
+  static const bool pdl = !(std::getenv("TG_PDL") && std::getenv("TG_PDL")[0] == '0');
   lc.attrs = at;
-  lc.numAttrs = 1;
+  lc.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelExC(&lc, reinterpret_cast<const void*>(fn), args);
 }
 

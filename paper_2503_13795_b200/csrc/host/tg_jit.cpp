@@ -486,19 +486,28 @@ bool fusable(const tgc::Program& P, std::string& why) {
 }
 
 struct FuseCode {
-  std::string decl;   // file scope: operand lists, helpers
-  std::string pro;    // inside tg_jit_tape, after the argument aliases
-  std::string epi;    // the tg_jit_epi kernel
+  std::string decl;       // file scope: operand lists, helpers
+  std::string pro_load;   // inside tg_jit_tape: params / consts -> sU (loads in flight, no barrier)
+  std::string pro_prog;   // barrier, then the uniform program on sU
+  std::string pro;        // pro_load + pro_prog
+  std::string epi;        // the tg_jit_epi kernel
 };
 
 FuseCode fuse_code(const tgc::Program& P, const JitConfig& cfg, const std::string& launch_bounds) {
   const bool f64 = P.dtype == TG_F64;
   FuseCode fc;
-  std::vector<std::uint32_t> ops;   // operand uv lists of the wide uniform instructions
-  auto list = [&](const Instr& in) {
+  // operand uv lists of the wide uniform instructions, read one per thread: a
+  // contiguous run is indexed directly, anything else comes from a __device__
+  // table (coalesced; a __constant__ table would serialise divergent reads)
+  std::vector<std::uint32_t> ops;
+  auto opx = [&](const Instr& in, const std::string& j) -> std::string {
+    const std::uint32_t o0 = P.opnd[in.opnd] & kIndexMask;
+    bool run = true;
+    for (std::uint32_t k = 1; k < in.nops && run; ++k) run = (P.opnd[in.opnd + k] & kIndexMask) == o0 + k;
+    if (run) return "(" + std::to_string(o0) + "u + (" + j + "))";
     const std::size_t off = ops.size();
-    for (std::uint32_t j = 0; j < in.nops; ++j) ops.push_back(P.opnd[in.opnd + j] & kIndexMask);
-    return off;
+    for (std::uint32_t k = 0; k < in.nops; ++k) ops.push_back(P.opnd[in.opnd + k] & kIndexMask);
+    return "gUO[" + std::to_string(off) + "u + (" + j + ")]";
   };
   const unsigned B = cfg.block;
   const std::string NUV = std::to_string(std::max<std::uint32_t>(1, P.n_uv));
@@ -508,21 +517,22 @@ FuseCode fuse_code(const tgc::Program& P, const JitConfig& cfg, const std::strin
     U.umode = true;
     U.su = true;
     std::ostringstream& o = U.o;
-    o << "  __shared__ T sU[" << NUV << "];\n  __shared__ T sRed_[32];\n  {\n"
-      << "    for (unsigned i = threadIdx.x; i < " << P.n_params << "u; i += " << B << "u) sU[i] = A.params[i];\n"
-      << "    for (unsigned i = threadIdx.x; i < " << P.n_uv - P.uv_const_base << "u; i += " << B << "u) sU["
-      << P.uv_const_base << "u + i] = A.consts[i];\n"
-      << "    __syncthreads();\n";
+    fc.pro_load = "  __shared__ T sU[" + NUV + "];\n  __shared__ T sRed_[32];\n"
+      "  for (unsigned i = threadIdx.x; i < " + std::to_string(P.n_params) + "u; i += " + std::to_string(B) +
+      "u) sU[i] = A.params[i];\n"
+      "  for (unsigned i = threadIdx.x; i < " + std::to_string(P.n_uv - P.uv_const_base) + "u; i += " +
+      std::to_string(B) + "u) sU[" + std::to_string(P.uv_const_base) + "u + i] = A.consts[i];\n";
+    o << "  __syncthreads();\n  {\n";
     for (const Instr& in : P.ufwd) {
       if (in.nops >= 64 && wide_op(in.op)) {
-        const std::size_t off = list(in);
         const std::uint32_t n = in.nops;
         const bool ip = in.op == InnerProductNoBias || in.op == InnerProductWithBias;
         const std::uint32_t m = in.op == InnerProductWithBias ? (n - 1) / 2 : (ip ? n / 2 : n);
+        const std::string xo = opx(in, "j"), yo = ip ? opx(in, std::to_string(m) + "u + j") : std::string();
         o << "    { T part = (T)0;\n"
-          << "      for (unsigned j = threadIdx.x; j < " << m << "u; j += " << B << "u) { const T v = sU[cUO[" << off
-          << "u + j]]; part += ";
-        if (ip) o << "v * sU[cUO[" << off + m << "u + j]]";
+          << "      for (unsigned j = threadIdx.x; j < " << m << "u; j += " << B << "u) { const T v = sU[" << xo
+          << "]; part += ";
+        if (ip) o << "v * sU[" << yo << "]";
         else if (in.op == SumOfSquaresVarying || in.op == MeanSquaresVarying) o << "v * v";
         else o << "v";
         o << "; }\n      part = tg_block_sum(part, sRed_);\n"
@@ -539,7 +549,8 @@ FuseCode fuse_code(const tgc::Program& P, const JitConfig& cfg, const std::strin
     }
     o << "    if (blockIdx.x == 0)  // UV for the epilogue and for diagnostics\n"
       << "      for (unsigned i = threadIdx.x; i < " << P.n_uv << "u; i += " << B << "u) A.UVw[i] = sU[i];\n  }\n";
-    fc.pro = o.str();
+    fc.pro_prog = o.str();
+    fc.pro = fc.pro_load + fc.pro_prog;
   }
   // ---- epilogue kernel ----
   {
@@ -555,15 +566,13 @@ FuseCode fuse_code(const tgc::Program& P, const JitConfig& cfg, const std::strin
       << "  if (warp < " << nd << "u) {\n"
       << "    const T* row = A.partial + (unsigned long long)warp * A.grid_rows;\n"
       << "    T t = (T)0;\n"
-      << "    unsigned c = lane;\n"
-      << "    for (; c + 224u < A.grid_rows; c += 256u) {  // 8 loads in flight, added in sequential order\n"
-      << "      T x[8];\n"
+      << "    for (unsigned c = lane; c < A.grid_rows; c += 512u) {  // 16 loads in flight, added in sequential order\n"
+      << "      T x[16];\n"
       << "#pragma unroll\n"
-      << "      for (int u = 0; u < 8; ++u) x[u] = __ldcg(row + c + 32u * u);\n"
+      << "      for (int u = 0; u < 16; ++u) x[u] = c + 32u * u < A.grid_rows ? __ldcg(row + c + 32u * u) : (T)0;\n"
       << "#pragma unroll\n"
-      << "      for (int u = 0; u < 8; ++u) t += x[u];\n"
+      << "      for (int u = 0; u < 16; ++u) if (c + 32u * u < A.grid_rows) t += x[u];\n"
       << "    }\n"
-      << "    for (; c < A.grid_rows; c += 32u) t += __ldcg(row + c);\n"
       << "    for (int m = 16; m > 0; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);\n"
       << "    if (lane == 0) A.partial2[warp] = t;\n  }\n"
       << "  __threadfence();\n  __syncthreads();\n"
@@ -571,7 +580,7 @@ FuseCode fuse_code(const tgc::Program& P, const JitConfig& cfg, const std::strin
       << "  __syncthreads();\n  if (!last) return;\n  __threadfence();\n"
       << "  for (unsigned i = threadIdx.x; i < " << P.n_uv << "u; i += 256u) { sU[i] = __ldcg(A.UVw + i); sG[i] = (T)0; }\n"
       << "  __syncthreads();\n"
-      << "  for (unsigned d = threadIdx.x; d < " << nd << "u; d += 256u) sG[cDU[d]] = __ldcg(A.partial2 + d);\n"
+      << "  for (unsigned d = threadIdx.x; d < " << nd << "u; d += 256u) sG[gDU[d]] = __ldcg(A.partial2 + d);\n"
       << "  if (threadIdx.x == 0) A.tickets[0] = 0u;\n"
       << "  __syncthreads();\n";
     if (P.root_uv != kNone) o << "  if (threadIdx.x == 0) sG[" << P.root_uv << "] += (T)A.batch;\n  __syncthreads();\n";
@@ -581,11 +590,11 @@ FuseCode fuse_code(const tgc::Program& P, const JitConfig& cfg, const std::strin
                         in.op == SumOfSquaresVarying || in.op == MeanSquaresVarying || in.op == InnerProductNoBias ||
                         in.op == InnerProductWithBias);
       if (par) {  // distinct children: one thread per child
-        const std::size_t off = list(in);
         const std::uint32_t n = in.nops;
+        const std::string uo = opx(in, "j");
         o << "  { const T g = sG[" << in.out << "];\n"
           << "    for (unsigned j = threadIdx.x; j < " << n << "u; j += 256u) {\n"
-          << "      const unsigned u = cUO[" << off << "u + j];\n      T c;\n";
+          << "      const unsigned u = " << uo << ";\n      T c;\n";
         switch (in.op) {
           case AddVarying: o << "      c = g;\n"; break;
           case SubVarying: o << "      c = j == 0u ? g : -g;\n"; break;
@@ -594,13 +603,14 @@ FuseCode fuse_code(const tgc::Program& P, const JitConfig& cfg, const std::strin
           case SumOfSquaresVarying: o << "      c = g * (T)2 * sU[u];\n"; break;
           case MeanSquaresVarying: o << "      c = (g * (T)2 / (T)" << n << ") * sU[u];\n"; break;
           case InnerProductNoBias:
-            o << "      c = g * sU[cUO[" << off << "u + (j < " << n / 2 << "u ? j + " << n / 2 << "u : j - " << n / 2
-              << "u)]];\n";
+            o << "      c = g * sU[" << opx(in, "j < " + std::to_string(n / 2) + "u ? j + " + std::to_string(n / 2) + "u : j - " +
+                                       std::to_string(n / 2) + "u") << "];\n";
             break;
           default: {
             const std::uint32_t m = (n - 1) / 2;
-            o << "      c = j == " << n - 1 << "u ? g : g * sU[cUO[" << off << "u + (j < " << m << "u ? j + " << m
-              << "u : j - " << m << "u)]];\n";
+            o << "      c = j == " << n - 1 << "u ? g : g * sU[" << opx(in, "j < " + std::to_string(m) + "u ? j + " +
+                                                                           std::to_string(m) + "u : j - " + std::to_string(m) + "u")
+              << "];\n";
           }
         }
         o << "      if (u < " << P.uv_const_base << "u) sG[u] += c;\n    }\n    __syncthreads(); }\n";
@@ -616,13 +626,13 @@ FuseCode fuse_code(const tgc::Program& P, const JitConfig& cfg, const std::strin
       << "    if (A.gd_params) A.gd_params[i] = A.gd_params[i] - A.gamma * gs / A.gd_batch;\n  }\n}\n";
     fc.epi = o.str();
     std::ostringstream d;
-    d << "__constant__ unsigned cDU[" << std::max(1u, nd) << "] = {";
+    d << "__device__ const unsigned gDU[" << std::max(1u, nd) << "] = {";
     for (unsigned i = 0; i < nd; ++i) d << (i ? ", " : "") << P.dest_uv[i] << "u";
     d << "};\n";
     fc.decl += d.str();
   }
   std::ostringstream d;
-  d << "__constant__ unsigned cUO[" << std::max<std::size_t>(1, ops.size()) << "] = {";
+  d << "__device__ const unsigned gUO[" << std::max<std::size_t>(1, ops.size()) << "] = {";
   for (std::size_t i = 0; i < ops.size(); ++i) d << (i ? ", " : "") << ops[i] << "u";
   d << "};\n"
     << "__device__ __forceinline__ T tg_block_sum(T v, T* red) {  // fixed order; result in thread 0\n"
@@ -1071,6 +1081,20 @@ std::string generate_grouped(const tgc::Program& P, const JitConfig& cfg, unsign
   Gen Gn(P, cfg);
   Gn.su = cfg.fuse;
   const FuseCode fc = cfg.fuse ? fuse_code(P, cfg, "") : FuseCode{};
+  // where the layer tables are staged from: params / consts straight from
+  // global (those loads overlap sU's), uniform nodes from sU after the program
+  auto tsrc = [&](std::uint32_t uv0, std::uint32_t cnt) -> std::string {
+    if (!cfg.fuse) return "UVg[";
+    if (uv0 + cnt <= P.n_params) return "A.params[";
+    if (uv0 >= P.uv_const_base) return "(A.consts - " + std::to_string(P.uv_const_base) + ")[";
+    return "sU[";
+  };
+  bool late = false;
+  for (const auto& D : P.dense) {
+    late = late || tsrc(D.w_uv, D.n_out * D.n_in) == "sU[";
+    if (D.b_uv != kNone) late = late || tsrc(D.b_uv, D.n_out) == "sU[";
+  }
+
   Gn.vslot.assign(P.n_rows, -1);
   Gn.gslot.assign(P.n_rows, -1);
   Gn.vsm.assign(P.n_rows, 0);
@@ -1093,8 +1117,7 @@ std::string generate_grouped(const tgc::Program& P, const JitConfig& cfg, unsign
   if (cfg.min_blocks) o << ", " << cfg.min_blocks;
   o << ") tg_jit_tape(const JitArgs A) {\n" << kArgAliases
     << (cfg.fuse ? "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");   // params of the previous step\n" : "")
-    << fc.pro
-    << (cfg.fuse ? "  const T* __restrict__ UVt = sU;\n" : "  const T* __restrict__ UVt = UVg;\n") << "  (void)UVt;\n"
+    << (late ? fc.pro : fc.pro_load)
     << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
     << "  T* sm = reinterpret_cast<T*>(smem_raw);\n"
     << "  T* sRed = sm + " << off + WPB * SPW * xs << "u;\n"
@@ -1106,18 +1129,18 @@ std::string generate_grouped(const tgc::Program& P, const JitConfig& cfg, unsign
   for (const auto& g : gr) {
     const tgc::Dense& D = *g.D;
     o << "  for (unsigned e = tid; e < " << D.n_in * G << "u; e += " << cfg.block << "u) { const unsigned k = e / " << Gs
-      << ", j = e % " << Gs << "; sm[" << g.wf << "u + e] = j < " << D.n_out << "u ? UVt[" << D.w_uv << "u + j * "
+      << ", j = e % " << Gs << "; sm[" << g.wf << "u + e] = j < " << D.n_out << "u ? " << tsrc(D.w_uv, D.n_out * D.n_in) << D.w_uv << "u + j * "
       << D.n_in << "u + k] : (T)0; }\n";
     if (g.xvec)
       o << "  for (unsigned e = tid; e < " << D.n_out * G << "u; e += " << cfg.block << "u) { const unsigned j = e / "
-        << Gs << ", k = e % " << Gs << "; sm[" << g.wb << "u + e] = k < " << D.n_in << "u ? UVt[" << D.w_uv
+        << Gs << ", k = e % " << Gs << "; sm[" << g.wb << "u + e] = k < " << D.n_in << "u ? " << tsrc(D.w_uv, D.n_out * D.n_in) << D.w_uv
         << "u + j * " << D.n_in << "u + k] : (T)0; }\n";
     o << "  for (unsigned e = tid; e < " << Gs << "; e += " << cfg.block << "u) sm[" << g.bb << "u + e] = ";
-    if (D.b_uv != kNone) o << "e < " << D.n_out << "u ? UVt[" << D.b_uv << "u + e] : (T)0;\n";
+    if (D.b_uv != kNone) o << "e < " << D.n_out << "u ? " << tsrc(D.b_uv, D.n_out) << D.b_uv << "u + e] : (T)0;\n";
     else o << "(T)0;\n";
   }
   o << "  for (unsigned e = tid; e < " << WPB * nd << "u; e += " << cfg.block << "u) sRed[e] = (T)0;\n"
-    << "  __syncthreads();\n";
+    << "  __syncthreads();\n" << (late ? std::string() : fc.pro_prog);
   // accumulators
   for (std::size_t i = 0; i < ng; ++i) {
     const Grp& g = gr[i];
@@ -1356,6 +1379,20 @@ std::string generate_dmma(const tgc::Program& P, const JitConfig& cfg, unsigned&
   Gen Gn(P, cfg);
   Gn.su = cfg.fuse;
   const FuseCode fc = cfg.fuse ? fuse_code(P, cfg, "") : FuseCode{};
+  // where the layer tables are staged from: params / consts straight from
+  // global (those loads overlap sU's), uniform nodes from sU after the program
+  auto tsrc = [&](std::uint32_t uv0, std::uint32_t cnt) -> std::string {
+    if (!cfg.fuse) return "UVg[";
+    if (uv0 + cnt <= P.n_params) return "A.params[";
+    if (uv0 >= P.uv_const_base) return "(A.consts - " + std::to_string(P.uv_const_base) + ")[";
+    return "sU[";
+  };
+  bool late = false;
+  for (const auto& D : P.dense) {
+    late = late || tsrc(D.w_uv, D.n_out * D.n_in) == "sU[";
+    if (D.b_uv != kNone) late = late || tsrc(D.b_uv, D.n_out) == "sU[";
+  }
+
   Gn.vslot.assign(P.n_rows, -1);
   Gn.gslot.assign(P.n_rows, -1);
   Gn.vsm.assign(P.n_rows, 0);
@@ -1396,8 +1433,7 @@ std::string generate_dmma(const tgc::Program& P, const JitConfig& cfg, unsigned&
   if (cfg.min_blocks) o << ", " << cfg.min_blocks;
   o << ") tg_jit_tape(const JitArgs A) {\n" << kArgAliases
     << (cfg.fuse ? "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");   // params of the previous step\n" : "")
-    << fc.pro
-    << (cfg.fuse ? "  const T* __restrict__ UVt = sU;\n" : "  const T* __restrict__ UVt = UVg;\n") << "  (void)UVt;\n"
+    << (late ? fc.pro : fc.pro_load)
     << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
     << "  T* sm = reinterpret_cast<T*>(smem_raw);\n"
     << "  const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;\n"
@@ -1417,26 +1453,26 @@ std::string generate_dmma(const tgc::Program& P, const JitConfig& cfg, unsigned&
       << "    const unsigned n = 8u * u + (L >> 2), cc = L & 3u;\n";
     if (gr[i].xvec)
       o << "    const unsigned k = 8u * (t >> 1) + 2u * cc + (t & 1u);\n"
-        << "    sm[" << q.bf << "u + e] = (n < " << NO << " && k < " << NI << ") ? UVt[" << W << " + n * " << NI << " + k] : (T)0;\n";
+        << "    sm[" << q.bf << "u + e] = (n < " << NO << " && k < " << NI << ") ? " << tsrc(D.w_uv, D.n_out * D.n_in) << W << " + n * " << NI << " + k] : (T)0;\n";
     else {
       o << "    const unsigned k = 4u * t + cc;\n"
         << "    T w = (T)0;\n"
-        << "    if (n < " << NO << ") { if (k < " << NI << ") w = UVt[" << W << " + n * " << NI << " + k];";
-      if (q.fb) o << " else if (k == " << NI << ") w = UVt[" << D.b_uv << "u + n];";
+        << "    if (n < " << NO << ") { if (k < " << NI << ") w = " << tsrc(D.w_uv, D.n_out * D.n_in) << W << " + n * " << NI << " + k];";
+      if (q.fb) o << " else if (k == " << NI << ") w = " << tsrc(D.b_uv, D.n_out) << D.b_uv << "u + n];";
       o << " }\n    sm[" << q.bf << "u + e] = w;\n";
     }
     o << "  }\n"
       << "  for (unsigned e = tid; e < " << 2 * q.ntO * q.ntX * 32 << "u; e += " << cfg.block << "u) {\n"
       << "    const unsigned t = e / " << q.ntX * 32 << "u, u = (e >> 5) % " << q.ntX << "u, L = e & 31u;\n"
       << "    const unsigned n = 8u * u + (L >> 2), k = 8u * (t >> 1) + 2u * (L & 3u) + (t & 1u);\n"
-      << "    sm[" << q.bk << "u + e] = (k < " << NO << " && n < " << NI << ") ? UVt[" << W << " + k * " << NI << " + n] : (T)0;\n"
+      << "    sm[" << q.bk << "u + e] = (k < " << NO << " && n < " << NI << ") ? " << tsrc(D.w_uv, D.n_out * D.n_in) << W << " + k * " << NI << " + n] : (T)0;\n"
       << "  }\n";
     if (gr[i].xvec && q.fb)
       o << "  for (unsigned e = tid; e < " << 8 * q.ntO << "u; e += " << cfg.block << "u) sm[" << q.bb << "u + e] = e < "
-        << NO << " ? UVt[" << D.b_uv << "u + e] : (T)0;\n";
+        << NO << " ? " << tsrc(D.b_uv, D.n_out) << D.b_uv << "u + e] : (T)0;\n";
   }
   o << "  for (unsigned e = tid; e < " << WPB * nd << "u; e += " << cfg.block << "u) sRed[e] = (T)0;\n"
-    << "  __syncthreads();\n";
+    << "  __syncthreads();\n" << (late ? std::string() : fc.pro_prog);
   for (std::size_t i = 0; i < ng; ++i)
     if (ge[i].contract)
       for (unsigned u = 0; u < ge[i].ntO; ++u)
