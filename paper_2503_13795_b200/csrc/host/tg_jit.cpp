@@ -562,6 +562,15 @@ FuseCode fuse_code(const tgc::Program& P, const JitConfig& cfg, const std::strin
     o << "extern \"C\" __global__ void __launch_bounds__(256) tg_jit_epi(const JitArgs A) {\n"
       << "  __shared__ T sU[" << NUV << "];\n  __shared__ T sG[" << NUV << "];\n  __shared__ unsigned last;\n"
       << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");   // tg_jit_tape's partials / UV\n"
+      << "  // UV and the parameters are final: fetched now, so the last CTA's serial\n"
+      << "  // tail only waits for the reduced totals\n"
+      << "  T uvp[" << (P.n_uv + 255) / 256 << "], pp[" << (P.n_params + 255) / 256 << "];\n"
+      << "#pragma unroll\n"
+      << "  for (int r = 0; r < " << (P.n_uv + 255) / 256 << "; ++r) { const unsigned i = threadIdx.x + 256u * r; uvp[r] = i < "
+      << P.n_uv << "u ? __ldcg(A.UVw + i) : (T)0; }\n"
+      << "#pragma unroll\n"
+      << "  for (int r = 0; r < " << (P.n_params + 255) / 256 << "; ++r) { const unsigned i = threadIdx.x + 256u * r; pp[r] = (A.gd_params && i < "
+      << P.n_params << "u) ? A.gd_params[i] : (T)0; }\n"
       << "  const unsigned warp = (blockIdx.x * 256u + threadIdx.x) >> 5, lane = threadIdx.x & 31u;\n"
       << "  if (warp < " << nd << "u) {\n"
       << "    const T* row = A.partial + (unsigned long long)warp * A.grid_rows;\n"
@@ -578,7 +587,9 @@ FuseCode fuse_code(const tgc::Program& P, const JitConfig& cfg, const std::strin
       << "  __threadfence();\n  __syncthreads();\n"
       << "  if (threadIdx.x == 0) last = atomicAdd(A.tickets, 1u) == gridDim.x - 1u;\n"
       << "  __syncthreads();\n  if (!last) return;\n  __threadfence();\n"
-      << "  for (unsigned i = threadIdx.x; i < " << P.n_uv << "u; i += 256u) { sU[i] = __ldcg(A.UVw + i); sG[i] = (T)0; }\n"
+      << "#pragma unroll\n"
+      << "  for (int r = 0; r < " << (P.n_uv + 255) / 256 << "; ++r) { const unsigned i = threadIdx.x + 256u * r; if (i < " << P.n_uv
+      << "u) { sU[i] = uvp[r]; sG[i] = (T)0; } }\n"
       << "  __syncthreads();\n"
       << "  for (unsigned d = threadIdx.x; d < " << nd << "u; d += 256u) sG[gDU[d]] = __ldcg(A.partial2 + d);\n"
       << "  if (threadIdx.x == 0) A.tickets[0] = 0u;\n"
@@ -620,10 +631,13 @@ FuseCode fuse_code(const tgc::Program& P, const JitConfig& cfg, const std::strin
         o << "  }\n  __syncthreads();\n";
       }
     }
-    o << "  for (unsigned i = threadIdx.x; i < " << P.n_params << "u; i += 256u) {\n"
-      << "    const T gs = sG[i];\n"
-      << "    if (A.grad_sum) A.grad_sum[i] = gs;\n"
-      << "    if (A.gd_params) A.gd_params[i] = A.gd_params[i] - A.gamma * gs / A.gd_batch;\n  }\n}\n";
+    o << "#pragma unroll\n"
+      << "  for (int r = 0; r < " << (P.n_params + 255) / 256 << "; ++r) {\n"
+      << "    const unsigned i = threadIdx.x + 256u * r;\n"
+      << "    if (i < " << P.n_params << "u) {\n"
+      << "      const T gs = sG[i];\n"
+      << "      if (A.grad_sum) A.grad_sum[i] = gs;\n"
+      << "      if (A.gd_params) A.gd_params[i] = pp[r] - A.gamma * gs / A.gd_batch;\n    }\n  }\n}\n";
     fc.epi = o.str();
     std::ostringstream d;
     d << "__device__ const unsigned gDU[" << std::max(1u, nd) << "] = {";
