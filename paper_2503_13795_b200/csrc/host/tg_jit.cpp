@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdlib>
+#include <cstring>
 #include <functional>
 #include <cstdio>
 #include <sstream>
@@ -564,7 +565,7 @@ FuseCode fuse_code(const tgc::Program& P, const JitConfig& cfg, const std::strin
       << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");   // tg_jit_tape's partials / UV\n"
       << "  // UV and the parameters are final: fetched now, so the last CTA's serial\n"
       << "  // tail only waits for the reduced totals\n"
-      << "  T uvp[" << (P.n_uv + 255) / 256 << "], pp[" << (P.n_params + 255) / 256 << "];\n"
+      << "  T uvp[" << std::max(1u, (P.n_uv + 255) / 256) << "], pp[" << std::max(1u, (P.n_params + 255) / 256) << "];\n"
       << "#pragma unroll\n"
       << "  for (int r = 0; r < " << (P.n_uv + 255) / 256 << "; ++r) { const unsigned i = threadIdx.x + 256u * r; uvp[r] = i < "
       << P.n_uv << "u ? __ldcg(A.UVw + i) : (T)0; }\n"
@@ -1777,7 +1778,11 @@ JitKernel build(const tgc::Program& P) {
   const nvrtcResult rc = nvrtcCompileProgram(prog, verbose ? 6 : 5, opts);
   std::size_t logn = 0;
   nvrtcGetProgramLogSize(prog, &logn);
-  if (logn > 1) { k.log.resize(logn); nvrtcGetProgramLog(prog, k.log.data()); }
+  if (logn > 1) {
+    k.log.resize(logn);
+    nvrtcGetProgramLog(prog, k.log.data());
+    k.log.resize(std::strlen(k.log.c_str()));   // drop the terminating NUL before appending
+  }
   if (rc != NVRTC_SUCCESS) { nvrtcDestroyProgram(&prog); k.log = "NVRTC: " + k.log; return k; }
   std::size_t n = 0;
   nvrtcGetCUBINSize(prog, &n);

@@ -173,3 +173,27 @@ def test_synthetic_generators_are_prefix_stable():
     assert k.min() >= 0 and k.max() < 27
     counts = np.bincount(k.ravel(), minlength=27)
     assert counts[0] > counts[5] > counts[20]   # Zipf: rank 1 most frequent
+
+
+@pytest.mark.parametrize("form", ["dmma", "group", "classic"])
+@pytest.mark.parametrize("fuse", ["1", "0"])
+def test_every_jit_program_compiles(form, fuse, monkeypatch):
+    """Every JIT-eligible workload and a sample of the reference's fuzzer
+    graphs generate NVRTC-clean sources in every form, fused and unfused (a
+    generator bug would otherwise surface on the GPU only as a silent
+    interpreter fallback)."""
+    from helpers import recipes, replay
+    monkeypatch.setenv("TG_JIT_FORM", form)
+    monkeypatch.setenv("TG_JIT_FUSE", fuse)
+    descs = [tg.build_model(m).describe() for m in ("fig1", "listing1", "moons")]
+    descs.append(tg.build_model("moons", None, "f32").describe())
+    for rec in list(recipes())[:12]:
+        for dt in ("f64", "f32"):
+            t, _ = replay(rec, dt, n_params=1)
+            descs.append(t.describe())
+    for d in descs:
+        p = tg.Program(d)
+        src, log, ms = ctypes.c_char_p(), ctypes.c_char_p(), ctypes.c_double()
+        _lib.lib.tg_program_jit(p._h, ctypes.byref(src), ctypes.byref(log), ctypes.byref(ms))
+        text = (log.value or b"").decode()
+        assert "compiled" in text or "not eligible" in text, text[-2000:]
