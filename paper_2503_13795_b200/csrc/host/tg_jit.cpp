@@ -71,7 +71,9 @@ struct Gen {
     if (gslot[r] >= 0 && !gsm[r] && !gstored[r]) { o << "      " << sg_(r) << " = " << g(r) << ";\n"; gstored[r] = 1; }
   }
 
-  Gen(const tgc::Program& p, const JitConfig& c) : P(p), cfg(c), f64(p.dtype == TG_F64) {}
+  Gen(const tgc::Program& p, const JitConfig& c) : P(p), cfg(c), f64(p.dtype == TG_F64) {
+    if (const char* e = std::getenv("TG_TANH")) tanh_fn = std::string(e) == "fp64" ? "tg_tanh_fp64" : "tg_tanh";
+  }
 
   std::string fn(const char* d, const char* f) const { return f64 ? d : f; }
   std::string v(std::uint32_t r) const { return "v" + std::to_string(r); }
@@ -104,6 +106,7 @@ struct Gen {
   // evaluated by each CTA; umode emits the uniform program itself (values
   // sU[u], adjoints sG[u]).
   bool su = false, umode = false;
+  std::string tanh_fn = "tg_tanh";   // fp64 tanh variant (kernels/tg_math.cuh)
   std::string ix_expr(const tgc::GatherTable& t) const {
     return "tg_ix(idx, " + std::to_string(t.col) + "ull * batch + s, " + std::to_string(t.n_rows) + "u)";
   }
@@ -176,7 +179,7 @@ struct Gen {
     const std::string Z = "(T)0", ONE = "(T)1", TWO = "(T)2";
     switch (in.op) {
       case Relu: o << out << a[0] << " > " << Z << " ? " << a[0] << " : " << Z << ";\n"; break;
-      case Tanh: o << out << fn("tg_tanh", "tanhf") << "(" << a[0] << ");\n"; break;
+      case Tanh: o << out << fn(tanh_fn.c_str(), "tanhf") << "(" << a[0] << ");\n"; break;
       case Exp: o << out << fn("exp", "expf") << "(" << a[0] << ");\n"; break;
       case NegLog: check("!(" + a[0] + " > (T)0)", in, a[0]); o << out << "-" << fn("log", "logf") << "(" << a[0] << ");\n"; break;
       case Sigmoid: o << out << ONE << " / (" << ONE << " + " << fn("exp", "expf") << "(-" << a[0] << "));\n"; break;
@@ -254,7 +257,7 @@ struct Gen {
       case Tanh: {
         const char* sk = std::getenv("TG_JIT_SKIP");  // profiling-only ablation
         if (sk && std::string(sk) == "tanh") return "(" + z + ")";
-        return fn("tg_tanh", "tanhf") + "(" + z + ")";
+        return fn(tanh_fn.c_str(), "tanhf") + "(" + z + ")";
       }
       case Exp: return fn("exp", "expf") + "(" + z + ")";
       case Sigmoid: return "((T)1 / ((T)1 + " + fn("exp", "expf") + "(-" + z + ")))";
@@ -1415,6 +1418,7 @@ std::string generate_dmma(const tgc::Program& P, const JitConfig& cfg, unsigned&
   Gn.vov.assign(P.n_rows, "");
   Gn.gov.assign(P.n_rows, "");
   Gn.gcond.assign(P.n_rows, "");
+  if (!std::getenv("TG_TANH")) Gn.tanh_fn = "tg_tanh_fp64";   // keeps the XU queue off the DMMA kernel's path
   Gn.gj.assign(P.n_rows, -1);
   auto nm = [](const char* p, std::size_t i, unsigned u, unsigned e) {
     return std::string(p) + std::to_string(i) + "_" + std::to_string(u) + "_" + std::to_string(e);
@@ -1752,6 +1756,13 @@ JitKernel build(const tgc::Program& P) {
   }
   if (!k.group) {
     k.form = "classic";
+    // the one-thread-per-sample form reads dense weights as constant-bank
+    // operands; fused, they would be shared-memory loads (42 -> 66 us on cfg2,
+    // measured), so it fuses only tapes without dense layers (cfg1: 49 -> 61 G/s)
+    if (cfg.fuse && !P.dense.empty()) {
+      cfg.fuse = false;
+      cfg.const_uv = std::size_t(std::max<std::uint32_t>(1, P.n_uv)) * ts <= kMaxConstBytes;
+    }
     std::size_t smem_elems = 0;
     k.source = generate(P, cfg, k.n_crow_g, k.n_crow_v, terms, toff, smem_elems);
     k.cfg = cfg;

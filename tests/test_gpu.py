@@ -278,9 +278,13 @@ def test_sample_invariant_root_and_lone_leaf():
 
 
 @pytest.mark.parametrize("tier", TIERS)
-def test_fp64_tanh_accuracy(tier):
-    """The branch-free fp64 tanh of the hot path (kernels/tg_math.cuh) vs a
-    correctly rounded reference: a few ulp over the whole range."""
+def test_fp64_tanh_accuracy(tier, monkeypatch):
+    """The branch-free fp64 tanh variants of the hot path (kernels/tg_math.cuh:
+    tg_tanh in the interpreter and the one-thread-per-sample JIT form,
+    tg_tanh_fp64 in the DMMA form, forced here with TG_TANH) vs a correctly
+    rounded reference: a few ulp over the whole range."""
+    if tier == "jit":
+        monkeypatch.setenv("TG_TANH", "fp64")
     t = tg.Tape(dtype="f64")
     a = t.input(0, 0.5)
     t.set_root(t.tanh(a))
