@@ -382,10 +382,17 @@ def main():
                 "algorithmic_flops_per_launch": alg,
                 "peak_source": "profiles/fp_peaks.json (FMA-throughput microbenchmark on this B200)",
                 "hbm_achieved_gbs": b * cfg["bytes"] / (tape_ms * 1e-3) / 1e9}
+        if cfg["bound"] == "tensor" and cfg["dtype"] == "f32":
+            # dense products on tcgen05 as 3xTF32 (three kind::tf32 MMAs per fp32
+            # product): the roof is the measured dense bf16 peak / 2 (TF32 rate) / 3
+            t_peak = pk["bf16_tflops"] / 2 / 3
+            roof.update({"peak": t_peak, "frac": achieved / t_peak,
+                         "peak_source": f"{pk['source']} bf16 dense {pk['bf16_tflops']} TF/s / 2 (TF32) / 3 (3xTF32 passes)",
+                         "frac_of_fp32_fma_peak": achieved / fp_peak if fp_peak else None})
     tier = ["smem-interpreter", "hbm-interpreter", "jit-register", "staged"][info["storage"]]
     roof["kernel"] = {"smem-interpreter": "tgk::k_tape<T,true>", "hbm-interpreter": "tgk::k_tape<T,false>",
                       "jit-register": "tg_jit_tape (NVRTC sm_100a)",
-                      "staged": "staged chain: k_gemm / k_umma_tf32x3 / k_tape_range"}[tier]
+                      "staged": "staged chain: k_umma_tma (tcgen05 3xTF32, TMA-fed) / k_tape_range"}[tier]
     roof["kernel_ms"] = tape_ms
     roof["kernel_share_of_step"] = tape_ms / ms
     roof["traffic"] = measured_traffic(args.config, b)

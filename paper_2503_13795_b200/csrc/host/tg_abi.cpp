@@ -426,11 +426,13 @@ template <class T>
 cudaError_t dense_gemm(const tg_program& pr, const tgk::GemmArgs<T>& g, std::uint32_t splits, cudaStream_t st) {
   if constexpr (std::is_same_v<T, float>) {
     // Roles on tcgen05: bit 0 forward Z = W X, bit 1 input adjoints, bit 2 weight
-    // gradients.  Default 6: tensor-core accumulation (~6e-6 relative at
-    // K ~ 1e3) in the forward would flip ReLU masks of near-zero
-    // pre-activations and move the batch gradient by ~5e-4 (measured, cfg5);
-    // backward products only scale errors, they switch no mask.
-    static const int mask = std::getenv("TG_UMMA_MASK") ? std::atoi(std::getenv("TG_UMMA_MASK")) : 6;
+    // gradients.  Default: all three.  The TMA-fed kernel drains its TMEM
+    // accumulator every k-tile into round-to-nearest fp32 sums, which removes
+    // the tensor core's accumulation bias (2.6e-7 normwise at any K, below the
+    // SIMT GEMM's 5e-7..6.5e-6; scripts/gemm_kerr.py).  With the biased
+    // accumulation of round 1 (~6e-6 at K ~ 1e3) the forward role had flipped
+    // ReLU masks and moved cfg5's gradient by 5.5e-4, so it had stayed on SIMT.
+    static const int mask = std::getenv("TG_UMMA_MASK") ? std::atoi(std::getenv("TG_UMMA_MASK")) : 7;
     const int role = g.epi == tgk::kEpiBiasAct ? 1 : g.epi == tgk::kEpiAccum ? 2 : 4;
     if (pr.umma && (mask & role)) return tgk::launch_gemm_umma(g, splits, st);
   }

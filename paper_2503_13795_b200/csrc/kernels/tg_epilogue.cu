@@ -148,11 +148,12 @@ __global__ void __launch_bounds__(kBlock) k_uniform_fwd(UniformArgs<T> a) {
     }
     __syncthreads();
   }
-  for (std::uint32_t i = threadIdx.x; i < a.n_uv; i += kBlock) {
-    const T v = V[i];
-    if (a.smem) a.UV[i] = v;
-    if (a.UVc) a.UVc[i] = v;   // mirror into the specialised kernel's __constant__ table
-  }
+  if (a.smem || a.UVc)
+    for (std::uint32_t i = threadIdx.x; i < a.n_uv; i += kBlock) {
+      const T v = V[i];
+      if (a.smem) a.UV[i] = v;
+      if (a.UVc) a.UVc[i] = v;   // mirror into the specialised kernel's __constant__ table
+    }
 }
 
 template <class T>

@@ -15,9 +15,12 @@
 // only after that mbarrier completes, so loads of tile t+1 overlap the MMAs
 // of tile t.  Epilogue: tcgen05.ld 32x32b (warp w owns TMEM lanes 32w..32w+31
 // = output rows), bias / activation / accumulate / split-K partial store.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "tg_ops.cuh"
 #include "tg_staged.cuh"
@@ -194,10 +197,332 @@ __global__ void __launch_bounds__(128, 1) k_umma_tf32x3(GemmArgs<float> g) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(BN));
 }
 
+
+// ---------------------------------------------------------------------------
+// TMA-fed, warp-specialised variant (k_umma_tma).
+//
+// Operand tiles travel HBM -> shared memory by TMA (cp.async.bulk.tensor,
+// SWIZZLE_128B) straight into the canonical UMMA layouts, whichever way the
+// operand is stored:
+//   K-major  (k contiguous):  one box {32 k, 128 rows}: rows of 128 B,
+//            8-row swizzle atoms (SBO = 1024 B); a K = 8 step advances the
+//            descriptor start address by 32 B inside the atom;
+//   MN-major (m/n contiguous): four boxes {32 mn, 32 k} (4 KB each, LBO =
+//            4 KB between them, SBO = 1024 B); a K = 8 step is +1024 B.
+// The 3xTF32 split is elementwise and therefore layout-agnostic: converter
+// warps round each landed fp32 tile in place to hi = tf32_rna(x) and write
+// lo = x - hi at the same offset of a parallel buffer.
+// Warp roles (192 threads): warp 0 TMA producer, warp 1 MMA issuer (one
+// lane), warps 2..5 converters and, after the K loop, the TMEM epilogue
+// (warp w reads TMEM lanes 32 (w % 4) ..).  A 3-stage ring of mbarriers:
+// full (TMA bytes landed) -> conv (128 converter threads done) -> empty
+// (tcgen05.commit: the MMAs that read the stage retired).
+constexpr int kTStages = 3;
+constexpr std::uint32_t kTTile = BM * BK * 4;                   // 16 KB: one operand tile
+constexpr std::uint32_t kTStage = 4 * kTTile;                   // A hi, A lo, B hi, B lo
+constexpr std::uint32_t kTSmem = kTStages * kTStage + 1024 + 512;
+
+struct TmaOperand {
+  bool mn;   // MN-major (m / n contiguous) vs K-major
+};
+
+__device__ __forceinline__ void mbar_init(std::uint32_t mbar, std::uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(std::uint32_t mbar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(mbar));
+}
+__device__ __forceinline__ void mbar_expect_tx(std::uint32_t mbar, std::uint32_t bytes) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(mbar), "r"(bytes));
+}
+__device__ __forceinline__ void mbar_wait2(std::uint32_t mbar, std::uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "TG_WAIT2:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra TG_DONE2;\n\t"
+      "bra TG_WAIT2;\n"
+      "TG_DONE2:\n\t}\n" ::"r"(mbar),
+      "r"(parity));
+}
+__device__ __forceinline__ void tma_load_2d(std::uint32_t dst, const CUtensorMap* map, int c0, int c1, std::uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<std::uint64_t>(map)), "r"(c0), "r"(c1), "r"(mbar)
+      : "memory");
+}
+// SWIZZLE_128B smem descriptor (sm_100 version 1).
+__device__ __forceinline__ std::uint64_t umma_desc_sw128(std::uint32_t saddr, std::uint32_t lbo, std::uint32_t sbo) {
+  return static_cast<std::uint64_t>((saddr & 0x3FFFFu) >> 4) | (static_cast<std::uint64_t>(lbo >> 4) << 16) |
+         (static_cast<std::uint64_t>(sbo >> 4) << 32) | (1ull << 46) | (2ull << 61);
+}
+// Issue the TMA loads of one operand's k-tile (rows r0.., k0..) into dst.
+__device__ __forceinline__ void tma_operand(const CUtensorMap* map, bool mn, std::uint32_t dst, int r0, int k0,
+                                            std::uint32_t mbar) {
+  if (mn) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tma_load_2d(dst + c * 4096, map, r0 + 32 * c, k0, mbar);
+  } else {
+    tma_load_2d(dst, map, k0, r0, mbar);
+  }
+}
+// MN-major 32-bit operands: the only UMMA layout is SWIZZLE_128B_BASE32B
+// (layout type 1; Swizzle<2,5,2>: 32-byte granules XOR row % 4, 4-row atoms of
+// 512 B), written by TMA's SWIZZLE_128B_ATOM_32B mode.  LBO = 4 KB between the
+// 32-wide MN chunks, SBO = 512 B between 4-row K groups.
+__device__ __forceinline__ std::uint64_t umma_desc_b32(std::uint32_t saddr, std::uint32_t lbo, std::uint32_t sbo) {
+  return static_cast<std::uint64_t>((saddr & 0x3FFFFu) >> 4) | (static_cast<std::uint64_t>(lbo >> 4) << 16) |
+         (static_cast<std::uint64_t>(sbo >> 4) << 32) | (1ull << 46) | (1ull << 61);
+}
+__device__ __forceinline__ std::uint64_t operand_desc(std::uint32_t base, bool mn, int ks) {
+  if (!mn) return umma_desc_sw128(base + ks * 32, 16, 1024);
+  return umma_desc_b32(base + ks * 1024, 4096, 512);
+}
+
+// Accumulation.  tcgen05's fp32 accumulation is biased (measured: mean
+// relative error -1.1e-8 x K on positive data, 1.4e-5 normwise at K = 2048),
+// so no TMEM accumulator sums more than kFlush k-tiles (12 x kFlush MMAs):
+// the issuer alternates between two TMEM buffers, and the converter warps
+// drain each finished buffer into fp32 round-to-nearest register sums (one
+// output row per thread) while the tensor core fills the other one.
+constexpr int kFlush = 1;
+
+__global__ void __launch_bounds__(192, 1) k_umma_tma(GemmArgs<float> g, const __grid_constant__ CUtensorMap tmA,
+                                                     const __grid_constant__ CUtensorMap tmB, int a_mn, int b_mn) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-byte alignment for the swizzle atoms
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
+  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + kTStages * kTStage);
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 3 * kTStages + 4);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  auto full = [&](int s) { return smem_u32(&bars[s]); };
+  auto conv = [&](int s) { return smem_u32(&bars[kTStages + s]); };
+  auto empty = [&](int s) { return smem_u32(&bars[2 * kTStages + s]); };
+  auto tfull = [&](int b) { return smem_u32(&bars[3 * kTStages + b]); };
+  auto tempty = [&](int b) { return smem_u32(&bars[3 * kTStages + 2 + b]); };
+
+  if (tid == 0) {
+    for (int s = 0; s < kTStages; ++s) {
+      mbar_init(full(s), 1);
+      mbar_init(conv(s), 128);
+      mbar_init(empty(s), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull(b), 1);
+      mbar_init(tempty(b), 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "n"(2 * BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const std::uint32_t tmem = *tmem_slot;
+
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  std::uint32_t k_begin = 0, k_end = g.K;
+  if (g.epi == kEpiSplitK) {
+    k_begin = blockIdx.z * g.k_chunk;
+    k_end = min(g.K, k_begin + g.k_chunk);
+  }
+  const std::uint32_t T = k_end > k_begin ? (k_end - k_begin + BK - 1) / BK : 0;
+  const std::uint32_t NG = (T + kFlush - 1) / kFlush;   // accumulation groups
+
+  if (warp == 0) {
+    // ===== TMA producer =====
+    if (lane == 0)
+      for (std::uint32_t t = 0; t < T; ++t) {
+        const int s = t % kTStages;
+        if (t >= kTStages) mbar_wait2(empty(s), ((t / kTStages) - 1) & 1);
+        const std::uint32_t base = smem_u32(smem + s * kTStage);
+        mbar_expect_tx(full(s), 2 * kTTile);
+        const int k0 = static_cast<int>(k_begin + t * BK);
+        tma_operand(&tmA, a_mn, base, m0, k0, full(s));
+        tma_operand(&tmB, b_mn, base + 2 * kTTile, n0, k0, full(s));
+      }
+  } else if (warp == 1) {
+    // ===== MMA issuer =====
+    // kind::tf32: D F32 (bit 4), A/B TF32 (bits 7, 10), majors (bits 15, 16), N >> 3 at 17, M >> 4 at 24
+    const std::uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (std::uint32_t(a_mn) << 15) |
+                                (std::uint32_t(b_mn) << 16) | ((BN >> 3) << 17) | ((BM >> 4) << 24);
+    for (std::uint32_t t = 0; t < T; ++t) {
+      const int s = t % kTStages;
+      const std::uint32_t grp = t / kFlush;
+      const int buf = grp & 1;
+      if (t % kFlush == 0 && grp >= 2) mbar_wait2(tempty(buf), ((grp >> 1) - 1) & 1);   // buffer drained
+      mbar_wait2(conv(s), (t / kTStages) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      if (lane == 0) {
+        const std::uint32_t a_hi = smem_u32(smem + s * kTStage), a_lo = a_hi + kTTile;
+        const std::uint32_t b_hi = a_hi + 2 * kTTile, b_lo = a_hi + 3 * kTTile;
+        const std::uint32_t td = tmem + buf * BN;
+#pragma unroll
+        for (int ks = 0; ks < BK / 8; ++ks) {
+          const std::uint64_t dAh = operand_desc(a_hi, a_mn, ks), dAl = operand_desc(a_lo, a_mn, ks);
+          const std::uint64_t dBh = operand_desc(b_hi, b_mn, ks), dBl = operand_desc(b_lo, b_mn, ks);
+          mma_tf32(td, dAl, dBh, idesc, (t % kFlush != 0 || ks != 0) ? 1u : 0u);
+          mma_tf32(td, dAh, dBl, idesc, 1u);
+          mma_tf32(td, dAh, dBh, idesc, 1u);
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(empty(s)));
+        if (t % kFlush == kFlush - 1 || t == T - 1)
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(tfull(buf)));
+      }
+      __syncwarp();
+    }
+  } else {
+    // ===== converters (hi = tf32_rna(x) in place, lo = x - hi) + accumulation drain =====
+    const int ct = tid - 64;   // 0..127
+    const int wq = warp & 3;   // this warp's TMEM lane quarter (32 rows)
+    float acc[BN];
+#pragma unroll
+    for (int j = 0; j < BN; ++j) acc[j] = 0.f;
+    auto drain = [&](std::uint32_t grp) {
+      const int buf = grp & 1;
+      mbar_wait2(tfull(buf), (grp >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+      for (int c = 0; c < BN; c += 16) {
+        std::uint32_t r[16];
+        const std::uint32_t taddr = tmem + buf * BN + (static_cast<std::uint32_t>(wq * 32) << 16) + c;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+              "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[c + j] += __uint_as_float(r[j]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      mbar_arrive(tempty(buf));
+    };
+    for (std::uint32_t t = 0; t < T; ++t) {
+      const int s = t % kTStages;
+      mbar_wait2(full(s), (t / kTStages) & 1);
+      unsigned char* base = smem + s * kTStage;
+#pragma unroll
+      for (int op = 0; op < 2; ++op) {
+        float4* hi = reinterpret_cast<float4*>(base + op * 2 * kTTile);
+        float4* lo = reinterpret_cast<float4*>(base + op * 2 * kTTile + kTTile);
+#pragma unroll 4
+        for (int i = ct; i < static_cast<int>(kTTile / 16); i += 128) {
+          const float4 x = hi[i];
+          float4 h, l;
+          h.x = tf32_rna(x.x); l.x = tf32_rna(x.x - h.x);
+          h.y = tf32_rna(x.y); l.y = tf32_rna(x.y - h.y);
+          h.z = tf32_rna(x.z); l.z = tf32_rna(x.z - h.z);
+          h.w = tf32_rna(x.w); l.w = tf32_rna(x.w - h.w);
+          hi[i] = h;
+          lo[i] = l;
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;");   // generic-proxy stores -> tensor-core reads
+      mbar_arrive(conv(s));
+      // the previous group's accumulator is complete once this tile's conversion is handed over
+      if (t % kFlush == 0 && t > 0) drain(t / kFlush - 1);
+    }
+    if (NG > 0) drain(NG - 1);
+    // ===== epilogue: row m = this thread's TMEM lane =====
+    const std::uint32_t m = m0 + wq * 32 + lane;
+    if (m < g.M) {
+#pragma unroll
+      for (int j = 0; j < BN; ++j) {
+        const std::uint32_t n = n0 + j;
+        if (n >= g.N) continue;
+        const float a = acc[j];
+        if (g.epi == kEpiBiasAct) {
+          const float z = (g.bias ? g.bias[m] : 0.f) + a;
+          g.C[std::size_t(m) * g.ldc + n] = z;
+          if (g.act) g.C2[std::size_t(m) * g.ldc + n] = act_fwd<float>(g.act, z);
+        } else if (g.epi == kEpiAccum) {
+          float* p = &g.C[std::size_t(m) * g.ldc + n];
+          *p = g.beta ? *p + a : a;
+        } else {
+          g.C[(std::size_t(blockIdx.z) * g.M + m) * g.N + n] = a;
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * BN));
+}
+
+// Host: 2D tensor map of an operand view for TMA (SWIZZLE_128B, zero OOB fill).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    cudaGetLastError();
+  }
+  return fn;
+}
+
+// rows x k operand; mn: element (r, k) at P[k * ld + r], else at P[r * ld + k]
+bool make_operand_map(CUtensorMap* map, const float* P, std::size_t ld, bool mn, std::uint32_t rows, std::uint32_t K) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  if ((reinterpret_cast<std::uintptr_t>(P) & 15) || ((ld * 4) & 15) || ld * 4 >= (1ull << 40)) return false;
+  cuuint64_t dims[2], strides[1] = {static_cast<cuuint64_t>(ld) * 4};
+  cuuint32_t box[2], estr[2] = {1, 1};
+  if (mn) {
+    dims[0] = rows; dims[1] = K;
+    box[0] = 32; box[1] = 32;
+  } else {
+    dims[0] = K; dims[1] = rows;
+    box[0] = 32; box[1] = BM;
+  }
+  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(P), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, mn ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
 }  // namespace
 
-cudaError_t launch_gemm_umma(const GemmArgs<float>& g, std::uint32_t splits, cudaStream_t st) {
-  if (g.M == 0 || g.N == 0) return cudaSuccess;
+cudaError_t launch_gemm_umma(const GemmArgs<float>& g0, std::uint32_t splits, cudaStream_t st) {
+  if (g0.M == 0 || g0.N == 0) return cudaSuccess;
+  // TMA-fed path: operands that satisfy the tensor-map rules (16-byte aligned
+  // base and row stride); split-K slices start on 32-element k boundaries so a
+  // k-tile never reads into the next slice (TMA zero-fills only past K).
+  static const bool use_tma = !(std::getenv("TG_UMMA_TMA") && std::getenv("TG_UMMA_TMA")[0] == '0');
+  if (use_tma) {
+    GemmArgs<float> g = g0;
+    if (g.epi == kEpiSplitK) g.k_chunk = (g.k_chunk + BK - 1) / BK * BK;
+    CUtensorMap ta, tb;
+    const bool a_mn = !g.a_kmaj, b_mn = g.b_nmaj;
+    if (make_operand_map(&ta, g.A, g.lda, a_mn, g.M, g.K) && make_operand_map(&tb, g.B, g.ldb, b_mn, g.N, g.K)) {
+      static bool attr = false;
+      if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_umma_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTSmem));
+        if (e != cudaSuccess) return e;
+        attr = true;
+      }
+      const dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, g.epi == kEpiSplitK ? splits : 1);
+      k_umma_tma<<<grid, 192, kTSmem, st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0);
+      return cudaGetLastError();
+    }
+  }
+  const GemmArgs<float>& g = g0;
+  // register-staged fallback (operands TMA cannot describe): its accumulator
+  // is never drained, so its bias grows with K; beyond K = 1024 per launch the
+  // SIMT GEMM is the more accurate engine
+  {
+    const std::uint32_t keff = g.epi == kEpiSplitK ? g.k_chunk : g.K;
+    if (keff > 1024) return launch_gemm<float>(g, splits, st);
+  }
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_umma_tf32x3, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem));

@@ -429,3 +429,30 @@ def test_jit_forms_vs_reference(form, fuse, name, dt, b, monkeypatch):
     prog.gd_update(P2, Gt, 0.05, b)
     torch.cuda.synchronize()
     assert torch.equal(P1, P2)
+
+
+@pytest.mark.parametrize("engine", [0, 1])
+@pytest.mark.parametrize("a_kmaj,b_nmaj", [(True, False), (True, True), (False, True)])
+def test_dense_gemm_long_k_accuracy(engine, a_kmaj, b_nmaj):
+    """Long reduction axis (the weight-gradient role contracts over samples):
+    the tcgen05 kernel drains its TMEM accumulator every k-tile, so its error
+    does not grow with K (the tensor core's own fp32 accumulation is biased,
+    -1.1e-8 x K relative, which would miss the 1e-5 bar by K ~ 2,000)."""
+    import ctypes as C
+    from paper_2503_13795_b200 import _lib
+    M, N, K = 256, 192, 49152
+    torch.manual_seed(1)
+    A = torch.rand(M * K, device="cuda")          # positive data: no cancellation hides a bias
+    B = torch.rand(K * N, device="cuda")
+    Am = A.view(M, K) if a_kmaj else A.view(K, M).t()
+    Bm = B.view(K, N) if b_nmaj else B.view(N, K).t()
+    ref = Am.double() @ Bm.double()
+    Cm = torch.empty(M * N, device="cuda")
+    assert _lib.lib.tg_gemm(1, engine, M, N, K, C.c_void_p(A.data_ptr()), K if a_kmaj else M, int(a_kmaj),
+                            C.c_void_p(B.data_ptr()), N if b_nmaj else K, int(b_nmaj), C.c_void_p(Cm.data_ptr()), N, 0,
+                            None) == 0
+    torch.cuda.synchronize()
+    err = float((Cm.view(M, N).double() - ref).norm() / ref.norm())
+    # tcgen05 (drained accumulator): ~3e-7 at any K; SIMT's sequential fp32 sums
+    # grow with K (~5e-6 here) and are held to the fp32 parity bar
+    assert err < (2e-6 if engine == 1 else 1e-5), err
