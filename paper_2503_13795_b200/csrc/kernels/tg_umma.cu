@@ -286,12 +286,17 @@ __device__ __forceinline__ std::uint64_t operand_desc(std::uint32_t base, bool m
 // drain each finished buffer into fp32 round-to-nearest register sums (one
 // output row per thread) while the tensor core fills the other one.
 constexpr int kFlush = 1;
+__device__ int g_umma_exp = 0;   // profiling ablations (wrong results): 1 skip conversion, 2 one MMA per k-step, 3 TMA ring only
+constexpr int kConvThreads = 256;                 // 8 converter / drain warps
+constexpr int kTThreads = 64 + kConvThreads;      // + TMA producer + MMA issuer
 
-__global__ void __launch_bounds__(192, 1) k_umma_tma(GemmArgs<float> g, const __grid_constant__ CUtensorMap tmA,
+__global__ void __launch_bounds__(kTThreads, 1) k_umma_tma(GemmArgs<float> g, const __grid_constant__ CUtensorMap tmA,
                                                      const __grid_constant__ CUtensorMap tmB, int a_mn, int b_mn) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  // 1024-byte alignment for the swizzle atoms
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
+  // 1024-byte alignment for the swizzle atoms, by pointer arithmetic on the
+  // shared array (an integer round trip would turn every converter access
+  // into a generic LD/ST instead of LDS/STS)
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + kTStages * kTStage);
   std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 3 * kTStages + 4);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -304,12 +309,12 @@ __global__ void __launch_bounds__(192, 1) k_umma_tma(GemmArgs<float> g, const __
   if (tid == 0) {
     for (int s = 0; s < kTStages; ++s) {
       mbar_init(full(s), 1);
-      mbar_init(conv(s), 128);
+      mbar_init(conv(s), kConvThreads);
       mbar_init(empty(s), 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(tfull(b), 1);
-      mbar_init(tempty(b), 128);
+      mbar_init(tempty(b), kConvThreads);
     }
     asm volatile("fence.mbarrier_init.release.cluster;");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tmA)) : "memory");
@@ -324,7 +329,9 @@ __global__ void __launch_bounds__(192, 1) k_umma_tma(GemmArgs<float> g, const __
   asm volatile("tcgen05.fence::after_thread_sync;");
   const std::uint32_t tmem = *tmem_slot;
 
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  // M tiles are the fast grid index: the CTAs that read the same B tile (the
+  // sample-axis operand, too large for L2) run together and share it in L2
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
   std::uint32_t k_begin = 0, k_end = g.K;
   if (g.epi == kEpiSplitK) {
     k_begin = blockIdx.z * g.k_chunk;
@@ -365,6 +372,11 @@ __global__ void __launch_bounds__(192, 1) k_umma_tma(GemmArgs<float> g, const __
         for (int ks = 0; ks < BK / 8; ++ks) {
           const std::uint64_t dAh = operand_desc(a_hi, a_mn, ks), dAl = operand_desc(a_lo, a_mn, ks);
           const std::uint64_t dBh = operand_desc(b_hi, b_mn, ks), dBl = operand_desc(b_lo, b_mn, ks);
+          if (g_umma_exp == 3) continue;   // no MMAs at all: the TMA ring alone
+          if (g_umma_exp == 2) {
+            mma_tf32(td, dAh, dBh, idesc, (t % kFlush != 0 || ks != 0) ? 1u : 0u);
+            continue;
+          }
           mma_tf32(td, dAl, dBh, idesc, (t % kFlush != 0 || ks != 0) ? 1u : 0u);
           mma_tf32(td, dAh, dBl, idesc, 1u);
           mma_tf32(td, dAh, dBh, idesc, 1u);
@@ -377,19 +389,23 @@ __global__ void __launch_bounds__(192, 1) k_umma_tma(GemmArgs<float> g, const __
     }
   } else {
     // ===== converters (hi = tf32_rna(x) in place, lo = x - hi) + accumulation drain =====
-    const int ct = tid - 64;   // 0..127
-    const int wq = warp & 3;   // this warp's TMEM lane quarter (32 rows)
-    float acc[BN];
+    // 8 warps, two per SMSP; for the drain, warps w and w + 4 share TMEM lane
+    // quarter w % 4 (32 rows) and take column halves [0, 64) / [64, 128)
+    const int ct = tid - 64;                    // 0..255
+    const int wq = warp & 3;                    // TMEM lane quarter
+    const int c0 = ((warp - 2) >> 2) * (BN / 2);  // column half
+    constexpr int kCols = BN / 2;
+    float acc[kCols];
 #pragma unroll
-    for (int j = 0; j < BN; ++j) acc[j] = 0.f;
+    for (int j = 0; j < kCols; ++j) acc[j] = 0.f;
     auto drain = [&](std::uint32_t grp) {
       const int buf = grp & 1;
       mbar_wait2(tfull(buf), (grp >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
-      for (int c = 0; c < BN; c += 16) {
+      for (int c = 0; c < kCols; c += 16) {
         std::uint32_t r[16];
-        const std::uint32_t taddr = tmem + buf * BN + (static_cast<std::uint32_t>(wq * 32) << 16) + c;
+        const std::uint32_t taddr = tmem + buf * BN + (static_cast<std::uint32_t>(wq * 32) << 16) + c0 + c;
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
             : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
@@ -406,12 +422,13 @@ __global__ void __launch_bounds__(192, 1) k_umma_tma(GemmArgs<float> g, const __
       const int s = t % kTStages;
       mbar_wait2(full(s), (t / kTStages) & 1);
       unsigned char* base = smem + s * kTStage;
+      const int nop = (g_umma_exp == 1 || g_umma_exp == 3) ? 0 : 2;
 #pragma unroll
-      for (int op = 0; op < 2; ++op) {
+      for (int op = 0; op < nop; ++op) {
         float4* hi = reinterpret_cast<float4*>(base + op * 2 * kTTile);
         float4* lo = reinterpret_cast<float4*>(base + op * 2 * kTTile + kTTile);
 #pragma unroll 4
-        for (int i = ct; i < static_cast<int>(kTTile / 16); i += 128) {
+        for (int i = ct; i < static_cast<int>(kTTile / 16); i += kConvThreads) {
           const float4 x = hi[i];
           float4 h, l;
           h.x = tf32_rna(x.x); l.x = tf32_rna(x.x - h.x);
@@ -428,25 +445,51 @@ __global__ void __launch_bounds__(192, 1) k_umma_tma(GemmArgs<float> g, const __
       if (t % kFlush == 0 && t > 0) drain(t / kFlush - 1);
     }
     if (NG > 0) drain(NG - 1);
-    // ===== epilogue: row m = this thread's TMEM lane =====
-    const std::uint32_t m = m0 + wq * 32 + lane;
-    if (m < g.M) {
+    // ===== epilogue: through shared memory, then whole 512-byte rows per warp =====
+    // (one row per thread straight to global made every store touch 32 rows:
+    // ~14 us of fixed cost per CTA, measured by scripts/gemm_ksweep.py)
+    constexpr int kLd = BN + 4;   // row stride in floats: 16-byte aligned, conflict-free float4 stores
+    float* tile = reinterpret_cast<float*>(smem);   // the pipeline stages are idle now
+    asm volatile("bar.sync 1, %0;" ::"n"(kConvThreads));   // every stage consumed, every drain done
+    {
+      const int r = wq * 32 + lane;
 #pragma unroll
-      for (int j = 0; j < BN; ++j) {
-        const std::uint32_t n = n0 + j;
-        if (n >= g.N) continue;
-        const float a = acc[j];
-        if (g.epi == kEpiBiasAct) {
-          const float z = (g.bias ? g.bias[m] : 0.f) + a;
-          g.C[std::size_t(m) * g.ldc + n] = z;
-          if (g.act) g.C2[std::size_t(m) * g.ldc + n] = act_fwd<float>(g.act, z);
-        } else if (g.epi == kEpiAccum) {
-          float* p = &g.C[std::size_t(m) * g.ldc + n];
-          *p = g.beta ? *p + a : a;
+      for (int j = 0; j < kCols; j += 4)
+        *reinterpret_cast<float4*>(tile + r * kLd + c0 + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(kConvThreads));
+    const int cw = (tid - 64) >> 5;   // converter warp 0..7
+    const std::uint32_t n = n0 + 4 * lane;
+    const bool vec = (g.ldc % 4 == 0) && (g.epi != kEpiSplitK || g.N % 4 == 0);
+    for (int r = cw; r < BM; r += kConvThreads / 32) {
+      const std::uint32_t m = m0 + r;
+      if (m >= g.M || n >= g.N) continue;
+      const float4 v = *reinterpret_cast<const float4*>(tile + r * kLd + 4 * lane);
+      float a4[4] = {v.x, v.y, v.z, v.w};
+      float* dst = g.epi == kEpiSplitK ? g.C + (std::size_t(blockIdx.z) * g.M + m) * g.N + n : g.C + std::size_t(m) * g.ldc + n;
+      const int cnt = min(4u, g.N - n);
+      if (g.epi == kEpiBiasAct) {
+        const float bv = g.bias ? g.bias[m] : 0.f;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) a4[e] += bv;
+        if (g.act) {
+          float h4[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) h4[e] = act_fwd<float>(g.act, a4[e]);
+          float* d2 = g.C2 + std::size_t(m) * g.ldc + n;
+          if (vec && cnt == 4) *reinterpret_cast<float4*>(d2) = make_float4(h4[0], h4[1], h4[2], h4[3]);
+          else for (int e = 0; e < cnt; ++e) d2[e] = h4[e];
+        }
+      } else if (g.epi == kEpiAccum && g.beta) {
+        if (vec && cnt == 4) {
+          const float4 o = *reinterpret_cast<const float4*>(dst);
+          a4[0] += o.x; a4[1] += o.y; a4[2] += o.z; a4[3] += o.w;
         } else {
-          g.C[(std::size_t(blockIdx.z) * g.M + m) * g.N + n] = a;
+          for (int e = 0; e < cnt; ++e) a4[e] += dst[e];
         }
       }
+      if (vec && cnt == 4) *reinterpret_cast<float4*>(dst) = make_float4(a4[0], a4[1], a4[2], a4[3]);
+      else for (int e = 0; e < cnt; ++e) dst[e] = a4[e];
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -498,6 +541,14 @@ cudaError_t launch_gemm_umma(const GemmArgs<float>& g0, std::uint32_t splits, cu
   // base and row stride); split-K slices start on 32-element k boundaries so a
   // k-tile never reads into the next slice (TMA zero-fills only past K).
   static const bool use_tma = !(std::getenv("TG_UMMA_TMA") && std::getenv("TG_UMMA_TMA")[0] == '0');
+  static bool exp_set = false;
+  if (!exp_set) {
+    exp_set = true;
+    if (const char* e = std::getenv("TG_UMMA_EXP")) {
+      const int v = std::atoi(e);
+      cudaMemcpyToSymbol(g_umma_exp, &v, sizeof(int));
+    }
+  }
   if (use_tma) {
     GemmArgs<float> g = g0;
     if (g.epi == kEpiSplitK) g.k_chunk = (g.k_chunk + BK - 1) / BK * BK;
@@ -510,8 +561,8 @@ cudaError_t launch_gemm_umma(const GemmArgs<float>& g0, std::uint32_t splits, cu
         if (e != cudaSuccess) return e;
         attr = true;
       }
-      const dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, g.epi == kEpiSplitK ? splits : 1);
-      k_umma_tma<<<grid, 192, kTSmem, st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0);
+      const dim3 grid((g.M + BM - 1) / BM, (g.N + BN - 1) / BN, g.epi == kEpiSplitK ? splits : 1);
+      k_umma_tma<<<grid, kTThreads, kTSmem, st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0);
       return cudaGetLastError();
     }
   }
