@@ -291,7 +291,8 @@ std::size_t partial_rows(std::size_t batch) {
 }
 
 std::size_t jit_grid(const tg_program& pr, std::size_t batch) {
-  const std::size_t tiles = (batch + pr.jit.tile - 1) / pr.jit.tile;
+  const std::size_t unit = pr.jit.balanced ? 32 : pr.jit.tile;   // balanced: contiguous shares of >= 32 samples
+  const std::size_t tiles = (batch + unit - 1) / unit;
   std::size_t g = std::min<std::size_t>(tiles, std::size_t(pr.jit.occ) * pr.nsm);
   return std::max<std::size_t>(1, std::min(g, partial_rows(batch)));
 }
@@ -752,8 +753,11 @@ tg_status run_fused(tg_program& pr, const void* inputs, const std::int32_t* idx,
   TG_CUDA_TRY(launch_pdl(pr.jit.fn, ja.grid_rows, pr.jit.cfg.block, pr.jit.smem_bytes, args, st));
   if (e1) TG_CUDA_TRY(cudaEventRecord(e1, st));
   const unsigned nd = pr.n_dest();
-  TG_CUDA_TRY(launch_pdl(pr.jit.fn_epi, std::max(1u, (nd + 7) / 8), 256, 0, args, st));
-  pr.launches += 2;
+  ++pr.launches;
+  if (nd > 0 || !pr.P.ubwd.empty()) {   // nothing to reduce or propagate (cfg1): no epilogue launch
+    TG_CUDA_TRY(launch_pdl(pr.jit.fn_epi, std::max(1u, (nd + 7) / 8), 256, 0, args, st));
+    ++pr.launches;
+  }
   // diagnosis of a domain error re-runs the interpreter on this launch's inputs
   tgk::MainArgs<T> ma{};
   ma.fwd = pr.d_fwd;

@@ -766,14 +766,22 @@ std::string generate(const tgc::Program& P, const JitConfig& cfg, unsigned& n_cr
     << "  const unsigned tid = threadIdx.x;\n";
   if (dense) o << "  for (unsigned q = tid; q < " << nd << "u; q += " << cfg.block << "u) sDW[q] = (T)0;\n";
   if (reg_acc && nd) o << "  T acc[" << ndpt << "]; for (int q = 0; q < " << ndpt << "; ++q) acc[q] = 0;\n";
-  o << "  for (unsigned long long tile = blockIdx.x; tile * " << tile << "ull < batch; tile += gridDim.x) {\n"
-    << "    const unsigned long long base = tile * " << tile << "ull;\n"
+  // each CTA owns a contiguous share of the batch (a multiple of 32 samples),
+  // walked in tiles; a partial last tile instead of a whole extra tile on a
+  // few CTAs (cfg1: 1,954 tiles on 1,776 resident CTAs left the GPU 40% idle)
+  o << "  const unsigned long long per = ((batch + gridDim.x - 1) / gridDim.x + 31ull) / 32ull * 32ull;\n"
+    << "  const unsigned long long lo = (unsigned long long)blockIdx.x * per;\n"
+    << "  const unsigned long long hi = lo + per < batch ? lo + per : batch;\n";
+  if (nd && !reg_acc)
+    o << "  if (lo >= hi)\n    for (unsigned d = tid; d < " << nd << "u; d += " << cfg.block
+      << "u) partial[(unsigned long long)d * grid_rows + blockIdx.x] = (T)0;\n";
+  o << "  for (unsigned long long base = lo; base < hi; base += " << tile << "ull) {\n"
     << "#pragma unroll\n"
     << "    for (unsigned jj = 0; jj < " << cfg.spt << "u; ++jj) {\n"
     << "    const unsigned long long s = base + jj * " << cfg.block << "u + tid;\n"
     << "    const unsigned col = jj * " << cfg.block << "u + tid;\n"
     << "    (void)col;\n"
-    << "    if (s < batch) {\n";
+    << "    if (s < hi) {\n";
   G.vstored.assign(P.n_rows, 0);
   if (const char* e = std::getenv("TG_JIT_RELOAD")) G.reload = std::atoi(e) != 0;
   G.gstored.assign(P.n_rows, 0);
@@ -821,7 +829,7 @@ std::string generate(const tgc::Program& P, const JitConfig& cfg, unsigned& n_cr
   o << "    }\n    }\n";
   if (nd && !skip_con) {
     o << "    __syncthreads();\n"
-      << "    const unsigned valid = (unsigned)((batch - base) < " << tile << "ull ? (batch - base) : " << tile << "ull);\n"
+      << "    const unsigned valid = (unsigned)((hi - base) < " << tile << "ull ? (hi - base) : " << tile << "ull);\n"
       << "    T totq[" << ndpt << "];\n"
       << "#pragma unroll 1\n"
       << "    for (unsigned q = 0; q < " << ndpt << "u; ++q) {\n"
@@ -900,7 +908,7 @@ std::string generate(const tgc::Program& P, const JitConfig& cfg, unsigned& n_cr
       << "      const T tot = totq[q]" << (dense ? " + sDW[d]" : "") << ";\n";
     if (reg_acc) o << "      acc[q] += tot;\n";
     else o << "      T* dst = partial + (unsigned long long)d * grid_rows + blockIdx.x;\n"
-           << "      *dst = (tile == blockIdx.x) ? tot : *dst + tot;\n";
+           << "      *dst = (base == lo) ? tot : *dst + tot;\n";
     o << "    }\n    __syncthreads();\n";
   }
   o << "  }\n";
@@ -1756,6 +1764,7 @@ JitKernel build(const tgc::Program& P) {
   }
   if (!k.group) {
     k.form = "classic";
+    k.balanced = true;
     // the one-thread-per-sample form reads dense weights as constant-bank
     // operands; fused, they would be shared-memory loads (42 -> 66 us on cfg2,
     // measured), so it fuses only tapes without dense layers (cfg1: 49 -> 61 G/s)

@@ -59,6 +59,7 @@ struct JitKernel {
   std::string group_log;         // why the dmma / grouped form was not used
   std::string form;              // "dmma" | "group" | "classic"
   bool fused = false;            // prologue + epilogue (+ GD) inside the kernel: one launch per step
+  bool balanced = false;         // CTAs take contiguous shares of the batch (grid sized by 32-sample units)
   std::size_t smem_bytes = 0;    // contraction rows
   unsigned n_crow_g = 0, n_crow_v = 0;
   int occ = 0;
