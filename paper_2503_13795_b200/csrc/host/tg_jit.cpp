@@ -99,6 +99,9 @@ struct Gen {
     return gsm[r] ? sg_(r) : g(r);
   }
   std::string uv(std::uint32_t i) const {
+    // tape constants are known when the program is compiled: literals (x / 2
+    // becomes an exact multiply, domain checks on constants fold away)
+    if (i >= P.uv_const_base && i < P.n_uv) return lit(P.uv_init[i], f64);
     if (su) return "sU[" + std::to_string(i) + "]";
     return cfg.const_uv ? "cUV[" + std::to_string(i) + "]" : "UVg[" + std::to_string(i) + "]";
   }
@@ -775,8 +778,23 @@ std::string generate(const tgc::Program& P, const JitConfig& cfg, unsigned& n_cr
   if (nd && !reg_acc)
     o << "  if (lo >= hi)\n    for (unsigned d = tid; d < " << nd << "u; d += " << cfg.block
       << "u) partial[(unsigned long long)d * grid_rows + blockIdx.x] = (T)0;\n";
-  o << "  for (unsigned long long base = lo; base < hi; base += " << tile << "ull) {\n"
-    << "#pragma unroll\n"
+  // the tile's inputs are loaded before any per-sample code, so every load of
+  // the thread is in flight at once (stores of one sample would otherwise sit
+  // between the loads of the next)
+  std::vector<std::uint32_t> incols;
+  for (const Instr& in : P.fwd)
+    if (in.kind == tgc::kInputLoad) incols.push_back(in.aux);
+  o << "  for (unsigned long long base = lo; base < hi; base += " << tile << "ull) {\n";
+  for (std::uint32_t c : incols)
+    o << "    T pin" << c << "[" << cfg.spt << "];\n";
+  if (!incols.empty()) {
+    o << "#pragma unroll\n    for (unsigned jj = 0; jj < " << cfg.spt << "u; ++jj) {\n"
+      << "      const unsigned long long sp = base + jj * " << cfg.block << "u + tid;\n";
+    for (std::uint32_t c : incols)
+      o << "      pin" << c << "[jj] = sp < hi ? in[" << c << "ull * batch + sp] : (T)0;\n";
+    o << "    }\n";
+  }
+  o << "#pragma unroll\n"
     << "    for (unsigned jj = 0; jj < " << cfg.spt << "u; ++jj) {\n"
     << "    const unsigned long long s = base + jj * " << cfg.block << "u + tid;\n"
     << "    const unsigned col = jj * " << cfg.block << "u + tid;\n"
@@ -786,7 +804,8 @@ std::string generate(const tgc::Program& P, const JitConfig& cfg, unsigned& n_cr
   if (const char* e = std::getenv("TG_JIT_RELOAD")) G.reload = std::atoi(e) != 0;
   G.gstored.assign(P.n_rows, 0);
   for (const Instr& in : P.fwd) {
-    G.forward(in);
+    if (in.kind == tgc::kInputLoad) o << "      const T " << G.v(in.out) << " = pin" << in.aux << "[jj];\n";
+    else G.forward(in);
     if (in.kind == tgc::kDense) {
       const tgc::Dense& D = P.dense[in.aux];
       for (std::uint32_t j = 0; j < D.n_out; ++j) {
