@@ -231,6 +231,28 @@ void tg_pipeline_free(tg_pipeline_t pl);
 tg_status tg_host_alloc(size_t bytes, void** out);
 void tg_host_free(void* ptr);
 
+/* ---- bit-exact serialization of value / gradient ranges ----
+ * Raw range format: headerless, count x scalar, little-endian IEEE-754 (width
+ * 4 or 8), values then gradients when given: bytes = width * count * (1 or 2)
+ * (7 fp64 values = 56 bytes, Table 4).  Snapshot format: "BTSG",
+ * version u32 (1), precision u8 (0 fp32 / 1 fp64), flags u8 (bit 0: grads),
+ * count u64, values, then grads.  NaN payloads travel verbatim.  values /
+ * grads may be device or host pointers (grads NULL: values only); byte
+ * buffers are host memory.  Loads check the byte count / header first and
+ * never apply partially (TG_FORMAT on a mismatch). */
+size_t tg_range_bytes(tg_dtype dtype, size_t count, int with_grads);
+tg_status tg_save_range(tg_dtype dtype, const void* values, const void* grads, size_t count, void* out, size_t out_bytes,
+                        size_t* written);
+tg_status tg_load_range(tg_dtype dtype, void* values, void* grads, size_t count, const void* in, size_t in_bytes);
+size_t tg_snapshot_bytes(tg_dtype dtype, size_t count, int with_grads);
+tg_status tg_save_snapshot(tg_dtype dtype, const void* values, const void* grads, size_t count, void* out,
+                           size_t out_bytes, size_t* written);
+/* Reads the header into dtype_out / count_out / with_grads_out, checks it
+ * against `capacity`, then writes values (and grads when present and
+ * grads != NULL). */
+tg_status tg_load_snapshot(const void* in, size_t in_bytes, void* values, void* grads, size_t capacity,
+                           tg_dtype* dtype_out, size_t* count_out, int* with_grads_out);
+
 /* Synchronises `stream` and reports the first per-sample domain violation
  * seen since the last check as TG_DOMAIN with the reference message. */
 tg_status tg_check_device_error(tg_program_t p, tg_stream_t stream, int64_t* sample_out,

@@ -118,6 +118,12 @@ def _load():
         "tg_pipeline_free": (None, [P]),
         "tg_host_alloc": (st, [sz, C.POINTER(P)]),
         "tg_host_free": (None, [P]),
+        "tg_range_bytes": (sz, [st, sz, C.c_int]),
+        "tg_save_range": (st, [st, P, P, sz, P, sz, C.POINTER(sz)]),
+        "tg_load_range": (st, [st, P, P, sz, P, sz]),
+        "tg_snapshot_bytes": (sz, [st, sz, C.c_int]),
+        "tg_save_snapshot": (st, [st, P, P, sz, P, sz, C.POINTER(sz)]),
+        "tg_load_snapshot": (st, [P, sz, P, P, sz, C.POINTER(st), C.POINTER(sz), C.POINTER(C.c_int)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

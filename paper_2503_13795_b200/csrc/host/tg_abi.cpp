@@ -1539,3 +1539,127 @@ void tg_host_free(void* ptr) {
 }
 
 }  // extern "C"
+
+// ===========================================================================
+// Bit-exact serialization: raw ranges and BTSG snapshots.
+namespace {
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();   // no device / unregistered host memory
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// dst <- src (bytes), either side on the device or the host.  The byte image
+// of an IEEE value is copied verbatim; the hosts this runs on are little-endian.
+tg_status copy_bytes(void* dst, const void* src, std::size_t n) {
+  if (n == 0) return TG_OK;
+  if (is_device_ptr(dst) || is_device_ptr(src)) {
+    TG_CUDA_TRY(cudaMemcpy(dst, src, n, cudaMemcpyDefault));
+  } else {
+    std::memcpy(dst, src, n);
+  }
+  return TG_OK;
+}
+
+std::size_t width_of(tg_dtype d) { return d == TG_F64 ? 8 : 4; }
+constexpr std::size_t kSnapHeader = 4 + 4 + 1 + 1 + 8;
+constexpr std::uint32_t kSnapVersion = 1;
+
+}  // namespace
+
+static_assert(__BYTE_ORDER__ == __ORDER_LITTLE_ENDIAN__, "raw range format is little-endian");
+
+extern "C" {
+
+size_t tg_range_bytes(tg_dtype dtype, size_t count, int with_grads) {
+  return width_of(dtype) * count * (with_grads ? 2 : 1);
+}
+
+tg_status tg_save_range(tg_dtype dtype, const void* values, const void* grads, size_t count, void* out, size_t out_bytes,
+                        size_t* written) {
+  return guard([&] {
+    if (dtype != TG_F64 && dtype != TG_F32) return fail(TG_INVALID_ARGUMENT, "save_range: dtype");
+    const std::size_t w = width_of(dtype), need = tg_range_bytes(dtype, count, grads != nullptr);
+    if (count && !values) return fail(TG_INVALID_ARGUMENT, "save_range: values is NULL");
+    if (out_bytes < need || (need && !out)) return fail(TG_INVALID_ARGUMENT, "save_range: output buffer too small");
+    char* o = static_cast<char*>(out);
+    TG_TRY(copy_bytes(o, values, w * count));
+    if (grads) TG_TRY(copy_bytes(o + w * count, grads, w * count));
+    if (written) *written = need;
+    return TG_OK;
+  });
+}
+
+tg_status tg_load_range(tg_dtype dtype, void* values, void* grads, size_t count, const void* in, size_t in_bytes) {
+  return guard([&] {
+    if (dtype != TG_F64 && dtype != TG_F32) return fail(TG_INVALID_ARGUMENT, "load_range: dtype");
+    const std::size_t w = width_of(dtype), need = tg_range_bytes(dtype, count, grads != nullptr);
+    if (in_bytes != need)
+      return fail(TG_FORMAT, "load_range: " + std::to_string(in_bytes) + " bytes, expected " + std::to_string(need));
+    if (count && (!values || !in)) return fail(TG_INVALID_ARGUMENT, "load_range: NULL buffer");
+    const char* i = static_cast<const char*>(in);
+    TG_TRY(copy_bytes(values, i, w * count));
+    if (grads) TG_TRY(copy_bytes(grads, i + w * count, w * count));
+    return TG_OK;
+  });
+}
+
+size_t tg_snapshot_bytes(tg_dtype dtype, size_t count, int with_grads) {
+  return kSnapHeader + tg_range_bytes(dtype, count, with_grads);
+}
+
+tg_status tg_save_snapshot(tg_dtype dtype, const void* values, const void* grads, size_t count, void* out,
+                           size_t out_bytes, size_t* written) {
+  return guard([&] {
+    if (dtype != TG_F64 && dtype != TG_F32) return fail(TG_INVALID_ARGUMENT, "save_snapshot: dtype");
+    const std::size_t need = tg_snapshot_bytes(dtype, count, grads != nullptr);
+    if (out_bytes < need || !out) return fail(TG_INVALID_ARGUMENT, "save_snapshot: output buffer too small");
+    unsigned char* o = static_cast<unsigned char*>(out);
+    std::memcpy(o, "BTSG", 4);
+    const std::uint32_t ver = kSnapVersion;
+    std::memcpy(o + 4, &ver, 4);
+    o[8] = dtype == TG_F64 ? 1 : 0;
+    o[9] = grads ? 1 : 0;
+    const std::uint64_t n = count;
+    std::memcpy(o + 10, &n, 8);
+    std::size_t w = 0;
+    TG_TRY(tg_save_range(dtype, values, grads, count, o + kSnapHeader, out_bytes - kSnapHeader, &w));
+    if (written) *written = kSnapHeader + w;
+    return TG_OK;
+  });
+}
+
+tg_status tg_load_snapshot(const void* in, size_t in_bytes, void* values, void* grads, size_t capacity,
+                           tg_dtype* dtype_out, size_t* count_out, int* with_grads_out) {
+  return guard([&] {
+    if (!in || in_bytes < kSnapHeader) return fail(TG_FORMAT, "load_snapshot: truncated header");
+    const unsigned char* i = static_cast<const unsigned char*>(in);
+    if (std::memcmp(i, "BTSG", 4) != 0) return fail(TG_FORMAT, "load_snapshot: bad magic");
+    std::uint32_t ver = 0;
+    std::memcpy(&ver, i + 4, 4);
+    if (ver != kSnapVersion) return fail(TG_FORMAT, "load_snapshot: unsupported version " + std::to_string(ver));
+    if (i[8] > 1 || i[9] > 1) return fail(TG_FORMAT, "load_snapshot: bad precision / flags");
+    const tg_dtype dt = i[8] ? TG_F64 : TG_F32;
+    const bool with_grads = i[9] & 1;
+    std::uint64_t n = 0;
+    std::memcpy(&n, i + 10, 8);
+    if (in_bytes != tg_snapshot_bytes(dt, n, with_grads)) return fail(TG_FORMAT, "load_snapshot: payload size mismatch");
+    if (n > capacity) return fail(TG_CAPACITY, "load_snapshot: " + std::to_string(n) + " values exceed capacity " +
+                                                   std::to_string(capacity));
+    if (dtype_out) *dtype_out = dt;
+    if (count_out) *count_out = n;
+    if (with_grads_out) *with_grads_out = with_grads ? 1 : 0;
+    const std::size_t w = width_of(dt);
+    if (n && !values) return fail(TG_INVALID_ARGUMENT, "load_snapshot: values is NULL");
+    TG_TRY(copy_bytes(values, i + kSnapHeader, w * n));
+    if (with_grads && grads) TG_TRY(copy_bytes(grads, i + kSnapHeader + w * n, w * n));
+    return TG_OK;
+  });
+}
+
+}  // extern "C"

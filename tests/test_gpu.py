@@ -456,3 +456,27 @@ def test_dense_gemm_long_k_accuracy(engine, a_kmaj, b_nmaj):
     # tcgen05 (drained accumulator): ~3e-7 at any K; SIMT's sequential fp32 sums
     # grow with K (~5e-6 here) and are held to the fp32 parity bar
     assert err < (2e-6 if engine == 1 else 1e-5), err
+
+
+def test_serialize_device_params_round_trip():
+    """Parameters and grad_sum on the device saved as a raw range / snapshot and
+    loaded back bit-exactly (tg_save_range / tg_load_range on device pointers)."""
+    from paper_2503_13795_b200 import serialize as ser
+    desc = tg.build_model("moons").describe()
+    b = 512
+    x, _ = tg.synth_batch("moons", batch=b, seed=4)
+    prog = make_prog(desc, "jit")
+    _, _, Gh = run(prog, desc, x, np.zeros((0, b), np.int32), desc.param_values(), b)
+    P = torch.tensor(desc.param_values(), device="cuda")
+    G = torch.tensor(Gh, device="cuda")
+    raw = ser.save_range(P, G)
+    assert len(raw) == 2 * 8 * desc.n_params
+    assert raw[:8 * desc.n_params] == P.cpu().numpy().astype("<f8").tobytes()
+    P2, G2 = torch.zeros_like(P), torch.zeros_like(G)
+    ser.load_range(raw, P2, G2)
+    torch.cuda.synchronize()
+    assert torch.equal(P.view(torch.int64), P2.view(torch.int64)) and torch.equal(G.view(torch.int64), G2.view(torch.int64))
+    snap = ser.save_snapshot(P)
+    P3 = torch.zeros_like(P)
+    assert ser.load_snapshot(snap, P3)["count"] == desc.n_params
+    assert torch.equal(P.view(torch.int64), P3.view(torch.int64))
