@@ -405,7 +405,7 @@ tg_status upload(tg_program& pr) {
   pr.d_ticket = reinterpret_cast<unsigned*>(static_cast<char*>(e) + 32);
   TG_CUDA_TRY(cudaMemset(e, 0xff, 8));
   TG_CUDA_TRY(cudaMemset(static_cast<char*>(e) + 16, 0xff, 4));
-  TG_CUDA_TRY(cudaMemset(static_cast<char*>(e) + 32, 0, 4));
+  TG_CUDA_TRY(cudaMemset(static_cast<char*>(e) + 32, 0, 8));   // ticket / grid-barrier count + generation
   if (P.dtype == TG_F64) pr.occ = tgk::tape_occupancy<double>(pr.smem, pr.S, pr.smem_bytes);
   else pr.occ = tgk::tape_occupancy<float>(pr.smem, pr.S, pr.smem_bytes);
   cudaGetLastError();
@@ -690,18 +690,28 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
 // Launch with programmatic stream serialisation: the kernel may be scheduled
 // while its stream predecessor drains; it waits (griddepcontrol.wait) before
 // its first dependent read.
-cudaError_t launch_pdl(cudaKernel_t fn, unsigned grid, unsigned block, std::size_t smem, void** args, cudaStream_t st) {
+cudaError_t launch_pdl(cudaKernel_t fn, unsigned grid, unsigned block, std::size_t smem, void** args, cudaStream_t st,
+                       bool cooperative = false) {
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(grid);
   lc.blockDim = dim3(block);
   lc.dynamicSmemBytes = smem;
   lc.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute at[2];
+  unsigned n = 0;
   static const bool pdl = !(std::getenv("TG_PDL") && std::getenv("TG_PDL")[0] == '0');
+  if (pdl) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (cooperative) {   // grid barriers inside the kernel: every CTA must be resident
+    at[n].id = cudaLaunchAttributeCooperative;
+    at[n].val.cooperative = 1;
+    ++n;
+  }
   lc.attrs = at;
-  lc.numAttrs = pdl ? 1 : 0;
+  lc.numAttrs = n;
   return cudaLaunchKernelExC(&lc, reinterpret_cast<const void*>(fn), args);
 }
 
@@ -750,11 +760,13 @@ tg_status run_fused(tg_program& pr, const void* inputs, const std::int32_t* idx,
     e1 = pr.ev[pr.ev_used].second;
     ++pr.ev_used;
   }
-  TG_CUDA_TRY(launch_pdl(pr.jit.fn, ja.grid_rows, pr.jit.cfg.block, pr.jit.smem_bytes, args, st));
+  TG_CUDA_TRY(launch_pdl(pr.jit.fn, ja.grid_rows, pr.jit.cfg.block, pr.jit.smem_bytes, args, st, pr.jit.coop));
   if (e1) TG_CUDA_TRY(cudaEventRecord(e1, st));
   const unsigned nd = pr.n_dest();
   ++pr.launches;
-  if (nd > 0 || !pr.P.ubwd.empty()) {   // nothing to reduce or propagate (cfg1): no epilogue launch
+  // the cooperative kernel runs the epilogue itself; programs with nothing to
+  // reduce or propagate (cfg1) need none
+  if (!pr.jit.coop && (nd > 0 || !pr.P.ubwd.empty())) {
     TG_CUDA_TRY(launch_pdl(pr.jit.fn_epi, std::max(1u, (nd + 7) / 8), 256, 0, args, st));
     ++pr.launches;
   }

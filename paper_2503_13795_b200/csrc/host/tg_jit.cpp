@@ -493,6 +493,7 @@ bool fusable(const tgc::Program& P, std::string& why) {
 }
 
 struct FuseCode {
+  std::string tail;       // inside tg_jit_tape, at its end (cooperative grid-wide epilogue)
   std::string decl;       // file scope: operand lists, helpers
   std::string pro_load;   // inside tg_jit_tape: params / consts -> sU (loads in flight, no barrier)
   std::string pro_prog;   // barrier, then the uniform program on sU
@@ -559,47 +560,16 @@ FuseCode fuse_code(const tgc::Program& P, const JitConfig& cfg, const std::strin
     fc.pro_prog = o.str();
     fc.pro = fc.pro_load + fc.pro_prog;
   }
-  // ---- epilogue kernel ----
-  {
-    const unsigned nd = static_cast<unsigned>(P.dest_uv.size());
-    Gen U(P, cfg);
-    U.umode = true;
-    U.su = true;
-    std::ostringstream& o = U.o;
-    o << "extern \"C\" __global__ void __launch_bounds__(256) tg_jit_epi(const JitArgs A) {\n"
-      << "  __shared__ T sU[" << NUV << "];\n  __shared__ T sG[" << NUV << "];\n  __shared__ unsigned last;\n"
-      << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");   // tg_jit_tape's partials / UV\n"
-      << "  // UV and the parameters are final: fetched now, so the last CTA's serial\n"
-      << "  // tail only waits for the reduced totals\n"
-      << "  T uvp[" << std::max(1u, (P.n_uv + 255) / 256) << "], pp[" << std::max(1u, (P.n_params + 255) / 256) << "];\n"
-      << "#pragma unroll\n"
-      << "  for (int r = 0; r < " << (P.n_uv + 255) / 256 << "; ++r) { const unsigned i = threadIdx.x + 256u * r; uvp[r] = i < "
-      << P.n_uv << "u ? __ldcg(A.UVw + i) : (T)0; }\n"
-      << "#pragma unroll\n"
-      << "  for (int r = 0; r < " << (P.n_params + 255) / 256 << "; ++r) { const unsigned i = threadIdx.x + 256u * r; pp[r] = (A.gd_params && i < "
-      << P.n_params << "u) ? A.gd_params[i] : (T)0; }\n"
-      << "  const unsigned warp = (blockIdx.x * 256u + threadIdx.x) >> 5, lane = threadIdx.x & 31u;\n"
-      << "  if (warp < " << nd << "u) {\n"
-      << "    const T* row = A.partial + (unsigned long long)warp * A.grid_rows;\n"
-      << "    T t = (T)0;\n"
-      << "    for (unsigned c = lane; c < A.grid_rows; c += 512u) {  // 16 loads in flight, added in sequential order\n"
-      << "      T x[16];\n"
-      << "#pragma unroll\n"
-      << "      for (int u = 0; u < 16; ++u) x[u] = c + 32u * u < A.grid_rows ? __ldcg(row + c + 32u * u) : (T)0;\n"
-      << "#pragma unroll\n"
-      << "      for (int u = 0; u < 16; ++u) if (c + 32u * u < A.grid_rows) t += x[u];\n"
-      << "    }\n"
-      << "    for (int m = 16; m > 0; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);\n"
-      << "    if (lane == 0) A.partial2[warp] = t;\n  }\n"
-      << "  __threadfence();\n  __syncthreads();\n"
-      << "  if (threadIdx.x == 0) last = atomicAdd(A.tickets, 1u) == gridDim.x - 1u;\n"
-      << "  __syncthreads();\n  if (!last) return;\n  __threadfence();\n"
-      << "#pragma unroll\n"
-      << "  for (int r = 0; r < " << (P.n_uv + 255) / 256 << "; ++r) { const unsigned i = threadIdx.x + 256u * r; if (i < " << P.n_uv
-      << "u) { sU[i] = uvp[r]; sG[i] = (T)0; } }\n"
+  // ---- epilogue: fixed-order reduction of the per-CTA partials, then the
+  // uniform reverse sweep, grad_sum and GD on one CTA ----
+  const unsigned nd = static_cast<unsigned>(P.dest_uv.size());
+  // The reverse sweep from the reduced totals (in A.partial2) on one CTA of
+  // `nt` threads; sU holds the uniform table; pp(r) the parameter values.
+  auto tail = [&](std::ostringstream& o, Gen& U, unsigned nt, const std::function<std::string(unsigned)>& pp) {
+    const std::string NT = std::to_string(nt) + "u";
+    o << "  for (unsigned i = threadIdx.x; i < " << P.n_uv << "u; i += " << NT << ") sG[i] = (T)0;\n"
       << "  __syncthreads();\n"
-      << "  for (unsigned d = threadIdx.x; d < " << nd << "u; d += 256u) sG[gDU[d]] = __ldcg(A.partial2 + d);\n"
-      << "  if (threadIdx.x == 0) A.tickets[0] = 0u;\n"
+      << "  for (unsigned d = threadIdx.x; d < " << nd << "u; d += " << NT << ") sG[gDU[d]] = __ldcg(A.partial2 + d);\n"
       << "  __syncthreads();\n";
     if (P.root_uv != kNone) o << "  if (threadIdx.x == 0) sG[" << P.root_uv << "] += (T)A.batch;\n  __syncthreads();\n";
     for (const Instr& in : P.ubwd) {
@@ -611,7 +581,7 @@ FuseCode fuse_code(const tgc::Program& P, const JitConfig& cfg, const std::strin
         const std::uint32_t n = in.nops;
         const std::string uo = opx(in, "j");
         o << "  { const T g = sG[" << in.out << "];\n"
-          << "    for (unsigned j = threadIdx.x; j < " << n << "u; j += 256u) {\n"
+          << "    for (unsigned j = threadIdx.x; j < " << n << "u; j += " << NT << ") {\n"
           << "      const unsigned u = " << uo << ";\n      T c;\n";
         switch (in.op) {
           case AddVarying: o << "      c = g;\n"; break;
@@ -638,18 +608,101 @@ FuseCode fuse_code(const tgc::Program& P, const JitConfig& cfg, const std::strin
         o << "  }\n  __syncthreads();\n";
       }
     }
+    const unsigned rounds = (P.n_params + nt - 1) / nt;
     o << "#pragma unroll\n"
-      << "  for (int r = 0; r < " << (P.n_params + 255) / 256 << "; ++r) {\n"
-      << "    const unsigned i = threadIdx.x + 256u * r;\n"
+      << "  for (int r = 0; r < " << rounds << "; ++r) {\n"
+      << "    const unsigned i = threadIdx.x + " << NT << " * r;\n"
       << "    if (i < " << P.n_params << "u) {\n"
       << "      const T gs = sG[i];\n"
       << "      if (A.grad_sum) A.grad_sum[i] = gs;\n"
-      << "      if (A.gd_params) A.gd_params[i] = pp[r] - A.gamma * gs / A.gd_batch;\n    }\n  }\n}\n";
+      << "      if (A.gd_params) A.gd_params[i] = " << pp(rounds) << " - A.gamma * gs / A.gd_batch;\n    }\n  }\n";
+  };
+  // warp-per-destination reduction of partial rows: destinations d0, d0 + dstride, ...
+  auto reduce = [&](std::ostringstream& o, const std::string& d0, const std::string& dstride) {
+    o << "  for (unsigned d = " << d0 << "; d < " << nd << "u; d += " << dstride << ") {\n"
+      << "    const T* row = A.partial + (unsigned long long)d * A.grid_rows;\n"
+      << "    const unsigned lane = threadIdx.x & 31u;\n"
+      << "    T t = (T)0;\n"
+      << "    for (unsigned c = lane; c < A.grid_rows; c += 512u) {  // 16 loads in flight, added in sequential order\n"
+      << "      T x[16];\n"
+      << "#pragma unroll\n"
+      << "      for (int u = 0; u < 16; ++u) x[u] = c + 32u * u < A.grid_rows ? __ldcg(row + c + 32u * u) : (T)0;\n"
+      << "#pragma unroll\n"
+      << "      for (int u = 0; u < 16; ++u) if (c + 32u * u < A.grid_rows) t += x[u];\n"
+      << "    }\n"
+      << "    for (int m = 16; m > 0; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);\n"
+      << "    if (lane == 0) A.partial2[d] = t;\n  }\n";
+  };
+  if (cfg.coop) {
+    // in the tape kernel itself (cooperative launch: every CTA is resident):
+    // grid barrier, reduction spread over all warps, grid barrier, tail on CTA 0
+    Gen U(P, cfg);
+    U.umode = true;
+    U.su = true;
+    std::ostringstream& o = U.o;
+    const std::string W = std::to_string(cfg.block / 32) + "u";
+    o << "  // ---- grid-wide epilogue (cooperative launch) ----\n"
+      << "  tg_grid_barrier(A.tickets);\n";
+    reduce(o, "blockIdx.x * " + W + " + (threadIdx.x >> 5)", "gridDim.x * " + W);
+    o << "  tg_grid_barrier(A.tickets);\n"
+      << "  if (blockIdx.x == 0) {\n"
+      << "  __shared__ T sG[" << NUV << "];\n";
+    tail(o, U, cfg.block, [&](unsigned) { return std::string("A.gd_params[i]"); });
+    o << "  }\n";
+    fc.tail = o.str();
+  } else if (nd > 0 || !P.ubwd.empty()) {   // nothing to reduce or propagate (cfg1): no epilogue
+    Gen U(P, cfg);
+    U.umode = true;
+    U.su = true;
+    std::ostringstream& o = U.o;
+    o << "extern \"C\" __global__ void __launch_bounds__(256) tg_jit_epi(const JitArgs A) {\n"
+      << "  __shared__ T sU[" << NUV << "];\n  __shared__ T sG[" << NUV << "];\n  __shared__ unsigned last;\n"
+      << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");   // tg_jit_tape's partials / UV\n"
+      << "  // UV and the parameters are final: fetched now, so the last CTA's serial\n"
+      << "  // tail only waits for the reduced totals\n"
+      << "  T uvp[" << std::max(1u, (P.n_uv + 255) / 256) << "], pp[" << std::max(1u, (P.n_params + 255) / 256) << "];\n"
+      << "#pragma unroll\n"
+      << "  for (int r = 0; r < " << (P.n_uv + 255) / 256 << "; ++r) { const unsigned i = threadIdx.x + 256u * r; uvp[r] = i < "
+      << P.n_uv << "u ? __ldcg(A.UVw + i) : (T)0; }\n"
+      << "#pragma unroll\n"
+      << "  for (int r = 0; r < " << (P.n_params + 255) / 256 << "; ++r) { const unsigned i = threadIdx.x + 256u * r; pp[r] = (A.gd_params && i < "
+      << P.n_params << "u) ? A.gd_params[i] : (T)0; }\n";
+    reduce(o, "(blockIdx.x * 256u + threadIdx.x) >> 5", "gridDim.x * 8u");
+    o << "  __threadfence();\n  __syncthreads();\n"
+      << "  if (threadIdx.x == 0) last = atomicAdd(A.tickets, 1u) == gridDim.x - 1u;\n"
+      << "  __syncthreads();\n  if (!last) return;\n  __threadfence();\n"
+      << "  if (threadIdx.x == 0) A.tickets[0] = 0u;\n"
+      << "#pragma unroll\n"
+      << "  for (int r = 0; r < " << (P.n_uv + 255) / 256 << "; ++r) { const unsigned i = threadIdx.x + 256u * r; if (i < " << P.n_uv
+      << "u) sU[i] = uvp[r]; }\n";
+    tail(o, U, 256, [&](unsigned) { return std::string("pp[r]"); });
+    o << "}\n";
     fc.epi = o.str();
+  }
+  {
     std::ostringstream d;
     d << "__device__ const unsigned gDU[" << std::max(1u, nd) << "] = {";
     for (unsigned i = 0; i < nd; ++i) d << (i ? ", " : "") << P.dest_uv[i] << "u";
-    d << "};\n";
+    d << "};\n"
+      << "// grid-wide barrier of a cooperative launch: bar[0] arrivals, bar[1] generation;\n"
+      << "// the last arrival resets the count and opens the next generation\n"
+      << "__device__ __forceinline__ void tg_grid_barrier(unsigned* bar) {\n"
+      << "  __syncthreads();\n"
+      << "  if (threadIdx.x == 0) {\n"
+      << "    volatile unsigned* gen = bar + 1;\n"
+      << "    const unsigned g = *gen;\n"
+      << "    __threadfence();\n"
+      << "    if (atomicAdd(bar, 1u) == gridDim.x - 1u) {\n"
+      << "      bar[0] = 0u;\n"
+      << "      __threadfence();\n"
+      << "      atomicAdd(bar + 1, 1u);\n"
+      << "    } else {\n"
+      << "      while (*gen == g) __nanosleep(32);\n"
+      << "    }\n"
+      << "    __threadfence();\n"
+      << "  }\n"
+      << "  __syncthreads();\n"
+      << "}\n";
     fc.decl += d.str();
   }
   std::ostringstream d;
@@ -934,7 +987,7 @@ std::string generate(const tgc::Program& P, const JitConfig& cfg, unsigned& n_cr
   if (reg_acc && nd)
     o << "  for (int q = 0; q < " << ndpt << "; ++q) { const unsigned d = q * " << cfg.block << "u + tid;\n"
       << "    if (d < " << nd << "u) partial[(unsigned long long)d * grid_rows + blockIdx.x] = acc[q]; }\n";
-  o << "}\n" << fc.epi;
+  o << fc.tail << "}\n" << fc.epi;
   return o.str();
 }
 
@@ -1342,7 +1395,7 @@ std::string generate_grouped(const tgc::Program& P, const JitConfig& cfg, unsign
     << "  for (unsigned d = tid; d < " << nd << "u; d += " << cfg.block << "u) {\n"
     << "    T t = (T)0;\n"
     << "    for (unsigned w = 0; w < " << WPB << "u; ++w) t += sRed[w * " << nd << "u + d];\n"
-    << "    partial[(unsigned long long)d * grid_rows + blockIdx.x] = t;\n  }\n}\n" << fc.epi;
+    << "    partial[(unsigned long long)d * grid_rows + blockIdx.x] = t;\n  }\n" << fc.tail << "}\n" << fc.epi;
   return o.str();
 }
 
@@ -1712,7 +1765,7 @@ std::string generate_dmma(const tgc::Program& P, const JitConfig& cfg, unsigned&
     << "  for (unsigned d = tid; d < " << nd << "u; d += " << cfg.block << "u) {\n"
     << "    T t = (T)0;\n"
     << "    for (unsigned w = 0; w < " << WPB << "u; ++w) t += sRed[w * " << nd << "u + d];\n"
-    << "    partial[(unsigned long long)d * grid_rows + blockIdx.x] = t;\n  }\n}\n" << fc.epi;
+    << "    partial[(unsigned long long)d * grid_rows + blockIdx.x] = t;\n  }\n" << fc.tail << "}\n" << fc.epi;
   return o.str();
 }
 
@@ -1742,6 +1795,12 @@ JitKernel build(const tgc::Program& P) {
     std::string why;
     cfg.fuse = !(fu && fu[0] == '0') && fusable(P, why);
     if (cfg.fuse) cfg.const_uv = false;
+    // TG_JIT_COOP=1: epilogue inside the tape kernel behind two grid barriers
+    // (cooperative launch).  Off by default: on cfg2 the barriers over 444 CTAs
+    // cost more than the PDL-overlapped epilogue launch (37.8 vs 30.7 us/step,
+    // 29.0 vs 23.3 us back to back, measured)
+    const char* co = std::getenv("TG_JIT_COOP");
+    cfg.coop = cfg.fuse && (co && co[0] == '1') && (!P.dest_uv.empty() || !P.ubwd.empty());
   }
   // specialised forms for dense-layer chains before the one-thread-per-sample form
   // form: TG_JIT_FORM = dmma | group | classic (default: first that applies, in that order)
@@ -1791,6 +1850,7 @@ JitKernel build(const tgc::Program& P) {
     // measured), so it fuses only tapes without dense layers (cfg1: 49 -> 61 G/s)
     if (cfg.fuse && !P.dense.empty()) {
       cfg.fuse = false;
+      cfg.coop = false;
       cfg.const_uv = std::size_t(std::max<std::uint32_t>(1, P.n_uv)) * ts <= kMaxConstBytes;
     }
     std::size_t smem_elems = 0;
@@ -1843,7 +1903,9 @@ JitKernel build(const tgc::Program& P) {
     k.log = std::string("library load failed: ") + cudaGetErrorString(cudaGetLastError());
     return k;
   }
-  if (k.cfg.fuse && cudaLibraryGetKernel(&k.fn_epi, k.lib, "tg_jit_epi") != cudaSuccess) {
+  k.coop = k.cfg.fuse && k.cfg.coop;
+  const bool has_epi = k.cfg.fuse && !k.coop && (!P.dest_uv.empty() || !P.ubwd.empty());   // see fuse_code
+  if (has_epi && cudaLibraryGetKernel(&k.fn_epi, k.lib, "tg_jit_epi") != cudaSuccess) {
     k.log = "tg_jit_epi lookup failed";
     return k;
   }

@@ -29,6 +29,7 @@ struct JitConfig {
   unsigned unroll_j = 4;         // dense-layer output loop unroll (independent chains)
   bool dense_loop = false;       // dense layers as loops (rows in smem) vs unrolled (rows in registers)
   bool fuse = false;             // prologue in the kernel + generated epilogue kernel (tg_jit_epi)
+  bool coop = false;             // fused epilogue inside the tape kernel (cooperative launch, grid barriers)
 };
 
 // Kernel argument block of tg_jit_tape, passed by value; the generated code
@@ -60,6 +61,7 @@ struct JitKernel {
   std::string form;              // "dmma" | "group" | "classic"
   bool fused = false;            // prologue + epilogue (+ GD) inside the kernel: one launch per step
   bool balanced = false;         // CTAs take contiguous shares of the batch (grid sized by 32-sample units)
+  bool coop = false;             // one cooperative launch per step (no tg_jit_epi)
   std::size_t smem_bytes = 0;    // contraction rows
   unsigned n_crow_g = 0, n_crow_v = 0;
   int occ = 0;

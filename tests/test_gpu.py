@@ -391,7 +391,7 @@ def test_pipeline_host_buffers_equal_device_steps(model, pinned, b):
 
 
 @pytest.mark.parametrize("form", ["dmma", "group", "classic"])
-@pytest.mark.parametrize("fuse", ["1", "0"])
+@pytest.mark.parametrize("fuse", ["1", "0", "coop"])
 @pytest.mark.parametrize("name,dt,b", [("moons", "f64", 64), ("listing1", "f64", 64), ("fig1", "f64", 64),
                                        ("moons", "f64", 3001), ("moons", "f32", 3001)])
 def test_jit_forms_vs_reference(form, fuse, name, dt, b, monkeypatch):
@@ -402,7 +402,8 @@ def test_jit_forms_vs_reference(form, fuse, name, dt, b, monkeypatch):
     next one; all must match.  The fused GD step equals forward_backward +
     gd_update bit for bit."""
     monkeypatch.setenv("TG_JIT_FORM", form)
-    monkeypatch.setenv("TG_JIT_FUSE", fuse)
+    monkeypatch.setenv("TG_JIT_FUSE", "0" if fuse == "0" else "1")
+    monkeypatch.setenv("TG_JIT_COOP", "1" if fuse == "coop" else "0")   # epilogue behind grid barriers
     desc = tg.build_model(name, None, dt, seed=5).describe()
     x, k = tg.synth_batch(name, None, dt, seed=77, batch=b, n_inputs=desc.n_inputs, n_index=desc.n_index_inputs)
     prog = make_prog(desc, "jit")
