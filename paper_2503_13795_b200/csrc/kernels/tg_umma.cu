@@ -554,6 +554,39 @@ cudaError_t launch_gemm_umma(const GemmArgs<float>& g0, std::uint32_t splits, cu
     if (g.epi == kEpiSplitK) g.k_chunk = (g.k_chunk + BK - 1) / BK * BK;
     CUtensorMap ta, tb;
     const bool a_mn = !g.a_kmaj, b_mn = g.b_nmaj;
+    // An operand TMA cannot describe (row stride not a multiple of 16 bytes,
+    // e.g. cfg3's 200 x 30 weight) is copied to a padded scratch first when it
+    // is small: one strided device copy (stream-ordered, graph-capturable)
+    // instead of the register-staged kernel, whose per-tile fixed cost
+    // dominated those products (880 us per call at K = 30, measured).
+    float* pad_a = nullptr;
+    float* pad_b = nullptr;
+    auto pad = [&](const float* P, std::size_t ld, bool mn, std::uint32_t rows, float*& buf, std::size_t& ldp) {
+      const std::size_t inner = mn ? rows : g.K, outer = mn ? g.K : rows;
+      if (inner * outer > (std::size_t(1) << 22)) return P;
+      ldp = (inner + 3) / 4 * 4;
+      if (cudaMallocAsync(reinterpret_cast<void**>(&buf), ldp * outer * sizeof(float), st) != cudaSuccess ||
+          cudaMemcpy2DAsync(buf, ldp * sizeof(float), P, ld * sizeof(float), inner * sizeof(float), outer,
+                            cudaMemcpyDeviceToDevice, st) != cudaSuccess) {
+        cudaGetLastError();
+        return P;
+      }
+      return static_cast<const float*>(buf);
+    };
+    if (!make_operand_map(&ta, g.A, g.lda, a_mn, g.M, g.K)) {
+      std::size_t ldp = g.lda;
+      g.A = pad(g.A, g.lda, a_mn, g.M, pad_a, ldp);
+      g.lda = ldp;
+    }
+    if (!make_operand_map(&tb, g.B, g.ldb, b_mn, g.N, g.K)) {
+      std::size_t ldp = g.ldb;
+      g.B = pad(g.B, g.ldb, b_mn, g.N, pad_b, ldp);
+      g.ldb = ldp;
+    }
+    auto release = [&] {
+      if (pad_a) cudaFreeAsync(pad_a, st);
+      if (pad_b) cudaFreeAsync(pad_b, st);
+    };
     if (make_operand_map(&ta, g.A, g.lda, a_mn, g.M, g.K) && make_operand_map(&tb, g.B, g.ldb, b_mn, g.N, g.K)) {
       static bool attr = false;
       if (!attr) {
@@ -563,8 +596,11 @@ cudaError_t launch_gemm_umma(const GemmArgs<float>& g0, std::uint32_t splits, cu
       }
       const dim3 grid((g.M + BM - 1) / BM, (g.N + BN - 1) / BN, g.epi == kEpiSplitK ? splits : 1);
       k_umma_tma<<<grid, kTThreads, kTSmem, st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0);
-      return cudaGetLastError();
+      const cudaError_t e = cudaGetLastError();
+      release();
+      return e;
     }
+    release();
   }
   const GemmArgs<float>& g = g0;
   // register-staged fallback (operands TMA cannot describe): its accumulator
