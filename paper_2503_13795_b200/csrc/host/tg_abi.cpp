@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <chrono>
+#include <map>
 #include <memory>
 #include <new>
 #include <stdexcept>
@@ -149,6 +150,14 @@ struct tg_program {
   std::vector<DensePlan> dplan;
   std::vector<std::uint32_t> gen_dests;
   std::uint32_t* d_gen_dests = nullptr;
+  // table-scatter dests (all terms kind 1) as histograms per (adjoint row, index column)
+  std::vector<tgk::ScatterGroup> sc_groups;
+  std::vector<tgk::ScatterUse> sc_uses;
+  std::vector<std::uint32_t> sc_use_off, sc_dests;
+  std::uint32_t sc_rmax = 0, sc_chunks = 1;
+  tgk::ScatterGroup* d_sc_groups = nullptr;
+  tgk::ScatterUse* d_sc_uses = nullptr;
+  std::uint32_t *d_sc_use_off = nullptr, *d_sc_dests = nullptr;
   std::size_t chunk = 0;          // samples per chunk (0 = by batch)
   bool umma = true;               // fp32 dense layers on tcgen05 (3xTF32); TG_UMMA=0 -> SIMT GEMM
   ~tg_program() {
@@ -220,7 +229,42 @@ void build_staged_plan(tg_program& pr) {
         if (P.oflag[D.x_opnd + k] & tgc::kAssign) dp.zero_x.push_back(dp.xrow0 + k);
   }
   pr.gen_dests.clear();
-  for (std::uint32_t d = 0; d < P.dest_uv.size(); ++d) if (!covered[d]) pr.gen_dests.push_back(d);
+  pr.sc_groups.clear();
+  pr.sc_uses.clear();
+  pr.sc_use_off.assign(1, 0);
+  pr.sc_dests.clear();
+  pr.sc_rmax = 0;
+  std::map<std::pair<std::uint32_t, std::uint32_t>, std::uint32_t> group_of;
+  const std::uint32_t r_cap = pr.tsz() == 8 ? 192 : 384;   // bins[R][128] in shared memory
+  for (std::uint32_t d = 0; d < P.dest_uv.size(); ++d) {
+    if (covered[d]) continue;
+    bool scatter = P.term_off[d + 1] > P.term_off[d];
+    for (std::uint32_t q = P.term_off[d]; q < P.term_off[d + 1] && scatter; ++q)
+      scatter = P.terms[q].kind == 1 && P.terms[q].row >= 0 && static_cast<std::uint32_t>(P.terms[q].row) < r_cap;
+    if (!scatter) {
+      pr.gen_dests.push_back(d);
+      continue;
+    }
+    for (std::uint32_t q = P.term_off[d]; q < P.term_off[d + 1]; ++q) {
+      const tgc::Term& t = P.terms[q];
+      const auto key = std::make_pair(t.a, t.f);
+      auto it = group_of.find(key);
+      if (it == group_of.end()) {
+        it = group_of.emplace(key, static_cast<std::uint32_t>(pr.sc_groups.size())).first;
+        pr.sc_groups.push_back({t.a, t.f, 0, 0});
+      }
+      tgk::ScatterGroup& g = pr.sc_groups[it->second];
+      g.rows = std::max<std::uint32_t>(g.rows, static_cast<std::uint32_t>(t.row) + 1);
+      pr.sc_uses.push_back({it->second, static_cast<std::uint32_t>(t.row), t.coef});
+    }
+    pr.sc_dests.push_back(d);
+    pr.sc_use_off.push_back(static_cast<std::uint32_t>(pr.sc_uses.size()));
+  }
+  for (const auto& g : pr.sc_groups) pr.sc_rmax = std::max(pr.sc_rmax, g.rows);
+  // sample chunks: about four CTAs per SM over all groups
+  pr.sc_chunks = pr.sc_groups.empty() ? 1 : std::max<std::uint32_t>(
+      1, std::min<std::uint32_t>(256, (592 + static_cast<std::uint32_t>(pr.sc_groups.size()) - 1) /
+                                          static_cast<std::uint32_t>(pr.sc_groups.size())));
   auto split = [&](const std::vector<tgc::Instr>& list, std::vector<tg_program::Stage>& out) {
     out.clear();
     std::uint32_t b = 0;
@@ -306,7 +350,7 @@ std::size_t grid_for(const tg_program& pr, std::size_t batch) {
 std::size_t align_up(std::size_t x) { return (x + 255) & ~std::size_t(255); }
 
 struct Layout {
-  std::size_t done, uv, ug, partial, gv, gg, sk, total;
+  std::size_t done, uv, ug, partial, gv, gg, sk, sp, total;
 };
 Layout layout(const tg_program& pr, std::size_t batch) {
   const std::size_t t = pr.tsz();
@@ -325,6 +369,7 @@ Layout layout(const tg_program& pr, std::size_t batch) {
       if (pr.dplan[i].gemm && pr.dplan[i].dw_dest0 != tgc::kNone)
         sk = std::max<std::size_t>(sk, std::size_t(splitk_splits(pr.P.dense[i], cb, t)) * pr.P.dense[i].n_out * pr.P.dense[i].n_in);
     L.sk = off; off = align_up(off + std::max<std::size_t>(1, sk) * t);
+    L.sp = off; off = align_up(off + std::max<std::size_t>(1, std::size_t(pr.sc_groups.size()) * pr.sc_chunks * pr.sc_rmax) * t);
     L.total = off;
     return L;
   }
@@ -413,6 +458,10 @@ tg_status upload(tg_program& pr) {
   if (!pr.staged && !(env && env[0] == '0') && tgj::eligible(P)) pr.jit = tgj::build(P);
   if (pr.staged) {
     TG_TRY(upload_vec(pr, pr.gen_dests, &pr.d_gen_dests));
+    TG_TRY(upload_vec(pr, pr.sc_groups, &pr.d_sc_groups));
+    TG_TRY(upload_vec(pr, pr.sc_uses, &pr.d_sc_uses));
+    TG_TRY(upload_vec(pr, pr.sc_use_off, &pr.d_sc_use_off));
+    TG_TRY(upload_vec(pr, pr.sc_dests, &pr.d_sc_dests));
     for (auto& dp : pr.dplan) TG_TRY(upload_vec(pr, dp.zero_x, &dp.d_zero_x));
   }
   if (env && env[0] == 'v' && !pr.jit.ok) std::fprintf(stderr, "[tg] JIT not used: %s\n", pr.jit.log.c_str());
@@ -669,9 +718,18 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
       TG_CUDA_TRY(tgk::launch_tape_range<T>(ra, st));
       ++pr.launches;
     }
-    TG_CUDA_TRY(tgk::launch_contract<T>(pr.d_gen_dests, static_cast<std::uint32_t>(pr.gen_dests.size()), pr.d_termoff,
-                                        pr.d_terms, G, V, idx, batch, s0, n, cb, acc, st));
-    ++pr.launches;
+    if (!pr.gen_dests.empty()) {
+      TG_CUDA_TRY(tgk::launch_contract<T>(pr.d_gen_dests, static_cast<std::uint32_t>(pr.gen_dests.size()), pr.d_termoff,
+                                          pr.d_terms, G, V, idx, batch, s0, n, cb, acc, st));
+      ++pr.launches;
+    }
+    if (!pr.sc_groups.empty()) {
+      TG_CUDA_TRY(tgk::launch_scatter<T>(pr.d_sc_groups, static_cast<std::uint32_t>(pr.sc_groups.size()), pr.sc_rmax,
+                                         pr.d_sc_uses, pr.d_sc_use_off, pr.d_sc_dests,
+                                         static_cast<std::uint32_t>(pr.sc_dests.size()), G, idx, batch, s0, n, cb,
+                                         reinterpret_cast<T*>(w + L.sp), pr.sc_chunks, acc, st));
+      pr.launches += 2;
+    }
   }
   if (e1) TG_CUDA_TRY(cudaEventRecord(e1, st));
   // fused: acc -> UG -> uniform reverse sweep -> grad_sum (-> GD)

@@ -274,15 +274,26 @@ __global__ void k_act_bwd(T* G, const T* V, std::uint32_t z_row, std::uint32_t h
   const std::size_t s = std::size_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (s >= n) return;
   const std::size_t zr = std::size_t(z_row + blockIdx.y) * ld + s, hr = std::size_t(h_row + blockIdx.y) * ld + s;
-  G[zr] = act_bwd<T>(act, G[hr], V[hr], V[zr]);
+  // tanh / sigmoid / exp derivatives use the output only: skip the z read (a quarter of the bytes)
+  const bool need_z = act == Relu || act == Sqr || act == Cub;
+  G[zr] = act_bwd<T>(act, G[hr], V[hr], need_z ? V[zr] : T(0));
 }
 
 template <class T>
 __global__ void __launch_bounds__(256) k_rowsum(const T* G, std::uint32_t row0, std::size_t n, std::size_t ld, T* dst) {
   __shared__ T red[256];
   const T* row = G + std::size_t(row0 + blockIdx.x) * ld;
+  // 8 loads in flight per thread, summed in sequential order (deterministic)
   T t = 0;
-  for (std::size_t s = threadIdx.x; s < n; s += 256) t += row[s];
+  std::size_t s = threadIdx.x;
+  for (; s + 7 * 256 < n; s += 8 * 256) {
+    T x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = row[s + u * 256];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t += x[u];
+  }
+  for (; s < n; s += 256) t += row[s];
   red[threadIdx.x] = t;
   __syncthreads();
   for (int o = 128; o > 0; o >>= 1) {
@@ -331,7 +342,75 @@ __global__ void __launch_bounds__(256) k_contract(const std::uint32_t* dests, co
   if (threadIdx.x == 0) acc[d] += red[0];
 }
 
+// Table-scatter contraction as histograms (cfg3 / cfg4 embedding gradients).
+// Group g = (adjoint row a, index column f, rows R): H_g[r] = sum_s [idx[f][s]
+// == r] G[a][s].  Every thread accumulates its samples (in order) into its own
+// shared-memory column bins[r][thread]; each bin row is then reduced in a
+// fixed order, giving per-chunk partials part[g][chunk][r].  k_contract's
+// one-CTA-per-destination scan read every G row once per table row.
+template <class T>
+__global__ void __launch_bounds__(128) k_scatter_hist(const ScatterGroup* groups, const T* G, const std::int32_t* idx,
+                                                       std::size_t batch, std::size_t s0, std::size_t n, std::size_t ld,
+                                                       std::uint32_t n_chunks, std::uint32_t r_max, T* part) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* bins = reinterpret_cast<T*>(smem_raw);
+  const ScatterGroup gp = groups[blockIdx.x];
+  const std::uint32_t tid = threadIdx.x, chunk = blockIdx.y;
+  for (std::uint32_t r = 0; r < gp.rows; ++r) bins[r * 128 + tid] = T(0);
+  const std::size_t lo = n * chunk / n_chunks, hi = n * (chunk + 1) / n_chunks;
+  const T* ga = G + std::size_t(gp.a) * ld;
+  const std::int32_t* ix = idx + std::size_t(gp.f) * batch + s0;
+  for (std::size_t s = lo + tid; s < hi; s += 128) {
+    const std::int32_t r = ix[s];
+    if (static_cast<std::uint32_t>(r) < gp.rows) bins[r * 128 + tid] += ga[s];
+  }
+  __syncthreads();
+  const std::uint32_t warp = tid >> 5, lane = tid & 31;
+  for (std::uint32_t r = warp; r < gp.rows; r += 4) {
+    const T* b = bins + r * 128;
+    T t = ((b[lane] + b[lane + 32]) + (b[lane + 64] + b[lane + 96]));
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
+    if (lane == 0) part[(std::size_t(blockIdx.x) * n_chunks + chunk) * r_max + r] = t;
+  }
+}
+
+// acc[dest] += sum over the dest's uses (g, r, coef) of coef * sum_chunks part[g][chunk][r]   (fixed order)
+template <class T>
+__global__ void k_scatter_apply(const ScatterUse* uses, const std::uint32_t* use_off, const std::uint32_t* dests,
+                                std::uint32_t n_dests, const T* part, std::uint32_t n_chunks, std::uint32_t r_max, T* acc) {
+  const std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_dests) return;
+  T tot = 0;
+  for (std::uint32_t u = use_off[i]; u < use_off[i + 1]; ++u) {
+    const ScatterUse su = uses[u];
+    T h = 0;
+    for (std::uint32_t c = 0; c < n_chunks; ++c) h += part[(std::size_t(su.g) * n_chunks + c) * r_max + su.r];
+    tot += static_cast<T>(su.coef) * h;
+  }
+  acc[dests[i]] += tot;
+}
+
 }  // namespace
+
+template <class T>
+cudaError_t launch_scatter(const ScatterGroup* groups, std::uint32_t n_groups, std::uint32_t r_max, const ScatterUse* uses,
+                           const std::uint32_t* use_off, const std::uint32_t* dests, std::uint32_t n_dests, const T* G,
+                           const std::int32_t* idx, std::size_t batch, std::size_t s0, std::size_t n, std::size_t ld,
+                           T* part, std::uint32_t n_chunks, T* acc, cudaStream_t st) {
+  if (n_groups == 0 || n == 0) return cudaSuccess;
+  const std::size_t smem = std::size_t(r_max) * 128 * sizeof(T);
+  static bool attr[2] = {false, false};
+  bool& a = attr[sizeof(T) == 8];
+  if (!a && smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(k_scatter_hist<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+    a = true;
+  }
+  k_scatter_hist<T><<<dim3(n_groups, n_chunks), 128, smem, st>>>(groups, G, idx, batch, s0, n, ld, n_chunks, r_max, part);
+  k_scatter_apply<T><<<(n_dests + 127) / 128, 128, 0, st>>>(uses, use_off, dests, n_dests, part, n_chunks, r_max, acc);
+  return cudaGetLastError();
+}
 
 template <class T>
 cudaError_t launch_tape_range(const RangeArgs<T>& a, cudaStream_t st) {
@@ -403,7 +482,11 @@ cudaError_t launch_contract(const std::uint32_t* dests, std::uint32_t n_dests, c
                                            cudaStream_t);                                                                  \
   template cudaError_t launch_contract<T>(const std::uint32_t*, std::uint32_t, const std::uint32_t*, const Term*,          \
                                           const T*, const T*, const std::int32_t*, std::size_t, std::size_t, std::size_t,  \
-                                          std::size_t, T*, cudaStream_t);
+                                          std::size_t, T*, cudaStream_t);                                                   \
+  template cudaError_t launch_scatter<T>(const ScatterGroup*, std::uint32_t, std::uint32_t, const ScatterUse*,             \
+                                         const std::uint32_t*, const std::uint32_t*, std::uint32_t, const T*,               \
+                                         const std::int32_t*, std::size_t, std::size_t, std::size_t, std::size_t, T*,      \
+                                         std::uint32_t, T*, cudaStream_t);
 TG_STAGED_INST(float)
 TG_STAGED_INST(double)
 

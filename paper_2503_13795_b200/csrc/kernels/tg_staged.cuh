@@ -76,6 +76,20 @@ struct GemmArgs {
   int epi;
 };
 
+// Table-scatter (kind-1) batch terms grouped by (adjoint row a, index column f).
+struct ScatterGroup {
+  std::uint32_t a, f, rows, pad;
+};
+struct ScatterUse {          // dest += coef * H_g[r]
+  std::uint32_t g, r;
+  double coef;
+};
+template <class T>
+cudaError_t launch_scatter(const ScatterGroup* groups, std::uint32_t n_groups, std::uint32_t r_max, const ScatterUse* uses,
+                           const std::uint32_t* use_off, const std::uint32_t* dests, std::uint32_t n_dests, const T* G,
+                           const std::int32_t* idx, std::size_t batch, std::size_t s0, std::size_t n, std::size_t ld,
+                           T* part, std::uint32_t n_chunks, T* acc, cudaStream_t st);
+
 template <class T> cudaError_t launch_tape_range(const RangeArgs<T>& a, cudaStream_t st);
 template <class T> cudaError_t launch_gemm(const GemmArgs<T>& g, std::uint32_t splits, cudaStream_t st);
 // fp32 GEMM on the 5th-gen tensor cores (tcgen05.mma kind::tf32, 3xTF32 split), tg_umma.cu

@@ -217,10 +217,13 @@ __global__ void __launch_bounds__(128, 1) k_umma_tf32x3(GemmArgs<float> g) {
 // (warp w reads TMEM lanes 32 (w % 4) ..).  A 3-stage ring of mbarriers:
 // full (TMA bytes landed) -> conv (128 converter threads done) -> empty
 // (tcgen05.commit: the MMAs that read the stage retired).
-constexpr int kTStages = 3;
+constexpr int kTStagesMax = 3;
 constexpr std::uint32_t kTTile = BM * BK * 4;                   // 16 KB: one operand tile
 constexpr std::uint32_t kTStage = 4 * kTTile;                   // A hi, A lo, B hi, B lo
-constexpr std::uint32_t kTSmem = kTStages * kTStage + 1024 + 512;
+// dynamic shared memory of a STAGES-deep ring (at least the staged-epilogue tile)
+__host__ __device__ constexpr std::uint32_t tma_smem(int stages) {
+  return (stages * kTStage > BM * (BN + 4) * 4 ? stages * kTStage : BM * (BN + 4) * 4) + 1024 + 512;
+}
 
 struct TmaOperand {
   bool mn;   // MN-major (m / n contiguous) vs K-major
@@ -290,6 +293,7 @@ __device__ int g_umma_exp = 0;   // profiling ablations (wrong results): 1 skip 
 constexpr int kConvThreads = 256;                 // 8 converter / drain warps
 constexpr int kTThreads = 64 + kConvThreads;      // + TMA producer + MMA issuer
 
+template <int kTStages>
 __global__ void __launch_bounds__(kTThreads, 1) k_umma_tma(GemmArgs<float> g, const __grid_constant__ CUtensorMap tmA,
                                                      const __grid_constant__ CUtensorMap tmB, int a_mn, int b_mn) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -297,7 +301,8 @@ __global__ void __launch_bounds__(kTThreads, 1) k_umma_tma(GemmArgs<float> g, co
   // shared array (an integer round trip would turn every converter access
   // into a generic LD/ST instead of LDS/STS)
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + kTStages * kTStage);
+  // barriers after the ring (or after the epilogue tile, whichever is larger)
+  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + tma_smem(kTStages) - 1024 - 512);
   std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 3 * kTStages + 4);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   auto full = [&](int s) { return smem_u32(&bars[s]); };
@@ -590,12 +595,21 @@ cudaError_t launch_gemm_umma(const GemmArgs<float>& g0, std::uint32_t splits, cu
     if (make_operand_map(&ta, g.A, g.lda, a_mn, g.M, g.K) && make_operand_map(&tb, g.B, g.ldb, b_mn, g.N, g.K)) {
       static bool attr = false;
       if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_umma_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTSmem));
-        if (e != cudaSuccess) return e;
+        for (cudaError_t e : {cudaFuncSetAttribute(k_umma_tma<kTStagesMax>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(tma_smem(kTStagesMax))),
+                              cudaFuncSetAttribute(k_umma_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(tma_smem(1)))})
+          if (e != cudaSuccess) return e;
         attr = true;
       }
       const dim3 grid((g.M + BM - 1) / BM, (g.N + BN - 1) / BN, g.epi == kEpiSplitK ? splits : 1);
-      k_umma_tma<<<grid, kTThreads, kTSmem, st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0);
+      // one k-tile per CTA (K <= 32): a 1-stage ring, so two CTAs share an SM
+      // and one's TMA / epilogue latency hides behind the other's work
+      const std::uint32_t kspan = g.epi == kEpiSplitK ? g.k_chunk : g.K;
+      if (kspan <= static_cast<std::uint32_t>(BK))
+        k_umma_tma<1><<<grid, kTThreads, tma_smem(1), st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0);
+      else
+        k_umma_tma<kTStagesMax><<<grid, kTThreads, tma_smem(kTStagesMax), st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0);
       const cudaError_t e = cudaGetLastError();
       release();
       return e;
