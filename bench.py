@@ -279,8 +279,10 @@ def main():
     value = b * world / (ms * 1e-3)
 
     # ---- dominant kernel time (CUDA events around the tape kernel) ----
+    # long steps (cfg4 / cfg5 at full batch): bounded extra passes (~5 s each)
+    cap = max(3, int(5000.0 / max(ms, 1e-3)))
     prog.profile(True)
-    for _ in range(max(args.steps // 4, 10)):
+    for _ in range(min(max(args.steps // 4, 10), cap)):
         flush.zero_()
         step()
     tape_ms, tape_n = prog.profile_read()
@@ -329,7 +331,7 @@ def main():
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    n_e2e = max(args.steps, 100)
+    n_e2e = min(max(args.steps, 100), cap)
     windows = []
     for _ in range(int(os.environ.get("TG_E2E_WINDOWS", "1"))):
         e0.record(stream)

@@ -136,7 +136,9 @@ struct tg_program {
   // register-resident specialisation (tg_jit.cpp)
   tgj::JitKernel jit;
   // staged execution over an HBM SoA workspace (large tapes, dense layers as GEMMs)
-  struct Stage { int dense; std::uint32_t begin, end; };     // dense >= 0: GEMM stage of that group
+  struct Stage { int dense; std::uint32_t begin, end; bool level = false; };   // dense >= 0: GEMM stage; level: one
+                                                                              // instruction per CTA column (k_level_range)
+  bool levels = false;            // staged lists reordered into dependency levels (TG_STAGED_LEVELS=0: off)
   struct DensePlan {
     bool gemm = false;
     std::uint32_t xrow0 = 0;
@@ -176,6 +178,146 @@ constexpr unsigned kMaxOcc = 32;
 
 // Dense layers with consecutive x rows run as GEMMs over the chunk; the rest of
 // the instruction stream runs on the interpreter in ranges between them.
+// Dependency-level schedule of the staged instruction lists.  Outside the
+// dense layers the staged interpreter ran one thread per sample through every
+// instruction of a range: for cfg4 (~6e5 nodes per sample) that is a serial,
+// latency-bound walk with only `batch` threads in flight.  Here the forward
+// list is stably sorted by dependency level (instructions of one level are
+// independent) and the reverse list by (reverse level, sub-level), where a
+// sub-level never holds two instructions pushing into the same adjoint row,
+// so one launch per level runs every instruction of the level on every sample
+// without atomics and in a fixed order.  Assign flags are recomputed for the
+// new order; rows reachable from a slot gather only ever accumulate and are
+// zeroed at the seed.  Both orders stay valid sequential orders, so the
+// interpreter (domain-error diagnosis) runs them unchanged.
+void level_schedule(tgc::Program& P, const std::vector<char>& gemm_dense) {
+  const std::uint32_t R = P.n_rows;
+  auto slot_rows = [&](std::uint32_t op, std::vector<std::uint32_t>& out) {
+    const std::uint32_t m = op >> tgc::kModeShift, i = op & tgc::kIndexMask;
+    if (m == tgc::kSlot) out.push_back(i);
+    else if (m == tgc::kSGather) {
+      const tgc::GatherTable& t = P.sgather[i];
+      for (std::uint32_t r = 0; r < t.n_rows; ++r) out.push_back(P.cand[t.cand_off + r]);
+    }
+  };
+  // ---- forward ----
+  std::vector<std::uint32_t> row_level(R, 0), lvl(P.fwd.size(), 0), rows;
+  for (std::size_t k = 0; k < P.fwd.size(); ++k) {
+    const tgc::Instr& in = P.fwd[k];
+    rows.clear();
+    if (in.kind == tgc::kNode) for (std::uint32_t j = 0; j < in.nops; ++j) slot_rows(P.opnd[in.opnd + j], rows);
+    if (in.kind == tgc::kDense) {
+      const tgc::Dense& D = P.dense[in.aux];
+      for (std::uint32_t j = 0; j < D.n_in; ++j) slot_rows(P.opnd[D.x_opnd + j], rows);
+    }
+    std::uint32_t L = 0;
+    for (std::uint32_t r : rows) L = std::max(L, row_level[r] + 1);
+    lvl[k] = L;
+    if (in.kind == tgc::kDense) {
+      const tgc::Dense& D = P.dense[in.aux];
+      for (std::uint32_t j = 0; j < D.n_out; ++j) {
+        row_level[D.out_row + j] = L;
+        if (D.act_op) row_level[D.act_row + j] = L;
+      }
+    } else {
+      row_level[in.out] = L;
+    }
+  }
+  std::vector<std::uint32_t> ord(P.fwd.size());
+  for (std::uint32_t k = 0; k < ord.size(); ++k) ord[k] = k;
+  auto is_gemm = [&](const tgc::Instr& in) { return in.kind == tgc::kDense && gemm_dense[in.aux]; };
+  // within a level the interpreter instructions first, then the GEMM stages
+  std::stable_sort(ord.begin(), ord.end(), [&](std::uint32_t a, std::uint32_t b) {
+    if (lvl[a] != lvl[b]) return lvl[a] < lvl[b];
+    return !is_gemm(P.fwd[a]) && is_gemm(P.fwd[b]);
+  });
+  std::vector<tgc::Instr> nf(P.fwd.size());
+  std::vector<std::uint32_t> nlvl(P.fwd.size());
+  for (std::size_t k = 0; k < ord.size(); ++k) { nf[k] = P.fwd[ord[k]]; nlvl[k] = lvl[ord[k]]; }
+  P.fwd.swap(nf);
+  P.fwd_level = nlvl;
+  // ---- reverse: level = 1 + max level of the instructions pushing into the rows it reads ----
+  std::vector<std::uint32_t> pushed_level(R, 0), rl(P.bwd.size(), 0), sub(P.bwd.size(), 0);
+  std::vector<char> has_push(R, 0);
+  std::vector<std::vector<std::uint32_t>> targets(P.bwd.size());
+  for (std::size_t k = 0; k < P.bwd.size(); ++k) {
+    const tgc::Instr& in = P.bwd[k];
+    rows.clear();
+    if (in.kind == tgc::kDense) {
+      const tgc::Dense& D = P.dense[in.aux];
+      for (std::uint32_t j = 0; j < D.n_out; ++j) rows.push_back(D.act_op ? D.act_row + j : D.out_row + j);
+      for (std::uint32_t j = 0; j < D.n_in; ++j) slot_rows(P.opnd[D.x_opnd + j], targets[k]);
+    } else {
+      rows.push_back(in.out);
+      for (std::uint32_t j = 0; j < in.nops; ++j) {
+        const std::uint32_t op = P.opnd[in.opnd + j];
+        if ((op >> tgc::kModeShift) == tgc::kUv) {
+          if (P.oflag[in.opnd + j] & tgc::kToAux) targets[k].push_back(P.oaux[in.opnd + j]);
+        } else {
+          slot_rows(op, targets[k]);
+        }
+      }
+    }
+    std::uint32_t L = 0;
+    for (std::uint32_t r : rows) if (has_push[r]) L = std::max(L, pushed_level[r] + 1);
+    rl[k] = L;
+    for (std::uint32_t t : targets[k]) {
+      pushed_level[t] = has_push[t] ? std::max(pushed_level[t], L) : L;
+      has_push[t] = 1;
+    }
+  }
+  // sub-levels: no two instructions of one sub-level push into the same row
+  std::unordered_map<std::uint64_t, std::uint32_t> last_sub;   // (level, row) -> last sub-level used
+  for (std::size_t k = 0; k < P.bwd.size(); ++k) {
+    std::uint32_t sl = 0;
+    for (std::uint32_t t : targets[k]) {
+      auto it = last_sub.find((std::uint64_t(rl[k]) << 32) | t);
+      if (it != last_sub.end()) sl = std::max(sl, it->second + 1);
+    }
+    sub[k] = sl;
+    for (std::uint32_t t : targets[k]) last_sub[(std::uint64_t(rl[k]) << 32) | t] = sl;
+  }
+  std::vector<std::uint32_t> bo(P.bwd.size());
+  for (std::uint32_t k = 0; k < bo.size(); ++k) bo[k] = k;
+  std::stable_sort(bo.begin(), bo.end(), [&](std::uint32_t a, std::uint32_t b) {
+    if (rl[a] != rl[b]) return rl[a] < rl[b];
+    if (sub[a] != sub[b]) return sub[a] < sub[b];
+    return !is_gemm(P.bwd[a]) && is_gemm(P.bwd[b]);
+  });
+  std::vector<tgc::Instr> nb(P.bwd.size());
+  std::vector<std::uint32_t> nbl(P.bwd.size());
+  for (std::size_t k = 0; k < bo.size(); ++k) {
+    nb[k] = P.bwd[bo[k]];
+    nbl[k] = (rl[bo[k]] << 12) | std::min<std::uint32_t>(sub[bo[k]], 4095);   // stage key
+  }
+  P.bwd.swap(nb);
+  P.bwd_level = nbl;
+  // ---- first-write (assign) flags for the new reverse order ----
+  std::vector<char> gather_target(R, 0), seen(R, 0);
+  for (const auto& t : P.sgather)
+    for (std::uint32_t r = 0; r < t.n_rows; ++r) gather_target[P.cand[t.cand_off + r]] = 1;
+  auto flag = [&](std::uint32_t pos) {
+    const std::uint32_t op = P.opnd[pos];
+    if ((op >> tgc::kModeShift) != tgc::kSlot) return;
+    const std::uint32_t r = op & tgc::kIndexMask;
+    if (!seen[r] && !gather_target[r]) P.oflag[pos] |= tgc::kAssign;
+    else P.oflag[pos] &= static_cast<std::uint8_t>(~tgc::kAssign);
+    seen[r] = 1;
+  };
+  for (const tgc::Instr& in : P.bwd) {
+    if (in.kind == tgc::kDense) {
+      const tgc::Dense& D = P.dense[in.aux];
+      for (std::uint32_t j = 0; j < D.n_in; ++j) flag(D.x_opnd + j);
+    } else {
+      for (std::uint32_t j = 0; j < in.nops; ++j) flag(in.opnd + j);
+    }
+  }
+  std::vector<char> zero(R, 0);
+  for (std::uint32_t r : P.zero_rows) zero[r] = 1;
+  for (std::uint32_t r = 0; r < R; ++r)
+    if (gather_target[r] && !zero[r]) P.zero_rows.push_back(r);
+}
+
 void build_staged_plan(tg_program& pr) {
   const tgc::Program& P = pr.P;
   const char* env = std::getenv("TG_STAGED");
@@ -195,6 +337,15 @@ void build_staged_plan(tg_program& pr) {
   pr.staged = env ? env[0] == '1' : (big && !tgj::eligible(P));
   if (const char* u = std::getenv("TG_UMMA")) pr.umma = u[0] != '0';
   if (!pr.staged || P.root_row == tgc::kNone) { pr.staged = false; return; }
+  {
+    const char* lv = std::getenv("TG_STAGED_LEVELS");
+    pr.levels = !(lv && lv[0] == '0');
+    if (pr.levels) {
+      std::vector<char> gd(P.dense.size(), 0);
+      for (std::size_t i = 0; i < P.dense.size(); ++i) gd[i] = pr.dplan[i].gemm ? 1 : 0;
+      level_schedule(pr.P, gd);
+    }
+  }
   // weight / bias gradient destinations handled by the GEMM path
   std::vector<std::uint8_t> covered(P.dest_uv.size(), 0);
   std::unordered_map<std::uint32_t, std::uint32_t> dest_of_uv;
@@ -265,26 +416,39 @@ void build_staged_plan(tg_program& pr) {
   pr.sc_chunks = pr.sc_groups.empty() ? 1 : std::max<std::uint32_t>(
       1, std::min<std::uint32_t>(256, (592 + static_cast<std::uint32_t>(pr.sc_groups.size()) - 1) /
                                           static_cast<std::uint32_t>(pr.sc_groups.size())));
-  auto split = [&](const std::vector<tgc::Instr>& list, std::vector<tg_program::Stage>& out) {
+  // stages: GEMM dense groups on their own; the rest either in instruction
+  // ranges (one thread per sample) or, with levels, one range per level key
+  auto split = [&](const std::vector<tgc::Instr>& list, const std::vector<std::uint32_t>& key,
+                   std::vector<tg_program::Stage>& out) {
     out.clear();
+    const bool lv = pr.levels && key.size() == list.size();
     std::uint32_t b = 0;
+    auto flush = [&](std::uint32_t e) {
+      if (e > b) out.push_back({-1, b, e, lv});
+      b = e;
+    };
     for (std::uint32_t k = 0; k < list.size(); ++k) {
       if (list[k].kind == tgc::kDense && pr.dplan[list[k].aux].gemm) {
-        if (k > b) out.push_back({-1, b, k});
-        out.push_back({static_cast<int>(list[k].aux), k, k + 1});
+        flush(k);
+        out.push_back({static_cast<int>(list[k].aux), k, k + 1, false});
         b = k + 1;
+      } else if (lv && k > b && key[k] != key[k - 1]) {
+        flush(k);
       }
     }
-    if (b < list.size()) out.push_back({-1, b, static_cast<std::uint32_t>(list.size())});
+    flush(static_cast<std::uint32_t>(list.size()));
   };
-  split(P.fwd, pr.sfwd);
-  split(P.bwd, pr.sbwd);
+  split(P.fwd, P.fwd_level, pr.sfwd);
+  split(P.bwd, P.bwd_level, pr.sbwd);
 }
 
 // Samples per chunk of the staged path: rows of V and G for the chunk within
-// ~4 GB (TG_STAGED_MB overrides), a multiple of 128.
+// 48 GB of the B200's 180 GB HBM (TG_STAGED_MB overrides), a multiple of 128.
+// One chunk covers cfg4 (b = 8,192, ~6e5 rows: 39 GB) and cfg5 (b = 1M:
+// 39 GB), so every stage runs once per step over the whole batch (a 4 GB
+// budget split cfg4 into ten chunks: 36k launches per step).
 std::size_t staged_chunk(const tg_program& pr, std::size_t batch) {
-  std::size_t budget = std::size_t(4096) << 20;
+  std::size_t budget = std::size_t(48) << 30;
   if (const char* e = std::getenv("TG_STAGED_MB")) budget = std::size_t(std::atoll(e)) << 20;
   const std::size_t per = 2 * std::max<std::size_t>(1, pr.P.n_rows) * pr.tsz();
   std::size_t cb = std::max<std::size_t>(128, (budget / per) / 128 * 128);
@@ -624,7 +788,7 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
         ra.flags = tgk::kRFwd;
         ra.fwd_begin = stg.begin;
         ra.fwd_end = stg.end;
-        TG_CUDA_TRY(tgk::launch_tape_range<T>(ra, st));
+        TG_CUDA_TRY(stg.level ? tgk::launch_level_range<T>(ra, st) : tgk::launch_tape_range<T>(ra, st));
       } else {
         const tgc::Dense& D = P.dense[stg.dense];
         const auto& dp = pr.dplan[stg.dense];
@@ -657,7 +821,7 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
         ra.flags = tgk::kRBwd;
         ra.bwd_begin = stg.begin;
         ra.bwd_end = stg.end;
-        TG_CUDA_TRY(tgk::launch_tape_range<T>(ra, st));
+        TG_CUDA_TRY(stg.level ? tgk::launch_level_range<T>(ra, st) : tgk::launch_tape_range<T>(ra, st));
         ++pr.launches;
         continue;
       }

@@ -149,6 +149,10 @@ struct Program {
   // processing order of the reference backward (recorded node ids)
   std::vector<std::uint32_t> order;
 
+  // staged tier with dependency levels (tg_abi.cpp level_schedule): stage key
+  // of each fwd / bwd instruction (level; reverse level << 12 | sub-level)
+  std::vector<std::uint32_t> fwd_level, bwd_level;
+
   std::uint32_t n_dense_nodes = 0;
   std::uint32_t n_sample_nodes = 0, n_uniform_nodes = 0;
 };

@@ -68,6 +68,75 @@ struct RowAccS {
   }
 };
 
+// One forward instruction for sample s (column col of the chunk rows).
+template <class T>
+__device__ __forceinline__ void fwd_instr(const RangeArgs<T>& a, RowAccS<T>& acc, std::uint32_t k, std::size_t s,
+                                          std::size_t col) {
+  T* V = a.V;
+  const std::size_t ld = a.ld;
+  const Instr in = a.fwd[k];
+  T v;
+  if (in.kind == tgc::kNode) {
+    acc.o = a.opnd + in.opnd;
+    bool bad = false;
+    T badv = 0;
+    v = eval_node<T>(in.op, in.nops, acc.o, in.cst, acc, bad, badv);
+    if (bad) record_error(a.err_key, s, in.node);
+  } else if (in.kind == tgc::kInputLoad) {
+    v = a.inputs[std::size_t(in.aux) * a.batch + s];
+  } else if (in.kind == tgc::kDense) {
+    const tgc::Dense D = a.dense[in.aux];
+    const std::uint32_t* xo = a.opnd + D.x_opnd;
+    for (std::uint32_t j = 0; j < D.n_out; ++j) {
+      T z = D.b_uv != tgc::kNone ? a.UV[D.b_uv + j] : T(0);
+      const T* w = a.UV + D.w_uv + std::size_t(j) * D.n_in;
+      for (std::uint32_t q = 0; q < D.n_in; ++q) z += V[std::size_t(xo[q] & kIndexMask) * ld + col] * w[q];
+      V[std::size_t(D.out_row + j) * ld + col] = z;
+      if (D.act_op) V[std::size_t(D.act_row + j) * ld + col] = act_fwd<T>(D.act_op, z);
+    }
+    return;
+  } else {
+    const GatherTable t = a.ug[in.aux];
+    std::int32_t r = a.idx[std::size_t(t.col) * a.batch + s];
+    if (r < 0 || static_cast<std::uint32_t>(r) >= t.n_rows) { record_error(a.err_key, s, 0xfffffffeu); r = 0; }
+    v = a.UV[a.cand[t.cand_off + r]];
+  }
+  V[std::size_t(in.out) * ld + col] = v;
+}
+
+// One reverse instruction for column col.
+template <class T>
+__device__ __forceinline__ void bwd_instr(const RangeArgs<T>& a, RowAccS<T>& acc, std::uint32_t k, std::size_t col) {
+  T* V = a.V;
+  T* G = a.G;
+  const std::size_t ld = a.ld;
+  const Instr in = a.bwd[k];
+  if (in.kind == tgc::kDense) {
+    const tgc::Dense D = a.dense[in.aux];
+    if (D.act_op)
+      for (std::uint32_t j = 0; j < D.n_out; ++j) {
+        const std::size_t hr = std::size_t(D.act_row + j) * ld + col, zr = std::size_t(D.out_row + j) * ld + col;
+        G[zr] = act_bwd<T>(D.act_op, G[hr], V[hr], V[zr]);
+      }
+    const std::uint32_t* xo = a.opnd + D.x_opnd;
+    const std::uint8_t* xf = a.oflag + D.x_opnd;
+    for (std::uint32_t q = 0; q < D.n_in; ++q) {
+      T dx = 0;
+      for (std::uint32_t j = 0; j < D.n_out; ++j)
+        dx += G[std::size_t(D.out_row + j) * ld + col] * a.UV[D.w_uv + std::size_t(j) * D.n_in + q];
+      T* p = &G[std::size_t(xo[q] & kIndexMask) * ld + col];
+      *p = (xf[q] & tgc::kAssign) ? dx : *p + dx;
+    }
+    return;
+  }
+  acc.o = a.opnd + in.opnd;
+  acc.fl = a.oflag + in.opnd;
+  acc.ax = a.oaux + in.opnd;
+  const T g = G[std::size_t(in.out) * ld + col];
+  const T y = V[std::size_t(in.out) * ld + col];
+  propagate<T>(in.op, in.nops, acc.o, in.cst, g, y, acc);
+}
+
 template <class T>
 __global__ void __launch_bounds__(128) k_tape_range(RangeArgs<T> a) {
   const std::size_t col = std::size_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -77,77 +146,33 @@ __global__ void __launch_bounds__(128) k_tape_range(RangeArgs<T> a) {
   T* G = a.G;
   const std::size_t ld = a.ld;
   RowAccS<T> acc{V, G, ld, col, a.UV, a.idx, a.batch, s, a.sg, a.cand, nullptr, nullptr, nullptr};
-  if (a.flags & kRFwd) {
-    for (std::uint32_t k = a.fwd_begin; k < a.fwd_end; ++k) {
-      const Instr in = a.fwd[k];
-      T v;
-      if (in.kind == tgc::kNode) {
-        acc.o = a.opnd + in.opnd;
-        bool bad = false;
-        T badv = 0;
-        v = eval_node<T>(in.op, in.nops, acc.o, in.cst, acc, bad, badv);
-        if (bad) record_error(a.err_key, s, in.node);
-      } else if (in.kind == tgc::kInputLoad) {
-        v = a.inputs[std::size_t(in.aux) * a.batch + s];
-      } else if (in.kind == tgc::kDense) {
-        const tgc::Dense D = a.dense[in.aux];
-        const std::uint32_t* xo = a.opnd + D.x_opnd;
-        for (std::uint32_t j = 0; j < D.n_out; ++j) {
-          T z = D.b_uv != tgc::kNone ? a.UV[D.b_uv + j] : T(0);
-          const T* w = a.UV + D.w_uv + std::size_t(j) * D.n_in;
-          for (std::uint32_t q = 0; q < D.n_in; ++q) z += V[std::size_t(xo[q] & kIndexMask) * ld + col] * w[q];
-          V[std::size_t(D.out_row + j) * ld + col] = z;
-          if (D.act_op) V[std::size_t(D.act_row + j) * ld + col] = act_fwd<T>(D.act_op, z);
-        }
-        continue;
-      } else {
-        const GatherTable t = a.ug[in.aux];
-        std::int32_t r = a.idx[std::size_t(t.col) * a.batch + s];
-        if (r < 0 || static_cast<std::uint32_t>(r) >= t.n_rows) { record_error(a.err_key, s, 0xfffffffeu); r = 0; }
-        v = a.UV[a.cand[t.cand_off + r]];
-      }
-      V[std::size_t(in.out) * ld + col] = v;
-    }
-  }
+  if (a.flags & kRFwd)
+    for (std::uint32_t k = a.fwd_begin; k < a.fwd_end; ++k) fwd_instr(a, acc, k, s, col);
   if (a.flags & kRSeed) {
     for (std::uint32_t z = 0; z < a.n_zero; ++z) G[std::size_t(a.zero_rows[z]) * ld + col] = T(0);
     if (a.loss) a.loss[s] = V[std::size_t(a.root_row) * ld + col];
     G[std::size_t(a.root_row) * ld + col] = T(1);
   }
-  if (a.flags & kRBwd) {
-    for (std::uint32_t k = a.bwd_begin; k < a.bwd_end; ++k) {
-      const Instr in = a.bwd[k];
-      if (in.kind == tgc::kDense) {
-        const tgc::Dense D = a.dense[in.aux];
-        if (D.act_op)
-          for (std::uint32_t j = 0; j < D.n_out; ++j) {
-            const std::size_t hr = std::size_t(D.act_row + j) * ld + col, zr = std::size_t(D.out_row + j) * ld + col;
-            G[zr] = act_bwd<T>(D.act_op, G[hr], V[hr], V[zr]);
-          }
-        const std::uint32_t* xo = a.opnd + D.x_opnd;
-        const std::uint8_t* xf = a.oflag + D.x_opnd;
-        for (std::uint32_t q = 0; q < D.n_in; ++q) {
-          T dx = 0;
-          for (std::uint32_t j = 0; j < D.n_out; ++j)
-            dx += G[std::size_t(D.out_row + j) * ld + col] * a.UV[D.w_uv + std::size_t(j) * D.n_in + q];
-          T* p = &G[std::size_t(xo[q] & kIndexMask) * ld + col];
-          *p = (xf[q] & tgc::kAssign) ? dx : *p + dx;
-        }
-        continue;
-      }
-      acc.o = a.opnd + in.opnd;
-      acc.fl = a.oflag + in.opnd;
-      acc.ax = a.oaux + in.opnd;
-      const T g = G[std::size_t(in.out) * ld + col];
-      const T y = V[std::size_t(in.out) * ld + col];
-      propagate<T>(in.op, in.nops, acc.o, in.cst, g, y, acc);
-    }
-  }
+  if (a.flags & kRBwd)
+    for (std::uint32_t k = a.bwd_begin; k < a.bwd_end; ++k) bwd_instr(a, acc, k, col);
   if ((a.flags & kROut) && a.igrad)
     for (std::uint32_t c = 0; c < a.n_inputs; ++c) {
       const std::uint32_t r = a.input_rows[c];
       if (r != tgc::kNone) a.igrad[std::size_t(c) * a.batch + s] = G[std::size_t(r) * ld + col];
     }
+}
+
+// One dependency level: instruction begin + blockIdx.x for the 128 samples of
+// blockIdx.y (instructions of a level are independent; in the reverse sweep no
+// two of them push into the same adjoint row).
+template <class T>
+__global__ void __launch_bounds__(128) k_level_range(RangeArgs<T> a) {
+  const std::size_t col = std::size_t(blockIdx.y) * blockDim.x + threadIdx.x;
+  if (col >= a.n) return;
+  const std::size_t s = a.s0 + col;
+  RowAccS<T> acc{a.V, a.G, a.ld, col, a.UV, a.idx, a.batch, s, a.sg, a.cand, nullptr, nullptr, nullptr};
+  if (a.flags & kRFwd) fwd_instr(a, acc, a.fwd_begin + blockIdx.x, s, col);
+  else bwd_instr(a, acc, a.bwd_begin + blockIdx.x, col);
 }
 
 // ---- register-tiled SIMT GEMM ------------------------------------------------
@@ -420,6 +445,14 @@ cudaError_t launch_tape_range(const RangeArgs<T>& a, cudaStream_t st) {
 }
 
 template <class T>
+cudaError_t launch_level_range(const RangeArgs<T>& a, cudaStream_t st) {
+  const std::uint32_t count = (a.flags & kRFwd) ? a.fwd_end - a.fwd_begin : a.bwd_end - a.bwd_begin;
+  if (a.n == 0 || count == 0) return cudaSuccess;
+  k_level_range<T><<<dim3(count, static_cast<unsigned>((a.n + 127) / 128)), 128, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <class T>
 cudaError_t launch_gemm(const GemmArgs<T>& g, std::uint32_t splits, cudaStream_t st) {
   constexpr int BM = GemmTile<T>::BM, BN = GemmTile<T>::BN;
   if (g.M == 0 || g.N == 0) return cudaSuccess;
@@ -472,6 +505,7 @@ cudaError_t launch_contract(const std::uint32_t* dests, std::uint32_t n_dests, c
 
 #define TG_STAGED_INST(T)                                                                                                  \
   template cudaError_t launch_tape_range<T>(const RangeArgs<T>&, cudaStream_t);                                            \
+  template cudaError_t launch_level_range<T>(const RangeArgs<T>&, cudaStream_t);                                           \
   template cudaError_t launch_gemm<T>(const GemmArgs<T>&, std::uint32_t, cudaStream_t);                                    \
   template cudaError_t launch_splitk_reduce<T>(const T*, T*, std::uint32_t, std::uint32_t, cudaStream_t);                  \
   template cudaError_t launch_act_bwd<T>(T*, const T*, std::uint32_t, std::uint32_t, std::uint32_t, std::size_t,           \

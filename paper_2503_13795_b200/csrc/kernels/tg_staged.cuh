@@ -91,6 +91,9 @@ cudaError_t launch_scatter(const ScatterGroup* groups, std::uint32_t n_groups, s
                            T* part, std::uint32_t n_chunks, T* acc, cudaStream_t st);
 
 template <class T> cudaError_t launch_tape_range(const RangeArgs<T>& a, cudaStream_t st);
+// One dependency level (fwd_begin/fwd_end with kRFwd, else bwd_begin/bwd_end):
+// one instruction per CTA column, 128 samples per CTA.
+template <class T> cudaError_t launch_level_range(const RangeArgs<T>& a, cudaStream_t st);
 template <class T> cudaError_t launch_gemm(const GemmArgs<T>& g, std::uint32_t splits, cudaStream_t st);
 // fp32 GEMM on the 5th-gen tensor cores (tcgen05.mma kind::tf32, 3xTF32 split), tg_umma.cu
 cudaError_t launch_gemm_umma(const GemmArgs<float>& g, std::uint32_t splits, cudaStream_t st);
