@@ -440,6 +440,32 @@ void build_staged_plan(tg_program& pr) {
   };
   split(P.fwd, P.fwd_level, pr.sfwd);
   split(P.bwd, P.bwd_level, pr.sbwd);
+  if (const char* v = std::getenv("TG_STAGED_VERBOSE"); v && v[0] == '1') {
+    std::size_t ng = 0;
+    for (std::size_t i = 0; i < P.dense.size(); ++i) {
+      ng += pr.dplan[i].gemm;
+      if (!pr.dplan[i].gemm)
+        std::fprintf(stderr, "[staged] dense %zu: %u x %u interpreted (x rows not consecutive)\n", i,
+                     P.dense[i].n_out, P.dense[i].n_in);
+    }
+    auto stats = [&](const char* name, const std::vector<tg_program::Stage>& st, const std::vector<tgc::Instr>& list) {
+      std::size_t nl = 0, ni = 0, nops = 0, small = 0;
+      for (const auto& s : st) {
+        if (s.dense >= 0) continue;
+        ++nl;
+        ni += s.end - s.begin;
+        small += (s.end - s.begin) < 128;
+        for (std::uint32_t k = s.begin; k < s.end; ++k)
+          nops += list[k].kind == tgc::kDense ? std::size_t(P.dense[list[k].aux].n_in) * P.dense[list[k].aux].n_out
+                                              : list[k].nops;
+      }
+      std::fprintf(stderr, "[staged] %s: %zu stages (%zu interpreter, %zu with <128 instrs), %zu instrs, %zu operands\n",
+                   name, st.size(), nl, small, ni, nops);
+    };
+    std::fprintf(stderr, "[staged] rows %u, dense %zu (%zu GEMM)\n", P.n_rows, P.dense.size(), ng);
+    stats("fwd", pr.sfwd, P.fwd);
+    stats("bwd", pr.sbwd, P.bwd);
+  }
 }
 
 // Samples per chunk of the staged path: rows of V and G for the chunk within

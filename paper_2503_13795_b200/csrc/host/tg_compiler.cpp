@@ -244,8 +244,58 @@ Program compile(const tg_tape_desc& d) {
       P.fwd.push_back(gl);
     }
   }
-  for (std::uint32_t i = 0; i < d.n_nodes; ++i)
-    if (c.cls[i] == cSample) { c.row[i] = nrow++; ++P.n_sample_nodes; }
+  // x-row blocks: the x operands of an inner product over a parameter row
+  // (a dense-layer candidate) get consecutive rows in operand order, so the
+  // staged tier can run the layer as one GEMM over a row block even when the
+  // producer interleaves them (layer-norm outputs, attention heads).  A block
+  // is placed where its first member appears; every other node keeps its
+  // order.  Rows are storage slots only: the numbering does not change any
+  // result.
+  std::vector<std::uint32_t> blk_of(d.n_nodes, kNone);
+  std::vector<std::vector<std::uint32_t>> blocks;
+  {
+    std::vector<std::uint8_t> mark(d.n_nodes, 0);
+    auto param_ip = [&](std::uint32_t i) {   // IP over a consecutive parameter row
+      if (c.cls[i] != cSample || (d.op[i] != IPNoBias && d.op[i] != IPWithBias)) return 0u;
+      const std::uint32_t n = c.nkids(i), m = d.op[i] == IPWithBias ? (n - 1) / 2 : n / 2;
+      const std::uint32_t* k = c.kids(i);
+      for (std::uint32_t j = 0; j < m; ++j) {
+        const std::uint32_t y = k[m + j];
+        if ((y & TG_GATHER_FLAG) || c.cls[y] != cParam || d.leaf_index[y] != d.leaf_index[k[m]] + j) return 0u;
+      }
+      return m;
+    };
+    for (std::uint32_t i = 0; i < d.n_nodes; ++i) {
+      const std::uint32_t m = param_ip(i);
+      if (m < 8) continue;
+      const std::uint32_t* k = c.kids(i);
+      bool ok = true, increasing = true;
+      for (std::uint32_t j = 0; ok && j < m; ++j) {
+        const std::uint32_t x = k[j];
+        ok = !(x & TG_GATHER_FLAG) && c.cls[x] == cSample && blk_of[x] == kNone && !mark[x];
+        if (ok) mark[x] = 1;
+        if (j && x <= k[j - 1]) increasing = false;
+      }
+      for (std::uint32_t j = 0; j < m; ++j) if (!(k[j] & TG_GATHER_FLAG)) mark[k[j]] = 0;
+      if (!ok) continue;   // shared with another block (or the same x list again)
+      // members that are themselves dense outputs keep their node order
+      if (!increasing)
+        for (std::uint32_t j = 0; ok && j < m; ++j) ok = param_ip(k[j]) == 0;
+      if (!ok) continue;
+      const std::uint32_t id = static_cast<std::uint32_t>(blocks.size());
+      blocks.emplace_back(k, k + m);
+      for (std::uint32_t j = 0; j < m; ++j) blk_of[k[j]] = id;
+    }
+  }
+  for (std::uint32_t i = 0; i < d.n_nodes; ++i) {
+    if (c.cls[i] != cSample || c.row[i] != kNone) continue;
+    if (blk_of[i] != kNone) {
+      for (std::uint32_t x : blocks[blk_of[i]]) { c.row[x] = nrow++; ++P.n_sample_nodes; }
+    } else {
+      c.row[i] = nrow++;
+      ++P.n_sample_nodes;
+    }
+  }
   // slot-gather candidate tables (rows are known now)
   for (std::uint32_t g = 0; g < d.n_gathers; ++g) {
     if (c.gkind[g] != 2) continue;
