@@ -136,8 +136,20 @@ struct tg_program {
   // register-resident specialisation (tg_jit.cpp)
   tgj::JitKernel jit;
   // staged execution over an HBM SoA workspace (large tapes, dense layers as GEMMs)
-  struct Stage { int dense; std::uint32_t begin, end; bool level = false; };   // dense >= 0: GEMM stage; level: one
+  struct Stage { int batch; std::uint32_t begin, end; bool level = false; };   // batch >= 0: GEMM stage; level: one
                                                                               // instruction per CTA column (k_level_range)
+  // Dense layers of one dependency level over the same weights (a GPT's 64
+  // positions): one launch per role with per-member row offsets.
+  struct Batch {
+    std::vector<std::uint32_t> members;   // dense ids, identical (w, b, n_out, n_in, act)
+    std::vector<uint4> tab;               // member rows: forward | input adjoints | weight gradient
+    uint4* d_tab = nullptr;
+    std::vector<std::uint32_t> zero_x;    // x adjoint rows zeroed before an accumulating dX
+    std::uint32_t* d_zero_x = nullptr;
+    int beta = 0;
+    bool bf = false, bx = false, bw = false;   // forward / dX / dW run batched (else per member)
+  };
+  std::vector<Batch> batches;
   bool levels = false;            // staged lists reordered into dependency levels (TG_STAGED_LEVELS=0: off)
   struct DensePlan {
     bool gemm = false;
@@ -227,9 +239,13 @@ void level_schedule(tgc::Program& P, const std::vector<char>& gemm_dense) {
   for (std::uint32_t k = 0; k < ord.size(); ++k) ord[k] = k;
   auto is_gemm = [&](const tgc::Instr& in) { return in.kind == tgc::kDense && gemm_dense[in.aux]; };
   // within a level the interpreter instructions first, then the GEMM stages
+  // grouped by weight block (adjacent layers over one weight form a batch)
+  auto gkey = [&](const tgc::Instr& in) -> std::uint64_t {
+    return is_gemm(in) ? 1 + std::uint64_t(P.dense[in.aux].w_uv) : 0;
+  };
   std::stable_sort(ord.begin(), ord.end(), [&](std::uint32_t a, std::uint32_t b) {
     if (lvl[a] != lvl[b]) return lvl[a] < lvl[b];
-    return !is_gemm(P.fwd[a]) && is_gemm(P.fwd[b]);
+    return gkey(P.fwd[a]) < gkey(P.fwd[b]);
   });
   std::vector<tgc::Instr> nf(P.fwd.size());
   std::vector<std::uint32_t> nlvl(P.fwd.size());
@@ -282,7 +298,7 @@ void level_schedule(tgc::Program& P, const std::vector<char>& gemm_dense) {
   std::stable_sort(bo.begin(), bo.end(), [&](std::uint32_t a, std::uint32_t b) {
     if (rl[a] != rl[b]) return rl[a] < rl[b];
     if (sub[a] != sub[b]) return sub[a] < sub[b];
-    return !is_gemm(P.bwd[a]) && is_gemm(P.bwd[b]);
+    return gkey(P.bwd[a]) < gkey(P.bwd[b]);
   });
   std::vector<tgc::Instr> nb(P.bwd.size());
   std::vector<std::uint32_t> nbl(P.bwd.size());
@@ -346,32 +362,66 @@ void build_staged_plan(tg_program& pr) {
       level_schedule(pr.P, gd);
     }
   }
-  // weight / bias gradient destinations handled by the GEMM path
+  // Weight / bias gradient destinations handled by the GEMM path.  Dense
+  // layers over one weight block (a GPT's positions) form a weight group; the
+  // group's dests are covered when every user runs as a GEMM and each dest's
+  // terms are exactly the users' products (dW[j][k]: G[out_u + j] . V[x_u + k];
+  // db[j]: G[out_u + j]), so the split-K GEMMs and row sums of the users
+  // accumulate the whole gradient.
   std::vector<std::uint8_t> covered(P.dest_uv.size(), 0);
   std::unordered_map<std::uint32_t, std::uint32_t> dest_of_uv;
   for (std::uint32_t d = 0; d < P.dest_uv.size(); ++d) dest_of_uv[P.dest_uv[d]] = d;
+  std::map<std::uint32_t, std::vector<std::uint32_t>> users;
+  for (std::uint32_t i = 0; i < P.dense.size(); ++i) users[P.dense[i].w_uv].push_back(i);
+  for (const auto& [w, us] : users) {
+    const tgc::Dense& D0 = P.dense[us.front()];
+    bool ok = true;
+    std::unordered_map<std::uint32_t, std::uint32_t> x_of_out;   // out_row -> x row0
+    for (std::uint32_t u : us) {
+      const tgc::Dense& D = P.dense[u];
+      ok = ok && pr.dplan[u].gemm && D.n_out == D0.n_out && D.n_in == D0.n_in;
+      x_of_out[D.out_row] = pr.dplan[u].xrow0;
+    }
+    if (!ok) continue;
+    const std::uint32_t nu = static_cast<std::uint32_t>(us.size());
+    auto it = dest_of_uv.find(w);
+    std::uint32_t d0 = it == dest_of_uv.end() ? tgc::kNone : it->second;
+    ok = d0 != tgc::kNone && d0 + std::size_t(D0.n_out) * D0.n_in <= P.dest_uv.size();
+    for (std::uint32_t j = 0; ok && j < D0.n_out; ++j)
+      for (std::uint32_t k = 0; ok && k < D0.n_in; ++k) {
+        const std::uint32_t d = d0 + j * D0.n_in + k;
+        ok = P.dest_uv[d] == w + j * D0.n_in + k && P.term_off[d + 1] - P.term_off[d] == nu;
+        for (std::uint32_t q = P.term_off[d]; ok && q < P.term_off[d + 1]; ++q) {
+          const tgc::Term& t = P.terms[q];
+          const auto x = t.a >= j ? x_of_out.find(t.a - j) : x_of_out.end();
+          ok = t.kind == 0 && t.coef == 1.0 && x != x_of_out.end() && t.f == x->second + k;
+        }
+      }
+    if (ok) {
+      for (std::uint32_t u : us) pr.dplan[u].dw_dest0 = d0;
+      for (std::uint32_t q = 0; q < D0.n_out * D0.n_in; ++q) covered[d0 + q] = 1;
+    }
+    bool bok = D0.b_uv != tgc::kNone;
+    for (std::uint32_t u : us) bok = bok && P.dense[u].b_uv == D0.b_uv;
+    auto bt = bok ? dest_of_uv.find(D0.b_uv) : dest_of_uv.end();
+    bok = bok && bt != dest_of_uv.end() && bt->second + D0.n_out <= P.dest_uv.size();
+    for (std::uint32_t j = 0; bok && j < D0.n_out; ++j) {
+      const std::uint32_t d = bt->second + j;
+      bok = P.dest_uv[d] == D0.b_uv + j && P.term_off[d + 1] - P.term_off[d] == nu;
+      for (std::uint32_t q = P.term_off[d]; bok && q < P.term_off[d + 1]; ++q) {
+        const tgc::Term& t = P.terms[q];
+        bok = t.kind == 0 && t.coef == 1.0 && t.f == tgc::kNone && t.a >= j && x_of_out.count(t.a - j);
+      }
+    }
+    if (bok) {
+      for (std::uint32_t u : us) pr.dplan[u].db_dest0 = bt->second;
+      for (std::uint32_t j = 0; j < D0.n_out; ++j) covered[bt->second + j] = 1;
+    }
+  }
   for (std::size_t i = 0; i < P.dense.size(); ++i) {
     const tgc::Dense& D = P.dense[i];
     tg_program::DensePlan& dp = pr.dplan[i];
     if (!dp.gemm) continue;
-    for (const tgc::DenseGrad& g : P.dgrad)
-      if (P.dest_uv[g.dest0] == D.w_uv && g.n_out == D.n_out && g.n_in == D.n_in) dp.dw_dest0 = g.dest0;
-    if (dp.dw_dest0 != tgc::kNone)
-      for (std::uint32_t q = 0; q < D.n_out * D.n_in; ++q) covered[dp.dw_dest0 + q] = 1;
-    if (D.b_uv != tgc::kNone) {
-      auto it = dest_of_uv.find(D.b_uv);
-      bool ok = it != dest_of_uv.end();
-      for (std::uint32_t j = 0; ok && j < D.n_out; ++j) {
-        const std::uint32_t d = it->second + j;
-        ok = d < P.dest_uv.size() && P.dest_uv[d] == D.b_uv + j && P.term_off[d + 1] - P.term_off[d] == 1 &&
-             P.terms[P.term_off[d]].kind == 0 && P.terms[P.term_off[d]].f == tgc::kNone &&
-             P.terms[P.term_off[d]].a == D.out_row + j;
-      }
-      if (ok) {
-        dp.db_dest0 = it->second;
-        for (std::uint32_t j = 0; j < D.n_out; ++j) covered[dp.db_dest0 + j] = 1;
-      }
-    }
     std::uint32_t n_assign = 0;
     for (std::uint32_t k = 0; k < D.n_in; ++k) n_assign += (P.oflag[D.x_opnd + k] & tgc::kAssign) ? 1 : 0;
     dp.beta = n_assign == D.n_in ? 0 : 1;
@@ -418,6 +468,13 @@ void build_staged_plan(tg_program& pr) {
                                           static_cast<std::uint32_t>(pr.sc_groups.size())));
   // stages: GEMM dense groups on their own; the rest either in instruction
   // ranges (one thread per sample) or, with levels, one range per level key
+  const char* be = std::getenv("TG_STAGED_BATCH");
+  const bool batching = !(be && be[0] == '0');
+  auto same_sig = [&](std::uint32_t a, std::uint32_t b) {
+    const tgc::Dense &A = P.dense[a], &B = P.dense[b];
+    return A.w_uv == B.w_uv && A.b_uv == B.b_uv && A.n_out == B.n_out && A.n_in == B.n_in && A.act_op == B.act_op &&
+           pr.dplan[a].dw_dest0 == pr.dplan[b].dw_dest0 && pr.dplan[a].db_dest0 == pr.dplan[b].db_dest0;
+  };
   auto split = [&](const std::vector<tgc::Instr>& list, const std::vector<std::uint32_t>& key,
                    std::vector<tg_program::Stage>& out) {
     out.clear();
@@ -430,7 +487,17 @@ void build_staged_plan(tg_program& pr) {
     for (std::uint32_t k = 0; k < list.size(); ++k) {
       if (list[k].kind == tgc::kDense && pr.dplan[list[k].aux].gemm) {
         flush(k);
-        out.push_back({static_cast<int>(list[k].aux), k, k + 1, false});
+        const std::uint32_t id = list[k].aux;
+        const bool join = lv && batching && !out.empty() && out.back().batch >= 0 && out.back().end == k &&
+                          key[k] == key[k - 1] && same_sig(pr.batches[out.back().batch].members.front(), id);
+        if (join) {
+          pr.batches[out.back().batch].members.push_back(id);
+          out.back().end = k + 1;
+        } else {
+          pr.batches.push_back({});
+          pr.batches.back().members.push_back(id);
+          out.push_back({static_cast<int>(pr.batches.size() - 1), k, k + 1, false});
+        }
         b = k + 1;
       } else if (lv && k > b && key[k] != key[k - 1]) {
         flush(k);
@@ -438,8 +505,38 @@ void build_staged_plan(tg_program& pr) {
     }
     flush(static_cast<std::uint32_t>(list.size()));
   };
+  pr.batches.clear();
   split(P.fwd, P.fwd_level, pr.sfwd);
   split(P.bwd, P.bwd_level, pr.sbwd);
+  // batch tables: forward {0, x, z, h}, input adjoints {0, z, x, 0}, weight gradient {z, x, 0, 0}
+  const bool tc = pr.tsz() == 4 && pr.umma;
+  for (auto& B : pr.batches) {
+    const std::uint32_t nm = static_cast<std::uint32_t>(B.members.size());
+    const tgc::Dense& D0 = P.dense[B.members.front()];
+    B.tab.assign(3 * std::size_t(nm), uint4{0, 0, 0, 0});
+    B.beta = 0;
+    for (std::uint32_t p = 0; p < nm; ++p) {
+      const tgc::Dense& D = P.dense[B.members[p]];
+      const auto& dp = pr.dplan[B.members[p]];
+      B.tab[p] = uint4{0, dp.xrow0, D.out_row, D.act_op ? D.act_row : 0};
+      B.tab[nm + p] = uint4{0, D.out_row, dp.xrow0, 0};
+      B.tab[2 * nm + p] = uint4{D.out_row, dp.xrow0, 0, 0};
+      B.beta |= dp.beta;
+    }
+    B.zero_x.clear();
+    for (std::uint32_t u : B.members) {
+      const auto& dp = pr.dplan[u];
+      if (B.beta && !dp.beta)
+        for (std::uint32_t k = 0; k < P.dense[u].n_in; ++k) B.zero_x.push_back(dp.xrow0 + k);
+      else
+        B.zero_x.insert(B.zero_x.end(), dp.zero_x.begin(), dp.zero_x.end());
+    }
+    // an offset MN-major operand must end on a k-tile: a tile past K would read
+    // the next rows (TMA zero-fills only past the map), so such roles loop
+    B.bf = tc && nm > 1 && D0.n_in % 32 == 0;
+    B.bx = tc && nm > 1 && D0.n_out % 32 == 0;
+    B.bw = tc && nm > 1 && pr.dplan[B.members.front()].dw_dest0 != tgc::kNone;
+  }
   if (const char* v = std::getenv("TG_STAGED_VERBOSE"); v && v[0] == '1') {
     std::size_t ng = 0;
     for (std::size_t i = 0; i < P.dense.size(); ++i) {
@@ -451,7 +548,7 @@ void build_staged_plan(tg_program& pr) {
     auto stats = [&](const char* name, const std::vector<tg_program::Stage>& st, const std::vector<tgc::Instr>& list) {
       std::size_t nl = 0, ni = 0, nops = 0, small = 0;
       for (const auto& s : st) {
-        if (s.dense >= 0) continue;
+        if (s.batch >= 0) continue;
         ++nl;
         ni += s.end - s.begin;
         small += (s.end - s.begin) < 128;
@@ -462,7 +559,10 @@ void build_staged_plan(tg_program& pr) {
       std::fprintf(stderr, "[staged] %s: %zu stages (%zu interpreter, %zu with <128 instrs), %zu instrs, %zu operands\n",
                    name, st.size(), nl, small, ni, nops);
     };
-    std::fprintf(stderr, "[staged] rows %u, dense %zu (%zu GEMM)\n", P.n_rows, P.dense.size(), ng);
+    std::size_t nb = 0, nbm = 0;
+    for (const auto& B : pr.batches) if (B.members.size() > 1) { ++nb; nbm += B.members.size(); }
+    std::fprintf(stderr, "[staged] rows %u, dense %zu (%zu GEMM), %zu batches (%zu with %zu members); %zu generic dests, %zu scatter dests\n",
+                 P.n_rows, P.dense.size(), ng, pr.batches.size(), nb, nbm, pr.gen_dests.size(), pr.sc_dests.size());
     stats("fwd", pr.sfwd, P.fwd);
     stats("bwd", pr.sbwd, P.bwd);
   }
@@ -488,6 +588,14 @@ std::uint32_t splitk_splits(const tgc::Dense& D, std::size_t n, std::size_t tsz)
   std::uint32_t s = std::max<std::uint32_t>(1, 296 / std::max(1u, tiles));
   s = std::min<std::uint32_t>(s, static_cast<std::uint32_t>(std::max<std::size_t>(1, n / 256)));
   return std::max(1u, s);
+}
+
+// Split-K slices per member of a batched weight-gradient product: about four
+// waves of CTAs over all members, slices of at least 256 samples.
+std::uint32_t batch_splits(const tgc::Dense& D, std::uint32_t nm, std::size_t n) {
+  const std::uint32_t tiles = ((D.n_out + 127) / 128) * ((D.n_in + 127) / 128) * std::max(1u, nm);
+  std::uint32_t z = std::max<std::uint32_t>(1, (592 + tiles - 1) / tiles);
+  return std::min<std::uint32_t>(z, static_cast<std::uint32_t>(std::max<std::size_t>(1, n / 256)));
 }
 
 void choose_config(tg_program& pr) {
@@ -558,6 +666,12 @@ Layout layout(const tg_program& pr, std::size_t batch) {
     for (std::size_t i = 0; i < pr.P.dense.size(); ++i)
       if (pr.dplan[i].gemm && pr.dplan[i].dw_dest0 != tgc::kNone)
         sk = std::max<std::size_t>(sk, std::size_t(splitk_splits(pr.P.dense[i], cb, t)) * pr.P.dense[i].n_out * pr.P.dense[i].n_in);
+    for (const auto& B : pr.batches)
+      if (B.bw) {
+        const tgc::Dense& D = pr.P.dense[B.members.front()];
+        const std::uint32_t nm = static_cast<std::uint32_t>(B.members.size());
+        sk = std::max<std::size_t>(sk, std::size_t(nm) * batch_splits(D, nm, cb) * D.n_out * D.n_in);
+      }
     L.sk = off; off = align_up(off + std::max<std::size_t>(1, sk) * t);
     L.sp = off; off = align_up(off + std::max<std::size_t>(1, std::size_t(pr.sc_groups.size()) * pr.sc_chunks * pr.sc_rmax) * t);
     L.total = off;
@@ -652,7 +766,10 @@ tg_status upload(tg_program& pr) {
     TG_TRY(upload_vec(pr, pr.sc_uses, &pr.d_sc_uses));
     TG_TRY(upload_vec(pr, pr.sc_use_off, &pr.d_sc_use_off));
     TG_TRY(upload_vec(pr, pr.sc_dests, &pr.d_sc_dests));
-    for (auto& dp : pr.dplan) TG_TRY(upload_vec(pr, dp.zero_x, &dp.d_zero_x));
+    for (auto& B : pr.batches) {
+      TG_TRY(upload_vec(pr, B.tab, &B.d_tab));
+      TG_TRY(upload_vec(pr, B.zero_x, &B.d_zero_x));
+    }
   }
   if (env && env[0] == 'v' && !pr.jit.ok) std::fprintf(stderr, "[tg] JIT not used: %s\n", pr.jit.log.c_str());
   cudaGetLastError();
@@ -804,46 +921,123 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
     ++pr.ev_used;
   }
 
+  // tensor-core roles (TG_UMMA_MASK bits: 1 forward, 2 input adjoints, 4 weight gradients)
+  static const int umask = std::getenv("TG_UMMA_MASK") ? std::atoi(std::getenv("TG_UMMA_MASK")) : 7;
   for (std::size_t s0 = 0; s0 < batch; s0 += cb) {
     const std::size_t n = std::min(cb, batch - s0);
     ra.s0 = s0;
     ra.n = n;
+    // Z[n_out][n] = W[n_out][n_in] . X[n_in][n] + b (one member)
+    auto fwd_one = [&](std::uint32_t u) -> cudaError_t {
+      const tgc::Dense& D = P.dense[u];
+      tgk::GemmArgs<T> g{};
+      g.A = UV + D.w_uv;
+      g.lda = D.n_in;
+      g.a_kmaj = true;
+      g.B = V + std::size_t(pr.dplan[u].xrow0) * cb;
+      g.ldb = cb;
+      g.b_nmaj = true;
+      g.C = V + std::size_t(D.out_row) * cb;
+      g.C2 = D.act_op ? V + std::size_t(D.act_row) * cb : nullptr;
+      g.ldc = cb;
+      g.bias = D.b_uv != tgc::kNone ? UV + D.b_uv : nullptr;
+      g.M = D.n_out;
+      g.N = static_cast<std::uint32_t>(n);
+      g.K = D.n_in;
+      g.act = D.act_op;
+      g.epi = tgk::kEpiBiasAct;
+      ++pr.launches;
+      return dense_gemm<T>(pr, g, 1, st);
+    };
+    // dX[n_in][n] (+)= W^T[n_in][n_out] . dZ[n_out][n] (one member)
+    auto dx_one = [&](std::uint32_t u, int beta) -> cudaError_t {
+      const tgc::Dense& D = P.dense[u];
+      tgk::GemmArgs<T> g{};
+      g.A = UV + D.w_uv;
+      g.lda = D.n_in;
+      g.a_kmaj = false;
+      g.B = G + std::size_t(D.out_row) * cb;
+      g.ldb = cb;
+      g.b_nmaj = true;
+      g.C = G + std::size_t(pr.dplan[u].xrow0) * cb;
+      g.ldc = cb;
+      g.M = D.n_in;
+      g.N = static_cast<std::uint32_t>(n);
+      g.K = D.n_out;
+      g.beta = beta;
+      g.epi = tgk::kEpiAccum;
+      ++pr.launches;
+      return dense_gemm<T>(pr, g, 1, st);
+    };
+    // dW[n_out][n_in] += dZ[n_out][n] . X^T, split-K over samples (one member)
+    auto dw_one = [&](std::uint32_t u) -> cudaError_t {
+      const tgc::Dense& D = P.dense[u];
+      const std::uint32_t splits = splitk_splits(D, n, sizeof(T));
+      tgk::GemmArgs<T> g{};
+      g.A = G + std::size_t(D.out_row) * cb;
+      g.lda = cb;
+      g.a_kmaj = true;
+      g.B = V + std::size_t(pr.dplan[u].xrow0) * cb;
+      g.ldb = cb;
+      g.b_nmaj = false;
+      g.C = sk;
+      g.M = D.n_out;
+      g.N = D.n_in;
+      g.K = static_cast<std::uint32_t>(n);
+      g.k_chunk = static_cast<std::uint32_t>((n + splits - 1) / splits);
+      g.epi = tgk::kEpiSplitK;
+      pr.launches += 2;
+      cudaError_t e = dense_gemm<T>(pr, g, splits, st);
+      if (e == cudaSuccess) e = tgk::launch_splitk_reduce<T>(sk, acc + pr.dplan[u].dw_dest0, D.n_out * D.n_in, splits, st);
+      return e;
+    };
     // ---- forward stages ----
     for (const auto& stg : pr.sfwd) {
-      if (stg.dense < 0) {
+      if (stg.batch < 0) {
         ra.flags = tgk::kRFwd;
         ra.fwd_begin = stg.begin;
         ra.fwd_end = stg.end;
         TG_CUDA_TRY(stg.level ? tgk::launch_level_range<T>(ra, st) : tgk::launch_tape_range<T>(ra, st));
-      } else {
-        const tgc::Dense& D = P.dense[stg.dense];
-        const auto& dp = pr.dplan[stg.dense];
-        tgk::GemmArgs<T> g{};   // Z[n_out][n] = W[n_out][n_in] . X[n_in][n] + b
-        g.A = UV + D.w_uv;
-        g.lda = D.n_in;
-        g.a_kmaj = true;
-        g.B = V + std::size_t(dp.xrow0) * cb;
-        g.ldb = cb;
-        g.b_nmaj = true;
-        g.C = V + std::size_t(D.out_row) * cb;
-        g.C2 = D.act_op ? V + std::size_t(D.act_row) * cb : nullptr;
-        g.ldc = cb;
-        g.bias = D.b_uv != tgc::kNone ? UV + D.b_uv : nullptr;
-        g.M = D.n_out;
-        g.N = static_cast<std::uint32_t>(n);
-        g.K = D.n_in;
-        g.act = D.act_op;
-        g.epi = tgk::kEpiBiasAct;
-        TG_CUDA_TRY(dense_gemm<T>(pr, g, 1, st));
+        ++pr.launches;
+        continue;
       }
-      ++pr.launches;
+      const auto& B = pr.batches[stg.batch];
+      const std::uint32_t nm = static_cast<std::uint32_t>(B.members.size());
+      if constexpr (std::is_same_v<T, float>) {
+        if (B.bf && (umask & 1)) {
+          const tgc::Dense& D = P.dense[B.members.front()];
+          tgk::GemmArgs<float> g{};
+          g.A = UV + D.w_uv;
+          g.lda = D.n_in;
+          g.a_kmaj = true;
+          g.B = V;
+          g.ldb = cb;
+          g.b_nmaj = true;
+          g.b_span = P.n_rows;
+          g.C = V;
+          g.C2 = D.act_op ? V : nullptr;
+          g.ldc = cb;
+          g.bias = D.b_uv != tgc::kNone ? UV + D.b_uv : nullptr;
+          g.M = D.n_out;
+          g.N = static_cast<std::uint32_t>(n);
+          g.K = D.n_in;
+          g.act = D.act_op;
+          g.epi = tgk::kEpiBiasAct;
+          g.mem = B.d_tab;
+          g.zs = 1;
+          TG_CUDA_TRY(tgk::launch_gemm_umma(g, nm, st));
+          ++pr.launches;
+          continue;
+        }
+      }
+      for (std::uint32_t u : B.members) TG_CUDA_TRY(fwd_one(u));
     }
     ra.flags = tgk::kRSeed;
     TG_CUDA_TRY(tgk::launch_tape_range<T>(ra, st));
     ++pr.launches;
     // ---- reverse stages ----
     for (const auto& stg : pr.sbwd) {
-      if (stg.dense < 0) {
+      if (stg.batch < 0) {
         ra.flags = tgk::kRBwd;
         ra.bwd_begin = stg.begin;
         ra.bwd_end = stg.end;
@@ -851,55 +1045,74 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
         ++pr.launches;
         continue;
       }
-      const tgc::Dense& D = P.dense[stg.dense];
-      const auto& dp = pr.dplan[stg.dense];
+      const auto& B = pr.batches[stg.batch];
+      const std::uint32_t nm = static_cast<std::uint32_t>(B.members.size());
+      const tgc::Dense& D = P.dense[B.members.front()];
+      const auto& dp0 = pr.dplan[B.members.front()];
       if (D.act_op) {
-        TG_CUDA_TRY(tgk::launch_act_bwd<T>(G, V, D.out_row, D.act_row, D.n_out, n, cb, D.act_op, st));
+        TG_CUDA_TRY(tgk::launch_act_bwd_batched<T>(G, V, B.d_tab, nm, D.n_out, n, cb, D.act_op, st));
         ++pr.launches;
       }
-      if (!dp.zero_x.empty()) {
-        TG_CUDA_TRY(tgk::launch_zero_rows<T>(G, dp.d_zero_x, static_cast<std::uint32_t>(dp.zero_x.size()), n, cb, st));
+      if (!B.zero_x.empty()) {
+        TG_CUDA_TRY(tgk::launch_zero_rows<T>(G, B.d_zero_x, static_cast<std::uint32_t>(B.zero_x.size()), n, cb, st));
         ++pr.launches;
       }
-      {  // dX[n_in][n] (+)= W^T[n_in][n_out] . dZ[n_out][n]
-        tgk::GemmArgs<T> g{};
-        g.A = UV + D.w_uv;
-        g.lda = D.n_in;
-        g.a_kmaj = false;
-        g.B = G + std::size_t(D.out_row) * cb;
-        g.ldb = cb;
-        g.b_nmaj = true;
-        g.C = G + std::size_t(dp.xrow0) * cb;
-        g.ldc = cb;
-        g.M = D.n_in;
-        g.N = static_cast<std::uint32_t>(n);
-        g.K = D.n_out;
-        g.beta = dp.beta;
-        g.epi = tgk::kEpiAccum;
-        TG_CUDA_TRY(dense_gemm<T>(pr, g, 1, st));
-        ++pr.launches;
+      bool dx_done = false, dw_done = false;
+      if constexpr (std::is_same_v<T, float>) {
+        if (B.bx && (umask & 2)) {
+          tgk::GemmArgs<float> g{};
+          g.A = UV + D.w_uv;
+          g.lda = D.n_in;
+          g.a_kmaj = false;
+          g.B = G;
+          g.ldb = cb;
+          g.b_nmaj = true;
+          g.b_span = P.n_rows;
+          g.C = G;
+          g.ldc = cb;
+          g.M = D.n_in;
+          g.N = static_cast<std::uint32_t>(n);
+          g.K = D.n_out;
+          g.beta = B.beta;
+          g.epi = tgk::kEpiAccum;
+          g.mem = B.d_tab + nm;
+          g.zs = 1;
+          TG_CUDA_TRY(tgk::launch_gemm_umma(g, nm, st));
+          ++pr.launches;
+          dx_done = true;
+        }
+        if (B.bw && (umask & 4)) {
+          const std::uint32_t zs = batch_splits(D, nm, n);
+          tgk::GemmArgs<float> g{};
+          g.A = G;
+          g.lda = cb;
+          g.a_kmaj = true;
+          g.a_span = P.n_rows;
+          g.B = V;
+          g.ldb = cb;
+          g.b_nmaj = false;
+          g.b_span = P.n_rows;
+          g.C = sk;
+          g.M = D.n_out;
+          g.N = D.n_in;
+          g.K = static_cast<std::uint32_t>(n);
+          g.k_chunk = static_cast<std::uint32_t>((n + zs - 1) / zs);
+          g.epi = tgk::kEpiSplitK;
+          g.mem = B.d_tab + 2 * nm;
+          g.zs = zs;
+          TG_CUDA_TRY(tgk::launch_gemm_umma(g, nm * zs, st));
+          TG_CUDA_TRY(tgk::launch_splitk_reduce<T>(sk, acc + dp0.dw_dest0, D.n_out * D.n_in, nm * zs, st));
+          pr.launches += 2;
+          dw_done = true;
+        }
       }
-      if (dp.dw_dest0 != tgc::kNone) {  // dW[n_out][n_in] = dZ[n_out][n] . X^T, split-K over samples
-        const std::uint32_t splits = splitk_splits(D, n, sizeof(T));
-        tgk::GemmArgs<T> g{};
-        g.A = G + std::size_t(D.out_row) * cb;
-        g.lda = cb;
-        g.a_kmaj = true;
-        g.B = V + std::size_t(dp.xrow0) * cb;
-        g.ldb = cb;
-        g.b_nmaj = false;
-        g.C = sk;
-        g.M = D.n_out;
-        g.N = D.n_in;
-        g.K = static_cast<std::uint32_t>(n);
-        g.k_chunk = static_cast<std::uint32_t>((n + splits - 1) / splits);
-        g.epi = tgk::kEpiSplitK;
-        TG_CUDA_TRY(dense_gemm<T>(pr, g, splits, st));
-        TG_CUDA_TRY(tgk::launch_splitk_reduce<T>(sk, acc + dp.dw_dest0, D.n_out * D.n_in, splits, st));
-        pr.launches += 2;
+      for (std::uint32_t u : B.members) {
+        // zeroed rows above follow the batch's beta; members that only assign keep their store
+        if (!dx_done) TG_CUDA_TRY(dx_one(u, B.beta ? pr.dplan[u].beta : 0));
+        if (!dw_done && pr.dplan[u].dw_dest0 != tgc::kNone) TG_CUDA_TRY(dw_one(u));
       }
-      if (dp.db_dest0 != tgc::kNone) {
-        TG_CUDA_TRY(tgk::launch_rowsum<T>(G, D.out_row, D.n_out, n, cb, acc + dp.db_dest0, st));
+      if (dp0.db_dest0 != tgc::kNone) {
+        TG_CUDA_TRY(tgk::launch_rowsum_batched<T>(G, B.d_tab, nm, D.n_out, n, cb, acc + dp0.db_dest0, st));
         ++pr.launches;
       }
     }

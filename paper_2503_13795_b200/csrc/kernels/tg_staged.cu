@@ -288,16 +288,30 @@ template <class T>
 __global__ void k_splitk_reduce(const T* __restrict__ part, T* __restrict__ dst, std::uint32_t MN, std::uint32_t splits) {
   const std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= MN) return;
+  // 8 partials in flight (batched weight gradients sum hundreds), summed in slice order
   T t = 0;
-  for (std::uint32_t z = 0; z < splits; ++z) t += part[std::size_t(z) * MN + i];
+  std::uint32_t z = 0;
+  for (; z + 8 <= splits; z += 8) {
+    T x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = part[std::size_t(z + u) * MN + i];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t += x[u];
+  }
+  for (; z < splits; ++z) t += part[std::size_t(z) * MN + i];
   dst[i] += t;
 }
 
 template <class T>
 __global__ void k_act_bwd(T* G, const T* V, std::uint32_t z_row, std::uint32_t h_row, std::size_t n, std::size_t ld,
-                          std::uint32_t act) {
+                          std::uint32_t act, const uint4* mem) {
   const std::size_t s = std::size_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (s >= n) return;
+  if (mem) {   // batch member blockIdx.z
+    const uint4 e = mem[blockIdx.z];
+    z_row = e.z;
+    h_row = e.w;
+  }
   const std::size_t zr = std::size_t(z_row + blockIdx.y) * ld + s, hr = std::size_t(h_row + blockIdx.y) * ld + s;
   // tanh / sigmoid / exp derivatives use the output only: skip the z read (a quarter of the bytes)
   const bool need_z = act == Relu || act == Sqr || act == Cub;
@@ -305,20 +319,24 @@ __global__ void k_act_bwd(T* G, const T* V, std::uint32_t z_row, std::uint32_t h
 }
 
 template <class T>
-__global__ void __launch_bounds__(256) k_rowsum(const T* G, std::uint32_t row0, std::size_t n, std::size_t ld, T* dst) {
+__global__ void __launch_bounds__(256) k_rowsum(const T* G, std::uint32_t row0, std::size_t n, std::size_t ld, T* dst,
+                                                const uint4* mem, std::uint32_t n_mem) {
   __shared__ T red[256];
-  const T* row = G + std::size_t(row0 + blockIdx.x) * ld;
-  // 8 loads in flight per thread, summed in sequential order (deterministic)
+  // 8 loads in flight per thread, summed in sequential order (deterministic);
+  // batched: the members' rows one after another
   T t = 0;
-  std::size_t s = threadIdx.x;
-  for (; s + 7 * 256 < n; s += 8 * 256) {
-    T x[8];
+  for (std::uint32_t p = 0; p < n_mem; ++p) {
+    const T* row = G + std::size_t((mem ? mem[p].z : row0) + blockIdx.x) * ld;
+    std::size_t s = threadIdx.x;
+    for (; s + 7 * 256 < n; s += 8 * 256) {
+      T x[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) x[u] = row[s + u * 256];
+      for (int u = 0; u < 8; ++u) x[u] = row[s + u * 256];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) t += x[u];
+      for (int u = 0; u < 8; ++u) t += x[u];
+    }
+    for (; s < n; s += 256) t += row[s];
   }
-  for (; s < n; s += 256) t += row[s];
   red[threadIdx.x] = t;
   __syncthreads();
   for (int o = 128; o > 0; o >>= 1) {
@@ -474,7 +492,15 @@ template <class T>
 cudaError_t launch_act_bwd(T* G, const T* V, std::uint32_t z_row, std::uint32_t h_row, std::uint32_t n_out, std::size_t n,
                            std::size_t ld, std::uint32_t act, cudaStream_t st) {
   if (n == 0 || n_out == 0) return cudaSuccess;
-  k_act_bwd<T><<<dim3(static_cast<unsigned>((n + 255) / 256), n_out), 256, 0, st>>>(G, V, z_row, h_row, n, ld, act);
+  k_act_bwd<T><<<dim3(static_cast<unsigned>((n + 255) / 256), n_out), 256, 0, st>>>(G, V, z_row, h_row, n, ld, act, nullptr);
+  return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t launch_act_bwd_batched(T* G, const T* V, const uint4* mem, std::uint32_t n_mem, std::uint32_t n_out, std::size_t n,
+                                   std::size_t ld, std::uint32_t act, cudaStream_t st) {
+  if (n == 0 || n_out == 0 || n_mem == 0) return cudaSuccess;
+  k_act_bwd<T><<<dim3(static_cast<unsigned>((n + 255) / 256), n_out, n_mem), 256, 0, st>>>(G, V, 0, 0, n, ld, act, mem);
   return cudaGetLastError();
 }
 
@@ -482,7 +508,15 @@ template <class T>
 cudaError_t launch_rowsum(const T* G, std::uint32_t row0, std::uint32_t rows, std::size_t n, std::size_t ld, T* dst,
                           cudaStream_t st) {
   if (rows == 0) return cudaSuccess;
-  k_rowsum<T><<<rows, 256, 0, st>>>(G, row0, n, ld, dst);
+  k_rowsum<T><<<rows, 256, 0, st>>>(G, row0, n, ld, dst, nullptr, 1);
+  return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t launch_rowsum_batched(const T* G, const uint4* mem, std::uint32_t n_mem, std::uint32_t rows, std::size_t n,
+                                  std::size_t ld, T* dst, cudaStream_t st) {
+  if (rows == 0 || n_mem == 0) return cudaSuccess;
+  k_rowsum<T><<<rows, 256, 0, st>>>(G, 0, n, ld, dst, mem, n_mem);
   return cudaGetLastError();
 }
 
@@ -512,6 +546,10 @@ cudaError_t launch_contract(const std::uint32_t* dests, std::uint32_t n_dests, c
                                          std::size_t, std::uint32_t, cudaStream_t);                                        \
   template cudaError_t launch_rowsum<T>(const T*, std::uint32_t, std::uint32_t, std::size_t, std::size_t, T*,              \
                                         cudaStream_t);                                                                     \
+  template cudaError_t launch_act_bwd_batched<T>(T*, const T*, const uint4*, std::uint32_t, std::uint32_t, std::size_t,   \
+                                                 std::size_t, std::uint32_t, cudaStream_t);                                \
+  template cudaError_t launch_rowsum_batched<T>(const T*, const uint4*, std::uint32_t, std::uint32_t, std::size_t,          \
+                                                std::size_t, T*, cudaStream_t);                                            \
   template cudaError_t launch_zero_rows<T>(T*, const std::uint32_t*, std::uint32_t, std::size_t, std::size_t,              \
                                            cudaStream_t);                                                                  \
   template cudaError_t launch_contract<T>(const std::uint32_t*, std::uint32_t, const std::uint32_t*, const Term*,          \

@@ -74,6 +74,14 @@ struct GemmArgs {
   int beta;
   bool a_kmaj, b_nmaj;
   int epi;
+  // Batched products (tcgen05 path only): blockIdx.z / zs selects a member
+  // whose row offsets {a, b, c, c2} shift the operands' outer (row)
+  // coordinate and the output rows; a_span / b_span are the row extents of
+  // the operand maps (0: the operand is shared, no offset).  Split-K partials
+  // are indexed by blockIdx.z = member * zs + slice.
+  const uint4* mem;
+  std::uint32_t zs;
+  std::uint32_t a_span, b_span;
 };
 
 // Table-scatter (kind-1) batch terms grouped by (adjoint row a, index column f).
@@ -105,6 +113,13 @@ template <class T> cudaError_t launch_act_bwd(T* G, const T* V, std::uint32_t z_
 // dst[j] += sum_s G[(row0 + j) * ld + s]   (fixed-order block tree per row)
 template <class T> cudaError_t launch_rowsum(const T* G, std::uint32_t row0, std::uint32_t rows, std::size_t n, std::size_t ld,
                                              T* dst, cudaStream_t st);
+// Batched forms over the members of a dense batch (mem[p].z = z row, .w = h row):
+// activation derivative for every member, and dst[j] += sum_p sum_s G[mem[p].z + j]
+// (members in order, then the fixed-order tree over samples).
+template <class T> cudaError_t launch_act_bwd_batched(T* G, const T* V, const uint4* mem, std::uint32_t n_mem, std::uint32_t n_out,
+                                                      std::size_t n, std::size_t ld, std::uint32_t act, cudaStream_t st);
+template <class T> cudaError_t launch_rowsum_batched(const T* G, const uint4* mem, std::uint32_t n_mem, std::uint32_t rows,
+                                                     std::size_t n, std::size_t ld, T* dst, cudaStream_t st);
 // zero `count` rows of X starting at row0 (first n columns)
 template <class T> cudaError_t launch_zero_rows(T* X, const std::uint32_t* rows, std::uint32_t count, std::size_t n, std::size_t ld, cudaStream_t st);
 // generic batch terms of the listed destinations over the chunk: acc[d] += ...

@@ -260,13 +260,15 @@ __device__ __forceinline__ std::uint64_t umma_desc_sw128(std::uint32_t saddr, st
          (static_cast<std::uint64_t>(sbo >> 4) << 32) | (1ull << 46) | (2ull << 61);
 }
 // Issue the TMA loads of one operand's k-tile (rows r0.., k0..) into dst.
-__device__ __forceinline__ void tma_operand(const CUtensorMap* map, bool mn, std::uint32_t dst, int r0, int k0,
+// `off` shifts the map's outer (row) coordinate: the k rows of an MN-major
+// operand, the m / n rows of a K-major one (batched products).
+__device__ __forceinline__ void tma_operand(const CUtensorMap* map, bool mn, std::uint32_t dst, int r0, int k0, int off,
                                             std::uint32_t mbar) {
   if (mn) {
 #pragma unroll
-    for (int c = 0; c < 4; ++c) tma_load_2d(dst + c * 4096, map, r0 + 32 * c, k0, mbar);
+    for (int c = 0; c < 4; ++c) tma_load_2d(dst + c * 4096, map, r0 + 32 * c, k0 + off, mbar);
   } else {
-    tma_load_2d(dst, map, k0, r0, mbar);
+    tma_load_2d(dst, map, k0, r0 + off, mbar);
   }
 }
 // MN-major 32-bit operands: the only UMMA layout is SWIZZLE_128B_BASE32B
@@ -337,9 +339,20 @@ __global__ void __launch_bounds__(kTThreads, 1) k_umma_tma(GemmArgs<float> g, co
   // M tiles are the fast grid index: the CTAs that read the same B tile (the
   // sample-axis operand, too large for L2) run together and share it in L2
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  std::uint32_t slice = blockIdx.z;
+  int a_off = 0, b_off = 0;
+  std::size_t c_off = 0, c2_off = 0;
+  if (g.mem) {   // batch member blockIdx.z / zs
+    const uint4 e = g.mem[blockIdx.z / g.zs];
+    slice = blockIdx.z % g.zs;
+    a_off = static_cast<int>(e.x);
+    b_off = static_cast<int>(e.y);
+    c_off = e.z;
+    c2_off = e.w;
+  }
   std::uint32_t k_begin = 0, k_end = g.K;
   if (g.epi == kEpiSplitK) {
-    k_begin = blockIdx.z * g.k_chunk;
+    k_begin = slice * g.k_chunk;
     k_end = min(g.K, k_begin + g.k_chunk);
   }
   const std::uint32_t T = k_end > k_begin ? (k_end - k_begin + BK - 1) / BK : 0;
@@ -354,8 +367,8 @@ __global__ void __launch_bounds__(kTThreads, 1) k_umma_tma(GemmArgs<float> g, co
         const std::uint32_t base = smem_u32(smem + s * kTStage);
         mbar_expect_tx(full(s), 2 * kTTile);
         const int k0 = static_cast<int>(k_begin + t * BK);
-        tma_operand(&tmA, a_mn, base, m0, k0, full(s));
-        tma_operand(&tmB, b_mn, base + 2 * kTTile, n0, k0, full(s));
+        tma_operand(&tmA, a_mn, base, m0, k0, a_off, full(s));
+        tma_operand(&tmB, b_mn, base + 2 * kTTile, n0, k0, b_off, full(s));
       }
   } else if (warp == 1) {
     // ===== MMA issuer =====
@@ -471,7 +484,8 @@ __global__ void __launch_bounds__(kTThreads, 1) k_umma_tma(GemmArgs<float> g, co
       if (m >= g.M || n >= g.N) continue;
       const float4 v = *reinterpret_cast<const float4*>(tile + r * kLd + 4 * lane);
       float a4[4] = {v.x, v.y, v.z, v.w};
-      float* dst = g.epi == kEpiSplitK ? g.C + (std::size_t(blockIdx.z) * g.M + m) * g.N + n : g.C + std::size_t(m) * g.ldc + n;
+      float* dst = g.epi == kEpiSplitK ? g.C + (std::size_t(blockIdx.z) * g.M + m) * g.N + n
+                                       : g.C + (c_off + m) * g.ldc + n;
       const int cnt = min(4u, g.N - n);
       if (g.epi == kEpiBiasAct) {
         const float bv = g.bias ? g.bias[m] : 0.f;
@@ -481,7 +495,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_umma_tma(GemmArgs<float> g, co
           float h4[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) h4[e] = act_fwd<float>(g.act, a4[e]);
-          float* d2 = g.C2 + std::size_t(m) * g.ldc + n;
+          float* d2 = g.C2 + (c2_off + m) * g.ldc + n;
           if (vec && cnt == 4) *reinterpret_cast<float4*>(d2) = make_float4(h4[0], h4[1], h4[2], h4[3]);
           else for (int e = 0; e < cnt; ++e) d2[e] = h4[e];
         }
@@ -578,6 +592,33 @@ cudaError_t launch_gemm_umma(const GemmArgs<float>& g0, std::uint32_t splits, cu
       }
       return static_cast<const float*>(buf);
     };
+    if (g.mem) {
+      // batched: one map per operand over its whole row span (rows are shifted
+      // per member in the kernel); every operand is row-aligned, no padding
+      if (!g.zs || (g.epi != kEpiSplitK && g.zs != 1)) return cudaErrorInvalidValue;
+      auto span_map = [&](CUtensorMap* m, const float* P, std::size_t ld, bool mn, std::uint32_t rows, std::uint32_t span) {
+        if (!span) return make_operand_map(m, P, ld, mn, rows, g.K);
+        return mn ? make_operand_map(m, P, ld, true, rows, span) : make_operand_map(m, P, ld, false, span, g.K);
+      };
+      if (!span_map(&ta, g.A, g.lda, a_mn, g.M, g.a_span) || !span_map(&tb, g.B, g.ldb, b_mn, g.N, g.b_span))
+        return cudaErrorInvalidValue;
+      static bool battr = false;
+      if (!battr) {
+        for (cudaError_t e : {cudaFuncSetAttribute(k_umma_tma<kTStagesMax>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(tma_smem(kTStagesMax))),
+                              cudaFuncSetAttribute(k_umma_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(tma_smem(1)))})
+          if (e != cudaSuccess) return e;
+        battr = true;
+      }
+      const dim3 grid((g.M + BM - 1) / BM, (g.N + BN - 1) / BN, splits);   // splits = members x zs
+      const std::uint32_t kspan = g.epi == kEpiSplitK ? g.k_chunk : g.K;
+      if (kspan <= static_cast<std::uint32_t>(BK))
+        k_umma_tma<1><<<grid, kTThreads, tma_smem(1), st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0);
+      else
+        k_umma_tma<kTStagesMax><<<grid, kTThreads, tma_smem(kTStagesMax), st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0);
+      return cudaGetLastError();
+    }
     if (!make_operand_map(&ta, g.A, g.lda, a_mn, g.M, g.K)) {
       std::size_t ldp = g.lda;
       g.A = pad(g.A, g.lda, a_mn, g.M, pad_a, ldp);
@@ -616,6 +657,7 @@ cudaError_t launch_gemm_umma(const GemmArgs<float>& g0, std::uint32_t splits, cu
     }
     release();
   }
+  if (g0.mem) return cudaErrorInvalidValue;   // batched products need the TMA path
   const GemmArgs<float>& g = g0;
   // register-staged fallback (operands TMA cannot describe): its accumulator
   // is never drained, so its bias grows with K; beyond K = 1024 per launch the

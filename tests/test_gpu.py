@@ -102,7 +102,8 @@ def test_reference_fuzzer_graphs(tier, dt):
 
 @pytest.mark.parametrize("tier", TIERS)
 @pytest.mark.parametrize("name,dims,dt,b", [("moons", None, "f64", 8192), ("char_mlp", None, "f32", 2048),
-                                            ("listing1", None, "f64", 5000), ("gpt", [17, 8, 16, 2, 2, 32], "f32", 24)])
+                                            ("listing1", None, "f64", 5000), ("gpt", [17, 8, 16, 2, 2, 32], "f32", 24),
+                                            ("gpt", [13, 8, 32, 2, 2, 64], "f32", 40)])
 def test_larger_batches_vs_oracle(tier, name, dims, dt, b):
     desc = tg.build_model(name, dims, dt, seed=2).describe()
     x, k = tg.synth_batch(name, dims, dt, seed=11, batch=b, n_inputs=desc.n_inputs, n_index=desc.n_index_inputs)
@@ -114,6 +115,27 @@ def test_larger_batches_vs_oracle(tier, name, dims, dt, b):
         assert rel(G, r["grad_sum"]) <= TOL[dt]
     if desc.n_inputs:
         assert rel(IG, r["input_grad"]) <= TOL[dt] * 10
+
+
+@pytest.mark.parametrize("batch_env", ["1", "0"])
+def test_gpt_cfg4_dims_vs_oracle(batch_env):
+    """cfg4's GPT (65/64/64/4H/4L) through the staged tier: the 64 positions'
+    dense layers over one weight run as batched tcgen05 products (forward,
+    input adjoints, split-K weight gradients summed over positions) —
+    TG_STAGED_BATCH=0 runs them one position at a time — against the oracle."""
+    desc = tg.build_model("gpt", None, "f32", seed=4).describe()
+    b = 12
+    x, k = tg.synth_batch("gpt", None, "f32", seed=21, batch=b, n_inputs=0, n_index=desc.n_index_inputs)
+    os.environ["TG_STAGED_BATCH"] = batch_env
+    try:
+        prog = tg.Program(desc)
+        L, IG, G = run(prog, desc, x, k, desc.param_values(), b, want_igrad=False)
+        assert prog.info["storage"] == 3
+    finally:
+        os.environ.pop("TG_STAGED_BATCH")
+    r = oracle.run(desc, x.astype(np.float64), k, desc.param_values(), threads=os.cpu_count() or 8)
+    assert close_rel(L, r["loss"], 1e-5, 1e-6)
+    assert rel(G, r["grad_sum"]) <= 1e-5
 
 
 @pytest.mark.parametrize("name,dims,b", [("char_mlp", None, 262144), ("wide_mlp", None, 512)])
