@@ -11,6 +11,7 @@
 #include <cstring>
 #include <chrono>
 #include <map>
+#include <set>
 #include <memory>
 #include <new>
 #include <stdexcept>
@@ -137,7 +138,8 @@ struct tg_program {
   tgj::JitKernel jit;
   // staged execution over an HBM SoA workspace (large tapes, dense layers as GEMMs)
   struct Stage { int batch; std::uint32_t begin, end; bool level = false; };   // batch >= 0: GEMM stage; level: one
-                                                                              // instruction per CTA column (k_level_range)
+                                                                              // instruction per CTA column (k_level_range);
+                                                                              // batch == kSumStage: sums[begin, end)
   // Dense layers of one dependency level over the same weights (a GPT's 64
   // positions): one launch per role with per-member row offsets.
   struct Batch {
@@ -150,6 +152,13 @@ struct tg_program {
     bool bf = false, bx = false, bw = false;   // forward / dX / dW run batched (else per member)
   };
   std::vector<Batch> batches;
+  // Contended adjoint rows of the reverse levels: pushes into a row with more
+  // than one pusher in a level store to temporaries (rows n_rows ..), summed
+  // into the row at the end of the level: {row, assign, first temporary, count}.
+  std::vector<uint4> sums;
+  std::vector<std::pair<std::uint32_t, std::uint32_t>> level_sums;   // per reverse level: [begin, end) of sums
+  uint4* d_sums = nullptr;
+  std::uint32_t n_tmp = 0;
   bool levels = false;            // staged lists reordered into dependency levels (TG_STAGED_LEVELS=0: off)
   struct DensePlan {
     bool gemm = false;
@@ -185,6 +194,7 @@ struct tg_program {
 
 namespace {
 
+constexpr int kSumStage = -2;
 constexpr std::size_t kSmemBudget = 200 * 1024;
 constexpr unsigned kMaxOcc = 32;
 
@@ -202,7 +212,8 @@ constexpr unsigned kMaxOcc = 32;
 // new order; rows reachable from a slot gather only ever accumulate and are
 // zeroed at the seed.  Both orders stay valid sequential orders, so the
 // interpreter (domain-error diagnosis) runs them unchanged.
-void level_schedule(tgc::Program& P, const std::vector<char>& gemm_dense) {
+void level_schedule(tg_program& pr, const std::vector<char>& gemm_dense) {
+  tgc::Program& P = pr.P;
   const std::uint32_t R = P.n_rows;
   auto slot_rows = [&](std::uint32_t op, std::vector<std::uint32_t>& out) {
     const std::uint32_t m = op >> tgc::kModeShift, i = op & tgc::kIndexMask;
@@ -253,45 +264,67 @@ void level_schedule(tgc::Program& P, const std::vector<char>& gemm_dense) {
   P.fwd.swap(nf);
   P.fwd_level = nlvl;
   // ---- reverse: level = 1 + max level of the instructions pushing into the rows it reads ----
+  // Pushes: "soft" (a slot operand of a node: may be redirected to a
+  // temporary) and "hard" (slot-gather candidates, dense-layer x rows).
+  struct Push { std::uint32_t row, pos; bool hard; };
+  std::vector<std::vector<Push>> pushes(P.bwd.size());
   std::vector<std::uint32_t> pushed_level(R, 0), rl(P.bwd.size(), 0), sub(P.bwd.size(), 0);
   std::vector<char> has_push(R, 0);
-  std::vector<std::vector<std::uint32_t>> targets(P.bwd.size());
   for (std::size_t k = 0; k < P.bwd.size(); ++k) {
     const tgc::Instr& in = P.bwd[k];
     rows.clear();
+    std::vector<std::uint32_t> uv_aux;
     if (in.kind == tgc::kDense) {
       const tgc::Dense& D = P.dense[in.aux];
       for (std::uint32_t j = 0; j < D.n_out; ++j) rows.push_back(D.act_op ? D.act_row + j : D.out_row + j);
-      for (std::uint32_t j = 0; j < D.n_in; ++j) slot_rows(P.opnd[D.x_opnd + j], targets[k]);
+      std::vector<std::uint32_t> xr;
+      for (std::uint32_t j = 0; j < D.n_in; ++j) slot_rows(P.opnd[D.x_opnd + j], xr);
+      for (std::uint32_t r : xr) pushes[k].push_back({r, tgc::kNone, true});
     } else {
       rows.push_back(in.out);
       for (std::uint32_t j = 0; j < in.nops; ++j) {
-        const std::uint32_t op = P.opnd[in.opnd + j];
-        if ((op >> tgc::kModeShift) == tgc::kUv) {
-          if (P.oflag[in.opnd + j] & tgc::kToAux) targets[k].push_back(P.oaux[in.opnd + j]);
+        const std::uint32_t pos = in.opnd + j, op = P.opnd[pos];
+        const std::uint32_t m = op >> tgc::kModeShift;
+        if (m == tgc::kUv) {
+          if (P.oflag[pos] & tgc::kToAux) uv_aux.push_back(P.oaux[pos]);
+        } else if (m == tgc::kSlot) {
+          pushes[k].push_back({op & tgc::kIndexMask, pos, false});
         } else {
-          slot_rows(op, targets[k]);
+          std::vector<std::uint32_t> cr;
+          slot_rows(op, cr);
+          for (std::uint32_t r : cr) pushes[k].push_back({r, pos, true});
         }
       }
     }
     std::uint32_t L = 0;
     for (std::uint32_t r : rows) if (has_push[r]) L = std::max(L, pushed_level[r] + 1);
     rl[k] = L;
-    for (std::uint32_t t : targets[k]) {
+    auto mark = [&](std::uint32_t t) {
       pushed_level[t] = has_push[t] ? std::max(pushed_level[t], L) : L;
       has_push[t] = 1;
-    }
+    };
+    for (const Push& q : pushes[k]) mark(q.row);
+    for (std::uint32_t t : uv_aux) mark(t);
   }
-  // sub-levels: no two instructions of one sub-level push into the same row
+  // pushers per (level, row): a soft push into a row with several pushers in
+  // its level goes to a temporary; hard pushes keep sub-levels among themselves
+  std::unordered_map<std::uint64_t, std::uint32_t> cnt;
+  for (std::size_t k = 0; k < P.bwd.size(); ++k)
+    for (const Push& q : pushes[k]) ++cnt[(std::uint64_t(rl[k]) << 32) | q.row];
+  auto contended = [&](std::size_t k, const Push& q) {
+    return !q.hard && cnt[(std::uint64_t(rl[k]) << 32) | q.row] > 1;
+  };
   std::unordered_map<std::uint64_t, std::uint32_t> last_sub;   // (level, row) -> last sub-level used
   for (std::size_t k = 0; k < P.bwd.size(); ++k) {
     std::uint32_t sl = 0;
-    for (std::uint32_t t : targets[k]) {
-      auto it = last_sub.find((std::uint64_t(rl[k]) << 32) | t);
+    for (const Push& q : pushes[k]) {
+      if (!q.hard) continue;
+      auto it = last_sub.find((std::uint64_t(rl[k]) << 32) | q.row);
       if (it != last_sub.end()) sl = std::max(sl, it->second + 1);
     }
     sub[k] = sl;
-    for (std::uint32_t t : targets[k]) last_sub[(std::uint64_t(rl[k]) << 32) | t] = sl;
+    for (const Push& q : pushes[k])
+      if (q.hard) last_sub[(std::uint64_t(rl[k]) << 32) | q.row] = sl;
   }
   std::vector<std::uint32_t> bo(P.bwd.size());
   for (std::uint32_t k = 0; k < bo.size(); ++k) bo[k] = k;
@@ -302,13 +335,19 @@ void level_schedule(tgc::Program& P, const std::vector<char>& gemm_dense) {
   });
   std::vector<tgc::Instr> nb(P.bwd.size());
   std::vector<std::uint32_t> nbl(P.bwd.size());
+  std::vector<std::vector<Push>> np(P.bwd.size());
+  std::vector<std::uint32_t> nrl(P.bwd.size());
   for (std::size_t k = 0; k < bo.size(); ++k) {
     nb[k] = P.bwd[bo[k]];
     nbl[k] = (rl[bo[k]] << 12) | std::min<std::uint32_t>(sub[bo[k]], 4095);   // stage key
+    nrl[k] = rl[bo[k]];
+    np[k] = std::move(pushes[bo[k]]);
   }
+  for (std::size_t k = 0; k < bo.size(); ++k) rl[k] = nrl[k];   // cnt keys stay valid: same levels
   P.bwd.swap(nb);
   P.bwd_level = nbl;
-  // ---- first-write (assign) flags for the new reverse order ----
+  // ---- temporaries (consecutive per contended row, in execution order) and
+  // first-write (assign) flags for the new reverse order ----
   std::vector<char> gather_target(R, 0), seen(R, 0);
   for (const auto& t : P.sgather)
     for (std::uint32_t r = 0; r < t.n_rows; ++r) gather_target[P.cand[t.cand_off + r]] = 1;
@@ -320,13 +359,55 @@ void level_schedule(tgc::Program& P, const std::vector<char>& gemm_dense) {
     else P.oflag[pos] &= static_cast<std::uint8_t>(~tgc::kAssign);
     seen[r] = 1;
   };
-  for (const tgc::Instr& in : P.bwd) {
-    if (in.kind == tgc::kDense) {
-      const tgc::Dense& D = P.dense[in.aux];
-      for (std::uint32_t j = 0; j < D.n_in; ++j) flag(D.x_opnd + j);
-    } else {
-      for (std::uint32_t j = 0; j < in.nops; ++j) flag(in.opnd + j);
+  pr.sums.clear();
+  pr.level_sums.clear();
+  pr.n_tmp = 0;
+  for (std::size_t k0 = 0; k0 < P.bwd.size();) {
+    std::size_t k1 = k0;
+    while (k1 < P.bwd.size() && rl[k1] == rl[k0]) ++k1;
+    std::vector<std::uint32_t> order;                               // contended rows, first-use order
+    std::unordered_map<std::uint32_t, std::vector<std::uint32_t>> uses;   // row -> operand positions
+    for (std::size_t k = k0; k < k1; ++k) {
+      const tgc::Instr& in = P.bwd[k];
+      if (in.kind == tgc::kDense) {
+        const tgc::Dense& D = P.dense[in.aux];
+        for (std::uint32_t j = 0; j < D.n_in; ++j) flag(D.x_opnd + j);
+        continue;
+      }
+      std::unordered_map<std::uint32_t, char> hot;   // positions of this instruction going to temporaries
+      for (const Push& q : np[k])
+        if (contended(k, q)) {
+          auto& u = uses[q.row];
+          if (u.empty()) order.push_back(q.row);
+          u.push_back(q.pos);
+          hot[q.pos] = 1;
+        }
+      for (std::uint32_t j = 0; j < in.nops; ++j) {
+        const std::uint32_t pos = in.opnd + j;
+        if ((P.opnd[pos] >> tgc::kModeShift) != tgc::kSlot) continue;
+        if (hot.count(pos)) {
+          P.oflag[pos] = static_cast<std::uint8_t>((P.oflag[pos] | tgc::kToAux) & ~tgc::kAssign);
+        } else {
+          P.oflag[pos] &= static_cast<std::uint8_t>(~tgc::kToAux);
+          flag(pos);
+        }
+      }
     }
+    const std::uint32_t lv = rl[k0];
+    if (pr.level_sums.size() <= lv) pr.level_sums.resize(lv + 1, {0, 0});
+    const std::uint32_t sb = static_cast<std::uint32_t>(pr.sums.size());
+    std::uint32_t next = 0;
+    for (std::uint32_t r : order) {
+      const auto& u = uses[r];
+      for (std::size_t i = 0; i < u.size(); ++i) P.oaux[u[i]] = R + next + static_cast<std::uint32_t>(i);
+      const bool assign = !seen[r] && !gather_target[r];
+      seen[r] = 1;
+      pr.sums.push_back(uint4{r, assign ? 1u : 0u, R + next, static_cast<std::uint32_t>(u.size())});
+      next += static_cast<std::uint32_t>(u.size());
+    }
+    pr.level_sums[lv] = {sb, static_cast<std::uint32_t>(pr.sums.size())};
+    pr.n_tmp = std::max(pr.n_tmp, next);
+    k0 = k1;
   }
   std::vector<char> zero(R, 0);
   for (std::uint32_t r : P.zero_rows) zero[r] = 1;
@@ -359,7 +440,7 @@ void build_staged_plan(tg_program& pr) {
     if (pr.levels) {
       std::vector<char> gd(P.dense.size(), 0);
       for (std::size_t i = 0; i < P.dense.size(); ++i) gd[i] = pr.dplan[i].gemm ? 1 : 0;
-      level_schedule(pr.P, gd);
+      level_schedule(pr, gd);
     }
   }
   // Weight / bias gradient destinations handled by the GEMM path.  Dense
@@ -476,7 +557,7 @@ void build_staged_plan(tg_program& pr) {
            pr.dplan[a].dw_dest0 == pr.dplan[b].dw_dest0 && pr.dplan[a].db_dest0 == pr.dplan[b].db_dest0;
   };
   auto split = [&](const std::vector<tgc::Instr>& list, const std::vector<std::uint32_t>& key,
-                   std::vector<tg_program::Stage>& out) {
+                   std::vector<tg_program::Stage>& out, bool sums) {
     out.clear();
     const bool lv = pr.levels && key.size() == list.size();
     std::uint32_t b = 0;
@@ -484,7 +565,18 @@ void build_staged_plan(tg_program& pr) {
       if (e > b) out.push_back({-1, b, e, lv});
       b = e;
     };
+    // after the last stage of a reverse level: the sums of its contended rows
+    auto level_end = [&](std::uint32_t k) {
+      if (!sums || !lv) return;
+      const std::uint32_t L = key[k] >> 12;
+      if (L < pr.level_sums.size() && pr.level_sums[L].second > pr.level_sums[L].first)
+        out.push_back({kSumStage, pr.level_sums[L].first, pr.level_sums[L].second, false});
+    };
     for (std::uint32_t k = 0; k < list.size(); ++k) {
+      if (lv && k > 0 && (key[k] >> 12) != (key[k - 1] >> 12)) {
+        flush(k);
+        level_end(k - 1);
+      }
       if (list[k].kind == tgc::kDense && pr.dplan[list[k].aux].gemm) {
         flush(k);
         const std::uint32_t id = list[k].aux;
@@ -504,10 +596,11 @@ void build_staged_plan(tg_program& pr) {
       }
     }
     flush(static_cast<std::uint32_t>(list.size()));
+    if (!list.empty()) level_end(static_cast<std::uint32_t>(list.size() - 1));
   };
   pr.batches.clear();
-  split(P.fwd, P.fwd_level, pr.sfwd);
-  split(P.bwd, P.bwd_level, pr.sbwd);
+  split(P.fwd, P.fwd_level, pr.sfwd, false);
+  split(P.bwd, P.bwd_level, pr.sbwd, true);
   // batch tables: forward {0, x, z, h}, input adjoints {0, z, x, 0}, weight gradient {z, x, 0, 0}
   const bool tc = pr.tsz() == 4 && pr.umma;
   for (auto& B : pr.batches) {
@@ -548,7 +641,7 @@ void build_staged_plan(tg_program& pr) {
     auto stats = [&](const char* name, const std::vector<tg_program::Stage>& st, const std::vector<tgc::Instr>& list) {
       std::size_t nl = 0, ni = 0, nops = 0, small = 0;
       for (const auto& s : st) {
-        if (s.batch >= 0) continue;
+        if (s.batch != -1) continue;
         ++nl;
         ni += s.end - s.begin;
         small += (s.end - s.begin) < 128;
@@ -558,9 +651,22 @@ void build_staged_plan(tg_program& pr) {
       }
       std::fprintf(stderr, "[staged] %s: %zu stages (%zu interpreter, %zu with <128 instrs), %zu instrs, %zu operands\n",
                    name, st.size(), nl, small, ni, nops);
+      std::map<int, std::size_t> ops_small;
+      std::set<std::uint32_t> lv_small;
+      const auto& key = list.data() == P.fwd.data() ? P.fwd_level : P.bwd_level;
+      for (const auto& s : st)
+        if (s.batch == -1 && s.end - s.begin < 128)
+          for (std::uint32_t k = s.begin; k < s.end; ++k) {
+            ops_small[list[k].kind == tgc::kNode ? list[k].op : 1000 + list[k].kind]++;
+            if (key.size() == list.size()) lv_small.insert(key[k] >> 12);
+          }
+      std::fprintf(stderr, "[staged]   small stages span %zu levels; ops:", lv_small.size());
+      for (const auto& [op, c] : ops_small) std::fprintf(stderr, " %d:%zu", op, c);
+      std::fprintf(stderr, "\n");
     };
     std::size_t nb = 0, nbm = 0;
     for (const auto& B : pr.batches) if (B.members.size() > 1) { ++nb; nbm += B.members.size(); }
+    std::fprintf(stderr, "[staged] %zu contended-row sums, %u temporary rows\n", pr.sums.size(), pr.n_tmp);
     std::fprintf(stderr, "[staged] rows %u, dense %zu (%zu GEMM), %zu batches (%zu with %zu members); %zu generic dests, %zu scatter dests\n",
                  P.n_rows, P.dense.size(), ng, pr.batches.size(), nb, nbm, pr.gen_dests.size(), pr.sc_dests.size());
     stats("fwd", pr.sfwd, P.fwd);
@@ -568,15 +674,16 @@ void build_staged_plan(tg_program& pr) {
   }
 }
 
-// Samples per chunk of the staged path: rows of V and G for the chunk within
-// 48 GB of the B200's 180 GB HBM (TG_STAGED_MB overrides), a multiple of 128.
-// One chunk covers cfg4 (b = 8,192, ~6e5 rows: 39 GB) and cfg5 (b = 1M:
-// 39 GB), so every stage runs once per step over the whole batch (a 4 GB
-// budget split cfg4 into ten chunks: 36k launches per step).
+// Samples per chunk of the staged path: rows of V and G (plus the reverse
+// levels' contended-row temporaries) for the chunk within 64 GB of the B200's
+// 180 GB HBM (TG_STAGED_MB overrides), a multiple of 128.  One chunk covers
+// cfg4 (b = 8,192: 6.0e5 rows of V and G + 2.7e5 temporaries, 48 GB) and cfg5
+// (b = 1M: 39 GB), so every stage runs once per step over the whole batch (a
+// 4 GB budget split cfg4 into ten chunks: 36k launches per step).
 std::size_t staged_chunk(const tg_program& pr, std::size_t batch) {
-  std::size_t budget = std::size_t(48) << 30;
+  std::size_t budget = std::size_t(64) << 30;
   if (const char* e = std::getenv("TG_STAGED_MB")) budget = std::size_t(std::atoll(e)) << 20;
-  const std::size_t per = 2 * std::max<std::size_t>(1, pr.P.n_rows) * pr.tsz();
+  const std::size_t per = (2 * std::max<std::size_t>(1, pr.P.n_rows) + pr.n_tmp) * pr.tsz();
   std::size_t cb = std::max<std::size_t>(128, (budget / per) / 128 * 128);
   const std::size_t need = (std::max<std::size_t>(batch, 1) + 127) / 128 * 128;
   return std::min(cb, need);
@@ -661,7 +768,7 @@ Layout layout(const tg_program& pr, std::size_t batch) {
     L.ug = off; off = align_up(off + std::max<std::size_t>(1, pr.P.n_uv) * t);
     L.partial = off; off = align_up(off + std::max<std::uint32_t>(1, pr.n_dest()) * t);
     L.gv = off; off = align_up(off + std::size_t(pr.P.n_rows) * cb * t);
-    L.gg = off; off = align_up(off + std::size_t(pr.P.n_rows) * cb * t);
+    L.gg = off; off = align_up(off + (std::size_t(pr.P.n_rows) + pr.n_tmp) * cb * t);   // + contended-row temporaries
     std::size_t sk = 0;
     for (std::size_t i = 0; i < pr.P.dense.size(); ++i)
       if (pr.dplan[i].gemm && pr.dplan[i].dw_dest0 != tgc::kNone)
@@ -766,6 +873,7 @@ tg_status upload(tg_program& pr) {
     TG_TRY(upload_vec(pr, pr.sc_uses, &pr.d_sc_uses));
     TG_TRY(upload_vec(pr, pr.sc_use_off, &pr.d_sc_use_off));
     TG_TRY(upload_vec(pr, pr.sc_dests, &pr.d_sc_dests));
+    TG_TRY(upload_vec(pr, pr.sums, &pr.d_sums));
     for (auto& B : pr.batches) {
       TG_TRY(upload_vec(pr, B.tab, &B.d_tab));
       TG_TRY(upload_vec(pr, B.zero_x, &B.d_zero_x));
@@ -1037,6 +1145,11 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
     ++pr.launches;
     // ---- reverse stages ----
     for (const auto& stg : pr.sbwd) {
+      if (stg.batch == kSumStage) {
+        TG_CUDA_TRY(tgk::launch_row_sums<T>(pr.d_sums + stg.begin, stg.end - stg.begin, G, n, cb, st));
+        ++pr.launches;
+        continue;
+      }
       if (stg.batch < 0) {
         ra.flags = tgk::kRBwd;
         ra.bwd_begin = stg.begin;
@@ -1421,6 +1534,9 @@ tg_status diagnose(tg_program& pr, std::int64_t sample, cudaStream_t st) {
   ma.diag_sample = sample;
   ma.loss = nullptr;
   ma.igrad = nullptr;
+  // domain violations happen in the forward sweep; the reverse sweep of a
+  // staged program also writes temporaries beyond the interpreter's rows
+  ma.n_bwd = 0;
   TG_CUDA_TRY(tgk::launch_tape<T>(ma, pr.smem, 1, pr.S, pr.smem_bytes, st));
   ++pr.launches;
   return TG_OK;

@@ -57,13 +57,13 @@ struct RowAccS {
     const std::uint32_t op = o[k];
     const std::uint32_t m = op >> kModeShift, i = op & kIndexMask;
     const std::uint8_t f = fl[k];
-    if (m == tgc::kSlot) {
+    if (f & tgc::kToAux) {   // sample-invariant operand, or (staged levels) a contended row's temporary
+      G[std::size_t(ax[k]) * ld + col] = v;
+    } else if (m == tgc::kSlot) {
       T* p = &G[i * ld + col];
       *p = (f & tgc::kAssign) ? v : *p + v;
     } else if (m == tgc::kSGather) {
       G[sg_row(i) * ld + col] += v;
-    } else if (f & tgc::kToAux) {
-      G[std::size_t(ax[k]) * ld + col] = v;
     }
   }
 };
@@ -173,6 +173,27 @@ __global__ void __launch_bounds__(128) k_level_range(RangeArgs<T> a) {
   RowAccS<T> acc{a.V, a.G, a.ld, col, a.UV, a.idx, a.batch, s, a.sg, a.cand, nullptr, nullptr, nullptr};
   if (a.flags & kRFwd) fwd_instr(a, acc, a.fwd_begin + blockIdx.x, s, col);
   else bwd_instr(a, acc, a.bwd_begin + blockIdx.x, col);
+}
+
+// Sums of the contended rows of one reverse level (entry blockIdx.x, 128
+// samples per CTA row): the temporaries in execution order after the row's
+// earlier value, so the result does not depend on scheduling.
+template <class T>
+__global__ void __launch_bounds__(128) k_row_sums(const uint4* __restrict__ ent, T* G, std::size_t n, std::size_t ld) {
+  const std::size_t col = std::size_t(blockIdx.y) * blockDim.x + threadIdx.x;
+  if (col >= n) return;
+  const uint4 e = ent[blockIdx.x];
+  T v = (e.y & 1u) ? T(0) : G[std::size_t(e.x) * ld + col];
+  std::uint32_t i = 0;
+  for (; i + 4 <= e.w; i += 4) {
+    T x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = G[std::size_t(e.z + i + u) * ld + col];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v += x[u];
+  }
+  for (; i < e.w; ++i) v += G[std::size_t(e.z + i) * ld + col];
+  G[std::size_t(e.x) * ld + col] = v;
 }
 
 // ---- register-tiled SIMT GEMM ------------------------------------------------
@@ -497,6 +518,13 @@ cudaError_t launch_act_bwd(T* G, const T* V, std::uint32_t z_row, std::uint32_t 
 }
 
 template <class T>
+cudaError_t launch_row_sums(const uint4* ent, std::uint32_t n_ent, T* G, std::size_t n, std::size_t ld, cudaStream_t st) {
+  if (n == 0 || n_ent == 0) return cudaSuccess;
+  k_row_sums<T><<<dim3(n_ent, static_cast<unsigned>((n + 127) / 128)), 128, 0, st>>>(ent, G, n, ld);
+  return cudaGetLastError();
+}
+
+template <class T>
 cudaError_t launch_act_bwd_batched(T* G, const T* V, const uint4* mem, std::uint32_t n_mem, std::uint32_t n_out, std::size_t n,
                                    std::size_t ld, std::uint32_t act, cudaStream_t st) {
   if (n == 0 || n_out == 0 || n_mem == 0) return cudaSuccess;
@@ -546,6 +574,7 @@ cudaError_t launch_contract(const std::uint32_t* dests, std::uint32_t n_dests, c
                                          std::size_t, std::uint32_t, cudaStream_t);                                        \
   template cudaError_t launch_rowsum<T>(const T*, std::uint32_t, std::uint32_t, std::size_t, std::size_t, T*,              \
                                         cudaStream_t);                                                                     \
+  template cudaError_t launch_row_sums<T>(const uint4*, std::uint32_t, T*, std::size_t, std::size_t, cudaStream_t);       \
   template cudaError_t launch_act_bwd_batched<T>(T*, const T*, const uint4*, std::uint32_t, std::uint32_t, std::size_t,   \
                                                  std::size_t, std::uint32_t, cudaStream_t);                                \
   template cudaError_t launch_rowsum_batched<T>(const T*, const uint4*, std::uint32_t, std::uint32_t, std::size_t,          \

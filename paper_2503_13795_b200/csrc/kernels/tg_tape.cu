@@ -65,13 +65,13 @@ struct RowAcc {
     const std::uint32_t op = o[k];
     const std::uint32_t m = op >> kModeShift, i = op & kIndexMask;
     const std::uint8_t f = fl[k];
-    if (m == tgc::kSlot) {
+    if (f & tgc::kToAux) {   // sample-invariant operand, or (staged levels) a contended row's temporary
+      G[std::size_t(ax[k]) * ld + col] = v;
+    } else if (m == tgc::kSlot) {
       T* p = &G[i * ld + col];
       *p = (f & tgc::kAssign) ? v : *p + v;
     } else if (m == tgc::kSGather) {
       G[sg_row(i) * ld + col] += v;
-    } else if (f & tgc::kToAux) {
-      G[std::size_t(ax[k]) * ld + col] = v;
     }
   }
 };
