@@ -150,6 +150,7 @@ struct tg_program {
     std::uint32_t* d_zero_x = nullptr;
     int beta = 0;
     bool bf = false, bx = false, bw = false;   // forward / dX / dW run batched (else per member)
+    bool x_inputs = false;                     // every member's x rows are input leaves
   };
   std::vector<Batch> batches;
   // Contended adjoint rows of the reverse levels: pushes into a row with more
@@ -165,6 +166,7 @@ struct tg_program {
     std::uint32_t xrow0 = 0;
     std::uint32_t dw_dest0 = tgc::kNone, db_dest0 = tgc::kNone;
     int beta = 0;                 // dX: 0 store, 1 accumulate
+    bool x_inputs = false;        // x rows are all input leaves: dX only feeds the input gradients
     std::vector<std::uint32_t> zero_x;   // assign-flagged x rows zeroed first (mixed flags)
     std::uint32_t* d_zero_x = nullptr;
   };
@@ -499,10 +501,14 @@ void build_staged_plan(tg_program& pr) {
       for (std::uint32_t j = 0; j < D0.n_out; ++j) covered[bt->second + j] = 1;
     }
   }
+  std::vector<char> is_input(P.n_rows, 0);
+  for (std::uint32_t r : P.input_rows) if (r != tgc::kNone) is_input[r] = 1;
   for (std::size_t i = 0; i < P.dense.size(); ++i) {
     const tgc::Dense& D = P.dense[i];
     tg_program::DensePlan& dp = pr.dplan[i];
     if (!dp.gemm) continue;
+    dp.x_inputs = true;
+    for (std::uint32_t k = 0; k < D.n_in; ++k) dp.x_inputs = dp.x_inputs && is_input[dp.xrow0 + k];
     std::uint32_t n_assign = 0;
     for (std::uint32_t k = 0; k < D.n_in; ++k) n_assign += (P.oflag[D.x_opnd + k] & tgc::kAssign) ? 1 : 0;
     dp.beta = n_assign == D.n_in ? 0 : 1;
@@ -616,6 +622,8 @@ void build_staged_plan(tg_program& pr) {
       B.tab[2 * nm + p] = uint4{D.out_row, dp.xrow0, 0, 0};
       B.beta |= dp.beta;
     }
+    B.x_inputs = true;
+    for (std::uint32_t u : B.members) B.x_inputs = B.x_inputs && pr.dplan[u].x_inputs;
     B.zero_x.clear();
     for (std::uint32_t u : B.members) {
       const auto& dp = pr.dplan[u];
@@ -1166,13 +1174,15 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
         TG_CUDA_TRY(tgk::launch_act_bwd_batched<T>(G, V, B.d_tab, nm, D.n_out, n, cb, D.act_op, st));
         ++pr.launches;
       }
-      if (!B.zero_x.empty()) {
+      // input-leaf x rows: their adjoints are read only by the input-gradient output
+      bool dx_done = !igrad && B.x_inputs;
+      bool dw_done = false;
+      if (!dx_done && !B.zero_x.empty()) {
         TG_CUDA_TRY(tgk::launch_zero_rows<T>(G, B.d_zero_x, static_cast<std::uint32_t>(B.zero_x.size()), n, cb, st));
         ++pr.launches;
       }
-      bool dx_done = false, dw_done = false;
       if constexpr (std::is_same_v<T, float>) {
-        if (B.bx && (umask & 2)) {
+        if (!dx_done && B.bx && (umask & 2)) {
           tgk::GemmArgs<float> g{};
           g.A = UV + D.w_uv;
           g.lda = D.n_in;

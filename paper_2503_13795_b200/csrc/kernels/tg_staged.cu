@@ -335,8 +335,10 @@ __global__ void k_act_bwd(T* G, const T* V, std::uint32_t z_row, std::uint32_t h
   }
   const std::size_t zr = std::size_t(z_row + blockIdx.y) * ld + s, hr = std::size_t(h_row + blockIdx.y) * ld + s;
   // tanh / sigmoid / exp derivatives use the output only: skip the z read (a quarter of the bytes)
-  const bool need_z = act == Relu || act == Sqr || act == Cub;
-  G[zr] = act_bwd<T>(act, G[hr], V[hr], need_z ? V[zr] : T(0));
+  // relu: z > 0 exactly when h = relu(z) > 0 (NaN z gives h = 0), so the mask comes from h
+  const bool need_z = act == Sqr || act == Cub;
+  const T h = V[hr];
+  G[zr] = act == Relu ? (h > T(0) ? G[hr] : T(0)) : act_bwd<T>(act, G[hr], h, need_z ? V[zr] : T(0));
 }
 
 template <class T>

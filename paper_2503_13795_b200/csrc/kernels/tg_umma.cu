@@ -291,7 +291,8 @@ __device__ __forceinline__ std::uint64_t operand_desc(std::uint32_t base, bool m
 // drain each finished buffer into fp32 round-to-nearest register sums (one
 // output row per thread) while the tensor core fills the other one.
 constexpr int kFlush = 1;
-__device__ int g_umma_exp = 0;   // profiling ablations (wrong results): 1 skip conversion, 2 one MMA per k-step, 3 TMA ring only
+__device__ int g_umma_exp = 0;   // profiling ablations (wrong results): 1 skip conversion, 2 one MMA per k-step, 3 TMA ring
+                                 // only, 4 one MMA on the raw fp32 tiles (how kind::tf32 reads fp32 bits)
 constexpr int kConvThreads = 256;                 // 8 converter / drain warps
 constexpr int kTThreads = 64 + kConvThreads;      // + TMA producer + MMA issuer
 
@@ -391,7 +392,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_umma_tma(GemmArgs<float> g, co
           const std::uint64_t dAh = operand_desc(a_hi, a_mn, ks), dAl = operand_desc(a_lo, a_mn, ks);
           const std::uint64_t dBh = operand_desc(b_hi, b_mn, ks), dBl = operand_desc(b_lo, b_mn, ks);
           if (g_umma_exp == 3) continue;   // no MMAs at all: the TMA ring alone
-          if (g_umma_exp == 2) {
+          if (g_umma_exp == 2 || g_umma_exp == 4) {
             mma_tf32(td, dAh, dBh, idesc, (t % kFlush != 0 || ks != 0) ? 1u : 0u);
             continue;
           }
@@ -440,7 +441,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_umma_tma(GemmArgs<float> g, co
       const int s = t % kTStages;
       mbar_wait2(full(s), (t / kTStages) & 1);
       unsigned char* base = smem + s * kTStage;
-      const int nop = (g_umma_exp == 1 || g_umma_exp == 3) ? 0 : 2;
+      const int nop = (g_umma_exp == 1 || g_umma_exp == 3 || g_umma_exp == 4) ? 0 : 2;
 #pragma unroll
       for (int op = 0; op < nop; ++op) {
         float4* hi = reinterpret_cast<float4*>(base + op * 2 * kTTile);
