@@ -269,7 +269,9 @@ tg_status tg_profile_read(tg_program_t p, double* tape_ms, uint64_t* tape_launch
  *   A(m,k) = a_kmajor ? A[m*lda + k] : A[k*lda + m]
  *   B(k,n) = b_nmajor ? B[k*ldb + n] : B[n*ldb + k]
  * engine 0: SIMT register-tiled (fp32 / fp64); 1: tcgen05 tensor cores,
- * 3xTF32 (fp32 only).  accumulate != 0 adds into C.  Device pointers. */
+ * 3xTF32 (fp32 only; CTA pairs with 256 x 256 tiles when M > 128); 2: the
+ * same with single-CTA 128 x 128 tiles only.  accumulate != 0 adds into C.
+ * Device pointers. */
 tg_status tg_gemm(tg_dtype dtype, int engine, uint32_t M, uint32_t N, uint32_t K, const void* A, size_t lda,
                   int a_kmajor, const void* B, size_t ldb, int b_nmajor, void* C, size_t ldc, int accumulate,
                   tg_stream_t stream);

@@ -697,9 +697,16 @@ std::size_t staged_chunk(const tg_program& pr, std::size_t batch) {
   return std::min(cb, need);
 }
 
+// CTAs per split-K slice of a dense layer's weight-gradient product: the
+// tcgen05 kernel's (CTA pairs of 256 x 256 when n_out > 128) for fp32, the
+// SIMT kernel's 64 x 64 tiles for fp64.
+std::uint32_t dw_ctas(const tgc::Dense& D, std::size_t tsz) {
+  if (tsz == 4) return tgk::umma_ctas_per_slice(D.n_out, D.n_in);
+  return ((D.n_out + 63) / 64) * ((D.n_in + 63) / 64);
+}
+
 std::uint32_t splitk_splits(const tgc::Dense& D, std::size_t n, std::size_t tsz) {
-  const std::uint32_t bm = tsz == 8 ? 64 : 128;
-  const std::uint32_t tiles = ((D.n_out + bm - 1) / bm) * ((D.n_in + bm - 1) / bm);
+  const std::uint32_t tiles = dw_ctas(D, tsz);
   std::uint32_t s = std::max<std::uint32_t>(1, 296 / std::max(1u, tiles));
   s = std::min<std::uint32_t>(s, static_cast<std::uint32_t>(std::max<std::size_t>(1, n / 256)));
   return std::max(1u, s);
@@ -708,7 +715,7 @@ std::uint32_t splitk_splits(const tgc::Dense& D, std::size_t n, std::size_t tsz)
 // Split-K slices per member of a batched weight-gradient product: about four
 // waves of CTAs over all members, slices of at least 256 samples.
 std::uint32_t batch_splits(const tgc::Dense& D, std::uint32_t nm, std::size_t n) {
-  const std::uint32_t tiles = ((D.n_out + 127) / 128) * ((D.n_in + 127) / 128) * std::max(1u, nm);
+  const std::uint32_t tiles = dw_ctas(D, 4) * std::max(1u, nm);
   std::uint32_t z = std::max<std::uint32_t>(1, (592 + tiles - 1) / tiles);
   return std::min<std::uint32_t>(z, static_cast<std::uint32_t>(std::max<std::size_t>(1, n / 256)));
 }
@@ -1906,9 +1913,10 @@ extern "C" tg_status tg_gemm(tg_dtype dtype, int engine, uint32_t M, uint32_t N,
     if (dtype == TG_F32) {
       tgk::GemmArgs<float> g{};
       fill(static_cast<const float*>(A), static_cast<const float*>(B), static_cast<float*>(C), g);
-      TG_CUDA_TRY(engine == 1 ? tgk::launch_gemm_umma(g, 1, st) : tgk::launch_gemm<float>(g, 1, st));
+      g.no_pair = engine == 2;   // engine 2: tcgen05 with single-CTA tiles only
+      TG_CUDA_TRY(engine >= 1 ? tgk::launch_gemm_umma(g, 1, st) : tgk::launch_gemm<float>(g, 1, st));
     } else {
-      if (engine == 1) return fail(TG_UNSUPPORTED, "tg_gemm: no fp64 tcgen05 kind");
+      if (engine >= 1) return fail(TG_UNSUPPORTED, "tg_gemm: no fp64 tcgen05 kind");
       tgk::GemmArgs<double> g{};
       fill(static_cast<const double*>(A), static_cast<const double*>(B), static_cast<double*>(C), g);
       TG_CUDA_TRY(tgk::launch_gemm<double>(g, 1, st));

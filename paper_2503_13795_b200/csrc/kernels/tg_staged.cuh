@@ -82,6 +82,7 @@ struct GemmArgs {
   const uint4* mem;
   std::uint32_t zs;
   std::uint32_t a_span, b_span;
+  bool no_pair;            // tcgen05 path: single-CTA tiles even when M > 128 (tg_gemm engine 2)
 };
 
 // Table-scatter (kind-1) batch terms grouped by (adjoint row a, index column f).
@@ -105,6 +106,8 @@ template <class T> cudaError_t launch_level_range(const RangeArgs<T>& a, cudaStr
 template <class T> cudaError_t launch_gemm(const GemmArgs<T>& g, std::uint32_t splits, cudaStream_t st);
 // fp32 GEMM on the 5th-gen tensor cores (tcgen05.mma kind::tf32, 3xTF32 split), tg_umma.cu
 cudaError_t launch_gemm_umma(const GemmArgs<float>& g, std::uint32_t splits, cudaStream_t st);
+// CTAs one split-K slice / batch member of a tcgen05 product launches (CTA pairs when M > 128)
+std::uint32_t umma_ctas_per_slice(std::uint32_t M, std::uint32_t N);
 // dst[m * N + n] += sum_kz part[kz][m][n]   (fixed order)
 template <class T> cudaError_t launch_splitk_reduce(const T* part, T* dst, std::uint32_t MN, std::uint32_t splits, cudaStream_t st);
 // G[z rows] = act'(G[h rows], V[h rows], V[z rows]) for n_out consecutive rows

@@ -517,6 +517,304 @@ __global__ void __launch_bounds__(kTThreads, 1) k_umma_tma(GemmArgs<float> g, co
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * BN));
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair variant (k_umma_pair): two CTAs of a (2,1,1) cluster on one TPC run
+// one 256 x 256 output tile with tcgen05.mma.cta_group::2 (M = 256, N = 256).
+// CTA r holds A rows [128 r, 128 r + 128) and B columns [128 r, 128 r + 128)
+// of the pair's tile in its own shared memory (the same per-CTA layout as
+// k_umma_tma), and TMEM lanes of its 128 output rows x all 256 columns.
+// Per k-tile a CTA lands and converts 32 KB as before but feeds twice the
+// MMA work, which halves the L2 -> SM traffic and the shared-memory traffic
+// per flop: in k_umma_tma (one CTA, N = 128) the MMAs' own operand reads
+// (8 KB per 64-cycle MMA) already fill the 128 B/cycle shared-memory port,
+// so TMA writes and the converter's hi/lo pass could only queue behind them.
+//
+// Roles per CTA are those of k_umma_tma with 16 converter / drain warps (the
+// 128 x 256 fp32 running sum is 64 registers per thread); only the leader's
+// warp 1 issues MMAs.
+// Cross-CTA signalling:
+//   full[s]   local: this CTA's TMA bytes landed;
+//   conv[s]   leader: one arrive per converter warp of both CTAs (32);
+//   empty[s]  both: tcgen05.commit multicast (the MMAs reading stage s retired);
+//   tfull[b]  both: commit multicast (accumulator buffer b complete);
+//   tempty[b] leader: one arrive per drain warp of both CTAs (32).
+// The accumulator is drained every kPFlush k-tiles (TMEM reads per k-tile
+// double with N = 256; 2 tiles = K 64 keeps the tensor core's biased fp32
+// accumulation at ~7e-7 relative).
+constexpr int kPN = 256;
+constexpr int kPFlush = 2;
+constexpr int kPConv = 512;                 // 16 converter / drain warps: 64 accumulator columns per thread
+constexpr int kPThreads = 64 + kPConv;
+__host__ __device__ constexpr std::uint32_t pair_smem(int stages) {
+  return (stages * kTStage > BM * (kPN + 4) * 4 ? stages * kTStage : BM * (kPN + 4) * 4) + 1024 + 512;
+}
+
+__device__ __forceinline__ std::uint32_t cluster_rank() {
+  std::uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of a local shared::cta address in CTA `rank`
+__device__ __forceinline__ std::uint32_t peer_addr(std::uint32_t local, std::uint32_t rank) {
+  std::uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(std::uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_acq(std::uint32_t mbar, std::uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "TG_WAITC:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra TG_DONEC;\n\t"
+      "bra TG_WAITC;\n"
+      "TG_DONEC:\n\t}\n" ::"r"(mbar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mma_tf32_pair(std::uint32_t tmem_d, std::uint64_t a, std::uint64_t b, std::uint32_t idesc,
+                                              std::uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void commit_pair(std::uint32_t mbar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(mbar),
+      "h"(static_cast<unsigned short>(3)));
+}
+
+template <int kTStages>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
+    k_umma_pair(GemmArgs<float> g, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                int a_mn, int b_mn) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + pair_smem(kTStages) - 1024 - 512);
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 3 * kTStages + 4);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const std::uint32_t rank = cluster_rank();
+  auto full = [&](int s) { return smem_u32(&bars[s]); };
+  auto conv = [&](int s) { return smem_u32(&bars[kTStages + s]); };
+  auto empty = [&](int s) { return smem_u32(&bars[2 * kTStages + s]); };
+  auto tfull = [&](int b) { return smem_u32(&bars[3 * kTStages + b]); };
+  auto tempty = [&](int b) { return smem_u32(&bars[3 * kTStages + 2 + b]); };
+  constexpr std::uint32_t kArrivals = 2 * (kPConv / 32);   // converter / drain warps of both CTAs
+
+  if (tid == 0) {
+    for (int s = 0; s < kTStages; ++s) {
+      mbar_init(full(s), 1);
+      mbar_init(conv(s), kArrivals);
+      mbar_init(empty(s), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull(b), 1);
+      mbar_init(tempty(b), kArrivals);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(2 * kPN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  cluster_sync_all();   // both CTAs' barriers initialised and TMEM allocated
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const std::uint32_t tmem = *tmem_slot;
+
+  const int m0 = static_cast<int>(blockIdx.x >> 1) * (2 * BM) + static_cast<int>(rank) * BM;
+  const int n0 = static_cast<int>(blockIdx.y) * kPN;
+  const int nb = n0 + static_cast<int>(rank) * BN;   // this CTA's B rows
+  std::uint32_t slice = blockIdx.z;
+  int a_off = 0, b_off = 0;
+  std::size_t c_off = 0, c2_off = 0;
+  if (g.mem) {
+    const uint4 e = g.mem[blockIdx.z / g.zs];
+    slice = blockIdx.z % g.zs;
+    a_off = static_cast<int>(e.x);
+    b_off = static_cast<int>(e.y);
+    c_off = e.z;
+    c2_off = e.w;
+  }
+  std::uint32_t k_begin = 0, k_end = g.K;
+  if (g.epi == kEpiSplitK) {
+    k_begin = slice * g.k_chunk;
+    k_end = min(g.K, k_begin + g.k_chunk);
+  }
+  const std::uint32_t T = k_end > k_begin ? (k_end - k_begin + BK - 1) / BK : 0;
+  const std::uint32_t NG = (T + kPFlush - 1) / kPFlush;
+
+  if (warp == 0) {
+    // ===== TMA producer (each CTA loads its own A rows and B columns) =====
+    if (lane == 0)
+      for (std::uint32_t t = 0; t < T; ++t) {
+        const int s = t % kTStages;
+        if (t >= kTStages) mbar_wait2(empty(s), ((t / kTStages) - 1) & 1);
+        const std::uint32_t base = smem_u32(smem + s * kTStage);
+        mbar_expect_tx(full(s), 2 * kTTile);
+        const int k0 = static_cast<int>(k_begin + t * BK);
+        tma_operand(&tmA, a_mn, base, m0, k0, a_off, full(s));
+        tma_operand(&tmB, b_mn, base + 2 * kTTile, nb, k0, b_off, full(s));
+      }
+  } else if (warp == 1) {
+    // ===== MMA issuer: the leader CTA only =====
+    if (rank == 0) {
+      const std::uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (std::uint32_t(a_mn) << 15) |
+                                  (std::uint32_t(b_mn) << 16) | ((kPN >> 3) << 17) | (((2 * BM) >> 4) << 24);
+      for (std::uint32_t t = 0; t < T; ++t) {
+        const int s = t % kTStages;
+        const std::uint32_t grp = t / kPFlush;
+        const int buf = grp & 1;
+        if (t % kPFlush == 0 && grp >= 2) mbar_wait_acq(tempty(buf), ((grp >> 1) - 1) & 1);
+        mbar_wait_acq(conv(s), (t / kTStages) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (lane == 0) {
+          const std::uint32_t a_hi = smem_u32(smem + s * kTStage), a_lo = a_hi + kTTile;
+          const std::uint32_t b_hi = a_hi + 2 * kTTile, b_lo = a_hi + 3 * kTTile;
+          const std::uint32_t td = tmem + buf * kPN;
+#pragma unroll
+          for (int ks = 0; ks < BK / 8; ++ks) {
+            const std::uint64_t dAh = operand_desc(a_hi, a_mn, ks), dAl = operand_desc(a_lo, a_mn, ks);
+            const std::uint64_t dBh = operand_desc(b_hi, b_mn, ks), dBl = operand_desc(b_lo, b_mn, ks);
+            if (g_umma_exp == 3) continue;
+            if (g_umma_exp == 2 || g_umma_exp == 4) {
+              mma_tf32_pair(td, dAh, dBh, idesc, (t % kPFlush != 0 || ks != 0) ? 1u : 0u);
+              continue;
+            }
+            mma_tf32_pair(td, dAl, dBh, idesc, (t % kPFlush != 0 || ks != 0) ? 1u : 0u);
+            mma_tf32_pair(td, dAh, dBl, idesc, 1u);
+            mma_tf32_pair(td, dAh, dBh, idesc, 1u);
+          }
+          commit_pair(empty(s));
+          if (t % kPFlush == kPFlush - 1 || t == T - 1) commit_pair(tfull(buf));
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ===== converters + accumulation drain (16 warps: TMEM lane quarter w % 4, column quarter) =====
+    const int ct = tid - 64;
+    const int wq = warp & 3;
+    const int c0 = ((warp - 2) >> 2) * (kPN / 4);
+    constexpr int kCols = kPN / 4;
+    const std::uint32_t leader_conv0 = peer_addr(conv(0), 0);
+    const std::uint32_t leader_tempty0 = peer_addr(tempty(0), 0);
+    float acc[kCols];
+#pragma unroll
+    for (int j = 0; j < kCols; ++j) acc[j] = 0.f;
+    auto drain = [&](std::uint32_t grp) {
+      const int buf = grp & 1;
+      mbar_wait2(tfull(buf), (grp >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+      for (int c = 0; c < kCols; c += 16) {
+        std::uint32_t r[16];
+        const std::uint32_t taddr = tmem + buf * kPN + (static_cast<std::uint32_t>(wq * 32) << 16) + c0 + c;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+              "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[c + j] += __uint_as_float(r[j]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(leader_tempty0 + buf * 8);
+    };
+    for (std::uint32_t t = 0; t < T; ++t) {
+      const int s = t % kTStages;
+      mbar_wait2(full(s), (t / kTStages) & 1);
+      unsigned char* base = smem + s * kTStage;
+      const int nop = (g_umma_exp == 1 || g_umma_exp == 3 || g_umma_exp == 4) ? 0 : 2;
+#pragma unroll
+      for (int op = 0; op < nop; ++op) {
+        float4* hi = reinterpret_cast<float4*>(base + op * 2 * kTTile);
+        float4* lo = reinterpret_cast<float4*>(base + op * 2 * kTTile + kTTile);
+#pragma unroll 4
+        for (int i = ct; i < static_cast<int>(kTTile / 16); i += kPConv) {
+          const float4 x = hi[i];
+          float4 h, l;
+          h.x = tf32_rna(x.x); l.x = tf32_rna(x.x - h.x);
+          h.y = tf32_rna(x.y); l.y = tf32_rna(x.y - h.y);
+          h.z = tf32_rna(x.z); l.z = tf32_rna(x.z - h.z);
+          h.w = tf32_rna(x.w); l.w = tf32_rna(x.w - h.w);
+          hi[i] = h;
+          lo[i] = l;
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;");   // generic-proxy stores -> tensor-core reads
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(leader_conv0 + s * 8);
+      if (t % kPFlush == 0 && t > 0) drain(t / kPFlush - 1);
+    }
+    if (NG > 0) drain(NG - 1);
+    // ===== epilogue: this CTA's 128 rows x 256 columns through shared memory =====
+    constexpr int kLd = kPN + 4;
+    float* tile = reinterpret_cast<float*>(smem);
+    asm volatile("bar.sync 1, %0;" ::"n"(kPConv));
+    {
+      const int r = wq * 32 + lane;
+#pragma unroll
+      for (int j = 0; j < kCols; j += 4)
+        *reinterpret_cast<float4*>(tile + r * kLd + c0 + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(kPConv));
+    const int cw = (tid - 64) >> 5;
+    const bool vec = (g.ldc % 4 == 0) && (g.epi != kEpiSplitK || g.N % 4 == 0);
+    for (int r = cw; r < BM; r += kPConv / 32) {
+      const std::uint32_t m = static_cast<std::uint32_t>(m0 + r);
+      if (m >= g.M) continue;
+#pragma unroll
+      for (int hlf = 0; hlf < 2; ++hlf) {
+        const std::uint32_t n = static_cast<std::uint32_t>(n0 + hlf * 128) + 4 * lane;
+        if (n >= g.N) continue;
+        const float4 v = *reinterpret_cast<const float4*>(tile + r * kLd + hlf * 128 + 4 * lane);
+        float a4[4] = {v.x, v.y, v.z, v.w};
+        float* dst = g.epi == kEpiSplitK ? g.C + (std::size_t(blockIdx.z) * g.M + m) * g.N + n
+                                         : g.C + (c_off + m) * g.ldc + n;
+        const int cnt = min(4u, g.N - n);
+        if (g.epi == kEpiBiasAct) {
+          const float bv = g.bias ? g.bias[m] : 0.f;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) a4[e] += bv;
+          if (g.act) {
+            float h4[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) h4[e] = act_fwd<float>(g.act, a4[e]);
+            float* d2 = g.C2 + (c2_off + m) * g.ldc + n;
+            if (vec && cnt == 4) *reinterpret_cast<float4*>(d2) = make_float4(h4[0], h4[1], h4[2], h4[3]);
+            else for (int e = 0; e < cnt; ++e) d2[e] = h4[e];
+          }
+        } else if (g.epi == kEpiAccum && g.beta) {
+          if (vec && cnt == 4) {
+            const float4 o = *reinterpret_cast<const float4*>(dst);
+            a4[0] += o.x; a4[1] += o.y; a4[2] += o.z; a4[3] += o.w;
+          } else {
+            for (int e = 0; e < cnt; ++e) a4[e] += dst[e];
+          }
+        }
+        if (vec && cnt == 4) *reinterpret_cast<float4*>(dst) = make_float4(a4[0], a4[1], a4[2], a4[3]);
+        else for (int e = 0; e < cnt; ++e) dst[e] = a4[e];
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  cluster_sync_all();   // no CTA leaves while its peer may still signal its barriers or read its tiles
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * kPN));
+}
+
 // Host: 2D tensor map of an operand view for TMA (SWIZZLE_128B, zero OOB fill).
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -553,7 +851,47 @@ bool make_operand_map(CUtensorMap* map, const float* P, std::size_t ld, bool mn,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
+
+// CTA pairs for products with more than one 128-row M tile (TG_UMMA_PAIR=0: single CTAs)
+bool use_pair(std::uint32_t M) {
+  static const bool on = !(std::getenv("TG_UMMA_PAIR") && std::getenv("TG_UMMA_PAIR")[0] == '0');
+  return on && M > static_cast<std::uint32_t>(BM);
+}
+
+cudaError_t launch_tma_kernel(const GemmArgs<float>& g, std::uint32_t z, const CUtensorMap& ta, const CUtensorMap& tb,
+                              bool a_mn, bool b_mn, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    for (cudaError_t e : {cudaFuncSetAttribute(k_umma_tma<kTStagesMax>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(tma_smem(kTStagesMax))),
+                          cudaFuncSetAttribute(k_umma_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(tma_smem(1))),
+                          cudaFuncSetAttribute(k_umma_pair<kTStagesMax>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(pair_smem(kTStagesMax)))})
+      if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (use_pair(g.M) && !g.no_pair) {
+    const dim3 grid(2 * ((g.M + 2 * BM - 1) / (2 * BM)), (g.N + kPN - 1) / kPN, z);
+    k_umma_pair<kTStagesMax><<<grid, kPThreads, pair_smem(kTStagesMax), st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0);
+    return cudaGetLastError();
+  }
+  const dim3 grid((g.M + BM - 1) / BM, (g.N + BN - 1) / BN, z);
+  // one k-tile per CTA (K <= 32): a 1-stage ring, so two CTAs share an SM
+  // and one's TMA / epilogue latency hides behind the other's work
+  const std::uint32_t kspan = g.epi == kEpiSplitK ? g.k_chunk : g.K;
+  if (kspan <= static_cast<std::uint32_t>(BK))
+    k_umma_tma<1><<<grid, kTThreads, tma_smem(1), st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0);
+  else
+    k_umma_tma<kTStagesMax><<<grid, kTThreads, tma_smem(kTStagesMax), st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0);
+  return cudaGetLastError();
+}
 }  // namespace
+
+std::uint32_t umma_ctas_per_slice(std::uint32_t M, std::uint32_t N) {
+  if (use_pair(M)) return 2 * ((M + 2 * BM - 1) / (2 * BM)) * ((N + kPN - 1) / kPN);
+  return ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+}
 
 cudaError_t launch_gemm_umma(const GemmArgs<float>& g0, std::uint32_t splits, cudaStream_t st) {
   if (g0.M == 0 || g0.N == 0) return cudaSuccess;
@@ -603,22 +941,7 @@ cudaError_t launch_gemm_umma(const GemmArgs<float>& g0, std::uint32_t splits, cu
       };
       if (!span_map(&ta, g.A, g.lda, a_mn, g.M, g.a_span) || !span_map(&tb, g.B, g.ldb, b_mn, g.N, g.b_span))
         return cudaErrorInvalidValue;
-      static bool battr = false;
-      if (!battr) {
-        for (cudaError_t e : {cudaFuncSetAttribute(k_umma_tma<kTStagesMax>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   static_cast<int>(tma_smem(kTStagesMax))),
-                              cudaFuncSetAttribute(k_umma_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   static_cast<int>(tma_smem(1)))})
-          if (e != cudaSuccess) return e;
-        battr = true;
-      }
-      const dim3 grid((g.M + BM - 1) / BM, (g.N + BN - 1) / BN, splits);   // splits = members x zs
-      const std::uint32_t kspan = g.epi == kEpiSplitK ? g.k_chunk : g.K;
-      if (kspan <= static_cast<std::uint32_t>(BK))
-        k_umma_tma<1><<<grid, kTThreads, tma_smem(1), st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0);
-      else
-        k_umma_tma<kTStagesMax><<<grid, kTThreads, tma_smem(kTStagesMax), st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0);
-      return cudaGetLastError();
+      return launch_tma_kernel(g, splits, ta, tb, a_mn, b_mn, st);   // splits = members x zs
     }
     if (!make_operand_map(&ta, g.A, g.lda, a_mn, g.M, g.K)) {
       std::size_t ldp = g.lda;
@@ -635,24 +958,7 @@ cudaError_t launch_gemm_umma(const GemmArgs<float>& g0, std::uint32_t splits, cu
       if (pad_b) cudaFreeAsync(pad_b, st);
     };
     if (make_operand_map(&ta, g.A, g.lda, a_mn, g.M, g.K) && make_operand_map(&tb, g.B, g.ldb, b_mn, g.N, g.K)) {
-      static bool attr = false;
-      if (!attr) {
-        for (cudaError_t e : {cudaFuncSetAttribute(k_umma_tma<kTStagesMax>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   static_cast<int>(tma_smem(kTStagesMax))),
-                              cudaFuncSetAttribute(k_umma_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   static_cast<int>(tma_smem(1)))})
-          if (e != cudaSuccess) return e;
-        attr = true;
-      }
-      const dim3 grid((g.M + BM - 1) / BM, (g.N + BN - 1) / BN, g.epi == kEpiSplitK ? splits : 1);
-      // one k-tile per CTA (K <= 32): a 1-stage ring, so two CTAs share an SM
-      // and one's TMA / epilogue latency hides behind the other's work
-      const std::uint32_t kspan = g.epi == kEpiSplitK ? g.k_chunk : g.K;
-      if (kspan <= static_cast<std::uint32_t>(BK))
-        k_umma_tma<1><<<grid, kTThreads, tma_smem(1), st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0);
-      else
-        k_umma_tma<kTStagesMax><<<grid, kTThreads, tma_smem(kTStagesMax), st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0);
-      const cudaError_t e = cudaGetLastError();
+      const cudaError_t e = launch_tma_kernel(g, g.epi == kEpiSplitK ? splits : 1, ta, tb, a_mn, b_mn, st);
       release();
       return e;
     }

@@ -325,7 +325,7 @@ def test_fp64_tanh_accuracy(tier, monkeypatch):
     assert np.max(np.abs(IG[0] - (1 - L * L))) <= 1e-15
 
 
-@pytest.mark.parametrize("engine,dt", [(1, "f32"), (0, "f32"), (0, "f64")])
+@pytest.mark.parametrize("engine,dt", [(1, "f32"), (2, "f32"), (0, "f32"), (0, "f64")])
 @pytest.mark.parametrize("a_kmaj,b_nmaj", [(True, True), (False, True), (True, False)])
 @pytest.mark.parametrize("M,N,K", [(128, 128, 32), (300, 1000, 784), (10, 4096, 1024), (1024, 784, 2000)])
 def test_dense_gemm_engines(engine, dt, a_kmaj, b_nmaj, M, N, K):
@@ -454,7 +454,7 @@ def test_jit_forms_vs_reference(form, fuse, name, dt, b, monkeypatch):
     assert torch.equal(P1, P2)
 
 
-@pytest.mark.parametrize("engine", [0, 1])
+@pytest.mark.parametrize("engine", [0, 1, 2])
 @pytest.mark.parametrize("a_kmaj,b_nmaj", [(True, False), (True, True), (False, True)])
 def test_dense_gemm_long_k_accuracy(engine, a_kmaj, b_nmaj):
     """Long reduction axis (the weight-gradient role contracts over samples):
