@@ -137,7 +137,7 @@ struct tg_program {
   // register-resident specialisation (tg_jit.cpp)
   tgj::JitKernel jit;
   // staged execution over an HBM SoA workspace (large tapes, dense layers as GEMMs)
-  struct Stage { int batch; std::uint32_t begin, end; bool level = false; };   // batch >= 0: GEMM stage; level: one
+  struct Stage { int batch; std::uint32_t begin, end; bool level = false; bool inputs_only = false; };   // batch >= 0: GEMM stage; level: one
                                                                               // instruction per CTA column (k_level_range);
                                                                               // batch == kSumStage: sums[begin, end)
   // Dense layers of one dependency level over the same weights (a GPT's 64
@@ -151,6 +151,11 @@ struct tg_program {
     int beta = 0;
     bool bf = false, bx = false, bw = false;   // forward / dX / dW run batched (else per member)
     bool x_inputs = false;                     // every member's x rows are input leaves
+    // dX writes dz of the layer below: C rows = the producing members' z rows
+    // (tab[nm + p].z), act' taken from their h rows (= this batch's x rows,
+    // tab[nm + p].w); the producing batch then skips its activation backward
+    std::uint32_t dx_act = 0;
+    bool skip_act = false;
   };
   std::vector<Batch> batches;
   // Contended adjoint rows of the reverse levels: pushes into a row with more
@@ -167,6 +172,7 @@ struct tg_program {
     std::uint32_t dw_dest0 = tgc::kNone, db_dest0 = tgc::kNone;
     int beta = 0;                 // dX: 0 store, 1 accumulate
     bool x_inputs = false;        // x rows are all input leaves: dX only feeds the input gradients
+    std::uint32_t x_col0 = tgc::kNone;   // x rows = input columns x_col0.. in order: GEMMs read the inputs array
     std::vector<std::uint32_t> zero_x;   // assign-flagged x rows zeroed first (mixed flags)
     std::uint32_t* d_zero_x = nullptr;
   };
@@ -638,6 +644,122 @@ void build_staged_plan(tg_program& pr) {
     B.bx = tc && nm > 1 && D0.n_out % 32 == 0;
     B.bw = tc && nm > 1 && pr.dplan[B.members.front()].dw_dest0 != tgc::kNone;
   }
+  // Input adjoints fused with the activation backward of the layer below.  A
+  // batch C whose x rows are exactly the activation rows h of a batch A (act'
+  // expressible in h), where C's dX is the only push into those rows and
+  // assigns them, and no batch term reads their adjoints, writes
+  // G[z_A] = act'(h) * (W^T dZ_C) in its GEMM epilogue: G[h] is never
+  // materialised and A's activation-backward pass (read G[h], V[h], write
+  // G[z]) disappears.  TG_DX_ACT=0 disables.
+  const char* dxa = std::getenv("TG_DX_ACT");
+  if (!(dxa && dxa[0] == '0')) {
+    std::vector<std::uint32_t> pushers(P.n_rows, 0);
+    auto push_opnd = [&](std::uint32_t o) {
+      if ((P.opnd[o] >> tgc::kModeShift) == tgc::kSlot && (P.opnd[o] & tgc::kIndexMask) < P.n_rows)
+        ++pushers[P.opnd[o] & tgc::kIndexMask];
+    };
+    for (const auto& I : P.fwd) {
+      if (I.kind == tgc::kNode)
+        for (std::uint32_t k = 0; k < I.nops; ++k) push_opnd(I.opnd + k);
+      else if (I.kind == tgc::kDense)
+        for (std::uint32_t k = 0; k < P.dense[I.aux].n_in; ++k) push_opnd(P.dense[I.aux].x_opnd + k);
+    }
+    std::vector<char> term_a(P.n_rows, 0);
+    for (const auto& t : P.terms)
+      if (t.a < P.n_rows) term_a[t.a] = 1;
+    // the reverse list's batches (the forward list has its own copies)
+    std::vector<char> in_bwd(pr.batches.size(), 0);
+    for (const auto& stg : pr.sbwd)
+      if (stg.batch >= 0) in_bwd[stg.batch] = 1;
+    std::unordered_map<std::uint32_t, std::pair<std::uint32_t, std::uint32_t>> act_owner;   // h row0 -> (batch, member)
+    for (std::uint32_t bi = 0; bi < pr.batches.size(); ++bi)
+      if (in_bwd[bi])
+      for (std::uint32_t p = 0; p < pr.batches[bi].members.size(); ++p) {
+        const tgc::Dense& D = P.dense[pr.batches[bi].members[p]];
+        if (D.act_op == std::uint32_t(tg::OpKind::Relu) || D.act_op == std::uint32_t(tg::OpKind::Tanh) ||
+            D.act_op == std::uint32_t(tg::OpKind::Exp) || D.act_op == std::uint32_t(tg::OpKind::Sigmoid))   // act' from h
+          act_owner[D.act_row] = {bi, p};
+      }
+    for (std::uint32_t ci = 0; ci < pr.batches.size(); ++ci) {
+      auto& C = pr.batches[ci];
+      const std::uint32_t nm = static_cast<std::uint32_t>(C.members.size());
+      bool ok = in_bwd[ci] && !C.x_inputs && C.zero_x.empty() && C.beta == 0;
+      std::int64_t ab = -1;
+      std::vector<std::uint32_t> zrow(nm);
+      std::vector<char> seen;
+      for (std::uint32_t p = 0; ok && p < nm; ++p) {
+        const tgc::Dense& D = P.dense[C.members[p]];
+        const auto& dp = pr.dplan[C.members[p]];
+        auto it = act_owner.find(dp.xrow0);
+        ok = dp.beta == 0 && it != act_owner.end() && (ab < 0 || ab == it->second.first);
+        if (!ok) break;
+        ab = it->second.first;
+        if (seen.empty()) seen.assign(pr.batches[ab].members.size(), 0);
+        const tgc::Dense& A = P.dense[pr.batches[ab].members[it->second.second]];
+        ok = A.n_out == D.n_in && !seen[it->second.second] && &pr.batches[ab] != &C;
+        seen[it->second.second] = 1;
+        for (std::uint32_t k = 0; ok && k < D.n_in; ++k)
+          ok = pushers[dp.xrow0 + k] == 1 && !term_a[dp.xrow0 + k];
+        zrow[p] = A.out_row;
+      }
+      ok = ok && ab >= 0 && pr.batches[ab].members.size() == nm;
+      if (!ok) continue;
+      C.dx_act = P.dense[pr.batches[ab].members.front()].act_op;
+      for (std::uint32_t p = 0; p < nm; ++p)
+        C.tab[nm + p] = uint4{0, P.dense[C.members[p]].out_row, zrow[p], pr.dplan[C.members[p]].xrow0};
+      pr.batches[ab].skip_act = true;
+    }
+  }
+  // Dense layers over input leaves read the caller's inputs array ([col][batch],
+  // the rows' own SoA layout) instead of copies in V; a forward stage of input
+  // loads whose rows no other consumer reads is then skipped (cfg5: 784 rows,
+  // 3.3 GB copied per step at b = 1M).  TG_DIRECT_X=0 disables.
+  const char* dxx = std::getenv("TG_DIRECT_X");
+  if (!(dxx && dxx[0] == '0') && pr.umma && pr.tsz() == 4) {
+    std::vector<std::uint32_t> col_of(P.n_rows, tgc::kNone);
+    for (std::uint32_t c = 0; c < P.input_rows.size(); ++c)
+      if (P.input_rows[c] != tgc::kNone && P.input_rows[c] < P.n_rows) col_of[P.input_rows[c]] = c;
+    std::vector<char> other(P.n_rows, 0);   // read by something other than a direct-input GEMM
+    for (std::size_t i = 0; i < P.dense.size(); ++i) {
+      const tgc::Dense& D = P.dense[i];
+      auto& dp = pr.dplan[i];
+      if (!dp.gemm || !dp.x_inputs || col_of[dp.xrow0] == tgc::kNone) continue;
+      bool ok = true;
+      for (std::uint32_t k = 0; ok && k < D.n_in; ++k) ok = col_of[dp.xrow0 + k] == col_of[dp.xrow0] + k;
+      if (ok) dp.x_col0 = col_of[dp.xrow0];
+    }
+    for (const auto& B : pr.batches)   // batched launches offset rows of V: single-member layers only
+      if (B.members.size() > 1)
+        for (std::uint32_t u : B.members) pr.dplan[u].x_col0 = tgc::kNone;
+    auto mark = [&](std::uint32_t o) {
+      if ((P.opnd[o] >> tgc::kModeShift) == tgc::kSlot && (P.opnd[o] & tgc::kIndexMask) < P.n_rows)
+        other[P.opnd[o] & tgc::kIndexMask] = 1;
+    };
+    for (const auto& I : P.fwd) {
+      if (I.kind == tgc::kNode)
+        for (std::uint32_t k = 0; k < I.nops; ++k) mark(I.opnd + k);
+      else if (I.kind == tgc::kDense && pr.dplan[I.aux].x_col0 == tgc::kNone)
+        for (std::uint32_t k = 0; k < P.dense[I.aux].n_in; ++k) mark(P.dense[I.aux].x_opnd + k);
+    }
+    // batch terms reading V of a row outside the GEMM-covered weight gradients
+    for (std::uint32_t d = 0; d < P.dest_uv.size(); ++d)
+      if (!covered[d])
+        for (std::uint32_t q = P.term_off[d]; q < P.term_off[d + 1]; ++q)
+          if (P.terms[q].kind == 0 && P.terms[q].f < P.n_rows) other[P.terms[q].f] = 1;
+    // (a direct-input layer's weight gradient must itself be GEMM-covered)
+    for (std::size_t i = 0; i < P.dense.size(); ++i) {
+      const auto& dp = pr.dplan[i];
+      if (dp.x_col0 != tgc::kNone && dp.dw_dest0 == tgc::kNone)
+        for (std::uint32_t k = 0; k < P.dense[i].n_in; ++k) other[dp.xrow0 + k] = 1;
+    }
+    for (auto& stg : pr.sfwd) {
+      if (stg.batch != -1) continue;
+      bool only = stg.end > stg.begin;
+      for (std::uint32_t k = stg.begin; only && k < stg.end; ++k)
+        only = P.fwd[k].kind == tgc::kInputLoad && P.fwd[k].out < P.n_rows && !other[P.fwd[k].out];
+      stg.inputs_only = only;
+    }
+  }
   if (const char* v = std::getenv("TG_STAGED_VERBOSE"); v && v[0] == '1') {
     std::size_t ng = 0;
     for (std::size_t i = 0; i < P.dense.size(); ++i) {
@@ -674,7 +796,12 @@ void build_staged_plan(tg_program& pr) {
     };
     std::size_t nb = 0, nbm = 0;
     for (const auto& B : pr.batches) if (B.members.size() > 1) { ++nb; nbm += B.members.size(); }
-    std::fprintf(stderr, "[staged] %zu contended-row sums, %u temporary rows\n", pr.sums.size(), pr.n_tmp);
+    std::size_t nfx = 0, nio = 0;
+    for (const auto& B : pr.batches) nfx += B.dx_act != 0;
+    for (const auto& stg : pr.sfwd) nio += stg.inputs_only ? stg.end - stg.begin : 0;
+    std::fprintf(stderr, "[staged] %zu input loads replaced by direct GEMM reads of the inputs\n", nio);
+    std::fprintf(stderr, "[staged] %zu contended-row sums, %u temporary rows; %zu dX products fused with act backward\n",
+                 pr.sums.size(), pr.n_tmp, nfx);
     std::fprintf(stderr, "[staged] rows %u, dense %zu (%zu GEMM), %zu batches (%zu with %zu members); %zu generic dests, %zu scatter dests\n",
                  P.n_rows, P.dense.size(), ng, pr.batches.size(), nb, nbm, pr.gen_dests.size(), pr.sc_dests.size());
     stats("fwd", pr.sfwd, P.fwd);
@@ -1046,6 +1173,17 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
 
   // tensor-core roles (TG_UMMA_MASK bits: 1 forward, 2 input adjoints, 4 weight gradients)
   static const int umask = std::getenv("TG_UMMA_MASK") ? std::atoi(std::getenv("TG_UMMA_MASK")) : 7;
+  // dense layers over input leaves read inputs[col][s] in place (TMA: 16-byte rows)
+  const bool direct_x = (umask & 5) == 5 && batch % 4 == 0 && inputs &&
+                        (reinterpret_cast<std::uintptr_t>(inputs) & 15) == 0;
+  auto x_ptr = [&](const tg_program::DensePlan& dp, const T* Vb, std::size_t s0, std::size_t& ld) -> const T* {
+    if (direct_x && dp.x_col0 != tgc::kNone) {
+      ld = batch;
+      return static_cast<const T*>(inputs) + std::size_t(dp.x_col0) * batch + s0;
+    }
+    ld = cb;
+    return Vb + std::size_t(dp.xrow0) * cb;
+  };
   for (std::size_t s0 = 0; s0 < batch; s0 += cb) {
     const std::size_t n = std::min(cb, batch - s0);
     ra.s0 = s0;
@@ -1057,8 +1195,7 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
       g.A = UV + D.w_uv;
       g.lda = D.n_in;
       g.a_kmaj = true;
-      g.B = V + std::size_t(pr.dplan[u].xrow0) * cb;
-      g.ldb = cb;
+      g.B = x_ptr(pr.dplan[u], V, s0, g.ldb);
       g.b_nmaj = true;
       g.C = V + std::size_t(D.out_row) * cb;
       g.C2 = D.act_op ? V + std::size_t(D.act_row) * cb : nullptr;
@@ -1073,7 +1210,8 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
       return dense_gemm<T>(pr, g, 1, st);
     };
     // dX[n_in][n] (+)= W^T[n_in][n_out] . dZ[n_out][n] (one member)
-    auto dx_one = [&](std::uint32_t u, int beta) -> cudaError_t {
+    // (dact: C = the producing layer's z rows c_row, act' from its h rows = x rows)
+    auto dx_one = [&](std::uint32_t u, int beta, std::uint32_t dact, std::uint32_t c_row) -> cudaError_t {
       const tgc::Dense& D = P.dense[u];
       tgk::GemmArgs<T> g{};
       g.A = UV + D.w_uv;
@@ -1082,7 +1220,9 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
       g.B = G + std::size_t(D.out_row) * cb;
       g.ldb = cb;
       g.b_nmaj = true;
-      g.C = G + std::size_t(pr.dplan[u].xrow0) * cb;
+      g.C = G + std::size_t(dact ? c_row : pr.dplan[u].xrow0) * cb;
+      g.dact = dact;
+      g.C2 = dact ? V + std::size_t(pr.dplan[u].xrow0) * cb : nullptr;
       g.ldc = cb;
       g.M = D.n_in;
       g.N = static_cast<std::uint32_t>(n);
@@ -1100,8 +1240,7 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
       g.A = G + std::size_t(D.out_row) * cb;
       g.lda = cb;
       g.a_kmaj = true;
-      g.B = V + std::size_t(pr.dplan[u].xrow0) * cb;
-      g.ldb = cb;
+      g.B = x_ptr(pr.dplan[u], V, s0, g.ldb);
       g.b_nmaj = false;
       g.C = sk;
       g.M = D.n_out;
@@ -1116,6 +1255,7 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
     };
     // ---- forward stages ----
     for (const auto& stg : pr.sfwd) {
+      if (stg.batch < 0 && stg.inputs_only && direct_x) continue;   // rows read in place by their GEMMs
       if (stg.batch < 0) {
         ra.flags = tgk::kRFwd;
         ra.fwd_begin = stg.begin;
@@ -1177,7 +1317,7 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
       const std::uint32_t nm = static_cast<std::uint32_t>(B.members.size());
       const tgc::Dense& D = P.dense[B.members.front()];
       const auto& dp0 = pr.dplan[B.members.front()];
-      if (D.act_op) {
+      if (D.act_op && !B.skip_act) {
         TG_CUDA_TRY(tgk::launch_act_bwd_batched<T>(G, V, B.d_tab, nm, D.n_out, n, cb, D.act_op, st));
         ++pr.launches;
       }
@@ -1204,6 +1344,8 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
           g.N = static_cast<std::uint32_t>(n);
           g.K = D.n_out;
           g.beta = B.beta;
+          g.dact = B.dx_act;
+          g.C2 = B.dx_act ? V : nullptr;
           g.epi = tgk::kEpiAccum;
           g.mem = B.d_tab + nm;
           g.zs = 1;
@@ -1236,9 +1378,10 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
           dw_done = true;
         }
       }
-      for (std::uint32_t u : B.members) {
+      for (std::uint32_t p = 0; p < nm; ++p) {
+        const std::uint32_t u = B.members[p];
         // zeroed rows above follow the batch's beta; members that only assign keep their store
-        if (!dx_done) TG_CUDA_TRY(dx_one(u, B.beta ? pr.dplan[u].beta : 0));
+        if (!dx_done) TG_CUDA_TRY(dx_one(u, B.beta ? pr.dplan[u].beta : 0, B.dx_act, B.tab[nm + p].z));
         if (!dw_done && pr.dplan[u].dw_dest0 != tgc::kNone) TG_CUDA_TRY(dw_one(u));
       }
       if (dp0.db_dest0 != tgc::kNone) {

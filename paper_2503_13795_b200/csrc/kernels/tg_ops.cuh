@@ -209,6 +209,25 @@ __device__ __forceinline__ T act_bwd(std::uint32_t op, T g, T y, T z) {
   }
 }
 
+// Derivative of an activation from its output alone (dz = g * act'(z) with
+// act'(z) written in h = act(z)), for the activations whose derivative needs
+// no z: relu masks on h > 0 (z > 0 exactly when relu(z) > 0), tanh 1 - h^2,
+// exp h, sigmoid h (1 - h).  Used where a dense layer's input adjoint product
+// writes dz of the layer below directly (act_bwd_from_h_ok).
+__host__ __device__ __forceinline__ bool act_bwd_from_h_ok(std::uint32_t op) {
+  return op == Relu || op == Tanh || op == Exp || op == Sigmoid;
+}
+template <class T>
+__device__ __forceinline__ T act_bwd_h(std::uint32_t op, T g, T h) {
+  switch (op) {
+    case Relu: return h > T(0) ? g : T(0);
+    case Tanh: return g * (T(1) - h * h);
+    case Exp: return g * h;
+    case Sigmoid: return g * h * (T(1) - h);
+    default: return g;
+  }
+}
+
 // Accessor over the sample-invariant table (uniform forward / reverse sweeps).
 template <class T>
 struct UvAcc {

@@ -297,7 +297,8 @@ __global__ void __launch_bounds__(256) k_gemm(GemmArgs<T> g) {
         if (g.act) g.C2[std::size_t(m) * g.ldc + n] = act_fwd<T>(g.act, z);
       } else if (g.epi == kEpiAccum) {
         T* p = &g.C[std::size_t(m) * g.ldc + n];
-        *p = g.beta ? *p + acc[i][j] : acc[i][j];
+        if (g.dact) *p = act_bwd_h<T>(g.dact, acc[i][j], g.C2[std::size_t(m) * g.ldc + n]);
+        else *p = g.beta ? *p + acc[i][j] : acc[i][j];
       } else {
         g.C[(std::size_t(blockIdx.z) * g.M + m) * g.N + n] = acc[i][j];
       }

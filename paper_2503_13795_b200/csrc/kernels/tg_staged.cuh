@@ -83,6 +83,10 @@ struct GemmArgs {
   std::uint32_t zs;
   std::uint32_t a_span, b_span;
   bool no_pair;            // tcgen05 path: single-CTA tiles even when M > 128 (tg_gemm engine 2)
+  // kEpiAccum with dact != 0 (beta = 0): C = act'(H) * acc, the derivative
+  // taken from the activation output H at C2 (+ member row offset c2), i.e.
+  // the input adjoint product writes dz of the layer below directly
+  std::uint32_t dact;
 };
 
 // Table-scatter (kind-1) batch terms grouped by (adjoint row a, index column f).

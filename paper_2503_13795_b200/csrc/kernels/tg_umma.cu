@@ -186,7 +186,8 @@ __global__ void __launch_bounds__(128, 1) k_umma_tf32x3(GemmArgs<float> g) {
         if (g.act) g.C2[std::size_t(m) * g.ldc + n] = act_fwd<float>(g.act, z);
       } else if (g.epi == kEpiAccum) {
         float* p = &g.C[std::size_t(m) * g.ldc + n];
-        *p = g.beta ? *p + acc : acc;
+        if (g.dact) *p = act_bwd_h<float>(g.dact, acc, g.C2[std::size_t(m) * g.ldc + n]);
+        else *p = g.beta ? *p + acc : acc;
       } else {
         g.C[(std::size_t(blockIdx.z) * g.M + m) * g.N + n] = acc;
       }
@@ -500,6 +501,17 @@ __global__ void __launch_bounds__(kTThreads, 1) k_umma_tma(GemmArgs<float> g, co
           if (vec && cnt == 4) *reinterpret_cast<float4*>(d2) = make_float4(h4[0], h4[1], h4[2], h4[3]);
           else for (int e = 0; e < cnt; ++e) d2[e] = h4[e];
         }
+      } else if (g.epi == kEpiAccum && g.dact) {
+        const float* hp = g.C2 + (c2_off + m) * g.ldc + n;
+        float h4[4] = {0.f, 0.f, 0.f, 0.f};
+        if (vec && cnt == 4) {
+          const float4 o = *reinterpret_cast<const float4*>(hp);
+          h4[0] = o.x; h4[1] = o.y; h4[2] = o.z; h4[3] = o.w;
+        } else {
+          for (int e = 0; e < cnt; ++e) h4[e] = hp[e];
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) a4[e] = act_bwd_h<float>(g.dact, a4[e], h4[e]);
       } else if (g.epi == kEpiAccum && g.beta) {
         if (vec && cnt == 4) {
           const float4 o = *reinterpret_cast<const float4*>(dst);
@@ -797,6 +809,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
             if (vec && cnt == 4) *reinterpret_cast<float4*>(d2) = make_float4(h4[0], h4[1], h4[2], h4[3]);
             else for (int e = 0; e < cnt; ++e) d2[e] = h4[e];
           }
+        } else if (g.epi == kEpiAccum && g.dact) {
+          const float* hp = g.C2 + (c2_off + m) * g.ldc + n;
+          float h4[4] = {0.f, 0.f, 0.f, 0.f};
+          if (vec && cnt == 4) {
+            const float4 o = *reinterpret_cast<const float4*>(hp);
+            h4[0] = o.x; h4[1] = o.y; h4[2] = o.z; h4[3] = o.w;
+          } else {
+            for (int e = 0; e < cnt; ++e) h4[e] = hp[e];
+          }
+  #pragma unroll
+          for (int e = 0; e < 4; ++e) a4[e] = act_bwd_h<float>(g.dact, a4[e], h4[e]);
         } else if (g.epi == kEpiAccum && g.beta) {
           if (vec && cnt == 4) {
             const float4 o = *reinterpret_cast<const float4*>(dst);

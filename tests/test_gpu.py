@@ -154,6 +154,30 @@ def test_full_size_tensor_configs(name, dims, b):
     assert rel(G, r["grad_sum"]) <= 1e-5
 
 
+@pytest.mark.parametrize("fuse", ["1", "0"])
+@pytest.mark.parametrize("name,dims,b", [("wide_mlp", [40, 300, 260, 10], 512), ("wide_mlp", [40, 300, 260, 10], 130),
+                                         ("char_mlp", None, 1000), ("gpt", [13, 8, 32, 2, 2, 64], 12)])
+def test_staged_fusions_vs_oracle(fuse, name, dims, b, monkeypatch):
+    """Staged-tier fusions on and off (TG_DX_ACT: input-adjoint GEMMs write dz
+    of the layer below through act'(h) in their epilogue; TG_DIRECT_X: dense
+    layers over input leaves read the inputs array in place, b % 4 == 0 only;
+    b = 130 keeps the copies), with and without input gradients, vs the oracle."""
+    monkeypatch.setenv("TG_DX_ACT", fuse)
+    monkeypatch.setenv("TG_DIRECT_X", fuse)
+    monkeypatch.setenv("TG_STAGED", "1")
+    desc = tg.build_model(name, dims, "f32", seed=5).describe()
+    x, k = tg.synth_batch(name, dims, "f32", seed=23, batch=b, n_inputs=desc.n_inputs, n_index=desc.n_index_inputs)
+    prog = tg.Program(desc)
+    assert prog.info["storage"] == 3
+    r = oracle.run(desc, x.astype(np.float64), k, desc.param_values(), threads=os.cpu_count() or 8)
+    for igrad in (False, True):
+        L, IG, G = run(prog, desc, x, k, desc.param_values(), b, want_igrad=igrad)
+        assert close_rel(L, r["loss"], 1e-5, 1e-6)
+        assert rel(G, r["grad_sum"]) <= 1e-5
+        if igrad and desc.n_inputs:
+            assert rel(IG, r["input_grad"]) <= 1e-4
+
+
 def test_cfg1_full_size_closed_form():
     """cfg1 at b = 1e6: every sample against the closed form of Fig. 1
     (g = e^2/2, e = (a+b) - (ab+b^3); dg/da = e(1-b), dg/db = e(1-a-3b^2))."""
