@@ -164,8 +164,10 @@ typedef struct tg_program_info {
   uint32_t smem_bytes;       /* dynamic shared memory per CTA            */
   uint32_t storage;          /* 0 = shared-memory tile interpreter,
                                 1 = HBM SoA interpreter,
-                                2 = register-resident specialised kernel */
+                                2 = register-resident specialised kernel,
+                                3 = staged (HBM rows, dense layers as GEMMs) */
   tg_dtype dtype;
+  uint32_t n_attn_heads;     /* softmax attention heads fused from the scalar graph */
 } tg_program_info;
 
 /* Lowers the tape to the device program (replaces the per-sample DFS of

@@ -112,6 +112,8 @@ struct tg_program {
   tgc::GatherTable *d_ug = nullptr, *d_sg = nullptr;
   tgc::Term* d_terms = nullptr;
   tgc::Dense* d_dense = nullptr;
+  tgc::Attn* d_attn = nullptr;
+  std::uint32_t* d_arows = nullptr;
   void* d_consts = nullptr;
   unsigned long long* d_err_key = nullptr;
   double* d_err_val = nullptr;
@@ -191,6 +193,7 @@ struct tg_program {
   std::uint32_t *d_sc_use_off = nullptr, *d_sc_dests = nullptr;
   std::size_t chunk = 0;          // samples per chunk (0 = by batch)
   bool umma = true;               // fp32 dense layers on tcgen05 (3xTF32); TG_UMMA=0 -> SIMT GEMM
+  bool attn_fast = false;         // fused heads on the shared-memory kernels (tg_attn.cu; TG_ATTN_FAST=0: interpreter)
   ~tg_program() {
     tgj::release(jit);
     for (auto& e : ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
@@ -203,6 +206,7 @@ struct tg_program {
 namespace {
 
 constexpr int kSumStage = -2;
+constexpr int kAttnStage = -3;   // fused attention heads [begin, end) of one level
 constexpr std::size_t kSmemBudget = 200 * 1024;
 constexpr unsigned kMaxOcc = 32;
 
@@ -220,6 +224,23 @@ constexpr unsigned kMaxOcc = 32;
 // new order; rows reachable from a slot gather only ever accumulate and are
 // zeroed at the seed.  Both orders stay valid sequential orders, so the
 // interpreter (domain-error diagnosis) runs them unchanged.
+// Rows of a fused attention head: reads (q of every unit, k and v of every
+// key) and outputs (o of every unit).
+void attn_in_rows(const tgc::Program& P, std::uint32_t id, std::vector<std::uint32_t>& out) {
+  const tgc::Attn& A = P.attn[id];
+  for (std::uint32_t u = 0; u < A.n_units; ++u)
+    for (std::uint32_t i = 0; i < A.hd; ++i) out.push_back(P.arows[A.unit_off + 3 * u] + i);
+  for (std::uint32_t j = 0; j < A.n_keys; ++j) {
+    for (std::uint32_t i = 0; i < A.hd; ++i) out.push_back(P.arows[A.key_off + 2 * j] + i);
+    for (std::uint32_t i = 0; i < A.dv; ++i) out.push_back(P.arows[A.key_off + 2 * j + 1] + i);
+  }
+}
+void attn_out_rows(const tgc::Program& P, std::uint32_t id, std::vector<std::uint32_t>& out) {
+  const tgc::Attn& A = P.attn[id];
+  for (std::uint32_t u = 0; u < A.n_units; ++u)
+    for (std::uint32_t i = 0; i < A.dv; ++i) out.push_back(P.arows[A.unit_off + 3 * u + 1] + i);
+}
+
 void level_schedule(tg_program& pr, const std::vector<char>& gemm_dense) {
   tgc::Program& P = pr.P;
   const std::uint32_t R = P.n_rows;
@@ -241,10 +262,15 @@ void level_schedule(tg_program& pr, const std::vector<char>& gemm_dense) {
       const tgc::Dense& D = P.dense[in.aux];
       for (std::uint32_t j = 0; j < D.n_in; ++j) slot_rows(P.opnd[D.x_opnd + j], rows);
     }
+    if (in.kind == tgc::kAttn) attn_in_rows(P, in.aux, rows);
     std::uint32_t L = 0;
     for (std::uint32_t r : rows) L = std::max(L, row_level[r] + 1);
     lvl[k] = L;
-    if (in.kind == tgc::kDense) {
+    if (in.kind == tgc::kAttn) {
+      std::vector<std::uint32_t> orows;
+      attn_out_rows(P, in.aux, orows);
+      for (std::uint32_t r : orows) row_level[r] = L;
+    } else if (in.kind == tgc::kDense) {
       const tgc::Dense& D = P.dense[in.aux];
       for (std::uint32_t j = 0; j < D.n_out; ++j) {
         row_level[D.out_row + j] = L;
@@ -260,6 +286,7 @@ void level_schedule(tg_program& pr, const std::vector<char>& gemm_dense) {
   // within a level the interpreter instructions first, then the GEMM stages
   // grouped by weight block (adjacent layers over one weight form a batch)
   auto gkey = [&](const tgc::Instr& in) -> std::uint64_t {
+    if (in.kind == tgc::kAttn) return std::uint64_t(1) << 40;   // fused heads: their own stage, after the rest
     return is_gemm(in) ? 1 + std::uint64_t(P.dense[in.aux].w_uv) : 0;
   };
   std::stable_sort(ord.begin(), ord.end(), [&](std::uint32_t a, std::uint32_t b) {
@@ -282,7 +309,12 @@ void level_schedule(tg_program& pr, const std::vector<char>& gemm_dense) {
     const tgc::Instr& in = P.bwd[k];
     rows.clear();
     std::vector<std::uint32_t> uv_aux;
-    if (in.kind == tgc::kDense) {
+    if (in.kind == tgc::kAttn) {
+      attn_out_rows(P, in.aux, rows);
+      std::vector<std::uint32_t> xr;
+      attn_in_rows(P, in.aux, xr);
+      for (std::uint32_t r : xr) pushes[k].push_back({r, tgc::kNone, true});
+    } else if (in.kind == tgc::kDense) {
       const tgc::Dense& D = P.dense[in.aux];
       for (std::uint32_t j = 0; j < D.n_out; ++j) rows.push_back(D.act_op ? D.act_row + j : D.out_row + j);
       std::vector<std::uint32_t> xr;
@@ -377,6 +409,12 @@ void level_schedule(tg_program& pr, const std::vector<char>& gemm_dense) {
     std::unordered_map<std::uint32_t, std::vector<std::uint32_t>> uses;   // row -> operand positions
     for (std::size_t k = k0; k < k1; ++k) {
       const tgc::Instr& in = P.bwd[k];
+      if (in.kind == tgc::kAttn) {   // stores its q / k / v adjoints
+        std::vector<std::uint32_t> xr;
+        attn_in_rows(P, in.aux, xr);
+        for (std::uint32_t r : xr) seen[r] = 1;
+        continue;
+      }
       if (in.kind == tgc::kDense) {
         const tgc::Dense& D = P.dense[in.aux];
         for (std::uint32_t j = 0; j < D.n_in; ++j) flag(D.x_opnd + j);
@@ -440,6 +478,11 @@ void build_staged_plan(tg_program& pr) {
     if (std::uint64_t(D.n_out) * D.n_in >= 2048) big = true;
   }
   pr.staged = env ? env[0] == '1' : (big && !tgj::eligible(P));
+  {
+    const char* af = std::getenv("TG_ATTN_FAST");
+    pr.attn_fast = pr.tsz() == 4 && !P.attn.empty() && !(af && af[0] == '0');
+    for (const auto& A : P.attn) pr.attn_fast = pr.attn_fast && tgk::attn_fast_ok(A);
+  }
   if (const char* u = std::getenv("TG_UMMA")) pr.umma = u[0] != '0';
   if (!pr.staged || P.root_row == tgc::kNone) { pr.staged = false; return; }
   {
@@ -603,6 +646,13 @@ void build_staged_plan(tg_program& pr) {
           out.push_back({static_cast<int>(pr.batches.size() - 1), k, k + 1, false});
         }
         b = k + 1;
+      } else if (list[k].kind == tgc::kAttn) {
+        flush(k);
+        if (!out.empty() && out.back().batch == kAttnStage && out.back().end == k && (!lv || key[k] == key[k - 1]))
+          out.back().end = k + 1;
+        else
+          out.push_back({kAttnStage, k, k + 1, lv});
+        b = k + 1;
       } else if (lv && k > b && key[k] != key[k - 1]) {
         flush(k);
       }
@@ -663,6 +713,11 @@ void build_staged_plan(tg_program& pr) {
         for (std::uint32_t k = 0; k < I.nops; ++k) push_opnd(I.opnd + k);
       else if (I.kind == tgc::kDense)
         for (std::uint32_t k = 0; k < P.dense[I.aux].n_in; ++k) push_opnd(P.dense[I.aux].x_opnd + k);
+      else if (I.kind == tgc::kAttn) {
+        std::vector<std::uint32_t> xr;
+        attn_in_rows(P, I.aux, xr);
+        for (std::uint32_t r : xr) ++pushers[r];
+      }
     }
     std::vector<char> term_a(P.n_rows, 0);
     for (const auto& t : P.terms)
@@ -740,6 +795,11 @@ void build_staged_plan(tg_program& pr) {
         for (std::uint32_t k = 0; k < I.nops; ++k) mark(I.opnd + k);
       else if (I.kind == tgc::kDense && pr.dplan[I.aux].x_col0 == tgc::kNone)
         for (std::uint32_t k = 0; k < P.dense[I.aux].n_in; ++k) mark(P.dense[I.aux].x_opnd + k);
+      else if (I.kind == tgc::kAttn) {
+        std::vector<std::uint32_t> xr;
+        attn_in_rows(P, I.aux, xr);
+        for (std::uint32_t r : xr) other[r] = 1;
+      }
     }
     // batch terms reading V of a row outside the GEMM-covered weight gradients
     for (std::uint32_t d = 0; d < P.dest_uv.size(); ++d)
@@ -806,6 +866,29 @@ void build_staged_plan(tg_program& pr) {
                  P.n_rows, P.dense.size(), ng, pr.batches.size(), nb, nbm, pr.gen_dests.size(), pr.sc_dests.size());
     stats("fwd", pr.sfwd, P.fwd);
     stats("bwd", pr.sbwd, P.bwd);
+    if (v[1] == '2')
+      for (int w = 0; w < 2; ++w) {
+        const auto& st = w ? pr.sbwd : pr.sfwd;
+        const auto& list = w ? P.bwd : P.fwd;
+        const auto& key = w ? P.bwd_level : P.fwd_level;
+        for (const auto& sg : st) {
+          std::map<int, std::size_t> ops;
+          for (std::uint32_t k = sg.begin; k < sg.end && sg.batch != kSumStage; ++k)
+            ops[list[k].kind == tgc::kNode ? list[k].op : 1000 + list[k].kind]++;
+          std::fprintf(stderr, "[staged] %s stage batch %d [%u,%u) key %u:%u members %zu ops", w ? "bwd" : "fwd", sg.batch,
+                       sg.begin, sg.end, sg.batch == kSumStage ? 0u : key[sg.begin] >> 12,
+                       sg.batch == kSumStage ? 0u : key[sg.begin] & 4095u,
+                       sg.batch >= 0 ? pr.batches[sg.batch].members.size() : std::size_t(0));
+          for (const auto& [op, c] : ops) std::fprintf(stderr, " %d:%zu", op, c);
+          if (sg.batch >= 0) {
+            const auto u = pr.batches[sg.batch].members.front();
+            std::fprintf(stderr, " | %ux%u w%u act%u dw%u db%u dxact%u skip%d", P.dense[u].n_out, P.dense[u].n_in,
+                         P.dense[u].w_uv, P.dense[u].act_op, pr.dplan[u].dw_dest0, pr.dplan[u].db_dest0,
+                         pr.batches[sg.batch].dx_act, int(pr.batches[sg.batch].skip_act));
+          }
+          std::fprintf(stderr, "\n");
+        }
+      }
   }
 }
 
@@ -981,6 +1064,8 @@ tg_status upload(tg_program& pr) {
   TG_TRY(upload_vec(pr, P.terms, &pr.d_terms));
   TG_TRY(upload_vec(pr, P.dest_uv, &pr.d_destuv));
   TG_TRY(upload_vec(pr, P.dense, &pr.d_dense));
+  TG_TRY(upload_vec(pr, P.attn, &pr.d_attn));
+  TG_TRY(upload_vec(pr, P.arows, &pr.d_arows));
   const std::uint32_t nc = P.n_uv - P.uv_const_base;
   if (P.dtype == TG_F64) {
     std::vector<double> c(P.uv_init.begin() + P.uv_const_base, P.uv_init.end());
@@ -1104,6 +1189,8 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
   ra.sg = pr.d_sg;
   ra.cand = pr.d_cand;
   ra.dense = pr.d_dense;
+  ra.attn = pr.d_attn;
+  ra.arows = pr.d_arows;
   ra.UV = UV;
   ra.inputs = static_cast<const T*>(inputs);
   ra.idx = idx;
@@ -1135,6 +1222,8 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
     ma.term_off = pr.d_termoff;
     ma.terms = pr.d_terms;
     ma.dense = pr.d_dense;
+    ma.attn = pr.d_attn;
+    ma.arows = pr.d_arows;
     ma.UV = UV;
     ma.inputs = static_cast<const T*>(inputs);
     ma.idx = idx;
@@ -1254,7 +1343,22 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
       return e;
     };
     // ---- forward stages ----
+    // fused attention heads: the shared-memory kernels (fp32, small heads) or,
+    // otherwise, one interpreter CTA row per head (attn_*_sample)
+    auto attn_stage = [&](const tg_program::Stage& stg, bool fwd) -> cudaError_t {
+      ++pr.launches;
+      if constexpr (std::is_same_v<T, float>) {
+        if (pr.attn_fast)
+          return tgk::launch_attn(fwd, fwd ? pr.d_fwd : pr.d_bwd, stg.begin, stg.end - stg.begin, pr.d_attn, pr.d_arows,
+                                  V, G, n, cb, st);
+      }
+      ra.flags = fwd ? tgk::kRFwd : tgk::kRBwd;
+      (fwd ? ra.fwd_begin : ra.bwd_begin) = stg.begin;
+      (fwd ? ra.fwd_end : ra.bwd_end) = stg.end;
+      return tgk::launch_level_range<T>(ra, st);
+    };
     for (const auto& stg : pr.sfwd) {
+      if (stg.batch == kAttnStage) { TG_CUDA_TRY(attn_stage(stg, true)); continue; }
       if (stg.batch < 0 && stg.inputs_only && direct_x) continue;   // rows read in place by their GEMMs
       if (stg.batch < 0) {
         ra.flags = tgk::kRFwd;
@@ -1300,6 +1404,7 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
     ++pr.launches;
     // ---- reverse stages ----
     for (const auto& stg : pr.sbwd) {
+      if (stg.batch == kAttnStage) { TG_CUDA_TRY(attn_stage(stg, false)); continue; }
       if (stg.batch == kSumStage) {
         TG_CUDA_TRY(tgk::launch_row_sums<T>(pr.d_sums + stg.begin, stg.end - stg.begin, G, n, cb, st));
         ++pr.launches;
@@ -1519,6 +1624,8 @@ tg_status run_fused(tg_program& pr, const void* inputs, const std::int32_t* idx,
   ma.term_off = pr.d_termoff;
   ma.terms = pr.d_terms;
   ma.dense = pr.d_dense;
+  ma.attn = pr.d_attn;
+  ma.arows = pr.d_arows;
   ma.UV = UV;
   ma.inputs = static_cast<const T*>(inputs);
   ma.idx = idx;
@@ -1608,6 +1715,8 @@ tg_status run_fb(tg_program& pr, const void* inputs, const std::int32_t* idx, st
     ma.term_off = pr.d_termoff;
     ma.terms = pr.d_terms;
     ma.dense = pr.d_dense;
+    ma.attn = pr.d_attn;
+    ma.arows = pr.d_arows;
     ma.UV = UV;
     ma.inputs = static_cast<const T*>(inputs);
     ma.idx = idx;
@@ -1901,6 +2010,7 @@ tg_status tg_program_info_get(tg_program_t p, tg_program_info* info) {
     i.smem_bytes = static_cast<uint32_t>(p->smem_bytes);
     i.storage = p->staged ? 3 : (p->jit.ok ? 2 : (p->smem ? 0 : 1));
     i.dtype = P.dtype;
+    i.n_attn_heads = static_cast<uint32_t>(P.attn.size());
     *info = i;
     return TG_OK;
   });

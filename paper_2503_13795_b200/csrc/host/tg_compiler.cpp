@@ -13,6 +13,9 @@
 //     y_k is g * x_k (ops.hpp:436-452), so its batch sum is sum_s g(s) x_k(s),
 //     a contraction over the sample axis evaluated per CTA tile.
 #include <algorithm>
+#include <map>
+#include <queue>
+#include <tuple>
 #include <stdexcept>
 #include <string>
 #include <unordered_map>
@@ -24,6 +27,7 @@ namespace {
 
 enum Cls : std::uint8_t { cParam, cInput, cConst, cUniform, cSample };
 
+constexpr std::uint8_t ExpOp = 3, DivOp = 16;
 constexpr std::uint8_t Leaf = 0, MulByConst = 15, Add = 12, Sub = 13, Mul = 14, Mean = 17,
                        NegativeMean = 20, AddVarying = 21, SubVarying = 22, MeanVarying = 24,
                        NegativeMeanVarying = 27, IPNoBias = 28, IPWithBias = 29,
@@ -181,6 +185,173 @@ std::vector<std::uint32_t> processing_order(const Ctx& c) {
   return post;  // processing order (children after parents)
 }
 
+// ---- softmax attention heads in the recorded graph (kAttn) -------------------
+// One query unit of a head is the node pattern the reference ops produce for
+// softmax(scale * q K^T) V:
+//   s_j = innerProduct(q, k_j)      c_j = mulByConstant(s_j, scale)
+//   m   = stopGradMax(c_0..c_{n-1}) sh_j = c_j - m      e_j = exp(sh_j)
+//   Z   = reduceSum(e_0..e_{n-1})   a_j = e_j / Z
+//   o_i = innerProduct(a_0..a_{n-1}, v_0[i]..v_{n-1}[i])
+// with q, k_j, v_j blocks of consecutive nodes.  Matching is structural and
+// exact (op, children in order, consumer counts), so a fused head computes
+// the same function; anything that does not match stays scalar.
+struct AttnUnit {
+  std::uint32_t q0 = 0, n = 0;
+  std::vector<std::uint32_t> kb, vb, o, interior;
+};
+struct AttnGroup {
+  std::uint32_t hd = 0, dv = 0;
+  double scale = 0;
+  std::vector<AttnUnit> units;
+  std::vector<std::uint32_t> kb, vb;   // longest key list
+  std::uint32_t last_o = 0, first_node = 0;
+  bool ok = true;
+};
+
+std::vector<AttnGroup> find_attention(const Ctx& c, const std::vector<std::uint32_t>& order) {
+  const tg_tape_desc& d = c.d;
+  const std::uint32_t N = d.n_nodes;
+  std::vector<AttnGroup> groups;
+  if (!d.constant) return groups;
+  std::vector<std::uint8_t> pinned(N, 0), reach(N, 0);
+  pinned[d.root] = 1;
+  for (std::uint32_t g = 0; g < d.n_gathers; ++g)
+    for (std::uint32_t r = 0; r < d.gathers[g].n_rows; ++r) pinned[c.cand(g, r)] = 1;
+  for (std::uint32_t nd : order) reach[nd] = 1;
+  std::vector<std::uint32_t> ccount(N, 0), cfirst(N, kNone), cmin(N, kNone);
+  std::vector<std::uint32_t> coff(N + 1, 0), cons;
+  for (std::uint32_t i = 0; i < N; ++i)
+    for (std::uint32_t j = 0; j < c.nkids(i); ++j) {
+      const std::uint32_t k = c.kids(i)[j];
+      if (k & TG_GATHER_FLAG) continue;
+      ++ccount[k];
+      ++coff[k + 1];
+      cmin[k] = std::min(cmin[k], i);
+    }
+  for (std::uint32_t i = 0; i < N; ++i) coff[i + 1] += coff[i];
+  cons.resize(coff[N]);
+  {
+    std::vector<std::uint32_t> fill(coff.begin(), coff.end() - 1);
+    for (std::uint32_t i = 0; i < N; ++i)
+      for (std::uint32_t j = 0; j < c.nkids(i); ++j) {
+        const std::uint32_t k = c.kids(i)[j];
+        if (!(k & TG_GATHER_FLAG)) cons[fill[k]++] = i;
+      }
+  }
+  auto plain = [&](std::uint32_t x) { return !(x & TG_GATHER_FLAG) && x < N; };
+  auto free_node = [&](std::uint32_t x) { return plain(x) && c.cls[x] == cSample && !pinned[x] && reach[x]; };
+  std::map<std::tuple<std::uint32_t, std::uint32_t, std::uint32_t, std::uint32_t, double>, std::uint32_t> gid;
+  for (std::uint32_t Z = 0; Z < N; ++Z) {
+    if (d.op[Z] != AddVarying || !free_node(Z)) continue;
+    const std::uint32_t n = c.nkids(Z);
+    const std::uint32_t* e = c.kids(Z);
+    AttnUnit U;
+    U.n = n;
+    bool ok = n >= 1 && ccount[Z] == n;
+    std::uint32_t m = kNone, hd = 0;
+    double scale = 0;
+    std::vector<std::uint32_t> cj(n), aj(n);
+    for (std::uint32_t j = 0; ok && j < n; ++j) {
+      const std::uint32_t ej = e[j];
+      ok = free_node(ej) && d.op[ej] == ExpOp && c.nkids(ej) == 1 && ccount[ej] == 2;
+      if (!ok) break;
+      const std::uint32_t sh = c.kids(ej)[0];
+      ok = free_node(sh) && d.op[sh] == Sub && ccount[sh] == 1;
+      if (!ok) break;
+      const std::uint32_t cc = c.kids(sh)[0], mm = c.kids(sh)[1];
+      if (j == 0) m = mm;
+      ok = free_node(cc) && plain(mm) && mm == m && d.op[cc] == MulByConst && ccount[cc] == 2;
+      if (!ok) break;
+      if (j == 0) scale = d.constant[cc];
+      ok = d.constant[cc] == scale;
+      const std::uint32_t sj = c.kids(cc)[0];
+      ok = ok && free_node(sj) && d.op[sj] == IPNoBias && ccount[sj] == 1 && c.nkids(sj) >= 2 && c.nkids(sj) % 2 == 0;
+      if (!ok) break;
+      const std::uint32_t h = c.nkids(sj) / 2;
+      if (j == 0) { hd = h; U.q0 = c.kids(sj)[0]; }
+      ok = h == hd;
+      const std::uint32_t* sk = c.kids(sj);
+      for (std::uint32_t i = 0; ok && i < hd; ++i)
+        ok = plain(sk[i]) && plain(sk[hd + i]) && sk[i] == U.q0 + i && sk[hd + i] == sk[hd] + i;
+      if (!ok) break;
+      U.kb.push_back(sk[hd]);
+      cj[j] = cc;
+      // a_j: the consumer of e_j other than Z, a_j = e_j / Z
+      std::uint32_t a = kNone;
+      for (std::uint32_t q = coff[ej]; q < coff[ej + 1]; ++q)
+        if (cons[q] != Z) a = cons[q];
+      ok = a != kNone && free_node(a) && d.op[a] == DivOp && c.kids(a)[0] == ej && c.kids(a)[1] == Z;
+      aj[j] = a;
+      U.interior.insert(U.interior.end(), {ej, sh, cc, sj});
+    }
+    // (the shift has no reverse children, so it is absent from the processing order)
+    ok = ok && m != kNone && plain(m) && c.cls[m] == cSample && !pinned[m] && d.op[m] == StopGradMax && c.nkids(m) == n && ccount[m] == n;
+    for (std::uint32_t j = 0; ok && j < n; ++j) ok = c.kids(m)[j] == cj[j];
+    if (!ok) continue;
+    // outputs: the consumers of a_0, each o_i = innerProduct(a_0..a_{n-1}, v_0[i]..v_{n-1}[i])
+    for (std::uint32_t q = coff[aj[0]]; q < coff[aj[0] + 1]; ++q) U.o.push_back(cons[q]);
+    std::sort(U.o.begin(), U.o.end());
+    const std::uint32_t dv = static_cast<std::uint32_t>(U.o.size());
+    ok = dv >= 1;
+    for (std::uint32_t j = 0; ok && j < n; ++j) ok = ccount[aj[j]] == dv;
+    for (std::uint32_t i = 0; ok && i < dv; ++i) {
+      const std::uint32_t o = U.o[i];
+      ok = plain(o) && c.cls[o] == cSample && reach[o] && d.op[o] == IPNoBias && c.nkids(o) == 2 * n;
+      for (std::uint32_t j = 0; ok && j < n; ++j) ok = c.kids(o)[j] == aj[j] && plain(c.kids(o)[n + j]);
+      if (ok && i > 0) ok = U.o[i] == U.o[0] + i;
+    }
+    for (std::uint32_t j = 0; ok && j < n; ++j) {
+      const std::uint32_t v0 = c.kids(U.o[0])[n + j];
+      U.vb.push_back(v0);
+      for (std::uint32_t i = 1; ok && i < dv; ++i) ok = c.kids(U.o[i])[n + j] == v0 + i;
+    }
+    if (!ok) continue;
+    U.interior.push_back(m);
+    U.interior.push_back(Z);
+    U.interior.insert(U.interior.end(), aj.begin(), aj.end());
+    const auto key = std::make_tuple(U.kb[0], U.vb[0], hd, dv, scale);
+    auto it = gid.find(key);
+    if (it == gid.end()) {
+      it = gid.emplace(key, static_cast<std::uint32_t>(groups.size())).first;
+      groups.emplace_back();
+      groups.back().hd = hd;
+      groups.back().dv = dv;
+      groups.back().scale = scale;
+    }
+    groups[it->second].units.push_back(std::move(U));
+  }
+  // group checks: prefix key lists, disjoint q / k / v / o blocks whose every
+  // consumer is inside the group, outputs consumed only after the last one
+  for (AttnGroup& G : groups) {
+    for (const AttnUnit& U : G.units)
+      if (U.kb.size() > G.kb.size()) { G.kb = U.kb; G.vb = U.vb; }
+    const std::uint32_t T = static_cast<std::uint32_t>(G.kb.size());
+    std::vector<std::uint32_t> users(T, 0);
+    std::unordered_map<std::uint32_t, std::uint32_t> owner;   // node -> role
+    auto claim = [&](std::uint32_t x, std::uint32_t role) {
+      if (!plain(x) || pinned[x] || (c.cls[x] != cSample && c.cls[x] != cInput) || owner.count(x)) return false;
+      owner[x] = role;
+      return true;
+    };
+    G.first_node = kNone;
+    for (const AttnUnit& U : G.units) {
+      for (std::uint32_t j = 0; G.ok && j < U.n; ++j) G.ok = U.kb[j] == G.kb[j] && U.vb[j] == G.vb[j];
+      for (std::uint32_t j = 0; j < U.n && j < T; ++j) ++users[j];
+      for (std::uint32_t i = 0; G.ok && i < G.hd; ++i) G.ok = claim(U.q0 + i, 0) && ccount[U.q0 + i] == U.n;
+      for (std::uint32_t x : U.o) G.last_o = std::max(G.last_o, x);
+      for (std::uint32_t x : U.interior) G.first_node = std::min(G.first_node, x);
+    }
+    for (std::uint32_t j = 0; G.ok && j < T; ++j) {
+      for (std::uint32_t i = 0; G.ok && i < G.hd; ++i) G.ok = claim(G.kb[j] + i, 1) && ccount[G.kb[j] + i] == users[j];
+      for (std::uint32_t i = 0; G.ok && i < G.dv; ++i) G.ok = claim(G.vb[j] + i, 2) && ccount[G.vb[j] + i] == users[j];
+    }
+    for (const AttnUnit& U : G.units)
+      for (std::uint32_t x : U.o) G.ok = G.ok && (cmin[x] == kNone || cmin[x] > G.last_o) && !owner.count(x);
+  }
+  groups.erase(std::remove_if(groups.begin(), groups.end(), [](const AttnGroup& G) { return !G.ok; }), groups.end());
+  return groups;
+}
+
 }  // namespace
 
 Program compile(const tg_tape_desc& d) {
@@ -215,6 +386,16 @@ Program compile(const tg_tape_desc& d) {
     }
   }
   P.n_uniform_nodes = nu;
+
+  // ---- softmax attention heads (kAttn): interior nodes get no rows ------------
+  std::vector<AttnGroup> agroups = find_attention(c, processing_order(c));
+  std::vector<std::int32_t> attn_of(d.n_nodes, -1);      // interior and output nodes -> group
+  std::vector<std::uint8_t> attn_interior(d.n_nodes, 0);
+  for (std::size_t g = 0; g < agroups.size(); ++g)
+    for (const AttnUnit& U : agroups[g].units) {
+      for (std::uint32_t x : U.interior) { attn_of[x] = static_cast<std::int32_t>(g); attn_interior[x] = 1; }
+      for (std::uint32_t x : U.o) attn_of[x] = static_cast<std::int32_t>(g);
+    }
 
   // ---- per-sample rows -------------------------------------------------------
   c.row.assign(d.n_nodes, kNone);
@@ -288,7 +469,7 @@ Program compile(const tg_tape_desc& d) {
     }
   }
   for (std::uint32_t i = 0; i < d.n_nodes; ++i) {
-    if (c.cls[i] != cSample || c.row[i] != kNone) continue;
+    if (c.cls[i] != cSample || c.row[i] != kNone || attn_interior[i]) continue;
     if (blk_of[i] != kNone) {
       for (std::uint32_t x : blocks[blk_of[i]]) { c.row[x] = nrow++; ++P.n_sample_nodes; }
     } else {
@@ -296,6 +477,49 @@ Program compile(const tg_tape_desc& d) {
       ++P.n_sample_nodes;
     }
   }
+  // attention blocks must be consecutive rows; a head whose blocks are not
+  // falls back to scalar nodes (its interior rows appended here)
+  for (std::size_t g = 0; g < agroups.size(); ++g) {
+    AttnGroup& G = agroups[g];
+    auto consec = [&](std::uint32_t x0, std::uint32_t n) {
+      for (std::uint32_t i = 0; i < n; ++i)
+        if (c.row[x0 + i] == kNone || c.row[x0 + i] != c.row[x0] + i) return false;
+      return true;
+    };
+    bool ok = true;
+    for (const AttnUnit& U : G.units) ok = ok && consec(U.q0, G.hd) && consec(U.o[0], G.dv);
+    for (std::size_t j = 0; ok && j < G.kb.size(); ++j) ok = consec(G.kb[j], G.hd) && consec(G.vb[j], G.dv);
+    if (ok) {
+      for (const AttnUnit& U : G.units) P.n_sample_nodes += static_cast<std::uint32_t>(U.interior.size());
+      continue;
+    }
+    G.ok = false;
+    for (const AttnUnit& U : G.units) {
+      for (std::uint32_t x : U.interior) { attn_of[x] = -1; attn_interior[x] = 0; c.row[x] = nrow++; ++P.n_sample_nodes; }
+      for (std::uint32_t x : U.o) attn_of[x] = -1;
+    }
+  }
+  std::vector<std::uint32_t> attn_id(agroups.size(), kNone);
+  for (std::size_t g = 0; g < agroups.size(); ++g) {
+    const AttnGroup& G = agroups[g];
+    if (!G.ok) continue;
+    Attn A{};
+    A.n_units = static_cast<std::uint32_t>(G.units.size());
+    A.n_keys = static_cast<std::uint32_t>(G.kb.size());
+    A.hd = G.hd;
+    A.dv = G.dv;
+    A.unit_off = static_cast<std::uint32_t>(P.arows.size());
+    for (const AttnUnit& U : G.units) P.arows.insert(P.arows.end(), {c.row[U.q0], c.row[U.o[0]], U.n});
+    A.key_off = static_cast<std::uint32_t>(P.arows.size());
+    for (std::size_t j = 0; j < G.kb.size(); ++j) P.arows.insert(P.arows.end(), {c.row[G.kb[j]], c.row[G.vb[j]]});
+    A.first_node = G.first_node;
+    A.n_nodes = 0;
+    for (const AttnUnit& U : G.units) A.n_nodes += static_cast<std::uint32_t>(U.interior.size() + U.o.size());
+    A.scale = G.scale;
+    attn_id[g] = static_cast<std::uint32_t>(P.attn.size());
+    P.attn.push_back(A);
+  }
+
   // slot-gather candidate tables (rows are known now)
   for (std::uint32_t g = 0; g < d.n_gathers; ++g) {
     if (c.gkind[g] != 2) continue;
@@ -320,6 +544,14 @@ Program compile(const tg_tape_desc& d) {
   std::vector<std::uint32_t> uinstr_of(d.n_nodes, kNone);  // uniform node -> ufwd index
   for (std::uint32_t i = 0; i < d.n_nodes; ++i) {
     if (c.cls[i] != cSample && c.cls[i] != cUniform) continue;
+    if (attn_of[i] >= 0) {   // fused head: one instruction where its last output node stood
+      const AttnGroup& G = agroups[attn_of[i]];
+      if (i == G.last_o) {
+        const Attn& A = P.attn[attn_id[attn_of[i]]];
+        P.fwd.push_back(Instr{kAttn, 0, 0, P.arows[A.unit_off + 1], 0, 0, attn_id[attn_of[i]], A.first_node, 0.0});
+      }
+      continue;
+    }
     Instr in{};
     in.kind = kNode;
     in.op = d.op[i];
@@ -369,8 +601,17 @@ Program compile(const tg_tape_desc& d) {
       }
     }
     if (c.cls[d.root] == cSample) uses[c.row[d.root]] += 2;
+    for (const Attn& A : P.attn) {   // rows read by fused heads
+      for (std::uint32_t u = 0; u < A.n_units; ++u)
+        for (std::uint32_t i = 0; i < A.hd; ++i) uses[P.arows[A.unit_off + 3 * u] + i] += 2;
+      for (std::uint32_t j = 0; j < A.n_keys; ++j) {
+        for (std::uint32_t i = 0; i < A.hd; ++i) uses[P.arows[A.key_off + 2 * j] + i] += 2;
+        for (std::uint32_t i = 0; i < A.dv; ++i) uses[P.arows[A.key_off + 2 * j + 1] + i] += 2;
+      }
+    }
     auto ip_shape = [&](std::uint32_t node, std::uint32_t& xo, std::uint32_t& m, std::uint32_t& w, std::uint32_t& b) -> bool {
-      if (node >= d.n_nodes || c.cls[node] != cSample || !reach[node] || (d.op[node] != IPNoBias && d.op[node] != IPWithBias))
+      if (node >= d.n_nodes || c.cls[node] != cSample || !reach[node] || (d.op[node] != IPNoBias && d.op[node] != IPWithBias) ||
+          attn_of[node] >= 0)
         return false;
       const Instr& in = nodefwd[instr_of[node]];
       const bool bias = d.op[node] == IPWithBias;
@@ -461,9 +702,29 @@ Program compile(const tg_tape_desc& d) {
   std::vector<PendingTerm> pend;
   auto new_aux_row = [&]() { const std::uint32_t r = nrow++; written.push_back(0); needs_zero.push_back(0); return r; };
 
+  // fused heads: the reverse instruction runs where the head's last node in
+  // processing order stood (every output adjoint is final there; the q / k / v
+  // producers, children of head nodes, all come later); it is the only pusher
+  // into its q / k / v rows and stores them
+  std::vector<std::uint32_t> attn_left(agroups.size(), 0);
+  for (std::uint32_t node : P.order)
+    if (attn_of[node] >= 0) ++attn_left[attn_of[node]];
   for (std::uint32_t node : P.order) {
     if (c.cls[node] == cUniform) { P.ubwd.push_back(P.ufwd[uinstr_of[node]]); continue; }
     if (c.cls[node] != cSample) continue;
+    if (attn_of[node] >= 0) {
+      if (--attn_left[attn_of[node]] > 0) continue;
+      const std::uint32_t id = attn_id[attn_of[node]];
+      const Attn& A = P.attn[id];
+      P.bwd.push_back(Instr{kAttn, 0, 0, P.arows[A.unit_off + 1], 0, 0, id, A.first_node, 0.0});
+      for (std::uint32_t u = 0; u < A.n_units; ++u)
+        for (std::uint32_t i = 0; i < A.hd; ++i) written[P.arows[A.unit_off + 3 * u] + i] = 1;
+      for (std::uint32_t j = 0; j < A.n_keys; ++j) {
+        for (std::uint32_t i = 0; i < A.hd; ++i) written[P.arows[A.key_off + 2 * j] + i] = 1;
+        for (std::uint32_t i = 0; i < A.dv; ++i) written[P.arows[A.key_off + 2 * j + 1] + i] = 1;
+      }
+      continue;
+    }
     if (dense_of[node] >= 0) {
       // the fused group runs where its last member would: every member's
       // adjoint is final there (parents precede children in this order)
@@ -550,6 +811,112 @@ Program compile(const tg_tape_desc& d) {
       const std::uint32_t u = c.uv[c.cand(g, r)];
       if (u >= P.uv_const_base) continue;
       pend.push_back({u, Term{c.grow[g], d.gathers[g].index_col, static_cast<std::int32_t>(r), 1, 1.0}});
+    }
+  }
+  // With fused heads the reference processing order is not always a valid
+  // order of the reverse instructions: a head's reverse runs once every output
+  // adjoint is final, but the processing order may reach a q / k / v producer
+  // (e.g. position 0's projection) before the last head node.  Re-sort the
+  // reverse list topologically over "pushes into a row -> reads that row's
+  // adjoint", keeping the original order wherever it is valid (Kahn's
+  // algorithm, smallest original index first), then recompute the first-write
+  // (assign) flags and the rows that must start at zero for the new order.
+  if (!P.attn.empty()) {
+    const std::size_t NB = P.bwd.size();
+    std::vector<std::uint32_t> reader(nrow, kNone);   // reverse instruction reading each row's adjoint
+    std::vector<std::vector<std::uint32_t>> pushes(NB);
+    std::vector<std::uint32_t> rows;
+    for (std::uint32_t k = 0; k < NB; ++k) {
+      const Instr& in = P.bwd[k];
+      rows.clear();
+      if (in.kind == kAttn) {
+        const Attn& A = P.attn[in.aux];
+        for (std::uint32_t u = 0; u < A.n_units; ++u) {
+          for (std::uint32_t i = 0; i < A.dv; ++i) reader[P.arows[A.unit_off + 3 * u + 1] + i] = k;
+          for (std::uint32_t i = 0; i < A.hd; ++i) rows.push_back(P.arows[A.unit_off + 3 * u] + i);
+        }
+        for (std::uint32_t j = 0; j < A.n_keys; ++j) {
+          for (std::uint32_t i = 0; i < A.hd; ++i) rows.push_back(P.arows[A.key_off + 2 * j] + i);
+          for (std::uint32_t i = 0; i < A.dv; ++i) rows.push_back(P.arows[A.key_off + 2 * j + 1] + i);
+        }
+      } else if (in.kind == kDense) {
+        const Dense& D = P.dense[in.aux];
+        for (std::uint32_t j = 0; j < D.n_out; ++j) {
+          reader[D.out_row + j] = k;
+          if (D.act_op) reader[D.act_row + j] = k;
+        }
+        for (std::uint32_t q = 0; q < D.n_in; ++q) rows.push_back(P.opnd[D.x_opnd + q] & kIndexMask);
+      } else {
+        reader[in.out] = k;
+        for (std::uint32_t j = 0; j < in.nops; ++j) {
+          const std::uint32_t o = P.opnd[in.opnd + j], mode = o >> kModeShift, idx = o & kIndexMask;
+          if (mode == kSlot) rows.push_back(idx);
+          else if (mode == kSGather) {
+            const GatherTable& T = P.sgather[idx];
+            for (std::uint32_t r = 0; r < T.n_rows; ++r) rows.push_back(P.cand[T.cand_off + r]);
+          }
+        }
+      }
+      pushes[k] = rows;
+    }
+    std::vector<std::uint32_t> indeg(NB, 0);
+    std::vector<std::vector<std::uint32_t>> succ(NB);
+    for (std::uint32_t k = 0; k < NB; ++k) {
+      std::sort(pushes[k].begin(), pushes[k].end());
+      pushes[k].erase(std::unique(pushes[k].begin(), pushes[k].end()), pushes[k].end());
+      for (std::uint32_t r : pushes[k])
+        if (reader[r] != kNone && reader[r] != k) { succ[k].push_back(reader[r]); ++indeg[reader[r]]; }
+    }
+    std::priority_queue<std::uint32_t, std::vector<std::uint32_t>, std::greater<std::uint32_t>> ready;
+    for (std::uint32_t k = 0; k < NB; ++k) if (!indeg[k]) ready.push(k);
+    std::vector<Instr> nb;
+    nb.reserve(NB);
+    while (!ready.empty()) {
+      const std::uint32_t k = ready.top();
+      ready.pop();
+      nb.push_back(P.bwd[k]);
+      for (std::uint32_t t : succ[k]) if (--indeg[t] == 0) ready.push(t);
+    }
+    if (nb.size() != NB) throw std::runtime_error("tg_compile: cyclic reverse order around a fused attention head");
+    P.bwd.swap(nb);
+    // first-write flags and zero-start rows for the new order
+    std::fill(written.begin(), written.end(), 0);
+    std::fill(needs_zero.begin(), needs_zero.end(), 0);
+    if (P.root_row != kNone) written[P.root_row] = 1;
+    for (std::size_t q = 0; q < P.oflag.size(); ++q)
+      if (P.oflag[q] & kToAux) written[P.oaux[q]] = 1;
+    for (const Instr& in : P.bwd) {
+      auto flag = [&](std::uint32_t pos) {
+        const std::uint32_t r = P.opnd[pos] & kIndexMask;
+        if (!written[r]) { P.oflag[pos] |= kAssign; written[r] = 1; }
+        else P.oflag[pos] &= static_cast<std::uint8_t>(~kAssign);
+      };
+      if (in.kind == kAttn) {
+        std::vector<std::uint32_t> rr;
+        const Attn& A = P.attn[in.aux];
+        for (std::uint32_t u = 0; u < A.n_units; ++u)
+          for (std::uint32_t i = 0; i < A.hd; ++i) written[P.arows[A.unit_off + 3 * u] + i] = 1;
+        for (std::uint32_t j = 0; j < A.n_keys; ++j) {
+          for (std::uint32_t i = 0; i < A.hd; ++i) written[P.arows[A.key_off + 2 * j] + i] = 1;
+          for (std::uint32_t i = 0; i < A.dv; ++i) written[P.arows[A.key_off + 2 * j + 1] + i] = 1;
+        }
+      } else if (in.kind == kDense) {
+        const Dense& D = P.dense[in.aux];
+        for (std::uint32_t j = 0; j < D.n_out; ++j) written[D.out_row + j] = 1;
+        for (std::uint32_t q = 0; q < D.n_in; ++q) flag(D.x_opnd + q);
+      } else {
+        for (std::uint32_t j = 0; j < in.nops; ++j) {
+          const std::uint32_t o = P.opnd[in.opnd + j], mode = o >> kModeShift, idx = o & kIndexMask;
+          if (mode == kSlot) flag(in.opnd + j);
+          else if (mode == kSGather) {
+            const GatherTable& T = P.sgather[idx];
+            for (std::uint32_t r = 0; r < T.n_rows; ++r) {
+              const std::uint32_t rr = P.cand[T.cand_off + r];
+              if (!written[rr]) { needs_zero[rr] = 1; written[rr] = 1; }
+            }
+          }
+        }
+      }
     }
   }
   // input rows never reached still report a zero input gradient

@@ -42,6 +42,7 @@ enum InstrKind : std::uint8_t {
   kInputLoad = 1,   // V[out] = inputs[aux][s]
   kGatherLoad = 2,  // V[out] = UV[table[idx[col][s]]]   (aux = uniform gather id)
   kDense = 3,       // rows [out, out+n_out) = W x + b   (aux = dense id)
+  kAttn = 4,        // softmax attention head over per-sample rows (aux = attn id)
 };
 
 // Operand flags for the reverse sweep.
@@ -101,6 +102,24 @@ struct DenseGrad {
   std::uint32_t dest0;
 };
 
+// A softmax attention head recognised in the recorded scalar graph (the
+// composition of SPEC.md:306-312 out of reference ops): query unit u reads
+// keys 0 .. n_u-1 of the head's key list and computes
+//   c_j = scale * <q_u, k_j>        (innerProduct + mulByConstant)
+//   m   = max_j c_j                 (stop-gradient shift)
+//   a_j = exp(c_j - m) / sum_l exp(c_l - m)   (sub, exp, reduceSum, div)
+//   o_u[i] = sum_j a_j v_j[i]       (innerProduct over the values' column i)
+// One macro-instruction runs every unit; the interior nodes (scores, shifts,
+// exponentials, normaliser, weights) get no rows.  Rows are hd (dv)
+// consecutive rows per block: arows[unit_off + 3u] = {q_row, o_row, n_keys},
+// arows[key_off + 2j] = {k_row, v_row}.
+struct Attn {
+  std::uint32_t n_units, n_keys, hd, dv;
+  std::uint32_t unit_off, key_off;
+  std::uint32_t first_node, n_nodes;   // recorded nodes covered (diagnostics, node-eval counts)
+  double scale;
+};
+
 struct GatherTable {          // candidate list of one gather
   std::uint32_t col;          // index column
   std::uint32_t n_rows;
@@ -127,6 +146,8 @@ struct Program {
   std::vector<std::uint32_t> zero_rows;   // adjoint rows that must start at 0
   std::vector<std::uint32_t> input_rows;  // row of input column c (kNone if unused)
   std::vector<Dense> dense;
+  std::vector<Attn> attn;
+  std::vector<std::uint32_t> arows;
 
   // gathers
   std::vector<GatherTable> ugather;       // sample-invariant tables (materialised)

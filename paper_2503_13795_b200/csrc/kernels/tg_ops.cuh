@@ -182,6 +182,92 @@ __device__ __forceinline__ void propagate(std::uint8_t op, std::uint32_t n, cons
   }
 }
 
+// ---- fused softmax attention head (kAttn, tg_program.hpp Attn), per sample ----
+// The interpreter form: one thread walks the head's units with the same
+// operations, in the same order, as the scalar nodes it replaces (eval_node /
+// propagate above): c_j = <q, k_j> * scale, m = max_j c_j, e_j = exp(c_j - m),
+// Z = sum_j e_j (left to right), a_j = e_j / Z, o_i = sum_j a_j v_j[i].
+// Reverse, node by node: dA_j = sum_i dO_i v_j[i] and dv_j[i] += dO_i a_j
+// (innerProduct), de_j = dA_j / Z and dZ = -sum_j dA_j e_j / Z^2 (div),
+// de_j += dZ (reduceSum), dc_j = de_j e_j (exp), the shift takes no gradient,
+// ds_j = dc_j scale (mulByConstant), dq += ds_j k_j and dk_j += ds_j q
+// (innerProduct).  Scores are recomputed: interior nodes have no rows.  The
+// head is the only pusher into its q / k / v rows, so it clears them first.
+template <class T>
+__device__ __forceinline__ T attn_score(const tgc::Attn& A, const T* V, std::size_t ld, std::size_t col,
+                                        std::uint32_t q, std::uint32_t kr) {
+  T acc = 0;
+  for (std::uint32_t i = 0; i < A.hd; ++i) acc += V[std::size_t(q + i) * ld + col] * V[std::size_t(kr + i) * ld + col];
+  return acc * static_cast<T>(A.scale);
+}
+
+template <class T>
+__device__ void attn_fwd_sample(const tgc::Attn A, const std::uint32_t* __restrict__ ar, T* V, std::size_t ld,
+                                std::size_t col) {
+  const std::uint32_t* K = ar + A.key_off;
+  for (std::uint32_t u = 0; u < A.n_units; ++u) {
+    const std::uint32_t q = ar[A.unit_off + 3 * u], o = ar[A.unit_off + 3 * u + 1], n = ar[A.unit_off + 3 * u + 2];
+    T m = attn_score<T>(A, V, ld, col, q, K[0]);
+    for (std::uint32_t j = 1; j < n; ++j) {
+      const T c = attn_score<T>(A, V, ld, col, q, K[2 * j]);
+      m = c > m ? c : m;
+    }
+    T Z = 0;
+    for (std::uint32_t j = 0; j < n; ++j) Z += d_exp(attn_score<T>(A, V, ld, col, q, K[2 * j]) - m);
+    for (std::uint32_t i = 0; i < A.dv; ++i) V[std::size_t(o + i) * ld + col] = T(0);
+    for (std::uint32_t j = 0; j < n; ++j) {
+      const T a = d_exp(attn_score<T>(A, V, ld, col, q, K[2 * j]) - m) / Z;
+      const std::uint32_t vr = K[2 * j + 1];
+      for (std::uint32_t i = 0; i < A.dv; ++i) V[std::size_t(o + i) * ld + col] += a * V[std::size_t(vr + i) * ld + col];
+    }
+  }
+}
+
+template <class T>
+__device__ void attn_bwd_sample(const tgc::Attn A, const std::uint32_t* __restrict__ ar, const T* V, T* G,
+                                std::size_t ld, std::size_t col) {
+  const std::uint32_t* K = ar + A.key_off;
+  const T scale = static_cast<T>(A.scale);
+  for (std::uint32_t j = 0; j < A.n_keys; ++j) {
+    for (std::uint32_t i = 0; i < A.hd; ++i) G[std::size_t(K[2 * j] + i) * ld + col] = T(0);
+    for (std::uint32_t i = 0; i < A.dv; ++i) G[std::size_t(K[2 * j + 1] + i) * ld + col] = T(0);
+  }
+  for (std::uint32_t u = 0; u < A.n_units; ++u) {
+    const std::uint32_t q = ar[A.unit_off + 3 * u], o = ar[A.unit_off + 3 * u + 1], n = ar[A.unit_off + 3 * u + 2];
+    for (std::uint32_t i = 0; i < A.hd; ++i) G[std::size_t(q + i) * ld + col] = T(0);
+    T m = attn_score<T>(A, V, ld, col, q, K[0]);
+    for (std::uint32_t j = 1; j < n; ++j) {
+      const T c = attn_score<T>(A, V, ld, col, q, K[2 * j]);
+      m = c > m ? c : m;
+    }
+    T Z = 0;
+    for (std::uint32_t j = 0; j < n; ++j) Z += d_exp(attn_score<T>(A, V, ld, col, q, K[2 * j]) - m);
+    auto dA = [&](std::uint32_t j) {
+      const std::uint32_t vr = K[2 * j + 1];
+      T acc = 0;
+      for (std::uint32_t i = 0; i < A.dv; ++i) acc += G[std::size_t(o + i) * ld + col] * V[std::size_t(vr + i) * ld + col];
+      return acc;
+    };
+    T dZ = 0;
+    for (std::uint32_t j = 0; j < n; ++j) {
+      const T e = d_exp(attn_score<T>(A, V, ld, col, q, K[2 * j]) - m);
+      dZ += -dA(j) * e / (Z * Z);
+    }
+    for (std::uint32_t j = 0; j < n; ++j) {
+      const std::uint32_t kr = K[2 * j], vr = K[2 * j + 1];
+      const T e = d_exp(attn_score<T>(A, V, ld, col, q, kr) - m);
+      const T a = e / Z;
+      const T da = dA(j);
+      for (std::uint32_t i = 0; i < A.dv; ++i) G[std::size_t(vr + i) * ld + col] += G[std::size_t(o + i) * ld + col] * a;
+      const T ds = (da / Z + dZ) * e * scale;
+      for (std::uint32_t i = 0; i < A.hd; ++i) {
+        G[std::size_t(q + i) * ld + col] += ds * V[std::size_t(kr + i) * ld + col];
+        G[std::size_t(kr + i) * ld + col] += ds * V[std::size_t(q + i) * ld + col];
+      }
+    }
+  }
+}
+
 // Fused activations of kDense groups (domain-free unary ops only); same
 // formulas as eval_node / propagate above.
 template <class T>

@@ -84,6 +84,9 @@ __device__ __forceinline__ void fwd_instr(const RangeArgs<T>& a, RowAccS<T>& acc
     if (bad) record_error(a.err_key, s, in.node);
   } else if (in.kind == tgc::kInputLoad) {
     v = a.inputs[std::size_t(in.aux) * a.batch + s];
+  } else if (in.kind == tgc::kAttn) {
+    attn_fwd_sample<T>(a.attn[in.aux], a.arows, V, ld, col);
+    return;
   } else if (in.kind == tgc::kDense) {
     const tgc::Dense D = a.dense[in.aux];
     const std::uint32_t* xo = a.opnd + D.x_opnd;
@@ -111,6 +114,10 @@ __device__ __forceinline__ void bwd_instr(const RangeArgs<T>& a, RowAccS<T>& acc
   T* G = a.G;
   const std::size_t ld = a.ld;
   const Instr in = a.bwd[k];
+  if (in.kind == tgc::kAttn) {
+    attn_bwd_sample<T>(a.attn[in.aux], a.arows, V, G, ld, col);
+    return;
+  }
   if (in.kind == tgc::kDense) {
     const tgc::Dense D = a.dense[in.aux];
     if (D.act_op)

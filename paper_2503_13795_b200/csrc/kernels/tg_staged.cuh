@@ -35,6 +35,8 @@ struct RangeArgs {
   const tgc::GatherTable* sg;
   const std::uint32_t* cand;
   const tgc::Dense* dense;
+  const tgc::Attn* attn;
+  const std::uint32_t* arows;
   const T* UV;
   const T* inputs;
   const std::int32_t* idx;
@@ -110,6 +112,11 @@ template <class T> cudaError_t launch_level_range(const RangeArgs<T>& a, cudaStr
 template <class T> cudaError_t launch_gemm(const GemmArgs<T>& g, std::uint32_t splits, cudaStream_t st);
 // fp32 GEMM on the 5th-gen tensor cores (tcgen05.mma kind::tf32, 3xTF32 split), tg_umma.cu
 cudaError_t launch_gemm_umma(const GemmArgs<float>& g, std::uint32_t splits, cudaStream_t st);
+// Fused softmax attention heads (kAttn) of one stage: instructions list[begin, begin + count),
+// one CTA per head and 8 samples (tg_attn.cu); fp32, hd / dv <= 16, <= 64 keys and units.
+bool attn_fast_ok(const tgc::Attn& A);
+cudaError_t launch_attn(bool fwd, const tgc::Instr* list, std::uint32_t begin, std::uint32_t count, const tgc::Attn* attn,
+                        const std::uint32_t* arows, float* V, float* G, std::size_t n, std::size_t ld, cudaStream_t st);
 // CTAs one split-K slice / batch member of a tcgen05 product launches (CTA pairs when M > 128)
 std::uint32_t umma_ctas_per_slice(std::uint32_t M, std::uint32_t N);
 // dst[m * N + n] += sum_kz part[kz][m][n]   (fixed order)

@@ -124,6 +124,9 @@ __global__ void __launch_bounds__(256) k_tape(MainArgs<T> a) {
           }
         } else if (in.kind == tgc::kInputLoad) {
           v = a.inputs[std::size_t(in.aux) * a.batch + s];
+        } else if (in.kind == tgc::kAttn) {
+          attn_fwd_sample<T>(a.attn[in.aux], a.arows, V, ld, col);
+          continue;
         } else if (in.kind == tgc::kDense) {  // dense layer: z_j = b_j + <x, W[j]>, h_j = act(z_j)
           const tgc::Dense D = a.dense[in.aux];
           const std::uint32_t* xo = a.opnd + D.x_opnd;
@@ -150,6 +153,10 @@ __global__ void __launch_bounds__(256) k_tape(MainArgs<T> a) {
       // ---- reverse sweep (reference processing order) ----
       for (std::uint32_t k = 0; k < a.n_bwd; ++k) {
         const Instr in = a.bwd[k];
+        if (in.kind == tgc::kAttn) {
+          attn_bwd_sample<T>(a.attn[in.aux], a.arows, V, G, ld, col);
+          continue;
+        }
         if (in.kind == tgc::kDense) {
           const tgc::Dense D = a.dense[in.aux];
           if (D.act_op)

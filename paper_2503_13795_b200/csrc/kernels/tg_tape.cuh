@@ -26,6 +26,8 @@ struct MainArgs {
   const std::uint32_t* term_off;
   const tgc::Term* terms;
   const tgc::Dense* dense;
+  const tgc::Attn* attn;
+  const std::uint32_t* arows;
   const T* UV;
   const T* inputs;
   const std::int32_t* idx;

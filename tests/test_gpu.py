@@ -117,22 +117,26 @@ def test_larger_batches_vs_oracle(tier, name, dims, dt, b):
         assert rel(IG, r["input_grad"]) <= TOL[dt] * 10
 
 
-@pytest.mark.parametrize("batch_env", ["1", "0"])
-def test_gpt_cfg4_dims_vs_oracle(batch_env):
+@pytest.mark.parametrize("batch_env,attn_fast", [("1", "1"), ("0", "1"), ("1", "0")])
+def test_gpt_cfg4_dims_vs_oracle(batch_env, attn_fast):
     """cfg4's GPT (65/64/64/4H/4L) through the staged tier: the 64 positions'
     dense layers over one weight run as batched tcgen05 products (forward,
     input adjoints, split-K weight gradients summed over positions) —
-    TG_STAGED_BATCH=0 runs them one position at a time — against the oracle."""
+    TG_STAGED_BATCH=0 runs them one position at a time — and the 16 attention
+    heads, recognised in the scalar graph, run fused (TG_ATTN_FAST=1: shared-
+    memory kernels; 0: the per-sample interpreter form), against the oracle."""
     desc = tg.build_model("gpt", None, "f32", seed=4).describe()
     b = 12
     x, k = tg.synth_batch("gpt", None, "f32", seed=21, batch=b, n_inputs=0, n_index=desc.n_index_inputs)
     os.environ["TG_STAGED_BATCH"] = batch_env
+    os.environ["TG_ATTN_FAST"] = attn_fast
     try:
         prog = tg.Program(desc)
         L, IG, G = run(prog, desc, x, k, desc.param_values(), b, want_igrad=False)
-        assert prog.info["storage"] == 3
+        assert prog.info["storage"] == 3 and prog.info["n_attn_heads"] == 16
     finally:
         os.environ.pop("TG_STAGED_BATCH")
+        os.environ.pop("TG_ATTN_FAST")
     r = oracle.run(desc, x.astype(np.float64), k, desc.param_values(), threads=os.cpu_count() or 8)
     assert close_rel(L, r["loss"], 1e-5, 1e-6)
     assert rel(G, r["grad_sum"]) <= 1e-5
