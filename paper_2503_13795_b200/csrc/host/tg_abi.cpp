@@ -194,6 +194,7 @@ struct tg_program {
   std::size_t chunk = 0;          // samples per chunk (0 = by batch)
   bool umma = true;               // fp32 dense layers on tcgen05 (3xTF32); TG_UMMA=0 -> SIMT GEMM
   bool attn_fast = false;         // fused heads on the shared-memory kernels (tg_attn.cu; TG_ATTN_FAST=0: interpreter)
+  std::uint32_t attn_hd = 0;      // widest key / value block of the fused heads
   ~tg_program() {
     tgj::release(jit);
     for (auto& e : ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
@@ -481,7 +482,10 @@ void build_staged_plan(tg_program& pr) {
   {
     const char* af = std::getenv("TG_ATTN_FAST");
     pr.attn_fast = pr.tsz() == 4 && !P.attn.empty() && !(af && af[0] == '0');
-    for (const auto& A : P.attn) pr.attn_fast = pr.attn_fast && tgk::attn_fast_ok(A);
+    for (const auto& A : P.attn) {
+      pr.attn_fast = pr.attn_fast && tgk::attn_fast_ok(A);
+      pr.attn_hd = std::max({pr.attn_hd, A.hd, A.dv});
+    }
   }
   if (const char* u = std::getenv("TG_UMMA")) pr.umma = u[0] != '0';
   if (!pr.staged || P.root_row == tgc::kNone) { pr.staged = false; return; }
@@ -1350,7 +1354,7 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
       if constexpr (std::is_same_v<T, float>) {
         if (pr.attn_fast)
           return tgk::launch_attn(fwd, fwd ? pr.d_fwd : pr.d_bwd, stg.begin, stg.end - stg.begin, pr.d_attn, pr.d_arows,
-                                  V, G, n, cb, st);
+                                  V, G, n, cb, pr.attn_hd, st);
       }
       ra.flags = fwd ? tgk::kRFwd : tgk::kRBwd;
       (fwd ? ra.fwd_begin : ra.bwd_begin) = stg.begin;

@@ -13,6 +13,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <type_traits>
 
 #include "tg_ops.cuh"
 #include "tg_staged.cuh"
@@ -180,6 +182,284 @@ __global__ void __launch_bounds__(128) k_level_range(RangeArgs<T> a) {
   RowAccS<T> acc{a.V, a.G, a.ld, col, a.UV, a.idx, a.batch, s, a.sg, a.cand, nullptr, nullptr, nullptr};
   if (a.flags & kRFwd) fwd_instr(a, acc, a.fwd_begin + blockIdx.x, s, col);
   else bwd_instr(a, acc, a.bwd_begin + blockIdx.x, col);
+}
+
+// ---- fp32 levels, four consecutive samples per thread ------------------------
+// The scalar level kernel keeps one 4-byte load in flight per thread behind
+// the operand decode, and launches one 128-thread CTA per instruction and 128
+// samples: at ~8k samples a level of 4k elementwise nodes ran at a third of the
+// HBM bandwidth (ncu: long-scoreboard bound, 500 instructions per thread).
+// Here a thread moves float4s (4 samples) for every slot operand and a CTA
+// walks kLvInstr instructions; the node math stays the scalar eval_node /
+// propagate per lane (same operations, same order, same domain checks), or an
+// explicit lane loop for the many-operand sums and inner products.  Partial
+// groups of four (chunk tail) take the scalar path.
+constexpr int kLvInstr = 4;   // instructions per CTA on large levels
+
+struct L4 {
+  float v[4];
+};
+__device__ __forceinline__ L4 ld4(const float* p) {
+  const float4 q = *reinterpret_cast<const float4*>(p);
+  return L4{{q.x, q.y, q.z, q.w}};
+}
+__device__ __forceinline__ void st4(float* p, const L4& x) {
+  *reinterpret_cast<float4*>(p) = make_float4(x.v[0], x.v[1], x.v[2], x.v[3]);
+}
+
+// operand accessor of one lane for nodes of at most two operands
+struct Pre2 {
+  std::uint32_t o0, o1;
+  float v0, v1;
+  float pv[2];
+  bool pushed[2];
+  __device__ __forceinline__ float val(std::uint32_t op) const { return op == o0 ? v0 : v1; }
+  __device__ __forceinline__ void push(std::uint32_t k, float v) {
+    pv[k] = v;
+    pushed[k] = true;
+  }
+};
+
+struct Lv4 {
+  const RangeArgs<float>& a;
+  std::size_t col, s;
+  __device__ __forceinline__ std::uint32_t sg_row(std::uint32_t i, int l) const {
+    const GatherTable t = a.sg[i];
+    std::int32_t r = a.idx[std::size_t(t.col) * a.batch + s + l];
+    if (r < 0 || static_cast<std::uint32_t>(r) >= t.n_rows) r = 0;
+    return a.cand[t.cand_off + r];
+  }
+  __device__ __forceinline__ L4 val(std::uint32_t op) const {
+    const std::uint32_t m = op >> kModeShift, i = op & kIndexMask;
+    if (m == tgc::kSlot) return ld4(a.V + std::size_t(i) * a.ld + col);
+    if (m == tgc::kUv) {
+      const float u = a.UV[i];
+      return L4{{u, u, u, u}};
+    }
+    L4 r;
+#pragma unroll
+    for (int l = 0; l < 4; ++l) r.v[l] = a.V[std::size_t(sg_row(i, l)) * a.ld + col + l];
+    return r;
+  }
+  // reverse push of operand position pos (operand code, flags and aux row of the instruction)
+  __device__ __forceinline__ void push(std::uint32_t pos, const L4& x) const {
+    const std::uint32_t op = a.opnd[pos], m = op >> kModeShift, i = op & kIndexMask;
+    const std::uint8_t f = a.oflag[pos];
+    if (f & tgc::kToAux) {
+      st4(a.G + std::size_t(a.oaux[pos]) * a.ld + col, x);
+    } else if (m == tgc::kSlot) {
+      float* p = a.G + std::size_t(i) * a.ld + col;
+      if (f & tgc::kAssign) {
+        st4(p, x);
+      } else {
+        L4 c = ld4(p);
+#pragma unroll
+        for (int l = 0; l < 4; ++l) c.v[l] += x.v[l];
+        st4(p, c);
+      }
+    } else if (m == tgc::kSGather) {
+#pragma unroll
+      for (int l = 0; l < 4; ++l) a.G[std::size_t(sg_row(i, l)) * a.ld + col + l] += x.v[l];
+    }
+  }
+};
+
+__device__ __forceinline__ bool many_operand_op(std::uint8_t op) {
+  return op == AddVarying || op == MeanVarying || op == NegativeMeanVarying || op == SubVarying ||
+         op == SumOfSquaresVarying || op == MeanSquaresVarying || op == InnerProductNoBias ||
+         op == InnerProductWithBias || op == StopGradMax;
+}
+
+__device__ void fwd_instr4(const RangeArgs<float>& a, std::uint32_t k, std::size_t col, std::size_t s) {
+  const Instr in = a.fwd[k];
+  Lv4 L{a, col, s};
+  L4 out;
+  if (in.kind == tgc::kInputLoad) {
+    const float* src = a.inputs + std::size_t(in.aux) * a.batch + s;
+    if ((reinterpret_cast<std::uintptr_t>(src) & 15) == 0) {
+      out = ld4(src);
+    } else {
+#pragma unroll
+      for (int l = 0; l < 4; ++l) out.v[l] = src[l];
+    }
+  } else if (in.kind == tgc::kNode && in.nops <= 2 && !many_operand_op(in.op)) {
+    const std::uint32_t* o = a.opnd + in.opnd;
+    const std::uint32_t o1 = in.nops > 1 ? o[1] : o[0];
+    const L4 x0 = L.val(o[0]), x1 = in.nops > 1 ? L.val(o1) : x0;
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      Pre2 p{o[0], o1, x0.v[l], x1.v[l], {0.f, 0.f}, {false, false}};
+      bool bad = false;
+      float badv = 0;
+      out.v[l] = eval_node<float>(in.op, in.nops, o, in.cst, p, bad, badv);
+      if (bad) record_error(a.err_key, s + l, in.node);
+    }
+  } else if (in.kind == tgc::kNode && many_operand_op(in.op)) {
+    const std::uint32_t* o = a.opnd + in.opnd;
+    const std::uint32_t n = in.nops;
+    const std::uint8_t op = in.op;
+    if (op == InnerProductNoBias || op == InnerProductWithBias) {
+      const std::uint32_t m = op == InnerProductWithBias ? (n - 1) / 2 : n / 2;
+      L4 acc = op == InnerProductWithBias ? L.val(o[n - 1]) : L4{{0.f, 0.f, 0.f, 0.f}};
+      for (std::uint32_t j = 0; j < m; ++j) {
+        const L4 x = L.val(o[j]), y = L.val(o[m + j]);
+#pragma unroll
+        for (int l = 0; l < 4; ++l) acc.v[l] += x.v[l] * y.v[l];
+      }
+      out = acc;
+    } else if (op == StopGradMax) {
+      out = L.val(o[0]);
+      for (std::uint32_t j = 1; j < n; ++j) {
+        const L4 x = L.val(o[j]);
+#pragma unroll
+        for (int l = 0; l < 4; ++l) out.v[l] = x.v[l] > out.v[l] ? x.v[l] : out.v[l];
+      }
+    } else if (op == SubVarying) {
+      out = L.val(o[0]);
+      for (std::uint32_t j = 1; j < n; ++j) {
+        const L4 x = L.val(o[j]);
+#pragma unroll
+        for (int l = 0; l < 4; ++l) out.v[l] -= x.v[l];
+      }
+    } else {   // sums (of squares), left to right, then the mean scaling of eval_node
+      const bool sq = op == SumOfSquaresVarying || op == MeanSquaresVarying;
+      L4 acc{{0.f, 0.f, 0.f, 0.f}};
+      std::uint32_t j = 0;
+      for (; j + 4 <= n; j += 4) {
+        L4 x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x[u] = L.val(o[j + u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int l = 0; l < 4; ++l) acc.v[l] += sq ? x[u].v[l] * x[u].v[l] : x[u].v[l];
+      }
+      for (; j < n; ++j) {
+        const L4 x = L.val(o[j]);
+#pragma unroll
+        for (int l = 0; l < 4; ++l) acc.v[l] += sq ? x.v[l] * x.v[l] : x.v[l];
+      }
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        if (op == MeanVarying || op == MeanSquaresVarying) acc.v[l] /= static_cast<float>(n);
+        if (op == NegativeMeanVarying) acc.v[l] = -acc.v[l] / static_cast<float>(n);
+      }
+      out = acc;
+    }
+  } else {
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      RowAccS<float> acc{a.V, a.G, a.ld, col + l, a.UV, a.idx, a.batch, s + l, a.sg, a.cand, nullptr, nullptr, nullptr};
+      fwd_instr(a, acc, k, s + l, col + l);
+    }
+    return;
+  }
+  st4(a.V + std::size_t(in.out) * a.ld + col, out);
+}
+
+__device__ void bwd_instr4(const RangeArgs<float>& a, std::uint32_t k, std::size_t col, std::size_t s) {
+  const Instr in = a.bwd[k];
+  if (in.kind != tgc::kNode || !(many_operand_op(in.op) || in.nops <= 2) || in.op == StopGradMax) {
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      RowAccS<float> acc{a.V, a.G, a.ld, col + l, a.UV, a.idx, a.batch, s + l, a.sg, a.cand, nullptr, nullptr, nullptr};
+      bwd_instr(a, acc, k, col + l);
+    }
+    return;
+  }
+  Lv4 L{a, col, s};
+  const std::uint32_t* o = a.opnd + in.opnd;
+  const std::uint32_t n = in.nops, p0 = in.opnd;
+  const std::uint8_t op = in.op;
+  const L4 g = ld4(a.G + std::size_t(in.out) * a.ld + col);
+  if (!many_operand_op(op)) {
+    const L4 y = ld4(a.V + std::size_t(in.out) * a.ld + col);
+    const std::uint32_t o1 = n > 1 ? o[1] : o[0];
+    const L4 x0 = L.val(o[0]), x1 = n > 1 ? L.val(o1) : x0;
+    L4 pv[2];
+    bool any[2] = {false, false};
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      Pre2 p{o[0], o1, x0.v[l], x1.v[l], {0.f, 0.f}, {false, false}};
+      propagate<float>(op, n, o, in.cst, g.v[l], y.v[l], p);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        pv[q].v[l] = p.pv[q];
+        any[q] = any[q] || p.pushed[q];
+      }
+    }
+    if (any[0]) L.push(p0, pv[0]);
+    if (n > 1 && any[1]) L.push(p0 + 1, pv[1]);
+    return;
+  }
+  auto scaled = [&](float c) {
+    L4 r;
+#pragma unroll
+    for (int l = 0; l < 4; ++l) r.v[l] = g.v[l] * c;
+    return r;
+  };
+  if (op == AddVarying) {
+    for (std::uint32_t j = 0; j < n; ++j) L.push(p0 + j, g);
+  } else if (op == SubVarying) {
+    L.push(p0, g);
+    const L4 ng = scaled(-1.f);
+    for (std::uint32_t j = 1; j < n; ++j) L.push(p0 + j, ng);
+  } else if (op == MeanVarying || op == NegativeMeanVarying) {
+    L4 dd;
+#pragma unroll
+    for (int l = 0; l < 4; ++l) dd.v[l] = (op == MeanVarying ? g.v[l] : -g.v[l]) / static_cast<float>(n);
+    for (std::uint32_t j = 0; j < n; ++j) L.push(p0 + j, dd);
+  } else if (op == SumOfSquaresVarying || op == MeanSquaresVarying) {
+    L4 sc;
+#pragma unroll
+    for (int l = 0; l < 4; ++l)
+      sc.v[l] = op == SumOfSquaresVarying ? g.v[l] * 2.f : g.v[l] * 2.f / static_cast<float>(n);
+    for (std::uint32_t j = 0; j < n; ++j) {
+      const L4 x = L.val(o[j]);
+      L4 r;
+#pragma unroll
+      for (int l = 0; l < 4; ++l) r.v[l] = op == SumOfSquaresVarying ? g.v[l] * 2.f * x.v[l] : sc.v[l] * x.v[l];
+      L.push(p0 + j, r);
+    }
+  } else {   // inner products: x and y adjoints interleaved as in propagate (ops.hpp:436-452)
+    const std::uint32_t m = op == InnerProductWithBias ? (n - 1) / 2 : n / 2;
+    for (std::uint32_t j = 0; j < m; ++j) {
+      const L4 x = L.val(o[j]), y = L.val(o[m + j]);
+      L4 gx, gy;
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        gx.v[l] = g.v[l] * y.v[l];
+        gy.v[l] = g.v[l] * x.v[l];
+      }
+      L.push(p0 + j, gx);
+      L.push(p0 + m + j, gy);
+    }
+    if (op == InnerProductWithBias) L.push(p0 + n - 1, g);
+  }
+}
+
+__device__ void level_instr1(const RangeArgs<float>& a, bool fwd, std::uint32_t k, std::size_t c) {
+  RowAccS<float> acc{a.V, a.G, a.ld, c, a.UV, a.idx, a.batch, a.s0 + c, a.sg, a.cand, nullptr, nullptr, nullptr};
+  if (fwd) fwd_instr(a, acc, k, a.s0 + c, c);
+  else bwd_instr(a, acc, k, c);
+}
+
+__global__ void __launch_bounds__(128) k_level_range4(RangeArgs<float> a, std::uint32_t ipc) {
+  const std::size_t col = (std::size_t(blockIdx.y) * blockDim.x + threadIdx.x) * 4;
+  if (col >= a.n) return;
+  const std::size_t s = a.s0 + col;
+  const bool fwd = a.flags & kRFwd;
+  const std::uint32_t begin = fwd ? a.fwd_begin : a.bwd_begin, end = fwd ? a.fwd_end : a.bwd_end;
+  const std::uint32_t k0 = begin + blockIdx.x * ipc, k1 = min(end, k0 + ipc);
+  if (col + 4 <= a.n) {
+    for (std::uint32_t k = k0; k < k1; ++k) {
+      if (fwd) fwd_instr4(a, k, col, s);
+      else bwd_instr4(a, k, col, s);
+    }
+    return;
+  }
+  for (std::size_t c = col; c < a.n; ++c)   // chunk tail
+    for (std::uint32_t k = k0; k < k1; ++k) level_instr1(a, fwd, k, c);
 }
 
 // Sums of the contended rows of one reverse level (entry blockIdx.x, 128
@@ -497,6 +777,19 @@ template <class T>
 cudaError_t launch_level_range(const RangeArgs<T>& a, cudaStream_t st) {
   const std::uint32_t count = (a.flags & kRFwd) ? a.fwd_end - a.fwd_begin : a.bwd_end - a.bwd_begin;
   if (a.n == 0 || count == 0) return cudaSuccess;
+  if constexpr (std::is_same_v<T, float>) {
+    static const bool vec = !(std::getenv("TG_LEVEL4") && std::getenv("TG_LEVEL4")[0] == '0');
+    if (vec && a.ld % 4 == 0 && (reinterpret_cast<std::uintptr_t>(a.V) & 15) == 0 &&
+        (reinterpret_cast<std::uintptr_t>(a.G) & 15) == 0) {
+      // instructions per CTA: kLvInstr (one load group) while the launch keeps
+      // >= ~16 CTAs per SM, else one (few-instruction levels, e.g. the
+      // layer-norm statistics, need the CTAs more than the grouping)
+      const std::uint32_t ys = static_cast<std::uint32_t>((a.n + 511) / 512);
+      const std::uint32_t ipc = std::uint64_t(count) * ys >= 4ull * 148 * 16 ? kLvInstr : 1;
+      k_level_range4<<<dim3((count + ipc - 1) / ipc, ys), 128, 0, st>>>(a, ipc);
+      return cudaGetLastError();
+    }
+  }
   k_level_range<T><<<dim3(count, static_cast<unsigned>((a.n + 127) / 128)), 128, 0, st>>>(a);
   return cudaGetLastError();
 }

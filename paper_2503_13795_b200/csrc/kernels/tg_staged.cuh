@@ -116,7 +116,8 @@ cudaError_t launch_gemm_umma(const GemmArgs<float>& g, std::uint32_t splits, cud
 // one CTA per head and 8 samples (tg_attn.cu); fp32, hd / dv <= 16, <= 64 keys and units.
 bool attn_fast_ok(const tgc::Attn& A);
 cudaError_t launch_attn(bool fwd, const tgc::Instr* list, std::uint32_t begin, std::uint32_t count, const tgc::Attn* attn,
-                        const std::uint32_t* arows, float* V, float* G, std::size_t n, std::size_t ld, cudaStream_t st);
+                        const std::uint32_t* arows, float* V, float* G, std::size_t n, std::size_t ld, std::uint32_t hd_max,
+                        cudaStream_t st);
 // CTAs one split-K slice / batch member of a tcgen05 product launches (CTA pairs when M > 128)
 std::uint32_t umma_ctas_per_slice(std::uint32_t M, std::uint32_t N);
 // dst[m * N + n] += sum_kz part[kz][m][n]   (fixed order)
