@@ -168,6 +168,7 @@ typedef struct tg_program_info {
                                 3 = staged (HBM rows, dense layers as GEMMs) */
   tg_dtype dtype;
   uint32_t n_attn_heads;     /* softmax attention heads fused from the scalar graph */
+  uint32_t n_layer_norms;    /* layer normalisations fused from the scalar graph */
 } tg_program_info;
 
 /* Lowers the tape to the device program (replaces the per-sample DFS of

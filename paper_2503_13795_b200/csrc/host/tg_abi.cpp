@@ -114,6 +114,9 @@ struct tg_program {
   tgc::Dense* d_dense = nullptr;
   tgc::Attn* d_attn = nullptr;
   std::uint32_t* d_arows = nullptr;
+  tgc::LNorm* d_lnorm = nullptr;
+  std::uint32_t* d_lnrows = nullptr;
+  std::uint8_t* d_lnflag = nullptr;
   void* d_consts = nullptr;
   unsigned long long* d_err_key = nullptr;
   double* d_err_val = nullptr;
@@ -139,7 +142,7 @@ struct tg_program {
   // register-resident specialisation (tg_jit.cpp)
   tgj::JitKernel jit;
   // staged execution over an HBM SoA workspace (large tapes, dense layers as GEMMs)
-  struct Stage { int batch; std::uint32_t begin, end; bool level = false; bool inputs_only = false; };   // batch >= 0: GEMM stage; level: one
+  struct Stage { int batch; std::uint32_t begin, end; bool level = false; bool inputs_only = false; bool macro = false; };   // batch >= 0: GEMM stage; level: one
                                                                               // instruction per CTA column (k_level_range);
                                                                               // batch == kSumStage: sums[begin, end)
   // Dense layers of one dependency level over the same weights (a GPT's 64
@@ -236,6 +239,18 @@ void attn_in_rows(const tgc::Program& P, std::uint32_t id, std::vector<std::uint
     for (std::uint32_t i = 0; i < A.dv; ++i) out.push_back(P.arows[A.key_off + 2 * j + 1] + i);
   }
 }
+// Rows of a fused layer norm: reads (x) and outputs (n_i and y_i).
+void ln_in_rows(const tgc::Program& P, std::uint32_t id, std::vector<std::uint32_t>& out) {
+  const tgc::LNorm& L = P.lnorm[id];
+  for (std::uint32_t i = 0; i < L.n; ++i) out.push_back(P.lnrows[L.off + i]);
+}
+void ln_out_rows(const tgc::Program& P, std::uint32_t id, std::vector<std::uint32_t>& out, bool with_n) {
+  const tgc::LNorm& L = P.lnorm[id];
+  for (std::uint32_t i = 0; i < L.n; ++i) {
+    if (with_n) out.push_back(P.lnrows[L.off + L.n + i]);
+    out.push_back(P.lnrows[L.off + 2 * L.n + i]);
+  }
+}
 void attn_out_rows(const tgc::Program& P, std::uint32_t id, std::vector<std::uint32_t>& out) {
   const tgc::Attn& A = P.attn[id];
   for (std::uint32_t u = 0; u < A.n_units; ++u)
@@ -264,10 +279,15 @@ void level_schedule(tg_program& pr, const std::vector<char>& gemm_dense) {
       for (std::uint32_t j = 0; j < D.n_in; ++j) slot_rows(P.opnd[D.x_opnd + j], rows);
     }
     if (in.kind == tgc::kAttn) attn_in_rows(P, in.aux, rows);
+    if (in.kind == tgc::kLNorm) ln_in_rows(P, in.aux, rows);
     std::uint32_t L = 0;
     for (std::uint32_t r : rows) L = std::max(L, row_level[r] + 1);
     lvl[k] = L;
-    if (in.kind == tgc::kAttn) {
+    if (in.kind == tgc::kLNorm) {
+      std::vector<std::uint32_t> orows;
+      ln_out_rows(P, in.aux, orows, true);
+      for (std::uint32_t r : orows) row_level[r] = L;
+    } else if (in.kind == tgc::kAttn) {
       std::vector<std::uint32_t> orows;
       attn_out_rows(P, in.aux, orows);
       for (std::uint32_t r : orows) row_level[r] = L;
@@ -310,7 +330,12 @@ void level_schedule(tg_program& pr, const std::vector<char>& gemm_dense) {
     const tgc::Instr& in = P.bwd[k];
     rows.clear();
     std::vector<std::uint32_t> uv_aux;
-    if (in.kind == tgc::kAttn) {
+    if (in.kind == tgc::kLNorm) {
+      ln_out_rows(P, in.aux, rows, false);
+      std::vector<std::uint32_t> xr;
+      ln_in_rows(P, in.aux, xr);
+      for (std::uint32_t r : xr) pushes[k].push_back({r, tgc::kNone, true});
+    } else if (in.kind == tgc::kAttn) {
       attn_out_rows(P, in.aux, rows);
       std::vector<std::uint32_t> xr;
       attn_in_rows(P, in.aux, xr);
@@ -410,6 +435,16 @@ void level_schedule(tg_program& pr, const std::vector<char>& gemm_dense) {
     std::unordered_map<std::uint32_t, std::vector<std::uint32_t>> uses;   // row -> operand positions
     for (std::size_t k = k0; k < k1; ++k) {
       const tgc::Instr& in = P.bwd[k];
+      if (in.kind == tgc::kLNorm) {   // x adjoints: pushes with first-write flags, like dense x operands
+        const tgc::LNorm& LN = P.lnorm[in.aux];
+        for (std::uint32_t i = 0; i < LN.n; ++i) {
+          const std::uint32_t r = P.lnrows[LN.off + i];
+          if (!seen[r] && !gather_target[r]) P.lnflag[LN.flag_off + i] |= tgc::kAssign;
+          else P.lnflag[LN.flag_off + i] &= static_cast<std::uint8_t>(~tgc::kAssign);
+          seen[r] = 1;
+        }
+        continue;
+      }
       if (in.kind == tgc::kAttn) {   // stores its q / k / v adjoints
         std::vector<std::uint32_t> xr;
         attn_in_rows(P, in.aux, xr);
@@ -667,6 +702,16 @@ void build_staged_plan(tg_program& pr) {
   pr.batches.clear();
   split(P.fwd, P.fwd_level, pr.sfwd, false);
   split(P.bwd, P.bwd_level, pr.sbwd, true);
+  // interpreter stages holding macro-instructions (fused layer norms, ...)
+  // run one sample per thread: the per-sample routines carry their own
+  // memory parallelism, and four samples per thread would serialise them
+  for (int w = 0; w < 2; ++w)
+    for (auto& stg : w ? pr.sbwd : pr.sfwd)
+      if (stg.batch == -1)
+        for (std::uint32_t k = stg.begin; k < stg.end && !stg.macro; ++k) {
+          const auto kind = (w ? P.bwd : P.fwd)[k].kind;
+          stg.macro = kind == tgc::kLNorm || kind == tgc::kDense || kind == tgc::kAttn;
+        }
   // batch tables: forward {0, x, z, h}, input adjoints {0, z, x, 0}, weight gradient {z, x, 0, 0}
   const bool tc = pr.tsz() == 4 && pr.umma;
   for (auto& B : pr.batches) {
@@ -717,9 +762,10 @@ void build_staged_plan(tg_program& pr) {
         for (std::uint32_t k = 0; k < I.nops; ++k) push_opnd(I.opnd + k);
       else if (I.kind == tgc::kDense)
         for (std::uint32_t k = 0; k < P.dense[I.aux].n_in; ++k) push_opnd(P.dense[I.aux].x_opnd + k);
-      else if (I.kind == tgc::kAttn) {
+      else if (I.kind == tgc::kAttn || I.kind == tgc::kLNorm) {
         std::vector<std::uint32_t> xr;
-        attn_in_rows(P, I.aux, xr);
+        if (I.kind == tgc::kAttn) attn_in_rows(P, I.aux, xr);
+        else ln_in_rows(P, I.aux, xr);
         for (std::uint32_t r : xr) ++pushers[r];
       }
     }
@@ -799,9 +845,10 @@ void build_staged_plan(tg_program& pr) {
         for (std::uint32_t k = 0; k < I.nops; ++k) mark(I.opnd + k);
       else if (I.kind == tgc::kDense && pr.dplan[I.aux].x_col0 == tgc::kNone)
         for (std::uint32_t k = 0; k < P.dense[I.aux].n_in; ++k) mark(P.dense[I.aux].x_opnd + k);
-      else if (I.kind == tgc::kAttn) {
+      else if (I.kind == tgc::kAttn || I.kind == tgc::kLNorm) {
         std::vector<std::uint32_t> xr;
-        attn_in_rows(P, I.aux, xr);
+        if (I.kind == tgc::kAttn) attn_in_rows(P, I.aux, xr);
+        else ln_in_rows(P, I.aux, xr);
         for (std::uint32_t r : xr) other[r] = 1;
       }
     }
@@ -1070,6 +1117,9 @@ tg_status upload(tg_program& pr) {
   TG_TRY(upload_vec(pr, P.dense, &pr.d_dense));
   TG_TRY(upload_vec(pr, P.attn, &pr.d_attn));
   TG_TRY(upload_vec(pr, P.arows, &pr.d_arows));
+  TG_TRY(upload_vec(pr, P.lnorm, &pr.d_lnorm));
+  TG_TRY(upload_vec(pr, P.lnrows, &pr.d_lnrows));
+  TG_TRY(upload_vec(pr, P.lnflag, &pr.d_lnflag));
   const std::uint32_t nc = P.n_uv - P.uv_const_base;
   if (P.dtype == TG_F64) {
     std::vector<double> c(P.uv_init.begin() + P.uv_const_base, P.uv_init.end());
@@ -1195,6 +1245,9 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
   ra.dense = pr.d_dense;
   ra.attn = pr.d_attn;
   ra.arows = pr.d_arows;
+  ra.lnorm = pr.d_lnorm;
+  ra.lnrows = pr.d_lnrows;
+  ra.lnflag = pr.d_lnflag;
   ra.UV = UV;
   ra.inputs = static_cast<const T*>(inputs);
   ra.idx = idx;
@@ -1228,6 +1281,9 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
     ma.dense = pr.d_dense;
     ma.attn = pr.d_attn;
     ma.arows = pr.d_arows;
+    ma.lnorm = pr.d_lnorm;
+    ma.lnrows = pr.d_lnrows;
+    ma.lnflag = pr.d_lnflag;
     ma.UV = UV;
     ma.inputs = static_cast<const T*>(inputs);
     ma.idx = idx;
@@ -1368,6 +1424,7 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
         ra.flags = tgk::kRFwd;
         ra.fwd_begin = stg.begin;
         ra.fwd_end = stg.end;
+        ra.per_sample = stg.macro ? 1 : 0;
         TG_CUDA_TRY(stg.level ? tgk::launch_level_range<T>(ra, st) : tgk::launch_tape_range<T>(ra, st));
         ++pr.launches;
         continue;
@@ -1418,6 +1475,7 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
         ra.flags = tgk::kRBwd;
         ra.bwd_begin = stg.begin;
         ra.bwd_end = stg.end;
+        ra.per_sample = stg.macro ? 1 : 0;
         TG_CUDA_TRY(stg.level ? tgk::launch_level_range<T>(ra, st) : tgk::launch_tape_range<T>(ra, st));
         ++pr.launches;
         continue;
@@ -1630,6 +1688,9 @@ tg_status run_fused(tg_program& pr, const void* inputs, const std::int32_t* idx,
   ma.dense = pr.d_dense;
   ma.attn = pr.d_attn;
   ma.arows = pr.d_arows;
+  ma.lnorm = pr.d_lnorm;
+  ma.lnrows = pr.d_lnrows;
+  ma.lnflag = pr.d_lnflag;
   ma.UV = UV;
   ma.inputs = static_cast<const T*>(inputs);
   ma.idx = idx;
@@ -1721,6 +1782,9 @@ tg_status run_fb(tg_program& pr, const void* inputs, const std::int32_t* idx, st
     ma.dense = pr.d_dense;
     ma.attn = pr.d_attn;
     ma.arows = pr.d_arows;
+    ma.lnorm = pr.d_lnorm;
+    ma.lnrows = pr.d_lnrows;
+    ma.lnflag = pr.d_lnflag;
     ma.UV = UV;
     ma.inputs = static_cast<const T*>(inputs);
     ma.idx = idx;
@@ -2015,6 +2079,7 @@ tg_status tg_program_info_get(tg_program_t p, tg_program_info* info) {
     i.storage = p->staged ? 3 : (p->jit.ok ? 2 : (p->smem ? 0 : 1));
     i.dtype = P.dtype;
     i.n_attn_heads = static_cast<uint32_t>(P.attn.size());
+    i.n_layer_norms = static_cast<uint32_t>(P.lnorm.size());
     *info = i;
     return TG_OK;
   });

@@ -352,6 +352,136 @@ std::vector<AttnGroup> find_attention(const Ctx& c, const std::vector<std::uint3
   return groups;
 }
 
+// ---- layer normalisations in the recorded graph (kLNorm) ----------------------
+// The node pattern of SPEC.md:288-296 built from reference ops (tg_models.hpp
+// layer_norm): mu = meanVarying(x), ms = meanSquaresVarying(x), mu2 = mu^2,
+// var = ms - mu2, ve = var + eps, rstd = invSqrt(ve), and per element
+// c_i = x_i - mu, n_i = c_i * rstd, g_i = n_i * gamma_i, y_i = g_i + beta_i
+// (gamma, beta parameters).  Exact structural match with consumer counts.
+struct LnMatch {
+  std::vector<std::uint32_t> x, nn, y, gamma, beta, interior;
+  std::uint32_t rstd = 0, last_y = 0, first_node = 0;
+  double eps = 0;
+};
+
+std::vector<LnMatch> find_layernorm(const Ctx& c, const std::vector<std::uint32_t>& order) {
+  const tg_tape_desc& d = c.d;
+  const std::uint32_t N = d.n_nodes;
+  std::vector<LnMatch> out;
+  if (!d.leaf_value) return out;
+  constexpr std::uint8_t SqrOp = 7, InvSqrtOp = 11, MeanVaryingOp = 24, MeanSquaresVaryingOp = 26;
+  std::vector<std::uint8_t> pinned(N, 0), reach(N, 0);
+  pinned[d.root] = 1;
+  for (std::uint32_t g = 0; g < d.n_gathers; ++g)
+    for (std::uint32_t r = 0; r < d.gathers[g].n_rows; ++r) pinned[c.cand(g, r)] = 1;
+  for (std::uint32_t nd : order) reach[nd] = 1;
+  std::vector<std::uint32_t> ccount(N, 0), cmin(N, kNone), coff(N + 1, 0), cons;
+  for (std::uint32_t i = 0; i < N; ++i)
+    for (std::uint32_t j = 0; j < c.nkids(i); ++j) {
+      const std::uint32_t k = c.kids(i)[j];
+      if (k & TG_GATHER_FLAG) continue;
+      ++ccount[k];
+      ++coff[k + 1];
+      cmin[k] = std::min(cmin[k], i);
+    }
+  for (std::uint32_t i = 0; i < N; ++i) coff[i + 1] += coff[i];
+  cons.resize(coff[N]);
+  {
+    std::vector<std::uint32_t> fill(coff.begin(), coff.end() - 1);
+    for (std::uint32_t i = 0; i < N; ++i)
+      for (std::uint32_t j = 0; j < c.nkids(i); ++j) {
+        const std::uint32_t k = c.kids(i)[j];
+        if (!(k & TG_GATHER_FLAG)) cons[fill[k]++] = i;
+      }
+  }
+  auto plain = [&](std::uint32_t x) { return !(x & TG_GATHER_FLAG) && x < N; };
+  auto interior_ok = [&](std::uint32_t x) { return plain(x) && c.cls[x] == cSample && !pinned[x]; };
+  auto kid = [&](std::uint32_t i, std::uint32_t j) { return c.kids(i)[j]; };
+  std::vector<std::uint8_t> used(N, 0);
+  for (std::uint32_t mu = 0; mu < N; ++mu) {
+    if (d.op[mu] != MeanVaryingOp || !interior_ok(mu) || used[mu]) continue;
+    const std::uint32_t n = c.nkids(mu);
+    if (n < 2 || ccount[mu] != n + 1) continue;
+    LnMatch M;
+    bool ok = true;
+    for (std::uint32_t i = 0; ok && i < n; ++i) {
+      const std::uint32_t xi = kid(mu, i);
+      ok = plain(xi) && (c.cls[xi] == cSample || c.cls[xi] == cInput);
+      for (std::uint32_t j = 0; ok && j < i; ++j) ok = kid(mu, j) != xi;
+      M.x.push_back(xi);
+    }
+    if (!ok) continue;
+    std::uint32_t ms = kNone, mu2 = kNone;
+    for (std::uint32_t q = coff[M.x[0]]; q < coff[M.x[0] + 1]; ++q) {
+      const std::uint32_t cand = cons[q];
+      if (d.op[cand] != MeanSquaresVaryingOp || c.nkids(cand) != n) continue;
+      bool same = true;
+      for (std::uint32_t i = 0; same && i < n; ++i) same = kid(cand, i) == M.x[i];
+      if (same) ms = cand;
+    }
+    ok = ms != kNone && interior_ok(ms) && ccount[ms] == 1;
+    // consumers of mu: mu^2 and the n centred values (x_i - mu)
+    std::vector<std::uint32_t> cidx(n, kNone);
+    for (std::uint32_t q = coff[mu]; ok && q < coff[mu + 1]; ++q) {
+      const std::uint32_t u = cons[q];
+      if (d.op[u] == SqrOp && c.nkids(u) == 1) {
+        ok = mu2 == kNone;
+        mu2 = u;
+        continue;
+      }
+      ok = d.op[u] == Sub && c.nkids(u) == 2 && kid(u, 1) == mu;
+      std::uint32_t i = 0;
+      while (ok && i < n && M.x[i] != kid(u, 0)) ++i;
+      ok = ok && i < n && cidx[i] == kNone;
+      if (ok) cidx[i] = u;
+    }
+    ok = ok && mu2 != kNone && interior_ok(mu2) && ccount[mu2] == 1;
+    if (!ok) continue;
+    const std::uint32_t var = cons[coff[mu2]];
+    ok = interior_ok(var) && d.op[var] == Sub && kid(var, 0) == ms && kid(var, 1) == mu2 && ccount[var] == 1 &&
+         cons[coff[ms]] == var;
+    if (!ok) continue;
+    const std::uint32_t ve = cons[coff[var]];
+    ok = interior_ok(ve) && d.op[ve] == Add && kid(ve, 0) == var && plain(kid(ve, 1)) && c.cls[kid(ve, 1)] == cConst &&
+         d.op[kid(ve, 1)] == Leaf && ccount[ve] == 1;
+    if (!ok) continue;
+    M.eps = d.leaf_value[kid(ve, 1)];
+    const std::uint32_t rstd = cons[coff[ve]];
+    ok = interior_ok(rstd) && d.op[rstd] == InvSqrtOp && ccount[rstd] == n;
+    for (std::uint32_t i = 0; ok && i < n; ++i) {
+      const std::uint32_t ci = cidx[i];
+      ok = ci != kNone && interior_ok(ci) && ccount[ci] == 1;
+      if (!ok) break;
+      const std::uint32_t ni = cons[coff[ci]];
+      ok = interior_ok(ni) && reach[ni] && d.op[ni] == Mul && kid(ni, 0) == ci && kid(ni, 1) == rstd && ccount[ni] == 1;
+      if (!ok) break;
+      const std::uint32_t gi = cons[coff[ni]];
+      ok = interior_ok(gi) && d.op[gi] == Mul && kid(gi, 0) == ni && plain(kid(gi, 1)) && c.cls[kid(gi, 1)] == cParam &&
+           ccount[gi] == 1;
+      if (!ok) break;
+      const std::uint32_t yi = cons[coff[gi]];
+      ok = plain(yi) && c.cls[yi] == cSample && !pinned[yi] && reach[yi] && d.op[yi] == Add && kid(yi, 0) == gi &&
+           plain(kid(yi, 1)) && c.cls[kid(yi, 1)] == cParam;
+      if (!ok) break;
+      M.nn.push_back(ni);
+      M.y.push_back(yi);
+      M.gamma.push_back(d.leaf_index[kid(gi, 1)]);
+      M.beta.push_back(d.leaf_index[kid(yi, 1)]);
+      M.interior.push_back(ci);
+      M.interior.push_back(gi);
+      M.last_y = std::max(M.last_y, yi);
+    }
+    for (std::uint32_t i = 0; ok && i < n; ++i) ok = cmin[M.y[i]] == kNone || cmin[M.y[i]] > M.last_y;
+    if (!ok) continue;
+    M.rstd = rstd;
+    M.interior.insert(M.interior.end(), {mu, ms, mu2, var, ve, rstd});
+    M.first_node = *std::min_element(M.interior.begin(), M.interior.end());
+    for (std::uint32_t x : M.interior) used[x] = 1;
+    out.push_back(std::move(M));
+  }
+  return out;
+}
+
 }  // namespace
 
 Program compile(const tg_tape_desc& d) {
@@ -396,6 +526,18 @@ Program compile(const tg_tape_desc& d) {
       for (std::uint32_t x : U.interior) { attn_of[x] = static_cast<std::int32_t>(g); attn_interior[x] = 1; }
       for (std::uint32_t x : U.o) attn_of[x] = static_cast<std::int32_t>(g);
     }
+
+  std::vector<LnMatch> lns = find_layernorm(c, processing_order(c));
+  std::vector<std::int32_t> ln_of(d.n_nodes, -1);        // interior, n_i and y_i nodes -> instance
+  for (std::size_t g = 0; g < lns.size(); ++g) {
+    bool clash = false;   // an attention head already owns one of its nodes
+    for (std::uint32_t x : lns[g].interior) clash = clash || attn_of[x] >= 0;
+    for (std::uint32_t x : lns[g].y) clash = clash || attn_of[x] >= 0;
+    if (clash) { lns[g].x.clear(); continue; }
+    for (std::uint32_t x : lns[g].interior) { ln_of[x] = static_cast<std::int32_t>(g); attn_interior[x] = 1; }
+    for (std::uint32_t x : lns[g].nn) ln_of[x] = static_cast<std::int32_t>(g);
+    for (std::uint32_t x : lns[g].y) ln_of[x] = static_cast<std::int32_t>(g);
+  }
 
   // ---- per-sample rows -------------------------------------------------------
   c.row.assign(d.n_nodes, kNone);
@@ -499,6 +641,28 @@ Program compile(const tg_tape_desc& d) {
       for (std::uint32_t x : U.o) attn_of[x] = -1;
     }
   }
+  std::vector<std::uint32_t> ln_id(lns.size(), kNone);
+  for (std::size_t g = 0; g < lns.size(); ++g) {
+    const LnMatch& M = lns[g];
+    if (M.x.empty()) continue;
+    LNorm L{};
+    L.n = static_cast<std::uint32_t>(M.x.size());
+    L.off = static_cast<std::uint32_t>(P.lnrows.size());
+    for (std::uint32_t x : M.x) P.lnrows.push_back(c.row[x]);
+    for (std::uint32_t x : M.nn) P.lnrows.push_back(c.row[x]);
+    for (std::uint32_t x : M.y) P.lnrows.push_back(c.row[x]);
+    P.lnrows.insert(P.lnrows.end(), M.gamma.begin(), M.gamma.end());
+    P.lnrows.insert(P.lnrows.end(), M.beta.begin(), M.beta.end());
+    L.flag_off = static_cast<std::uint32_t>(P.lnflag.size());
+    P.lnflag.resize(P.lnflag.size() + L.n, 0);
+    L.rstd_node = M.rstd;
+    L.first_node = M.first_node;
+    L.n_nodes = static_cast<std::uint32_t>(M.interior.size() + 2 * M.x.size());
+    L.eps = M.eps;
+    ln_id[g] = static_cast<std::uint32_t>(P.lnorm.size());
+    P.lnorm.push_back(L);
+    P.n_sample_nodes += static_cast<std::uint32_t>(M.interior.size());
+  }
   std::vector<std::uint32_t> attn_id(agroups.size(), kNone);
   for (std::size_t g = 0; g < agroups.size(); ++g) {
     const AttnGroup& G = agroups[g];
@@ -544,6 +708,14 @@ Program compile(const tg_tape_desc& d) {
   std::vector<std::uint32_t> uinstr_of(d.n_nodes, kNone);  // uniform node -> ufwd index
   for (std::uint32_t i = 0; i < d.n_nodes; ++i) {
     if (c.cls[i] != cSample && c.cls[i] != cUniform) continue;
+    if (ln_of[i] >= 0) {     // fused layer norm: one instruction where its last output stood
+      const LnMatch& M = lns[ln_of[i]];
+      if (i == M.last_y) {
+        const LNorm& L = P.lnorm[ln_id[ln_of[i]]];
+        P.fwd.push_back(Instr{kLNorm, 0, 0, P.lnrows[L.off + 2 * L.n], 0, 0, ln_id[ln_of[i]], L.first_node, L.eps});
+      }
+      continue;
+    }
     if (attn_of[i] >= 0) {   // fused head: one instruction where its last output node stood
       const AttnGroup& G = agroups[attn_of[i]];
       if (i == G.last_o) {
@@ -601,6 +773,8 @@ Program compile(const tg_tape_desc& d) {
       }
     }
     if (c.cls[d.root] == cSample) uses[c.row[d.root]] += 2;
+    for (const LNorm& L : P.lnorm)   // rows read by fused layer norms
+      for (std::uint32_t i = 0; i < L.n; ++i) uses[P.lnrows[L.off + i]] += 2;
     for (const Attn& A : P.attn) {   // rows read by fused heads
       for (std::uint32_t u = 0; u < A.n_units; ++u)
         for (std::uint32_t i = 0; i < A.hd; ++i) uses[P.arows[A.unit_off + 3 * u] + i] += 2;
@@ -706,12 +880,30 @@ Program compile(const tg_tape_desc& d) {
   // processing order stood (every output adjoint is final there; the q / k / v
   // producers, children of head nodes, all come later); it is the only pusher
   // into its q / k / v rows and stores them
-  std::vector<std::uint32_t> attn_left(agroups.size(), 0);
-  for (std::uint32_t node : P.order)
+  std::vector<std::uint32_t> attn_left(agroups.size(), 0), ln_left(lns.size(), 0);
+  for (std::uint32_t node : P.order) {
     if (attn_of[node] >= 0) ++attn_left[attn_of[node]];
+    if (ln_of[node] >= 0) ++ln_left[ln_of[node]];
+  }
   for (std::uint32_t node : P.order) {
     if (c.cls[node] == cUniform) { P.ubwd.push_back(P.ufwd[uinstr_of[node]]); continue; }
     if (c.cls[node] != cSample) continue;
+    if (ln_of[node] >= 0) {
+      if (--ln_left[ln_of[node]] > 0) continue;
+      const std::uint32_t id = ln_id[ln_of[node]];
+      const LNorm& L = P.lnorm[id];
+      P.bwd.push_back(Instr{kLNorm, 0, 0, P.lnrows[L.off + 2 * L.n], 0, 0, id, L.first_node, L.eps});
+      for (std::uint32_t i = 0; i < L.n; ++i) {
+        const std::uint32_t xr = P.lnrows[L.off + i];
+        if (!written[xr]) { P.lnflag[L.flag_off + i] |= kAssign; written[xr] = 1; }
+        // gamma_i: sum_s dy_i n_i (the adjoint of n_i * gamma_i equals dy_i); beta_i: sum_s dy_i
+        const std::uint32_t yr = P.lnrows[L.off + 2 * L.n + i], nr = P.lnrows[L.off + L.n + i];
+        const std::uint32_t gu = P.lnrows[L.off + 3 * L.n + i], bu = P.lnrows[L.off + 4 * L.n + i];
+        pend.push_back({gu, Term{yr, nr, -1, 0, 1.0}});
+        pend.push_back({bu, Term{yr, kNone, -1, 0, 1.0}});
+      }
+      continue;
+    }
     if (attn_of[node] >= 0) {
       if (--attn_left[attn_of[node]] > 0) continue;
       const std::uint32_t id = attn_id[attn_of[node]];
@@ -821,7 +1013,7 @@ Program compile(const tg_tape_desc& d) {
   // adjoint", keeping the original order wherever it is valid (Kahn's
   // algorithm, smallest original index first), then recompute the first-write
   // (assign) flags and the rows that must start at zero for the new order.
-  if (!P.attn.empty()) {
+  if (!P.attn.empty() || !P.lnorm.empty()) {
     const std::size_t NB = P.bwd.size();
     std::vector<std::uint32_t> reader(nrow, kNone);   // reverse instruction reading each row's adjoint
     std::vector<std::vector<std::uint32_t>> pushes(NB);
@@ -829,7 +1021,13 @@ Program compile(const tg_tape_desc& d) {
     for (std::uint32_t k = 0; k < NB; ++k) {
       const Instr& in = P.bwd[k];
       rows.clear();
-      if (in.kind == kAttn) {
+      if (in.kind == kLNorm) {
+        const LNorm& L = P.lnorm[in.aux];
+        for (std::uint32_t i = 0; i < L.n; ++i) {
+          reader[P.lnrows[L.off + 2 * L.n + i]] = k;
+          rows.push_back(P.lnrows[L.off + i]);
+        }
+      } else if (in.kind == kAttn) {
         const Attn& A = P.attn[in.aux];
         for (std::uint32_t u = 0; u < A.n_units; ++u) {
           for (std::uint32_t i = 0; i < A.dv; ++i) reader[P.arows[A.unit_off + 3 * u + 1] + i] = k;
@@ -891,7 +1089,14 @@ Program compile(const tg_tape_desc& d) {
         if (!written[r]) { P.oflag[pos] |= kAssign; written[r] = 1; }
         else P.oflag[pos] &= static_cast<std::uint8_t>(~kAssign);
       };
-      if (in.kind == kAttn) {
+      if (in.kind == kLNorm) {
+        const LNorm& L = P.lnorm[in.aux];
+        for (std::uint32_t i = 0; i < L.n; ++i) {
+          const std::uint32_t r = P.lnrows[L.off + i];
+          if (!written[r]) { P.lnflag[L.flag_off + i] |= kAssign; written[r] = 1; }
+          else P.lnflag[L.flag_off + i] &= static_cast<std::uint8_t>(~kAssign);
+        }
+      } else if (in.kind == kAttn) {
         std::vector<std::uint32_t> rr;
         const Attn& A = P.attn[in.aux];
         for (std::uint32_t u = 0; u < A.n_units; ++u)

@@ -724,7 +724,7 @@ FuseCode fuse_code(const tgc::Program& P, const JitConfig& cfg, const std::strin
 }
 
 bool eligible(const tgc::Program& P) {
-  return P.root_row != kNone && P.n_edges <= kMaxEdges && P.n_rows <= 4096 && P.attn.empty();   // no kAttn codegen
+  return P.root_row != kNone && P.n_edges <= kMaxEdges && P.n_rows <= 4096 && P.attn.empty() && P.lnorm.empty();   // no kAttn / kLNorm codegen
 }
 
 std::string generate(const tgc::Program& P, const JitConfig& cfg, unsigned& n_crow_g, unsigned& n_crow_v,

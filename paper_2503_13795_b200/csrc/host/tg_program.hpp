@@ -43,6 +43,7 @@ enum InstrKind : std::uint8_t {
   kGatherLoad = 2,  // V[out] = UV[table[idx[col][s]]]   (aux = uniform gather id)
   kDense = 3,       // rows [out, out+n_out) = W x + b   (aux = dense id)
   kAttn = 4,        // softmax attention head over per-sample rows (aux = attn id)
+  kLNorm = 5,       // layer normalisation of n per-sample rows (aux = lnorm id)
 };
 
 // Operand flags for the reverse sweep.
@@ -120,6 +121,20 @@ struct Attn {
   double scale;
 };
 
+// Layer normalisation recognised in the recorded graph (the SPEC.md:288-296
+// composition out of reference ops):
+//   mu = mean(x), ms = meanSquares(x), var = ms - mu^2, rstd = invSqrt(var + eps),
+//   n_i = (x_i - mu) * rstd,  y_i = n_i * gamma_i + beta_i.
+// One macro-instruction; the scalar statistics and c_i, n_i * gamma_i get no
+// rows; n_i keeps its row (the gamma gradient term reads it).  lnrows[off ..]
+// holds five lists of n: x rows, n rows, y rows, gamma uv, beta uv.  The x
+// adjoints are pushes like a dense layer's: lnflag[flag_off + i] & kAssign.
+struct LNorm {
+  std::uint32_t n, off, flag_off;
+  std::uint32_t rstd_node, first_node, n_nodes;
+  double eps;
+};
+
 struct GatherTable {          // candidate list of one gather
   std::uint32_t col;          // index column
   std::uint32_t n_rows;
@@ -148,6 +163,9 @@ struct Program {
   std::vector<Dense> dense;
   std::vector<Attn> attn;
   std::vector<std::uint32_t> arows;
+  std::vector<LNorm> lnorm;
+  std::vector<std::uint32_t> lnrows;
+  std::vector<std::uint8_t> lnflag;
 
   // gathers
   std::vector<GatherTable> ugather;       // sample-invariant tables (materialised)

@@ -268,6 +268,74 @@ __device__ void attn_bwd_sample(const tgc::Attn A, const std::uint32_t* __restri
   }
 }
 
+// ---- fused layer normalisation (kLNorm, tg_program.hpp LNorm), per sample ----
+// Forward as the nodes it replaces: mu = sum(x)/n, ms = sum(x^2)/n,
+// var = ms - mu*mu, rstd = 1/sqrt(var + eps) (invSqrt domain check: the
+// reference's std::domain_error), n_i = (x_i - mu) * rstd, y_i = n_i g_i + b_i.
+// Reverse, node by node: dn_i = dy_i g_i, dc_i = dn_i rstd,
+// drstd = sum_i dn_i c_i, dve = -drstd rstd / (2 ve), dms = dve, dmu2 = -dve,
+// dmu = -sum_i dc_i + 2 mu dmu2, dx_i += dc_i + (2 dms / n) x_i + dmu / n.
+// The gamma / beta gradients are batch terms over dy and n (compiler).
+template <class T>
+__device__ __forceinline__ void ln_stats(const tgc::LNorm& L, const std::uint32_t* __restrict__ lr, const T* V,
+                                         std::size_t ld, std::size_t col, T& mu, T& ve) {
+  T s1 = 0, s2 = 0;
+#pragma unroll 8
+  for (std::uint32_t i = 0; i < L.n; ++i) {
+    const T x = V[std::size_t(lr[L.off + i]) * ld + col];
+    s1 += x;
+    s2 += x * x;
+  }
+  mu = s1 / static_cast<T>(L.n);
+  const T ms = s2 / static_cast<T>(L.n);
+  ve = (ms - mu * mu) + static_cast<T>(L.eps);
+}
+
+template <class T>
+__device__ bool ln_fwd_sample(const tgc::LNorm L, const std::uint32_t* __restrict__ lr, const T* __restrict__ UV, T* V,
+                              std::size_t ld, std::size_t col) {
+  T mu, ve;
+  ln_stats<T>(L, lr, V, ld, col, mu, ve);
+  const bool bad = !(ve > T(0));
+  const T rstd = T(1) / d_sqrt(ve);
+#pragma unroll 4
+  for (std::uint32_t i = 0; i < L.n; ++i) {
+    const T x = V[std::size_t(lr[L.off + i]) * ld + col];
+    const T nv = (x - mu) * rstd;
+    V[std::size_t(lr[L.off + L.n + i]) * ld + col] = nv;
+    V[std::size_t(lr[L.off + 2 * L.n + i]) * ld + col] = nv * UV[lr[L.off + 3 * L.n + i]] + UV[lr[L.off + 4 * L.n + i]];
+  }
+  return bad;
+}
+
+template <class T>
+__device__ void ln_bwd_sample(const tgc::LNorm L, const std::uint32_t* __restrict__ lr, const std::uint8_t* __restrict__ lf,
+                              const T* __restrict__ UV, const T* V, T* G, std::size_t ld, std::size_t col) {
+  T mu, ve;
+  ln_stats<T>(L, lr, V, ld, col, mu, ve);
+  const T rstd = T(1) / d_sqrt(ve);
+  T drstd = 0, sdc = 0;
+#pragma unroll 4
+  for (std::uint32_t i = 0; i < L.n; ++i) {
+    const T dn = G[std::size_t(lr[L.off + 2 * L.n + i]) * ld + col] * UV[lr[L.off + 3 * L.n + i]];
+    const T cval = V[std::size_t(lr[L.off + i]) * ld + col] - mu;
+    drstd += dn * cval;
+    sdc += dn * rstd;
+  }
+  const T dve = -drstd * rstd / (T(2) * ve);
+  const T dms = dve;
+  const T dmu = -sdc + (-dve) * T(2) * mu;
+  const T cx = dms * T(2) / static_cast<T>(L.n), cm = dmu / static_cast<T>(L.n);
+#pragma unroll 4
+  for (std::uint32_t i = 0; i < L.n; ++i) {
+    const T dc = G[std::size_t(lr[L.off + 2 * L.n + i]) * ld + col] * UV[lr[L.off + 3 * L.n + i]] * rstd;
+    const T x = V[std::size_t(lr[L.off + i]) * ld + col];
+    const T dx = dc + cx * x + cm;
+    T* p = &G[std::size_t(lr[L.off + i]) * ld + col];
+    *p = (lf[L.flag_off + i] & tgc::kAssign) ? dx : *p + dx;
+  }
+}
+
 // Fused activations of kDense groups (domain-free unary ops only); same
 // formulas as eval_node / propagate above.
 template <class T>

@@ -89,6 +89,10 @@ __device__ __forceinline__ void fwd_instr(const RangeArgs<T>& a, RowAccS<T>& acc
   } else if (in.kind == tgc::kAttn) {
     attn_fwd_sample<T>(a.attn[in.aux], a.arows, V, ld, col);
     return;
+  } else if (in.kind == tgc::kLNorm) {
+    const tgc::LNorm L = a.lnorm[in.aux];
+    if (ln_fwd_sample<T>(L, a.lnrows, a.UV, V, ld, col)) record_error(a.err_key, s, L.rstd_node);
+    return;
   } else if (in.kind == tgc::kDense) {
     const tgc::Dense D = a.dense[in.aux];
     const std::uint32_t* xo = a.opnd + D.x_opnd;
@@ -118,6 +122,10 @@ __device__ __forceinline__ void bwd_instr(const RangeArgs<T>& a, RowAccS<T>& acc
   const Instr in = a.bwd[k];
   if (in.kind == tgc::kAttn) {
     attn_bwd_sample<T>(a.attn[in.aux], a.arows, V, G, ld, col);
+    return;
+  }
+  if (in.kind == tgc::kLNorm) {
+    ln_bwd_sample<T>(a.lnorm[in.aux], a.lnrows, a.lnflag, a.UV, V, G, ld, col);
     return;
   }
   if (in.kind == tgc::kDense) {
@@ -779,7 +787,7 @@ cudaError_t launch_level_range(const RangeArgs<T>& a, cudaStream_t st) {
   if (a.n == 0 || count == 0) return cudaSuccess;
   if constexpr (std::is_same_v<T, float>) {
     static const bool vec = !(std::getenv("TG_LEVEL4") && std::getenv("TG_LEVEL4")[0] == '0');
-    if (vec && a.ld % 4 == 0 && (reinterpret_cast<std::uintptr_t>(a.V) & 15) == 0 &&
+    if (vec && !a.per_sample && a.ld % 4 == 0 && (reinterpret_cast<std::uintptr_t>(a.V) & 15) == 0 &&
         (reinterpret_cast<std::uintptr_t>(a.G) & 15) == 0) {
       // instructions per CTA: kLvInstr (one load group) while the launch keeps
       // >= ~16 CTAs per SM, else one (few-instruction levels, e.g. the

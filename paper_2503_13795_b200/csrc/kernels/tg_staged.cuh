@@ -37,6 +37,9 @@ struct RangeArgs {
   const tgc::Dense* dense;
   const tgc::Attn* attn;
   const std::uint32_t* arows;
+  const tgc::LNorm* lnorm;
+  const std::uint32_t* lnrows;
+  const std::uint8_t* lnflag;
   const T* UV;
   const T* inputs;
   const std::int32_t* idx;
@@ -51,6 +54,7 @@ struct RangeArgs {
   std::size_t ld;         // row stride of V / G (chunk capacity)
   std::uint32_t fwd_begin, fwd_end, bwd_begin, bwd_end;
   std::uint32_t n_zero, n_inputs, root_row, flags;
+  std::uint32_t per_sample;   // level stages of macro-instructions (layer norms ...): one sample per thread
 };
 
 // C(m, n) = sum_k A(m, k) B(k, n) over an operand view:

@@ -127,6 +127,19 @@ __global__ void __launch_bounds__(256) k_tape(MainArgs<T> a) {
         } else if (in.kind == tgc::kAttn) {
           attn_fwd_sample<T>(a.attn[in.aux], a.arows, V, ld, col);
           continue;
+        } else if (in.kind == tgc::kLNorm) {
+          const tgc::LNorm L = a.lnorm[in.aux];
+          if (ln_fwd_sample<T>(L, a.lnrows, a.UV, V, ld, col)) {
+            record_error(a.err_key, s, L.rstd_node);
+            if (diag && !seen_bad) {
+              seen_bad = true;
+              *a.err_op = 11;   // invSqrt
+              T mu, ve;
+              ln_stats<T>(L, a.lnrows, V, ld, col, mu, ve);
+              *a.err_val = static_cast<double>(ve);
+            }
+          }
+          continue;
         } else if (in.kind == tgc::kDense) {  // dense layer: z_j = b_j + <x, W[j]>, h_j = act(z_j)
           const tgc::Dense D = a.dense[in.aux];
           const std::uint32_t* xo = a.opnd + D.x_opnd;
@@ -155,6 +168,10 @@ __global__ void __launch_bounds__(256) k_tape(MainArgs<T> a) {
         const Instr in = a.bwd[k];
         if (in.kind == tgc::kAttn) {
           attn_bwd_sample<T>(a.attn[in.aux], a.arows, V, G, ld, col);
+          continue;
+        }
+        if (in.kind == tgc::kLNorm) {
+          ln_bwd_sample<T>(a.lnorm[in.aux], a.lnrows, a.lnflag, a.UV, V, G, ld, col);
           continue;
         }
         if (in.kind == tgc::kDense) {

@@ -28,6 +28,9 @@ struct MainArgs {
   const tgc::Dense* dense;
   const tgc::Attn* attn;
   const std::uint32_t* arows;
+  const tgc::LNorm* lnorm;
+  const std::uint32_t* lnrows;
+  const std::uint8_t* lnflag;
   const T* UV;
   const T* inputs;
   const std::int32_t* idx;

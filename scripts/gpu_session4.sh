@@ -1,4 +1,4 @@
-O=gpurun_out/s12
+O=gpurun_out/s15
 mkdir -p $O
 timeout 1500 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $O/pytest_gpu.log
 for c in cfg3 cfg4 cfg5; do

@@ -133,7 +133,7 @@ def test_gpt_cfg4_dims_vs_oracle(batch_env, attn_fast):
     try:
         prog = tg.Program(desc)
         L, IG, G = run(prog, desc, x, k, desc.param_values(), b, want_igrad=False)
-        assert prog.info["storage"] == 3 and prog.info["n_attn_heads"] == 16
+        assert prog.info["storage"] == 3 and prog.info["n_attn_heads"] == 16 and prog.info["n_layer_norms"] == 9 * 64
     finally:
         os.environ.pop("TG_STAGED_BATCH")
         os.environ.pop("TG_ATTN_FAST")
