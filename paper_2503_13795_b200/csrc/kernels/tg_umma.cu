@@ -481,7 +481,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_umma_tma(GemmArgs<float> g, co
     const int cw = (tid - 64) >> 5;   // converter warp 0..7
     const std::uint32_t n = n0 + 4 * lane;
     const bool vec = (g.ldc % 4 == 0) && (g.epi != kEpiSplitK || g.N % 4 == 0);
-    for (int r = cw; r < BM; r += kConvThreads / 32) {
+    for (int r = cw; r < BM && g_umma_exp != 5; r += kConvThreads / 32) {   // (ablation 5: no output stores)
       const std::uint32_t m = m0 + r;
       if (m >= g.M || n >= g.N) continue;
       const float4 v = *reinterpret_cast<const float4*>(tile + r * kLd + 4 * lane);
@@ -522,6 +522,257 @@ __global__ void __launch_bounds__(kTThreads, 1) k_umma_tma(GemmArgs<float> g, co
       }
       if (vec && cnt == 4) *reinterpret_cast<float4*>(dst) = make_float4(a4[0], a4[1], a4[2], a4[3]);
       else for (int e = 0; e < cnt; ++e) dst[e] = a4[e];
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * BN));
+}
+
+// ---------------------------------------------------------------------------
+// Persistent variant (k_umma_tma_p) for short reductions.  With K <= 256 a
+// 128 x 128 tile is 2-8 k-tiles: measured on cfg4's shapes, a CTA spent
+// ~6 us per tile of which the MMAs were well under one (prologue, first TMA
+// round trip, drain, epilogue; ablations in scripts/gemm_bench.py).  Here a
+// CTA per SM walks tiles L = blockIdx.x, + gridDim.x, ... (M fastest, then
+// N, then the z slice / batch member); the k-tile and accumulation-group
+// counters run on across tiles, so the TMA producer prefetches the next
+// tile's operands while the converter warps drain and store the current one,
+// and the prologue is paid once.  The epilogue tile has its own shared
+// memory (two ring stages + epilogue tile).
+constexpr int kPStages = 2;
+__host__ __device__ constexpr std::uint32_t persist_smem() {
+  return kPStages * kTStage + BM * (BN + 4) * 4 + 1024 + 512;
+}
+
+__global__ void __launch_bounds__(kTThreads, 1) k_umma_tma_p(GemmArgs<float> g, const __grid_constant__ CUtensorMap tmA,
+                                                      const __grid_constant__ CUtensorMap tmB, int a_mn, int b_mn,
+                                                      std::uint32_t mt, std::uint32_t nt, std::uint32_t n_tiles) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  float* etile = reinterpret_cast<float*>(smem + kPStages * kTStage);
+  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + persist_smem() - 1024 - 512);
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 3 * kPStages + 4);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  auto full = [&](int s) { return smem_u32(&bars[s]); };
+  auto conv = [&](int s) { return smem_u32(&bars[kPStages + s]); };
+  auto empty = [&](int s) { return smem_u32(&bars[2 * kPStages + s]); };
+  auto tfull = [&](int b) { return smem_u32(&bars[3 * kPStages + b]); };
+  auto tempty = [&](int b) { return smem_u32(&bars[3 * kPStages + 2 + b]); };
+  if (tid == 0) {
+    for (int s = 0; s < kPStages; ++s) {
+      mbar_init(full(s), 1);
+      mbar_init(conv(s), kConvThreads);
+      mbar_init(empty(s), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull(b), 1);
+      mbar_init(tempty(b), kConvThreads);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "n"(2 * BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const std::uint32_t tmem = *tmem_slot;
+
+  struct Tile {
+    int m0, n0, a_off, b_off;
+    std::size_t c_off, c2_off;
+    std::uint32_t z, k_begin, T;
+  };
+  auto tile_of = [&](std::uint32_t L) {
+    Tile t;
+    const std::uint32_t mi = L % mt, ni = (L / mt) % nt, z = L / (mt * nt);
+    t.m0 = static_cast<int>(mi) * BM;
+    t.n0 = static_cast<int>(ni) * BN;
+    t.z = z;
+    std::uint32_t slice = z;
+    t.a_off = t.b_off = 0;
+    t.c_off = t.c2_off = 0;
+    if (g.mem) {
+      const uint4 e = g.mem[z / g.zs];
+      slice = z % g.zs;
+      t.a_off = static_cast<int>(e.x);
+      t.b_off = static_cast<int>(e.y);
+      t.c_off = e.z;
+      t.c2_off = e.w;
+    }
+    std::uint32_t k_end = g.K;
+    t.k_begin = 0;
+    if (g.epi == kEpiSplitK) {
+      t.k_begin = slice * g.k_chunk;
+      k_end = min(g.K, t.k_begin + g.k_chunk);
+    }
+    t.T = k_end > t.k_begin ? (k_end - t.k_begin + BK - 1) / BK : 0;
+    return t;
+  };
+
+  if (warp == 0) {
+    // ===== TMA producer =====
+    if (lane == 0) {
+      std::uint32_t gt = 0;
+      for (std::uint32_t L = blockIdx.x; L < n_tiles; L += gridDim.x) {
+        const Tile tl = tile_of(L);
+        for (std::uint32_t t = 0; t < tl.T; ++t, ++gt) {
+          const int s = gt % kPStages;
+          if (gt >= static_cast<std::uint32_t>(kPStages)) mbar_wait2(empty(s), ((gt / kPStages) - 1) & 1);
+          const std::uint32_t base = smem_u32(smem + s * kTStage);
+          mbar_expect_tx(full(s), 2 * kTTile);
+          const int k0 = static_cast<int>(tl.k_begin + t * BK);
+          tma_operand(&tmA, a_mn, base, tl.m0, k0, tl.a_off, full(s));
+          tma_operand(&tmB, b_mn, base + 2 * kTTile, tl.n0, k0, tl.b_off, full(s));
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer (one accumulation group per k-tile) =====
+    const std::uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (std::uint32_t(a_mn) << 15) |
+                                (std::uint32_t(b_mn) << 16) | ((BN >> 3) << 17) | ((BM >> 4) << 24);
+    std::uint32_t gt = 0;
+    for (std::uint32_t L = blockIdx.x; L < n_tiles; L += gridDim.x) {
+      const Tile tl = tile_of(L);
+      for (std::uint32_t t = 0; t < tl.T; ++t, ++gt) {
+        const int s = gt % kPStages;
+        const int buf = gt & 1;
+        if (gt >= 2) mbar_wait2(tempty(buf), ((gt >> 1) - 1) & 1);
+        mbar_wait2(conv(s), (gt / kPStages) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (lane == 0) {
+          const std::uint32_t a_hi = smem_u32(smem + s * kTStage), a_lo = a_hi + kTTile;
+          const std::uint32_t b_hi = a_hi + 2 * kTTile, b_lo = a_hi + 3 * kTTile;
+          const std::uint32_t td = tmem + buf * BN;
+#pragma unroll
+          for (int ks = 0; ks < BK / 8; ++ks) {
+            const std::uint64_t dAh = operand_desc(a_hi, a_mn, ks), dAl = operand_desc(a_lo, a_mn, ks);
+            const std::uint64_t dBh = operand_desc(b_hi, b_mn, ks), dBl = operand_desc(b_lo, b_mn, ks);
+            mma_tf32(td, dAl, dBh, idesc, ks != 0 ? 1u : 0u);
+            mma_tf32(td, dAh, dBl, idesc, 1u);
+            mma_tf32(td, dAh, dBh, idesc, 1u);
+          }
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(empty(s)));
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(tfull(buf)));
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ===== converters + drain + epilogue =====
+    const int ct = tid - 64;
+    const int wq = warp & 3;
+    const int c0 = ((warp - 2) >> 2) * (BN / 2);
+    constexpr int kCols = BN / 2;
+    constexpr int kLd = BN + 4;
+    const int cw = (tid - 64) >> 5;
+    float acc[kCols];
+    auto drain = [&](std::uint32_t grp) {
+      const int buf = grp & 1;
+      mbar_wait2(tfull(buf), (grp >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+      for (int c = 0; c < kCols; c += 16) {
+        std::uint32_t r[16];
+        const std::uint32_t taddr = tmem + buf * BN + (static_cast<std::uint32_t>(wq * 32) << 16) + c0 + c;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+              "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[c + j] += __uint_as_float(r[j]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      mbar_arrive(tempty(buf));
+    };
+    std::uint32_t gt = 0;
+    for (std::uint32_t L = blockIdx.x; L < n_tiles; L += gridDim.x) {
+      const Tile tl = tile_of(L);
+#pragma unroll
+      for (int j = 0; j < kCols; ++j) acc[j] = 0.f;
+      for (std::uint32_t t = 0; t < tl.T; ++t, ++gt) {
+        const int s = gt % kPStages;
+        mbar_wait2(full(s), (gt / kPStages) & 1);
+        unsigned char* base = smem + s * kTStage;
+#pragma unroll
+        for (int op = 0; op < 2; ++op) {
+          float4* hi = reinterpret_cast<float4*>(base + op * 2 * kTTile);
+          float4* lo = reinterpret_cast<float4*>(base + op * 2 * kTTile + kTTile);
+#pragma unroll 4
+          for (int i = ct; i < static_cast<int>(kTTile / 16); i += kConvThreads) {
+            const float4 x = hi[i];
+            float4 h, l;
+            h.x = tf32_rna(x.x); l.x = tf32_rna(x.x - h.x);
+            h.y = tf32_rna(x.y); l.y = tf32_rna(x.y - h.y);
+            h.z = tf32_rna(x.z); l.z = tf32_rna(x.z - h.z);
+            h.w = tf32_rna(x.w); l.w = tf32_rna(x.w - h.w);
+            hi[i] = h;
+            lo[i] = l;
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;");
+        mbar_arrive(conv(s));
+        if (t > 0) drain(gt - 1);
+      }
+      if (tl.T > 0) drain(gt - 1);
+      // epilogue through the dedicated tile (the previous tile's row stores are done)
+      asm volatile("bar.sync 1, %0;" ::"n"(kConvThreads));
+      {
+        const int r = wq * 32 + lane;
+#pragma unroll
+        for (int j = 0; j < kCols; j += 4)
+          *reinterpret_cast<float4*>(etile + r * kLd + c0 + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kConvThreads));
+      const std::uint32_t n = tl.n0 + 4 * lane;
+      const bool vec = (g.ldc % 4 == 0) && (g.epi != kEpiSplitK || g.N % 4 == 0);
+      for (int r = cw; r < BM; r += kConvThreads / 32) {
+        const std::uint32_t m = tl.m0 + r;
+        if (m >= g.M || n >= g.N) continue;
+        const float4 v = *reinterpret_cast<const float4*>(etile + r * kLd + 4 * lane);
+        float a4[4] = {v.x, v.y, v.z, v.w};
+        float* dst = g.epi == kEpiSplitK ? g.C + (std::size_t(tl.z) * g.M + m) * g.N + n : g.C + (tl.c_off + m) * g.ldc + n;
+        const int cnt = min(4u, g.N - n);
+        if (g.epi == kEpiBiasAct) {
+          const float bv = g.bias ? g.bias[m] : 0.f;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) a4[e] += bv;
+          if (g.act) {
+            float h4[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) h4[e] = act_fwd<float>(g.act, a4[e]);
+            float* d2 = g.C2 + (tl.c2_off + m) * g.ldc + n;
+            if (vec && cnt == 4) *reinterpret_cast<float4*>(d2) = make_float4(h4[0], h4[1], h4[2], h4[3]);
+            else for (int e = 0; e < cnt; ++e) d2[e] = h4[e];
+          }
+        } else if (g.epi == kEpiAccum && g.dact) {
+          const float* hp = g.C2 + (tl.c2_off + m) * g.ldc + n;
+          float h4[4] = {0.f, 0.f, 0.f, 0.f};
+          if (vec && cnt == 4) {
+            const float4 o = *reinterpret_cast<const float4*>(hp);
+            h4[0] = o.x; h4[1] = o.y; h4[2] = o.z; h4[3] = o.w;
+          } else {
+            for (int e = 0; e < cnt; ++e) h4[e] = hp[e];
+          }
+#pragma unroll
+          for (int e = 0; e < 4; ++e) a4[e] = act_bwd_h<float>(g.dact, a4[e], h4[e]);
+        } else if (g.epi == kEpiAccum && g.beta) {
+          if (vec && cnt == 4) {
+            const float4 o = *reinterpret_cast<const float4*>(dst);
+            a4[0] += o.x; a4[1] += o.y; a4[2] += o.z; a4[3] += o.w;
+          } else {
+            for (int e = 0; e < cnt; ++e) a4[e] += dst[e];
+          }
+        }
+        if (vec && cnt == 4) *reinterpret_cast<float4*>(dst) = make_float4(a4[0], a4[1], a4[2], a4[3]);
+        else for (int e = 0; e < cnt; ++e) dst[e] = a4[e];
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -899,11 +1150,40 @@ cudaError_t launch_tma_kernel(const GemmArgs<float>& g, std::uint32_t z, const C
     k_umma_pair<kTStagesMax><<<grid, kPThreads, pair_smem(kTStagesMax), st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0);
     return cudaGetLastError();
   }
+  static const bool persist = !(std::getenv("TG_UMMA_PERSIST") && std::getenv("TG_UMMA_PERSIST")[0] == '0');
+  const std::uint32_t kspan0 = g.epi == kEpiSplitK ? g.k_chunk : g.K;
+  if (persist && kspan0 <= 256) {
+    static bool pattr = false;
+    if (!pattr) {
+      const cudaError_t e = cudaFuncSetAttribute(k_umma_tma_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(persist_smem()));
+      if (e != cudaSuccess) return e;
+      pattr = true;
+    }
+    const std::uint32_t mt = (g.M + BM - 1) / BM, nt = (g.N + BN - 1) / BN;
+    const std::uint32_t tiles = mt * nt * z;
+    int nsm = 148;
+    {
+      static int cached = 0;
+      if (!cached) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
+        if (cached <= 0) cached = 148;
+      }
+      nsm = cached;
+    }
+    const std::uint32_t grid = std::min<std::uint32_t>(tiles, static_cast<std::uint32_t>(nsm));
+    if (grid == 0) return cudaSuccess;
+    k_umma_tma_p<<<grid, kTThreads, persist_smem(), st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0, mt, nt, tiles);
+    return cudaGetLastError();
+  }
   const dim3 grid((g.M + BM - 1) / BM, (g.N + BN - 1) / BN, z);
   // one k-tile per CTA (K <= 32): a 1-stage ring, so two CTAs share an SM
   // and one's TMA / epilogue latency hides behind the other's work
   const std::uint32_t kspan = g.epi == kEpiSplitK ? g.k_chunk : g.K;
-  if (kspan <= static_cast<std::uint32_t>(BK))
+  static const std::uint32_t k1max = std::getenv("TG_UMMA_K1") ? std::atoi(std::getenv("TG_UMMA_K1")) : BK;
+  if (kspan <= k1max)
     k_umma_tma<1><<<grid, kTThreads, tma_smem(1), st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0);
   else
     k_umma_tma<kTStagesMax><<<grid, kTThreads, tma_smem(kTStagesMax), st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0);

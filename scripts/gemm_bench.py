@@ -13,6 +13,8 @@ from paper_2503_13795_b200 import _lib  # noqa: E402
 
 S = int(os.environ.get("GB_S", "65536"))
 # (name, M, N, K, a_kmaj, b_nmaj): forward Z = W X, input adjoint dX = W^T dZ, weight grad dW = dZ X^T
+SHAPES_CFG4 = [("c4_m64_k64", 64, S, 64, True, True), ("c4_m64_k256", 64, S, 256, True, True),
+               ("c4_m192_k64", 192, S, 64, True, True), ("c4_m256_k64", 256, S, 64, True, True)]
 SHAPES = [("fwd_l1", 1024, S, 784, True, True), ("fwd_l2", 1024, S, 1024, True, True),
           ("dx_l2", 1024, S, 1024, False, True), ("dw_l2", 1024, 1024, S, True, False),
           ("dw_l1", 1024, 784, S, True, False)]
@@ -42,6 +44,8 @@ def run(engine, M, N, K, a_kmaj, b_nmaj, A, B, Cm, reps):
 
 
 out = {}
+if os.environ.get("GB_SET") == "cfg4":
+    SHAPES = SHAPES_CFG4
 for name, M, N, K, ak, bn in SHAPES:
     A, B = mat(M, N, K, ak, bn)
     Am = A.view(M, K) if ak else A.view(K, M).t()
