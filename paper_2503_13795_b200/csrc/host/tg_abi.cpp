@@ -943,6 +943,16 @@ void build_staged_plan(tg_program& pr) {
   }
 }
 
+// The pre-activation rows of a GEMM dense layer are read by nobody when the
+// activation's derivative is taken from its output (relu, tanh, exp, sigmoid:
+// k_act_bwd and the fused dX epilogue read h): the forward stores h only.
+bool z_dead(const tgc::Dense& D) {
+  static const bool off = std::getenv("TG_KEEP_Z") && std::getenv("TG_KEEP_Z")[0] == '1';
+  const auto a = D.act_op;
+  return !off && (a == std::uint32_t(tg::OpKind::Relu) || a == std::uint32_t(tg::OpKind::Tanh) ||
+                  a == std::uint32_t(tg::OpKind::Exp) || a == std::uint32_t(tg::OpKind::Sigmoid));
+}
+
 // Samples per chunk of the staged path: rows of V and G (plus the reverse
 // levels' contended-row temporaries) for the chunk within 64 GB of the B200's
 // 180 GB HBM (TG_STAGED_MB overrides), a multiple of 128.  One chunk covers
@@ -1348,6 +1358,7 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
       g.b_nmaj = true;
       g.C = V + std::size_t(D.out_row) * cb;
       g.C2 = D.act_op ? V + std::size_t(D.act_row) * cb : nullptr;
+      g.no_z = z_dead(D);
       g.ldc = cb;
       g.bias = D.b_uv != tgc::kNone ? UV + D.b_uv : nullptr;
       g.M = D.n_out;
@@ -1444,6 +1455,7 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
           g.b_span = P.n_rows;
           g.C = V;
           g.C2 = D.act_op ? V : nullptr;
+          g.no_z = z_dead(D);
           g.ldc = cb;
           g.bias = D.b_uv != tgc::kNone ? UV + D.b_uv : nullptr;
           g.M = D.n_out;

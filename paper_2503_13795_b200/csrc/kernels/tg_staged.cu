@@ -588,7 +588,7 @@ __global__ void __launch_bounds__(256) k_gemm(GemmArgs<T> g) {
       if (n >= g.N) continue;
       if (g.epi == kEpiBiasAct) {
         const T z = (g.bias ? g.bias[m] : T(0)) + acc[i][j];
-        g.C[std::size_t(m) * g.ldc + n] = z;
+        if (!(g.no_z && g.act)) g.C[std::size_t(m) * g.ldc + n] = z;
         if (g.act) g.C2[std::size_t(m) * g.ldc + n] = act_fwd<T>(g.act, z);
       } else if (g.epi == kEpiAccum) {
         T* p = &g.C[std::size_t(m) * g.ldc + n];

@@ -93,6 +93,8 @@ struct GemmArgs {
   // taken from the activation output H at C2 (+ member row offset c2), i.e.
   // the input adjoint product writes dz of the layer below directly
   std::uint32_t dact;
+  // kEpiBiasAct with act: store only H (C2); the pre-activation Z has no reader
+  bool no_z;
 };
 
 // Table-scatter (kind-1) batch terms grouped by (adjoint row a, index column f).

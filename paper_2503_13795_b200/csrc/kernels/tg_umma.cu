@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(128, 1) k_umma_tf32x3(GemmArgs<float> g) {
       const float acc = T > 0 ? __uint_as_float(r[j]) : 0.f;
       if (g.epi == kEpiBiasAct) {
         const float z = (g.bias ? g.bias[m] : 0.f) + acc;
-        g.C[std::size_t(m) * g.ldc + n] = z;
+        if (!(g.no_z && g.act)) g.C[std::size_t(m) * g.ldc + n] = z;
         if (g.act) g.C2[std::size_t(m) * g.ldc + n] = act_fwd<float>(g.act, z);
       } else if (g.epi == kEpiAccum) {
         float* p = &g.C[std::size_t(m) * g.ldc + n];
@@ -520,6 +520,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_umma_tma(GemmArgs<float> g, co
           for (int e = 0; e < cnt; ++e) a4[e] += dst[e];
         }
       }
+      if (g.no_z && g.act && g.epi == kEpiBiasAct) continue;   // z has no reader
       if (vec && cnt == 4) *reinterpret_cast<float4*>(dst) = make_float4(a4[0], a4[1], a4[2], a4[3]);
       else for (int e = 0; e < cnt; ++e) dst[e] = a4[e];
     }
@@ -770,6 +771,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_umma_tma_p(GemmArgs<float> g, 
             for (int e = 0; e < cnt; ++e) a4[e] += dst[e];
           }
         }
+        if (g.no_z && g.act && g.epi == kEpiBiasAct) continue;   // z has no reader
         if (vec && cnt == 4) *reinterpret_cast<float4*>(dst) = make_float4(a4[0], a4[1], a4[2], a4[3]);
         else for (int e = 0; e < cnt; ++e) dst[e] = a4[e];
       }
@@ -1079,6 +1081,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
             for (int e = 0; e < cnt; ++e) a4[e] += dst[e];
           }
         }
+        if (g.no_z && g.act && g.epi == kEpiBiasAct) continue;   // z has no reader
         if (vec && cnt == 4) *reinterpret_cast<float4*>(dst) = make_float4(a4[0], a4[1], a4[2], a4[3]);
         else for (int e = 0; e < cnt; ++e) dst[e] = a4[e];
       }

@@ -1,0 +1,6 @@
+O=gpurun_out/s19
+mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu.py -x -q -k "gpt or full_size or fusions or workloads or larger or gemm" > $O/pytest.log 2>&1; echo "exit $?" >> $O/pytest.log
+for c in cfg3 cfg4 cfg5; do
+  timeout 600 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_$c.json 2>&1
+done
