@@ -710,7 +710,7 @@ void build_staged_plan(tg_program& pr) {
       if (stg.batch == -1)
         for (std::uint32_t k = stg.begin; k < stg.end && !stg.macro; ++k) {
           const auto kind = (w ? P.bwd : P.fwd)[k].kind;
-          stg.macro = kind == tgc::kLNorm || kind == tgc::kDense || kind == tgc::kAttn;
+          stg.macro = kind == tgc::kDense || kind == tgc::kAttn;   // (kLNorm has a four-sample form)
         }
   // batch tables: forward {0, x, z, h}, input adjoints {0, z, x, 0}, weight gradient {z, x, 0, 0}
   const bool tc = pr.tsz() == 4 && pr.umma;

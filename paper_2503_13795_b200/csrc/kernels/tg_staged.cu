@@ -272,6 +272,100 @@ struct Lv4 {
   }
 };
 
+// Layer norm of four consecutive samples (ln_fwd_sample / ln_bwd_sample, one float4 per row).
+__device__ void ln_fwd4(const RangeArgs<float>& a, const tgc::LNorm& L, std::size_t col, std::size_t s,
+                        std::uint32_t node_err) {
+  const std::uint32_t* lr = a.lnrows;
+  L4 s1{{0.f, 0.f, 0.f, 0.f}}, s2{{0.f, 0.f, 0.f, 0.f}};
+#pragma unroll 4
+  for (std::uint32_t i = 0; i < L.n; ++i) {
+    const L4 x = ld4(a.V + std::size_t(lr[L.off + i]) * a.ld + col);
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      s1.v[l] += x.v[l];
+      s2.v[l] += x.v[l] * x.v[l];
+    }
+  }
+  L4 mu, rstd;
+#pragma unroll
+  for (int l = 0; l < 4; ++l) {
+    mu.v[l] = s1.v[l] / static_cast<float>(L.n);
+    const float ve = (s2.v[l] / static_cast<float>(L.n) - mu.v[l] * mu.v[l]) + static_cast<float>(L.eps);
+    if (!(ve > 0.f)) record_error(a.err_key, s + l, node_err);
+    rstd.v[l] = 1.f / d_sqrt(ve);
+  }
+#pragma unroll 4
+  for (std::uint32_t i = 0; i < L.n; ++i) {
+    const L4 x = ld4(a.V + std::size_t(lr[L.off + i]) * a.ld + col);
+    const float gm = a.UV[lr[L.off + 3 * L.n + i]], bt = a.UV[lr[L.off + 4 * L.n + i]];
+    L4 nv, y;
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      nv.v[l] = (x.v[l] - mu.v[l]) * rstd.v[l];
+      y.v[l] = nv.v[l] * gm + bt;
+    }
+    st4(a.V + std::size_t(lr[L.off + L.n + i]) * a.ld + col, nv);
+    st4(a.V + std::size_t(lr[L.off + 2 * L.n + i]) * a.ld + col, y);
+  }
+}
+
+__device__ void ln_bwd4(const RangeArgs<float>& a, const tgc::LNorm& L, std::size_t col) {
+  const std::uint32_t* lr = a.lnrows;
+  L4 s1{{0.f, 0.f, 0.f, 0.f}}, s2{{0.f, 0.f, 0.f, 0.f}};
+#pragma unroll 4
+  for (std::uint32_t i = 0; i < L.n; ++i) {
+    const L4 x = ld4(a.V + std::size_t(lr[L.off + i]) * a.ld + col);
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      s1.v[l] += x.v[l];
+      s2.v[l] += x.v[l] * x.v[l];
+    }
+  }
+  L4 mu, ve, rstd, drstd{{0.f, 0.f, 0.f, 0.f}}, sdc{{0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+  for (int l = 0; l < 4; ++l) {
+    mu.v[l] = s1.v[l] / static_cast<float>(L.n);
+    ve.v[l] = (s2.v[l] / static_cast<float>(L.n) - mu.v[l] * mu.v[l]) + static_cast<float>(L.eps);
+    rstd.v[l] = 1.f / d_sqrt(ve.v[l]);
+  }
+#pragma unroll 4
+  for (std::uint32_t i = 0; i < L.n; ++i) {
+    const L4 dy = ld4(a.G + std::size_t(lr[L.off + 2 * L.n + i]) * a.ld + col);
+    const L4 x = ld4(a.V + std::size_t(lr[L.off + i]) * a.ld + col);
+    const float gm = a.UV[lr[L.off + 3 * L.n + i]];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const float dn = dy.v[l] * gm;
+      drstd.v[l] += dn * (x.v[l] - mu.v[l]);
+      sdc.v[l] += dn * rstd.v[l];
+    }
+  }
+  L4 cx, cm;
+#pragma unroll
+  for (int l = 0; l < 4; ++l) {
+    const float dve = -drstd.v[l] * rstd.v[l] / (2.f * ve.v[l]);
+    const float dmu = -sdc.v[l] + (-dve) * 2.f * mu.v[l];
+    cx.v[l] = dve * 2.f / static_cast<float>(L.n);
+    cm.v[l] = dmu / static_cast<float>(L.n);
+  }
+#pragma unroll 4
+  for (std::uint32_t i = 0; i < L.n; ++i) {
+    const L4 dy = ld4(a.G + std::size_t(lr[L.off + 2 * L.n + i]) * a.ld + col);
+    const L4 x = ld4(a.V + std::size_t(lr[L.off + i]) * a.ld + col);
+    const float gm = a.UV[lr[L.off + 3 * L.n + i]];
+    float* p = a.G + std::size_t(lr[L.off + i]) * a.ld + col;
+    L4 dx;
+#pragma unroll
+    for (int l = 0; l < 4; ++l) dx.v[l] = dy.v[l] * gm * rstd.v[l] + cx.v[l] * x.v[l] + cm.v[l];
+    if (!(a.lnflag[L.flag_off + i] & tgc::kAssign)) {
+      const L4 c = ld4(p);
+#pragma unroll
+      for (int l = 0; l < 4; ++l) dx.v[l] += c.v[l];
+    }
+    st4(p, dx);
+  }
+}
+
 __device__ __forceinline__ bool many_operand_op(std::uint8_t op) {
   return op == AddVarying || op == MeanVarying || op == NegativeMeanVarying || op == SubVarying ||
          op == SumOfSquaresVarying || op == MeanSquaresVarying || op == InnerProductNoBias ||
@@ -282,6 +376,10 @@ __device__ void fwd_instr4(const RangeArgs<float>& a, std::uint32_t k, std::size
   const Instr in = a.fwd[k];
   Lv4 L{a, col, s};
   L4 out;
+  if (in.kind == tgc::kLNorm) {
+    ln_fwd4(a, a.lnorm[in.aux], col, s, a.lnorm[in.aux].rstd_node);
+    return;
+  }
   if (in.kind == tgc::kInputLoad) {
     const float* src = a.inputs + std::size_t(in.aux) * a.batch + s;
     if ((reinterpret_cast<std::uintptr_t>(src) & 15) == 0) {
@@ -367,6 +465,10 @@ __device__ void fwd_instr4(const RangeArgs<float>& a, std::uint32_t k, std::size
 
 __device__ void bwd_instr4(const RangeArgs<float>& a, std::uint32_t k, std::size_t col, std::size_t s) {
   const Instr in = a.bwd[k];
+  if (in.kind == tgc::kLNorm) {
+    ln_bwd4(a, a.lnorm[in.aux], col);
+    return;
+  }
   if (in.kind != tgc::kNode || !(many_operand_op(in.op) || in.nops <= 2) || in.op == StopGradMax) {
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
