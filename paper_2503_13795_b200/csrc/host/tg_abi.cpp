@@ -1564,7 +1564,8 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
         if (!dw_done && pr.dplan[u].dw_dest0 != tgc::kNone) TG_CUDA_TRY(dw_one(u));
       }
       if (dp0.db_dest0 != tgc::kNone) {
-        TG_CUDA_TRY(tgk::launch_rowsum_batched<T>(G, B.d_tab, nm, D.n_out, n, cb, acc + dp0.db_dest0, st));
+        TG_CUDA_TRY(tgk::launch_rowsum_batched<T>(G, B.d_tab, nm, D.n_out, n, cb, acc + dp0.db_dest0, sk,
+                                                  (L.sp - L.sk) / sizeof(T), st));   // split-K scratch, free here
         ++pr.launches;
       }
     }

@@ -767,6 +767,51 @@ __global__ void __launch_bounds__(256) k_rowsum(const T* G, std::uint32_t row0, 
   if (threadIdx.x == 0) dst[blockIdx.x] += red[0];
 }
 
+// Two-pass form of the bias row sums for many samples: CTA (row, chunk c) sums
+// the c-th contiguous share of the (member, sample) sequence of a row, then
+// k_rowsum_fin adds the shares in chunk order (deterministic; one CTA per row
+// had left most SMs idle when a layer has 64 rows).
+template <class T>
+__global__ void __launch_bounds__(256) k_rowsum_part(const T* G, std::size_t n, std::size_t ld, const uint4* mem,
+                                                     std::uint32_t n_mem, std::size_t per, T* part) {
+  __shared__ T red[256];
+  const std::size_t total = std::size_t(n_mem) * n;
+  const std::size_t b = std::size_t(blockIdx.y) * per, e = min(total, b + per);
+  T t = 0;
+  std::size_t q = b;
+  while (q < e) {   // runs of one member's row
+    const std::uint32_t p = static_cast<std::uint32_t>(q / n);
+    const std::size_t s0 = q % n, s1 = min(n, s0 + (e - q));
+    const T* row = G + std::size_t(mem[p].z + blockIdx.x) * ld;
+    std::size_t s = s0 + threadIdx.x;
+    for (; s + 7 * 256 < s1; s += 8 * 256) {
+      T x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = row[s + u * 256];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) t += x[u];
+    }
+    for (; s < s1; s += 256) t += row[s];
+    q += s1 - s0;
+  }
+  red[threadIdx.x] = t;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[std::size_t(blockIdx.x) * gridDim.y + blockIdx.y] = red[0];
+}
+
+template <class T>
+__global__ void k_rowsum_fin(const T* part, std::uint32_t rows, std::uint32_t chunks, T* dst) {
+  const std::uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= rows) return;
+  T t = 0;
+  for (std::uint32_t c = 0; c < chunks; ++c) t += part[std::size_t(j) * chunks + c];
+  dst[j] += t;
+}
+
 template <class T>
 __global__ void k_zero_rows(T* X, const std::uint32_t* rows, std::size_t n, std::size_t ld) {
   const std::size_t s = std::size_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -955,9 +1000,20 @@ cudaError_t launch_rowsum(const T* G, std::uint32_t row0, std::uint32_t rows, st
 
 template <class T>
 cudaError_t launch_rowsum_batched(const T* G, const uint4* mem, std::uint32_t n_mem, std::uint32_t rows, std::size_t n,
-                                  std::size_t ld, T* dst, cudaStream_t st) {
+                                  std::size_t ld, T* dst, T* scratch, std::size_t scratch_elems, cudaStream_t st) {
   if (rows == 0 || n_mem == 0) return cudaSuccess;
-  k_rowsum<T><<<rows, 256, 0, st>>>(G, 0, n, ld, dst, mem, n_mem);
+  // about four CTAs per SM over all rows, shares of >= 8k elements
+  const std::size_t total = std::size_t(n_mem) * n;
+  std::size_t chunks = std::max<std::size_t>(1, (592 + rows - 1) / rows);
+  chunks = std::min<std::size_t>(chunks, std::max<std::size_t>(1, total / 8192));
+  if (scratch) chunks = std::min<std::size_t>(chunks, std::max<std::size_t>(1, scratch_elems / rows));
+  if (!scratch || chunks <= 1) {
+    k_rowsum<T><<<rows, 256, 0, st>>>(G, 0, n, ld, dst, mem, n_mem);
+    return cudaGetLastError();
+  }
+  const std::size_t per = (total + chunks - 1) / chunks;
+  k_rowsum_part<T><<<dim3(rows, static_cast<unsigned>(chunks)), 256, 0, st>>>(G, n, ld, mem, n_mem, per, scratch);
+  k_rowsum_fin<T><<<(rows + 127) / 128, 128, 0, st>>>(scratch, rows, static_cast<std::uint32_t>(chunks), dst);
   return cudaGetLastError();
 }
 
@@ -991,7 +1047,7 @@ cudaError_t launch_contract(const std::uint32_t* dests, std::uint32_t n_dests, c
   template cudaError_t launch_act_bwd_batched<T>(T*, const T*, const uint4*, std::uint32_t, std::uint32_t, std::size_t,   \
                                                  std::size_t, std::uint32_t, cudaStream_t);                                \
   template cudaError_t launch_rowsum_batched<T>(const T*, const uint4*, std::uint32_t, std::uint32_t, std::size_t,          \
-                                                std::size_t, T*, cudaStream_t);                                            \
+                                                std::size_t, T*, T*, std::size_t, cudaStream_t);                           \
   template cudaError_t launch_zero_rows<T>(T*, const std::uint32_t*, std::uint32_t, std::size_t, std::size_t,              \
                                            cudaStream_t);                                                                  \
   template cudaError_t launch_contract<T>(const std::uint32_t*, std::uint32_t, const std::uint32_t*, const Term*,          \

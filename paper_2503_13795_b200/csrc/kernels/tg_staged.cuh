@@ -140,7 +140,8 @@ template <class T> cudaError_t launch_rowsum(const T* G, std::uint32_t row0, std
 template <class T> cudaError_t launch_act_bwd_batched(T* G, const T* V, const uint4* mem, std::uint32_t n_mem, std::uint32_t n_out,
                                                       std::size_t n, std::size_t ld, std::uint32_t act, cudaStream_t st);
 template <class T> cudaError_t launch_rowsum_batched(const T* G, const uint4* mem, std::uint32_t n_mem, std::uint32_t rows,
-                                                     std::size_t n, std::size_t ld, T* dst, cudaStream_t st);
+                                                     std::size_t n, std::size_t ld, T* dst, T* scratch,
+                                                     std::size_t scratch_elems, cudaStream_t st);
 // Contended adjoint rows at the end of a reverse level, e = {row, assign, t0, count}:
 // G[row] = (assign ? 0 : G[row]) + G[t0] + ... + G[t0 + count - 1]   (in order)
 template <class T> cudaError_t launch_row_sums(const uint4* ent, std::uint32_t n_ent, T* G, std::size_t n, std::size_t ld,
