@@ -680,6 +680,8 @@ Program compile(const tg_tape_desc& d) {
     A.n_nodes = 0;
     for (const AttnUnit& U : G.units) A.n_nodes += static_cast<std::uint32_t>(U.interior.size() + U.o.size());
     A.scale = G.scale;
+    A.stat_row = nrow;
+    nrow += 2 * A.n_units;
     attn_id[g] = static_cast<std::uint32_t>(P.attn.size());
     P.attn.push_back(A);
   }

@@ -118,6 +118,8 @@ struct Attn {
   std::uint32_t n_units, n_keys, hd, dv;
   std::uint32_t unit_off, key_off;
   std::uint32_t first_node, n_nodes;   // recorded nodes covered (diagnostics, node-eval counts)
+  std::uint32_t stat_row;              // rows stat_row + 2u, + 2u + 1: softmax max and 1 / sum of unit u
+                                       // (written by the staged forward kernel for its reverse)
   double scale;
 };
 

@@ -129,6 +129,8 @@ __global__ void __launch_bounds__(kThreads) k_attn_fwd(AttnStage a) {
 #pragma unroll
       for (int i = 0; i < HD; ++i)
         if (i < static_cast<int>(dv)) a.V[std::size_t(orow + i) * a.ld + col] = acc[i] * inv;
+      a.V[std::size_t(A.stat_row + 2 * u) * a.ld + col] = m;        // for the reverse kernel
+      a.V[std::size_t(A.stat_row + 2 * u + 1) * a.ld + col] = inv;
     }
 }
 
@@ -171,21 +173,9 @@ __global__ void __launch_bounds__(kThreads) k_attn_bwd(AttnStage a) {
           if (i < static_cast<int>(dv)) D += dO[i] * a.V[std::size_t(orow + i) * a.ld + col];
           dq[i] = 0.f;
         }
-        float m = -INFINITY, l = 0.f;
-        for (std::uint32_t j = 0; j < n; ++j) {
-          const float* kj = S0 + j * HD * kS + s;
-          float c = 0.f;
-#pragma unroll
-          for (int i = 0; i < HD; ++i)
-            c += q[i] * kj[i * kS];
-          c *= scale;
-          if (c > m) {
-            l *= expf(m - c);
-            m = c;
-          }
-          l += expf(c - m);
-        }
-        const float inv = 1.f / l;
+        // softmax statistics of the forward pass (stat rows)
+        const float m = a.V[std::size_t(A.stat_row + 2 * u) * a.ld + col];
+        const float inv = a.V[std::size_t(A.stat_row + 2 * u + 1) * a.ld + col];
         for (std::uint32_t j = 0; j < n; ++j) {
           const float* kj = S0 + j * HD * kS + s;
           const float* vj = S1 + j * HD * kS + s;

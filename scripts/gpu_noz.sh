@@ -1,4 +1,4 @@
-O=gpurun_out/s22
+O=gpurun_out/s23
 mkdir -p $O
 timeout 900 python -m pytest tests/test_gpu.py -x -q -k "gpt or full_size or fusions or workloads or larger or gemm" > $O/pytest.log 2>&1; echo "exit $?" >> $O/pytest.log
 for c in cfg3 cfg4 cfg5; do
