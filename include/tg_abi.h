@@ -183,6 +183,19 @@ tg_status tg_program_order(tg_program_t p, const uint32_t** order, uint32_t* n_o
  * PAPER.md:1357-1359). */
 tg_status tg_workspace_size(tg_program_t p, size_t batch, size_t* bytes);
 
+/* Sequential-accumulation memory mode (
+ * SURVEY.md §8f row 1): the staged tier streams the batch through its
+ * HBM-resident rows in chunks of samples whose rows fit `bytes`, summing the
+ * gradient chunk by chunk, so tg_workspace_size stops growing with the batch
+ * once the batch exceeds one chunk.  0 restores the default (64 GB, or env
+ * TG_STAGED_MB in MiB).  Set it before sizing the workspace.  Other tiers
+ * keep their rows in registers / shared memory (workspace bounded by the grid
+ * already). */
+tg_status tg_set_memory_budget(tg_program_t p, size_t bytes);
+/* Samples per chunk that tg_forward_backward will use for `batch` (the batch
+ * itself for tiers without chunking). */
+tg_status tg_chunk_samples(tg_program_t p, size_t batch, size_t* samples);
+
 /* Forward sweep + reverse sweep + batch reduction for `batch` samples:
  * replaces, per sample, rewind/build (tape.hpp:235-242), zero_grads
  * (backprop.hpp:100-109), backward_with_scratch (backprop.hpp:139-184) and

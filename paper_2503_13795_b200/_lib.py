@@ -100,6 +100,8 @@ def _load():
         "tg_program_info_get": (st, [P, C.POINTER(tg_program_info)]),
         "tg_program_order": (st, [P, C.POINTER(C.POINTER(u32)), C.POINTER(u32)]),
         "tg_workspace_size": (st, [P, sz, C.POINTER(sz)]),
+        "tg_set_memory_budget": (st, [P, sz]),
+        "tg_chunk_samples": (st, [P, sz, C.POINTER(sz)]),
         "tg_forward_backward": (st, [P, P, P, sz, P, P, P, P, P, sz, P]),
         "tg_gd_update": (st, [P, P, P, C.c_double, sz, P]),
         "tg_train_step": (st, [P, P, P, sz, P, P, P, C.c_double, P, sz, P]),

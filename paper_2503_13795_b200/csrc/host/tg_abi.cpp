@@ -195,6 +195,7 @@ struct tg_program {
   tgk::ScatterUse* d_sc_uses = nullptr;
   std::uint32_t *d_sc_use_off = nullptr, *d_sc_dests = nullptr;
   std::size_t chunk = 0;          // samples per chunk (0 = by batch)
+  std::size_t mem_budget = 0;     // staged rows per chunk within this many bytes (0: TG_STAGED_MB or 64 GB)
   bool umma = true;               // fp32 dense layers on tcgen05 (3xTF32); TG_UMMA=0 -> SIMT GEMM
   bool attn_fast = false;         // fused heads on the shared-memory kernels (tg_attn.cu; TG_ATTN_FAST=0: interpreter)
   std::uint32_t attn_hd = 0;      // widest key / value block of the fused heads
@@ -962,6 +963,7 @@ bool z_dead(const tgc::Dense& D) {
 std::size_t staged_chunk(const tg_program& pr, std::size_t batch) {
   std::size_t budget = std::size_t(64) << 30;
   if (const char* e = std::getenv("TG_STAGED_MB")) budget = std::size_t(std::atoll(e)) << 20;
+  if (pr.mem_budget) budget = pr.mem_budget;
   const std::size_t per = (2 * std::max<std::size_t>(1, pr.P.n_rows) + pr.n_tmp) * pr.tsz();
   std::size_t cb = std::max<std::size_t>(128, (budget / per) / 128 * 128);
   const std::size_t need = (std::max<std::size_t>(batch, 1) + 127) / 128 * 128;
@@ -2102,6 +2104,22 @@ tg_status tg_program_order(tg_program_t p, const uint32_t** order, uint32_t* n) 
   *order = p->P.order.data();
   *n = static_cast<uint32_t>(p->P.order.size());
   return TG_OK;
+}
+
+tg_status tg_set_memory_budget(tg_program_t p, size_t bytes) {
+  return guard([&] {
+    if (!p) return fail(TG_INVALID_HANDLE, "tg_set_memory_budget: null program");
+    p->mem_budget = bytes;
+    return TG_OK;
+  });
+}
+
+tg_status tg_chunk_samples(tg_program_t p, size_t batch, size_t* samples) {
+  return guard([&] {
+    if (!p || !samples) return fail(TG_INVALID_ARGUMENT, "tg_chunk_samples: null argument");
+    *samples = p->staged ? std::min(staged_chunk(*p, batch), std::max<std::size_t>(batch, 1)) : std::max<std::size_t>(batch, 1);
+    return TG_OK;
+  });
 }
 
 tg_status tg_workspace_size(tg_program_t p, size_t batch, size_t* bytes) {

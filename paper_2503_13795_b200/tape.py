@@ -349,6 +349,15 @@ class Program:
         check(lib.tg_workspace_size(self._h, int(batch), C.byref(out)))
         return out.value
 
+    def set_memory_budget(self, nbytes: int) -> None:
+        """Sequential-accumulation mode: staged rows of at most `nbytes` per chunk (0: default)."""
+        check(lib.tg_set_memory_budget(self._h, int(nbytes)))
+
+    def chunk_samples(self, batch: int) -> int:
+        out = C.c_size_t()
+        check(lib.tg_chunk_samples(self._h, int(batch), C.byref(out)))
+        return out.value
+
     @property
     def launches(self) -> int:
         return int(lib.tg_launch_count(self._h))

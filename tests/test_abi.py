@@ -199,3 +199,22 @@ def test_every_jit_program_compiles(form, fuse, monkeypatch):
         _lib.lib.tg_program_jit(p._h, ctypes.byref(src), ctypes.byref(log), ctypes.byref(ms))
         text = (log.value or b"").decode()
         assert "compiled" in text or "not eligible" in text, text[-2000:]
+
+
+@pytest.mark.parametrize("name,dims", [("char_mlp", None), ("wide_mlp", None), ("gpt", None)])
+def test_memory_budget_bounds_staged_workspace(name, dims):
+    """Sequential-accumulation mode: with a memory
+    budget the staged workspace stops growing with the batch (peak device
+    memory independent of b), chunks are multiples of 128 samples, and 0
+    restores the one-chunk default."""
+    p = tg.Program(tg.build_model(name, dims, "f32"))
+    assert p.info["storage"] == 3
+    big = p.workspace_size(1 << 20)
+    p.set_memory_budget(64 << 20)
+    cb = p.chunk_samples(1 << 20)
+    assert cb % 128 == 0 and 128 <= cb < (1 << 20)
+    sizes = [p.workspace_size(b) for b in (cb, 4 * cb, 1 << 20, 1 << 22)]
+    assert len(set(sizes)) == 1 and sizes[0] < big
+    assert p.chunk_samples(100) == 100
+    p.set_memory_budget(0)
+    assert p.workspace_size(1 << 20) == big

@@ -531,3 +531,30 @@ def test_serialize_device_params_round_trip():
     P3 = torch.zeros_like(P)
     assert ser.load_snapshot(snap, P3)["count"] == desc.n_params
     assert torch.equal(P.view(torch.int64), P3.view(torch.int64))
+
+
+@pytest.mark.parametrize("name,dims,b,budget_mb", [("char_mlp", None, 20000, 2), ("wide_mlp", [40, 300, 260, 10], 3000, 3),
+                                                    ("gpt", [17, 8, 16, 2, 2, 32], 300, 4)])
+def test_sequential_accumulation_chunks_vs_oracle(name, dims, b, budget_mb):
+    """Sequential-accumulation memory mode (PAPER.md:73,
+    SPEC.md:437): a small tg_set_memory_budget streams the batch through the
+    staged rows in several chunks (ragged last chunk), the gradient summed
+    chunk by chunk.  The result equals the oracle and the one-chunk run to the
+    fp32 bar, and the workspace is the chunk's, not the batch's."""
+    desc = tg.build_model(name, dims, "f32", seed=5).describe()
+    x, k = tg.synth_batch(name, dims, "f32", seed=23, batch=b, n_inputs=desc.n_inputs, n_index=desc.n_index_inputs)
+    one = make_prog(desc, "staged")
+    L1, IG1, G1 = run(one, desc, x, k, desc.param_values(), b)
+    prog = make_prog(desc, "staged")
+    prog.set_memory_budget(budget_mb << 20)
+    cb = prog.chunk_samples(b)
+    assert 128 <= cb < b and b % cb != 0, cb            # several chunks, ragged tail
+    assert prog.workspace_size(b) == prog.workspace_size(8 * b) < one.workspace_size(b)
+    L, IG, G = run(prog, desc, x, k, desc.param_values(), b)
+    r = oracle.run(desc, x.astype(np.float64), k, desc.param_values(), threads=os.cpu_count() or 8)
+    assert close_rel(L, r["loss"], 1e-5, 1e-6)
+    assert rel(G, r["grad_sum"]) <= 1e-5
+    assert rel(G, G1) <= 1e-5
+    assert close_rel(L, L1, 1e-6, 1e-7)
+    if desc.n_inputs:
+        assert rel(IG, r["input_grad"]) <= 1e-4
