@@ -371,6 +371,45 @@ def main():
         e2e_ms = float(t.item())
     prog.check_device_error()
 
+    # ---- on-device input pipeline: each step's batch is
+    # generated on the GPU (tg_synth_ctr_device, fresh samples every step, the
+    # bits of the host generator tg_synth_ctr), then the step, then the losses
+    # back to pinned host memory: no input bytes cross PCIe ----
+    def synth_into(i):
+        tg.synth_ctr_device(cfg["model"], X, K, cfg["dims"], cfg["dtype"], seed=2000,
+                            first=(i * world + rank) * b, batch=b, stream=stream)
+
+    def dev_step(i):
+        synth_into(i)
+        run_step()
+        lh.copy_(L, non_blocking=True)
+
+    for i in range(args.warmup):
+        dev_step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    n_dev = min(max(args.steps, 20), cap)
+    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    d0.record(stream)
+    for i in range(n_dev):
+        dev_step(args.warmup + i)
+    d1.record(stream)
+    torch.cuda.synchronize()
+    dev_ms = d0.elapsed_time(d1) / n_dev
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0.record(stream)
+    for i in range(n_dev):
+        synth_into(i)
+    g1.record(stream)
+    torch.cuda.synchronize()
+    synth_ms = g0.elapsed_time(g1) / n_dev
+    if world > 1:
+        t = torch.tensor([dev_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms = float(t.item())
+    prog.check_device_error()
+
     # ---- roofline of the dominant kernel ----
     pk = peaks()
     info = prog.info
@@ -422,6 +461,10 @@ def main():
                 "h2d_link_gbs": h2d / (copy_ms * 1e-3) / 1e9 if h2d else None,
                 "api": ("tg_pipeline_step (pinned host inputs in, per-sample losses out, 4 steps in flight)"
                         if pipe is not None else "copies + tg_forward_backward + NCCL all-reduce + tg_gd_update")},
+        "device_input_pipeline": {"value": b * world / (dev_ms * 1e-3), "unit": "grad/s", "ms_per_step": dev_ms,
+                                  "synth_ms_per_step": synth_ms, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": d2h,
+                                  "api": "tg_synth_ctr_device (fresh counter-based samples each step) + the step + "
+                                         "losses to pinned host memory"},
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

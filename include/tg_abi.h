@@ -150,6 +150,19 @@ tg_status tg_build_model(tg_model model, const tg_model_args* args, uint64_t see
 tg_status tg_synth_batch(tg_model model, const tg_model_args* args, uint64_t seed, size_t batch,
                          void* inputs, int32_t* index_inputs);
 
+/* Counter-based synthetic batches (the on-device input
+ * pipeline).  Same columns, layouts and per-sample draw order as
+ * tg_synth_batch, but draw j of global sample s comes from Philox4x32-10
+ * keyed by `seed` at counter (s, j/2), so samples [first_sample,
+ * first_sample + batch) are generated independently of one another: the host
+ * version and the device version (written into device arrays on `stream`, no
+ * host traffic) give identical bits, for any split of the sample range across
+ * calls, chunks or ranks.  Zipf vocabularies up to 1024 ids on the device. */
+tg_status tg_synth_ctr(tg_model model, const tg_model_args* args, uint64_t seed, uint64_t first_sample, size_t batch,
+                       void* inputs, int32_t* index_inputs);
+tg_status tg_synth_ctr_device(tg_model model, const tg_model_args* args, uint64_t seed, uint64_t first_sample,
+                              size_t batch, void* inputs, int32_t* index_inputs, tg_stream_t stream);
+
 /* ---- compile and run ------------------------------------------------------ */
 typedef struct tg_program* tg_program_t;
 

@@ -6,5 +6,5 @@ and GD update.  See DESIGN.md.
 """
 from ._lib import DomainError, InvalidArgument, TgError  # noqa: F401  (raises if libtg.so is missing)
 from .tape import (  # noqa: F401
-    MODELS, OpKind, Pipeline, Program, Tape, TapeDesc, build_model, op_name, synth_batch,
+    MODELS, OpKind, Pipeline, Program, Tape, TapeDesc, build_model, op_name, synth_batch, synth_ctr, synth_ctr_device,
 )

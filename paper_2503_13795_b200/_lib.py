@@ -96,6 +96,8 @@ def _load():
         "tg_rec_describe": (st, [P, C.POINTER(tg_tape_desc)]),
         "tg_build_model": (st, [st, C.POINTER(tg_model_args), u64, C.POINTER(P)]),
         "tg_synth_batch": (st, [st, C.POINTER(tg_model_args), u64, sz, P, C.POINTER(i32)]),
+        "tg_synth_ctr": (st, [st, C.POINTER(tg_model_args), u64, u64, sz, P, C.POINTER(i32)]),
+        "tg_synth_ctr_device": (st, [st, C.POINTER(tg_model_args), u64, u64, sz, P, C.POINTER(i32), P]),
         "tg_compile": (st, [C.POINTER(tg_tape_desc), C.POINTER(P)]),
         "tg_program_info_get": (st, [P, C.POINTER(tg_program_info)]),
         "tg_program_order": (st, [P, C.POINTER(C.POINTER(u32)), C.POINTER(u32)]),

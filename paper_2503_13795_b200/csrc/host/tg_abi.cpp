@@ -27,6 +27,11 @@
 #include "tg_recorder.hpp"
 #include "../kernels/tg_staged.cuh"
 #include "../kernels/tg_tape.cuh"
+#include "../kernels/tg_synth.cuh"
+
+namespace tgk {
+cudaError_t launch_synth(const tgs::SynthArgs& a, const double* cdf_host, cudaStream_t st);
+}
 
 namespace {
 
@@ -2061,6 +2066,58 @@ tg_status tg_synth_batch(tg_model model, const tg_model_args* args, uint64_t see
     const tg_dtype dt = args ? args->dtype : TG_F64;
     if (dt == TG_F64) tgm::synth<double>(model, D, seed, batch, static_cast<double*>(inputs), index_inputs);
     else tgm::synth<float>(model, D, seed, batch, static_cast<float*>(inputs), index_inputs);
+    return TG_OK;
+  });
+}
+
+// Counter-based synthetic batches (tg_synth.cuh): arguments shared by the
+// host and device generators.
+namespace {
+tgs::SynthArgs synth_args(tg_model model, const tg_model_args* args, uint64_t seed, uint64_t first, size_t batch,
+                          void* inputs, int32_t* index_inputs, std::vector<double>& cdf) {
+  const tgm::Dims D = tgm::Dims::resolve(model, args ? args->dims : nullptr);
+  tgs::SynthArgs a{};
+  a.model = model;
+  a.f64 = (args ? args->dtype : TG_F64) == TG_F64;
+  tgm::io_shape(model, D, a.n_inputs, a.n_index);
+  if (batch && ((a.n_inputs && !inputs) || (a.n_index && !index_inputs)))
+    throw std::invalid_argument("tg_synth: NULL output for a model with " + std::to_string(a.n_inputs) + " input and " +
+                                std::to_string(a.n_index) + " index columns");
+  a.n_classes = int(model) == tgm::kWideMlp ? D.d[3] : 0;
+  if (int(model) == tgm::kCharMlp || int(model) == tgm::kGpt) {
+    cdf = tgm::Zipf(D.d[0], int(model) == tgm::kCharMlp ? 1.1 : 1.0).cdf;
+    a.V = static_cast<std::uint32_t>(cdf.size());
+    a.cdf = cdf.data();
+  }
+  a.seed = seed;
+  a.first = first;
+  a.batch = batch;
+  a.x = inputs;
+  a.idx = index_inputs;
+  return a;
+}
+}  // namespace
+
+tg_status tg_synth_ctr(tg_model model, const tg_model_args* args, uint64_t seed, uint64_t first_sample, size_t batch,
+                       void* inputs, int32_t* index_inputs) {
+  return guard([&] {
+    std::vector<double> cdf;
+    const tgs::SynthArgs a = synth_args(model, args, seed, first_sample, batch, inputs, index_inputs, cdf);
+    for (std::size_t i = 0; i < batch; ++i) {
+      if (a.f64) tgs::synth_sample<double>(a, i);
+      else tgs::synth_sample<float>(a, i);
+    }
+    return TG_OK;
+  });
+}
+
+tg_status tg_synth_ctr_device(tg_model model, const tg_model_args* args, uint64_t seed, uint64_t first_sample,
+                              size_t batch, void* inputs, int32_t* index_inputs, tg_stream_t stream) {
+  return guard([&] {
+    std::vector<double> cdf;
+    const tgs::SynthArgs a = synth_args(model, args, seed, first_sample, batch, inputs, index_inputs, cdf);
+    if (a.V > 1024) return fail(TG_INVALID_ARGUMENT, "tg_synth_ctr_device: Zipf vocabulary above 1024 ids");
+    TG_CUDA_TRY(tgk::launch_synth(a, cdf.data(), static_cast<cudaStream_t>(stream)));
     return TG_OK;
   });
 }

@@ -313,6 +313,44 @@ def synth_batch(model, dims=None, dtype: str | None = None, seed: int = 0, batch
     return x[:n_inputs], k[:n_index]
 
 
+def _io_cols(m, dims, dtype, n_inputs, n_index):
+    if n_inputs is None or n_index is None:
+        d = build_model(m, dims, dtype, seed=0).describe()
+        n_inputs, n_index = d.n_inputs, d.n_index_inputs
+    return n_inputs, n_index
+
+
+def synth_ctr(model, dims=None, dtype: str | None = None, seed: int = 0, first: int = 0, batch: int = 1,
+              n_inputs: int | None = None, n_index: int | None = None):
+    """Host counter-based batch of samples [first, first + batch) (tg_synth_ctr):
+    the bits synth_ctr_device writes on the GPU."""
+    m = model_id(model)
+    dtype = dtype or DEFAULT_DTYPE[m]
+    n_inputs, n_index = _io_cols(m, dims, dtype, n_inputs, n_index)
+    x = np.zeros((max(n_inputs, 1), batch), _NP[dtype])
+    k = np.zeros((max(n_index, 1), batch), np.int32)
+    check(lib.tg_synth_ctr(m, C.byref(_args(m, dims, dtype)), int(seed), int(first), int(batch),
+                           x.ctypes.data_as(C.c_void_p), k.ctypes.data_as(C.POINTER(C.c_int32))))
+    return x[:n_inputs], k[:n_index]
+
+
+def synth_ctr_device(model, x, k, dims=None, dtype: str | None = None, seed: int = 0, first: int = 0,
+                     batch: int | None = None, stream=None):
+    """Writes samples [first, first + batch) into device tensors x [n_inputs][batch]
+    and k [n_index][batch] (either may be None when the model has no such columns)
+    on `stream` (tg_synth_ctr_device)."""
+    import torch
+    m = model_id(model)
+    dtype = dtype or DEFAULT_DTYPE[m]
+    if batch is None:
+        batch = (x if x is not None else k).shape[-1]
+    s = stream if stream is not None else torch.cuda.current_stream()
+    check(lib.tg_synth_ctr_device(m, C.byref(_args(m, dims, dtype)), int(seed), int(first), int(batch),
+                                  None if x is None else C.c_void_p(x.data_ptr()),
+                                  None if k is None else C.cast(C.c_void_p(k.data_ptr()), C.POINTER(C.c_int32)),
+                                  C.c_void_p(s.cuda_stream)))
+
+
 class Program:
     """A compiled tape: batch forward/backward + GD on the GPU (tg_compile)."""
 

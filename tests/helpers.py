@@ -93,3 +93,45 @@ def replay(rec, dtype="f64", n_params=1):
 def tdtype(dt):
     import torch
     return torch.float64 if dt == "f64" else torch.float32
+
+
+# ---- independent restatement of the counter-based generator (tg_synth.cuh) ----
+M0, M1, W0, W1 = 0xD2511F53, 0xCD9E8D57, 0x9E3779B9, 0xBB67AE85
+
+
+def philox4x32_10(ctr, key):
+    """Philox4x32-10 over numpy uint32 arrays: ctr (4, n), key (2, n) -> (4, n)."""
+    c = [np.asarray(v, np.uint64) for v in ctr]
+    k0, k1 = (np.asarray(v, np.uint64) for v in key)
+    m32 = np.uint64(0xFFFFFFFF)
+    for _ in range(10):
+        p0 = np.uint64(M0) * c[0]
+        p1 = np.uint64(M1) * c[2]
+        h0, l0 = p0 >> np.uint64(32), p0 & m32
+        h1, l1 = p1 >> np.uint64(32), p1 & m32
+        c = [h1 ^ c[1] ^ k0, l1, h0 ^ c[3] ^ k1, l0]
+        k0 = (k0 + np.uint64(W0)) & m32
+        k1 = (k1 + np.uint64(W1)) & m32
+    return [v.astype(np.uint32) for v in c]
+
+
+def ctr_draws(seed, samples, n_draws):
+    """u64 draws [n_draws][len(samples)]: draw j of sample s = word j % 2 of
+    Philox(key = seed, counter = (s, j / 2))."""
+    s = np.asarray(samples, np.uint64)
+    key = (np.full_like(s, seed & 0xFFFFFFFF), np.full_like(s, seed >> 32))
+    out = []
+    for p in range((n_draws + 1) // 2):
+        ctr = (s & np.uint64(0xFFFFFFFF), s >> np.uint64(32), np.full_like(s, p & 0xFFFFFFFF), np.full_like(s, p >> 32))
+        w = [v.astype(np.uint64) for v in philox4x32_10(ctr, key)]
+        out.append(w[0] | (w[1] << np.uint64(32)))
+        out.append(w[2] | (w[3] << np.uint64(32)))
+    return out[:n_draws]
+
+
+def unit53(u):
+    return (u >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+
+
+def below(u, n):
+    return np.array([(int(v) * n) >> 64 for v in u], np.int64)

@@ -218,3 +218,69 @@ def test_memory_budget_bounds_staged_workspace(name, dims):
     assert p.chunk_samples(100) == 100
     p.set_memory_budget(0)
     assert p.workspace_size(1 << 20) == big
+
+
+def test_philox_known_answers():
+    """The test-side Philox4x32-10 against the Random123 known-answer vectors."""
+    from helpers import philox4x32_10
+    cases = [((0, 0, 0, 0), (0, 0), (0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8)),
+             ((0xFFFFFFFF,) * 4, (0xFFFFFFFF,) * 2, (0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD)),
+             ((0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344), (0xA4093822, 0x299F31D0),
+              (0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1))]
+    for ctr, key, want in cases:
+        got = philox4x32_10([np.array([v]) for v in ctr], [np.array([v]) for v in key])
+        assert [int(g[0]) for g in got] == list(want)
+
+
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_counter_synth_matches_restatement_and_is_split_invariant(dt):
+    """tg_synth_ctr: every integer draw (Zipf ids, labels)
+    and every uniform equals the independent numpy restatement bit for bit;
+    any split of the sample range gives the same bits."""
+    from helpers import below, ctr_draws, unit53
+    seed, first, b = 0x1234_5678_9ABC, 1000, 700
+    # uniforms: Fig. 1 leaves U[-4, 4] (one fma), wide-MLP pixels U[0, 1) and labels
+    x, _ = tg.synth_ctr("fig1", dtype="f64", seed=seed, first=first, batch=b)
+    d = ctr_draws(seed, np.arange(first, first + b), 2)
+    want = [np.array([np.float64(8.0) * u + np.float64(-4.0) for u in unit53(d[j])]) for j in range(2)]
+    # fma(8, u, -4) is exact for 53-bit u (8u is exact), so the plain numpy expression matches it
+    assert np.array_equal(x[0], want[0]) and np.array_equal(x[1], want[1])
+    dims = [20, 8, 8, 7]
+    x, k = tg.synth_ctr("wide_mlp", dims, dt, seed=seed, first=first, batch=b)
+    d = ctr_draws(seed, np.arange(first, first + b), 21)
+    for c in range(20):
+        assert np.array_equal(x[c], unit53(d[c]).astype(x.dtype))
+    assert np.array_equal(k[0], below(d[20], 7))
+    # Zipf ids: inverse CDF over p_k ∝ k^-s (s = 1.1, V = 27)
+    _, k = tg.synth_ctr("char_mlp", dtype="f32", seed=seed, first=first, batch=b)
+    p = np.arange(1, 28, dtype=np.float64) ** -1.1
+    cdf = np.cumsum(p) / p.sum()
+    d = ctr_draws(seed, np.arange(first, first + b), 4)
+    for c in range(4):
+        assert np.array_equal(k[c], np.searchsorted(cdf, unit53(d[c]), side="right"))
+    # split invariance for every model
+    for m, dm in [("fig1", None), ("moons", None), ("char_mlp", None), ("gpt", [17, 8, 16, 2, 2, 32]), ("wide_mlp", dims)]:
+        xa, ka = tg.synth_ctr(m, dm, dt, seed=9, first=0, batch=1000)
+        xb, kb = tg.synth_ctr(m, dm, dt, seed=9, first=333, batch=401)
+        assert np.array_equal(xa[:, 333:734], xb) and np.array_equal(ka[:, 333:734], kb)
+
+
+def test_counter_synth_math_accuracy():
+    """Moons: the generator's own cos/sin/log polynomials (tg_synth.cuh) against
+    libm through the restated draws: x = arc(theta) + N(0, 0.1) noise agrees to
+    a few ulp of 1, labels exactly."""
+    from helpers import below, ctr_draws, unit53
+    b = 20000
+    x, _ = tg.synth_ctr("moons", dtype="f64", seed=77, first=5, batch=b)
+    d = ctr_draws(77, np.arange(5, 5 + b), 6)
+    second = below(d[0], 2) == 1
+    th = np.pi * unit53(d[1])
+    a, c = np.cos(th), np.sin(th)
+    a = np.where(second, 1.0 - a, a)
+    c = np.where(second, 0.5 - c, c)
+
+    def noise(u1, u2):
+        return 0.1 * np.sqrt(-2.0 * np.log(1.0 - unit53(u1))) * np.cos(2 * np.pi * unit53(u2))
+    assert np.max(np.abs(x[0] - (a + noise(d[2], d[3])))) < 2e-15
+    assert np.max(np.abs(x[1] - (c + noise(d[4], d[5])))) < 2e-15
+    assert np.array_equal(x[2], np.where(second, 1.0, -1.0))

@@ -558,3 +558,59 @@ def test_sequential_accumulation_chunks_vs_oracle(name, dims, b, budget_mb):
     assert close_rel(L, L1, 1e-6, 1e-7)
     if desc.n_inputs:
         assert rel(IG, r["input_grad"]) <= 1e-4
+
+
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+@pytest.mark.parametrize("name,dims", [("fig1", None), ("moons", None), ("char_mlp", None), ("gpt", None),
+                                       ("wide_mlp", [784, 16, 16, 10])])
+def test_device_synth_bit_exact_vs_host(name, dims, dt):
+    """On-device input pipeline: tg_synth_ctr_device
+    writes the same bits as the host generator tg_synth_ctr, for a ragged
+    batch at an offset and for the same range written in two pieces."""
+    desc = tg.build_model(name, dims, dt, seed=0).describe()
+    ni, nk = desc.n_inputs, desc.n_index_inputs
+    first, b = 12345, 70001
+    xh, kh = tg.synth_ctr(name, dims, dt, seed=99, first=first, batch=b, n_inputs=ni, n_index=nk)
+    X = torch.full((max(ni, 1), b), float("nan"), device="cuda", dtype=tdtype(dt))
+    K = torch.full((max(nk, 1), b), -7, device="cuda", dtype=torch.int32)
+    tg.synth_ctr_device(name, X if ni else None, K if nk else None, dims, dt, seed=99, first=first, batch=b)
+    torch.cuda.synchronize()
+    assert np.array_equal(X.cpu().numpy()[:ni], xh) and np.array_equal(K.cpu().numpy()[:nk], kh)
+    # two pieces into column slices of one array
+    X2 = torch.zeros_like(X)
+    K2 = torch.zeros_like(K)
+    cut = 30000
+    for lo, hi in [(0, cut), (cut, b)]:
+        xs = X2[:, lo:hi].contiguous()
+        ks = K2[:, lo:hi].contiguous()
+        tg.synth_ctr_device(name, xs if ni else None, ks if nk else None, dims, dt, seed=99, first=first + lo,
+                            batch=hi - lo)
+        X2[:, lo:hi] = xs
+        K2[:, lo:hi] = ks
+    torch.cuda.synchronize()
+    assert torch.equal(X2[:ni], X[:ni]) and torch.equal(K2[:nk], K[:nk])
+
+
+@pytest.mark.parametrize("name,dt,b", [("moons", "f64", 4096), ("char_mlp", "f32", 4096)])
+def test_train_on_device_generated_batches(name, dt, b):
+    """A GD step over a device-generated batch equals the step over the same
+    batch generated on the host and uploaded, bit for bit, and matches the
+    oracle."""
+    desc = tg.build_model(name, None, dt, seed=1).describe()
+    ni, nk = desc.n_inputs, desc.n_index_inputs
+    xh, kh = tg.synth_ctr(name, None, dt, seed=5, first=0, batch=b, n_inputs=ni, n_index=nk)
+    X = torch.empty((max(ni, 1), b), device="cuda", dtype=tdtype(dt))
+    K = torch.empty((max(nk, 1), b), device="cuda", dtype=torch.int32)
+    tg.synth_ctr_device(name, X if ni else None, K if nk else None, None, dt, seed=5, first=0, batch=b)
+    prog = tg.Program(desc)
+    tdt = tdtype(dt)
+    P = torch.tensor(desc.param_values(), device="cuda", dtype=tdt)
+    Ld = torch.zeros(b, device="cuda", dtype=tdt)
+    Gd = torch.zeros(max(desc.n_params, 1), device="cuda", dtype=tdt)
+    prog.forward_backward(X if ni else None, K if nk else None, b, P, Ld, None, Gd)   # inputs never left the GPU
+    torch.cuda.synchronize()
+    L1, G1 = Ld.cpu().double().numpy(), Gd.cpu().double().numpy()[:desc.n_params]
+    L2, _, G2 = run(prog, desc, xh, kh, desc.param_values(), b, want_igrad=False)
+    assert np.array_equal(G1, G2) and np.array_equal(L1, L2)
+    r = oracle.run(desc, xh.astype(np.float64), kh, desc.param_values(), threads=os.cpu_count() or 8)
+    assert rel(G1, r["grad_sum"]) <= TOL[dt]
