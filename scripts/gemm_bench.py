@@ -43,9 +43,14 @@ def run(engine, M, N, K, a_kmaj, b_nmaj, A, B, Cm, reps):
     return e0.elapsed_time(e1) / reps
 
 
+SHAPES_SHORTK = [("c3_l1_k30", 200, 262144, 30, True, True), ("c5_dx3_k10", 1024, 1048576, 10, False, True),
+                 ("c5_fwd3_m10", 10, 1048576, 1024, True, True), ("c5_dw3_m10", 10, 1024, 1048576, True, False),
+                 ("c4_m64_k64", 64, 524288, 64, True, True), ("c4_m64_k256", 64, 524288, 256, True, True)]
 out = {}
 if os.environ.get("GB_SET") == "cfg4":
     SHAPES = SHAPES_CFG4
+if os.environ.get("GB_SET") == "shortk":
+    SHAPES = SHAPES_SHORTK
 for name, M, N, K, ak, bn in SHAPES:
     A, B = mat(M, N, K, ak, bn)
     Am = A.view(M, K) if ak else A.view(K, M).t()
