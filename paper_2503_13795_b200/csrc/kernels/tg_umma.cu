@@ -1201,8 +1201,105 @@ std::uint32_t umma_ctas_per_slice(std::uint32_t M, std::uint32_t N) {
   return ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
 }
 
+// ---------------------------------------------------------------------------
+// Short reductions (K <= 32) on the FP32 pipe: k_gemm_shortk.  With one
+// k-tile per output tile the tensor-core kernels are bound by their per-tile
+// fixed cost (TMA round trip, hi/lo split, TMEM drain, staged epilogue: cfg3's
+// 200 x 30 layer ran at 275 us for 210 MB of output).  Here a CTA owns 64
+// rows x 256 samples: the A tile sits in shared memory (warp-uniform
+// broadcast reads), each thread keeps 4 k-rows of its 4 samples (float4 loads
+// straight from HBM, 512 B per warp) in registers and accumulates 16 rows x 4
+// samples with FFMA; the epilogue stores whole 512-byte row segments.  fp32
+// FMA over K <= 32 is as accurate as the 3xTF32 split (no TF32 rounding).
+constexpr int kSkM = 64, kSkN = 256, kSkRows = 16;
+
+template <bool AK>
+__global__ void __launch_bounds__(256, 2) k_gemm_shortk(GemmArgs<float> g) {
+  __shared__ __align__(16) float As[kSkM][32 + 4];
+  const int tid = threadIdx.x;
+  const std::uint32_t m0 = blockIdx.y * kSkM;
+  for (int i = tid; i < kSkM * 32; i += 256) {
+    int mm, kk;
+    if (AK) { mm = i >> 5; kk = i & 31; } else { kk = i / kSkM; mm = i % kSkM; }
+    const std::uint32_t gm = m0 + mm;
+    float v = 0.f;
+    if (gm < g.M && static_cast<std::uint32_t>(kk) < g.K)
+      v = AK ? g.A[std::size_t(gm) * g.lda + kk] : g.A[std::size_t(kk) * g.lda + gm];
+    As[mm][kk] = v;
+  }
+  __syncthreads();
+  const int mg = tid >> 6;
+  const std::size_t n = std::size_t(blockIdx.x) * kSkN + 4 * (tid & 63);
+  if (n >= g.N) return;
+  float acc[kSkRows][4];
+#pragma unroll
+  for (int r = 0; r < kSkRows; ++r)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[r][e] = 0.f;
+  for (std::uint32_t k0 = 0; k0 < g.K; k0 += 4) {
+    float4 b[4];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+      b[kk] = k0 + kk < g.K ? __ldg(reinterpret_cast<const float4*>(g.B + std::size_t(k0 + kk) * g.ldb + n))
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int r = 0; r < kSkRows; ++r) {
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[mg * kSkRows + r][k0]);
+      const float av[4] = {a0.x, a0.y, a0.z, a0.w};
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        acc[r][0] = fmaf(av[kk], b[kk].x, acc[r][0]);
+        acc[r][1] = fmaf(av[kk], b[kk].y, acc[r][1]);
+        acc[r][2] = fmaf(av[kk], b[kk].z, acc[r][2]);
+        acc[r][3] = fmaf(av[kk], b[kk].w, acc[r][3]);
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < kSkRows; ++r) {
+    const std::uint32_t m = m0 + mg * kSkRows + r;
+    if (m >= g.M) break;
+    float a4[4] = {acc[r][0], acc[r][1], acc[r][2], acc[r][3]};
+    float* dst = g.C + std::size_t(m) * g.ldc + n;
+    if (g.epi == kEpiBiasAct) {
+      const float bv = g.bias ? g.bias[m] : 0.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) a4[e] += bv;
+      if (g.act) {
+        float h4[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) h4[e] = act_fwd<float>(g.act, a4[e]);
+        *reinterpret_cast<float4*>(g.C2 + std::size_t(m) * g.ldc + n) = make_float4(h4[0], h4[1], h4[2], h4[3]);
+        if (g.no_z) continue;   // z has no reader
+      }
+    } else if (g.dact) {
+      const float4 o = *reinterpret_cast<const float4*>(g.C2 + std::size_t(m) * g.ldc + n);
+      const float h4[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) a4[e] = act_bwd_h<float>(g.dact, a4[e], h4[e]);
+    } else if (g.beta) {
+      const float4 o = *reinterpret_cast<const float4*>(dst);
+      a4[0] += o.x; a4[1] += o.y; a4[2] += o.z; a4[3] += o.w;
+    }
+    *reinterpret_cast<float4*>(dst) = make_float4(a4[0], a4[1], a4[2], a4[3]);
+  }
+}
+
+bool shortk_ok(const GemmArgs<float>& g) {
+  static const bool on = !(std::getenv("TG_SHORTK") && std::getenv("TG_SHORTK")[0] == '0');
+  auto al = [](const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15) == 0; };
+  return on && !g.mem && !g.no_pair && g.epi != kEpiSplitK && g.K <= 32 && g.b_nmaj && g.N % 4 == 0 &&
+         g.ldb % 4 == 0 && g.ldc % 4 == 0 && al(g.B) && al(g.C) && (!g.C2 || al(g.C2));
+}
+
 cudaError_t launch_gemm_umma(const GemmArgs<float>& g0, std::uint32_t splits, cudaStream_t st) {
   if (g0.M == 0 || g0.N == 0) return cudaSuccess;
+  if (shortk_ok(g0)) {
+    const dim3 grid((g0.N + kSkN - 1) / kSkN, (g0.M + kSkM - 1) / kSkM);
+    if (g0.a_kmaj) k_gemm_shortk<true><<<grid, 256, 0, st>>>(g0);
+    else k_gemm_shortk<false><<<grid, 256, 0, st>>>(g0);
+    return cudaGetLastError();
+  }
   // TMA-fed path: operands that satisfy the tensor-map rules (16-byte aligned
   // base and row stride); split-K slices start on 32-element k boundaries so a
   // k-tile never reads into the next slice (TMA zero-fills only past K).
