@@ -27,13 +27,18 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, ctr=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     desc = tg.build_model("moons").describe()
     b = 1000
-    x, k = tg.synth_batch("moons", batch=b, seed=4)
     lo, hi = shard(b, rank, world)
+    if ctr:   # each rank generates only its own shard (counter-based generator, §8f row 2)
+        xs, ks = tg.synth_ctr("moons", seed=4, first=lo, batch=hi - lo)
+        x = np.zeros((xs.shape[0], b)); x[:, lo:hi] = xs
+        k = np.zeros((0, b), np.int32)
+    else:
+        x, k = tg.synth_batch("moons", batch=b, seed=4)
     params = torch.tensor(desc.param_values(), dtype=torch.float64)
     grad = torch.zeros(desc.n_params, dtype=torch.float64)
 
@@ -62,11 +67,15 @@ def test_shard_covers_batch():
         shard(10, 2, 2)
 
 
-def test_world_size_2_gloo_equals_full_batch():
+@pytest.mark.parametrize("ctr", [False, True])
+def test_world_size_2_gloo_equals_full_batch(ctr):
+    """ctr: every rank generates its own shard with the counter-based
+    generator (no data exchange); the full-batch reference generates samples
+    [0, b) in one call."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, q, ctr)) for r in range(2)]
     for p in ps:
         p.start()
     res = q.get(timeout=180)
@@ -76,7 +85,7 @@ def test_world_size_2_gloo_equals_full_batch():
     np.testing.assert_array_equal(res[0], res[1])          # replicas stay identical
     # single-process reference: three full-batch steps
     desc = tg.build_model("moons").describe()
-    x, k = tg.synth_batch("moons", batch=1000, seed=4)
+    x, k = tg.synth_ctr("moons", seed=4, first=0, batch=1000) if ctr else tg.synth_batch("moons", batch=1000, seed=4)
     p = desc.param_values().copy()
     for _ in range(3):
         g = oracle.run(desc, x, k, p)["grad_sum"]
