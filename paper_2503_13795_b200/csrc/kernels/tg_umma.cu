@@ -733,60 +733,6 @@ __global__ void __launch_bounds__(kTThreads, 1) k_umma_tma_p(GemmArgs<float> g, 
       asm volatile("bar.sync 1, %0;" ::"n"(kConvThreads));
       const std::uint32_t n = tl.n0 + 4 * lane;
       const bool vec = (g.ldc % 4 == 0) && (g.epi != kEpiSplitK || g.N % 4 == 0);
-      // Fast path (full 128-column tile, float4 rows, no split-K): the rows of
-      // this warp go out in groups of four whose global operands (bias, the
-      // dX epilogue's h, the accumulated C) are all loaded before any store,
-      // so the loads' latency overlaps instead of serialising per row (the
-      // per-row bias load was 13% of this kernel's stall samples, r05c).
-      if (vec && g.epi != kEpiSplitK && tl.n0 + BN <= g.N) {
-        constexpr int kRowsW = BM / (kConvThreads / 32);
-#pragma unroll
-        for (int j0 = 0; j0 < kRowsW; j0 += 4) {
-          float4 v[4], o[4];
-          float bv[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int r = cw + (j0 + j) * (kConvThreads / 32);
-            const std::uint32_t m = tl.m0 + r;
-            const bool ok = m < g.M;
-            v[j] = *reinterpret_cast<const float4*>(etile + r * kLd + 4 * lane);
-            bv[j] = (g.epi == kEpiBiasAct && g.bias && ok) ? __ldg(g.bias + m) : 0.f;
-            o[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (ok && g.epi == kEpiAccum && (g.dact || g.beta)) {
-              const float* src = g.dact ? g.C2 + (tl.c2_off + m) * g.ldc + n : g.C + (tl.c_off + m) * g.ldc + n;
-              o[j] = *reinterpret_cast<const float4*>(src);
-            }
-          }
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int r = cw + (j0 + j) * (kConvThreads / 32);
-            const std::uint32_t m = tl.m0 + r;
-            if (m >= g.M) continue;
-            float a4[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
-            const float o4[4] = {o[j].x, o[j].y, o[j].z, o[j].w};
-            float* dst = g.C + (tl.c_off + m) * g.ldc + n;
-            if (g.epi == kEpiBiasAct) {
-#pragma unroll
-              for (int e = 0; e < 4; ++e) a4[e] += bv[j];
-              if (g.act) {
-                float h4[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) h4[e] = act_fwd<float>(g.act, a4[e]);
-                *reinterpret_cast<float4*>(g.C2 + (tl.c2_off + m) * g.ldc + n) = make_float4(h4[0], h4[1], h4[2], h4[3]);
-                if (g.no_z) continue;   // z has no reader
-              }
-            } else if (g.epi == kEpiAccum && g.dact) {
-#pragma unroll
-              for (int e = 0; e < 4; ++e) a4[e] = act_bwd_h<float>(g.dact, a4[e], o4[e]);
-            } else if (g.epi == kEpiAccum && g.beta) {
-#pragma unroll
-              for (int e = 0; e < 4; ++e) a4[e] += o4[e];
-            }
-            *reinterpret_cast<float4*>(dst) = make_float4(a4[0], a4[1], a4[2], a4[3]);
-          }
-        }
-        continue;
-      }
       for (int r = cw; r < BM; r += kConvThreads / 32) {
         const std::uint32_t m = tl.m0 + r;
         if (m >= g.M || n >= g.N) continue;
@@ -1092,59 +1038,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
     asm volatile("bar.sync 1, %0;" ::"n"(kPConv));
     const int cw = (tid - 64) >> 5;
     const bool vec = (g.ldc % 4 == 0) && (g.epi != kEpiSplitK || g.N % 4 == 0);
-    // fast path (full 256-column tile, float4 rows, no split-K): four row
-    // segments' global operands are loaded before any of their stores (see
-    // k_umma_tma_p)
-    const bool fast = vec && g.epi != kEpiSplitK && static_cast<std::uint32_t>(n0) + kPN <= g.N;
-    constexpr int kSegW = 2 * BM / (kPConv / 32);   // row segments (row, half) per warp
-#pragma unroll
-    for (int j0 = 0; fast && j0 < kSegW; j0 += 4) {
-      float4 v[4], o[4];
-      float bv[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int r = cw + ((j0 + j) >> 1) * (kPConv / 32), hlf = (j0 + j) & 1;
-        const std::uint32_t m = static_cast<std::uint32_t>(m0 + r);
-        const std::uint32_t n = static_cast<std::uint32_t>(n0 + hlf * 128) + 4 * lane;
-        const bool ok = m < g.M;
-        v[j] = *reinterpret_cast<const float4*>(tile + r * kLd + hlf * 128 + 4 * lane);
-        bv[j] = (g.epi == kEpiBiasAct && g.bias && ok) ? __ldg(g.bias + m) : 0.f;
-        o[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (ok && g.epi == kEpiAccum && (g.dact || g.beta)) {
-          const float* src = g.dact ? g.C2 + (c2_off + m) * g.ldc + n : g.C + (c_off + m) * g.ldc + n;
-          o[j] = *reinterpret_cast<const float4*>(src);
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int r = cw + ((j0 + j) >> 1) * (kPConv / 32), hlf = (j0 + j) & 1;
-        const std::uint32_t m = static_cast<std::uint32_t>(m0 + r);
-        const std::uint32_t n = static_cast<std::uint32_t>(n0 + hlf * 128) + 4 * lane;
-        if (m >= g.M) continue;
-        float a4[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
-        const float o4[4] = {o[j].x, o[j].y, o[j].z, o[j].w};
-        float* dst = g.C + (c_off + m) * g.ldc + n;
-        if (g.epi == kEpiBiasAct) {
-#pragma unroll
-          for (int e = 0; e < 4; ++e) a4[e] += bv[j];
-          if (g.act) {
-            float h4[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) h4[e] = act_fwd<float>(g.act, a4[e]);
-            *reinterpret_cast<float4*>(g.C2 + (c2_off + m) * g.ldc + n) = make_float4(h4[0], h4[1], h4[2], h4[3]);
-            if (g.no_z) continue;   // z has no reader
-          }
-        } else if (g.epi == kEpiAccum && g.dact) {
-#pragma unroll
-          for (int e = 0; e < 4; ++e) a4[e] = act_bwd_h<float>(g.dact, a4[e], o4[e]);
-        } else if (g.epi == kEpiAccum && g.beta) {
-#pragma unroll
-          for (int e = 0; e < 4; ++e) a4[e] += o4[e];
-        }
-        *reinterpret_cast<float4*>(dst) = make_float4(a4[0], a4[1], a4[2], a4[3]);
-      }
-    }
-    for (int r = cw; !fast && r < BM; r += kPConv / 32) {
+    for (int r = cw; r < BM; r += kPConv / 32) {
       const std::uint32_t m = static_cast<std::uint32_t>(m0 + r);
       if (m >= g.M) continue;
 #pragma unroll
