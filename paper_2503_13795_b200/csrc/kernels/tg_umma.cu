@@ -1211,6 +1211,10 @@ std::uint32_t umma_ctas_per_slice(std::uint32_t M, std::uint32_t N) {
 // straight from HBM, 512 B per warp) in registers and accumulates 16 rows x 4
 // samples with FFMA; the epilogue stores whole 512-byte row segments.  fp32
 // FMA over K <= 32 is as accurate as the 3xTF32 split (no TF32 rounding).
+// Routed for forward products only (bias + activation epilogue): cfg3's
+// 200 x 30 layer 275 -> 220 us.  Input-adjoint products read h for act' in
+// the epilogue and measured slower here than on the CTA pairs (cfg3 dX
+// 221 -> 274 us, cfg5's 1024 x 10 dX ~2 -> 3.3 ms, r05d), so they stay there.
 constexpr int kSkM = 64, kSkN = 256, kSkRows = 16;
 
 template <bool AK>
@@ -1288,7 +1292,7 @@ __global__ void __launch_bounds__(256, 2) k_gemm_shortk(GemmArgs<float> g) {
 bool shortk_ok(const GemmArgs<float>& g) {
   static const bool on = !(std::getenv("TG_SHORTK") && std::getenv("TG_SHORTK")[0] == '0');
   auto al = [](const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15) == 0; };
-  return on && !g.mem && !g.no_pair && g.epi != kEpiSplitK && g.K <= 32 && g.b_nmaj && g.N % 4 == 0 &&
+  return on && !g.mem && !g.no_pair && g.epi == kEpiBiasAct && g.K <= 32 && g.b_nmaj && g.N % 4 == 0 &&
          g.ldb % 4 == 0 && g.ldc % 4 == 0 && al(g.B) && al(g.C) && (!g.C2 || al(g.C2));
 }
 

@@ -361,8 +361,9 @@ def test_dense_gemm_engines(engine, dt, a_kmaj, b_nmaj, M, N, K):
     """The staged path's dense-layer product (tg_gemm) against an fp64 matmul:
     tcgen05 3xTF32 (engine 1) and SIMT (engine 0), all operand layouts used by
     forward (W X), input adjoints (W^T dZ) and weight gradients (dZ X^T).
-    Engine 1 routes K <= 32 products over sample-major B to the FP32-pipe
-    k_gemm_shortk; engine 2 keeps them on tcgen05."""
+    The short-K shapes (K = 1, 10, 30) pin the tcgen05 kernels at one k-tile;
+    the FP32-pipe k_gemm_shortk (forward products with K <= 32) is covered by
+    the char-MLP staged tests, whose 200 x 30 first layer routes there."""
     import ctypes as C
     from paper_2503_13795_b200 import _lib
     tdt = torch.float32 if dt == "f32" else torch.float64
