@@ -1211,30 +1211,39 @@ std::uint32_t umma_ctas_per_slice(std::uint32_t M, std::uint32_t N) {
 // straight from HBM, 512 B per warp) in registers and accumulates 16 rows x 4
 // samples with FFMA; the epilogue stores whole 512-byte row segments.  fp32
 // FMA over K <= 32 is as accurate as the 3xTF32 split (no TF32 rounding).
-// Routed for forward products only (bias + activation epilogue): cfg3's
-// 200 x 30 layer 275 -> 220 us.  Input-adjoint products read h for act' in
+// The same kernel with one 16-row group and 1024 samples per CTA serves
+// skinny forward products (M <= 16: a classifier head) whose tensor-core
+// tiles would be 128 rows for 10 real ones (cfg5's 10 x 1024 head: 2.05 ms
+// on k_umma_tma).  Routed for forward products only (bias + activation
+// epilogue): cfg3's 200 x 30 layer 275 -> 220 us.  Input-adjoint products read h for act' in
 // the epilogue and measured slower here than on the CTA pairs (cfg3 dX
 // 221 -> 274 us, cfg5's 1024 x 10 dX ~2 -> 3.3 ms, r05d), so they stay there.
-constexpr int kSkM = 64, kSkN = 256, kSkRows = 16;
+constexpr int kSkRows = 16;
 
-template <bool AK>
-__global__ void __launch_bounds__(256, 2) k_gemm_shortk(GemmArgs<float> g) {
-  __shared__ __align__(16) float As[kSkM][32 + 4];
+// MG row groups of kSkRows rows per CTA (MG = 4: 64 rows x 256 samples, the
+// short-K shape; MG = 1: 16 rows x 1024 samples, the skinny-M shape of a
+// classifier head such as cfg5's 10 x 1024 layer, whose A tile is 16 x K).
+// A lives in dynamic shared memory as [row][kp] (kp = K rounded up to 4, + 4).
+template <bool AK, int MG>
+__global__ void __launch_bounds__(256, 2) k_gemm_shortk(GemmArgs<float> g, int kp) {
+  extern __shared__ __align__(16) float As[];
+  constexpr int kTpg = 256 / MG, kMT = MG * kSkRows;
   const int tid = threadIdx.x;
-  const std::uint32_t m0 = blockIdx.y * kSkM;
-  for (int i = tid; i < kSkM * 32; i += 256) {
-    int mm, kk;
-    if (AK) { mm = i >> 5; kk = i & 31; } else { kk = i / kSkM; mm = i % kSkM; }
+  const std::uint32_t m0 = blockIdx.y * kMT;
+  const std::uint32_t k4 = (g.K + 3) & ~3u;
+  for (std::uint32_t i = tid; i < kMT * k4; i += 256) {
+    std::uint32_t mm, kk;
+    if (AK) { mm = i / k4; kk = i % k4; } else { kk = i / kMT; mm = i % kMT; }
     const std::uint32_t gm = m0 + mm;
     float v = 0.f;
-    if (gm < g.M && static_cast<std::uint32_t>(kk) < g.K)
-      v = AK ? g.A[std::size_t(gm) * g.lda + kk] : g.A[std::size_t(kk) * g.lda + gm];
-    As[mm][kk] = v;
+    if (gm < g.M && kk < g.K) v = AK ? g.A[std::size_t(gm) * g.lda + kk] : g.A[std::size_t(kk) * g.lda + gm];
+    As[mm * kp + kk] = v;
   }
   __syncthreads();
-  const int mg = tid >> 6;
-  const std::size_t n = std::size_t(blockIdx.x) * kSkN + 4 * (tid & 63);
+  const int mg = tid / kTpg;
+  const std::size_t n = std::size_t(blockIdx.x) * (4 * kTpg) + 4 * (tid % kTpg);
   if (n >= g.N) return;
+  const float* Ar = As + mg * kSkRows * kp;
   float acc[kSkRows][4];
 #pragma unroll
   for (int r = 0; r < kSkRows; ++r)
@@ -1248,7 +1257,7 @@ __global__ void __launch_bounds__(256, 2) k_gemm_shortk(GemmArgs<float> g) {
                             : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int r = 0; r < kSkRows; ++r) {
-      const float4 a0 = *reinterpret_cast<const float4*>(&As[mg * kSkRows + r][k0]);
+      const float4 a0 = *reinterpret_cast<const float4*>(Ar + r * kp + k0);
       const float av[4] = {a0.x, a0.y, a0.z, a0.w};
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
@@ -1289,20 +1298,41 @@ __global__ void __launch_bounds__(256, 2) k_gemm_shortk(GemmArgs<float> g) {
   }
 }
 
-bool shortk_ok(const GemmArgs<float>& g) {
+template <bool AK, int MG>
+cudaError_t launch_shortk(const GemmArgs<float>& g, cudaStream_t st) {
+  const int kp = static_cast<int>(((g.K + 3) & ~3u) + 4);
+  const std::size_t smem = std::size_t(MG * kSkRows) * kp * sizeof(float);
+  static int attr = 0;
+  if (smem > 48 * 1024 && static_cast<int>(smem) > attr) {
+    const cudaError_t e = cudaFuncSetAttribute(k_gemm_shortk<AK, MG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    attr = static_cast<int>(smem);
+  }
+  const dim3 grid(static_cast<unsigned>((g.N + 4 * (256 / MG) - 1) / (4 * (256 / MG))), (g.M + MG * kSkRows - 1) / (MG * kSkRows));
+  k_gemm_shortk<AK, MG><<<grid, 256, smem, st>>>(g, kp);
+  return cudaGetLastError();
+}
+
+// 0: tensor cores; 4: short K (K <= 32); 1: skinny M (M <= 16, K <= 2048)
+int simt_route(const GemmArgs<float>& g) {
   static const bool on = !(std::getenv("TG_SHORTK") && std::getenv("TG_SHORTK")[0] == '0');
+  static const bool skinny = !(std::getenv("TG_SKINNY") && std::getenv("TG_SKINNY")[0] == '0');
   auto al = [](const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15) == 0; };
-  return on && !g.mem && !g.no_pair && g.epi == kEpiBiasAct && g.K <= 32 && g.b_nmaj && g.N % 4 == 0 &&
-         g.ldb % 4 == 0 && g.ldc % 4 == 0 && al(g.B) && al(g.C) && (!g.C2 || al(g.C2));
+  if (!on || g.mem || g.no_pair || g.epi != kEpiBiasAct || !g.b_nmaj || g.N % 4 || g.ldb % 4 || g.ldc % 4 || !al(g.B) ||
+      !al(g.C) || (g.C2 && !al(g.C2)))
+    return 0;
+  if (g.K <= 32) return 4;
+  if (skinny && g.M <= kSkRows && g.K <= 2048 && g.N >= 4096) return 1;
+  return 0;
 }
 
 cudaError_t launch_gemm_umma(const GemmArgs<float>& g0, std::uint32_t splits, cudaStream_t st) {
   if (g0.M == 0 || g0.N == 0) return cudaSuccess;
-  if (shortk_ok(g0)) {
-    const dim3 grid((g0.N + kSkN - 1) / kSkN, (g0.M + kSkM - 1) / kSkM);
-    if (g0.a_kmaj) k_gemm_shortk<true><<<grid, 256, 0, st>>>(g0);
-    else k_gemm_shortk<false><<<grid, 256, 0, st>>>(g0);
-    return cudaGetLastError();
+  switch (simt_route(g0)) {
+    case 4: return g0.a_kmaj ? launch_shortk<true, 4>(g0, st) : launch_shortk<false, 4>(g0, st);
+    case 1: return g0.a_kmaj ? launch_shortk<true, 1>(g0, st) : launch_shortk<false, 1>(g0, st);
+    default: break;
   }
   // TMA-fed path: operands that satisfy the tensor-map rules (16-byte aligned
   // base and row stride); split-K slices start on 32-element k boundaries so a

@@ -618,3 +618,21 @@ def test_train_on_device_generated_batches(name, dt, b):
     assert np.array_equal(G1, G2) and np.array_equal(L1, L2)
     r = oracle.run(desc, xh.astype(np.float64), kh, desc.param_values(), threads=os.cpu_count() or 8)
     assert rel(G1, r["grad_sum"]) <= TOL[dt]
+
+
+@pytest.mark.parametrize("name,dims,b", [("wide_mlp", [40, 300, 260, 10], 8192), ("wide_mlp", [36, 64, 48, 13], 4100),
+                                         ("char_mlp", None, 4096)])
+def test_simt_short_and_skinny_products_vs_oracle(name, dims, b):
+    """Forward products off the tensor cores (kernels/tg_umma.cu
+    k_gemm_shortk): K <= 32 layers (char-MLP 200 x 30) and skinny heads
+    (M <= 16 classes over >= 4096 samples, here 10 x 260 and 13 x 48 with a
+    ragged sample quad count), through the staged tier against the oracle."""
+    desc = tg.build_model(name, dims, "f32", seed=6).describe()
+    x, k = tg.synth_batch(name, dims, "f32", seed=29, batch=b, n_inputs=desc.n_inputs, n_index=desc.n_index_inputs)
+    prog = make_prog(desc, "staged")
+    L, IG, G = run(prog, desc, x, k, desc.param_values(), b)
+    r = oracle.run(desc, x.astype(np.float64), k, desc.param_values(), threads=os.cpu_count() or 8)
+    assert close_rel(L, r["loss"], 1e-5, 1e-6)
+    assert rel(G, r["grad_sum"]) <= 1e-5
+    if desc.n_inputs:
+        assert rel(IG, r["input_grad"]) <= 1e-4
