@@ -166,14 +166,8 @@ struct tg_program {
     // tab[nm + p].w); the producing batch then skips its activation backward
     std::uint32_t dx_act = 0;
     bool skip_act = false;
-    // Fused bias row sums: this batch's dX epilogue (CTA pairs, dact) writes
-    // the row partials of the dz it produces into region rp_out; the batch
-    // below (bias_rp = the same region) finishes its bias gradient from them
-    // instead of re-reading its dz rows (TG_BIAS_FUSE=0: off)
-    std::int32_t rp_out = -1, bias_rp = -1;
   };
   std::vector<Batch> batches;
-  std::uint32_t n_rp = 0, rp_rows = 0;   // fused bias row-partial regions (Batch::rp_out)
   // Contended adjoint rows of the reverse levels: pushes into a row with more
   // than one pusher in a level store to temporaries (rows n_rows ..), summed
   // into the row at the end of the level: {row, assign, first temporary, count}.
@@ -825,16 +819,6 @@ void build_staged_plan(tg_program& pr) {
       for (std::uint32_t p = 0; p < nm; ++p)
         C.tab[nm + p] = uint4{0, P.dense[C.members[p]].out_row, zrow[p], pr.dplan[C.members[p]].xrow0};
       pr.batches[ab].skip_act = true;
-      {
-        static const bool fuse = !(std::getenv("TG_BIAS_FUSE") && std::getenv("TG_BIAS_FUSE")[0] == '0');
-        static const int mask = std::getenv("TG_UMMA_MASK") ? std::atoi(std::getenv("TG_UMMA_MASK")) : 7;
-        auto& Lb = pr.batches[ab];
-        if (fuse && nm == 1 && pr.tsz() == 4 && pr.umma && (mask & 2) &&
-            tgk::umma_pair_route(P.dense[C.members.front()].n_in) && pr.dplan[Lb.members.front()].db_dest0 != tgc::kNone) {
-          C.rp_out = Lb.bias_rp = static_cast<std::int32_t>(pr.n_rp++);
-          pr.rp_rows = std::max(pr.rp_rows, P.dense[Lb.members.front()].n_out);
-        }
-      }
     }
   }
   // Dense layers over input leaves read the caller's inputs array ([col][batch],
@@ -1062,11 +1046,9 @@ std::size_t grid_for(const tg_program& pr, std::size_t batch) {
 }
 
 std::size_t align_up(std::size_t x) { return (x + 255) & ~std::size_t(255); }
-// row-partial slots of a fused dX over n samples: two per 256-sample CTA-pair tile
-std::uint32_t rp_parts(std::size_t n) { return static_cast<std::uint32_t>(2 * ((n + 255) / 256)); }
 
 struct Layout {
-  std::size_t done, uv, ug, partial, gv, gg, sk, sp, rp, total;
+  std::size_t done, uv, ug, partial, gv, gg, sk, sp, total;
 };
 Layout layout(const tg_program& pr, std::size_t batch) {
   const std::size_t t = pr.tsz();
@@ -1092,7 +1074,6 @@ Layout layout(const tg_program& pr, std::size_t batch) {
       }
     L.sk = off; off = align_up(off + std::max<std::size_t>(1, sk) * t);
     L.sp = off; off = align_up(off + std::max<std::size_t>(1, std::size_t(pr.sc_groups.size()) * pr.sc_chunks * pr.sc_rmax) * t);
-    L.rp = off; off = align_up(off + std::size_t(pr.n_rp) * pr.rp_rows * rp_parts(cb) * t);
     L.total = off;
     return L;
   }
@@ -1397,11 +1378,9 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
     };
     // dX[n_in][n] (+)= W^T[n_in][n_out] . dZ[n_out][n] (one member)
     // (dact: C = the producing layer's z rows c_row, act' from its h rows = x rows)
-    auto dx_one = [&](std::uint32_t u, int beta, std::uint32_t dact, std::uint32_t c_row, T* rowpart = nullptr) -> cudaError_t {
+    auto dx_one = [&](std::uint32_t u, int beta, std::uint32_t dact, std::uint32_t c_row) -> cudaError_t {
       const tgc::Dense& D = P.dense[u];
       tgk::GemmArgs<T> g{};
-      g.rowpart = rowpart;
-      g.rp_parts = rp_parts(n);
       g.A = UV + D.w_uv;
       g.lda = D.n_in;
       g.a_kmaj = false;
@@ -1524,12 +1503,6 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
       const std::uint32_t nm = static_cast<std::uint32_t>(B.members.size());
       const tgc::Dense& D = P.dense[B.members.front()];
       const auto& dp0 = pr.dplan[B.members.front()];
-      T* const rp_base = reinterpret_cast<T*>(w + L.rp);
-      auto rp_region = [&](std::int32_t k) { return rp_base + std::size_t(k) * pr.rp_rows * rp_parts(cb); };
-      if (B.bias_rp >= 0) {   // bias gradient from the row partials the dX above left (before this stage's own dX reuses regions)
-        TG_CUDA_TRY(tgk::launch_rowpart_fin<T>(rp_region(B.bias_rp), D.n_out, rp_parts(n), acc + dp0.db_dest0, st));
-        ++pr.launches;
-      }
       if (D.act_op && !B.skip_act) {
         TG_CUDA_TRY(tgk::launch_act_bwd_batched<T>(G, V, B.d_tab, nm, D.n_out, n, cb, D.act_op, st));
         ++pr.launches;
@@ -1560,8 +1533,6 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
           g.dact = B.dx_act;
           g.C2 = B.dx_act ? V : nullptr;
           g.epi = tgk::kEpiAccum;
-          g.rowpart = B.rp_out >= 0 ? rp_region(B.rp_out) : nullptr;
-          g.rp_parts = rp_parts(n);
           g.mem = B.d_tab + nm;
           g.zs = 1;
           TG_CUDA_TRY(tgk::launch_gemm_umma(g, nm, st));
@@ -1596,12 +1567,10 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
       for (std::uint32_t p = 0; p < nm; ++p) {
         const std::uint32_t u = B.members[p];
         // zeroed rows above follow the batch's beta; members that only assign keep their store
-        if (!dx_done)
-          TG_CUDA_TRY(dx_one(u, B.beta ? pr.dplan[u].beta : 0, B.dx_act, B.tab[nm + p].z,
-                             B.rp_out >= 0 ? rp_region(B.rp_out) : nullptr));
+        if (!dx_done) TG_CUDA_TRY(dx_one(u, B.beta ? pr.dplan[u].beta : 0, B.dx_act, B.tab[nm + p].z));
         if (!dw_done && pr.dplan[u].dw_dest0 != tgc::kNone) TG_CUDA_TRY(dw_one(u));
       }
-      if (dp0.db_dest0 != tgc::kNone && B.bias_rp < 0) {
+      if (dp0.db_dest0 != tgc::kNone) {
         TG_CUDA_TRY(tgk::launch_rowsum_batched<T>(G, B.d_tab, nm, D.n_out, n, cb, acc + dp0.db_dest0, sk,
                                                   (L.sp - L.sk) / sizeof(T), st));   // split-K scratch, free here
         ++pr.launches;

@@ -812,20 +812,6 @@ __global__ void k_rowsum_fin(const T* part, std::uint32_t rows, std::uint32_t ch
   dst[j] += t;
 }
 
-// Bias gradients from the per-(row, half tile) partials of a fused dX epilogue
-// (GemmArgs::rowpart): a warp per row, lanes stride the slots, xor tree.
-template <class T>
-__global__ void __launch_bounds__(256) k_rowpart_fin(const T* part, std::uint32_t rows, std::uint32_t parts, T* dst) {
-  const std::uint32_t r = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (r >= rows) return;
-  const T* p = part + std::size_t(r) * parts;
-  T t = 0;
-  for (std::uint32_t c = lane; c < parts; c += 32) t += p[c];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-  if (lane == 0) dst[r] += t;
-}
-
 template <class T>
 __global__ void k_zero_rows(T* X, const std::uint32_t* rows, std::size_t n, std::size_t ld) {
   const std::size_t s = std::size_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -962,15 +948,6 @@ cudaError_t launch_level_range(const RangeArgs<T>& a, cudaStream_t st) {
   k_level_range<T><<<dim3(count, static_cast<unsigned>((a.n + 127) / 128)), 128, 0, st>>>(a);
   return cudaGetLastError();
 }
-
-template <class T>
-cudaError_t launch_rowpart_fin(const T* part, std::uint32_t rows, std::uint32_t parts, T* dst, cudaStream_t st) {
-  if (rows == 0) return cudaSuccess;
-  k_rowpart_fin<T><<<(rows + 7) / 8, 256, 0, st>>>(part, rows, parts, dst);
-  return cudaGetLastError();
-}
-template cudaError_t launch_rowpart_fin<float>(const float*, std::uint32_t, std::uint32_t, float*, cudaStream_t);
-template cudaError_t launch_rowpart_fin<double>(const double*, std::uint32_t, std::uint32_t, double*, cudaStream_t);
 
 template <class T>
 cudaError_t launch_gemm(const GemmArgs<T>& g, std::uint32_t splits, cudaStream_t st) {

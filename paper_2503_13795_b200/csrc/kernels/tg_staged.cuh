@@ -95,12 +95,6 @@ struct GemmArgs {
   std::uint32_t dact;
   // kEpiBiasAct with act: store only H (C2); the pre-activation Z has no reader
   bool no_z;
-  // kEpiAccum with dact (CTA-pair kernel, one member): per (row, 128-sample
-  // half tile) sums of the written dz go to rowpart[row * rp_parts + slot],
-  // the bias gradient of the layer below without re-reading dz (rp_parts =
-  // 2 * 256-sample tiles; every slot is written)
-  T* rowpart;
-  std::uint32_t rp_parts;
 };
 
 // Table-scatter (kind-1) batch terms grouped by (adjoint row a, index column f).
@@ -118,11 +112,6 @@ cudaError_t launch_scatter(const ScatterGroup* groups, std::uint32_t n_groups, s
                            T* part, std::uint32_t n_chunks, T* acc, cudaStream_t st);
 
 template <class T> cudaError_t launch_tape_range(const RangeArgs<T>& a, cudaStream_t st);
-// dst[r] += sum_c part[r * parts + c], one warp per row, fixed order
-template <class T> cudaError_t launch_rowpart_fin(const T* part, std::uint32_t rows, std::uint32_t parts, T* dst,
-                                                  cudaStream_t st);
-// true when launch_gemm_umma runs an fp32 product of M rows on the CTA-pair kernel
-bool umma_pair_route(std::uint32_t M);
 // One dependency level (fwd_begin/fwd_end with kRFwd, else bwd_begin/bwd_end):
 // one instruction per CTA column, 128 samples per CTA.
 template <class T> cudaError_t launch_level_range(const RangeArgs<T>& a, cudaStream_t st);

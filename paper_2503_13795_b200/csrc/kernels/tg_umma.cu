@@ -1048,7 +1048,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
     for (int r = cw; r < BM; r += kPConv / 32) {
       const std::uint32_t m = static_cast<std::uint32_t>(m0 + r);
       if (m >= g.M) continue;
-      float rs[2] = {0.f, 0.f};   // this lane's share of the row's dz sums (GemmArgs::rowpart)
 #pragma unroll
       for (int hlf = 0; hlf < 2; ++hlf) {
         const std::uint32_t n = static_cast<std::uint32_t>(n0 + hlf * 128) + 4 * lane;
@@ -1081,7 +1080,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
           }
   #pragma unroll
           for (int e = 0; e < 4; ++e) a4[e] = act_bwd_h<float>(g.dact, a4[e], h4[e]);
-          for (int e = 0; e < cnt; ++e) rs[hlf] += a4[e];
         } else if (g.epi == kEpiAccum && g.beta) {
           if (vec && cnt == 4) {
             const float4 o = *reinterpret_cast<const float4*>(dst);
@@ -1093,15 +1091,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
         if (g.no_z && g.act && g.epi == kEpiBiasAct) continue;   // z has no reader
         if (vec && cnt == 4) *reinterpret_cast<float4*>(dst) = make_float4(a4[0], a4[1], a4[2], a4[3]);
         else for (int e = 0; e < cnt; ++e) dst[e] = a4[e];
-      }
-      if (g.rowpart) {   // warp-uniform: every lane is back here
-#pragma unroll
-        for (int hlf = 0; hlf < 2; ++hlf) {
-          float t = rs[hlf];
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-          if (lane == 0) g.rowpart[std::size_t(m) * g.rp_parts + 2 * blockIdx.y + hlf] = t;
-        }
       }
     }
   }
@@ -1155,7 +1144,6 @@ bool use_pair(std::uint32_t M) {
 
 cudaError_t launch_tma_kernel(const GemmArgs<float>& g, std::uint32_t z, const CUtensorMap& ta, const CUtensorMap& tb,
                               bool a_mn, bool b_mn, cudaStream_t st) {
-  if (g.rowpart && !(use_pair(g.M) && !g.no_pair && g.epi == kEpiAccum && g.dact)) return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
     for (cudaError_t e : {cudaFuncSetAttribute(k_umma_tma<kTStagesMax>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1214,8 +1202,6 @@ cudaError_t launch_tma_kernel(const GemmArgs<float>& g, std::uint32_t z, const C
   return cudaGetLastError();
 }
 }  // namespace
-
-bool umma_pair_route(std::uint32_t M) { return use_pair(M); }
 
 std::uint32_t umma_ctas_per_slice(std::uint32_t M, std::uint32_t N) {
   if (use_pair(M)) return 2 * ((M + 2 * BM - 1) / (2 * BM)) * ((N + kPN - 1) / kPN);
@@ -1424,7 +1410,7 @@ cudaError_t launch_gemm_umma(const GemmArgs<float>& g0, std::uint32_t splits, cu
     }
     release();
   }
-  if (g0.mem || g0.rowpart) return cudaErrorInvalidValue;   // batched products / fused row partials need the TMA path
+  if (g0.mem) return cudaErrorInvalidValue;   // batched products need the TMA path
   const GemmArgs<float>& g = g0;
   // register-staged fallback (operands TMA cannot describe): its accumulator
   // is never drained, so its bias grows with K; beyond K = 1024 per launch the
