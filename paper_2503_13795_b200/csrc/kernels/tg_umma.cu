@@ -729,11 +729,6 @@ __global__ void __launch_bounds__(kTThreads, 1) k_umma_tma_p(GemmArgs<float> g, 
 #pragma unroll
         for (int j = 0; j < kCols; j += 4)
           *reinterpret_cast<float4*>(etile + r * kLd + c0 + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
-        // the row's bias rides in the tile's padding column: one load per row,
-        // issued with the tile stores instead of one dependent load per row
-        // of the store loop (13% of this kernel's stall samples, r05c)
-        if (c0 == 0 && g.epi == kEpiBiasAct)
-          etile[r * kLd + BN] = (g.bias && tl.m0 + r < static_cast<int>(g.M)) ? g.bias[tl.m0 + r] : 0.f;
       }
       asm volatile("bar.sync 1, %0;" ::"n"(kConvThreads));
       const std::uint32_t n = tl.n0 + 4 * lane;
@@ -746,7 +741,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_umma_tma_p(GemmArgs<float> g, 
         float* dst = g.epi == kEpiSplitK ? g.C + (std::size_t(tl.z) * g.M + m) * g.N + n : g.C + (tl.c_off + m) * g.ldc + n;
         const int cnt = min(4u, g.N - n);
         if (g.epi == kEpiBiasAct) {
-          const float bv = etile[r * kLd + BN];
+          const float bv = g.bias ? g.bias[m] : 0.f;
 #pragma unroll
           for (int e = 0; e < 4; ++e) a4[e] += bv;
           if (g.act) {
@@ -1039,8 +1034,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
 #pragma unroll
       for (int j = 0; j < kCols; j += 4)
         *reinterpret_cast<float4*>(tile + r * kLd + c0 + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
-      if (c0 == 0 && g.epi == kEpiBiasAct)   // the row's bias in the padding column (see k_umma_tma_p)
-        tile[r * kLd + kPN] = (g.bias && m0 + r < static_cast<int>(g.M)) ? g.bias[m0 + r] : 0.f;
     }
     asm volatile("bar.sync 1, %0;" ::"n"(kPConv));
     const int cw = (tid - 64) >> 5;
@@ -1058,7 +1051,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
                                          : g.C + (c_off + m) * g.ldc + n;
         const int cnt = min(4u, g.N - n);
         if (g.epi == kEpiBiasAct) {
-          const float bv = tile[r * kLd + kPN];
+          const float bv = g.bias ? g.bias[m] : 0.f;
 #pragma unroll
           for (int e = 0; e < 4; ++e) a4[e] += bv;
           if (g.act) {
