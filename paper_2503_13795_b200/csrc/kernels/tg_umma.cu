@@ -548,18 +548,12 @@ __host__ __device__ constexpr std::uint32_t persist_smem() {
 
 __global__ void __launch_bounds__(kTThreads, 1) k_umma_tma_p(GemmArgs<float> g, const __grid_constant__ CUtensorMap tmA,
                                                       const __grid_constant__ CUtensorMap tmB, int a_mn, int b_mn,
-                                                      std::uint32_t mt, std::uint32_t nt, std::uint32_t n_tiles,
-                                                      int a_reuse) {
+                                                      std::uint32_t mt, std::uint32_t nt, std::uint32_t n_tiles) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* etile = reinterpret_cast<float*>(smem + kPStages * kTStage);
   std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + persist_smem() - 1024 - 512);
   std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 3 * kPStages + 4);
-  // A reuse: when a stage's next A tile (the shared weight block) is the one
-  // it already holds converted (same m0, k0, member offset: K <= 64 products
-  // walk the same k-tiles through the same stages tile after tile), the
-  // producer lands only B and the converters split only B.
-  volatile std::uint32_t* askip = tmem_slot + 1;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   auto full = [&](int s) { return smem_u32(&bars[s]); };
   auto conv = [&](int s) { return smem_u32(&bars[kPStages + s]); };
@@ -625,21 +619,16 @@ __global__ void __launch_bounds__(kTThreads, 1) k_umma_tma_p(GemmArgs<float> g, 
     // ===== TMA producer =====
     if (lane == 0) {
       std::uint32_t gt = 0;
-      int lm[kPStages], lk[kPStages], la[kPStages];
-      for (int s = 0; s < kPStages; ++s) lm[s] = lk[s] = la[s] = -1;
       for (std::uint32_t L = blockIdx.x; L < n_tiles; L += gridDim.x) {
         const Tile tl = tile_of(L);
         for (std::uint32_t t = 0; t < tl.T; ++t, ++gt) {
           const int s = gt % kPStages;
           if (gt >= static_cast<std::uint32_t>(kPStages)) mbar_wait2(empty(s), ((gt / kPStages) - 1) & 1);
           const std::uint32_t base = smem_u32(smem + s * kTStage);
+          mbar_expect_tx(full(s), 2 * kTTile);
           const int k0 = static_cast<int>(tl.k_begin + t * BK);
-          const bool reuse = a_reuse && lm[s] == tl.m0 && lk[s] == k0 && la[s] == tl.a_off;
-          askip[s] = reuse ? 1u : 0u;   // published by the expect-tx arrive (release) below
-          mbar_expect_tx(full(s), reuse ? kTTile : 2 * kTTile);
-          if (!reuse) tma_operand(&tmA, a_mn, base, tl.m0, k0, tl.a_off, full(s));
+          tma_operand(&tmA, a_mn, base, tl.m0, k0, tl.a_off, full(s));
           tma_operand(&tmB, b_mn, base + 2 * kTTile, tl.n0, k0, tl.b_off, full(s));
-          lm[s] = tl.m0; lk[s] = k0; la[s] = tl.a_off;
         }
       }
     }
@@ -712,10 +701,8 @@ __global__ void __launch_bounds__(kTThreads, 1) k_umma_tma_p(GemmArgs<float> g, 
         const int s = gt % kPStages;
         mbar_wait2(full(s), (gt / kPStages) & 1);
         unsigned char* base = smem + s * kTStage;
-        const int op0 = askip[s] ? 1 : 0;
 #pragma unroll
         for (int op = 0; op < 2; ++op) {
-          if (op < op0) continue;
           float4* hi = reinterpret_cast<float4*>(base + op * 2 * kTTile);
           float4* lo = reinterpret_cast<float4*>(base + op * 2 * kTTile + kTTile);
 #pragma unroll 4
@@ -1193,9 +1180,7 @@ cudaError_t launch_tma_kernel(const GemmArgs<float>& g, std::uint32_t z, const C
     }
     const std::uint32_t grid = std::min<std::uint32_t>(tiles, static_cast<std::uint32_t>(nsm));
     if (grid == 0) return cudaSuccess;
-    static const bool a_reuse = !(std::getenv("TG_PERSIST_AREUSE") && std::getenv("TG_PERSIST_AREUSE")[0] == '0');
-    k_umma_tma_p<<<grid, kTThreads, persist_smem(), st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0, mt, nt, tiles,
-                                                          a_reuse ? 1 : 0);
+    k_umma_tma_p<<<grid, kTThreads, persist_smem(), st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0, mt, nt, tiles);
     return cudaGetLastError();
   }
   const dim3 grid((g.M + BM - 1) / BM, (g.N + BN - 1) / BN, z);
