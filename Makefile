@@ -34,7 +34,7 @@ $(BUILD)/%.o: $(PKG)/csrc/host/%.cpp $(HDRS) $(BUILD)/tg_math.inc
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
 $(PKG)/libtg.so: $(CU_OBJ) $(CXX_OBJ)
-	$(NVCC) $(ARCH) -shared -o $@ $^ -L$(CUDA)/lib64 -lcudart -lnvrtc -Xlinker -rpath,$(CUDA)/lib64
+	$(NVCC) $(ARCH) -shared -o $@ $^ -L$(CUDA)/lib64 -lcudart -lnvrtc -ldl -Xlinker -rpath,$(CUDA)/lib64
 
 oracle:
 	$(MAKE) -C oracle
@@ -43,7 +43,10 @@ clean:
 	rm -rf $(BUILD) $(PKG)/libtg.so
 	$(MAKE) -C oracle clean
 
-tools: build/fp_peak
+tools: build/fp_peak build/mma_peak
 build/fp_peak: tools/fp_peak.cu
+	@mkdir -p $(BUILD)
+	$(NVCC) $(ARCH) -O3 $< -o $@
+build/mma_peak: tools/mma_peak.cu
 	@mkdir -p $(BUILD)
 	$(NVCC) $(ARCH) -O3 $< -o $@

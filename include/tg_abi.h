@@ -43,7 +43,8 @@ typedef enum tg_status {
   TG_FORMAT = 6,            /* FormatError (errors.hpp:29-31)                            */
   TG_IO = 7,                /* IoError (errors.hpp:34-36)                                */
   TG_CUDA = 8,              /* CUDA runtime failure (no reference equivalent)            */
-  TG_UNSUPPORTED = 9        /* program shape outside what a kernel path supports         */
+  TG_UNSUPPORTED = 9,       /* program shape outside what a kernel path supports         */
+  TG_NCCL = 10              /* NCCL failure or NCCL not loadable (no reference equivalent) */
 } tg_status;
 
 typedef enum tg_dtype { TG_F64 = 0, TG_F32 = 1 } tg_dtype;
@@ -224,6 +225,27 @@ tg_status tg_forward_backward(tg_program_t p, const void* inputs, const int32_t*
 tg_status tg_gd_update(tg_program_t p, void* params, const void* grad_sum, double gamma,
                        size_t global_batch, tg_stream_t stream);
 
+/* ---- data parallelism over NCCL (north_star (d)) -------
+ * One process per GPU; the batch is sharded, parameters are replicated.  After
+ * tg_forward_backward of its shard, every rank calls tg_allreduce_gd_step:
+ * one in-place ncclAllReduce(sum) of grad_sum (n_params scalars, the
+ * tape dtype) on `stream`, then params -= gamma * grad_sum / global_batch
+ * (sgd_step) on every rank, so replicas stay identical
+ * without a broadcast.  comm == NULL is the single-GPU case (the update only).
+ * NCCL is bound at run time (dlopen: the already-loaded libnccl.so.2 first,
+ * then TG_NCCL_LIB, then the system soname); TG_NCCL when absent or failing.
+ * Communicators come from tg_nccl_comm_init (rank 0's tg_nccl_get_unique_id
+ * bytes shared with every rank out of band) or are any ncclComm_t. */
+typedef void* tg_comm_t;   /* ncclComm_t */
+#define TG_NCCL_UNIQUE_ID_BYTES 128
+tg_status tg_nccl_get_unique_id(void* id_out /* TG_NCCL_UNIQUE_ID_BYTES */);
+tg_status tg_nccl_comm_init(int nranks, const void* id, int rank, tg_comm_t* out);
+tg_status tg_nccl_comm_destroy(tg_comm_t comm);
+/* NCCL_VERSION_CODE of the bound library, 0 when none could be bound. */
+int tg_nccl_version(void);
+tg_status tg_allreduce_gd_step(tg_program_t p, void* params, void* grad_sum, double gamma, size_t global_batch,
+                               tg_comm_t comm, tg_stream_t stream);
+
 /* Fused single-GPU step: forward_backward + gd_update. */
 tg_status tg_train_step(tg_program_t p, const void* inputs, const int32_t* index_inputs,
                         size_t batch, void* params, void* loss_out, void* grad_sum,
@@ -276,11 +298,13 @@ tg_status tg_load_range(tg_dtype dtype, void* values, void* grads, size_t count,
 size_t tg_snapshot_bytes(tg_dtype dtype, size_t count, int with_grads);
 tg_status tg_save_snapshot(tg_dtype dtype, const void* values, const void* grads, size_t count, void* out,
                            size_t out_bytes, size_t* written);
-/* Reads the header into dtype_out / count_out / with_grads_out, checks it
- * against `capacity`, then writes values (and grads when present and
- * grads != NULL). */
-tg_status tg_load_snapshot(const void* in, size_t in_bytes, void* values, void* grads, size_t capacity,
-                           tg_dtype* dtype_out, size_t* count_out, int* with_grads_out);
+/* Reads the header, checks it against the target range (`dtype`, room for
+ * `capacity` scalars of that dtype in values / grads) before writing anything
+ * (a precision mismatch is TG_FORMAT, a larger count TG_CAPACITY), then writes
+ * values (and grads when present and grads != NULL) and reports the count and
+ * grads flag. */
+tg_status tg_load_snapshot(const void* in, size_t in_bytes, tg_dtype dtype, void* values, void* grads,
+                           size_t capacity, size_t* count_out, int* with_grads_out);
 
 /* Synchronises `stream` and reports the first per-sample domain violation
  * seen since the last check as TG_DOMAIN with the reference message. */

@@ -125,6 +125,13 @@ def _reflib():
                                   C.POINTER(C.c_uint64), P, P, P, P, P, C.POINTER(C.c_uint32)]
         lib.ref_run.restype = C.c_int
         lib.ref_run.argtypes = [C.c_int, P, C.c_int, P, P, P, sz, P, P, P, C.c_int]
+        lib.ref_params.restype = C.c_int
+        lib.ref_params.argtypes = [C.c_int, P, C.c_uint64, C.c_int, P, C.POINTER(C.c_uint32)]
+        lib.ref_synth.restype = C.c_int
+        lib.ref_synth.argtypes = [C.c_int, P, C.c_int, C.c_uint64, sz, P, P, C.POINTER(C.c_uint32),
+                                  C.POINTER(C.c_uint32)]
+        lib.ref_describe.restype = C.c_int
+        lib.ref_describe.argtypes = [C.c_int, P, C.c_uint64, C.c_int, P, P]
         lib.ref_recipe.restype = C.c_int
         lib.ref_recipe.argtypes = [C.c_uint64, sz, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
         lib.ref_recipe_fetch.restype = None
@@ -165,6 +172,53 @@ def ref_build(model: int, dims, seed: int, dtype: str, x1, idx1):
         raise OracleError(st, lib.ref_last_error().decode())
     return {"op": ops, "child_offset": off, "child": ch[:e.value], "constant": cs, "value": vals,
             "root": root.value}
+
+
+def ref_params(model: int, dims, dtype: str, seed: int = 0):
+    """Initial parameters of `model` recorded on the reference tape (make_params)."""
+    lib = _reflib()
+    n = C.c_uint32()
+    dm = _dims(dims)
+    st = lib.ref_params(model, _d(dm), seed, _DT[dtype], None, C.byref(n))
+    if st:
+        raise OracleError(st, lib.ref_last_error().decode())
+    out = np.zeros(max(n.value, 1))
+    st = lib.ref_params(model, _d(dm), seed, _DT[dtype], _d(out), C.byref(n))
+    if st:
+        raise OracleError(st, lib.ref_last_error().decode())
+    return out[:n.value]
+
+
+def ref_synth(model: int, dims, dtype: str, seed: int, batch: int):
+    """Synthetic batch (x [n_inputs][batch] float64, idx [n_index][batch] int32),
+    the same bits as the product's tg_synth_batch for the same seed."""
+    lib = _reflib()
+    dm = _dims(dims)
+    ni, nk = C.c_uint32(), C.c_uint32()
+    st = lib.ref_synth(model, _d(dm), _DT[dtype], seed, batch, None, None, C.byref(ni), C.byref(nk))
+    if st:
+        raise OracleError(st, lib.ref_last_error().decode())
+    x = np.zeros((max(ni.value, 1), batch))
+    k = np.zeros((max(nk.value, 1), batch), np.int32)
+    st = lib.ref_synth(model, _d(dm), _DT[dtype], seed, batch, _d(x), _d(k), C.byref(ni), C.byref(nk))
+    if st:
+        raise OracleError(st, lib.ref_last_error().decode())
+    return x[:ni.value], k[:nk.value]
+
+
+def ref_describe(model: int, dims, dtype: str, seed: int = 0, x1=None):
+    """A template sample recorded on the UNMODIFIED reference tape with the
+    drop-in adapter (include/tg_from_tapegrad.hpp: tgadapt::Recording +
+    describe): a tape.TapeDesc the product compiles like its own recordings."""
+    from paper_2503_13795_b200 import _lib as plib
+    from paper_2503_13795_b200.tape import _desc_from_c
+    lib = _reflib()
+    d = plib.tg_tape_desc()
+    x = None if x1 is None else np.ascontiguousarray(x1, np.float64)
+    st = lib.ref_describe(model, _d(_dims(dims)), seed, _DT[dtype], _d(x), C.byref(d))
+    if st:
+        raise OracleError(st, lib.ref_last_error().decode())
+    return _desc_from_c(d)
 
 
 def ref_run(model: int, dims, dtype: str, params, x, idx, threads: int = 1):

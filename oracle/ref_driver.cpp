@@ -30,6 +30,7 @@ template <> tapegrad::ValueRef tapegrad::Tape<float>::leaf(float v) {
 #include <string>
 #include <thread>
 
+#include "tg_from_tapegrad.hpp"
 #include "tg_models.hpp"
 
 namespace testsupport {
@@ -46,6 +47,7 @@ struct RefBuilder {
   using VR = tapegrad::ValueRef;
   tapegrad::Tape<S>& t;
   std::vector<std::pair<std::uint32_t, std::uint32_t>> inputs;  // (col, node)
+  tgadapt::Recording* rec = nullptr;   // drop-in description (tg_from_tapegrad.hpp)
 
   VR param(S v) { return t.leaf(v); }
   VR constant(S v) { return t.leaf(v); }
@@ -55,11 +57,14 @@ struct RefBuilder {
     return r;
   }
   // A re-recorded sample wires the selected node directly.
-  VR gather(VR first, std::uint32_t stride, std::uint32_t, std::uint32_t, std::uint32_t off, std::int32_t idx) {
+  VR gather(VR first, std::uint32_t stride, std::uint32_t n_rows, std::uint32_t col, std::uint32_t off,
+            std::int32_t idx) {
+    if (rec) return rec->select(t, first, stride, n_rows, col, off, idx);
     return VR{first.index + stride * static_cast<std::uint32_t>(idx) + off};
   }
   // Softmax shift: a non-differentiable constant leaf.
   VR stopgrad_max(std::span<const VR> xs) {
+    if (rec) return rec->stopgrad_max(t, xs);
     S m = t.value_of(xs[0]);
     for (std::size_t i = 1; i < xs.size(); ++i) m = std::max(m, t.value_of(xs[i]));
     return t.leaf(m);
@@ -194,6 +199,104 @@ int ref_build(int model, const std::uint32_t* dims, std::uint64_t seed, int dtyp
         }
         child_off[tape.size()] = off;
       }
+      return 0;
+    };
+    return dtype == 0 ? go(double{}) : go(float{});
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+/// Initial parameter values of `model` recorded on a reference tape
+/// (make_params over tapegrad::Tape<S>, values read back as S).  Call with
+/// out = NULL to get the count.  The bench's reference arm takes its
+/// parameters from here, never from the product library.
+int ref_params(int model, const std::uint32_t* dims, std::uint64_t seed, int dtype, double* out,
+               std::uint32_t* n_out) {
+  try {
+    auto go = [&](auto tag) -> int {
+      using S = decltype(tag);
+      const tgm::Dims D = tgm::Dims::resolve(model, dims);
+      tapegrad::Tape<S> tape(tapegrad::TapeConfig{.capacity = 1 << 16});
+      RefBuilder<S> b{tape, {}};
+      const auto P = tgm::make_params(b, model, D, seed);
+      std::uint32_t n = 0;
+      for (const auto& blk : P.blocks)
+        for (auto v : blk.v) {
+          if (out) out[n] = static_cast<double>(tape.value_of(v));
+          ++n;
+        }
+      *n_out = n;
+      return 0;
+    };
+    return dtype == 0 ? go(double{}) : go(float{});
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+/// Synthetic batch of `model` (tgm::synth, the SURVEY.md §8d generators) in
+/// the tape's scalar type, widened to double: x [n_inputs][batch], idx
+/// [n_index][batch].  Same bits as the product's tg_synth_batch for the same
+/// seed, so both bench arms see identical samples.
+int ref_synth(int model, const std::uint32_t* dims, int dtype, std::uint64_t seed, std::size_t batch, double* x,
+              std::int32_t* idx, std::uint32_t* n_inputs, std::uint32_t* n_index) {
+  try {
+    const tgm::Dims D = tgm::Dims::resolve(model, dims);
+    std::uint32_t ni = 0, nk = 0;
+    tgm::io_shape(model, D, ni, nk);
+    *n_inputs = ni;
+    *n_index = nk;
+    if (!x && !idx) return 0;
+    auto go = [&](auto tag) {
+      using S = decltype(tag);
+      std::vector<S> xs(std::max<std::size_t>(std::size_t(ni) * batch, 1));
+      tgm::synth<S>(model, D, seed, batch, xs.data(), idx);
+      for (std::size_t i = 0; i < std::size_t(ni) * batch; ++i) x[i] = static_cast<double>(xs[i]);
+    };
+    if (dtype == 0) go(double{}); else go(float{});
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+/// A template sample of `model` recorded on the UNMODIFIED reference tape with
+/// the drop-in adapter's side record (tgadapt::Recording: selections and max
+/// shifts), described by tgadapt::describe into *out (arrays valid until the
+/// next call on this thread).  Template index inputs are idx[c] = c mod rows
+/// (distinct rows per table); template inputs x[c] = x1[c] when given.
+int ref_describe(int model, const std::uint32_t* dims, std::uint64_t seed, int dtype, const double* x1,
+                 tg_tape_desc* out) {
+  thread_local tgadapt::DescArrays keep;
+  try {
+    auto go = [&](auto tag) -> int {
+      using S = decltype(tag);
+      const tgm::Dims D = tgm::Dims::resolve(model, dims);
+      std::uint32_t ni = 0, nk = 0;
+      tgm::io_shape(model, D, ni, nk);
+      std::vector<double> xs(std::max<std::uint32_t>(ni, 1), 0.5);
+      if (x1) std::copy(x1, x1 + ni, xs.begin());
+      std::vector<std::int32_t> ks(std::max<std::uint32_t>(nk, 1));
+      for (std::uint32_t c = 0; c < nk; ++c) ks[c] = static_cast<std::int32_t>(c);
+      const std::uint32_t rows = model == tgm::kWideMlp ? D.d[3] : D.d[0];   // classes / vocabulary
+      for (std::uint32_t c = 0; c < nk; ++c) ks[c] %= static_cast<std::int32_t>(rows);
+      tapegrad::Tape<S> tape(tapegrad::TapeConfig{.capacity = 1 << 24});
+      tgadapt::Recording rec;
+      RefBuilder<S> b{tape, {}, &rec};
+      const auto P = tgm::make_params(b, model, D, seed);
+      std::vector<std::pair<std::uint32_t, tgadapt::LeafRole>> roles;
+      std::uint32_t pid = 0;
+      for (const auto& blk : P.blocks)
+        for (auto v : blk.v) roles.push_back({v.index, {TG_LEAF_PARAM, pid++}});
+      const tgm::Sample smp{xs.data(), ks.data()};
+      const auto root = tgm::build_sample(b, model, D, P, smp);
+      for (auto [col, node] : b.inputs) roles.push_back({node, {TG_LEAF_INPUT, col}});
+      keep = tgadapt::describe(tape, root.index, roles, &rec);
+      *out = keep.desc;
       return 0;
     };
     return dtype == 0 ? go(double{}) : go(float{});

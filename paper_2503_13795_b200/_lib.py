@@ -20,7 +20,7 @@ TG_OP_STOPGRAD_MAX = 64
 STATUS = {
     0: "TG_OK", 1: "TG_INVALID_ARGUMENT", 2: "TG_CAPACITY", 3: "TG_INVALID_HANDLE",
     4: "TG_INVALID_CHECKPOINT", 5: "TG_DOMAIN", 6: "TG_FORMAT", 7: "TG_IO", 8: "TG_CUDA",
-    9: "TG_UNSUPPORTED",
+    9: "TG_UNSUPPORTED", 10: "TG_NCCL",
 }
 
 
@@ -127,7 +127,12 @@ def _load():
         "tg_load_range": (st, [st, P, P, sz, P, sz]),
         "tg_snapshot_bytes": (sz, [st, sz, C.c_int]),
         "tg_save_snapshot": (st, [st, P, P, sz, P, sz, C.POINTER(sz)]),
-        "tg_load_snapshot": (st, [P, sz, P, P, sz, C.POINTER(st), C.POINTER(sz), C.POINTER(C.c_int)]),
+        "tg_load_snapshot": (st, [P, sz, C.c_int, P, P, sz, C.POINTER(sz), C.POINTER(C.c_int)]),
+        "tg_nccl_get_unique_id": (st, [P]),
+        "tg_nccl_comm_init": (st, [C.c_int, P, C.c_int, C.POINTER(P)]),
+        "tg_nccl_comm_destroy": (st, [P]),
+        "tg_nccl_version": (C.c_int, []),
+        "tg_allreduce_gd_step": (st, [P, P, P, C.c_double, sz, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

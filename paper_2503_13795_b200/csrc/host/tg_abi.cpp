@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "tg_abi.h"
+#include "tg_comm.hpp"
 #include "tg_jit.hpp"
 #include "tg_models.hpp"
 #include "tg_program.hpp"
@@ -92,6 +93,8 @@ struct TgBuilder {
 
 }  // namespace
 
+tg_status tgcomm::fail_status(tg_status s, const std::string& msg) { return fail(s, msg); }
+
 struct tg_recorder {
   tg_dtype dtype;
   std::unique_ptr<tg::Tape<double>> t64;
@@ -126,7 +129,7 @@ struct tg_program {
   unsigned long long* d_err_key = nullptr;
   double* d_err_val = nullptr;
   std::uint32_t* d_err_op = nullptr;
-  unsigned* d_ticket = nullptr;   // last-CTA ticket of the generated epilogue (self-resetting)
+  unsigned* d_ticket = nullptr;   // grid-barrier words of the cooperative JIT form (TG_JIT_COOP=1 only)
   // launch configuration
   bool smem = true;
   unsigned S = 128;
@@ -1662,7 +1665,7 @@ tg_status run_fused(tg_program& pr, const void* inputs, const std::int32_t* idx,
   ja.params = static_cast<const T*>(params);
   ja.consts = static_cast<const T*>(pr.d_consts);
   ja.UVw = UV;
-  ja.tickets = pr.d_ticket;
+  ja.tickets = pr.jit.coop ? pr.d_ticket : reinterpret_cast<unsigned*>(w + L.done);   // see tg_jit.cpp fuse_wait
   ja.partial2 = UG;
   ja.grad_sum = static_cast<T*>(grad_sum);
   ja.gd_params = static_cast<T*>(gd_params);
@@ -1918,6 +1921,7 @@ const char* tg_status_name(tg_status s) {
     case TG_IO: return "TG_IO";
     case TG_CUDA: return "TG_CUDA";
     case TG_UNSUPPORTED: return "TG_UNSUPPORTED";
+    case TG_NCCL: return "TG_NCCL";
   }
   return "?";
 }
@@ -2135,6 +2139,8 @@ tg_status tg_compile(const tg_tape_desc* desc, tg_program_t* out) {
 
 tg_status tg_program_info_get(tg_program_t p, tg_program_info* info) {
   return guard([&] {
+    if (!p) return fail(TG_INVALID_HANDLE, "tg_program_info_get: NULL program");
+    if (!info) return fail(TG_INVALID_ARGUMENT, "tg_program_info_get: NULL info");
     const tgc::Program& P = p->P;
     tg_program_info i{};
     i.n_params = P.n_params;
@@ -2158,6 +2164,8 @@ tg_status tg_program_info_get(tg_program_t p, tg_program_info* info) {
 }
 
 tg_status tg_program_order(tg_program_t p, const uint32_t** order, uint32_t* n) {
+  if (!p) return fail(TG_INVALID_HANDLE, "tg_program_order: NULL program");
+  if (!order || !n) return fail(TG_INVALID_ARGUMENT, "tg_program_order: NULL argument");
   *order = p->P.order.data();
   *n = static_cast<uint32_t>(p->P.order.size());
   return TG_OK;
@@ -2181,6 +2189,8 @@ tg_status tg_chunk_samples(tg_program_t p, size_t batch, size_t* samples) {
 
 tg_status tg_workspace_size(tg_program_t p, size_t batch, size_t* bytes) {
   return guard([&] {
+    if (!p) return fail(TG_INVALID_HANDLE, "tg_workspace_size: NULL program");
+    if (!bytes) return fail(TG_INVALID_ARGUMENT, "tg_workspace_size: NULL bytes");
     *bytes = layout(*p, batch).total;
     return TG_OK;
   });
@@ -2199,6 +2209,8 @@ tg_status tg_forward_backward(tg_program_t p, const void* inputs, const int32_t*
 tg_status tg_gd_update(tg_program_t p, void* params, const void* grad_sum, double gamma, size_t global_batch,
                        tg_stream_t stream) {
   return guard([&] {
+    if (!p) return fail(TG_INVALID_HANDLE, "tg_gd_update: NULL program");
+    if (p->P.n_params && (!params || !grad_sum)) return fail(TG_INVALID_ARGUMENT, "tg_gd_update: NULL buffer");
     auto st = static_cast<cudaStream_t>(stream);
     if (global_batch == 0) return fail(TG_INVALID_ARGUMENT, "train_step: batch empty");
     if (p->P.dtype == TG_F64)
@@ -2209,6 +2221,21 @@ tg_status tg_gd_update(tg_program_t p, void* params, const void* grad_sum, doubl
                                         p->P.n_params, gamma, static_cast<double>(global_batch), st));
     ++p->launches;
     return TG_OK;
+  });
+}
+
+tg_status tg_allreduce_gd_step(tg_program_t p, void* params, void* grad_sum, double gamma, size_t global_batch,
+                               tg_comm_t comm, tg_stream_t stream) {
+  return guard([&] {
+    if (!p) return fail(TG_INVALID_HANDLE, "tg_allreduce_gd_step: NULL program");
+    if (global_batch == 0) return fail(TG_INVALID_ARGUMENT, "train_step: batch empty");
+    if (p->P.n_params && (!params || !grad_sum)) return fail(TG_INVALID_ARGUMENT, "tg_allreduce_gd_step: NULL buffer");
+    auto st = static_cast<cudaStream_t>(stream);
+    if (comm && p->P.n_params) {
+      std::string err;
+      if (!tgcomm::allreduce_sum(grad_sum, p->P.n_params, p->P.dtype, comm, st, err)) return fail(TG_NCCL, err);
+    }
+    return tg_gd_update(p, params, grad_sum, gamma, global_batch, stream);
   });
 }
 
@@ -2227,6 +2254,7 @@ tg_status tg_train_step(tg_program_t p, const void* inputs, const int32_t* idx, 
 
 tg_status tg_check_device_error(tg_program_t p, tg_stream_t stream, int64_t* sample_out, uint32_t* node_out) {
   return guard([&] {
+    if (!p) return fail(TG_INVALID_HANDLE, "tg_check_device_error: NULL program");
     if (!p->uploaded) return TG_OK;
     auto st = static_cast<cudaStream_t>(stream);
     TG_CUDA_TRY(cudaStreamSynchronize(st));
@@ -2257,6 +2285,7 @@ tg_status tg_check_device_error(tg_program_t p, tg_stream_t stream, int64_t* sam
 }
 
 tg_status tg_profile_enable(tg_program_t p, int on) {
+  if (!p) return fail(TG_INVALID_HANDLE, "tg_profile_enable: NULL program");
   p->profiling = on != 0;
   p->ev_used = 0;
   return TG_OK;
@@ -2264,6 +2293,8 @@ tg_status tg_profile_enable(tg_program_t p, int on) {
 
 tg_status tg_profile_read(tg_program_t p, double* ms, uint64_t* n) {
   return guard([&] {
+    if (!p) return fail(TG_INVALID_HANDLE, "tg_profile_read: NULL program");
+    if (!ms || !n) return fail(TG_INVALID_ARGUMENT, "tg_profile_read: NULL argument");
     double tot = 0;
     for (std::size_t i = 0; i < p->ev_used; ++i) {
       TG_CUDA_TRY(cudaEventSynchronize(p->ev[i].second));
@@ -2280,6 +2311,8 @@ tg_status tg_profile_read(tg_program_t p, double* ms, uint64_t* n) {
 
 tg_status tg_program_jit(tg_program_t p, const char** source, const char** log, double* compile_ms) {
   return guard([&] {
+    if (!p) return fail(TG_INVALID_HANDLE, "tg_program_jit: NULL program");
+    if (!source || !log) return fail(TG_INVALID_ARGUMENT, "tg_program_jit: NULL argument");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
       cudaGetLastError();
@@ -2651,9 +2684,10 @@ tg_status tg_save_snapshot(tg_dtype dtype, const void* values, const void* grads
   });
 }
 
-tg_status tg_load_snapshot(const void* in, size_t in_bytes, void* values, void* grads, size_t capacity,
-                           tg_dtype* dtype_out, size_t* count_out, int* with_grads_out) {
+tg_status tg_load_snapshot(const void* in, size_t in_bytes, tg_dtype dtype, void* values, void* grads, size_t capacity,
+                           size_t* count_out, int* with_grads_out) {
   return guard([&] {
+    if (dtype != TG_F64 && dtype != TG_F32) return fail(TG_INVALID_ARGUMENT, "load_snapshot: dtype");
     if (!in || in_bytes < kSnapHeader) return fail(TG_FORMAT, "load_snapshot: truncated header");
     const unsigned char* i = static_cast<const unsigned char*>(in);
     if (std::memcmp(i, "BTSG", 4) != 0) return fail(TG_FORMAT, "load_snapshot: bad magic");
@@ -2666,9 +2700,13 @@ tg_status tg_load_snapshot(const void* in, size_t in_bytes, void* values, void* 
     std::uint64_t n = 0;
     std::memcpy(&n, i + 10, 8);
     if (in_bytes != tg_snapshot_bytes(dt, n, with_grads)) return fail(TG_FORMAT, "load_snapshot: payload size mismatch");
+    // every check before the first byte is written: a cross-precision or
+    // oversized load is an error with no partial write
+    if (dt != dtype)
+      return fail(TG_FORMAT, std::string("load_snapshot: snapshot precision ") + (dt == TG_F64 ? "fp64" : "fp32") +
+                                 " differs from the target range's " + (dtype == TG_F64 ? "fp64" : "fp32"));
     if (n > capacity) return fail(TG_CAPACITY, "load_snapshot: " + std::to_string(n) + " values exceed capacity " +
                                                    std::to_string(capacity));
-    if (dtype_out) *dtype_out = dt;
     if (count_out) *count_out = n;
     if (with_grads_out) *with_grads_out = with_grads ? 1 : 0;
     const std::size_t w = width_of(dt);

@@ -22,6 +22,18 @@
 
 namespace tgj {
 namespace {
+// TG_JIT_SKIP=bwd|contract|tanh: work-skipping ablations (wrong results) that
+// exist only in a -DTG_PROFILING build; the product library ignores the variable.
+const char* profiling_skip() {
+#ifdef TG_PROFILING
+  return std::getenv("TG_JIT_SKIP");
+#else
+  return nullptr;
+#endif
+}
+}  // namespace
+
+namespace {
 
 using tgc::Instr;
 using tgc::kIndexMask;
@@ -258,7 +270,7 @@ struct Gen {
     switch (op) {
       case Relu: return "(" + z + " > (T)0 ? " + z + " : (T)0)";
       case Tanh: {
-        const char* sk = std::getenv("TG_JIT_SKIP");  // profiling-only ablation
+        const char* sk = profiling_skip();
         if (sk && std::string(sk) == "tanh") return "(" + z + ")";
         return fn(tanh_fn.c_str(), "tanhf") + "(" + z + ")";
       }
@@ -456,6 +468,19 @@ const char* kArgAliases =
     "  const T* __restrict__ UVg = A.UVg; const unsigned* __restrict__ cand = A.cand;\n"
     "  const unsigned* __restrict__ toff = A.toff; const TermC* __restrict__ terms = A.terms;\n"
     "  (void)in; (void)idx; (void)loss; (void)igrad; (void)UVg; (void)cand; (void)toff; (void)terms; (void)err_key;\n";
+
+// Prologue of a fused tg_jit_tape: wait for the previous kernel on the stream
+// (PDL), then CTA 0 resets the generated epilogue's last-CTA ticket, which
+// lives in the caller's workspace (tickets == workspace + Layout::done), so
+// launches of one program on several streams / workspaces never share it.
+// The previous launch's epilogue has completed once griddepcontrol.wait
+// returns, and this launch's epilogue only counts after this kernel is done.
+// The cooperative form keeps its grid-barrier words in the program instead.
+std::string fuse_wait(bool coop) {
+  std::string s = "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");   // params of the previous step\n";
+  if (!coop) s += "  if (blockIdx.x == 0 && threadIdx.x == 0) A.tickets[0] = 0u;   // epilogue ticket (workspace)\n";
+  return s;
+}
 
 }  // namespace
 
@@ -810,7 +835,7 @@ std::string generate(const tgc::Program& P, const JitConfig& cfg, unsigned& n_cr
   o << "extern \"C\" __global__ void __launch_bounds__(" << cfg.block;
   if (cfg.min_blocks) o << ", " << cfg.min_blocks;
   o << ") tg_jit_tape(const JitArgs A) {\n" << kArgAliases
-    << (cfg.fuse ? "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");   // params of the previous step\n" : "")
+    << (cfg.fuse ? fuse_wait(cfg.coop) : std::string())
     << fc.pro
     << (cfg.fuse ? "  const T* __restrict__ UVt = sU;\n" : "  const T* __restrict__ UVt = UVg;\n") << "  (void)UVt;\n";
   o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
@@ -877,7 +902,7 @@ std::string generate(const tgc::Program& P, const JitConfig& cfg, unsigned& n_cr
   if (G.gsm[P.root_row]) o << "      " << G.sg_(P.root_row) << " = (T)1;\n";
   else o << "      T " << G.g(P.root_row) << " = (T)1;\n";
   // profiling-only ablations (wrong results): TG_JIT_SKIP=bwd|contract
-  const char* skip = std::getenv("TG_JIT_SKIP");
+  const char* skip = profiling_skip();
   const bool skip_bwd = skip && std::string(skip) == "bwd", skip_con = skip && std::string(skip) == "contract";
   if (!skip_bwd)
     for (const Instr& in : P.bwd) {
@@ -1214,7 +1239,7 @@ std::string generate_grouped(const tgc::Program& P, const JitConfig& cfg, unsign
   o << "extern \"C\" __global__ void __launch_bounds__(" << cfg.block;
   if (cfg.min_blocks) o << ", " << cfg.min_blocks;
   o << ") tg_jit_tape(const JitArgs A) {\n" << kArgAliases
-    << (cfg.fuse ? "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");   // params of the previous step\n" : "")
+    << (cfg.fuse ? fuse_wait(cfg.coop) : std::string())
     << (late ? fc.pro : fc.pro_load)
     << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
     << "  T* sm = reinterpret_cast<T*>(smem_raw);\n"
@@ -1531,7 +1556,7 @@ std::string generate_dmma(const tgc::Program& P, const JitConfig& cfg, unsigned&
   o << "extern \"C\" __global__ void __launch_bounds__(" << cfg.block;
   if (cfg.min_blocks) o << ", " << cfg.min_blocks;
   o << ") tg_jit_tape(const JitArgs A) {\n" << kArgAliases
-    << (cfg.fuse ? "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");   // params of the previous step\n" : "")
+    << (cfg.fuse ? fuse_wait(cfg.coop) : std::string())
     << (late ? fc.pro : fc.pro_load)
     << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
     << "  T* sm = reinterpret_cast<T*>(smem_raw);\n"

@@ -27,6 +27,7 @@
 #include <cstdint>
 
 #include "tg_ops.cuh"
+#include "tg_devcache.cuh"
 #include "tg_staged.cuh"
 
 namespace tgk {
@@ -254,13 +255,14 @@ bool attn_fast_ok(const tgc::Attn& A) {
 namespace {
 template <int HD>
 cudaError_t launch_attn_hd(bool fwd, const AttnStage& a, dim3 grid, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    for (cudaError_t e : {cudaFuncSetAttribute(k_attn_fwd<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fwd_smem<HD>())),
-                          cudaFuncSetAttribute(k_attn_bwd<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bwd_smem<HD>()))})
-      if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static PerDeviceOnce attr;
+  if (const cudaError_t e0 = attr.ensure([] {
+        for (cudaError_t e : {cudaFuncSetAttribute(k_attn_fwd<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fwd_smem<HD>())),
+                              cudaFuncSetAttribute(k_attn_bwd<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bwd_smem<HD>()))})
+          if (e != cudaSuccess) return e;
+        return cudaSuccess;
+      }); e0 != cudaSuccess)
+    return e0;
   if (fwd) k_attn_fwd<HD><<<grid, kThreads, fwd_smem<HD>(), st>>>(a);
   else k_attn_bwd<HD><<<grid, kThreads, bwd_smem<HD>(), st>>>(a);
   return cudaGetLastError();

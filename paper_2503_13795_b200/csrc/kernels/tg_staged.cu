@@ -17,6 +17,7 @@
 #include <type_traits>
 
 #include "tg_ops.cuh"
+#include "tg_devcache.cuh"
 #include "tg_staged.cuh"
 
 namespace tgk {
@@ -909,13 +910,12 @@ cudaError_t launch_scatter(const ScatterGroup* groups, std::uint32_t n_groups, s
                            T* part, std::uint32_t n_chunks, T* acc, cudaStream_t st) {
   if (n_groups == 0 || n == 0) return cudaSuccess;
   const std::size_t smem = std::size_t(r_max) * 128 * sizeof(T);
-  static bool attr[2] = {false, false};
-  bool& a = attr[sizeof(T) == 8];
-  if (!a && smem > 48 * 1024) {
-    const cudaError_t e = cudaFuncSetAttribute(k_scatter_hist<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
-    a = true;
-  }
+  static PerDeviceOnce attr;
+  if (smem > 48 * 1024)
+    if (const cudaError_t e = attr.ensure([] {
+          return cudaFuncSetAttribute(k_scatter_hist<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        }); e != cudaSuccess)
+      return e;
   k_scatter_hist<T><<<dim3(n_groups, n_chunks), 128, smem, st>>>(groups, G, idx, batch, s0, n, ld, n_chunks, r_max, part);
   k_scatter_apply<T><<<(n_dests + 127) / 128, 128, 0, st>>>(uses, use_off, dests, n_dests, part, n_chunks, r_max, acc);
   return cudaGetLastError();

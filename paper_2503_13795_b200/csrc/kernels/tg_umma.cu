@@ -23,6 +23,7 @@
 #include <cstdlib>
 
 #include "tg_ops.cuh"
+#include "tg_devcache.cuh"
 #include "tg_staged.cuh"
 
 namespace tgk {
@@ -292,8 +293,17 @@ __device__ __forceinline__ std::uint64_t operand_desc(std::uint32_t base, bool m
 // drain each finished buffer into fp32 round-to-nearest register sums (one
 // output row per thread) while the tensor core fills the other one.
 constexpr int kFlush = 1;
-__device__ int g_umma_exp = 0;   // profiling ablations (wrong results): 1 skip conversion, 2 one MMA per k-step, 3 TMA ring
+// float4 epilogue stores need 16-byte aligned C / C2 bases (tg_gemm accepts any
+// device pointer: a view offset by one float must take the scalar stores)
+__device__ __forceinline__ bool c_aligned16(const GemmArgs<float>& g) {
+  return ((reinterpret_cast<std::uintptr_t>(g.C) | reinterpret_cast<std::uintptr_t>(g.C2)) & 15u) == 0;
+}
+#ifdef TG_PROFILING
+__device__ int g_umma_exp = 0;   // TG_UMMA_EXP (profiling build only) ablations (wrong results): 1 skip conversion, 2 one MMA per k-step, 3 TMA ring
                                  // only, 4 one MMA on the raw fp32 tiles (how kind::tf32 reads fp32 bits)
+#else
+constexpr int g_umma_exp = 0;    // product build: no setting can make a kernel skip work
+#endif
 constexpr int kConvThreads = 256;                 // 8 converter / drain warps
 constexpr int kTThreads = 64 + kConvThreads;      // + TMA producer + MMA issuer
 
@@ -480,7 +490,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_umma_tma(GemmArgs<float> g, co
     asm volatile("bar.sync 1, %0;" ::"n"(kConvThreads));
     const int cw = (tid - 64) >> 5;   // converter warp 0..7
     const std::uint32_t n = n0 + 4 * lane;
-    const bool vec = (g.ldc % 4 == 0) && (g.epi != kEpiSplitK || g.N % 4 == 0);
+    const bool vec = (g.ldc % 4 == 0) && (g.epi != kEpiSplitK || g.N % 4 == 0) && c_aligned16(g);
     for (int r = cw; r < BM && g_umma_exp != 5; r += kConvThreads / 32) {   // (ablation 5: no output stores)
       const std::uint32_t m = m0 + r;
       if (m >= g.M || n >= g.N) continue;
@@ -732,7 +742,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_umma_tma_p(GemmArgs<float> g, 
       }
       asm volatile("bar.sync 1, %0;" ::"n"(kConvThreads));
       const std::uint32_t n = tl.n0 + 4 * lane;
-      const bool vec = (g.ldc % 4 == 0) && (g.epi != kEpiSplitK || g.N % 4 == 0);
+      const bool vec = (g.ldc % 4 == 0) && (g.epi != kEpiSplitK || g.N % 4 == 0) && c_aligned16(g);
       for (int r = cw; r < BM; r += kConvThreads / 32) {
         const std::uint32_t m = tl.m0 + r;
         if (m >= g.M || n >= g.N) continue;
@@ -1037,7 +1047,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
     }
     asm volatile("bar.sync 1, %0;" ::"n"(kPConv));
     const int cw = (tid - 64) >> 5;
-    const bool vec = (g.ldc % 4 == 0) && (g.epi != kEpiSplitK || g.N % 4 == 0);
+    const bool vec = (g.ldc % 4 == 0) && (g.epi != kEpiSplitK || g.N % 4 == 0) && c_aligned16(g);
     for (int r = cw; r < BM; r += kPConv / 32) {
       const std::uint32_t m = static_cast<std::uint32_t>(m0 + r);
       if (m >= g.M) continue;
@@ -1094,17 +1104,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
 
 // Host: 2D tensor map of an operand view for TMA (SWIZZLE_128B, zero OOB fill).
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {   // thread-safe one-time lookup
+    PFN_cuTensorMapEncodeTiled_v12000 f = nullptr;
     cudaDriverEntryPointQueryResult q;
     void* p = nullptr;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+      f = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
     cudaGetLastError();
-  }
+    return f;
+  }();
   return fn;
 }
 
@@ -1137,17 +1146,18 @@ bool use_pair(std::uint32_t M) {
 
 cudaError_t launch_tma_kernel(const GemmArgs<float>& g, std::uint32_t z, const CUtensorMap& ta, const CUtensorMap& tb,
                               bool a_mn, bool b_mn, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    for (cudaError_t e : {cudaFuncSetAttribute(k_umma_tma<kTStagesMax>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               static_cast<int>(tma_smem(kTStagesMax))),
-                          cudaFuncSetAttribute(k_umma_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               static_cast<int>(tma_smem(1))),
-                          cudaFuncSetAttribute(k_umma_pair<kTStagesMax>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               static_cast<int>(pair_smem(kTStagesMax)))})
-      if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static PerDeviceOnce attr;
+  if (const cudaError_t e0 = attr.ensure([] {
+        for (cudaError_t e : {cudaFuncSetAttribute(k_umma_tma<kTStagesMax>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(tma_smem(kTStagesMax))),
+                              cudaFuncSetAttribute(k_umma_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(tma_smem(1))),
+                              cudaFuncSetAttribute(k_umma_pair<kTStagesMax>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(pair_smem(kTStagesMax)))})
+          if (e != cudaSuccess) return e;
+        return cudaSuccess;
+      }); e0 != cudaSuccess)
+    return e0;
   // (routing short-K products with M > 128 to the persistent single-CTA tiles
   // instead was measured slower end to end: cfg3 1.61 -> 1.83 ms, cfg4 34.6 -> 37.0 ms)
   if (use_pair(g.M) && !g.no_pair) {
@@ -1158,26 +1168,15 @@ cudaError_t launch_tma_kernel(const GemmArgs<float>& g, std::uint32_t z, const C
   static const bool persist = !(std::getenv("TG_UMMA_PERSIST") && std::getenv("TG_UMMA_PERSIST")[0] == '0');
   const std::uint32_t kspan0 = g.epi == kEpiSplitK ? g.k_chunk : g.K;
   if (persist && kspan0 <= 256) {
-    static bool pattr = false;
-    if (!pattr) {
-      const cudaError_t e = cudaFuncSetAttribute(k_umma_tma_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 static_cast<int>(persist_smem()));
-      if (e != cudaSuccess) return e;
-      pattr = true;
-    }
+    static PerDeviceOnce pattr;
+    if (const cudaError_t e = pattr.ensure([] {
+          return cudaFuncSetAttribute(k_umma_tma_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(persist_smem()));
+        }); e != cudaSuccess)
+      return e;
     const std::uint32_t mt = (g.M + BM - 1) / BM, nt = (g.N + BN - 1) / BN;
     const std::uint32_t tiles = mt * nt * z;
-    int nsm = 148;
-    {
-      static int cached = 0;
-      if (!cached) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
-        if (cached <= 0) cached = 148;
-      }
-      nsm = cached;
-    }
+    const int nsm = sm_count();
     const std::uint32_t grid = std::min<std::uint32_t>(tiles, static_cast<std::uint32_t>(nsm));
     if (grid == 0) return cudaSuccess;
     k_umma_tma_p<<<grid, kTThreads, persist_smem(), st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0, mt, nt, tiles);
@@ -1302,13 +1301,12 @@ template <bool AK, int MG>
 cudaError_t launch_shortk(const GemmArgs<float>& g, cudaStream_t st) {
   const int kp = static_cast<int>(((g.K + 3) & ~3u) + 4);
   const std::size_t smem = std::size_t(MG * kSkRows) * kp * sizeof(float);
-  static int attr = 0;
-  if (smem > 48 * 1024 && static_cast<int>(smem) > attr) {
-    const cudaError_t e = cudaFuncSetAttribute(k_gemm_shortk<AK, MG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    attr = static_cast<int>(smem);
-  }
+  static PerDeviceMax attr;
+  if (smem > 48 * 1024)
+    if (const cudaError_t e = attr.raise_to(static_cast<int>(smem), [](int v) {
+          return cudaFuncSetAttribute(k_gemm_shortk<AK, MG>, cudaFuncAttributeMaxDynamicSharedMemorySize, v);
+        }); e != cudaSuccess)
+      return e;
   const dim3 grid(static_cast<unsigned>((g.N + 4 * (256 / MG) - 1) / (4 * (256 / MG))), (g.M + MG * kSkRows - 1) / (MG * kSkRows));
   k_gemm_shortk<AK, MG><<<grid, 256, smem, st>>>(g, kp);
   return cudaGetLastError();
@@ -1338,6 +1336,7 @@ cudaError_t launch_gemm_umma(const GemmArgs<float>& g0, std::uint32_t splits, cu
   // base and row stride); split-K slices start on 32-element k boundaries so a
   // k-tile never reads into the next slice (TMA zero-fills only past K).
   static const bool use_tma = !(std::getenv("TG_UMMA_TMA") && std::getenv("TG_UMMA_TMA")[0] == '0');
+#ifdef TG_PROFILING
   static bool exp_set = false;
   if (!exp_set) {
     exp_set = true;
@@ -1346,6 +1345,7 @@ cudaError_t launch_gemm_umma(const GemmArgs<float>& g0, std::uint32_t splits, cu
       cudaMemcpyToSymbol(g_umma_exp, &v, sizeof(int));
     }
   }
+#endif
   if (use_tma) {
     GemmArgs<float> g = g0;
     if (g.epi == kEpiSplitK) g.k_chunk = (g.k_chunk + BK - 1) / BK * BK;
@@ -1412,12 +1412,11 @@ cudaError_t launch_gemm_umma(const GemmArgs<float>& g0, std::uint32_t splits, cu
     const std::uint32_t keff = g.epi == kEpiSplitK ? g.k_chunk : g.K;
     if (keff > 1024) return launch_gemm<float>(g, splits, st);
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_umma_tf32x3, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static PerDeviceOnce attr;
+  if (const cudaError_t e = attr.ensure([] {
+        return cudaFuncSetAttribute(k_umma_tf32x3, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem));
+      }); e != cudaSuccess)
+    return e;
   const dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, g.epi == kEpiSplitK ? splits : 1);
   k_umma_tf32x3<<<grid, 128, kSmem, st>>>(g);
   return cudaGetLastError();

@@ -8,11 +8,17 @@ x -= gamma * g / b_global (sgd_step) — identical parameters
 on all ranks without a broadcast.
 
 The reference has no parallelism (PAPER.md:748 single core); this is the
-B200 build's scaling axis.  The path has exactly one exchange per step, so
-the collective is torch.distributed's NCCL all-reduce (NVLS in-switch
-reduction when NCCL selects it).
+B200 build's scaling axis.  The path has exactly one exchange per step.  The
+exchange runs either through libtg's own NCCL communicator
+(tg_allreduce_gd_step, the C-ABI a C++ caller uses; `NcclComm`) or through
+torch.distributed's all-reduce; both are enqueued on the caller's stream, so
+the GD update that follows never races the reduction.
 """
 from __future__ import annotations
+
+import ctypes as C
+
+from ._lib import check, lib
 
 
 def shard(global_batch: int, rank: int, world: int) -> tuple[int, int]:
@@ -22,26 +28,74 @@ def shard(global_batch: int, rank: int, world: int) -> tuple[int, int]:
     return global_batch * rank // world, global_batch * (rank + 1) // world
 
 
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through libtg (rank 0 creates it, every rank receives it)."""
+    buf = (C.c_char * 128)()
+    check(lib.tg_nccl_get_unique_id(buf))
+    return bytes(buf)
+
+
+class NcclComm:
+    """An NCCL communicator created by libtg (tg_nccl_comm_init) on the current
+    CUDA device.  `uid` is rank 0's nccl_unique_id(); when it is None the id is
+    broadcast from rank 0 over the initialised torch.distributed group (any
+    backend)."""
+
+    def __init__(self, rank: int, world: int, uid: bytes | None = None, group=None):
+        if uid is None:
+            import torch.distributed as dist
+            obj = [nccl_unique_id() if rank == 0 else None]
+            if world > 1:
+                dist.broadcast_object_list(obj, src=0, group=group)
+            uid = obj[0]
+        h = C.c_void_p()
+        check(lib.tg_nccl_comm_init(int(world), C.c_char_p(uid), int(rank), C.byref(h)))
+        self.handle = h.value
+        self.rank, self.world = rank, world
+
+    def close(self):
+        if getattr(self, "handle", None):
+            check(lib.tg_nccl_comm_destroy(C.c_void_p(self.handle)))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class DataParallelStep:
     """One DP training step over a compiled Program.
 
-    local_grad(params) must fill and return the local gradient sum tensor
-    (by default Program.forward_backward on this rank's shard).
+    comm: an NcclComm (the exchange and the update go through
+    tg_allreduce_gd_step on `stream`), or None to use torch.distributed's
+    all-reduce (enqueued on `stream` too).  local_grad(params) must fill the
+    local gradient sum tensor when given.
     """
 
-    def __init__(self, program=None, group=None):
+    def __init__(self, program=None, group=None, comm: NcclComm | None = None):
         self.program = program
         self.group = group
+        self.comm = comm
 
     def step(self, params, grad, gamma: float, global_batch: int, local_grad=None, stream=None):
-        import torch.distributed as dist
-
         if local_grad is not None:
             local_grad(params)
-        if dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1:
-            dist.all_reduce(grad, op=dist.ReduceOp.SUM, group=self.group)
+        if self.comm is not None and self.program is not None:
+            self.program.allreduce_gd_step(params, grad, gamma, global_batch, self.comm, stream)
+            return params
+        import torch.distributed as dist
+        multi = dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1
         if self.program is not None:
-            self.program.gd_update(params, grad, gamma, global_batch, stream)
+            import torch
+            s = stream if stream is not None else torch.cuda.current_stream()
+            with torch.cuda.stream(s):          # the all-reduce is ordered on the caller's stream
+                if multi:
+                    dist.all_reduce(grad, op=dist.ReduceOp.SUM, group=self.group)
+                self.program.gd_update(params, grad, gamma, global_batch, s)
         else:  # host-side update for CPU process groups (tests): same formula as k_gd
+            if multi:
+                dist.all_reduce(grad, op=dist.ReduceOp.SUM, group=self.group)
             params.sub_(gamma * grad / global_batch)
         return params

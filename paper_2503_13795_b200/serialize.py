@@ -67,8 +67,6 @@ def save_snapshot(values, grads=None) -> bytes:
 def load_snapshot(data: bytes, values, grads=None) -> dict:
     """Loads a BTSG snapshot into values (and grads); returns its header fields."""
     vp, gp, n, dt = _pair(values, grads)
-    odt, on, og = C.c_int(), C.c_size_t(), C.c_int()
-    check(lib.tg_load_snapshot(data, len(data), vp, gp, n, C.byref(odt), C.byref(on), C.byref(og)))
-    if odt.value != dt:
-        raise _lib.TgError(6, "load_snapshot: precision of the snapshot differs from the target range")
-    return {"dtype": "f64" if odt.value == _lib.TG_F64 else "f32", "count": on.value, "grads": bool(og.value)}
+    on, og = C.c_size_t(), C.c_int()
+    check(lib.tg_load_snapshot(data, len(data), dt, vp, gp, n, C.byref(on), C.byref(og)))
+    return {"dtype": "f64" if dt == _lib.TG_F64 else "f32", "count": on.value, "grads": bool(og.value)}

@@ -428,6 +428,13 @@ class Program:
         check(lib.tg_gd_update(self._h, self._ptr(params), self._ptr(grad_sum), float(gamma),
                                int(global_batch), self._stream(stream)))
 
+    def allreduce_gd_step(self, params, grad_sum, gamma: float, global_batch: int, comm=None, stream=None):
+        """In-place NCCL all-reduce (sum) of grad_sum, then the GD update with the
+        global batch (tg_allreduce_gd_step); comm None: the update only."""
+        c = None if comm is None else C.c_void_p(comm.handle if hasattr(comm, "handle") else int(comm))
+        check(lib.tg_allreduce_gd_step(self._h, self._ptr(params), self._ptr(grad_sum), float(gamma),
+                                       int(global_batch), c, self._stream(stream)))
+
     def train_step(self, inputs, index_inputs, batch, params, loss, grad_sum, gamma, workspace, stream=None):
         check(lib.tg_train_step(self._h, self._ptr(inputs), self._ptr(index_inputs), int(batch),
                                 self._ptr(params), self._ptr(loss), self._ptr(grad_sum), float(gamma),

@@ -284,3 +284,51 @@ def test_counter_synth_math_accuracy():
     assert np.max(np.abs(x[0] - (a + noise(d[2], d[3])))) < 2e-15
     assert np.max(np.abs(x[1] - (c + noise(d[4], d[5])))) < 2e-15
     assert np.array_equal(x[2], np.where(second, 1.0, -1.0))
+
+
+def test_null_program_handle_is_invalid_handle_everywhere():
+    """Every entry point that takes a program handle returns TG_INVALID_HANDLE
+    for NULL instead of dereferencing it (reference InvalidHandle,
+    tape.hpp:268-273)."""
+    L = _lib.lib
+    P = None
+    i = _lib.tg_program_info()
+    pu32 = ctypes.POINTER(ctypes.c_uint32)()
+    n32, sz, i64 = ctypes.c_uint32(), ctypes.c_size_t(), ctypes.c_int64()
+    d, u64 = ctypes.c_double(), ctypes.c_uint64()
+    s = ctypes.c_char_p()
+    calls = {
+        "tg_program_info_get": lambda: L.tg_program_info_get(P, ctypes.byref(i)),
+        "tg_program_order": lambda: L.tg_program_order(P, ctypes.byref(pu32), ctypes.byref(n32)),
+        "tg_workspace_size": lambda: L.tg_workspace_size(P, 10, ctypes.byref(sz)),
+        "tg_set_memory_budget": lambda: L.tg_set_memory_budget(P, 10),
+        "tg_forward_backward": lambda: L.tg_forward_backward(P, None, None, 1, None, None, None, None, None, 0, None),
+        "tg_gd_update": lambda: L.tg_gd_update(P, None, None, 0.1, 1, None),
+        "tg_allreduce_gd_step": lambda: L.tg_allreduce_gd_step(P, None, None, 0.1, 1, None, None),
+        "tg_train_step": lambda: L.tg_train_step(P, None, None, 1, None, None, None, 0.1, None, 0, None),
+        "tg_check_device_error": lambda: L.tg_check_device_error(P, None, ctypes.byref(i64), ctypes.byref(n32)),
+        "tg_profile_enable": lambda: L.tg_profile_enable(P, 1),
+        "tg_profile_read": lambda: L.tg_profile_read(P, ctypes.byref(d), ctypes.byref(u64)),
+        "tg_program_jit": lambda: L.tg_program_jit(P, ctypes.byref(s), ctypes.byref(s), ctypes.byref(d)),
+        "tg_pipeline_new": lambda: L.tg_pipeline_new(P, 1, None, None, ctypes.byref(ctypes.c_void_p())),
+    }
+    for name, f in calls.items():
+        assert f() == 3, name
+    assert L.tg_launch_count(P) == 0
+
+
+def test_nccl_binding_and_argument_checks():
+    """The NCCL exchange is bound at run time (tg_comm.cpp): the library
+    reports the bound version, and bad communicator arguments are rejected
+    before NCCL is called."""
+    L = _lib.lib
+    v = L.tg_nccl_version()
+    assert v == 0 or v >= 21000
+    h = ctypes.c_void_p()
+    uid = (ctypes.c_char * 128)()
+    assert L.tg_nccl_comm_init(2, uid, 2, ctypes.byref(h)) == 1
+    assert L.tg_nccl_comm_init(0, uid, 0, ctypes.byref(h)) == 1
+    assert L.tg_nccl_comm_init(1, None, 0, ctypes.byref(h)) == 1
+    assert L.tg_nccl_get_unique_id(None) == 1
+    assert L.tg_nccl_comm_destroy(None) == 0
+    assert _lib.lib.tg_status_name(10).decode() == "TG_NCCL"

@@ -176,3 +176,51 @@ def test_sgd_step_formula():
     p = np.array([1.0])
     oracle.sgd("f64", p, np.array([4.0]), 0.5, 2)  # mean 2
     assert p[0] == 0.0
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("name,dims,dt", [("char_mlp", None, "f32"), ("gpt", [13, 8, 16, 2, 2, 32], "f32"),
+                                         ("wide_mlp", [24, 16, 12, 10], "f32"), ("moons", None, "f64")])
+def test_reference_recording_drop_in_describes_like_tg_tape(name, dims, dt):
+    """A model recorded with the UNMODIFIED tapegrad::Tape plus the drop-in
+    adapter's side record (include/tg_from_tapegrad.hpp: per-sample row
+    selections become gathers, the softmax max-shift leaf becomes the
+    per-sample stop-gradient max) describes to exactly the arrays this
+    package's own recorder produces: ops, children with gather references,
+    gather table, leaf roles, parameter values."""
+    from paper_2503_13795_b200.tape import model_id
+    a = oracle.ref_describe(model_id(name), dims, dt, seed=3)
+    b = tg.build_model(name, dims, dt, seed=3).describe()
+    for f in ("op", "child_offset", "child", "constant", "leaf_class", "leaf_index", "gathers"):
+        np.testing.assert_array_equal(getattr(a, f), getattr(b, f), err_msg=f)
+    assert (a.root, a.n_params, a.n_inputs, a.n_index_inputs) == (b.root, b.n_params, b.n_inputs, b.n_index_inputs)
+    np.testing.assert_array_equal(a.param_values(), b.param_values())
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built")
+def test_reference_recording_rejects_ambiguous_selection():
+    """Two columns selecting the same row of one table in the template sample
+    cannot be told apart on a reference tape: describe refuses."""
+    import ctypes as C
+    lib = oracle._reflib()
+    from paper_2503_13795_b200 import _lib as plib
+    d = plib.tg_tape_desc()
+    # gpt with a vocabulary of 3 over 8 positions: the template's idx[c] = c % 3 repeats rows
+    st = lib.ref_describe(5, oracle._d(oracle._dims([3, 8, 16, 2, 1, 32])), 0, 1, None, C.byref(d))
+    assert st != 0 and b"selected twice" in lib.ref_last_error()
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("name,dims,dt", [("char_mlp", None, "f32"), ("wide_mlp", [24, 16, 12, 10], "f32"),
+                                         ("moons", None, "f64"), ("gpt", None, "f32"), ("fig1", None, "f64")])
+def test_reference_side_inputs_equal_product_generators(name, dims, dt):
+    """The bench's reference arm takes its parameters and samples from
+    oracle/_ref (ref_params / ref_synth), never from the product library;
+    they are the same bits as the product's for the same seeds."""
+    from paper_2503_13795_b200.tape import model_id
+    d = tg.build_model(name, dims, dt, seed=0).describe()
+    np.testing.assert_array_equal(oracle.ref_params(model_id(name), dims, dt, seed=0), d.param_values())
+    x, k = tg.synth_batch(name, dims, dt, seed=1234, batch=300, n_inputs=d.n_inputs, n_index=d.n_index_inputs)
+    xr, kr = oracle.ref_synth(model_id(name), dims, dt, 1234, 300)
+    np.testing.assert_array_equal(xr, x.astype(np.float64))
+    np.testing.assert_array_equal(kr, k)

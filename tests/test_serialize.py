@@ -74,3 +74,23 @@ def test_snapshot_header_round_trip_and_errors():
         ser.load_snapshot(s[:4] + (2).to_bytes(4, "little") + s[8:], v2)   # unsupported version
     with pytest.raises(TgError, match="TG_CAPACITY"):
         ser.load_snapshot(s, np.zeros(3))
+
+
+def test_cross_precision_snapshot_is_format_error_without_partial_write():
+    """An fp64 snapshot loaded into an fp32 range (and the reverse) is
+    TG_FORMAT before any byte is written: the range and a guard region past
+    it keep their contents (all-or-nothing loads)."""
+    v = np.arange(4, dtype=np.float64) + 0.5
+    s64 = ser.save_snapshot(v)
+    buf = np.full(8, 7.0, np.float32)
+    with pytest.raises(TgError, match="TG_FORMAT"):
+        ser.load_snapshot(s64, buf[:4])
+    np.testing.assert_array_equal(buf, 7.0)
+    s32 = ser.save_snapshot(v.astype(np.float32))
+    buf64 = np.full(8, 7.0)
+    with pytest.raises(TgError, match="TG_FORMAT"):
+        ser.load_snapshot(s32, buf64[:4])
+    np.testing.assert_array_equal(buf64, 7.0)
+    assert ser.load_snapshot(s32, buf[:4])["count"] == 4
+    np.testing.assert_array_equal(buf[:4], v.astype(np.float32))
+    np.testing.assert_array_equal(buf[4:], 7.0)
