@@ -128,6 +128,40 @@ tg_status tg_rec_set_root(tg_recorder_t r, uint32_t node);
 /* Fills desc with views into the recorder (valid until the next mutation). */
 tg_status tg_rec_describe(tg_recorder_t r, tg_tape_desc* desc);
 
+/* Fixed-capacity recorder (TapeConfig{capacity, fixed_capacity, child_capacity},
+ * tape.hpp:40-53, :79-81): no storage growth after construction; exceeding
+ * either capacity is TG_CAPACITY with the reference's message (tape.hpp:278-295).
+ * child_capacity 0 selects 8 x capacity, as the reference does.              */
+tg_status tg_recorder_new_fixed(tg_dtype dtype, size_t capacity, size_t child_capacity, tg_recorder_t* out);
+
+/* Checkpoint / rewind (Tape::checkpoint / rewind, tape.hpp:228-242).  Rewind
+ * discards every node at index >= mark; surviving values and the child-pool
+ * cursor are restored exactly, handles into the discarded range become
+ * TG_INVALID_HANDLE, and the next node reuses index mark.  A mark ahead of the
+ * live size is TG_INVALID_CHECKPOINT with the reference's message.           */
+typedef struct tg_checkpoint {
+  uint32_t mark;          /* live node count at capture                       */
+  uint32_t params;        /* parameter leaves at capture (recorder extension) */
+  uint64_t child_mark;    /* child-pool cursor at capture                      */
+  uint32_t gathers;       /* gather references at capture (extension)          */
+  uint32_t reserved;
+} tg_checkpoint;
+tg_status tg_rec_checkpoint(tg_recorder_t r, tg_checkpoint* out);
+tg_status tg_rec_rewind(tg_recorder_t r, const tg_checkpoint* cp);
+
+/* Recorder size and high-water marks (Tape::size / peak_nodes / child_pool_size
+ * / peak_children / peak_arena_bytes / max_arity, tape.hpp:98-125).          */
+typedef struct tg_rec_stats {
+  uint32_t size;
+  uint32_t peak_nodes;
+  uint64_t child_pool_size;
+  uint64_t peak_children;
+  uint64_t peak_arena_bytes;
+  uint32_t max_arity;
+  uint32_t n_params;
+} tg_rec_stats;
+tg_status tg_rec_get_stats(tg_recorder_t r, tg_rec_stats* out);
+
 /* ---- built-in workloads (BASELINE.json configs) -------------------------- */
 typedef enum tg_model {
   TG_MODEL_FIG1 = 1,     /* cfg1: Fig. 1 tiny graph            */

@@ -42,6 +42,17 @@ class tg_tape_desc(C.Structure):
     ]
 
 
+class tg_checkpoint(C.Structure):
+    _fields_ = [("mark", C.c_uint32), ("params", C.c_uint32), ("child_mark", C.c_uint64),
+                ("gathers", C.c_uint32), ("reserved", C.c_uint32)]
+
+
+class tg_rec_stats(C.Structure):
+    _fields_ = [("size", C.c_uint32), ("peak_nodes", C.c_uint32), ("child_pool_size", C.c_uint64),
+                ("peak_children", C.c_uint64), ("peak_arena_bytes", C.c_uint64), ("max_arity", C.c_uint32),
+                ("n_params", C.c_uint32)]
+
+
 class tg_model_args(C.Structure):
     _fields_ = [("dims", C.c_uint32 * 8), ("dtype", C.c_int)]
 
@@ -94,6 +105,10 @@ def _load():
         "tg_rec_value": (st, [P, u32, C.POINTER(C.c_double)]),
         "tg_rec_set_root": (st, [P, u32]),
         "tg_rec_describe": (st, [P, C.POINTER(tg_tape_desc)]),
+        "tg_recorder_new_fixed": (st, [st, sz, sz, C.POINTER(P)]),
+        "tg_rec_checkpoint": (st, [P, C.POINTER(tg_checkpoint)]),
+        "tg_rec_rewind": (st, [P, C.POINTER(tg_checkpoint)]),
+        "tg_rec_get_stats": (st, [P, C.POINTER(tg_rec_stats)]),
         "tg_build_model": (st, [st, C.POINTER(tg_model_args), u64, C.POINTER(P)]),
         "tg_synth_batch": (st, [st, C.POINTER(tg_model_args), u64, sz, P, C.POINTER(i32)]),
         "tg_synth_ctr": (st, [st, C.POINTER(tg_model_args), u64, u64, sz, P, C.POINTER(i32)]),

@@ -1953,6 +1953,52 @@ tg_status tg_recorder_new(tg_dtype dtype, size_t capacity, tg_recorder_t* out) {
 
 void tg_recorder_free(tg_recorder_t r) { delete r; }
 
+tg_status tg_recorder_new_fixed(tg_dtype dtype, size_t capacity, size_t child_capacity, tg_recorder_t* out) {
+  return guard([&] {
+    if (!out) return fail(TG_INVALID_ARGUMENT, "tg_recorder_new_fixed: out is NULL");
+    if (dtype != TG_F64 && dtype != TG_F32) return fail(TG_INVALID_ARGUMENT, "tg_recorder_new_fixed: bad dtype");
+    const tg::TapeConfig cfg{.capacity = capacity, .fixed_capacity = true, .child_capacity = child_capacity};
+    auto r = std::make_unique<tg_recorder>();
+    r->dtype = dtype;
+    if (dtype == TG_F64) r->t64 = std::make_unique<tg::Tape<double>>(cfg);
+    else r->t32 = std::make_unique<tg::Tape<float>>(cfg);
+    *out = r.release();
+    return TG_OK;
+  });
+}
+
+tg_status tg_rec_checkpoint(tg_recorder_t r, tg_checkpoint* out) {
+  return guard([&] {
+    if (!r) return fail(TG_INVALID_HANDLE, "tg_rec_checkpoint: recorder is NULL");
+    if (!out) return fail(TG_INVALID_ARGUMENT, "tg_rec_checkpoint: out is NULL");
+    const tg::Checkpoint cp = r->visit([](auto& t) { return t.checkpoint(); });
+    *out = tg_checkpoint{cp.mark, cp.params, cp.child_mark, cp.gathers, 0};
+    return TG_OK;
+  });
+}
+
+tg_status tg_rec_rewind(tg_recorder_t r, const tg_checkpoint* cp) {
+  return guard([&] {
+    if (!r) return fail(TG_INVALID_HANDLE, "tg_rec_rewind: recorder is NULL");
+    if (!cp) return fail(TG_INVALID_ARGUMENT, "tg_rec_rewind: checkpoint is NULL");
+    const tg::Checkpoint c{cp->mark, static_cast<std::size_t>(cp->child_mark), cp->params, cp->gathers};
+    r->visit([&](auto& t) { t.rewind(c); return 0; });
+    return TG_OK;
+  });
+}
+
+tg_status tg_rec_get_stats(tg_recorder_t r, tg_rec_stats* out) {
+  return guard([&] {
+    if (!r) return fail(TG_INVALID_HANDLE, "tg_rec_get_stats: recorder is NULL");
+    if (!out) return fail(TG_INVALID_ARGUMENT, "tg_rec_get_stats: out is NULL");
+    *out = r->visit([](auto& t) {
+      return tg_rec_stats{t.size(), t.peak_nodes(), t.child_pool_size(), t.peak_children(), t.peak_arena_bytes(),
+                          t.max_arity(), t.n_params()};
+    });
+    return TG_OK;
+  });
+}
+
 tg_status tg_rec_param(tg_recorder_t r, double v, uint32_t* node) {
   return guard([&] {
     *node = r->visit([&](auto& t) { return t.param(static_cast<typename std::decay_t<decltype(t)>::scalar_type>(v)).index; });

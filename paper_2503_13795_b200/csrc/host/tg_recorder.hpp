@@ -128,6 +128,17 @@ class Tape {
   NodeIndex peak_nodes() const noexcept { return peak_nodes_; }
   std::size_t child_pool_size() const noexcept { return child_pool_.size(); }
   std::uint32_t max_arity() const noexcept { return max_arity_; }
+  /// High-water mark of the child-pool cursor (reference Tape::peak_children).
+  std::size_t peak_children() const noexcept { return peak_children_; }
+  /// Bytes of recorder storage touched at the high-water marks, accounted from
+  /// this recorder's own per-node buffers (value, op, constant, child offset,
+  /// leaf class and index) and the child pool, as the reference's
+  /// peak_arena_bytes (tape.hpp:118-125) accounts from its arenas.
+  std::size_t peak_arena_bytes() const noexcept {
+    constexpr std::size_t per_node = 2 * sizeof(Scalar) + 1 + sizeof(std::uint64_t) + 1 + sizeof(std::uint32_t);
+    return static_cast<std::size_t>(peak_nodes_) * per_node + peak_children_ * sizeof(std::uint32_t);
+  }
+  bool fixed_capacity() const noexcept { return fixed_; }
 
   // ---- leaves -----------------------------------------------------------
   /// Reference Tape::leaf (tape.hpp:169).  A bare leaf is a constant: its
@@ -187,6 +198,9 @@ class Tape {
     if (cp.mark > size())
       throw InvalidCheckpoint("rewind: checkpoint mark " + std::to_string(cp.mark) +
                               " is ahead of tape size " + std::to_string(size()));
+    if (cp.child_mark > child_pool_.size() || cp.params > n_params_ || cp.gathers > gathers_.size())
+      throw InvalidCheckpoint("rewind: checkpoint child mark " + std::to_string(cp.child_mark) +
+                              " is ahead of child pool cursor " + std::to_string(child_pool_.size()));
     values_.resize(cp.mark);
     ops_.resize(cp.mark);
     consts_.resize(cp.mark);
@@ -216,6 +230,7 @@ class Tape {
     leaf_index_.push_back(0);
     child_off_.push_back(child_pool_.size());
     peak_nodes_ = std::max(peak_nodes_, size());
+    peak_children_ = std::max(peak_children_, child_pool_.size());
     max_arity_ = std::max<std::uint32_t>(max_arity_, static_cast<std::uint32_t>(kids.size()));
     return ValueRef{size() - 1};
   }
@@ -283,6 +298,7 @@ class Tape {
   std::uint32_t n_params_{0}, n_inputs_{0}, n_index_inputs_{0};
   NodeIndex root_{0};
   NodeIndex peak_nodes_{0};
+  std::size_t peak_children_{0};
   std::uint32_t max_arity_{0};
 };
 

@@ -162,14 +162,38 @@ class Tape:
     (std::invalid_argument), TgError(TG_INVALID_HANDLE) for stale handles.
     """
 
-    def __init__(self, capacity: int = 1024, dtype: str = "f64", _handle=None):
+    def __init__(self, capacity: int = 1024, dtype: str = "f64", _handle=None, fixed_capacity: bool = False,
+                 child_capacity: int = 0):
         self.dtype = dtype
         if _handle is not None:
             self._h = _handle
         else:
             h = C.c_void_p()
-            check(lib.tg_recorder_new(_DT[dtype], capacity, C.byref(h)))
+            if fixed_capacity:   # TapeConfig{capacity, fixed_capacity, child_capacity} (tape.hpp:40-53)
+                check(lib.tg_recorder_new_fixed(_DT[dtype], capacity, child_capacity, C.byref(h)))
+            else:
+                check(lib.tg_recorder_new(_DT[dtype], capacity, C.byref(h)))
             self._h = h
+
+    # ---- checkpoint / rewind / high-water marks (tape.hpp:98-125, :228-242) ----
+    def checkpoint(self) -> _lib.tg_checkpoint:
+        cp = _lib.tg_checkpoint()
+        check(lib.tg_rec_checkpoint(self._h, C.byref(cp)))
+        return cp
+
+    def rewind(self, cp: _lib.tg_checkpoint) -> None:
+        check(lib.tg_rec_rewind(self._h, C.byref(cp)))
+
+    def stats(self) -> dict:
+        s = _lib.tg_rec_stats()
+        check(lib.tg_rec_get_stats(self._h, C.byref(s)))
+        return {f: getattr(s, f) for f, _ in s._fields_}
+
+    def size(self) -> int:
+        return self.stats()["size"]
+
+    def peak_nodes(self) -> int:
+        return self.stats()["peak_nodes"]
 
     def __del__(self):
         h = getattr(self, "_h", None)

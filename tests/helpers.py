@@ -16,8 +16,18 @@ TOL = {"f64": 1e-12, "f32": 1e-5}
 
 
 def rel(got, want):
+    """Normwise relative error over the finite entries; entries where both
+    sides are the same non-finite value (both NaN, equal infinities: the
+    reference itself overflowed) are equal, any other non-finite mismatch is
+    an infinite error."""
     got = np.asarray(got, np.float64)
     want = np.asarray(want, np.float64)
+    fin = np.isfinite(got) & np.isfinite(want)
+    if not fin.all():
+        same = (got == want) | (np.isnan(got) & np.isnan(want))
+        if not np.all(fin | same):
+            return float("inf")
+        got, want = np.where(fin, got, 0.0), np.where(fin, want, 0.0)
     den = max(float(np.linalg.norm(want)), 1e-300)
     return float(np.linalg.norm(got - want)) / den
 
