@@ -32,6 +32,22 @@ def rel(got, want):
     return float(np.linalg.norm(got - want)) / den
 
 
+def rel_sum(got, want, terms):
+    """Normwise error of a batch sum relative to the sum of its terms'
+    magnitudes: ||got - want|| / || sum_i |terms[:, i]| || (terms: [n][batch]).
+    Equals rel() when the terms do not cancel."""
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    t = np.abs(np.asarray(terms, np.float64)).sum(axis=1)
+    fin = np.isfinite(got) & np.isfinite(want) & np.isfinite(t)
+    if not fin.all():
+        same = (got == want) | (np.isnan(got) & np.isnan(want))
+        if not np.all(fin | same):
+            return float("inf")
+    den = max(float(np.linalg.norm(t[fin])), 1e-300)
+    return float(np.linalg.norm(got[fin] - want[fin])) / den
+
+
 def close_rel(got, want, rel_tol, abs_tol=1e-8):
     got = np.asarray(got, np.float64)
     want = np.asarray(want, np.float64)
