@@ -54,6 +54,21 @@ struct PerDeviceMax {
   }
 };
 
+/// An int computed once per device by f() (a positive value; 0 = not yet computed).
+struct PerDeviceValue {
+  std::atomic<int> v[kMaxDevices] = {};
+  template <class F>
+  int get(F&& f) {
+    std::atomic<int>& c = v[current_device()];
+    int n = c.load(std::memory_order_acquire);
+    if (n <= 0) {
+      n = f();
+      c.store(n, std::memory_order_release);
+    }
+    return n;
+  }
+};
+
 /// Streaming multiprocessors of the current device (148 on B200).
 inline int sm_count() {
   static std::atomic<int> cache[kMaxDevices] = {};
