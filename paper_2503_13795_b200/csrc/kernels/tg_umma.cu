@@ -20,7 +20,6 @@
 #include <cudaTypedefs.h>
 
 #include <cstdint>
-#include <cstdio>
 #include <cstdlib>
 
 #include "tg_ops.cuh"
@@ -257,13 +256,6 @@ __device__ __forceinline__ void tma_load_2d(std::uint32_t dst, const CUtensorMap
       "l"(reinterpret_cast<std::uint64_t>(map)), "r"(c0), "r"(c1), "r"(mbar)
       : "memory");
 }
-__device__ __forceinline__ void tma_load_3d(std::uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
-                                            std::uint32_t mbar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
-      "l"(reinterpret_cast<std::uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(mbar)
-      : "memory");
-}
 // SWIZZLE_128B smem descriptor (sm_100 version 1).
 __device__ __forceinline__ std::uint64_t umma_desc_sw128(std::uint32_t saddr, std::uint32_t lbo, std::uint32_t sbo) {
   return static_cast<std::uint64_t>((saddr & 0x3FFFFu) >> 4) | (static_cast<std::uint64_t>(lbo >> 4) << 16) |
@@ -272,13 +264,9 @@ __device__ __forceinline__ std::uint64_t umma_desc_sw128(std::uint32_t saddr, st
 // Issue the TMA loads of one operand's k-tile (rows r0.., k0..) into dst.
 // `off` shifts the map's outer (row) coordinate: the k rows of an MN-major
 // operand, the m / n rows of a K-major one (batched products).
-// mn == 2: the MN-major operand's 3D map (make_mn3_map), one load for all
-// four 32-wide chunks.
-__device__ __forceinline__ void tma_operand(const CUtensorMap* map, int mn, std::uint32_t dst, int r0, int k0, int off,
+__device__ __forceinline__ void tma_operand(const CUtensorMap* map, bool mn, std::uint32_t dst, int r0, int k0, int off,
                                             std::uint32_t mbar) {
-  if (mn == 2) {
-    tma_load_3d(dst, map, 0, k0 + off, r0 / 32, mbar);
-  } else if (mn) {
+  if (mn) {
 #pragma unroll
     for (int c = 0; c < 4; ++c) tma_load_2d(dst + c * 4096, map, r0 + 32 * c, k0 + off, mbar);
   } else {
@@ -1114,399 +1102,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * kPN));
 }
 
-// ---------------------------------------------------------------------------
-// k_pair_ws: persistent, warp-specialised CTA-pair 3xTF32 GEMM.
-//
-// k_umma_pair's converter warps also drained the accumulator and ran the
-// epilogue, so every drain waited on MMA completion before the next tile's
-// conversion could start, and every output tile ended in an epilogue the
-// tensor core sat idle through (ncu: tensor pipe 54% active, 199 TF/s of a
-// measured 370 TF/s 3xTF32 roof on cfg5's layer-2 product).  Here each role
-// has its own warps and the CTA pair walks output tiles persistently:
-//   warp 0      TMA producer (A rows / B columns of this CTA into a 3-deep ring)
-//   warp 1      MMA issuer (leader CTA): 12 kind::tf32 MMAs per 32-wide k-tile
-//   warps 2-7   converters: hi = tf32_rna(x) in place, lo = x - hi
-//   warps 8-15  accumulation drain + epilogue: one TMEM lane quarter and one
-//               128-column half each, 128 fp32 register sums per thread
-// setmaxnreg moves registers from warpgroups 0-1 (72) to 2-3 (184).  The two
-// 256-column TMEM buffers alternate per accumulation group (kPFlush k-tiles)
-// across output tiles, so the MMA runs up to two groups of the next tile
-// while the drain warps store the current one (through a 32 x 33 per-warp
-// shared-memory transpose: 128-byte row segments per store).  Cross-CTA
-// signals (converted stages, drained buffers) are release.cluster arrives on
-// the leader's barriers, acquired at cluster scope by the MMA issuer.
-// ---------------------------------------------------------------------------
-constexpr int kWsStages = 3;
-constexpr int kWsDrainWarps = 8;
-// setmaxnreg moves registers within the CTA's launch allocation (threads x the
-// launch-bounds register count, rounded down to 8): an increase that the
-// decreases cannot cover spins in USETMAXREG.TRY_ALLOC forever.
-template <int NC> struct WsShape {                      // NC converter warps (6 or 10)
-  static constexpr int kDrain0 = 2 + NC;                // first drain warp (a warpgroup boundary)
-  static constexpr int kThreads = 32 * (kDrain0 + kWsDrainWarps);
-  static constexpr int kLaunchRegs = (65536 / kThreads) / 8 * 8;
-  static constexpr int kPool = kThreads * kLaunchRegs;
-  static constexpr int kRegOther = NC == 6 ? 72 : NC == 10 ? 40 : 32;   // NC 14: 32
-  static constexpr int kRegDrain = ((kPool - 32 * kDrain0 * kRegOther) / (32 * kWsDrainWarps)) / 8 * 8;
-  static_assert(kDrain0 % 4 == 0, "drain warps start a warpgroup");
-  static_assert(32 * kDrain0 * kRegOther + 32 * kWsDrainWarps * kRegDrain <= kPool, "setmaxnreg budget");
-  static_assert(kRegDrain >= 152 && kRegDrain <= 256 && kRegOther >= 24, "register split");
-};
-constexpr int kWsXLd = 33;                                      // epilogue transpose row stride (floats)
-constexpr std::uint32_t kWsXBytes = 32 * kWsXLd * 4;            // per drain warp
-// Operand rings.  In-place mode (RAW = false): kWsStages stages of
-// [A hi | A lo | B hi | B lo] (64 KB), TMA landing in the hi slots.  Raw mode
-// (RAW = true): the landed fp32 tiles are the hi operands themselves (kind::tf32
-// reads the top 19 bits of each 32-bit element), converters only write
-// lo = tf32_rna(x - trunc_tf32(x)) into a separate ring, so the 4-deep raw ring
-// covers three k-tiles of TMA latency and the conversion has its own two slots.
-template <bool RAW> struct WsRing {
-  static constexpr int kRaw = RAW ? 4 : kWsStages;              // landing stages
-  static constexpr int kLo = RAW ? 2 : kWsStages;               // converted stages
-  static constexpr std::uint32_t kRawBytes = RAW ? 2 * kTTile : kTStage;
-  static constexpr std::uint32_t kLoBytes = RAW ? 2 * kTTile : 0;
-  static constexpr std::uint32_t kOperands = kRaw * kRawBytes + kLo * kLoBytes;
-  static constexpr std::uint32_t kSmem = kOperands + kWsDrainWarps * kWsXBytes + 1024 + 512;
-  static_assert(kSmem <= 232448, "k_pair_ws shared memory");
-};
-__host__ __device__ constexpr std::uint32_t ws_smem(bool raw) {
-  return raw ? WsRing<true>::kSmem : WsRing<false>::kSmem;
-}
-
-__device__ __forceinline__ void mbar_arrive_remote_rel(std::uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-// Drain warps signal a drained TMEM buffer with a relaxed cluster-scope
-// arrive: their tcgen05.ld's have completed (tcgen05.wait::ld, then
-// tcgen05.fence::before_thread_sync) before the arrive issues, so the leader's
-// next MMA into that buffer cannot overtake them; a release here compiles to
-// MEMBAR.ALL.GPU, which waits for the warp's outstanding epilogue stores
-// (r06e: 15% of the kernel's stall samples, the MMA issuer waiting on it).
-__device__ __forceinline__ void mbar_arrive_remote_relaxed(std::uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-__device__ __forceinline__ void mbar_wait_cluster(std::uint32_t mbar, std::uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "TG_WAITK:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@P1 bra TG_DONEK;\n\t"
-      "bra TG_WAITK;\n"
-      "TG_DONEK:\n\t}\n" ::"r"(mbar),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ int g_ws_relax = 0;   // EXPERIMENT
-__device__ unsigned long long g_ws_trace[2][8][64];   // EXPERIMENT: [cta][event][k-tile 100..163]
-__device__ __forceinline__ void ws_trace(std::uint32_t cta, int ev, std::uint32_t gk) {
-  if (cta < 2 && gk >= 100 && gk < 164) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_ws_trace[cta][ev][gk - 100] = t;
-  }
-}
-template <int kWsConvWarps, bool RAW>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(WsShape<kWsConvWarps>::kThreads, 1)
-    k_pair_ws(GemmArgs<float> g, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-              int a_mn, int b_mn, std::uint32_t mp, std::uint32_t nt, std::uint32_t n_tiles) {
-  using Ring = WsRing<RAW>;
-  constexpr int RS = Ring::kRaw, LS = Ring::kLo;
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  float* xpose = reinterpret_cast<float*>(smem + Ring::kOperands);
-  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + Ring::kSmem - 1024 - 512);
-  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 2 * RS + 2 * LS + 4);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const std::uint32_t rank = cluster_rank();
-  const std::uint32_t cid = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
-  auto full = [&](int s) { return smem_u32(&bars[s]); };              // raw stage landed
-  auto rempty = [&](int s) { return smem_u32(&bars[RS + s]); };       // raw stage consumed by the MMAs
-  auto conv = [&](int s) { return smem_u32(&bars[2 * RS + s]); };     // lo (converted) stage written
-  auto lempty = [&](int s) { return smem_u32(&bars[2 * RS + LS + s]); };  // lo stage consumed (RAW)
-  auto tfull = [&](int b) { return smem_u32(&bars[2 * RS + 2 * LS + b]); };
-  auto tempty = [&](int b) { return smem_u32(&bars[2 * RS + 2 * LS + 2 + b]); };
-  // operand tile addresses of raw stage r / lo stage l
-  auto a_hi = [&](int r) { return smem_u32(smem + r * Ring::kRawBytes); };
-  auto b_hi = [&](int r) { return a_hi(r) + (RAW ? kTTile : 2 * kTTile); };
-  auto a_lo = [&](int r, int l) {
-    return RAW ? smem_u32(smem + RS * Ring::kRawBytes + l * Ring::kLoBytes) : a_hi(r) + kTTile;
-  };
-  auto b_lo = [&](int r, int l) { return a_lo(r, l) + (RAW ? kTTile : 2 * kTTile); };
-
-  if (tid == 0) {
-    for (int s = 0; s < RS; ++s) {
-      mbar_init(full(s), 1);
-      mbar_init(rempty(s), 1);
-    }
-    for (int s = 0; s < LS; ++s) {
-      mbar_init(conv(s), rank == 0 ? kWsConvWarps + 1 : kWsConvWarps);   // leader: + the peer's relay
-      mbar_init(lempty(s), 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(tfull(b), 1);
-      mbar_init(tempty(b), 2 * kWsDrainWarps);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tmA)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tmB)) : "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(2 * kPN));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  cluster_sync_all();
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  const std::uint32_t tmem = *tmem_slot;
-
-  struct Tile {
-    int m0, n0, a_off, b_off;
-    std::size_t c_off, c2_off;
-    std::uint32_t z, k_begin, T;
-  };
-  auto tile_of = [&](std::uint32_t L) {
-    Tile t;
-    const std::uint32_t mi = L % mp, ni = (L / mp) % nt, z = L / (mp * nt);
-    t.m0 = static_cast<int>(mi) * (2 * BM) + static_cast<int>(rank) * BM;   // this CTA's 128 rows
-    t.n0 = static_cast<int>(ni) * kPN;
-    t.z = z;
-    std::uint32_t slice = z;
-    t.a_off = t.b_off = 0;
-    t.c_off = t.c2_off = 0;
-    if (g.mem) {
-      const uint4 e = g.mem[z / g.zs];
-      slice = z % g.zs;
-      t.a_off = static_cast<int>(e.x);
-      t.b_off = static_cast<int>(e.y);
-      t.c_off = e.z;
-      t.c2_off = e.w;
-    }
-    std::uint32_t k_end = g.K;
-    t.k_begin = 0;
-    if (g.epi == kEpiSplitK) {
-      t.k_begin = slice * g.k_chunk;
-      k_end = min(g.K, t.k_begin + g.k_chunk);
-    }
-    t.T = k_end > t.k_begin ? (k_end - t.k_begin + BK - 1) / BK : 0;
-    return t;
-  };
-
-  using Shape = WsShape<kWsConvWarps>;
-  if (warp < Shape::kDrain0) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Shape::kRegOther));
-    if (warp == 0) {
-      // ===== TMA producer =====
-      if (lane == 0) {
-        std::uint32_t gk = 0;
-        for (std::uint32_t L = cid; L < n_tiles; L += n_clusters) {
-          const Tile tl = tile_of(L);
-          const int nb = tl.n0 + static_cast<int>(rank) * BN;   // this CTA's B rows
-          for (std::uint32_t t = 0; t < tl.T; ++t, ++gk) {
-            const int s = gk % RS;
-            if (gk >= static_cast<std::uint32_t>(RS)) mbar_wait2(rempty(s), ((gk / RS) - 1) & 1);
-            if (gk >= static_cast<std::uint32_t>(RS)) ws_trace(blockIdx.x, 7, gk - RS);
-            ws_trace(blockIdx.x, 0, gk);
-            mbar_expect_tx(full(s), 2 * kTTile);
-            const int k0 = static_cast<int>(tl.k_begin + t * BK);
-            tma_operand(&tmA, a_mn, a_hi(s), tl.m0, k0, tl.a_off, full(s));
-            tma_operand(&tmB, b_mn, b_hi(s), nb, k0, tl.b_off, full(s));
-          }
-        }
-        // every commit to this CTA's barriers has landed before it may exit
-        for (std::uint32_t j = gk > static_cast<std::uint32_t>(RS) ? gk - RS : 0; j < gk; ++j)
-          mbar_wait2(rempty(j % RS), (j / RS) & 1);
-        if (RAW)
-          for (std::uint32_t j = gk > static_cast<std::uint32_t>(LS) ? gk - LS : 0; j < gk; ++j)
-            mbar_wait2(lempty(j % LS), (j / LS) & 1);
-      }
-    } else if (warp == 1) {
-      if (rank != 0) {
-        // ===== peer CTA: relay of its converted stages to the leader =====
-        // Acquire the local converters' arrivals (cta scope), then one
-        // release.cluster arrive on the leader's barrier: by cumulativity the
-        // converted tiles are visible to the leader's MMA, with one cluster-
-        // scope fence per stage instead of one per converter warp.
-        if (lane == 0) {
-          const std::uint32_t leader_conv0 = peer_addr(conv(0), 0);
-          std::uint32_t gk = 0;
-          for (std::uint32_t L = cid; L < n_tiles; L += n_clusters) {
-            const std::uint32_t T = tile_of(L).T;
-            for (std::uint32_t t = 0; t < T; ++t, ++gk) {
-              const int s = gk % LS;
-              mbar_wait_acq(conv(s), (gk / LS) & 1);
-              ws_trace(blockIdx.x, 3, gk);
-              if (g_ws_relax & 1) mbar_arrive_remote_relaxed(leader_conv0 + s * 8);   // EXPERIMENT
-              else mbar_arrive_remote_rel(leader_conv0 + s * 8);
-              ws_trace(blockIdx.x, 4, gk);
-            }
-          }
-        }
-      } else {
-        // ===== MMA issuer: the leader CTA only =====
-        const std::uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (std::uint32_t(a_mn != 0) << 15) |
-                                    (std::uint32_t(b_mn != 0) << 16) | ((kPN >> 3) << 17) | (((2 * BM) >> 4) << 24);
-        std::uint32_t gk = 0, G = 0;
-        for (std::uint32_t L = cid; L < n_tiles; L += n_clusters) {
-          const Tile tl = tile_of(L);
-          for (std::uint32_t t = 0; t < tl.T; ++t, ++gk) {
-            const int r = gk % RS, l = gk % LS;
-            if (t % kPFlush == 0 && G >= 2) mbar_wait_cluster(tempty(G & 1), ((G >> 1) - 1) & 1);
-            const int buf = G & 1;
-            mbar_wait_cluster(conv(l), (gk / LS) & 1);
-            if (lane == 0) ws_trace(blockIdx.x, 5, gk);
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            if (lane == 0) {
-              const std::uint32_t ah = a_hi(r), al = a_lo(r, l), bh = b_hi(r), bl = b_lo(r, l);
-              const std::uint32_t td = tmem + buf * kPN;
-#pragma unroll
-              for (int ks = 0; ks < BK / 8; ++ks) {
-                const std::uint64_t dAh = operand_desc(ah, a_mn != 0, ks), dAl = operand_desc(al, a_mn != 0, ks);
-                const std::uint64_t dBh = operand_desc(bh, b_mn != 0, ks), dBl = operand_desc(bl, b_mn != 0, ks);
-                mma_tf32_pair(td, dAl, dBh, idesc, (t % kPFlush != 0 || ks != 0) ? 1u : 0u);
-                if (g_ws_relax & 8) continue;   // EXPERIMENT
-                mma_tf32_pair(td, dAh, dBl, idesc, 1u);
-                mma_tf32_pair(td, dAh, dBh, idesc, 1u);
-              }
-              if (RAW) commit_pair(lempty(l));
-              commit_pair(rempty(r));
-              ws_trace(blockIdx.x, 6, gk);
-              if (t % kPFlush == kPFlush - 1 || t == tl.T - 1) commit_pair(tfull(buf));
-            }
-            __syncwarp();
-            if (t % kPFlush == kPFlush - 1 || t == tl.T - 1) ++G;
-          }
-        }
-      }
-    } else {
-      // ===== converters: elementwise over this CTA's A and B tiles =====
-      const int ct = tid - 64;
-      std::uint32_t gk = 0;
-      for (std::uint32_t L = cid; L < n_tiles; L += n_clusters) {
-        const std::uint32_t T = tile_of(L).T;
-        for (std::uint32_t t = 0; t < T; ++t, ++gk) {
-          const int r = gk % RS, l = gk % LS;
-          mbar_wait2(full(r), (gk / RS) & 1);
-          if (ct == 0) ws_trace(blockIdx.x, 1, gk);
-          if (RAW) {
-            if (gk >= static_cast<std::uint32_t>(LS)) mbar_wait2(lempty(l), ((gk / LS) - 1) & 1);
-            // [A raw | B raw] -> [A lo | B lo]: one flat elementwise pass
-            const float4* src = reinterpret_cast<const float4*>(smem + r * Ring::kRawBytes);
-            float4* dst = reinterpret_cast<float4*>(smem + RS * Ring::kRawBytes + l * Ring::kLoBytes);
-#pragma unroll 4
-            for (int i = ct; i < static_cast<int>(2 * kTTile / 16) && !(g_ws_relax & 2); i += kWsConvWarps * 32) {
-              const float4 x = src[i];
-              float4 o;
-              o.x = tf32_rna(x.x - __uint_as_float(__float_as_uint(x.x) & 0xffffe000u));
-              o.y = tf32_rna(x.y - __uint_as_float(__float_as_uint(x.y) & 0xffffe000u));
-              o.z = tf32_rna(x.z - __uint_as_float(__float_as_uint(x.z) & 0xffffe000u));
-              o.w = tf32_rna(x.w - __uint_as_float(__float_as_uint(x.w) & 0xffffe000u));
-              dst[i] = o;
-            }
-          } else {
-            unsigned char* base = smem + r * Ring::kRawBytes;
-#pragma unroll 1
-            for (int op = 0; op < 2; ++op) {
-              float4* hi = reinterpret_cast<float4*>(base + op * 2 * kTTile);
-              float4* lo = reinterpret_cast<float4*>(base + op * 2 * kTTile + kTTile);
-#pragma unroll 2
-              for (int i = ct; i < static_cast<int>(kTTile / 16); i += kWsConvWarps * 32) {
-                const float4 x = hi[i];
-                float4 h, o;
-                h.x = tf32_rna(x.x); o.x = tf32_rna(x.x - h.x);
-                h.y = tf32_rna(x.y); o.y = tf32_rna(x.y - h.y);
-                h.z = tf32_rna(x.z); o.z = tf32_rna(x.z - h.z);
-                h.w = tf32_rna(x.w); o.w = tf32_rna(x.w - h.w);
-                hi[i] = h;
-                lo[i] = o;
-              }
-            }
-          }
-          asm volatile("fence.proxy.async.shared::cta;");   // generic-proxy stores -> tensor-core reads
-          __syncwarp();
-          if (lane == 0) mbar_arrive(conv(l));   // leader: its MMA waits here; peer: the relay does
-          if (ct == 0) ws_trace(blockIdx.x, 2, gk);
-        }
-      }
-    }
-  } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(Shape::kRegDrain));
-    // ===== drain + epilogue: 8 warps; TMEM lane quarter w % 4, column half =====
-    const int wq = warp & 3;
-    const int ch = (warp - Shape::kDrain0) >> 2;
-    constexpr int kCols = kPN / 2;
-    const std::uint32_t leader_tempty0 = peer_addr(tempty(0), 0);
-    float* xb = xpose + (warp - Shape::kDrain0) * (32 * kWsXLd);
-    std::uint32_t G = 0;
-    for (std::uint32_t L = cid; L < n_tiles; L += n_clusters) {
-      const Tile tl = tile_of(L);
-      float acc[kCols];
-#pragma unroll
-      for (int j = 0; j < kCols; ++j) acc[j] = 0.f;
-      const std::uint32_t NGt = (tl.T + kPFlush - 1) / kPFlush;
-      for (std::uint32_t q = 0; q < NGt; ++q, ++G) {
-        const int buf = G & 1;
-        mbar_wait2(tfull(buf), (G >> 1) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-#pragma unroll
-        for (int c = 0; c < kCols; c += 16) {
-          if (g_ws_relax & 4) break;   // EXPERIMENT
-          std::uint32_t v[16];
-          const std::uint32_t taddr = tmem + buf * kPN + (static_cast<std::uint32_t>(wq * 32) << 16) + ch * kCols + c;
-          asm volatile(
-              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-              : "r"(taddr));
-          asm volatile("tcgen05.wait::ld.sync.aligned;");
-#pragma unroll
-          for (int j = 0; j < 16; ++j) acc[c + j] += __uint_as_float(v[j]);
-        }
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        __syncwarp();
-        if (lane == 0) mbar_arrive_remote_relaxed(leader_tempty0 + buf * 8);
-      }
-      // ===== epilogue: rows m0 + 32 wq + i, columns n0 + 128 ch + [0, 128) =====
-      const int mrow0 = tl.m0 + wq * 32;
-      const int ncol0 = tl.n0 + ch * kCols;
-#pragma unroll
-      for (int c = 0; c < kCols; c += 32) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) xb[lane * kWsXLd + j] = acc[c + j];
-        __syncwarp();
-        const std::uint32_t n = static_cast<std::uint32_t>(ncol0 + c + lane);
-#pragma unroll 4
-        for (int i = 0; i < 32; ++i) {
-          const std::uint32_t m = static_cast<std::uint32_t>(mrow0 + i);
-          if (m >= g.M) break;
-          if (n >= g.N) continue;
-          float v = xb[i * kWsXLd + lane];
-          if (g.epi == kEpiSplitK) {
-            g.C[(std::size_t(tl.z) * g.M + m) * g.N + n] = v;
-            continue;
-          }
-          float* dst = g.C + (tl.c_off + m) * g.ldc + n;
-          if (g.epi == kEpiBiasAct) {
-            v += g.bias ? g.bias[m] : 0.f;
-            if (g.act) g.C2[(tl.c2_off + m) * g.ldc + n] = act_fwd<float>(g.act, v);
-            if (g.no_z && g.act) continue;   // z has no reader
-          } else if (g.epi == kEpiAccum && g.dact) {
-            v = act_bwd_h<float>(g.dact, v, g.C2[(tl.c2_off + m) * g.ldc + n]);
-          } else if (g.epi == kEpiAccum && g.beta) {
-            v += *dst;
-          }
-          *dst = v;
-        }
-        __syncwarp();
-      }
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  cluster_sync_all();   // no CTA leaves while its peer may still signal its barriers or read its tiles
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * kPN));
-}
-
 // Host: 2D tensor map of an operand view for TMA (SWIZZLE_128B, zero OOB fill).
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {   // thread-safe one-time lookup
@@ -1543,88 +1138,10 @@ bool make_operand_map(CUtensorMap* map, const float* P, std::size_t ld, bool mn,
   return r == CUDA_SUCCESS;
 }
 
-// MN-major operand as a 3D map {32 rows, K, rows / 32} with strides {ld, 32}
-// elements: one TMA load fills the four 32-wide SWIZZLE_128B chunks of a
-// 128-row k-tile ([chunk][k][32] in shared memory, the 2D layout), where the
-// 2D map needs four.  rows must be a multiple of 32.
-bool make_mn3_map(CUtensorMap* map, const float* P, std::size_t ld, std::uint32_t rows, std::uint32_t K) {
-  auto enc = tensor_map_encoder();
-  if (!enc || rows % 32 != 0) return false;
-  if ((reinterpret_cast<std::uintptr_t>(P) & 15) || ((ld * 4) & 15) || ld * 4 >= (1ull << 40)) return false;
-  cuuint64_t dims[3] = {32, K, rows / 32};
-  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 4, 128};
-  cuuint32_t box[3] = {32, 32, 4};
-  cuuint32_t estr[3] = {1, 1, 1};
-  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(P), dims, strides, box, estr,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
-                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
-
 // CTA pairs for products with more than one 128-row M tile (TG_UMMA_PAIR=0: single CTAs)
 bool use_pair(std::uint32_t M) {
   static const bool on = !(std::getenv("TG_UMMA_PAIR") && std::getenv("TG_UMMA_PAIR")[0] == '0');
   return on && M > static_cast<std::uint32_t>(BM);
-}
-
-// Persistent warp-specialised CTA pairs (TG_UMMA_WS=0: the non-persistent k_umma_pair, for A/B runs)
-bool use_ws() {
-  static const bool on = !(std::getenv("TG_UMMA_WS") && std::getenv("TG_UMMA_WS")[0] == '0');
-  return on;
-}
-// co-resident (2,1,1) clusters of k_pair_ws on this device (one per SM pair at best)
-template <int NC, bool RAW>
-cudaError_t launch_ws(const GemmArgs<float>& g, const CUtensorMap& ta, const CUtensorMap& tb, int a_mn, int b_mn,
-                      std::uint32_t mp, std::uint32_t nt, std::uint32_t tiles, cudaStream_t st) {
-  static PerDeviceOnce attr;
-  static PerDeviceValue clusters;
-  if (const cudaError_t e = attr.ensure([] {
-        return cudaFuncSetAttribute(k_pair_ws<NC, RAW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(WsRing<RAW>::kSmem));
-      }); e != cudaSuccess)
-    return e;
-  // co-resident (2,1,1) clusters on this device (one per SM pair at best)
-  const int nc = clusters.get([] {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(2 * 512, 1, 1);
-    cfg.blockDim = dim3(WsShape<NC>::kThreads, 1, 1);
-    cfg.dynamicSmemBytes = WsRing<RAW>::kSmem;
-    cudaLaunchAttribute at{};
-    at.id = cudaLaunchAttributeClusterDimension;
-    at.val.clusterDim.x = 2;
-    at.val.clusterDim.y = 1;
-    at.val.clusterDim.z = 1;
-    cfg.attrs = &at;
-    cfg.numAttrs = 1;
-    int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, k_pair_ws<NC, RAW>, &cfg) != cudaSuccess || n <= 0) {
-      cudaGetLastError();
-      n = sm_count() / 2;
-    }
-    return n;
-  });
-  static const bool relax = [] {
-    int v = std::getenv("TG_WS_RELAX") ? std::atoi(std::getenv("TG_WS_RELAX")) : 0;
-    cudaMemcpyToSymbol(g_ws_relax, &v, sizeof(int));
-    return v;
-  }();
-  (void)relax;
-  static const bool fullgrid = std::getenv("TG_WS_FULLGRID") != nullptr;   // EXPERIMENT
-  const std::uint32_t grid = 2 * (fullgrid ? tiles : std::min<std::uint32_t>(tiles, static_cast<std::uint32_t>(nc)));
-  k_pair_ws<NC, RAW><<<grid, WsShape<NC>::kThreads, WsRing<RAW>::kSmem, st>>>(g, ta, tb, a_mn, b_mn, mp, nt, tiles);
-  if (std::getenv("TG_WS_TRACE")) {   // EXPERIMENT
-    static unsigned long long h[2][8][64];
-    cudaDeviceSynchronize();
-    cudaMemcpyFromSymbol(h, g_ws_trace, sizeof(h));
-    const unsigned long long t0 = h[0][0][0];
-    for (int c = 0; c < 2; ++c)
-      for (int k = 0; k < 64; k += 8) {
-        std::fprintf(stderr, "cta%d gk%3d:", c, 100 + k);
-        for (int e = 0; e < 8; ++e) std::fprintf(stderr, " %8.3f", h[c][e][k] ? (double)(long long)(h[c][e][k] - t0) * 1e-3 : -1.0);
-        std::fprintf(stderr, "\n");
-      }
-  }
-  return cudaGetLastError();
 }
 
 cudaError_t launch_tma_kernel(const GemmArgs<float>& g, std::uint32_t z, const CUtensorMap& ta, const CUtensorMap& tb,
@@ -1643,26 +1160,6 @@ cudaError_t launch_tma_kernel(const GemmArgs<float>& g, std::uint32_t z, const C
     return e0;
   // (routing short-K products with M > 128 to the persistent single-CTA tiles
   // instead was measured slower end to end: cfg3 1.61 -> 1.83 ms, cfg4 34.6 -> 37.0 ms)
-  if (use_pair(g.M) && !g.no_pair && use_ws()) {
-    const std::uint32_t mp = (g.M + 2 * BM - 1) / (2 * BM), nt = (g.N + kPN - 1) / kPN;
-    const std::uint32_t tiles = mp * nt * z;
-    if (tiles == 0) return cudaSuccess;
-    static const int nconv = std::getenv("TG_WS_CONV") ? std::atoi(std::getenv("TG_WS_CONV")) : 10;
-    static const bool raw = !(std::getenv("TG_WS_RAW") && std::getenv("TG_WS_RAW")[0] == '0');
-    int a = a_mn ? 1 : 0, b = b_mn ? 1 : 0;
-    CUtensorMap ta3 = ta, tb3 = tb;
-    static const bool mn3 = !(std::getenv("TG_WS_MN3") && std::getenv("TG_WS_MN3")[0] == '0');
-    if (mn3 && a && make_mn3_map(&ta3, g.A, g.lda, g.M, g.a_span ? g.a_span : g.K)) a = 2;
-    if (mn3 && b && make_mn3_map(&tb3, g.B, g.ldb, g.N, g.b_span ? g.b_span : g.K)) b = 2;
-    cudaError_t e = cudaSuccess;
-    if (nconv == 14) e = launch_ws<14, true>(g, ta3, tb3, a, b, mp, nt, tiles, st);
-    else if (nconv == 6 && raw) e = launch_ws<6, true>(g, ta3, tb3, a, b, mp, nt, tiles, st);
-    else if (nconv == 6) e = launch_ws<6, false>(g, ta3, tb3, a, b, mp, nt, tiles, st);
-    else if (raw) e = launch_ws<10, true>(g, ta3, tb3, a, b, mp, nt, tiles, st);
-    else e = launch_ws<10, false>(g, ta3, tb3, a, b, mp, nt, tiles, st);
-    if (e != cudaSuccess) return e;
-    return cudaGetLastError();
-  }
   if (use_pair(g.M) && !g.no_pair) {
     const dim3 grid(2 * ((g.M + 2 * BM - 1) / (2 * BM)), (g.N + kPN - 1) / kPN, z);
     k_umma_pair<kTStagesMax><<<grid, kPThreads, pair_smem(kTStagesMax), st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0);
