@@ -6,7 +6,11 @@ CXX     ?= g++
 PKG     := paper_2503_13795_b200
 BUILD   := build
 ARCH    := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -lineinfo -O3 -std=c++20 -Xcompiler -fPIC -Xptxas -v -Iinclude -I$(PKG)/csrc/host
+# NCCL >= 2.28 headers (symmetric-memory device API) for tg_exchange.cu: the
+# torch-bundled NCCL's; the system /usr/include/nccl.h is 2.27
+NCCL_INC ?= $(firstword $(wildcard /opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/include) \
+            $(shell python3 -c "import nvidia, os; print(os.path.join(list(nvidia.__path__)[0], 'nccl', 'include'))" 2>/dev/null))
+NVFLAGS := $(ARCH) -lineinfo -O3 -std=c++20 -Xcompiler -fPIC -Xptxas -v -Iinclude -I$(PKG)/csrc/host -I$(NCCL_INC)
 CXXFLAGS:= -std=c++20 -O2 -fPIC -Wall -Iinclude -I$(PKG)/csrc/host -I$(CUDA)/include -I$(BUILD)
 BUILD   := build
 

@@ -240,6 +240,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "fused"],
+                    help="N > 1: NCCL all-reduce + GD (tg_allreduce_gd_step) or the fused exchange + GD kernel over "
+                         "NCCL symmetric memory (tg_window_allreduce_gd, NVLS multicast when available)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = dict(CONFIGS[args.config])
@@ -288,6 +291,11 @@ def main():
     X, K, L = Xs[0], Ks[0], Ls[0]
     P = torch.tensor(params0, device=dev, dtype=tdt)
     G = torch.zeros(max(desc.n_params, 1), device=dev, dtype=tdt)
+    win = None
+    if world > 1 and args.exchange == "fused" and desc.n_params:
+        from paper_2503_13795_b200.dp import SymmetricWindow
+        win = SymmetricWindow(comm, cfg["dtype"], desc.n_params)   # G is this rank's window buffer
+        G = win.grad
     W = prog.alloc_workspace(b)
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
@@ -312,7 +320,10 @@ def main():
             prog.train_step(Xi, Ki, b, P, Ls[j], G, cfg["gamma"], W, st)
         else:              # local sum -> NCCL all-reduce of the d-vector -> GD with the global batch
             prog.forward_backward(Xi, Ki, b, P, Ls[j], None, G, W, st)
-            prog.allreduce_gd_step(P, G, cfg["gamma"], gb, comm, st)
+            if win is not None:
+                win.allreduce_gd(P, cfg["gamma"], gb, st)
+            else:
+                prog.allreduce_gd_step(P, G, cfg["gamma"], gb, comm, st)
 
     l0 = prog.launches
     step()
@@ -461,6 +472,9 @@ def main():
         "l2": ("rotating buffer sets > 2x L2, back to back" if hbm_bound else
                "flushed between timed steps (256 MiB write, then 256 MiB read so no dirty lines remain)"),
         "cuda_graph": graphs is not None, "kernel_tier": tier, "tile_samples": info["tile_samples"],
+        "exchange": ("none (one rank: GD fused in the reduction epilogue)" if world == 1 else
+                     "tg_allreduce_gd_step (NCCL all-reduce + GD)" if win is None else
+                     "tg_window_allreduce_gd (fused, %s)" % ("NVLS multimem" if win.multimem else "NVLink peer loads")),
         "node_evals_per_s": value * (info["n_sample_nodes"] + info["n_uniform_nodes"] / max(b, 1)),
         "roofline": roof,
         "gpu_launches": launches_per_step * args.steps,
@@ -472,6 +486,8 @@ def main():
         line["cpu_baseline"], line["cpu_baseline_1core"] = cpu_baselines(cfg, b)
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if win is not None:
+        win.close()
     if comm is not None:
         comm.close()
     if world > 1:

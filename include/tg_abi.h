@@ -280,6 +280,30 @@ int tg_nccl_version(void);
 tg_status tg_allreduce_gd_step(tg_program_t p, void* params, void* grad_sum, double gamma, size_t global_batch,
                                tg_comm_t comm, tg_stream_t stream);
 
+/* ---- fused exchange + GD over symmetric peer memory ----
+ * A window is NCCL symmetric memory for the d-length gradient sum
+ * (ncclMemAlloc + ncclCommWindowRegister(NCCL_WIN_COLL_SYMMETRIC) + the NCCL
+ * >= 2.28 device API): every rank's buffer is load/store reachable from every
+ * rank over NVLink, and with TG_WINDOW_MULTIMEM (fp32) on an NVSwitch fabric
+ * that supports it, through one multicast (NVLS) address.  Collective: every
+ * rank calls create / allreduce_gd / destroy in the same order.
+ * tg_window_buffer is this rank's gradient buffer: pass it as grad_sum to
+ * tg_forward_backward, then tg_window_allreduce_gd replaces
+ * tg_allreduce_gd_step with ONE kernel: sum over ranks (switch-side
+ * multimem.ld_reduce + multimem.st, or peer loads summed in rank order and
+ * stored back to every rank), then x -= gamma * g / global_batch on `params`
+ * (the sgd_step of SPEC.md:424-430; equal to tg_gd_update bit for bit on one
+ * rank).  On return the window holds the global sum on every rank.
+ * Replaces, with tg_allreduce_gd_step, the reference's sequential
+ * GradAccumulator + sgd_step at N > 1.                    */
+typedef struct tg_window* tg_window_t;
+#define TG_WINDOW_MULTIMEM 1
+tg_status tg_window_create(tg_comm_t comm, tg_dtype dtype, size_t count, int flags, tg_window_t* out);
+tg_status tg_window_destroy(tg_window_t w);
+void* tg_window_buffer(tg_window_t w);
+int tg_window_multimem(tg_window_t w);
+tg_status tg_window_allreduce_gd(tg_window_t w, void* params, double gamma, size_t global_batch, tg_stream_t stream);
+
 /* Fused single-GPU step: forward_backward + gd_update. */
 tg_status tg_train_step(tg_program_t p, const void* inputs, const int32_t* index_inputs,
                         size_t batch, void* params, void* loss_out, void* grad_sum,

@@ -148,6 +148,11 @@ def _load():
         "tg_nccl_comm_destroy": (st, [P]),
         "tg_nccl_version": (C.c_int, []),
         "tg_allreduce_gd_step": (st, [P, P, P, C.c_double, sz, P, P]),
+        "tg_window_create": (st, [P, st, sz, C.c_int, C.POINTER(P)]),
+        "tg_window_destroy": (st, [P]),
+        "tg_window_buffer": (P, [P]),
+        "tg_window_multimem": (C.c_int, [P]),
+        "tg_window_allreduce_gd": (st, [P, P, C.c_double, sz, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

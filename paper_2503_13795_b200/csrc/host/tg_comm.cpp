@@ -89,6 +89,11 @@ bool allreduce_sum(void* buf, std::size_t count, tg_dtype dtype, void* comm, cud
   return true;
 }
 
+void* nccl_symbol(const char* name) {
+  Nccl& n = nccl();
+  return n.so ? dlsym(n.so, name) : nullptr;
+}
+
 int comm_size(void* comm) {
   Nccl& n = nccl();
   int c = 0;

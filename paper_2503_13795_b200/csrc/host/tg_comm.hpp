@@ -19,5 +19,7 @@ bool available(std::string& err);
 bool allreduce_sum(void* buf, std::size_t count, tg_dtype dtype, void* comm, cudaStream_t st, std::string& err);
 /// ncclCommCount, -1 on failure.
 int comm_size(void* comm);
+/// dlsym of the bound NCCL library (nullptr when absent or not exported).
+void* nccl_symbol(const char* name);
 
 }  // namespace tgcomm

@@ -65,6 +65,53 @@ class NcclComm:
             pass
 
 
+class _CudaArray:
+    """__cuda_array_interface__ view of a raw device buffer (torch.as_tensor wraps it without a copy)."""
+
+    def __init__(self, ptr: int, n: int, dtype: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8" if dtype == "f64" else "<f4",
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+class SymmetricWindow:
+    """The gradient buffer of the fused exchange: NCCL
+    symmetric memory on every rank of `comm` (tg_window_create).  `grad` is
+    this rank's buffer as a torch tensor (zero-copy): pass it as grad_sum to
+    forward_backward, then allreduce_gd() sums it over the ranks and applies
+    the GD update in one kernel (multicast / NVLS when `multimem`, NVLink peer
+    loads summed in rank order otherwise).  Collective on all ranks."""
+
+    def __init__(self, comm: NcclComm, dtype: str, count: int, multimem: bool = True):
+        import torch
+        h = C.c_void_p()
+        check(lib.tg_window_create(C.c_void_p(comm.handle), 0 if dtype == "f64" else 1, int(count),
+                                   1 if multimem else 0, C.byref(h)))
+        self.handle = h.value
+        self.dtype, self.count = dtype, count
+        self.multimem = bool(lib.tg_window_multimem(h))
+        ptr = lib.tg_window_buffer(h)
+        self.grad = torch.as_tensor(_CudaArray(ptr, count, dtype), device="cuda")
+
+    def allreduce_gd(self, params, gamma: float, global_batch: int, stream=None):
+        import torch
+        s = stream if stream is not None else torch.cuda.current_stream()
+        check(lib.tg_window_allreduce_gd(C.c_void_p(self.handle), C.c_void_p(params.data_ptr()), float(gamma),
+                                         int(global_batch), C.c_void_p(s.cuda_stream)))
+        return params
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.grad = None
+            check(lib.tg_window_destroy(C.c_void_p(self.handle)))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class DataParallelStep:
     """One DP training step over a compiled Program.
 
@@ -74,14 +121,19 @@ class DataParallelStep:
     local gradient sum tensor when given.
     """
 
-    def __init__(self, program=None, group=None, comm: NcclComm | None = None):
+    def __init__(self, program=None, group=None, comm: NcclComm | None = None, window: SymmetricWindow | None = None):
         self.program = program
         self.group = group
         self.comm = comm
+        self.window = window   # fused exchange + GD (grad must be window.grad)
 
     def step(self, params, grad, gamma: float, global_batch: int, local_grad=None, stream=None):
         if local_grad is not None:
             local_grad(params)
+        if self.window is not None:
+            if grad is not None and grad.data_ptr() != self.window.grad.data_ptr():
+                raise ValueError("DataParallelStep: with a window the gradient buffer is window.grad")
+            return self.window.allreduce_gd(params, gamma, global_batch, stream)
         if self.comm is not None and self.program is not None:
             self.program.allreduce_gd_step(params, grad, gamma, global_batch, self.comm, stream)
             return params

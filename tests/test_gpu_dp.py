@@ -91,3 +91,41 @@ def test_allreduce_gd_step_without_comm_is_gd_update():
     prog.allreduce_gd_step(P2, G, 0.1, 1000, comm=None)
     torch.cuda.synchronize()
     assert torch.equal(P1, P2)
+
+
+@pytest.mark.parametrize("name,dt,b", [("moons", "f64", 4096), ("char_mlp", "f32", 4096), ("wide_mlp", "f32", 512)])
+def test_fused_window_exchange_equals_nccl_path(name, dt, b):
+    """§8f row 4: the fused exchange + GD kernel over NCCL symmetric memory
+    (tg_window_allreduce_gd) against the NCCL path (tg_allreduce_gd_step) on a
+    single-rank communicator: identical parameters and global gradient sums,
+    bit for bit, over several steps (the window's barrier epochs advance)."""
+    from paper_2503_13795_b200.dp import SymmetricWindow
+    desc, x, k, prog, T, X, K = _setup(name, dt, b)
+    W = prog.alloc_workspace(b)
+    comm = NcclComm(0, 1, uid=nccl_unique_id())
+    try:
+        win = SymmetricWindow(comm, dt, desc.n_params)
+    except tg.TgError as e:
+        comm.close()
+        pytest.skip(f"no NCCL symmetric-memory device API here: {e}")
+    try:
+        P1 = torch.tensor(desc.param_values(), device="cuda", dtype=T)
+        P2 = P1.clone()
+        L = torch.zeros(b, device="cuda", dtype=T)
+        G1 = torch.zeros(desc.n_params, device="cuda", dtype=T)
+        dp = DataParallelStep(prog, window=win)
+        side = torch.cuda.Stream()
+        for _ in range(4):
+            prog.forward_backward(X, K, b, P1, L, None, G1, W)
+            prog.allreduce_gd_step(P1, G1, 0.05, b, comm)
+            side.wait_stream(torch.cuda.current_stream())
+            prog.forward_backward(X, K, b, P2, L, None, win.grad, W, stream=side)
+            dp.step(P2, win.grad, 0.05, b, stream=side)
+            torch.cuda.current_stream().wait_stream(side)
+            torch.cuda.synchronize()
+            assert torch.equal(G1, win.grad), "global gradient sums differ"
+            assert torch.equal(P1, P2), "parameters differ"
+        assert not bool(torch.isnan(P2).any())
+    finally:
+        win.close()
+        comm.close()
