@@ -64,20 +64,28 @@ __device__ __forceinline__ void mm_st(float* p, float v) {
   asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
 
+// The call's epoch comes from the barrier counter itself, so a captured CUDA
+// graph replays correctly: when CTA c of this rank reads flagsA[c] at the start
+// of call e it holds (e - 1) * W plus the arrivals of faster peers for call e
+// (< W: no rank arrives for call e + 1 before this one passed barrier B of e).
 template <class T, bool MM>
 __global__ void __launch_bounds__(kThreads) k_allreduce_gd(const Bases* __restrict__ bases, std::size_t flags_off,
-                                                           std::size_t count, int rank, int world, unsigned epoch,
+                                                           std::size_t count, int rank, int world,
                                                            T* __restrict__ params, T gamma, T b) {
   const unsigned C = gridDim.x, c = blockIdx.x;
   T* grad = reinterpret_cast<T*>(bases->peer[rank]);
   unsigned* flagsA = reinterpret_cast<unsigned*>(bases->peer[rank] + flags_off);
   unsigned* flagB = flagsA + kMaxCtas;
+  __shared__ unsigned s_epoch;
   if (threadIdx.x == 0) {
+    const unsigned epoch = ld_acquire_sys(flagsA + c) / static_cast<unsigned>(world) + 1u;
+    s_epoch = epoch;
     for (int p = 0; p < world; ++p) red_release_sys(reinterpret_cast<unsigned*>(bases->peer[p] + flags_off) + c, 1u);
     while (ld_acquire_sys(flagsA + c) < epoch * static_cast<unsigned>(world)) {
     }
   }
   __syncthreads();
+  const unsigned epoch = s_epoch;
   const std::size_t chunk = (count + world - 1) / world;
   const std::size_t lo = static_cast<std::size_t>(rank) * chunk;
   const std::size_t hi = lo + chunk < count ? lo + chunk : count;
@@ -128,7 +136,6 @@ struct tg_window {
   ncclDevComm dev{};
   bool dev_ok = false;
   tgx::Bases* d_bases = nullptr;
-  unsigned epoch = 0;
 };
 
 namespace {
@@ -254,18 +261,17 @@ tg_status tg_window_allreduce_gd(tg_window_t w, void* params, double gamma, size
   unsigned grid = static_cast<unsigned>((per_rank + tgx::kThreads * 4 - 1) / (tgx::kThreads * 4));
   grid = grid < 1 ? 1 : grid > 128 ? 128 : grid;   // co-resident on any B200 (spin barriers)
   // every rank must launch the same grid: it depends on count and world only
-  ++w->epoch;
   if (w->dtype == TG_F64) {
     tgx::k_allreduce_gd<double, false><<<grid, tgx::kThreads, 0, st>>>(
-        w->d_bases, w->flags_off, w->count, w->rank, w->world, w->epoch, static_cast<double*>(params), gamma,
+        w->d_bases, w->flags_off, w->count, w->rank, w->world, static_cast<double*>(params), gamma,
         static_cast<double>(global_batch));
   } else if (w->multimem) {
     tgx::k_allreduce_gd<float, true><<<grid, tgx::kThreads, 0, st>>>(
-        w->d_bases, w->flags_off, w->count, w->rank, w->world, w->epoch, static_cast<float*>(params),
+        w->d_bases, w->flags_off, w->count, w->rank, w->world, static_cast<float*>(params),
         static_cast<float>(gamma), static_cast<float>(global_batch));
   } else {
     tgx::k_allreduce_gd<float, false><<<grid, tgx::kThreads, 0, st>>>(
-        w->d_bases, w->flags_off, w->count, w->rank, w->world, w->epoch, static_cast<float*>(params),
+        w->d_bases, w->flags_off, w->count, w->rank, w->world, static_cast<float*>(params),
         static_cast<float>(gamma), static_cast<float>(global_batch));
   }
   const cudaError_t e = cudaGetLastError();

@@ -129,3 +129,47 @@ def test_fused_window_exchange_equals_nccl_path(name, dt, b):
     finally:
         win.close()
         comm.close()
+
+
+def test_fused_window_exchange_in_cuda_graph():
+    """The fused exchange's barrier epochs live on the device, so a captured
+    CUDA graph (forward_backward + tg_window_allreduce_gd) replays correctly:
+    five replays equal five eager NCCL-path steps bit for bit."""
+    from paper_2503_13795_b200.dp import SymmetricWindow
+    desc, x, k, prog, T, X, K = _setup("char_mlp", "f32", 2048)
+    b = 2048
+    W = prog.alloc_workspace(b)
+    comm = NcclComm(0, 1, uid=nccl_unique_id())
+    try:
+        win = SymmetricWindow(comm, "f32", desc.n_params)
+    except tg.TgError as e:
+        comm.close()
+        pytest.skip(f"no NCCL symmetric-memory device API here: {e}")
+    try:
+        P1 = torch.tensor(desc.param_values(), device="cuda", dtype=T)
+        P2 = P1.clone()
+        L1 = torch.zeros(b, device="cuda", dtype=T)
+        L2 = torch.zeros(b, device="cuda", dtype=T)
+        G1 = torch.zeros(desc.n_params, device="cuda", dtype=T)
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):     # warm-up call outside the capture (first-use allocations)
+            prog.forward_backward(X, K, b, P2, L2, None, win.grad, W, stream=s)
+            win.allreduce_gd(P2, 0.0, b, s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            prog.forward_backward(X, K, b, P2, L2, None, win.grad, W, stream=s)
+            win.allreduce_gd(P2, 0.05, b, s)
+        torch.cuda.synchronize()
+        for _ in range(5):
+            prog.forward_backward(X, K, b, P1, L1, None, G1, W)
+            prog.allreduce_gd_step(P1, G1, 0.05, b, comm)
+            torch.cuda.synchronize()
+            g.replay()
+            torch.cuda.synchronize()
+            assert torch.equal(G1, win.grad) and torch.equal(P1, P2) and torch.equal(L1, L2)
+    finally:
+        del g
+        win.close()
+        comm.close()
