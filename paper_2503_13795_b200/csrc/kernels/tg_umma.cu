@@ -471,10 +471,13 @@ __global__ void __launch_bounds__(kTThreads, 1) k_umma_tma(GemmArgs<float> g, co
       }
       asm volatile("fence.proxy.async.shared::cta;");   // generic-proxy stores -> tensor-core reads
       mbar_arrive(conv(s));
-      // the previous group's accumulator is complete once this tile's conversion is handed over
-      if (t % kFlush == 0 && t > 0) drain(t / kFlush - 1);
+      // drain two groups back: its MMAs retired before the previous group's
+      // began, so the converters never wait on the tensor core here (draining
+      // the previous group stalled the next conversion until those MMAs were
+      // done, a bubble in front of every group's MMAs)
+      if (t % kFlush == 0 && t / kFlush >= 2) drain(t / kFlush - 2);
     }
-    if (NG > 0) drain(NG - 1);
+    for (std::uint32_t q = NG >= 2 ? NG - 2 : 0; q < NG; ++q) drain(q);
     // ===== epilogue: through shared memory, then whole 512-byte rows per warp =====
     // (one row per thread straight to global made every store touch 32 rows:
     // ~14 us of fixed cost per CTA, measured by scripts/gemm_ksweep.py)
@@ -1032,9 +1035,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
       asm volatile("fence.proxy.async.shared::cta;");   // generic-proxy stores -> tensor-core reads
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(leader_conv0 + s * 8);
-      if (t % kPFlush == 0 && t > 0) drain(t / kPFlush - 1);
+      // two groups back (see k_umma_tma): no converter stall on the tensor core
+      if (t % kPFlush == 0 && t / kPFlush >= 2) drain(t / kPFlush - 2);
     }
-    if (NG > 0) drain(NG - 1);
+    for (std::uint32_t q = NG >= 2 ? NG - 2 : 0; q < NG; ++q) drain(q);
     // ===== epilogue: this CTA's 128 rows x 256 columns through shared memory =====
     constexpr int kLd = kPN + 4;
     float* tile = reinterpret_cast<float*>(smem);
