@@ -1068,12 +1068,13 @@ Layout layout(const tg_program& pr, std::size_t batch) {
     std::size_t sk = 0;
     for (std::size_t i = 0; i < pr.P.dense.size(); ++i)
       if (pr.dplan[i].gemm && pr.dplan[i].dw_dest0 != tgc::kNone)
-        sk = std::max<std::size_t>(sk, std::size_t(splitk_splits(pr.P.dense[i], cb, t)) * pr.P.dense[i].n_out * pr.P.dense[i].n_in);
+        sk = std::max<std::size_t>(sk, std::size_t(splitk_splits(pr.P.dense[i], cb, t)) *
+                                           (std::size_t(pr.P.dense[i].n_out) * pr.P.dense[i].n_in + pr.P.dense[i].n_out));
     for (const auto& B : pr.batches)
       if (B.bw) {
         const tgc::Dense& D = pr.P.dense[B.members.front()];
         const std::uint32_t nm = static_cast<std::uint32_t>(B.members.size());
-        sk = std::max<std::size_t>(sk, std::size_t(nm) * batch_splits(D, nm, cb) * D.n_out * D.n_in);
+        sk = std::max<std::size_t>(sk, std::size_t(nm) * batch_splits(D, nm, cb) * (std::size_t(D.n_out) * D.n_in + D.n_out));
       }
     L.sk = off; off = align_up(off + std::max<std::size_t>(1, sk) * t);
     L.sp = off; off = align_up(off + std::max<std::size_t>(1, std::size_t(pr.sc_groups.size()) * pr.sc_chunks * pr.sc_rmax) * t);
@@ -1188,6 +1189,12 @@ tg_status upload(tg_program& pr) {
 
 // Dense-layer GEMM: tcgen05 tensor cores for fp32 (3xTF32), SIMT for fp64
 // (there is no fp64 tcgen05 kind) or when disabled.
+// role bits of the tcgen05 path (TG_UMMA_MASK): 1 forward, 2 input adjoints, 4 weight gradients
+bool umma_role(const tg_program& pr, int role) {
+  static const int mask = std::getenv("TG_UMMA_MASK") ? std::atoi(std::getenv("TG_UMMA_MASK")) : 7;
+  return pr.umma && (mask & role);
+}
+
 template <class T>
 cudaError_t dense_gemm(const tg_program& pr, const tgk::GemmArgs<T>& g, std::uint32_t splits, cudaStream_t st) {
   if constexpr (std::is_same_v<T, float>) {
@@ -1198,9 +1205,8 @@ cudaError_t dense_gemm(const tg_program& pr, const tgk::GemmArgs<T>& g, std::uin
     // SIMT GEMM's 5e-7..6.5e-6; scripts/gemm_kerr.py).  With the biased
     // accumulation of round 1 (~6e-6 at K ~ 1e3) the forward role had flipped
     // ReLU masks and moved cfg5's gradient by 5.5e-4, so it had stayed on SIMT.
-    static const int mask = std::getenv("TG_UMMA_MASK") ? std::atoi(std::getenv("TG_UMMA_MASK")) : 7;
     const int role = g.epi == tgk::kEpiBiasAct ? 1 : g.epi == tgk::kEpiAccum ? 2 : 4;
-    if (pr.umma && (mask & role)) return tgk::launch_gemm_umma(g, splits, st);
+    if (umma_role(pr, role)) return tgk::launch_gemm_umma(g, splits, st);
   }
   return tgk::launch_gemm<T>(g, splits, st);
 }
@@ -1403,7 +1409,9 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
       return dense_gemm<T>(pr, g, 1, st);
     };
     // dW[n_out][n_in] += dZ[n_out][n] . X^T, split-K over samples (one member)
-    auto dw_one = [&](std::uint32_t u) -> cudaError_t {
+    bool db_fused_u = false;   // the last dw_one also produced its layer's bias gradient
+    auto dw_one = [&](std::uint32_t u, bool fuse_db) -> cudaError_t {
+      db_fused_u = false;
       const tgc::Dense& D = P.dense[u];
       const std::uint32_t splits = splitk_splits(D, n, sizeof(T));
       tgk::GemmArgs<T> g{};
@@ -1419,8 +1427,19 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
       g.k_chunk = static_cast<std::uint32_t>((n + splits - 1) / splits);
       g.epi = tgk::kEpiSplitK;
       pr.launches += 2;
+      // the bias gradient (row sums of dz) rides in the CTA-pair product's converters
+      bool rs = false;
+      if constexpr (std::is_same_v<T, float>) {
+        rs = fuse_db && pr.dplan[u].db_dest0 != tgc::kNone && umma_role(pr, 4) && tgk::umma_rowsum_fusable(g);
+        if (rs) g.rowsum = sk + std::size_t(splits) * D.n_out * D.n_in;
+      }
       cudaError_t e = dense_gemm<T>(pr, g, splits, st);
       if (e == cudaSuccess) e = tgk::launch_splitk_reduce<T>(sk, acc + pr.dplan[u].dw_dest0, D.n_out * D.n_in, splits, st);
+      if (e == cudaSuccess && rs) {
+        e = tgk::launch_splitk_reduce<T>(g.rowsum, acc + pr.dplan[u].db_dest0, D.n_out, splits, st);
+        ++pr.launches;
+        db_fused_u = true;
+      }
       return e;
     };
     // ---- forward stages ----
@@ -1512,7 +1531,7 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
       }
       // input-leaf x rows: their adjoints are read only by the input-gradient output
       bool dx_done = !igrad && B.x_inputs;
-      bool dw_done = false;
+      bool dw_done = false, db_done = false;
       if (!dx_done && !B.zero_x.empty()) {
         TG_CUDA_TRY(tgk::launch_zero_rows<T>(G, B.d_zero_x, static_cast<std::uint32_t>(B.zero_x.size()), n, cb, st));
         ++pr.launches;
@@ -1561,9 +1580,17 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
           g.epi = tgk::kEpiSplitK;
           g.mem = B.d_tab + 2 * nm;
           g.zs = zs;
+          // the bias gradient (row sums of dz) rides in the product's converters
+          const bool rs = dp0.db_dest0 != tgc::kNone && tgk::umma_rowsum_fusable(g);
+          if (rs) g.rowsum = sk + std::size_t(nm) * zs * D.n_out * D.n_in;
           TG_CUDA_TRY(tgk::launch_gemm_umma(g, nm * zs, st));
           TG_CUDA_TRY(tgk::launch_splitk_reduce<T>(sk, acc + dp0.dw_dest0, D.n_out * D.n_in, nm * zs, st));
           pr.launches += 2;
+          if (rs) {
+            TG_CUDA_TRY(tgk::launch_splitk_reduce<T>(g.rowsum, acc + dp0.db_dest0, D.n_out, nm * zs, st));
+            ++pr.launches;
+            db_done = true;
+          }
           dw_done = true;
         }
       }
@@ -1571,9 +1598,12 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
         const std::uint32_t u = B.members[p];
         // zeroed rows above follow the batch's beta; members that only assign keep their store
         if (!dx_done) TG_CUDA_TRY(dx_one(u, B.beta ? pr.dplan[u].beta : 0, B.dx_act, B.tab[nm + p].z));
-        if (!dw_done && pr.dplan[u].dw_dest0 != tgc::kNone) TG_CUDA_TRY(dw_one(u));
+        if (!dw_done && pr.dplan[u].dw_dest0 != tgc::kNone) {
+          TG_CUDA_TRY(dw_one(u, nm == 1));
+          if (db_fused_u) db_done = true;
+        }
       }
-      if (dp0.db_dest0 != tgc::kNone) {
+      if (dp0.db_dest0 != tgc::kNone && !db_done) {
         TG_CUDA_TRY(tgk::launch_rowsum_batched<T>(G, B.d_tab, nm, D.n_out, n, cb, acc + dp0.db_dest0, sk,
                                                   (L.sp - L.sk) / sizeof(T), st));   // split-K scratch, free here
         ++pr.launches;

@@ -95,6 +95,9 @@ struct GemmArgs {
   std::uint32_t dact;
   // kEpiBiasAct with act: store only H (C2); the pre-activation Z has no reader
   bool no_z;
+  // kEpiSplitK, K-major A on the CTA pairs (umma_rowsum_fusable): also write
+  // the row sums of A over this split's k range to rowsum[z * M + m]
+  T* rowsum;
 };
 
 // Table-scatter (kind-1) batch terms grouped by (adjoint row a, index column f).
@@ -126,6 +129,7 @@ cudaError_t launch_attn(bool fwd, const tgc::Instr* list, std::uint32_t begin, s
                         cudaStream_t st);
 // CTAs one split-K slice / batch member of a tcgen05 product launches (CTA pairs when M > 128)
 std::uint32_t umma_ctas_per_slice(std::uint32_t M, std::uint32_t N);
+bool umma_rowsum_fusable(const GemmArgs<float>& g);
 // dst[m * N + n] += sum_kz part[kz][m][n]   (fixed order)
 template <class T> cudaError_t launch_splitk_reduce(const T* part, T* dst, std::uint32_t MN, std::uint32_t splits, cudaStream_t st);
 // G[z rows] = act'(G[h rows], V[h rows], V[z rows]) for n_out consecutive rows

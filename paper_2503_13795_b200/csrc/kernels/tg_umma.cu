@@ -990,6 +990,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
     float acc[kCols];
 #pragma unroll
     for (int j = 0; j < kCols; ++j) acc[j] = 0.f;
+    // fused bias row sums of a K-major A (weight-gradient products, g.rowsum):
+    // thread ct holds A rows ct / 8 and ct / 8 + 64 of every k-tile (one
+    // 16-byte chunk of each: row r is float4s [8r, 8r + 8) whatever the
+    // swizzle); the N-tile-0 CTAs of each split sum them in k order
+    const bool rs_on = g.rowsum && !a_mn && blockIdx.y == 0;
+    float rs[static_cast<int>(kTTile / 16) / kPConv] = {};
     auto drain = [&](std::uint32_t grp) {
       const int buf = grp & 1;
       mbar_wait2(tfull(buf), (grp >> 1) & 1);
@@ -1020,9 +1026,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
       for (int op = 0; op < nop; ++op) {
         float4* hi = reinterpret_cast<float4*>(base + op * 2 * kTTile);
         float4* lo = reinterpret_cast<float4*>(base + op * 2 * kTTile + kTTile);
-#pragma unroll 4
-        for (int i = ct; i < static_cast<int>(kTTile / 16); i += kPConv) {
+#pragma unroll
+        for (int it = 0; it < static_cast<int>(kTTile / 16) / kPConv; ++it) {
+          const int i = ct + it * kPConv;
           const float4 x = hi[i];
+          if (op == 0 && rs_on) rs[it] += (x.x + x.y) + (x.z + x.w);   // A row (i / 8), four consecutive k
           float4 h, l;
           h.x = tf32_rna(x.x); l.x = tf32_rna(x.x - h.x);
           h.y = tf32_rna(x.y); l.y = tf32_rna(x.y - h.y);
@@ -1039,6 +1047,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
       if (t % kPFlush == 0 && t / kPFlush >= 2) drain(t / kPFlush - 2);
     }
     for (std::uint32_t q = NG >= 2 ? NG - 2 : 0; q < NG; ++q) drain(q);
+    if (rs_on) {   // eight threads per row (consecutive lanes): fixed-order tree, one store per row
+#pragma unroll
+      for (int it = 0; it < static_cast<int>(kTTile / 16) / kPConv; ++it) {
+        float v = rs[it];
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        const std::uint32_t m = static_cast<std::uint32_t>(m0 + (ct + it * kPConv) / 8);
+        if ((ct & 7) == 0 && m < g.M) g.rowsum[std::size_t(blockIdx.z) * g.M + m] = v;
+      }
+    }
     // ===== epilogue: this CTA's 128 rows x 256 columns through shared memory =====
     constexpr int kLd = kPN + 4;
     float* tile = reinterpret_cast<float*>(smem);
@@ -1314,6 +1333,19 @@ cudaError_t launch_shortk(const GemmArgs<float>& g, cudaStream_t st) {
   const dim3 grid(static_cast<unsigned>((g.N + 4 * (256 / MG) - 1) / (4 * (256 / MG))), (g.M + MG * kSkRows - 1) / (MG * kSkRows));
   k_gemm_shortk<AK, MG><<<grid, 256, smem, st>>>(g, kp);
   return cudaGetLastError();
+}
+
+int simt_route(const GemmArgs<float>& g);
+// A batched weight-gradient product that runs on the CTA pairs can also leave
+// the row sums of its K-major A (the bias gradient) in g.rowsum: partials
+// [z][M] for the caller's split reduce.
+bool umma_rowsum_fusable(const GemmArgs<float>& g) {
+  static const bool use_tma = !(std::getenv("TG_UMMA_TMA") && std::getenv("TG_UMMA_TMA")[0] == '0');
+  if (!use_tma || g.epi != kEpiSplitK || !g.a_kmaj || !use_pair(g.M) || g.no_pair || simt_route(g) != 0) return false;
+  if (g.mem) return true;   // batched products always take the TMA maps
+  // unbatched: the pair path runs exactly when both operand maps encode as given
+  CUtensorMap ta, tb;
+  return make_operand_map(&ta, g.A, g.lda, false, g.M, g.K) && make_operand_map(&tb, g.B, g.ldb, g.b_nmaj, g.N, g.K);
 }
 
 // 0: tensor cores; 4: short K (K <= 32); 1: skinny M (M <= 16, K <= 2048)
