@@ -1335,6 +1335,104 @@ cudaError_t launch_shortk(const GemmArgs<float>& g, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Skinny weight gradients on the FP32 pipe: dW = dZ X^T with M <= 16 output
+// rows (a classifier head: cfg5's 10 x 1024 weight over 1M samples) is a
+// 16x-padded tile on the tensor core (k_umma_tma: 1.73 ms for 20 GFLOP) and
+// an HBM stream of X here.  CTA (n-block, split z): 8 warps x 4 rows n of
+// B(k, n) = X[n][k] (K-major: every row is contiguous in k), lane l takes k =
+// kb + l of each 512-wide sub-chunk whose A(m, k) = dZ[m][k] columns the CTA
+// stages in shared memory; per 4 k: 4 coalesced 16-byte row loads, M shared
+// loads, 16 M FMAs (M exact: one instantiation per even row count).  Each lane sums its k in order, the warp folds lanes in a fixed tree,
+// and the split partials [z][M][N] take the split-K reduce (deterministic).
+constexpr int kSwRows = 16, kSwK = 512, kSwWarps = 8, kSwN = 4;
+template <int MR>
+__global__ void __launch_bounds__(256, 2) k_dw_skinny(GemmArgs<float> g) {
+  __shared__ __align__(16) float As[MR][kSwK];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const std::uint32_t z = blockIdx.y;
+  const std::uint32_t k_begin = min(g.K, z * g.k_chunk);
+  const std::uint32_t k_end = min(g.K, k_begin + g.k_chunk);
+  const std::uint32_t n0 = (blockIdx.x * kSwWarps + warp) * kSwN;
+  float acc[kSwN][MR];
+#pragma unroll
+  for (int j = 0; j < kSwN; ++j)
+#pragma unroll
+    for (int m = 0; m < MR; ++m) acc[j][m] = 0.f;
+  for (std::uint32_t kb = k_begin; kb < k_end; kb += kSwK) {
+    const std::uint32_t kn = min(static_cast<std::uint32_t>(kSwK), k_end - kb);
+    __syncthreads();
+    for (std::uint32_t i = threadIdx.x; i < MR * kSwK; i += 256) {
+      const std::uint32_t m = i / kSwK, k = i % kSwK;
+      As[m][k] = (m < g.M && k < kn) ? g.A[std::size_t(m) * g.lda + kb + k] : 0.f;
+    }
+    __syncthreads();
+    const float* rows[kSwN];
+#pragma unroll
+    for (int j = 0; j < kSwN; ++j) rows[j] = g.B + std::size_t(min(n0 + j, g.N - 1)) * g.ldb + kb;
+    // four consecutive k per lane (16-byte loads: 512 bytes per row per warp in flight)
+#pragma unroll 4
+    for (std::uint32_t k = 4 * lane; k < kn; k += 128) {
+      float4 b[kSwN];
+      if (k + 3 < kn) {
+#pragma unroll
+        for (int j = 0; j < kSwN; ++j) b[j] = __ldg(reinterpret_cast<const float4*>(rows[j] + k));
+      } else {
+#pragma unroll
+        for (int j = 0; j < kSwN; ++j)
+          b[j] = make_float4(rows[j][k], k + 1 < kn ? rows[j][k + 1] : 0.f, k + 2 < kn ? rows[j][k + 2] : 0.f, 0.f);
+      }
+#pragma unroll
+      for (int m = 0; m < MR; ++m) {
+        const float4 a = *reinterpret_cast<const float4*>(&As[m][k]);
+#pragma unroll
+        for (int j = 0; j < kSwN; ++j) {
+          float t = acc[j][m];
+          t = fmaf(a.x, b[j].x, t);
+          t = fmaf(a.y, b[j].y, t);
+          t = fmaf(a.z, b[j].z, t);
+          t = fmaf(a.w, b[j].w, t);
+          acc[j][m] = t;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kSwN; ++j)
+#pragma unroll
+    for (int m = 0; m < MR; ++m) {
+      float v = acc[j][m];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      acc[j][m] = v;
+    }
+  if (lane == 0)
+#pragma unroll
+    for (int j = 0; j < kSwN; ++j)
+#pragma unroll
+      for (int m = 0; m < MR; ++m)
+        if (m < static_cast<int>(g.M) && n0 + j < g.N) g.C[(std::size_t(z) * g.M + m) * g.N + n0 + j] = acc[j][m];
+}
+
+cudaError_t launch_dw_skinny(const GemmArgs<float>& g0, std::uint32_t splits, cudaStream_t st) {
+  // split ranges on sub-chunk boundaries (16-byte aligned loads); trailing splits may be empty (zero partials)
+  GemmArgs<float> g = g0;
+  g.k_chunk = (g.K + splits - 1) / splits;
+  g.k_chunk = (g.k_chunk + kSwK - 1) / kSwK * kSwK;
+  const dim3 grid((g.N + kSwWarps * kSwN - 1) / (kSwWarps * kSwN), splits);
+  switch ((g.M + 1) / 2) {
+    case 1: k_dw_skinny<2><<<grid, 256, 0, st>>>(g); break;
+    case 2: k_dw_skinny<4><<<grid, 256, 0, st>>>(g); break;
+    case 3: k_dw_skinny<6><<<grid, 256, 0, st>>>(g); break;
+    case 4: k_dw_skinny<8><<<grid, 256, 0, st>>>(g); break;
+    case 5: k_dw_skinny<10><<<grid, 256, 0, st>>>(g); break;
+    case 6: k_dw_skinny<12><<<grid, 256, 0, st>>>(g); break;
+    case 7: k_dw_skinny<14><<<grid, 256, 0, st>>>(g); break;
+    default: k_dw_skinny<16><<<grid, 256, 0, st>>>(g); break;
+  }
+  return cudaGetLastError();
+}
+
 int simt_route(const GemmArgs<float>& g);
 // A batched weight-gradient product that runs on the CTA pairs can also leave
 // the row sums of its K-major A (the bias gradient) in g.rowsum: partials
@@ -1348,11 +1446,15 @@ bool umma_rowsum_fusable(const GemmArgs<float>& g) {
   return make_operand_map(&ta, g.A, g.lda, false, g.M, g.K) && make_operand_map(&tb, g.B, g.ldb, g.b_nmaj, g.N, g.K);
 }
 
-// 0: tensor cores; 4: short K (K <= 32); 1: skinny M (M <= 16, K <= 2048)
+// 0: tensor cores; 4: short K (K <= 32); 1: skinny M (M <= 16, K <= 2048);
+// 2: skinny weight gradient (M <= 16 split-K over >= 65,536 samples)
 int simt_route(const GemmArgs<float>& g) {
   static const bool on = !(std::getenv("TG_SHORTK") && std::getenv("TG_SHORTK")[0] == '0');
   static const bool skinny = !(std::getenv("TG_SKINNY") && std::getenv("TG_SKINNY")[0] == '0');
   auto al = [](const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15) == 0; };
+  if (skinny && !g.mem && !g.no_pair && g.epi == kEpiSplitK && g.a_kmaj && !g.b_nmaj && g.M <= kSwRows &&
+      g.K >= 65536 && g.ldb % 4 == 0 && al(g.B))
+    return 2;
   if (!on || g.mem || g.no_pair || g.epi != kEpiBiasAct || !g.b_nmaj || g.N % 4 || g.ldb % 4 || g.ldc % 4 || !al(g.B) ||
       !al(g.C) || (g.C2 && !al(g.C2)))
     return 0;
@@ -1364,6 +1466,7 @@ int simt_route(const GemmArgs<float>& g) {
 cudaError_t launch_gemm_umma(const GemmArgs<float>& g0, std::uint32_t splits, cudaStream_t st) {
   if (g0.M == 0 || g0.N == 0) return cudaSuccess;
   switch (simt_route(g0)) {
+    case 2: return launch_dw_skinny(g0, splits, st);
     case 4: return g0.a_kmaj ? launch_shortk<true, 4>(g0, st) : launch_shortk<false, 4>(g0, st);
     case 1: return g0.a_kmaj ? launch_shortk<true, 1>(g0, st) : launch_shortk<false, 1>(g0, st);
     default: break;
