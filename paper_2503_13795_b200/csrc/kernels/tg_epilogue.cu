@@ -162,7 +162,14 @@ __global__ void __launch_bounds__(kBlock) k_reduce_epilogue(ReduceArgs<T> r, Uni
   // ---- fixed-order reduction of the per-CTA partials ----
   const std::uint32_t warp = (blockIdx.x * kBlock + threadIdx.x) >> 5;
   const std::uint32_t lane = threadIdx.x & 31;
-  if (warp < r.n_dest) {
+  if (r.n_rows == 1) {
+    // one partial row (the staged tier's chunk accumulator): a grid-stride
+    // copy, not a warp per destination (cfg5: 1.86M destinations had made
+    // this launch 232,962 CTAs and 0.56 ms)
+    for (std::size_t d = std::size_t(blockIdx.x) * kBlock + threadIdx.x; d < r.n_dest;
+         d += std::size_t(gridDim.x) * kBlock)
+      a.UG[r.dest_uv[d]] = r.partial[d];
+  } else if (warp < r.n_dest) {
     const T* row = r.partial + std::size_t(warp) * r.n_rows;
     T tot = 0;
     for (std::uint32_t c = lane; c < r.n_rows; c += 32) tot += row[c];
@@ -247,7 +254,8 @@ template <class T>
 cudaError_t launch_reduce_epilogue(const ReduceArgs<T>& r, const UniformArgs<T>& a, cudaStream_t st,
                                    std::uint64_t& launches) {
   const unsigned warps_per_block = kBlock / 32;
-  const unsigned grid = r.n_dest ? (r.n_dest + warps_per_block - 1) / warps_per_block : 1;
+  unsigned grid = r.n_dest ? (r.n_dest + warps_per_block - 1) / warps_per_block : 1;
+  if (r.n_rows == 1) grid = std::max(1u, std::min<unsigned>(1184u, (r.n_dest + kBlock - 1) / kBlock));
   UniformArgs<T> b = a;
   b.copy = a.n_params <= kGridCopy;
   b.smem = a.n_uv <= kSmemUV;
