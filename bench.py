@@ -419,6 +419,12 @@ def main():
         dip = measure_device_pipeline(args, cfg, tg, prog, X, K, L, b, gb, first, rank, world, stream, dev, cap, run_step)
     prog.check_device_error()
 
+    # ---- sequential-accumulation memory mode: the same step with a bounded workspace ----
+    mem = None
+    if prog.info["storage"] == 3 and not args.no_e2e:
+        mem = measure_bounded_memory(prog, cfg, X, K, P, L, G, b, stream, world)
+    prog.check_device_error()
+
     # ---- roofline of the dominant kernel ----
     pk = peaks()
     info = prog.info
@@ -480,6 +486,7 @@ def main():
         "gpu_launches": launches_per_step * args.steps,
         "e2e": e2e,
         "device_input_pipeline": dip,
+        "memory": mem,
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -575,6 +582,40 @@ def measure_e2e(args, cfg, prog, x, k, b, gb, P, L, stream, world, dev, tdt, cap
             "api": ("tg_pipeline_step (pinned host inputs in, per-sample losses out, 4 steps in flight)"
                     if world == 1 and not hbm_bound else
                     "copies + tg_forward_backward (+ tg_allreduce_gd_step over NCCL at N > 1)")}
+
+
+def measure_bounded_memory(prog, cfg, X, K, P, L, G, b, stream, world, budget=4 << 30, steps=3):
+    """The staged tier with its rows bounded to `budget` bytes per chunk
+    (tg_set_memory_budget): workspace and step time beside the default
+    one-chunk run — peak device memory independent of b."""
+    import torch
+    full = prog.workspace_size(b)
+    full_chunk = prog.chunk_samples(b)
+    prog.set_memory_budget(budget)
+    try:
+        ws = prog.workspace_size(b)
+        chunk = prog.chunk_samples(b)
+        W2 = torch.empty(max(ws, 1), dtype=torch.uint8, device=P.device)
+        P2 = P.clone()
+        G2 = torch.empty_like(G)
+        for _ in range(2):
+            prog.train_step(X, K, b, P2, L, G2, cfg["gamma"], W2, stream)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            prog.train_step(X, K, b, P2, L, G2, cfg["gamma"], W2, stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        del W2, P2, G2
+    finally:
+        prog.set_memory_budget(0)
+    return {"default": {"workspace_gb": full / 1e9, "chunk_samples": full_chunk},
+            "bounded": {"budget_gb": budget / 2**30, "workspace_gb": ws / 1e9, "chunk_samples": chunk,
+                        "chunks": -(-b // chunk), "ms_per_step": ms, "value": b / (ms * 1e-3),
+                        "note": "same step, rows streamed chunk by chunk into one grad_sum (tg_set_memory_budget); "
+                                "L2 not flushed between these steps"}}
 
 
 def measure_device_pipeline(args, cfg, tg, prog, X, K, L, b, gb, first, rank, world, stream, dev, cap, run_step):
