@@ -217,6 +217,7 @@ typedef struct tg_program_info {
   tg_dtype dtype;
   uint32_t n_attn_heads;     /* softmax attention heads fused from the scalar graph */
   uint32_t n_layer_norms;    /* layer normalisations fused from the scalar graph */
+  uint32_t fused_mlp;        /* 1: the staged tape runs as one embedding-MLP / softmax-CE kernel */
 } tg_program_info;
 
 /* Lowers the tape to the device program (replaces the per-sample DFS of

@@ -64,6 +64,7 @@ class tg_program_info(C.Structure):
         ("n_dense_groups", C.c_uint32), ("n_fwd_instr", C.c_uint32), ("n_bwd_instr", C.c_uint32),
         ("n_edges", C.c_uint64), ("tile_samples", C.c_uint32), ("smem_bytes", C.c_uint32),
         ("storage", C.c_uint32), ("dtype", C.c_int), ("n_attn_heads", C.c_uint32), ("n_layer_norms", C.c_uint32),
+        ("fused_mlp", C.c_uint32),
     ]
 
 

@@ -189,6 +189,13 @@ struct tg_program {
     std::vector<std::uint32_t> zero_x;   // assign-flagged x rows zeroed first (mixed flags)
     std::uint32_t* d_zero_x = nullptr;
   };
+  // embedding-MLP / softmax-CE tape run as one kernel (fused_mlp_plan, kernels/tg_fused.cu)
+  struct FusedMlp {
+    bool on = false;
+    tgk::FusedMlpArgs args{};            // dims and parameter offsets (pointers set per call)
+    std::vector<std::uint32_t> dmap;     // q -> destination
+    std::uint32_t* d_dmap = nullptr;
+  } fmlp;
   bool staged = false;
   std::vector<Stage> sfwd, sbwd;
   std::vector<DensePlan> dplan;
@@ -506,6 +513,142 @@ void level_schedule(tg_program& pr, const std::vector<char>& gemm_dense) {
     if (gather_target[r] && !zero[r]) P.zero_rows.push_back(r);
 }
 
+// Recognises the embedding-MLP / softmax-CE composition (
+// tg_models.hpp char_mlp: gathers -> linear(act) -> linear -> softmax_ce) in
+// the compiled program, exactly: C x E gathered inputs of one V x E parameter
+// table, two dense layers in a chain (the first with a fused activation whose
+// derivative reads its output), and the CE nodes StopGradMax, O Sub, O Exp,
+// AddVarying, Log, Sub(log, gather of the shifted logits by the target
+// column) as the root.  Anything else keeps the staged chain.
+bool fused_mlp_plan(const tgc::Program& P, tg_program::FusedMlp& fm, std::string& why) {
+  using tgc::kNone;
+  auto no = [&](const char* w) { why = w; return false; };
+  if (P.dtype != TG_F32) return no("fp64");
+  if (P.dense.size() != 2 || !P.attn.empty() || !P.lnorm.empty() || !P.ufwd.empty() || P.root_row == kNone ||
+      P.n_inputs != 0 || !P.ugather.size())
+    return no("not two dense layers over gathers with a per-sample root");
+  auto slot = [&](std::uint32_t op, std::uint32_t& r) {
+    r = op & tgc::kIndexMask;
+    return (op >> tgc::kModeShift) == tgc::kSlot;
+  };
+  int i0 = -1, i1 = -1;
+  for (int a = 0; a < 2 && i1 < 0; ++a) {
+    const tgc::Dense& A = P.dense[a];
+    const tgc::Dense& B = P.dense[1 - a];
+    if (!A.act_op || A.act_row == kNone || B.act_op || B.n_in != A.n_out) continue;
+    bool chain = true;
+    for (std::uint32_t k = 0; k < B.n_in && chain; ++k) {
+      std::uint32_t r;
+      chain = slot(P.opnd[B.x_opnd + k], r) && r == A.act_row + k;
+    }
+    if (chain) { i0 = a; i1 = 1 - a; }
+  }
+  if (i0 < 0) return no("dense layers are not a chain");
+  const tgc::Dense& D0 = P.dense[i0];
+  const tgc::Dense& D1 = P.dense[i1];
+  {
+    using tg::OpKind;
+    const std::uint32_t ao = D0.act_op;
+    if (ao != std::uint32_t(OpKind::Relu) && ao != std::uint32_t(OpKind::Tanh) && ao != std::uint32_t(OpKind::Exp) &&
+        ao != std::uint32_t(OpKind::Sigmoid))
+      return no("activation derivative needs z");
+  }
+  const std::uint32_t NI = D0.n_in, H = D0.n_out, O = D1.n_out;
+  // rows written by gather loads
+  std::vector<int> gat(P.n_rows, -1);
+  std::uint32_t n_node = 0, n_gather = 0, n_dense = 0;
+  for (const tgc::Instr& in : P.fwd) {
+    if (in.kind == tgc::kGatherLoad) { gat[in.out] = static_cast<int>(in.aux); ++n_gather; }
+    else if (in.kind == tgc::kDense) ++n_dense;
+    else if (in.kind == tgc::kNode) ++n_node;
+    else return no("other instruction kinds");
+  }
+  if (n_gather != NI || n_dense != 2 || n_node != 2 * O + 4) return no("extra instructions");
+  // gathered inputs: x[c E + e] = T[idx[col_c]][e], T at uv_E with row stride E
+  std::uint32_t rows0, E = 0, V = 0, uvE = 0;
+  if (!slot(P.opnd[D0.x_opnd], rows0) || gat[rows0] < 0) return no("first layer input is not gathered");
+  {
+    const tgc::GatherTable& g0 = P.ugather[gat[rows0]];
+    V = g0.n_rows;
+    uvE = P.cand[g0.cand_off];
+    if (V < 2) return no("table of one row");
+    E = P.cand[g0.cand_off + 1] - uvE;
+  }
+  if (E == 0 || NI % E || NI / E > 8) return no("gather layout");
+  const std::uint32_t C = NI / E;
+  tgk::FusedMlpArgs& a = fm.args;
+  a = tgk::FusedMlpArgs{};
+  for (std::uint32_t k = 0; k < NI; ++k) {
+    std::uint32_t r;
+    if (!slot(P.opnd[D0.x_opnd + k], r) || gat[r] < 0) return no("first layer input is not gathered");
+    const tgc::GatherTable& g = P.ugather[gat[r]];
+    const std::uint32_t c = k / E, e = k % E;
+    if (g.n_rows != V) return no("gather tables differ in size");
+    if (e == 0) a.ctx_col[c] = g.col;
+    else if (g.col != a.ctx_col[c]) return no("one context over several index columns");
+    for (std::uint32_t v = 0; v < V; ++v)
+      if (P.cand[g.cand_off + v] != uvE + v * E + e) return no("gather candidates are not one table");
+  }
+  // the CE nodes, from the root down
+  std::vector<int> ins(P.n_rows, -1);
+  for (std::size_t i = 0; i < P.fwd.size(); ++i)
+    if (P.fwd[i].kind == tgc::kNode) ins[P.fwd[i].out] = static_cast<int>(i);
+  using tg::OpKind;
+  auto node = [&](std::uint32_t row, OpKind op, std::uint32_t nops) -> const tgc::Instr* {
+    if (row >= P.n_rows || ins[row] < 0) return nullptr;
+    const tgc::Instr& in = P.fwd[ins[row]];
+    return (in.op == static_cast<std::uint8_t>(op) && in.nops == nops) ? &in : nullptr;
+  };
+  const tgc::Instr* root = node(P.root_row, OpKind::Sub, 2);
+  if (!root) return no("root is not a subtraction");
+  std::uint32_t lrow, trow, mrow = kNone;
+  if (!slot(P.opnd[root->opnd], lrow)) return no("CE log operand");
+  const std::uint32_t zt = P.opnd[root->opnd + 1];
+  if ((zt >> tgc::kModeShift) != tgc::kSGather) return no("CE target is not a gather");
+  const tgc::GatherTable& tg = P.sgather[zt & tgc::kIndexMask];
+  if (tg.n_rows != O) return no("CE target table size");
+  const tgc::Instr* lg = node(lrow, OpKind::Log, 1);
+  if (!lg || !slot(P.opnd[lg->opnd], trow)) return no("CE log");
+  const tgc::Instr* tot = node(trow, OpKind::AddVarying, O);
+  if (!tot) return no("CE sum");
+  for (std::uint32_t j = 0; j < O; ++j) {
+    std::uint32_t er, sr, zr, mr;
+    const tgc::Instr* ex = slot(P.opnd[tot->opnd + j], er) ? node(er, OpKind::Exp, 1) : nullptr;
+    const tgc::Instr* sb = ex && slot(P.opnd[ex->opnd], sr) ? node(sr, OpKind::Sub, 2) : nullptr;
+    if (!sb || !slot(P.opnd[sb->opnd], zr) || zr != D1.out_row + j || !slot(P.opnd[sb->opnd + 1], mr))
+      return no("CE shifted exponentials");
+    if (P.cand[tg.cand_off + j] != sr) return no("CE target candidates");
+    if (mrow == kNone) mrow = mr;
+    else if (mr != mrow) return no("CE shift");
+  }
+  const tgc::Instr* mx = node(mrow, OpKind::StopGradMax, O);
+  if (!mx) return no("CE shift is not a stop-gradient max");
+  for (std::uint32_t j = 0; j < O; ++j) {
+    std::uint32_t zr;
+    if (!slot(P.opnd[mx->opnd + j], zr) || zr != D1.out_row + j) return no("CE max operands");
+  }
+  a.C = C; a.E = E; a.V = V; a.H = H; a.O = O; a.act = D0.act_op; a.tgt_col = tg.col;
+  a.uv_E = uvE; a.uv_W1 = D0.w_uv; a.uv_b1 = D0.b_uv; a.uv_W2 = D1.w_uv; a.uv_b2 = D1.b_uv;
+  a.nq = H * NI + H + O * H + O + V * E;
+  // destinations, and no destination the kernel does not produce
+  std::vector<std::uint32_t> inv(P.n_uv, kNone);
+  for (std::uint32_t d = 0; d < P.dest_uv.size(); ++d) inv[P.dest_uv[d]] = d;
+  fm.dmap.assign(a.nq, kNone);
+  std::uint32_t covered = 0;
+  auto map = [&](std::uint32_t q, std::uint32_t u) {
+    if (u < P.n_params && inv[u] != kNone) { fm.dmap[q] = inv[u]; ++covered; }
+  };
+  std::uint32_t q = 0;
+  for (std::uint32_t i = 0; i < H * NI; ++i) map(q++, a.uv_W1 + i);
+  for (std::uint32_t i = 0; i < H; ++i, ++q) if (a.uv_b1 != kNone) map(q, a.uv_b1 + i);
+  for (std::uint32_t i = 0; i < O * H; ++i) map(q++, a.uv_W2 + i);
+  for (std::uint32_t i = 0; i < O; ++i, ++q) if (a.uv_b2 != kNone) map(q, a.uv_b2 + i);
+  for (std::uint32_t i = 0; i < V * E; ++i) map(q++, uvE + i);
+  if (covered != P.dest_uv.size()) return no("gradient destinations outside the fused layers");
+  if (tgk::fused_mlp_smem(a) > 227 * 1024) return no("does not fit one SM's shared memory");
+  return true;
+}
+
 void build_staged_plan(tg_program& pr) {
   const tgc::Program& P = pr.P;
   const char* env = std::getenv("TG_STAGED");
@@ -533,6 +676,11 @@ void build_staged_plan(tg_program& pr) {
   }
   if (const char* u = std::getenv("TG_UMMA")) pr.umma = u[0] != '0';
   if (!pr.staged || P.root_row == tgc::kNone) { pr.staged = false; return; }
+  {
+    const char* fe = std::getenv("TG_FUSED_MLP");   // 0: keep the staged chain (A/B runs)
+    std::string why;
+    pr.fmlp.on = !(fe && fe[0] == '0') && fused_mlp_plan(P, pr.fmlp, why);
+  }
   {
     const char* lv = std::getenv("TG_STAGED_LEVELS");
     pr.levels = !(lv && lv[0] == '0');
@@ -1076,6 +1224,8 @@ Layout layout(const tg_program& pr, std::size_t batch) {
         const std::uint32_t nm = static_cast<std::uint32_t>(B.members.size());
         sk = std::max<std::size_t>(sk, std::size_t(nm) * batch_splits(D, nm, cb) * (std::size_t(D.n_out) * D.n_in + D.n_out));
       }
+    if (pr.fmlp.on)   // the fused kernel's per-CTA gradient partials
+      sk = std::max<std::size_t>(sk, std::size_t(tgk::fused_mlp_grid(batch, pr.nsm)) * pr.fmlp.args.nq);
     L.sk = off; off = align_up(off + std::max<std::size_t>(1, sk) * t);
     L.sp = off; off = align_up(off + std::max<std::size_t>(1, std::size_t(pr.sc_groups.size()) * pr.sc_chunks * pr.sc_rmax) * t);
     L.total = off;
@@ -1132,6 +1282,7 @@ tg_status upload(tg_program& pr) {
   TG_TRY(upload_vec(pr, P.ugather, &pr.d_ug));
   TG_TRY(upload_vec(pr, P.sgather, &pr.d_sg));
   TG_TRY(upload_vec(pr, P.cand, &pr.d_cand));
+  if (pr.fmlp.on) TG_TRY(upload_vec(pr, pr.fmlp.dmap, &pr.fmlp.d_dmap));
   TG_TRY(upload_vec(pr, P.term_off, &pr.d_termoff));
   TG_TRY(upload_vec(pr, P.terms, &pr.d_terms));
   TG_TRY(upload_vec(pr, P.dest_uv, &pr.d_destuv));
@@ -1359,7 +1510,20 @@ tg_status run_staged(tg_program& pr, const void* inputs, const std::int32_t* idx
     ld = cb;
     return Vb + std::size_t(dp.xrow0) * cb;
   };
-  for (std::size_t s0 = 0; s0 < batch; s0 += cb) {
+  if constexpr (std::is_same_v<T, float>) {
+    if (pr.fmlp.on) {   // the whole tape in one kernel, no HBM rows
+      tgk::FusedMlpArgs fa = pr.fmlp.args;
+      fa.UV = UV;
+      fa.idx = idx;
+      fa.batch = batch;
+      fa.loss = static_cast<float*>(loss);
+      fa.part = sk;
+      const unsigned grid = tgk::fused_mlp_grid(batch, pr.nsm);
+      TG_CUDA_TRY(tgk::launch_fused_mlp(fa, grid, pr.fmlp.d_dmap, acc, st));
+      pr.launches += 2;
+    }
+  }
+  for (std::size_t s0 = 0; s0 < batch && !pr.fmlp.on; s0 += cb) {
     const std::size_t n = std::min(cb, batch - s0);
     ra.s0 = s0;
     ra.n = n;
@@ -2234,6 +2398,7 @@ tg_status tg_program_info_get(tg_program_t p, tg_program_info* info) {
     i.dtype = P.dtype;
     i.n_attn_heads = static_cast<uint32_t>(P.attn.size());
     i.n_layer_norms = static_cast<uint32_t>(P.lnorm.size());
+    i.fused_mlp = p->fmlp.on ? 1u : 0u;
     *info = i;
     return TG_OK;
   });

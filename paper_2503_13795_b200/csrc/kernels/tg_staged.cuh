@@ -158,4 +158,25 @@ cudaError_t launch_contract(const std::uint32_t* dests, std::uint32_t n_dests, c
                             const T* G, const T* V, const std::int32_t* idx, std::size_t batch, std::size_t s0, std::size_t n,
                             std::size_t ld, T* acc, cudaStream_t st);
 
+// Embedding-MLP / softmax-CE tape as one kernel (tg_fused.cu): C contexts of an
+// E-wide table of V rows -> H units (act) -> O logits -> CE against the target
+// column.  Parameter UV offsets; gradients as partials [cta][q] in q order
+// [W1 (H x C E) | b1 (H) | W2 (O x H) | b2 (O) | E (V x E)], reduced into
+// acc[dmap[q]] (dmap[q] == kNone: no destination).
+struct FusedMlpArgs {
+  const float* UV;
+  const std::int32_t* idx;   // [n_index_inputs][batch]
+  std::size_t batch;
+  std::uint32_t C, E, V, H, O, act;
+  std::uint32_t ctx_col[8], tgt_col;
+  std::uint32_t uv_E, uv_W1, uv_b1, uv_W2, uv_b2;   // b: kNone when absent
+  std::uint32_t nq;
+  float* loss;
+  float* part;               // [grid][nq]
+};
+std::size_t fused_mlp_smem(const FusedMlpArgs& a);
+unsigned fused_mlp_grid(std::size_t batch, int nsm);
+cudaError_t launch_fused_mlp(const FusedMlpArgs& a, unsigned grid, const std::uint32_t* dmap, float* acc,
+                             cudaStream_t st);
+
 }  // namespace tgk

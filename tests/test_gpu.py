@@ -669,3 +669,26 @@ def test_reference_recorded_token_models_on_gpu(name, dims, b):
                        threads=os.cpu_count() or 8)
     assert close_rel(L, r["loss"], 1e-5, 1e-6), rel(L, r["loss"])
     assert rel(G, r["grad_sum"]) <= 1e-5
+
+
+@pytest.mark.parametrize("dims,b", [(None, 4096), (None, 1000), ([27, 5, 6, 96], 777), ([40, 2, 16, 192], 2048)])
+def test_fused_embedding_mlp_ce_vs_oracle_and_staged_chain(dims, b):
+    """The embedding-MLP / softmax-CE tape recognised and run as one kernel
+    (tg_fused.cu) against the oracle (per-sample reference loop) at the fp32
+    bar, and against the staged chain it replaces (TG_FUSED_MLP=0); ragged
+    batches exercise the padded last tile."""
+    desc = tg.build_model("char_mlp", dims, "f32", seed=3).describe()
+    x, k = tg.synth_batch("char_mlp", dims, "f32", seed=19, batch=b, n_inputs=desc.n_inputs, n_index=desc.n_index_inputs)
+    os.environ["TG_STAGED"] = "1"
+    prog = tg.Program(desc)
+    os.environ["TG_FUSED_MLP"] = "0"
+    chain = tg.Program(desc)
+    os.environ.pop("TG_FUSED_MLP")
+    os.environ.pop("TG_STAGED")
+    assert prog.info["fused_mlp"] == 1 and chain.info["fused_mlp"] == 0
+    L, _, G = run(prog, desc, x, k, desc.param_values(), b, want_igrad=False)
+    L2, _, G2 = run(chain, desc, x, k, desc.param_values(), b, want_igrad=False)
+    r = oracle.run(desc, x.astype(np.float64), k, desc.param_values(), threads=os.cpu_count() or 8)
+    assert close_rel(L, r["loss"], TOL["f32"], 1e-6), rel(L, r["loss"])
+    assert rel(G, r["grad_sum"]) <= TOL["f32"], rel(G, r["grad_sum"])
+    assert rel(G, G2) <= TOL["f32"] and close_rel(L, L2, TOL["f32"], 1e-6)
