@@ -677,9 +677,11 @@ void build_staged_plan(tg_program& pr) {
   if (const char* u = std::getenv("TG_UMMA")) pr.umma = u[0] != '0';
   if (!pr.staged || P.root_row == tgc::kNone) { pr.staged = false; return; }
   {
-    const char* fe = std::getenv("TG_FUSED_MLP");   // 0: keep the staged chain (A/B runs)
+    // opt-in (TG_FUSED_MLP=1): the one-kernel form is correct but measured slower
+    // than the staged chain on cfg3 (1.90 vs 1.43 ms, profiles/r07/README.md)
+    const char* fe = std::getenv("TG_FUSED_MLP");
     std::string why;
-    pr.fmlp.on = !(fe && fe[0] == '0') && fused_mlp_plan(P, pr.fmlp, why);
+    pr.fmlp.on = fe && fe[0] == '1' && fused_mlp_plan(P, pr.fmlp, why);
   }
   {
     const char* lv = std::getenv("TG_STAGED_LEVELS");

@@ -4,7 +4,7 @@
 //   loss = log(sum_j exp(z_j - m)) - (z_t - m),  m = stop-gradient max z
 // recognised in the recorded scalar graph by tg_abi.cpp (fused_mlp_plan).
 //
-// The staged chain ran this as 31 launches over HBM rows (1.44 ms for
+// The staged chain runs this as 31 launches over HBM rows (1.43 ms for
 // b = 262,144: every 200-wide activation written and re-read).  Here a CTA
 // keeps the 47.6 KB of weights and the same-sized gradient accumulators in
 // shared memory and walks tiles of kS samples: gather, two products, the CE
@@ -14,6 +14,10 @@
 // are written once, as partials [cta][q], and reduced over CTAs in a fixed
 // order (k_fused_reduce) into the step's gradient accumulator — the same
 // deterministic contract as the rest of the staged tier.
+// Measured 1.90 ms on cfg3 (r07f: issue 49%, a quarter of the stall samples at
+// barriers between phases whose products leave most threads idle: 27 x 32 and
+// 30 x 32 outputs over K = 200), so it is opt-in (TG_FUSED_MLP=1); warp-level
+// tensor-core tiles for the six products are what it needs to beat the chain.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -27,7 +31,7 @@ namespace {
 
 constexpr int kS = 32;            // samples per tile
 constexpr int kLd = kS + 1;       // activation row stride (bank-conflict free column walks)
-constexpr int kThreads = 256;
+constexpr int kThreads = 512;
 
 // C[m][n] = sum_k a(m, k) b(k, n) over a TM x TN register tile per thread;
 // n is the fast thread index (B reads along n are consecutive, A reads broadcast).
@@ -79,7 +83,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_mlp_ce(FusedMlpArgs a) {
   float* Hh = X + NI * kLd;     // [H][kLd]    hidden activations
   float* Z = Hh + H * kLd;      // [O][kLd]    logits, then their adjoints
   float* D = Z + O * kLd;       // [H][kLd]    hidden pre-activation adjoints
-  int* tok = reinterpret_cast<int*>(D + H * kLd);   // [C + 1][kS]: context tokens, target
+  float* XT = D + H * kLd;      // [kS][NI + 1]  x transposed (weight-gradient products read rows of samples)
+  float* HT = XT + kS * (NI + 1);   // [kS][H + 1]
+  int* tok = reinterpret_cast<int*>(HT + kS * (H + 1));   // [C + 1][kS]: context tokens, target
 
   const std::uint32_t nq = a.nq;
   for (std::uint32_t q = threadIdx.x; q < nq; q += kThreads) {
@@ -107,13 +113,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_mlp_ce(FusedMlpArgs a) {
     __syncthreads();
     for (int i = threadIdx.x; i < NI * kS; i += kThreads) {
       const int q = i / kS, s = i % kS;
-      X[q * kLd + s] = s < ns ? sE[tok[(q / E) * kS + s] * E + q % E] : 0.f;
+      const float v = s < ns ? sE[tok[(q / E) * kS + s] * E + q % E] : 0.f;
+      X[q * kLd + s] = v;
+      XT[s * (NI + 1) + q] = v;
     }
     __syncthreads();
     // ---- h = act(W1 x + b1) ----
     tile_gemm<4, 4>(
         H, kS, NI, [&](int j, int k) { return sW1[j * NI + k]; }, [&](int k, int s) { return X[k * kLd + s]; },
-        [&](int j, int s, float v) { Hh[j * kLd + s] = act_fwd<float>(a.act, v + sb1[j]); });
+        [&](int j, int s, float v) {
+          const float h = act_fwd<float>(a.act, v + sb1[j]);
+          Hh[j * kLd + s] = h;
+          HT[s * (H + 1) + j] = h;
+        });
     __syncthreads();
     // ---- z = W2 h + b2 ----
     tile_gemm<2, 2>(
@@ -142,7 +154,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_mlp_ce(FusedMlpArgs a) {
     __syncthreads();
     // ---- gW2 += dz h^T, gb2 += sum_s dz ----
     tile_gemm<2, 4>(
-        O, H, kS, [&](int c, int s) { return Z[c * kLd + s]; }, [&](int s, int j) { return Hh[j * kLd + s]; },
+        O, H, kS, [&](int c, int s) { return Z[c * kLd + s]; }, [&](int s, int j) { return HT[s * (H + 1) + j]; },
         [&](int c, int j, float v) { gW2[c * H + j] += v; });
     if (threadIdx.x < O) {
       float t = 0.f;
@@ -156,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_mlp_ce(FusedMlpArgs a) {
     __syncthreads();
     // ---- gW1 += dz1 x^T, gb1 += sum_s dz1 ----
     tile_gemm<4, 2>(
-        H, NI, kS, [&](int j, int s) { return D[j * kLd + s]; }, [&](int s, int k) { return X[k * kLd + s]; },
+        H, NI, kS, [&](int j, int s) { return D[j * kLd + s]; }, [&](int s, int k) { return XT[s * (NI + 1) + k]; },
         [&](int j, int k, float v) { gW1[j * NI + k] += v; });
     for (int j = threadIdx.x; j < H; j += kThreads) {
       float t = 0.f;
@@ -197,7 +209,8 @@ __global__ void k_fused_reduce(const float* __restrict__ part, std::uint32_t nq,
 
 std::size_t fused_mlp_smem(const FusedMlpArgs& a) {
   const std::size_t NI = std::size_t(a.C) * a.E;
-  return (2 * std::size_t(a.nq) + (NI + 2 * a.H + a.O) * kLd) * sizeof(float) + (a.C + 1) * kS * sizeof(int);
+  return (2 * std::size_t(a.nq) + (NI + 2 * a.H + a.O) * kLd + kS * (NI + 1 + a.H + 1)) * sizeof(float) +
+         (a.C + 1) * kS * sizeof(int);
 }
 
 unsigned fused_mlp_grid(std::size_t batch, int nsm) {

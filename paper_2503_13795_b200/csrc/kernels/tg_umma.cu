@@ -256,14 +256,6 @@ __device__ __forceinline__ void tma_load_2d(std::uint32_t dst, const CUtensorMap
       "l"(reinterpret_cast<std::uint64_t>(map)), "r"(c0), "r"(c1), "r"(mbar)
       : "memory");
 }
-// L2 prefetch of the same box (no shared memory, no barrier): issued a few
-// k-tiles ahead of the ring so the ring's own loads hit L2 instead of HBM.
-__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
-  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
-                   reinterpret_cast<std::uint64_t>(map)),
-               "r"(c0), "r"(c1)
-               : "memory");
-}
 // SWIZZLE_128B smem descriptor (sm_100 version 1).
 __device__ __forceinline__ std::uint64_t umma_desc_sw128(std::uint32_t saddr, std::uint32_t lbo, std::uint32_t sbo) {
   return static_cast<std::uint64_t>((saddr & 0x3FFFFu) >> 4) | (static_cast<std::uint64_t>(lbo >> 4) << 16) |
@@ -285,14 +277,6 @@ __device__ __forceinline__ void tma_operand(const CUtensorMap* map, bool mn, std
 // (layout type 1; Swizzle<2,5,2>: 32-byte granules XOR row % 4, 4-row atoms of
 // 512 B), written by TMA's SWIZZLE_128B_ATOM_32B mode.  LBO = 4 KB between the
 // 32-wide MN chunks, SBO = 512 B between 4-row K groups.
-__device__ __forceinline__ void tma_prefetch_operand(const CUtensorMap* map, bool mn, int r0, int k0, int off) {
-  if (mn) {
-#pragma unroll
-    for (int c = 0; c < 4; ++c) tma_prefetch_2d(map, r0 + 32 * c, k0 + off);
-  } else {
-    tma_prefetch_2d(map, k0, r0 + off);
-  }
-}
 __device__ __forceinline__ std::uint64_t umma_desc_b32(std::uint32_t saddr, std::uint32_t lbo, std::uint32_t sbo) {
   return static_cast<std::uint64_t>((saddr & 0x3FFFFu) >> 4) | (static_cast<std::uint64_t>(lbo >> 4) << 16) |
          (static_cast<std::uint64_t>(sbo >> 4) << 32) | (1ull << 46) | (1ull << 61);
@@ -836,7 +820,6 @@ __global__ void __launch_bounds__(kTThreads, 1) k_umma_tma_p(GemmArgs<float> g, 
 // double with N = 256; 2 tiles = K 64 keeps the tensor core's biased fp32
 // accumulation at ~7e-7 relative).
 constexpr int kPN = 256;
-constexpr std::uint32_t kL2Ahead = 4;   // k-tiles between an L2 prefetch and the ring load of the same tile
 constexpr int kPFlush = 2;
 constexpr int kPConv = 512;                 // 16 converter / drain warps: 64 accumulator columns per thread
 constexpr int kPThreads = 64 + kPConv;
@@ -954,11 +937,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
     if (lane == 0)
       for (std::uint32_t t = 0; t < T; ++t) {
         const int s = t % kTStages;
-        if (t + kL2Ahead < T) {   // warm L2 for a k-tile the ring will load kL2Ahead tiles from now
-          const int kp = static_cast<int>(k_begin + (t + kL2Ahead) * BK);
-          tma_prefetch_operand(&tmA, a_mn, m0, kp, a_off);
-          tma_prefetch_operand(&tmB, b_mn, nb, kp, b_off);
-        }
         if (t >= kTStages) mbar_wait2(empty(s), ((t / kTStages) - 1) & 1);
         const std::uint32_t base = smem_u32(smem + s * kTStage);
         mbar_expect_tx(full(s), 2 * kTTile);

@@ -674,12 +674,13 @@ def test_reference_recorded_token_models_on_gpu(name, dims, b):
 @pytest.mark.parametrize("dims,b", [(None, 4096), (None, 1000), ([27, 5, 6, 96], 777), ([40, 2, 16, 192], 2048)])
 def test_fused_embedding_mlp_ce_vs_oracle_and_staged_chain(dims, b):
     """The embedding-MLP / softmax-CE tape recognised and run as one kernel
-    (tg_fused.cu) against the oracle (per-sample reference loop) at the fp32
-    bar, and against the staged chain it replaces (TG_FUSED_MLP=0); ragged
+    (tg_fused.cu, opt-in TG_FUSED_MLP=1) against the oracle (per-sample
+    reference loop) at the fp32 bar, and against the staged chain; ragged
     batches exercise the padded last tile."""
     desc = tg.build_model("char_mlp", dims, "f32", seed=3).describe()
     x, k = tg.synth_batch("char_mlp", dims, "f32", seed=19, batch=b, n_inputs=desc.n_inputs, n_index=desc.n_index_inputs)
     os.environ["TG_STAGED"] = "1"
+    os.environ["TG_FUSED_MLP"] = "1"
     prog = tg.Program(desc)
     os.environ["TG_FUSED_MLP"] = "0"
     chain = tg.Program(desc)
