@@ -682,6 +682,7 @@ void build_staged_plan(tg_program& pr) {
     const char* fe = std::getenv("TG_FUSED_MLP");
     std::string why;
     pr.fmlp.on = fe && fe[0] == '1' && fused_mlp_plan(P, pr.fmlp, why);
+    if (fe && fe[0] == '1' && !pr.fmlp.on && std::getenv("TG_FUSED_MLP_WHY")) std::fprintf(stderr, "fused_mlp: %s\n", why.c_str());
   }
   {
     const char* lv = std::getenv("TG_STAGED_LEVELS");

@@ -332,3 +332,39 @@ def test_nccl_binding_and_argument_checks():
     assert L.tg_nccl_get_unique_id(None) == 1
     assert L.tg_nccl_comm_destroy(None) == 0
     assert _lib.lib.tg_status_name(10).decode() == "TG_NCCL"
+
+
+def test_fused_mlp_recogniser_accepts_the_composition_only(monkeypatch):
+    """tg_fused.cu's pattern (gathers -> dense(act) -> dense -> softmax CE) is
+    recognised exactly in the compiled graph (opt-in TG_FUSED_MLP=1): char-MLP
+    variants are, the other workloads and a CE with an extra node are not."""
+    monkeypatch.setenv("TG_FUSED_MLP", "1")
+    monkeypatch.setenv("TG_STAGED", "1")
+    for dims in (None, [27, 5, 6, 96], [40, 2, 16, 192]):
+        d = tg.build_model("char_mlp", dims, "f32", seed=0).describe()
+        assert tg.Program(d).info["fused_mlp"] == 1, dims
+    assert tg.Program(tg.build_model("char_mlp", [40, 2, 16, 256], "f32", seed=0).describe()).info["fused_mlp"] == 0  # smem
+    assert tg.Program(tg.build_model("char_mlp", None, "f64", seed=0).describe()).info["fused_mlp"] == 0
+    for name, dims in (("wide_mlp", [24, 16, 12, 10]), ("gpt", [11, 6, 8, 2, 2, 16])):
+        assert tg.Program(tg.build_model(name, dims, "f32", seed=0).describe()).info["fused_mlp"] == 0
+    # the composition as tg_models.hpp records it (all inner products, then the
+    # activations); with one extra node on the loss (x 1.0) it is not the pattern
+    t = tg.Tape(4096, "f32")
+    V, C, E, H = 5, 2, 3, 8
+    emb = [t.param(0.01 * i) for i in range(V * E)]
+    x = [t.gather(emb[0], E, V, c, e, 1) for c in range(C) for e in range(E)]
+    w1 = [[t.param(0.02 * (j + k)) for k in range(C * E)] for j in range(H)]
+    b1 = [t.param(0.0) for _ in range(H)]
+    h = [t.unary(OpKind.Tanh, zj) for zj in [t.inner_product_with_bias(x, w1[j], b1[j]) for j in range(H)]]
+    w2 = [[t.param(0.03 * (c - j)) for j in range(H)] for c in range(V)]
+    b2 = [t.param(0.0) for _ in range(V)]
+    z = [t.inner_product_with_bias(h, w2[c], b2[c]) for c in range(V)]
+    m = t.op(OpKind.StopGradMax, z)
+    sh = [t.sub(zc, m) for zc in z]
+    lse = t.unary(OpKind.Log, t.reduce_sum([t.unary(OpKind.Exp, s) for s in sh]))
+    zt = t.gather(sh[0], 1, V, C, 0, 2)
+    loss = t.sub(lse, zt)
+    t.set_root(loss)
+    assert tg.Program(t.describe()).info["fused_mlp"] == 1
+    t.set_root(t.mul_by_constant(loss, 1.0))
+    assert tg.Program(t.describe()).info["fused_mlp"] == 0
