@@ -400,10 +400,11 @@ def main():
     tape_ms, tape_n = prog.profile_read()
     prog.profile(False)
     tape_ms = tape_ms / max(tape_n, 1)
-    if prog.info["storage"] == 3 and graphs is not None:
-        # staged tier: the "kernel" is the whole chain of the step; the eager
-        # profiling pass would also count host launch gaps between its kernels,
-        # so the chain is timed by the graph-replayed step itself
+    if graphs is not None and (prog.info["storage"] == 3 or launches_per_step == 1):
+        # staged tier: the "kernel" is the whole chain of the step; a
+        # one-launch step (cfg1) is the kernel itself.  The eager profiling
+        # pass would also count host launch gaps (cfg1: 16.0 us profiled vs
+        # 12.2 us per graph-replayed step), so they are timed by the step
         tape_ms = ms
     torch.cuda.synchronize()
 
