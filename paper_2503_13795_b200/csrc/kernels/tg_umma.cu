@@ -817,10 +817,11 @@ __global__ void __launch_bounds__(kTThreads, 1) k_umma_tma_p(GemmArgs<float> g, 
 //   tfull[b]  both: commit multicast (accumulator buffer b complete);
 //   tempty[b] leader: one arrive per drain warp of both CTAs (32).
 // The accumulator is drained every kPFlush k-tiles (TMEM reads per k-tile
-// double with N = 256; 2 tiles = K 64 keeps the tensor core's biased fp32
-// accumulation at ~7e-7 relative).
+// double with N = 256; 4 tiles = K 128 keeps the tensor core's biased fp32
+// accumulation at ~9e-7 relative: 1.06e-6 worst over scripts/gemm_shapes_err.py's
+// 160 cases; K 64 gave 4.7e-7 at 2.5% less throughput, r07g).
 constexpr int kPN = 256;
-constexpr int kPFlush = 2;
+constexpr int kPFlush = 4;
 constexpr int kPConv = 512;                 // 16 converter / drain warps: 64 accumulator columns per thread
 constexpr int kPThreads = 64 + kPConv;
 __host__ __device__ constexpr std::uint32_t pair_smem(int stages) {
