@@ -292,7 +292,7 @@ __device__ __forceinline__ std::uint64_t operand_desc(std::uint32_t base, bool m
 // the issuer alternates between two TMEM buffers, and the converter warps
 // drain each finished buffer into fp32 round-to-nearest register sums (one
 // output row per thread) while the tensor core fills the other one.
-constexpr int kFlush = 1;
+constexpr int kFlush = 4;   // K 128 per TMEM accumulation window (as the CTA pairs, r07g)
 // float4 epilogue stores need 16-byte aligned C / C2 bases (tg_gemm accepts any
 // device pointer: a view offset by one float must take the scalar stores)
 __device__ __forceinline__ bool c_aligned16(const GemmArgs<float>& g) {

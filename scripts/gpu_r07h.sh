@@ -1,0 +1,9 @@
+#!/bin/bash
+# r07h: single-CTA k_umma_tma drained every 4 k-tiles
+O=gpurun_out/r07h; mkdir -p $O
+timeout 300 python scripts/gemm_shapes_err.py > $O/shapes.log 2>&1
+GB_SET=shortk GB_S=262144 GB_ENGINES=1 timeout 120 python scripts/gemm_bench.py > $O/gemm_shortk.log 2>&1
+timeout 900 python -m pytest tests -m gpu -q -x > $O/pytest.log 2>&1; echo "exit $?" >> $O/pytest.log
+timeout 600 python bench.py --steps 10 --no-cpu-baseline --no-e2e > $O/bench_cfg5.json 2> $O/bench_cfg5.err
+timeout 600 python bench.py --config cfg4 --steps 5 --no-cpu-baseline --no-e2e > $O/bench_cfg4.json 2> $O/bench_cfg4.err
+timeout 600 python bench.py --config cfg3 --steps 20 --no-cpu-baseline --no-e2e > $O/bench_cfg3.json 2> $O/bench_cfg3.err
