@@ -366,14 +366,16 @@ def test_fp64_tanh_accuracy(tier, monkeypatch):
 @pytest.mark.parametrize("engine,dt", [(1, "f32"), (2, "f32"), (0, "f32"), (0, "f64")])
 @pytest.mark.parametrize("a_kmaj,b_nmaj", [(True, True), (False, True), (True, False)])
 @pytest.mark.parametrize("M,N,K", [(128, 128, 32), (300, 1000, 784), (10, 4096, 1024), (1024, 784, 2000),
-                                   (300, 1000, 10), (200, 4096, 30), (70, 2048, 1)])
+                                   (300, 1000, 10), (200, 4096, 30), (70, 2048, 1), (300, 4096, 10), (70, 4100, 13)])
 def test_dense_gemm_engines(engine, dt, a_kmaj, b_nmaj, M, N, K):
     """The staged path's dense-layer product (tg_gemm) against an fp64 matmul:
     tcgen05 3xTF32 (engine 1) and SIMT (engine 0), all operand layouts used by
     forward (W X), input adjoints (W^T dZ) and weight gradients (dZ X^T).
     The short-K shapes (K = 1, 10, 30) pin the tcgen05 kernels at one k-tile;
     the FP32-pipe k_gemm_shortk (forward products with K <= 32) is covered by
-    the char-MLP staged tests, whose 200 x 30 first layer routes there."""
+    the char-MLP staged tests, whose 200 x 30 first layer routes there.  The
+    last two shapes (K <= 16 over >= 4,096 columns, B n-major) take the
+    skinny input-adjoint stream k_dx_skinny on engine 1."""
     import ctypes as C
     from paper_2503_13795_b200 import _lib
     tdt = torch.float32 if dt == "f32" else torch.float64
