@@ -1126,287 +1126,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * kPN));
 }
 
-// ---------------------------------------------------------------------------
-// Persistent CTA pairs with a split ring (k_umma_pair_p).  k_umma_pair's k-tile
-// chain (TMA issue -> landed ~2.3 us, landed -> converted, converted -> MMAs
-// retired) is ~4.3 us against 0.9 us of MMA time per k-tile, and its ring holds
-// three 64 KB stages (hi and lo of both operands from the moment the TMA is
-// issued): 1.44 us per k-tile on cfg5's weight-gradient products, measured.
-// Here the ring is split by lifetime: kR raw stages of 32 KB (the landed fp32
-// tiles, rounded to hi in place) live from TMA issue to MMA retirement, kL lo
-// stages of 32 KB only from conversion to MMA retirement, so the same 224 KB
-// hold four k-tiles in flight behind the TMA latency instead of three.
-// The pair also walks tiles L = cluster, + clusters, ... (M pairs fastest,
-// then N, then the z slice / member) with the ring and accumulation-group
-// counters running on, so the producer lands the next tile's first stages
-// during the drain and epilogue, and barrier set-up, TMEM allocation and the
-// cluster sync are paid once.  The epilogue stores straight from the drain
-// registers (one output row per thread, 64 consecutive columns: 16-byte
-// stores whose 32-byte sectors the neighbouring store completes), so no
-// shared-memory tile overlays the ring.
-// A converter may overwrite lo stage (t % kL) once the MMAs of k-tile t - kL
-// retired: it waits on that k-tile's `empty` barrier, which the producer also
-// waits on one ring turn later (kL < kR, so the barrier cannot run two phases
-// ahead of the converter).
-constexpr int kRaw = 4, kLo = 3;
-constexpr std::uint32_t kHalfStage = 2 * kTTile;   // one k-tile of A and B (raw / hi, or lo)
-__host__ __device__ constexpr std::uint32_t pairp_smem() { return (kRaw + kLo) * kHalfStage + 1024 + 512; }
-
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
-    k_umma_pair_p(GemmArgs<float> g, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                  int a_mn, int b_mn, std::uint32_t mp, std::uint32_t nt, std::uint32_t n_tiles) {
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  unsigned char* lo_ring = smem + kRaw * kHalfStage;
-  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + pairp_smem() - 1024 - 512);
-  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 3 * kRaw + 4);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const std::uint32_t rank = cluster_rank();
-  auto full = [&](int s) { return smem_u32(&bars[s]); };
-  auto conv = [&](int s) { return smem_u32(&bars[kRaw + s]); };
-  auto empty = [&](int s) { return smem_u32(&bars[2 * kRaw + s]); };
-  auto tfull = [&](int b) { return smem_u32(&bars[3 * kRaw + b]); };
-  auto tempty = [&](int b) { return smem_u32(&bars[3 * kRaw + 2 + b]); };
-  constexpr std::uint32_t kArrivals = 2 * (kPConv / 32);   // converter / drain warps of both CTAs
-
-  if (tid == 0) {
-    for (int s = 0; s < kRaw; ++s) {
-      mbar_init(full(s), 1);
-      mbar_init(conv(s), kArrivals);
-      mbar_init(empty(s), 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(tfull(b), 1);
-      mbar_init(tempty(b), kArrivals);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tmA)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tmB)) : "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(2 * kPN));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  cluster_sync_all();   // both CTAs' barriers initialised and TMEM allocated
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  const std::uint32_t tmem = *tmem_slot;
-  const std::uint32_t cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-
-  struct Tile {
-    int m0, n0, a_off, b_off;
-    std::size_t c_off, c2_off;
-    std::uint32_t z, k_begin, T;
-  };
-  auto tile_of = [&](std::uint32_t L) {
-    Tile t;
-    const std::uint32_t mi = L % mp, ni = (L / mp) % nt, z = L / (mp * nt);
-    t.m0 = static_cast<int>(mi) * (2 * BM) + static_cast<int>(rank) * BM;
-    t.n0 = static_cast<int>(ni) * kPN;
-    t.z = z;
-    std::uint32_t slice = z;
-    t.a_off = t.b_off = 0;
-    t.c_off = t.c2_off = 0;
-    if (g.mem) {
-      const uint4 e = g.mem[z / g.zs];
-      slice = z % g.zs;
-      t.a_off = static_cast<int>(e.x);
-      t.b_off = static_cast<int>(e.y);
-      t.c_off = e.z;
-      t.c2_off = e.w;
-    }
-    std::uint32_t k_end = g.K;
-    t.k_begin = 0;
-    if (g.epi == kEpiSplitK) {
-      t.k_begin = slice * g.k_chunk;
-      k_end = min(g.K, t.k_begin + g.k_chunk);
-    }
-    t.T = k_end > t.k_begin ? (k_end - t.k_begin + BK - 1) / BK : 0;
-    return t;
-  };
-
-  if (warp == 0) {
-    // ===== TMA producer (each CTA loads its own A rows and B columns) =====
-    if (lane == 0) {
-      std::uint32_t gt = 0;
-      for (std::uint32_t L = cl; L < n_tiles; L += ncl) {
-        const Tile tl = tile_of(L);
-        for (std::uint32_t t = 0; t < tl.T; ++t, ++gt) {
-          const int s = gt % kRaw;
-          if (gt >= static_cast<std::uint32_t>(kRaw)) mbar_wait2(empty(s), ((gt / kRaw) - 1) & 1);
-          const std::uint32_t base = smem_u32(smem + s * kHalfStage);
-          mbar_expect_tx(full(s), kHalfStage);
-          const int k0 = static_cast<int>(tl.k_begin + t * BK);
-          tma_operand(&tmA, a_mn, base, tl.m0, k0, tl.a_off, full(s));
-          tma_operand(&tmB, b_mn, base + kTTile, tl.n0 + static_cast<int>(rank) * BN, k0, tl.b_off, full(s));
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ===== MMA issuer: the leader CTA only =====
-    if (rank == 0) {
-      const std::uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (std::uint32_t(a_mn) << 15) |
-                                  (std::uint32_t(b_mn) << 16) | ((kPN >> 3) << 17) | (((2 * BM) >> 4) << 24);
-      std::uint32_t gt = 0, gg = 0;
-      for (std::uint32_t L = cl; L < n_tiles; L += ncl) {
-        const Tile tl = tile_of(L);
-        for (std::uint32_t t = 0; t < tl.T; ++t, ++gt) {
-          const int s = gt % kRaw, l = gt % kLo;
-          const std::uint32_t grp = gg + t / kPFlush;
-          const int buf = grp & 1;
-          if (t % kPFlush == 0 && grp >= 2) mbar_wait_acq(tempty(buf), ((grp >> 1) - 1) & 1);
-          mbar_wait_acq(conv(s), (gt / kRaw) & 1);
-          asm volatile("tcgen05.fence::after_thread_sync;");
-          if (lane == 0) {
-            const std::uint32_t a_hi = smem_u32(smem + s * kHalfStage), b_hi = a_hi + kTTile;
-            const std::uint32_t a_lo = smem_u32(lo_ring + l * kHalfStage), b_lo = a_lo + kTTile;
-            const std::uint32_t td = tmem + buf * kPN;
-#pragma unroll
-            for (int ks = 0; ks < BK / 8; ++ks) {
-              const std::uint64_t dAh = operand_desc(a_hi, a_mn, ks), dAl = operand_desc(a_lo, a_mn, ks);
-              const std::uint64_t dBh = operand_desc(b_hi, b_mn, ks), dBl = operand_desc(b_lo, b_mn, ks);
-              mma_tf32_pair(td, dAl, dBh, idesc, (t % kPFlush != 0 || ks != 0) ? 1u : 0u);
-              mma_tf32_pair(td, dAh, dBl, idesc, 1u);
-              mma_tf32_pair(td, dAh, dBh, idesc, 1u);
-            }
-            commit_pair(empty(s));
-            if (t % kPFlush == kPFlush - 1 || t == tl.T - 1) commit_pair(tfull(buf));
-          }
-          __syncwarp();
-        }
-        gg += (tl.T + kPFlush - 1) / kPFlush;
-      }
-    }
-  } else {
-    // ===== converters + accumulation drain + epilogue (16 warps: TMEM lane quarter w % 4, column quarter) =====
-    const int ct = tid - 64;
-    const int wq = warp & 3;
-    const int c0 = ((warp - 2) >> 2) * (kPN / 4);
-    constexpr int kCols = kPN / 4;
-    const std::uint32_t leader_conv0 = peer_addr(conv(0), 0);
-    const std::uint32_t leader_tempty0 = peer_addr(tempty(0), 0);
-    float acc[kCols];
-#pragma unroll
-    for (int j = 0; j < kCols; ++j) acc[j] = 0.f;
-    constexpr int kIts = static_cast<int>(kTTile / 16) / kPConv;
-    float rs[kIts] = {};
-    auto drain = [&](std::uint32_t grp) {
-      const int buf = grp & 1;
-      mbar_wait2(tfull(buf), (grp >> 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;");
-#pragma unroll
-      for (int c = 0; c < kCols; c += 16) {
-        std::uint32_t r[16];
-        const std::uint32_t taddr = tmem + buf * kPN + (static_cast<std::uint32_t>(wq * 32) << 16) + c0 + c;
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-              "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;");
-#pragma unroll
-        for (int j = 0; j < 16; ++j) acc[c + j] += __uint_as_float(r[j]);
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      __syncwarp();
-      if (lane == 0) mbar_arrive_remote(leader_tempty0 + buf * 8);
-    };
-    std::uint32_t gt = 0, gg = 0;
-    for (std::uint32_t L = cl; L < n_tiles; L += ncl) {
-      const Tile tl = tile_of(L);
-      const std::uint32_t NG = (tl.T + kPFlush - 1) / kPFlush;
-      const bool rs_on = g.rowsum && !a_mn && tl.n0 == 0;
-      for (std::uint32_t t = 0; t < tl.T; ++t, ++gt) {
-        const int s = gt % kRaw, l = gt % kLo;
-        if (gt >= static_cast<std::uint32_t>(kLo)) mbar_wait2(empty((gt - kLo) % kRaw), ((gt - kLo) / kRaw) & 1);   // lo stage free
-        mbar_wait2(full(s), (gt / kRaw) & 1);
-        float4* hi = reinterpret_cast<float4*>(smem + s * kHalfStage);
-        float4* lo = reinterpret_cast<float4*>(lo_ring + l * kHalfStage);
-#pragma unroll
-        for (int it = 0; it < 2 * kIts; ++it) {   // A tile, then B tile (contiguous in both rings)
-          const int i = ct + it * kPConv;
-          const float4 x = hi[i];
-          if (it < kIts && rs_on) rs[it % kIts] += (x.x + x.y) + (x.z + x.w);   // A row (i / 8), four consecutive k
-          float4 h, w;
-          h.x = tf32_rna(x.x); w.x = tf32_rna(x.x - h.x);
-          h.y = tf32_rna(x.y); w.y = tf32_rna(x.y - h.y);
-          h.z = tf32_rna(x.z); w.z = tf32_rna(x.z - h.z);
-          h.w = tf32_rna(x.w); w.w = tf32_rna(x.w - h.w);
-          hi[i] = h;
-          lo[i] = w;
-        }
-        asm volatile("fence.proxy.async.shared::cta;");   // generic-proxy stores -> tensor-core reads
-        __syncwarp();
-        if (lane == 0) mbar_arrive_remote(leader_conv0 + s * 8);
-        // two groups back (see k_umma_tma): no converter stall on the tensor core
-        if (t % kPFlush == 0 && t / kPFlush >= 2) drain(gg + t / kPFlush - 2);
-      }
-      for (std::uint32_t q = NG >= 2 ? NG - 2 : 0; q < NG; ++q) drain(gg + q);
-      gg += NG;
-      if (rs_on) {   // eight threads per row (consecutive lanes): fixed-order tree, one store per row
-#pragma unroll
-        for (int it = 0; it < kIts; ++it) {
-          float v = rs[it];
-          v += __shfl_xor_sync(0xffffffffu, v, 1);
-          v += __shfl_xor_sync(0xffffffffu, v, 2);
-          v += __shfl_xor_sync(0xffffffffu, v, 4);
-          const std::uint32_t m = static_cast<std::uint32_t>(tl.m0 + (ct + it * kPConv) / 8);
-          if ((ct & 7) == 0 && m < g.M) g.rowsum[std::size_t(tl.z) * g.M + m] = v;
-          rs[it] = 0.f;
-        }
-      }
-      // ===== epilogue from the drain registers: row wq * 32 + lane, columns [c0, c0 + 64) =====
-      // (the host routes here only when every row segment takes 16-byte accesses:
-      // N and ldc multiples of 4, C / C2 16-byte aligned)
-      const std::uint32_t m = static_cast<std::uint32_t>(tl.m0 + wq * 32 + lane);
-      if (m < g.M) {
-        const std::uint32_t nb0 = static_cast<std::uint32_t>(tl.n0 + c0);
-        float* crow = g.epi == kEpiSplitK ? g.C + (std::size_t(tl.z) * g.M + m) * g.N + nb0 : g.C + (tl.c_off + m) * g.ldc + nb0;
-        float* c2row = g.C2 ? g.C2 + (tl.c2_off + m) * g.ldc + nb0 : nullptr;
-        const bool rd_h = g.epi == kEpiAccum && g.dact, rd_c = g.epi == kEpiAccum && !g.dact && g.beta;
-        const float* src = rd_h ? c2row : crow;
-        const float bv = (g.epi == kEpiBiasAct && g.bias) ? g.bias[m] : 0.f;
-#pragma unroll
-        for (int jb = 0; jb < kCols; jb += 16) {
-          float4 o[4];
-          if (rd_h || rd_c) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              if (nb0 + jb + 4 * q < g.N) o[q] = *reinterpret_cast<const float4*>(src + jb + 4 * q);
-          }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            if (nb0 + jb + 4 * q >= g.N) continue;
-            float4 a = make_float4(acc[jb + 4 * q], acc[jb + 4 * q + 1], acc[jb + 4 * q + 2], acc[jb + 4 * q + 3]);
-            if (g.epi == kEpiBiasAct) {
-              a.x += bv; a.y += bv; a.z += bv; a.w += bv;
-              if (g.act) {
-                *reinterpret_cast<float4*>(c2row + jb + 4 * q) = make_float4(
-                    act_fwd<float>(g.act, a.x), act_fwd<float>(g.act, a.y), act_fwd<float>(g.act, a.z), act_fwd<float>(g.act, a.w));
-                if (g.no_z) continue;   // z has no reader
-              }
-            } else if (rd_h) {
-              a.x = act_bwd_h<float>(g.dact, a.x, o[q].x);
-              a.y = act_bwd_h<float>(g.dact, a.y, o[q].y);
-              a.z = act_bwd_h<float>(g.dact, a.z, o[q].z);
-              a.w = act_bwd_h<float>(g.dact, a.w, o[q].w);
-            } else if (rd_c) {
-              a.x += o[q].x; a.y += o[q].y; a.z += o[q].z; a.w += o[q].w;
-            }
-            *reinterpret_cast<float4*>(crow + jb + 4 * q) = a;
-          }
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < kCols; ++j) acc[j] = 0.f;
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  cluster_sync_all();   // no CTA leaves while its peer may still signal its barriers or read its tiles
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * kPN));
-}
-
 // Host: 2D tensor map of an operand view for TMA (SWIZZLE_128B, zero OOB fill).
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {   // thread-safe one-time lookup
@@ -1466,26 +1185,6 @@ cudaError_t launch_tma_kernel(const GemmArgs<float>& g, std::uint32_t z, const C
   // (routing short-K products with M > 128 to the persistent single-CTA tiles
   // instead was measured slower end to end: cfg3 1.61 -> 1.83 ms, cfg4 34.6 -> 37.0 ms)
   if (use_pair(g.M) && !g.no_pair) {
-    // persistent pairs over a split ring (TG_PAIR_PERSIST=0: one tile per cluster, k_umma_pair)
-    static const bool pp = !(std::getenv("TG_PAIR_PERSIST") && std::getenv("TG_PAIR_PERSIST")[0] == '0');
-    const bool vec16 = g.ldc % 4 == 0 && g.N % 4 == 0 &&
-                       ((reinterpret_cast<std::uintptr_t>(g.C) | reinterpret_cast<std::uintptr_t>(g.C2)) & 15u) == 0;
-    if (pp && vec16) {
-      static PerDeviceOnce ppattr;
-      if (const cudaError_t e = ppattr.ensure([] {
-            return cudaFuncSetAttribute(k_umma_pair_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(pairp_smem()));
-          }); e != cudaSuccess)
-        return e;
-      const std::uint32_t mp = (g.M + 2 * BM - 1) / (2 * BM), nt = (g.N + kPN - 1) / kPN;
-      const std::uint64_t tiles64 = std::uint64_t(mp) * nt * z;
-      if (tiles64 > 0xffffffffull) return cudaErrorInvalidValue;
-      const std::uint32_t tiles = static_cast<std::uint32_t>(tiles64);
-      const std::uint32_t ncl = std::min<std::uint32_t>(tiles, static_cast<std::uint32_t>(std::max(1, sm_count() / 2)));
-      if (ncl == 0) return cudaSuccess;
-      k_umma_pair_p<<<2 * ncl, kPThreads, pairp_smem(), st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0, mp, nt, tiles);
-      return cudaGetLastError();
-    }
     const dim3 grid(2 * ((g.M + 2 * BM - 1) / (2 * BM)), (g.N + kPN - 1) / kPN, z);
     k_umma_pair<kTStagesMax><<<grid, kPThreads, pair_smem(kTStagesMax), st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0);
     return cudaGetLastError();
@@ -1573,12 +1272,20 @@ __global__ void __launch_bounds__(256, 2) k_gemm_shortk(GemmArgs<float> g, int k
   for (int r = 0; r < kSkRows; ++r)
 #pragma unroll
     for (int e = 0; e < 4; ++e) acc[r][e] = 0.f;
+  // the next four k-rows' loads are in flight while the current four are consumed
+  float4 bn[4];
+  auto load_b = [&](std::uint32_t k0) {
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+      bn[kk] = k0 + kk < g.K ? __ldg(reinterpret_cast<const float4*>(g.B + std::size_t(k0 + kk) * g.ldb + n))
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  load_b(0);
   for (std::uint32_t k0 = 0; k0 < g.K; k0 += 4) {
     float4 b[4];
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk)
-      b[kk] = k0 + kk < g.K ? __ldg(reinterpret_cast<const float4*>(g.B + std::size_t(k0 + kk) * g.ldb + n))
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int kk = 0; kk < 4; ++kk) b[kk] = bn[kk];
+    if (k0 + 4 < g.K) load_b(k0 + 4);
 #pragma unroll
     for (int r = 0; r < kSkRows; ++r) {
       const float4 a0 = *reinterpret_cast<const float4*>(Ar + r * kp + k0);
@@ -1648,9 +1355,15 @@ cudaError_t launch_shortk(const GemmArgs<float>& g, cudaStream_t st) {
 // loads, 16 M FMAs (M exact: one instantiation per even row count).  Each lane sums its k in order, the warp folds lanes in a fixed tree,
 // and the split partials [z][M][N] take the split-K reduce (deterministic).
 constexpr int kSwRows = 16, kSwK = 512, kSwWarps = 8, kSwN = 4;
+__device__ __forceinline__ void cp_async4_zfill(float* dst, const float* src, bool ok) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(ok ? 4 : 0) : "memory");
+}
 template <int MR>
 __global__ void __launch_bounds__(256, 2) k_dw_skinny(GemmArgs<float> g) {
-  __shared__ __align__(16) float As[MR][kSwK];
+  // the dZ chunk of the next 512 k lands (cp.async, zero-filled past M / the
+  // split's end) while the current one is consumed: one barrier per chunk and
+  // no exposed global round trip in front of it
+  extern __shared__ __align__(16) float Ab[];   // [2][MR][kSwK]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const std::uint32_t z = blockIdx.y;
   const std::uint32_t k_begin = min(g.K, z * g.k_chunk);
@@ -1661,14 +1374,22 @@ __global__ void __launch_bounds__(256, 2) k_dw_skinny(GemmArgs<float> g) {
   for (int j = 0; j < kSwN; ++j)
 #pragma unroll
     for (int m = 0; m < MR; ++m) acc[j][m] = 0.f;
-  for (std::uint32_t kb = k_begin; kb < k_end; kb += kSwK) {
-    const std::uint32_t kn = min(static_cast<std::uint32_t>(kSwK), k_end - kb);
-    __syncthreads();
+  auto stage = [&](int buf, std::uint32_t kb) {
     for (std::uint32_t i = threadIdx.x; i < MR * kSwK; i += 256) {
       const std::uint32_t m = i / kSwK, k = i % kSwK;
-      As[m][k] = (m < g.M && k < kn) ? g.A[std::size_t(m) * g.lda + kb + k] : 0.f;
+      const bool ok = m < g.M && kb + k < k_end;
+      cp_async4_zfill(Ab + (std::size_t(buf) * MR + m) * kSwK + k, ok ? g.A + std::size_t(m) * g.lda + kb + k : g.A, ok);
     }
-    __syncthreads();
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (k_begin < k_end) stage(0, k_begin);
+  int buf = 0;
+  for (std::uint32_t kb = k_begin; kb < k_end; kb += kSwK, buf ^= 1) {
+    const std::uint32_t kn = min(static_cast<std::uint32_t>(kSwK), k_end - kb);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();   // this chunk landed for every thread; the other buffer's readers are done
+    if (kb + kSwK < k_end) stage(buf ^ 1, kb + kSwK);
+    const float* As = Ab + std::size_t(buf) * MR * kSwK;
     const float* rows[kSwN];
 #pragma unroll
     for (int j = 0; j < kSwN; ++j) rows[j] = g.B + std::size_t(min(n0 + j, g.N - 1)) * g.ldb + kb;
@@ -1686,7 +1407,7 @@ __global__ void __launch_bounds__(256, 2) k_dw_skinny(GemmArgs<float> g) {
       }
 #pragma unroll
       for (int m = 0; m < MR; ++m) {
-        const float4 a = *reinterpret_cast<const float4*>(&As[m][k]);
+        const float4 a = *reinterpret_cast<const float4*>(As + m * kSwK + k);
 #pragma unroll
         for (int j = 0; j < kSwN; ++j) {
           float t = acc[j][m];
@@ -1722,15 +1443,28 @@ cudaError_t launch_dw_skinny(const GemmArgs<float>& g0, std::uint32_t splits, cu
   g.k_chunk = (g.K + splits - 1) / splits;
   g.k_chunk = (g.k_chunk + kSwK - 1) / kSwK * kSwK;
   const dim3 grid((g.N + kSwWarps * kSwN - 1) / (kSwWarps * kSwN), splits);
+  auto go = [&](auto mr) -> cudaError_t {
+    constexpr int MR = decltype(mr)::value;
+    constexpr int smem = 2 * MR * kSwK * static_cast<int>(sizeof(float));
+    if constexpr (smem > 48 * 1024) {
+      static PerDeviceOnce attr;
+      if (const cudaError_t e = attr.ensure([] {
+            return cudaFuncSetAttribute(k_dw_skinny<MR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+          }); e != cudaSuccess)
+        return e;
+    }
+    k_dw_skinny<MR><<<grid, 256, smem, st>>>(g);
+    return cudaGetLastError();
+  };
   switch ((g.M + 1) / 2) {
-    case 1: k_dw_skinny<2><<<grid, 256, 0, st>>>(g); break;
-    case 2: k_dw_skinny<4><<<grid, 256, 0, st>>>(g); break;
-    case 3: k_dw_skinny<6><<<grid, 256, 0, st>>>(g); break;
-    case 4: k_dw_skinny<8><<<grid, 256, 0, st>>>(g); break;
-    case 5: k_dw_skinny<10><<<grid, 256, 0, st>>>(g); break;
-    case 6: k_dw_skinny<12><<<grid, 256, 0, st>>>(g); break;
-    case 7: k_dw_skinny<14><<<grid, 256, 0, st>>>(g); break;
-    default: k_dw_skinny<16><<<grid, 256, 0, st>>>(g); break;
+    case 1: return go(std::integral_constant<int, 2>{});
+    case 2: return go(std::integral_constant<int, 4>{});
+    case 3: return go(std::integral_constant<int, 6>{});
+    case 4: return go(std::integral_constant<int, 8>{});
+    case 5: return go(std::integral_constant<int, 10>{});
+    case 6: return go(std::integral_constant<int, 12>{});
+    case 7: return go(std::integral_constant<int, 14>{});
+    default: return go(std::integral_constant<int, 16>{});
   }
   return cudaGetLastError();
 }
