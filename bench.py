@@ -501,6 +501,8 @@ def main():
         "config": config_dict(args, cfg, world),
         "l2": ("rotating buffer sets > 2x L2, back to back" if hbm_bound else
                "flushed between timed steps (256 MiB write, then 256 MiB read so no dirty lines remain)"),
+        "timed_as": ("one graph launch of the K steps (K kernel nodes back to back); launch by launch: %.4f ms per step"
+                     % ms_by_launch) if chain_ms is not None else "one graph launch (or eager call) per step",
         "cuda_graph": graphs is not None, "kernel_tier": tier, "tile_samples": info["tile_samples"],
         "exchange": ("none (one rank: GD fused in the reduction epilogue)" if world == 1 else
                      "tg_allreduce_gd_step (NCCL all-reduce + GD)" if win is None else

@@ -873,7 +873,7 @@ __device__ __forceinline__ void commit_pair(std::uint32_t mbar) {
 template <int kTStages>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
     k_umma_pair(GemmArgs<float> g, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                int a_mn, int b_mn) {
+                int a_mn, int b_mn, int n_tile) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + pair_smem(kTStages) - 1024 - 512);
@@ -912,8 +912,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
   const std::uint32_t tmem = *tmem_slot;
 
   const int m0 = static_cast<int>(blockIdx.x >> 1) * (2 * BM) + static_cast<int>(rank) * BM;
-  const int n0 = static_cast<int>(blockIdx.y) * kPN;
-  const int nb = n0 + static_cast<int>(rank) * BN;   // this CTA's B rows
+  // n_tile <= 256 output columns per pair (a multiple of 16: N spread evenly over its tiles, so a
+  // 784-column product runs four tiles of 208 instead of three full ones and one of 16)
+  const int n0 = static_cast<int>(blockIdx.y) * n_tile;
+  const int nb = n0 + static_cast<int>(rank) * (n_tile >> 1);   // this CTA's B rows (the MMA reads n_tile / 2 of the 128 landed)
   std::uint32_t slice = blockIdx.z;
   int a_off = 0, b_off = 0;
   std::size_t c_off = 0, c2_off = 0;
@@ -949,7 +951,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
     // ===== MMA issuer: the leader CTA only =====
     if (rank == 0) {
       const std::uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (std::uint32_t(a_mn) << 15) |
-                                  (std::uint32_t(b_mn) << 16) | ((kPN >> 3) << 17) | (((2 * BM) >> 4) << 24);
+                                  (std::uint32_t(b_mn) << 16) | ((std::uint32_t(n_tile) >> 3) << 17) | (((2 * BM) >> 4) << 24);
       for (std::uint32_t t = 0; t < T; ++t) {
         const int s = t % kTStages;
         const std::uint32_t grp = t / kPFlush;
@@ -1072,13 +1074,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
     asm volatile("bar.sync 1, %0;" ::"n"(kPConv));
     const int cw = (tid - 64) >> 5;
     const bool vec = (g.ldc % 4 == 0) && (g.epi != kEpiSplitK || g.N % 4 == 0) && c_aligned16(g);
+    if (g.epi == kEpiAccum && g.dact && vec && g.N % 4 == 0) {
+      // input adjoint through act': the 16 h segments of this warp's rows are all in
+      // flight before the first is consumed (the running sums are dead by now, so the
+      // registers are there); the general loop below waits for one row's h at a time
+      float4 hp[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int col = (i & 1) * 128 + 4 * lane;
+        const std::uint32_t m = static_cast<std::uint32_t>(m0 + cw + (i >> 1) * (kPConv / 32));
+        const std::uint32_t n = static_cast<std::uint32_t>(n0 + col);
+        if (m < g.M && n < g.N && col < n_tile) hp[i] = *reinterpret_cast<const float4*>(g.C2 + (c2_off + m) * g.ldc + n);
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int r = cw + (i >> 1) * (kPConv / 32), col = (i & 1) * 128 + 4 * lane;
+        const std::uint32_t m = static_cast<std::uint32_t>(m0 + r), n = static_cast<std::uint32_t>(n0 + col);
+        if (m >= g.M || n >= g.N || col >= n_tile) continue;
+        float4 v = *reinterpret_cast<const float4*>(tile + r * kLd + col);
+        v.x = act_bwd_h<float>(g.dact, v.x, hp[i].x);
+        v.y = act_bwd_h<float>(g.dact, v.y, hp[i].y);
+        v.z = act_bwd_h<float>(g.dact, v.z, hp[i].z);
+        v.w = act_bwd_h<float>(g.dact, v.w, hp[i].w);
+        *reinterpret_cast<float4*>(g.C + (c_off + m) * g.ldc + n) = v;
+      }
+    } else
     for (int r = cw; r < BM; r += kPConv / 32) {
       const std::uint32_t m = static_cast<std::uint32_t>(m0 + r);
       if (m >= g.M) continue;
 #pragma unroll
       for (int hlf = 0; hlf < 2; ++hlf) {
         const std::uint32_t n = static_cast<std::uint32_t>(n0 + hlf * 128) + 4 * lane;
-        if (n >= g.N) continue;
+        if (n >= g.N || hlf * 128 + 4 * lane >= n_tile) continue;
         const float4 v = *reinterpret_cast<const float4*>(tile + r * kLd + hlf * 128 + 4 * lane);
         float a4[4] = {v.x, v.y, v.z, v.w};
         float* dst = g.epi == kEpiSplitK ? g.C + (std::size_t(blockIdx.z) * g.M + m) * g.N + n
@@ -1185,8 +1212,10 @@ cudaError_t launch_tma_kernel(const GemmArgs<float>& g, std::uint32_t z, const C
   // (routing short-K products with M > 128 to the persistent single-CTA tiles
   // instead was measured slower end to end: cfg3 1.61 -> 1.83 ms, cfg4 34.6 -> 37.0 ms)
   if (use_pair(g.M) && !g.no_pair) {
-    const dim3 grid(2 * ((g.M + 2 * BM - 1) / (2 * BM)), (g.N + kPN - 1) / kPN, z);
-    k_umma_pair<kTStagesMax><<<grid, kPThreads, pair_smem(kTStagesMax), st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0);
+    const std::uint32_t nt = (g.N + kPN - 1) / kPN;
+    const int n_tile = static_cast<int>(((g.N + nt - 1) / nt + 15) / 16 * 16);
+    const dim3 grid(2 * ((g.M + 2 * BM - 1) / (2 * BM)), nt, z);
+    k_umma_pair<kTStagesMax><<<grid, kPThreads, pair_smem(kTStagesMax), st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0, n_tile);
     return cudaGetLastError();
   }
   static const bool persist = !(std::getenv("TG_UMMA_PERSIST") && std::getenv("TG_UMMA_PERSIST")[0] == '0');

@@ -2,8 +2,8 @@
 # Round evidence: GPU tests, smoke, bench lines of every config (device value,
 # e2e, roofline, cpu_baseline), the reference arm, ncu launch lists and full
 # captures of the dominant kernels (summaries + raw pages as text).
-# Usage (on the GPU box): bash scripts/profile_round.sh r07
-R=${1:-r07}
+# Usage (on the GPU box): bash scripts/profile_round.sh r08
+R=${1:-r08}
 O=gpurun_out/$R
 mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/gpu.txt
@@ -27,9 +27,16 @@ cap() {   # name config kernel-regex launch-skip
   ncu -i /tmp/$1.ncu-rep --page raw --csv > $O/ncu_full_$1_raw.csv 2>/dev/null
 }
 cap cfg5_pair cfg5 k_umma_pair 1
+cap cfg5_pair_dx2 cfg5 k_umma_pair 2
 cap cfg5_dw_skinny cfg5 k_dw_skinny 0
+cap cfg5_dx_skinny cfg5 k_dx_skinny 0
 cap cfg2_tape cfg2 tg_jit_tape 1
 cap cfg1_tape cfg1 tg_jit_tape 1
 cap cfg3_pair cfg3 k_umma_pair 0
 cap cfg4_attn_bwd cfg4 k_attn_bwd 0
+# DRAM traffic of one step (cold caches) for the staged configs whose kernels changed this round
+for c in cfg3 cfg5; do
+  timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 3000 --csv \
+      --print-units base --log-file $O/traffic_$c.csv python scripts/one_cfg.py $c 1 > $O/ncu_traffic_$c.log 2>&1
+done
 ls -la $O

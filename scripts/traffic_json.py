@@ -29,6 +29,8 @@ def parse(path):
 
 def main(d, label):
     out = {}
+    if os.path.exists("profiles/traffic.json"):   # configs without a new capture keep their entry
+        out = json.load(open("profiles/traffic.json"))
     for cfg, b in BATCH.items():
         p = os.path.join(d, f"traffic_{cfg}.csv")
         if not os.path.exists(p):
