@@ -873,7 +873,7 @@ __device__ __forceinline__ void commit_pair(std::uint32_t mbar) {
 template <int kTStages>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
     k_umma_pair(GemmArgs<float> g, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                int a_mn, int b_mn, int n_tile, int pf) {
+                int a_mn, int b_mn, int n_tile) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + pair_smem(kTStages) - 1024 - 512);
@@ -937,32 +937,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
 
   if (warp == 0) {
     // ===== TMA producer (each CTA loads its own A rows and B columns) =====
-    // pf > 0: every pf k-tiles the warp's lanes ask L2 for the NEXT window of pf k-tiles of
-    // both operand tiles, one request per operand row (K-major: pf * 128 contiguous bytes;
-    // MN-major: the tile's 512-byte k-rows), so DRAM serves long bursts and the ring's TMA
-    // loads hit L2; the lanes stay in step with the producer lane through the warp sync
-    auto l2_prefetch = [&](const float* P, std::size_t ld, bool mn, int r0, int off, std::uint32_t rows_total,
-                           std::uint32_t kp, std::uint32_t kw) {
-      if (r0 >= static_cast<int>(rows_total)) return;
-      const std::uint32_t rows = min(static_cast<std::uint32_t>(BM), rows_total - r0);
-      if (!mn) {
-        const std::uint32_t bytes = (kw & ~3u) * 4;
-        if (bytes)
-          for (std::uint32_t r = lane; r < rows; r += 32) {
-            const float* q = P + (std::size_t(r0 + r) + off) * ld + kp;
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(q), "r"(bytes) : "memory");
-          }
-      } else {
-        const std::uint32_t bytes = (rows & ~3u) * 4;
-        if (bytes)
-          for (std::uint32_t kk = lane; kk < kw; kk += 32) {
-            const float* q = P + (std::size_t(kp + kk) + off) * ld + r0;
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(q), "r"(bytes) : "memory");
-          }
-      }
-    };
-    for (std::uint32_t t = 0; t < T; ++t) {
-      if (lane == 0) {
+    if (lane == 0)
+      for (std::uint32_t t = 0; t < T; ++t) {
         const int s = t % kTStages;
         if (t >= kTStages) mbar_wait2(empty(s), ((t / kTStages) - 1) & 1);
         const std::uint32_t base = smem_u32(smem + s * kTStage);
@@ -971,16 +947,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
         tma_operand(&tmA, a_mn, base, m0, k0, a_off, full(s));
         tma_operand(&tmB, b_mn, base + 2 * kTTile, nb, k0, b_off, full(s));
       }
-      if (pf > 0) {
-        if (t % pf == 0 && t + pf < T) {
-          const std::uint32_t kp = k_begin + (t + pf) * BK;
-          const std::uint32_t kw = min(static_cast<std::uint32_t>(pf) * BK, k_end - kp);
-          l2_prefetch(g.A, g.lda, a_mn, m0, a_off, g.M, kp, kw);
-          l2_prefetch(g.B, g.ldb, b_mn, nb, b_off, g.N, kp, kw);
-        }
-        __syncwarp();
-      }
-    }
   } else if (warp == 1) {
     // ===== MMA issuer: the leader CTA only =====
     if (rank == 0) {
@@ -1249,10 +1215,7 @@ cudaError_t launch_tma_kernel(const GemmArgs<float>& g, std::uint32_t z, const C
     const std::uint32_t nt = (g.N + kPN - 1) / kPN;
     const int n_tile = static_cast<int>(((g.N + nt - 1) / nt + 15) / 16 * 16);
     const dim3 grid(2 * ((g.M + 2 * BM - 1) / (2 * BM)), nt, z);
-    // L2 prefetch window in k-tiles (TG_PAIR_PF; 0: off)
-    static const int pf = std::getenv("TG_PAIR_PF") ? std::atoi(std::getenv("TG_PAIR_PF")) : 0;
-    k_umma_pair<kTStagesMax><<<grid, kPThreads, pair_smem(kTStagesMax), st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0, n_tile,
-                                                                            g.mem ? 0 : pf);
+    k_umma_pair<kTStagesMax><<<grid, kPThreads, pair_smem(kTStagesMax), st>>>(g, ta, tb, a_mn ? 1 : 0, b_mn ? 1 : 0, n_tile);
     return cudaGetLastError();
   }
   static const bool persist = !(std::getenv("TG_UMMA_PERSIST") && std::getenv("TG_UMMA_PERSIST")[0] == '0');
