@@ -20,7 +20,7 @@ HDRS    := $(wildcard include/*.h $(PKG)/csrc/host/*.hpp $(PKG)/csrc/kernels/*.c
 CU_OBJ  := $(patsubst $(PKG)/csrc/kernels/%.cu,$(BUILD)/%.cu.o,$(CU_SRC))
 CXX_OBJ := $(patsubst $(PKG)/csrc/host/%.cpp,$(BUILD)/%.o,$(CXX_SRC))
 
-.PHONY: all lib oracle clean tools
+.PHONY: all lib oracle clean tools prof
 all: lib oracle tools
 lib: $(PKG)/libtg.so
 
@@ -54,3 +54,13 @@ build/fp_peak: tools/fp_peak.cu
 build/mma_peak: tools/mma_peak.cu
 	@mkdir -p $(BUILD)
 	$(NVCC) $(ARCH) -O3 $< -o $@
+
+# Profiling build (NOT the product): -DTG_PROFILING compiles the work-skipping ablations (TG_UMMA_EXP,
+# TG_JIT_SKIP) and the CTA-pair k-tile timeline (scripts/pair_trace.py) into build_prof/libtg_prof.so
+PROF    := build_prof
+prof: $(PROF)/libtg_prof.so
+$(PROF)/libtg_prof.so: $(CU_SRC) $(CXX_SRC) $(HDRS) $(BUILD)/tg_math.inc
+	@mkdir -p $(PROF)
+	for f in $(CU_SRC); do $(NVCC) $(NVFLAGS) -DTG_PROFILING -c $$f -o $(PROF)/$$(basename $$f).o 2> $(PROF)/$$(basename $$f).ptxas.txt || exit 1; done
+	for f in $(CXX_SRC); do $(CXX) $(CXXFLAGS) -DTG_PROFILING -c $$f -o $(PROF)/$$(basename $$f).o || exit 1; done
+	$(NVCC) $(ARCH) -shared -o $@ $(PROF)/*.o -L$(CUDA)/lib64 -lcudart -lnvrtc -ldl -Xlinker -rpath,$(CUDA)/lib64

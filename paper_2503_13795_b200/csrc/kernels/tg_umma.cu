@@ -870,6 +870,19 @@ __device__ __forceinline__ void commit_pair(std::uint32_t mbar) {
       "h"(static_cast<unsigned short>(3)));
 }
 
+#ifdef TG_PROFILING
+// k-tile timeline of one CTA pair's leader (profiling build only, scripts/pair_trace.py): SM clock stamps of
+// 0 TMA issue, 1 `full` seen by converter warp 2, 2 that warp's conv arrive, 3 `conv` seen by the MMA warp,
+// 4 MMAs issued + committed, 5 drain of the group two back finished (converter warp 2)
+constexpr int kTraceT = 96;
+__device__ long long g_pair_trace[7][kTraceT];   // row 6: 0 kernel entry, 1 set-up done, 2 last drain done, 3 tile staged, 4 stores issued, 5 exit
+#define TG_TRACE(ev, t)                                                                        \
+  do {                                                                                         \
+    if (traced && (t) < static_cast<std::uint32_t>(kTraceT)) g_pair_trace[ev][t] = clock64();  \
+  } while (0)
+#else
+#define TG_TRACE(ev, t) do { } while (0)
+#endif
 template <int kTStages>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
     k_umma_pair(GemmArgs<float> g, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -880,6 +893,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
   std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 3 * kTStages + 4);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const std::uint32_t rank = cluster_rank();
+#ifdef TG_PROFILING
+  const bool traced = rank == 0 && lane == 0 && blockIdx.x < 2 && blockIdx.y == gridDim.y / 2 && blockIdx.z == 0;
+  if (warp == 2) TG_TRACE(6, 0u);
+#endif
   auto full = [&](int s) { return smem_u32(&bars[s]); };
   auto conv = [&](int s) { return smem_u32(&bars[kTStages + s]); };
   auto empty = [&](int s) { return smem_u32(&bars[2 * kTStages + s]); };
@@ -910,6 +927,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
   cluster_sync_all();   // both CTAs' barriers initialised and TMEM allocated
   asm volatile("tcgen05.fence::after_thread_sync;");
   const std::uint32_t tmem = *tmem_slot;
+  if (warp == 2) TG_TRACE(6, 1u);
 
   const int m0 = static_cast<int>(blockIdx.x >> 1) * (2 * BM) + static_cast<int>(rank) * BM;
   // n_tile <= 256 output columns per pair (a multiple of 16: N spread evenly over its tiles, so a
@@ -942,6 +960,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
         const int s = t % kTStages;
         if (t >= kTStages) mbar_wait2(empty(s), ((t / kTStages) - 1) & 1);
         const std::uint32_t base = smem_u32(smem + s * kTStage);
+        TG_TRACE(0, t);
         mbar_expect_tx(full(s), 2 * kTTile);
         const int k0 = static_cast<int>(k_begin + t * BK);
         tma_operand(&tmA, a_mn, base, m0, k0, a_off, full(s));
@@ -958,6 +977,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
         const int buf = grp & 1;
         if (t % kPFlush == 0 && grp >= 2) mbar_wait_acq(tempty(buf), ((grp >> 1) - 1) & 1);
         mbar_wait_acq(conv(s), (t / kTStages) & 1);
+        TG_TRACE(3, t);
         asm volatile("tcgen05.fence::after_thread_sync;");
         if (lane == 0) {
           const std::uint32_t a_hi = smem_u32(smem + s * kTStage), a_lo = a_hi + kTTile;
@@ -978,6 +998,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
           }
           commit_pair(empty(s));
           if (t % kPFlush == kPFlush - 1 || t == T - 1) commit_pair(tfull(buf));
+          TG_TRACE(4, t);
         }
         __syncwarp();
       }
@@ -1023,6 +1044,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
     for (std::uint32_t t = 0; t < T; ++t) {
       const int s = t % kTStages;
       mbar_wait2(full(s), (t / kTStages) & 1);
+      if (warp == 2) TG_TRACE(1, t);
       unsigned char* base = smem + s * kTStage;
       const int nop = (g_umma_exp == 1 || g_umma_exp == 3 || g_umma_exp == 4) ? 0 : 2;
 #pragma unroll
@@ -1046,10 +1068,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
       asm volatile("fence.proxy.async.shared::cta;");   // generic-proxy stores -> tensor-core reads
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(leader_conv0 + s * 8);
+      if (warp == 2) TG_TRACE(2, t);
       // two groups back (see k_umma_tma): no converter stall on the tensor core
-      if (t % kPFlush == 0 && t / kPFlush >= 2) drain(t / kPFlush - 2);
+      if (t % kPFlush == 0 && t / kPFlush >= 2) {
+        drain(t / kPFlush - 2);
+        if (warp == 2) TG_TRACE(5, t);
+      }
     }
     for (std::uint32_t q = NG >= 2 ? NG - 2 : 0; q < NG; ++q) drain(q);
+    if (warp == 2) TG_TRACE(6, 2u);
     if (rs_on) {   // eight threads per row (consecutive lanes): fixed-order tree, one store per row
 #pragma unroll
       for (int it = 0; it < static_cast<int>(kTTile / 16) / kPConv; ++it) {
@@ -1072,6 +1099,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
         *reinterpret_cast<float4*>(tile + r * kLd + c0 + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
     }
     asm volatile("bar.sync 1, %0;" ::"n"(kPConv));
+    if (warp == 2) TG_TRACE(6, 3u);
     const int cw = (tid - 64) >> 5;
     const bool vec = (g.ldc % 4 == 0) && (g.epi != kEpiSplitK || g.N % 4 == 0) && c_aligned16(g);
     if (g.epi == kEpiAccum && g.dact && vec && g.N % 4 == 0) {
@@ -1148,8 +1176,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
       }
     }
   }
+  if (warp == 2) TG_TRACE(6, 4u);
   asm volatile("tcgen05.fence::before_thread_sync;");
   cluster_sync_all();   // no CTA leaves while its peer may still signal its barriers or read its tiles
+  if (warp == 2) TG_TRACE(6, 5u);
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * kPN));
 }
 
@@ -1719,4 +1749,11 @@ cudaError_t launch_gemm_umma(const GemmArgs<float>& g0, std::uint32_t splits, cu
   return cudaGetLastError();
 }
 
+#ifdef TG_PROFILING
+cudaError_t read_pair_trace(long long* out) { return cudaMemcpyFromSymbol(out, g_pair_trace, sizeof(g_pair_trace)); }
+#endif
+
 }  // namespace tgk
+#ifdef TG_PROFILING
+extern "C" int tg_debug_pair_trace(long long* out) { return static_cast<int>(tgk::read_pair_trace(out)); }
+#endif
