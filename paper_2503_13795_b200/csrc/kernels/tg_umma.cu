@@ -1142,9 +1142,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
       const float* tp = tile + cw * kLd + col;
       const float* bp = (ba && g.bias) ? g.bias + m0 + cw : nullptr;
       const int rows = static_cast<std::uint32_t>(m0) < g.M ? static_cast<int>(min(static_cast<std::uint32_t>(BM), g.M - static_cast<std::uint32_t>(m0))) : 0;   // (the pair's second CTA may lie wholly past M)
+      float bnext = (bp && cw < rows) ? bp[0] : 0.f;   // the next row's bias is loaded while this row is stored
       for (int r = cw; r < rows; r += kPConv / 32, d += (kPConv / 32) * rstride, d2 += (kPConv / 32) * g.ldc,
                tp += (kPConv / 32) * kLd) {
-        const float bv = bp ? bp[r - cw] : 0.f;
+        const float bv = bnext;
+        if (bp && r + kPConv / 32 < rows) bnext = bp[r + kPConv / 32 - cw];
         float4 v0 = *reinterpret_cast<const float4*>(tp), v1 = *reinterpret_cast<const float4*>(tp + 128);
         v0.x += bv; v0.y += bv; v0.z += bv; v0.w += bv;
         v1.x += bv; v1.y += bv; v1.z += bv; v1.w += bv;
