@@ -746,6 +746,66 @@ __global__ void __launch_bounds__(kTThreads, 1) k_umma_tma_p(GemmArgs<float> g, 
       asm volatile("bar.sync 1, %0;" ::"n"(kConvThreads));
       const std::uint32_t n = tl.n0 + 4 * lane;
       const bool vec = (g.ldc % 4 == 0) && (g.epi != kEpiSplitK || g.N % 4 == 0) && c_aligned16(g);
+      constexpr int kRS = kConvThreads / 32;   // rows between a warp's consecutive rows
+      const int rows = static_cast<std::uint32_t>(tl.m0) < g.M
+                           ? static_cast<int>(min(static_cast<std::uint32_t>(BM), g.M - static_cast<std::uint32_t>(tl.m0))) : 0;
+      if (vec && g.N % 4 == 0 && !(g.epi == kEpiAccum && (g.dact || g.beta))) {
+        // store-only epilogues with 16-byte row segments: one rolled loop with hoisted addressing and kind
+        // tests, the next row's bias loaded while this row is stored (as the CTA pairs; the general loop
+        // below waits for a global load and re-derives addresses on every one of the warp's 32 rows)
+        if (n < g.N) {
+          const bool ba = g.epi == kEpiBiasAct, wh = ba && g.act != 0, wz = !(wh && g.no_z);
+          const std::size_t rstride = g.epi == kEpiSplitK ? g.N : g.ldc;
+          float* d = (g.epi == kEpiSplitK ? g.C + (std::size_t(tl.z) * g.M + tl.m0 + cw) * g.N
+                                          : g.C + (tl.c_off + tl.m0 + cw) * g.ldc) + n;
+          float* d2 = wh ? g.C2 + (tl.c2_off + tl.m0 + cw) * g.ldc + n : nullptr;
+          const float* tp = etile + cw * kLd + 4 * lane;
+          const float* bp = (ba && g.bias) ? g.bias + tl.m0 + cw : nullptr;
+          float bnext = (bp && cw < rows) ? bp[0] : 0.f;
+          for (int r = cw; r < rows; r += kRS, d += kRS * rstride, d2 += kRS * g.ldc, tp += kRS * kLd) {
+            const float bv = bnext;
+            if (bp && r + kRS < rows) bnext = bp[r + kRS - cw];
+            float4 v = *reinterpret_cast<const float4*>(tp);
+            v.x += bv; v.y += bv; v.z += bv; v.w += bv;
+            if (wh)
+              *reinterpret_cast<float4*>(d2) = make_float4(act_fwd<float>(g.act, v.x), act_fwd<float>(g.act, v.y),
+                                                           act_fwd<float>(g.act, v.z), act_fwd<float>(g.act, v.w));
+            if (wz) *reinterpret_cast<float4*>(d) = v;
+          }
+        }
+      } else if (vec && g.N % 4 == 0 && g.epi == kEpiAccum && g.dact) {
+        // input adjoint through act': h of the warp's next eight rows is in flight while eight rows are consumed
+        if (n < g.N) {
+          constexpr int kCh = 8;
+          const float* hrow = g.C2 + (tl.c2_off + tl.m0 + cw) * g.ldc + n;
+          float* d = g.C + (tl.c_off + tl.m0 + cw) * g.ldc + n;
+          const float* tp = etile + cw * kLd + 4 * lane;
+          float4 hn[kCh];
+          auto load_h = [&](int r0) {
+#pragma unroll
+            for (int j = 0; j < kCh; ++j)
+              if (r0 + j * kRS < rows) hn[j] = *reinterpret_cast<const float4*>(hrow + std::size_t(r0 + j * kRS - cw) * g.ldc);
+          };
+          load_h(cw);
+          for (int r0 = cw; r0 < rows; r0 += kCh * kRS) {
+            float4 h[kCh];
+#pragma unroll
+            for (int j = 0; j < kCh; ++j) h[j] = hn[j];
+            load_h(r0 + kCh * kRS);
+#pragma unroll
+            for (int j = 0; j < kCh; ++j) {
+              const int r = r0 + j * kRS;
+              if (r >= rows) break;
+              float4 v = *reinterpret_cast<const float4*>(tp + std::size_t(r - cw) * kLd);
+              v.x = act_bwd_h<float>(g.dact, v.x, h[j].x);
+              v.y = act_bwd_h<float>(g.dact, v.y, h[j].y);
+              v.z = act_bwd_h<float>(g.dact, v.z, h[j].z);
+              v.w = act_bwd_h<float>(g.dact, v.w, h[j].w);
+              *reinterpret_cast<float4*>(d + std::size_t(r - cw) * g.ldc) = v;
+            }
+          }
+        }
+      } else
       for (int r = cw; r < BM; r += kConvThreads / 32) {
         const std::uint32_t m = tl.m0 + r;
         if (m >= g.M || n >= g.N) continue;
