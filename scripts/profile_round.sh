@@ -2,8 +2,8 @@
 # Round evidence: GPU tests, smoke, bench lines of every config (device value,
 # e2e, roofline, cpu_baseline), the reference arm, ncu launch lists and full
 # captures of the dominant kernels (summaries + raw pages as text).
-# Usage (on the GPU box): bash scripts/profile_round.sh r08
-R=${1:-r08}
+# Usage (on the GPU box): bash scripts/profile_round.sh r09
+R=${1:-r09}
 O=gpurun_out/$R
 mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/gpu.txt
